@@ -1,0 +1,167 @@
+/*
+ * tvdeblur_b200.h -- C ABI of the B200-native PCG hot path of the reference
+ * total-variation deblurring solver (tvdeblur, arXiv 1011.5964).
+ *
+ * The reference is pure Python; its "operator API" is the callable contract
+ * of krylov.pcg (reference pkg/src/tvdeblur/krylov.py:82) plus the duck-typed
+ * operator objects StructuredBlurOperator (blur.py:197-326),
+ * DiffusionOperator (tv.py:74-187), FactoredPreconditioner /
+ * assemble_preconditioner (precond.py:419-573) and the fixed-point driver
+ * restore (pipeline.py:182-276).  Each entry point below replaces one of
+ * those calls; the Python mirror in paper_1011_5964_b200/ binds them with
+ * ctypes.
+ *
+ * Conventions
+ *  - Arrays are caller-owned DEVICE buffers, float64, C-contiguous n x n
+ *    (row = axis 0) unless stated; the context owns only scratch.
+ *  - Inputs are never modified (out may alias nothing it reads unless noted).
+ *  - Every call returns an int status; TVD_OK == 0.  tvd_last_error() gives a
+ *    thread-local message for the last failure on the calling thread.
+ *  - One context = one device + one stream, used by one host thread at a time.
+ *    Calls on distinct contexts are reentrant.  Work is enqueued on the
+ *    context stream; calls that return host scalars synchronise it.
+ */
+#ifndef TVDEBLUR_B200_H
+#define TVDEBLUR_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TVD_ABI_VERSION 1
+
+/* status codes -> exception classes of the reference */
+#define TVD_OK 0
+#define TVD_ERR_INVALID 1    /* ValueError / ConfigurationError               */
+#define TVD_ERR_DIVERGED 2   /* krylov.SolverDivergenceError (krylov.py:31)   */
+#define TVD_ERR_INDEFINITE 3 /* krylov.IndefiniteOperatorError (krylov.py:39) */
+#define TVD_ERR_PRECOND 4    /* precond.IndefinitePreconditionerError (:60)   */
+#define TVD_ERR_SCALING 5    /* pipeline.InvalidScalingError (pipeline.py:60) */
+#define TVD_ERR_CUDA 6       /* CUDA runtime failure                          */
+
+/* blur boundary conditions (blur.py:34-38; only these two are transform-
+ * diagonalisable and in scope) */
+#define TVD_BC_REFLECTIVE 2
+#define TVD_BC_ANTI_REFLECTIVE 3
+
+/* transforms (transforms.py:35-39) */
+#define TVD_TRANSFORM_DST1 0
+#define TVD_TRANSFORM_SINE_HAT 1
+#define TVD_TRANSFORM_DCT 2
+
+/* preconditioner variants of one family (precond.py:516-573) */
+#define TVD_VARIANT_X 0   /* |lam_H|^2 + alpha proj(L)                */
+#define TVD_VARIANT_D_X 1 /* same eigenvalues, wrapped by sqrt(1+a diag L) */
+#define TVD_VARIANT_X_D 2 /* |lam_H|^2 |lam_D|^2 + alpha proj(s L s)     */
+
+/* inner-solve preconditioner kinds (pipeline.py:225-241) */
+#define TVD_PRECOND_NONE 0      /* apply_minv = None (identity)          */
+#define TVD_PRECOND_DIAG 1      /* w / (1 + alpha diag L)                */
+#define TVD_PRECOND_TRANSFORM 2 /* FactoredPreconditioner.apply_inverse  */
+
+typedef struct tvd_ctx tvd_ctx;
+typedef struct tvd_blur tvd_blur;
+
+/* system A w = H^T H w + alpha L w   (pipeline.py:209-210), optionally the
+ * diagonally scaled s .* A(s .* w)   (pipeline.py:145-164, selector X_D). */
+typedef struct tvd_system {
+  tvd_blur* blur;
+  double alpha;
+  double spacing;
+  const double* a_h; /* n x (n+1) horizontal diffusivities */
+  const double* a_v; /* (n+1) x n vertical diffusivities   */
+  const double* s;   /* NULL or n x n scaling              */
+} tvd_system;
+
+typedef struct tvd_precond {
+  int kind;              /* TVD_PRECOND_*                                   */
+  int family;            /* TVD_TRANSFORM_SINE_HAT or TVD_TRANSFORM_DCT     */
+  const double* inv_eig; /* TRANSFORM: n x n inverse eigenvalues            */
+  const double* d;       /* DIAG: divisor; TRANSFORM: d_sqrt (D_X) or NULL  */
+} tvd_precond;
+
+int tvd_abi_version(void);
+const char* tvd_last_error(void);
+
+/* ---- context ---------------------------------------------------------- */
+/* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) or 0 */
+int tvd_ctx_create(int device, void* stream, tvd_ctx** out);
+int tvd_ctx_set_stream(tvd_ctx* ctx, void* stream);
+int tvd_ctx_sync(tvd_ctx* ctx);
+int tvd_ctx_destroy(tvd_ctx* ctx);
+
+/* ---- blur operator H  (blur.py:197-326) -------------------------------- */
+/* psf: HOST (2m+1) x (2m+1) quadrantally symmetric, normalised.
+ * *separable receives 1 when the PSF is rank-1 (fast banded path). */
+int tvd_blur_create(tvd_ctx* ctx, int n, const double* psf, int width, int bc, tvd_blur** out,
+                    int* separable);
+int tvd_blur_destroy(tvd_blur* blur);
+/* exact H (transpose=0, blur.py:226-234) or H^T (transpose=1, blur.py:236-247) */
+int tvd_blur_apply(tvd_blur* blur, const double* in, double* out, int transpose);
+/* H^T H in  (reflective: H H, pipeline.py:175-176) */
+int tvd_blur_normal_apply(tvd_blur* blur, const double* in, double* out);
+/* eigenvalue grid lam[s,t] of the fast path (blur.py:265-291) */
+int tvd_blur_eigenvalues(tvd_blur* blur, double* lam);
+
+/* ---- TV diffusion  (tv.py:42-175, zero-Neumann) ------------------------ */
+int tvd_diffusivity(tvd_ctx* ctx, int n, double beta, double spacing, const double* u, double* a_h,
+                    double* a_v);
+int tvd_diffusion_apply(tvd_ctx* ctx, int n, double spacing, const double* a_h, const double* a_v,
+                        const double* w, double* out);
+/* block bands: diag n x n, inner (0,+-1) n x (n-1), block (+-1,0) (n-1) x n */
+int tvd_diffusion_bands(tvd_ctx* ctx, int n, double spacing, const double* a_h, const double* a_v,
+                        double* diag, double* inner, double* block);
+
+/* ---- transforms  (transforms.py:52-171) -------------------------------- */
+/* lines of length `len` (rows of a rows x len array when axis == 1, columns
+ * of a len x cols array when axis == 0); inverse selects DCT analysis */
+int tvd_transform_lines(tvd_ctx* ctx, int kind, int rows, int cols, int axis, const double* in,
+                        double* out, int inverse);
+/* X G X^T on a square n x n grid: axis 0 then axis 1 (tensor_apply_2d) */
+int tvd_transform_2d(tvd_ctx* ctx, int kind, int n, const double* in, double* out, int inverse);
+
+/* ---- preconditioner  (precond.py:369-573) ------------------------------ */
+/* Assemble eigenvalues of kind {R,D_R,R_D} (family DCT) or {M,D_M,M_D}
+ * (family SINE_HAT) from the blur eigenvalues and the diffusion bands.
+ * eig, inv_eig: n x n out.  dvec: n x n out, d_sqrt for D_X, s for X_D
+ * (may be NULL for X).  Host scalars: min/max eigenvalue, clamped count.
+ * TVD_ERR_PRECOND when 1 + alpha diag L or the eigenvalues are not > 0
+ * (*min_eig then holds the offending minimum). */
+int tvd_precond_assemble(tvd_ctx* ctx, int family, int variant, int n, double alpha,
+                         const double* lam_h, const double* diag, const double* inner,
+                         const double* block, double* eig, double* inv_eig, double* dvec,
+                         double* min_eig, double* max_eig, long long* n_clamped);
+/* z = X (inv_eig .* X^T (r / d_sqrt)) / d_sqrt   (precond.py:456-477) */
+int tvd_precond_apply_inverse(tvd_ctx* ctx, int family, int n, const double* inv_eig,
+                              const double* d_sqrt, const double* in, double* out);
+/* y = d_sqrt .* X (eig .* X^T (d_sqrt .* b))      (precond.py:463-469) */
+int tvd_precond_apply(tvd_ctx* ctx, int family, int n, const double* eig, const double* d_sqrt,
+                      const double* in, double* out);
+/* d = 1 + alpha diag (may be NULL), d_sqrt = sqrt(d), s = d^-1/2 (each nullable);
+ * TVD_ERR_SCALING when min d <= 0 (*min_d receives it). */
+int tvd_scaling(tvd_ctx* ctx, long long count, double alpha, const double* diag, double* d,
+                double* d_sqrt, double* s, double* min_d);
+
+/* ---- system and PCG  (pipeline.py:209-224, krylov.py:82-116) ----------- */
+int tvd_system_apply(tvd_ctx* ctx, const tvd_system* sys, const double* in, double* out);
+/* Full device-resident PCG.  x receives the solution (may equal x0).
+ * history: NULL or device buffer of max_iterations doubles (relative
+ * residuals).  On TVD_ERR_DIVERGED / TVD_ERR_INDEFINITE, *err_iteration and
+ * *err_value describe the failure as in the reference exceptions. */
+int tvd_pcg_solve(tvd_ctx* ctx, const tvd_system* sys, const tvd_precond* pre, const double* b,
+                  const double* x0, double* x, double tol, int max_iterations, double* history,
+                  int* iterations, int* converged, int* err_iteration, double* err_value);
+
+/* ---- vector helpers for the generic callable path ---------------------- */
+int tvd_vec_dot(tvd_ctx* ctx, long long count, const double* x, const double* y, double* out);
+/* out = a x + b y */
+int tvd_vec_axpby(tvd_ctx* ctx, long long count, double a, const double* x, double b,
+                  const double* y, double* out);
+/* out = x * y (op 0) or x / y (op 1) */
+int tvd_vec_binary(tvd_ctx* ctx, long long count, int op, const double* x, const double* y,
+                   double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TVDEBLUR_B200_H */

@@ -1,0 +1,164 @@
+"""ctypes binding of the C ABI in ``include/tvdeblur_b200.h``.
+
+This is the only place the Python mirror touches native code.  There is no
+CPU fallback: every operator in this package fails loudly (``RuntimeError``)
+when the library or a CUDA device is missing.  Device memory is owned by
+torch tensors; their raw pointers cross the ABI together with the current
+torch stream of the device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import threading
+
+import numpy as np
+import torch
+
+_LIB_PATH = pathlib.Path(__file__).resolve().parent / "libtvdeblur_b200.so"
+_lib = None
+_lock = threading.Lock()
+
+TVD_OK, TVD_ERR_INVALID, TVD_ERR_DIVERGED, TVD_ERR_INDEFINITE = 0, 1, 2, 3
+TVD_ERR_PRECOND, TVD_ERR_SCALING, TVD_ERR_CUDA = 4, 5, 6
+BC_REFLECTIVE, BC_ANTI_REFLECTIVE = 2, 3
+T_DST1, T_SINE_HAT, T_DCT = 0, 1, 2
+VARIANT_X, VARIANT_D_X, VARIANT_X_D = 0, 1, 2
+PRE_NONE, PRE_DIAG, PRE_TRANSFORM = 0, 1, 2
+
+_vp = ctypes.c_void_p
+_i = ctypes.c_int
+_d = ctypes.c_double
+_ll = ctypes.c_longlong
+
+
+class TvdSystem(ctypes.Structure):
+    _fields_ = [("blur", _vp), ("alpha", _d), ("spacing", _d),
+                ("a_h", _vp), ("a_v", _vp), ("s", _vp)]
+
+
+class TvdPrecond(ctypes.Structure):
+    _fields_ = [("kind", _i), ("family", _i), ("inv_eig", _vp), ("d", _vp)]
+
+
+_SIGNATURES = {
+    "tvd_abi_version": ([], _i),
+    "tvd_last_error": ([], ctypes.c_char_p),
+    "tvd_ctx_create": ([_i, _vp, ctypes.POINTER(_vp)], _i),
+    "tvd_ctx_set_stream": ([_vp, _vp], _i),
+    "tvd_ctx_sync": ([_vp], _i),
+    "tvd_ctx_destroy": ([_vp], _i),
+    "tvd_blur_create": ([_vp, _i, _vp, _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_i)], _i),
+    "tvd_blur_destroy": ([_vp], _i),
+    "tvd_blur_apply": ([_vp, _vp, _vp, _i], _i),
+    "tvd_blur_normal_apply": ([_vp, _vp, _vp], _i),
+    "tvd_blur_eigenvalues": ([_vp, _vp], _i),
+    "tvd_diffusivity": ([_vp, _i, _d, _d, _vp, _vp, _vp], _i),
+    "tvd_diffusion_apply": ([_vp, _i, _d, _vp, _vp, _vp, _vp], _i),
+    "tvd_diffusion_bands": ([_vp, _i, _d, _vp, _vp, _vp, _vp, _vp], _i),
+    "tvd_transform_lines": ([_vp, _i, _i, _i, _i, _vp, _vp, _i], _i),
+    "tvd_transform_2d": ([_vp, _i, _i, _vp, _vp, _i], _i),
+    "tvd_precond_assemble": ([_vp, _i, _i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                              ctypes.POINTER(_d), ctypes.POINTER(_d), ctypes.POINTER(_ll)], _i),
+    "tvd_precond_apply_inverse": ([_vp, _i, _i, _vp, _vp, _vp, _vp], _i),
+    "tvd_precond_apply": ([_vp, _i, _i, _vp, _vp, _vp, _vp], _i),
+    "tvd_scaling": ([_vp, _ll, _d, _vp, _vp, _vp, _vp, ctypes.POINTER(_d)], _i),
+    "tvd_system_apply": ([_vp, ctypes.POINTER(TvdSystem), _vp, _vp], _i),
+    "tvd_pcg_solve": ([_vp, ctypes.POINTER(TvdSystem), ctypes.POINTER(TvdPrecond), _vp, _vp, _vp,
+                       _d, _i, _vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i),
+                       ctypes.POINTER(_d)], _i),
+    "tvd_vec_dot": ([_vp, _ll, _vp, _vp, ctypes.POINTER(_d)], _i),
+    "tvd_vec_axpby": ([_vp, _ll, _d, _vp, _d, _vp, _vp], _i),
+    "tvd_vec_binary": ([_vp, _ll, _i, _vp, _vp, _vp], _i),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, message: str) -> None:
+        super().__init__(f"tvdeblur native error {code}: {message}")
+        self.code = code
+        self.message = message
+
+
+def load(path: pathlib.Path | str | None = None):
+    """Load (once) and return the ctypes library; raises if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = pathlib.Path(path) if path else _LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"native library {p} is missing; build it with "
+                "`python -m paper_1011_5964_b200.build` (no CPU fallback exists)")
+        lib = ctypes.CDLL(str(p))
+        for name, (args, res) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc != TVD_OK:
+        msg = load().tvd_last_error().decode(errors="replace")
+        raise NativeError(rc, msg)
+
+
+# ---------------------------------------------------------------- contexts
+_tls = threading.local()
+
+
+def _require_cuda(device: torch.device) -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("tvdeblur B200 path needs a CUDA device (no CPU fallback)")
+
+
+def context(device: torch.device | int | None = None) -> int:
+    """Per-thread, per-device native context bound to torch's current stream."""
+    lib = load()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                       (device if isinstance(device, int) else (device.index or 0)))
+    _require_cuda(dev)
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    h = ctxs.get(dev.index)
+    if h is None:
+        out = _vp()
+        check(lib.tvd_ctx_create(dev.index, _vp(stream), ctypes.byref(out)))
+        h = ctxs[dev.index] = out.value
+    else:
+        check(lib.tvd_ctx_set_stream(h, _vp(stream)))
+    return h
+
+
+def default_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("tvdeblur B200 path needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def to_device(x, device: torch.device | None = None) -> tuple[torch.Tensor, bool]:
+    """``(float64 contiguous CUDA tensor, came_from_numpy)``."""
+    if isinstance(x, torch.Tensor):
+        dev = x.device if x.is_cuda else (device or default_device())
+        t = x.to(device=dev, dtype=torch.float64)
+        return t.contiguous(), False
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    dev = device or default_device()
+    return torch.from_numpy(arr).to(dev), True
+
+
+def to_host_like(t: torch.Tensor, was_numpy: bool):
+    return t.cpu().numpy() if was_numpy else t

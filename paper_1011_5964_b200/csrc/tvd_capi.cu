@@ -1,0 +1,994 @@
+// Host side of the C ABI (include/tvdeblur_b200.h): contexts, FFT plans,
+// banded blur tables, preconditioner assembly and the device-resident PCG.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/tvdeblur_b200.h"
+#include "tvd_cg.h"
+#include "tvd_internal.h"
+#include "tvd_stencil.h"
+
+using namespace tvd;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define TVD_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(TVD_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+// ------------------------------------------------------------------ context
+enum Slot : int {
+  kSlotTmp = 0,
+  kSlotTmp2,
+  kSlotR,
+  kSlotZ,
+  kSlotP,
+  kSlotQ,
+  kSlotSP,
+  kSlotExtA,
+  kSlotExtB,
+  kSlotLam0,
+  kSlotLam1,
+  kSlotLamD,
+  kSlotS,
+  kSlotDiagS,
+  kSlotInnerS,
+  kSlotBlockS,
+  kSlotPartial,
+  kSlotPartial2,
+  kSlotCount
+};
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct tvd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::map<std::pair<int, int>, std::unique_ptr<TrigPlan>> plans;
+  DevBuf slots[kSlotCount];
+  PcgState* d_state = nullptr;
+  PcgState* h_state = nullptr;
+  double* h_scalar = nullptr;  // pinned scratch for host scalars (64 doubles)
+  double* d_scalar = nullptr;
+};
+
+struct tvd_blur {
+  tvd_ctx* ctx = nullptr;
+  int n = 0, m = 0, bc = 0;
+  bool separable = false;
+  std::vector<double> psf;   // host copy
+  double* d_psf = nullptr;   // device copy (general path)
+  // separable factors: axis 0 (rows index) and axis 1
+  BandOp h1[2], h1t[2], g[2];
+  std::vector<void*> owned;
+};
+
+static cudaError_t ensure(tvd_ctx* c, int slot, size_t bytes, void** out) {
+  DevBuf& b = c->slots[slot];
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      cudaError_t e = cudaStreamSynchronize(c->stream);
+      if (e != cudaSuccess) return e;
+      cudaFree(b.ptr);
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&b.ptr, bytes);
+    if (e != cudaSuccess) return e;
+    b.bytes = bytes;
+  }
+  *out = b.ptr;
+  return cudaSuccess;
+}
+
+#define TVD_SLOT(ctx, slot, count, ptr)                                                       \
+  do {                                                                                        \
+    void* p_;                                                                                 \
+    TVD_CUDA(ensure((ctx), (slot), (size_t)(count) * sizeof(double), &p_));                   \
+    (ptr) = static_cast<double*>(p_);                                                         \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ------------------------------------------------------------ FFT plans
+static std::vector<int> factorize(int L) {
+  std::vector<int> f;
+  int x = L;
+  for (int p = 2; (long)p * p <= x; ++p)
+    while (x % p == 0) {
+      f.push_back(p);
+      x /= p;
+    }
+  if (x > 1) f.push_back(x);
+  return f;
+}
+
+// (cos, sin)(pi * num / den) with octant reduction in long double.
+static void cis_pi(long long num, long long den, double* c, double* s) {
+  num %= 2 * den;
+  if (num < 0) num += 2 * den;
+  // angle in units of pi/4: t = 4 num / den
+  const long double pi = 3.141592653589793238462643383279502884L;
+  const long double a = pi * (long double)num / (long double)den;
+  long double ca, sa;
+  // reduce: use symmetric forms to keep the argument small
+  const long long q4 = (4 * num) / den;  // octant 0..7
+  long double r;
+  switch (q4) {
+    case 0: ca = cosl(a); sa = sinl(a); break;
+    case 1: r = pi / 2 - a; ca = sinl(r); sa = cosl(r); break;
+    case 2: r = a - pi / 2; ca = -sinl(r); sa = cosl(r); break;
+    case 3: r = pi - a; ca = -cosl(r); sa = sinl(r); break;
+    case 4: r = a - pi; ca = -cosl(r); sa = -sinl(r); break;
+    case 5: r = 3 * pi / 2 - a; ca = -sinl(r); sa = -cosl(r); break;
+    case 6: r = a - 3 * pi / 2; ca = sinl(r); sa = -cosl(r); break;
+    default: r = 2 * pi - a; ca = cosl(r); sa = -sinl(r); break;
+  }
+  *c = (double)ca;
+  *s = (double)sa;
+}
+
+template <class T>
+static cudaError_t upload(const std::vector<T>& h, T** d, std::vector<void*>& owned) {
+  cudaError_t e = cudaMalloc((void**)d, std::max<size_t>(1, h.size()) * sizeof(T));
+  if (e != cudaSuccess) return e;
+  owned.push_back(*d);
+  if (!h.empty()) e = cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+static int build_plan(int family, int len, std::unique_ptr<TrigPlan>& out) {
+  int L;
+  if (family == kFamDst1) L = len + 1;
+  else if (family == kFamSineHat) L = len - 1;
+  else L = len;
+  if (len < 1 || L < 1) return fail(TVD_ERR_INVALID, "transform length too small");
+  if (family == kFamSineHat && len < 3)
+    return fail(TVD_ERR_INVALID, "sine_hat requires length >= 3");
+  auto P = std::make_unique<TrigPlan>();
+  P->family = family;
+  P->n = len;
+  P->L = L;
+  std::vector<int> pr = factorize(L);
+  std::vector<int> big, small;
+  int n2 = 0;
+  for (int p : pr) {
+    if (p == 2) ++n2;
+    else if (p > 7) big.push_back(p);
+    else small.push_back(p);
+  }
+  std::sort(big.rbegin(), big.rend());
+  std::sort(small.rbegin(), small.rend());
+  std::vector<std::pair<int, int>> st;  // (radix, kind)
+  for (int p : big) st.push_back({p, kStageOdd});
+  while (n2 >= 3) { st.push_back({8, kStageReg}); n2 -= 3; }
+  if (n2 == 2) st.push_back({4, kStageReg});
+  if (n2 == 1) st.push_back({2, kStageReg});
+  for (int p : small) st.push_back({p, kStageReg});
+  if ((int)st.size() > kFftMaxStages) return fail(TVD_ERR_INVALID, "too many FFT stages");
+  for (int p : big)
+    if (p > 16383) return fail(TVD_ERR_INVALID, "FFT length has a prime factor above 16383");
+  std::vector<double2> coef, tw(L), wfull(L), whalf;
+  int ns = 1, maxi = 1;
+  P->fft.nst = (int)st.size();
+  P->fft.L = L;
+  for (size_t s = 0; s < st.size(); ++s) {
+    const int R = st[s].first;
+    FftStage& S = P->fft.st[s];
+    S.radix = R;
+    S.kind = st[s].second;
+    S.ns = ns;
+    S.coef = 0;
+    if (S.kind == kStageOdd) {
+      S.coef = (int)coef.size();
+      for (int t = 0; t < R; ++t) {
+        double c, sn;
+        cis_pi(2LL * t, R, &c, &sn);
+        coef.push_back(make_double2(c, sn));
+      }
+      const int H = (R - 1) / 2;
+      maxi = std::max(maxi, (L / R) * ((H + kFftKB - 1) / kFftKB));
+    } else {
+      maxi = std::max(maxi, L / R);
+    }
+    ns *= R;
+  }
+  for (int e = 0; e < L; ++e) {
+    double c, sn;
+    cis_pi(-2LL * e, L, &c, &sn);
+    tw[e] = make_double2(c, sn);
+    cis_pi(-(long long)e, L, &c, &sn);
+    wfull[e] = make_double2(c, sn);
+  }
+  if (family == kFamDct) {
+    whalf.resize(len);
+    for (int k = 0; k < len; ++k) {
+      double c, sn;
+      cis_pi(-(long long)k, 2LL * len, &c, &sn);
+      whalf[k] = make_double2(c, sn);
+    }
+  }
+  P->max_items_line = maxi;
+  if ((maxi + kFftSlots - 1) / kFftSlots > 512)
+    return fail(TVD_ERR_INVALID, "FFT stage too wide for one CTA");
+  double2 *dtw, *dcoef, *dwf, *dwh = nullptr;
+  if (upload(tw, &dtw, P->owned) != cudaSuccess || upload(coef, &dcoef, P->owned) != cudaSuccess ||
+      upload(wfull, &dwf, P->owned) != cudaSuccess)
+    return fail(TVD_ERR_CUDA, "plan upload failed");
+  if (family == kFamDct && upload(whalf, &dwh, P->owned) != cudaSuccess)
+    return fail(TVD_ERR_CUDA, "plan upload failed");
+  P->fft.tw = dtw;
+  P->fft.coef = dcoef;
+  P->wfull = dwf;
+  P->whalf = dwh;
+  out = std::move(P);
+  return TVD_OK;
+}
+
+static int get_plan(tvd_ctx* c, int family, int len, const TrigPlan** out) {
+  auto key = std::make_pair(family, len);
+  auto it = c->plans.find(key);
+  if (it == c->plans.end()) {
+    std::unique_ptr<TrigPlan> P;
+    int rc = build_plan(family, len, P);
+    if (rc) return rc;
+    it = c->plans.emplace(key, std::move(P)).first;
+  }
+  *out = it->second.get();
+  return TVD_OK;
+}
+
+static void free_plan(TrigPlan* P) {
+  for (void* p : P->owned) cudaFree(p);
+  P->owned.clear();
+}
+
+// ----------------------------------------------------------- line passes
+static LineGeom rows_geom(int rows, int cols) { return LineGeom{cols, rows, (long)cols, 1}; }
+static LineGeom cols_geom(int rows, int cols) { return LineGeom{rows, cols, 1, (long)cols}; }
+
+static int run_lines(tvd_ctx* c, int family, const LineGeom& g, int analysis, const LineIO& io,
+                     int* nb) {
+  const TrigPlan* P;
+  int rc = get_plan(c, family, g.len, &P);
+  if (rc) return rc;
+  TVD_CUDA(launch_trig(*P, g, analysis, io, nb, c->stream));
+  return TVD_OK;
+}
+
+static int partial_capacity(tvd_ctx* c, size_t count, double** out) {
+  TVD_SLOT(c, kSlotPartial, count, *out);
+  return TVD_OK;
+}
+
+// z = X (inv .* X^T (r / d)) / d  with optional r.z partials.  Returns #partials.
+static int precond_transform(tvd_ctx* c, int family, int n, const double* inv, const double* d,
+                             int dmul, const double* in, double* out, const double* dot_with,
+                             const int* skip, int* nb_out) {
+  if (family != kFamSineHat && family != kFamDct && family != kFamDst1)
+    return fail(TVD_ERR_INVALID, "unknown transform family");
+  double* tmp;
+  TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tmp);
+  double* partial = nullptr;
+  if (dot_with) {
+    int rc = partial_capacity(c, (size_t)n + 64, &partial);
+    if (rc) return rc;
+  }
+  LineIO a{};
+  a.in = in;
+  a.out = tmp;
+  a.pre = d;
+  a.pre_mul = dmul;
+  a.skip = skip;
+  int nb;
+  int rc = run_lines(c, family, rows_geom(n, n), 1, a, &nb);
+  if (rc) return rc;
+  LineIO b{};
+  b.in = tmp;
+  b.out = tmp;
+  b.mid_mul = inv;
+  b.skip = skip;
+  rc = run_lines(c, family, cols_geom(n, n), 1, b, &nb);
+  if (rc) return rc;
+  LineIO z{};
+  z.in = tmp;
+  z.out = out;
+  z.post = d;
+  z.post_mul = dmul;
+  z.dot_with = dot_with;
+  z.partial = partial;
+  z.skip = skip;
+  rc = run_lines(c, family, rows_geom(n, n), 0, z, &nb);
+  if (rc) return rc;
+  if (nb_out) *nb_out = nb;
+  return TVD_OK;
+}
+
+// ------------------------------------------------------------ blur tables
+struct Taps1D {
+  std::vector<double> table;  // n x (2w+1)
+  int w;
+};
+
+static void bc_map(int src, int n, int bc, int* cols, double* wts, int* cnt) {
+  if (src >= 0 && src < n) {
+    cols[0] = src; wts[0] = 1.0; *cnt = 1;
+    return;
+  }
+  if (bc == TVD_BC_ANTI_REFLECTIVE) {
+    if (src < 0) { cols[0] = 0; wts[0] = 2.0; cols[1] = -src; wts[1] = -1.0; }
+    else { const int s = src - (n - 1); cols[0] = n - 1; wts[0] = 2.0; cols[1] = n - 1 - s; wts[1] = -1.0; }
+    *cnt = 2;
+  } else {
+    if (src < 0) cols[0] = -src - 1;
+    else cols[0] = n - (src - (n - 1));
+    wts[0] = 1.0;
+    *cnt = 1;
+  }
+}
+
+// 1D blur operator of kernel g (length 2m+1): out_i = sum_a g[a] ext_{i+m-a}
+static Taps1D blur_table(const std::vector<double>& g, int n, int bc) {
+  const int m = ((int)g.size() - 1) / 2, W = 2 * m + 1;
+  Taps1D t;
+  t.w = m;
+  t.table.assign((size_t)n * W, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int k = -m; k <= m; ++k) {
+      int cols[2], cnt;
+      double wts[2];
+      bc_map(i + k, n, bc, cols, wts, &cnt);
+      for (int q = 0; q < cnt; ++q) t.table[(size_t)i * W + (cols[q] - i) + m] += wts[q] * g[m - k];
+    }
+  return t;
+}
+
+static Taps1D transpose_table(const Taps1D& a, int n) {
+  const int w = a.w, W = 2 * w + 1;
+  Taps1D t;
+  t.w = w;
+  t.table.assign((size_t)n * W, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int k = -w; k <= w; ++k) {
+      const int j = i + k;
+      if (j < 0 || j >= n) continue;
+      t.table[(size_t)i * W + k + w] = a.table[(size_t)j * W + (-k) + w];
+    }
+  return t;
+}
+
+// G = A^T A for a banded A of half-width w -> half-width 2w
+static Taps1D gram_table(const Taps1D& a, int n) {
+  const int w = a.w, W = 2 * w + 1, w2 = 2 * w, W2 = 2 * w2 + 1;
+  Taps1D t;
+  t.w = w2;
+  t.table.assign((size_t)n * W2, 0.0);
+  for (int l = 0; l < n; ++l)
+    for (int k1 = -w; k1 <= w; ++k1) {
+      const int c1 = l + k1;
+      if (c1 < 0 || c1 >= n) continue;
+      const double a1 = a.table[(size_t)l * W + k1 + w];
+      if (a1 == 0.0) continue;
+      for (int k2 = -w; k2 <= w; ++k2) {
+        const int c2 = l + k2;
+        if (c2 < 0 || c2 >= n) continue;
+        t.table[(size_t)c1 * W2 + (c2 - c1) + w2] += a1 * a.table[(size_t)l * W + k2 + w];
+      }
+    }
+  return t;
+}
+
+static int make_bandop(tvd_blur* b, const Taps1D& t, int border, BandOp* op) {
+  const int n = b->n, W = 2 * t.w + 1;
+  std::vector<double> taps(W, 0.0);
+  int B = border;
+  if (2 * B >= n) B = (n + 1) / 2;  // no interior rows
+  if (B < n - B) {
+    const int c = n / 2;
+    for (int k = 0; k <= t.w; ++k) {
+      const double v = t.table[(size_t)c * W + k + t.w];
+      taps[t.w + k] = v;
+      taps[t.w - k] = v;
+    }
+  }
+  double *dt, *dtab;
+  if (upload(taps, &dt, b->owned) != cudaSuccess || upload(t.table, &dtab, b->owned) != cudaSuccess)
+    return fail(TVD_ERR_CUDA, "band table upload failed");
+  op->n = n;
+  op->w = t.w;
+  op->B = B;
+  op->taps = dt;
+  op->table = dtab;
+  return TVD_OK;
+}
+
+// ------------------------------------------------------------ system apply
+// out = [s .*] (H^T H (s .* in) + alpha L (s .* in)); optional partial of dot_with . out
+static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double* in, double* out,
+                                 const double* dot_with, double* partial, const int* skip,
+                                 int* nb_out) {
+  tvd_blur* b = sys->blur;
+  const int n = b->n;
+  const long N = (long)n * n;
+  const double* w = in;
+  if (sys->s) {
+    double* sp;
+    TVD_SLOT(c, kSlotSP, N, sp);
+    TVD_CUDA(launch_mul(sys->s, in, sp, N, c->stream));
+    w = sp;
+  }
+  Epilogue ep{};
+  if (sys->a_h) {
+    ep.a_h = sys->a_h;
+    ep.a_v = sys->a_v;
+    ep.lw = w;
+    ep.alpha = sys->alpha;
+    ep.inv_h2 = 1.0 / (sys->spacing * sys->spacing);
+  }
+  ep.s = sys->s;
+  ep.dot_with = dot_with;
+  ep.partial = partial;
+  double* tmp;
+  TVD_SLOT(c, kSlotTmp, N, tmp);
+  if (b->separable) {
+    TVD_CUDA(launch_band_rows(b->g[1], w, tmp, skip, c->stream));
+    TVD_CUDA(launch_band_cols(b->g[0], tmp, out, ep, skip, c->stream));
+    if (nb_out) *nb_out = band_cols_blocks(n);
+  } else {
+    const int T = n + 2 * b->m;
+    double *ea, *eb, *t2;
+    TVD_SLOT(c, kSlotExtA, (size_t)T * T, ea);
+    TVD_SLOT(c, kSlotExtB, (size_t)T * T, eb);
+    TVD_SLOT(c, kSlotTmp2, N, t2);
+    TVD_CUDA(launch_general_blur(w, tmp, n, b->m, b->bc, b->d_psf, 0, ea, eb, c->stream));
+    const int back_t = b->bc == TVD_BC_REFLECTIVE ? 0 : 1;
+    TVD_CUDA(launch_general_blur(tmp, t2, n, b->m, b->bc, b->d_psf, back_t, ea, eb, c->stream));
+    TVD_CUDA(launch_normal_epilogue(t2, ep, n, out, skip, vec_blocks(), c->stream));
+    if (nb_out) *nb_out = vec_blocks();
+  }
+  return TVD_OK;
+}
+
+// ================================================================== ABI
+extern "C" {
+
+int tvd_abi_version(void) { return TVD_ABI_VERSION; }
+const char* tvd_last_error(void) { return g_last_error.c_str(); }
+
+int tvd_ctx_create(int device, void* stream, tvd_ctx** out) {
+  if (!out) return fail(TVD_ERR_INVALID, "null out pointer");
+  int count = 0;
+  TVD_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return fail(TVD_ERR_INVALID, "bad device index");
+  DeviceGuard g(device);
+  auto* c = new tvd_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  if (cudaMalloc(&c->d_state, sizeof(PcgState)) != cudaSuccess ||
+      cudaMallocHost(&c->h_state, sizeof(PcgState)) != cudaSuccess ||
+      cudaMallocHost(&c->h_scalar, 64 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->d_scalar, 64 * sizeof(double)) != cudaSuccess) {
+    delete c;
+    return fail(TVD_ERR_CUDA, "context allocation failed");
+  }
+  *out = c;
+  return TVD_OK;
+}
+
+int tvd_ctx_set_stream(tvd_ctx* c, void* stream) {
+  if (!c) return fail(TVD_ERR_INVALID, "null context");
+  c->stream = static_cast<cudaStream_t>(stream);
+  return TVD_OK;
+}
+
+int tvd_ctx_sync(tvd_ctx* c) {
+  if (!c) return fail(TVD_ERR_INVALID, "null context");
+  TVD_CUDA(cudaStreamSynchronize(c->stream));
+  return TVD_OK;
+}
+
+int tvd_ctx_destroy(tvd_ctx* c) {
+  if (!c) return TVD_OK;
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->plans) free_plan(kv.second.get());
+  for (auto& s : c->slots)
+    if (s.ptr) cudaFree(s.ptr);
+  cudaFree(c->d_state);
+  cudaFreeHost(c->h_state);
+  cudaFreeHost(c->h_scalar);
+  cudaFree(c->d_scalar);
+  delete c;
+  return TVD_OK;
+}
+
+// ---------------------------------------------------------------- blur
+int tvd_blur_create(tvd_ctx* c, int n, const double* psf, int width, int bc, tvd_blur** out,
+                    int* separable) {
+  if (!c || !psf || !out) return fail(TVD_ERR_INVALID, "null argument");
+  if (bc != TVD_BC_REFLECTIVE && bc != TVD_BC_ANTI_REFLECTIVE)
+    return fail(TVD_ERR_INVALID, "boundary condition must be reflective or anti-reflective");
+  if (width < 1 || width % 2 != 1) return fail(TVD_ERR_INVALID, "PSF needs odd width 2m+1");
+  const int m = (width - 1) / 2;
+  if (m >= n) return fail(TVD_ERR_INVALID, "PSF half-width must be below size");
+  DeviceGuard gd(c->device);
+  auto* b = new tvd_blur();
+  b->ctx = c;
+  b->n = n;
+  b->m = m;
+  b->bc = bc;
+  b->psf.assign(psf, psf + (size_t)width * width);
+  // rank-1 test: h ~= outer(g0, g1), g0 = row sums / total, g1 = column sums
+  std::vector<double> g0(width, 0.0), g1(width, 0.0);
+  double total = 0.0, hmax = 0.0;
+  for (int a = 0; a < width; ++a)
+    for (int q = 0; q < width; ++q) {
+      const double v = b->psf[(size_t)a * width + q];
+      g0[a] += v;
+      g1[q] += v;
+      total += v;
+      hmax = std::max(hmax, std::fabs(v));
+    }
+  double err = 0.0;
+  for (int a = 0; a < width; ++a)
+    for (int q = 0; q < width; ++q)
+      err = std::max(err, std::fabs(b->psf[(size_t)a * width + q] - g0[a] * g1[q] / total));
+  b->separable = total != 0.0 && err <= 1e-13 * hmax;
+  if (upload(b->psf, &b->d_psf, b->owned) != cudaSuccess) {
+    delete b;
+    return fail(TVD_ERR_CUDA, "psf upload failed");
+  }
+  if (b->separable) {
+    for (double& v : g0) v /= total;
+    const std::vector<double>* gs[2] = {&g0, &g1};
+    for (int ax = 0; ax < 2; ++ax) {
+      Taps1D h = blur_table(*gs[ax], n, bc);
+      Taps1D ht = transpose_table(h, n);
+      Taps1D gg = gram_table(h, n);
+      int rc = make_bandop(b, h, m, &b->h1[ax]);
+      if (!rc) rc = make_bandop(b, ht, 2 * m, &b->h1t[ax]);
+      if (!rc) rc = make_bandop(b, gg, 2 * m, &b->g[ax]);
+      if (rc) {
+        tvd_blur_destroy(b);
+        return rc;
+      }
+    }
+  }
+  if (separable) *separable = b->separable ? 1 : 0;
+  *out = b;
+  return TVD_OK;
+}
+
+int tvd_blur_destroy(tvd_blur* b) {
+  if (!b) return TVD_OK;
+  DeviceGuard g(b->ctx->device);
+  cudaStreamSynchronize(b->ctx->stream);
+  for (void* p : b->owned) cudaFree(p);
+  delete b;
+  return TVD_OK;
+}
+
+int tvd_blur_apply(tvd_blur* b, const double* in, double* out, int transpose) {
+  if (!b || !in || !out) return fail(TVD_ERR_INVALID, "null argument");
+  tvd_ctx* c = b->ctx;
+  DeviceGuard g(c->device);
+  const int n = b->n;
+  if (b->separable) {
+    double* tmp;
+    TVD_SLOT(c, kSlotTmp, (size_t)n * n, tmp);
+    const BandOp* ops = transpose ? b->h1t : b->h1;
+    Epilogue ep{};
+    TVD_CUDA(launch_band_cols(ops[0], in, tmp, ep, nullptr, c->stream));
+    TVD_CUDA(launch_band_rows(ops[1], tmp, out, nullptr, c->stream));
+  } else {
+    const int T = n + 2 * b->m;
+    double *ea, *eb;
+    TVD_SLOT(c, kSlotExtA, (size_t)T * T, ea);
+    TVD_SLOT(c, kSlotExtB, (size_t)T * T, eb);
+    TVD_CUDA(launch_general_blur(in, out, n, b->m, b->bc, b->d_psf, transpose ? 1 : 0, ea, eb,
+                                 c->stream));
+  }
+  return TVD_OK;
+}
+
+int tvd_blur_normal_apply(tvd_blur* b, const double* in, double* out) {
+  if (!b || !in || !out) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(b->ctx->device);
+  tvd_system sys{};
+  sys.blur = b;
+  return system_apply_internal(b->ctx, &sys, in, out, nullptr, nullptr, nullptr, nullptr);
+}
+
+int tvd_blur_eigenvalues(tvd_blur* b, double* lam) {
+  if (!b || !lam) return fail(TVD_ERR_INVALID, "null argument");
+  tvd_ctx* c = b->ctx;
+  DeviceGuard g(c->device);
+  const int n = b->n, m = b->m, K = 2 * m + 1;
+  std::vector<double> y(n), cs((size_t)n * K);
+  for (int s = 0; s < n; ++s) {
+    if (b->bc == TVD_BC_ANTI_REFLECTIVE) y[s] = s < n - 1 ? ((double)s * M_PI) / (double)(n - 1) : 0.0;
+    else y[s] = ((double)s * M_PI) / (double)n;
+  }
+  for (int s = 0; s < n; ++s)
+    for (int a = 0; a < K; ++a) cs[(size_t)s * K + a] = std::cos(y[s] * (double)(a - m));
+  double *dcs, *tmp;
+  std::vector<void*> owned;
+  if (upload(cs, &dcs, owned) != cudaSuccess) return fail(TVD_ERR_CUDA, "upload failed");
+  TVD_SLOT(c, kSlotTmp, (size_t)K * n, tmp);
+  cudaError_t e = launch_eigenvalues(dcs, b->d_psf, n, K, tmp, lam, c->stream);
+  cudaStreamSynchronize(c->stream);
+  for (void* p : owned) cudaFree(p);
+  if (e != cudaSuccess) return fail(TVD_ERR_CUDA, cudaGetErrorString(e));
+  return TVD_OK;
+}
+
+// ------------------------------------------------------------ diffusion
+int tvd_diffusivity(tvd_ctx* c, int n, double beta, double spacing, const double* u, double* a_h,
+                    double* a_v) {
+  if (!c || !u || !a_h || !a_v) return fail(TVD_ERR_INVALID, "null argument");
+  if (beta <= 0) return fail(TVD_ERR_INVALID, "beta must be positive");
+  if (spacing <= 0) return fail(TVD_ERR_INVALID, "spacing must be positive");
+  DeviceGuard g(c->device);
+  TVD_CUDA(launch_diffusivity(u, n, beta, spacing, a_h, a_v, c->stream));
+  return TVD_OK;
+}
+
+int tvd_diffusion_apply(tvd_ctx* c, int n, double spacing, const double* a_h, const double* a_v,
+                        const double* w, double* out) {
+  if (!c || !a_h || !a_v || !w || !out) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(c->device);
+  TVD_CUDA(launch_diffusion_apply(a_h, a_v, w, n, 1.0 / (spacing * spacing), out, c->stream));
+  return TVD_OK;
+}
+
+int tvd_diffusion_bands(tvd_ctx* c, int n, double spacing, const double* a_h, const double* a_v,
+                        double* diag, double* inner, double* block) {
+  if (!c || !a_h || !a_v || !diag || !inner || !block) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(c->device);
+  TVD_CUDA(launch_diffusion_bands(a_h, a_v, n, 1.0 / (spacing * spacing), diag, inner, block,
+                                  c->stream));
+  return TVD_OK;
+}
+
+// ------------------------------------------------------------ transforms
+int tvd_transform_lines(tvd_ctx* c, int kind, int rows, int cols, int axis, const double* in,
+                        double* out, int inverse) {
+  if (!c || !in || !out) return fail(TVD_ERR_INVALID, "null argument");
+  if (kind < 0 || kind > 2) return fail(TVD_ERR_INVALID, "unknown transform kind");
+  DeviceGuard g(c->device);
+  LineIO io{};
+  io.in = in;
+  io.out = out;
+  const LineGeom geom = axis == 1 ? rows_geom(rows, cols) : cols_geom(rows, cols);
+  return run_lines(c, kind, geom, inverse ? 1 : 0, io, nullptr);
+}
+
+int tvd_transform_2d(tvd_ctx* c, int kind, int n, const double* in, double* out, int inverse) {
+  int rc = tvd_transform_lines(c, kind, n, n, 0, in, out, inverse);
+  if (rc) return rc;
+  return tvd_transform_lines(c, kind, n, n, 1, out, out, inverse);
+}
+
+// -------------------------------------------------------- preconditioner
+static int host_minmax(tvd_ctx* c, const double* d_partial, int nb, double* mn, double* mx) {
+  std::vector<double> h(2 * (size_t)nb);
+  TVD_CUDA(cudaMemcpyAsync(h.data(), d_partial, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  TVD_CUDA(cudaStreamSynchronize(c->stream));
+  double a = INFINITY, z = -INFINITY;
+  for (int i = 0; i < nb; ++i) {
+    a = std::fmin(a, h[2 * i]);
+    z = std::fmax(z, h[2 * i + 1]);
+  }
+  *mn = a;
+  *mx = z;
+  return TVD_OK;
+}
+
+// level-2 projection of bands (diag[, inner, block]) into `out`, epilogue per BandLines.
+static int level2(tvd_ctx* c, const TrigPlan* P, int n, const double* diag, const double* inner,
+                  const double* block, double* out, int epi, const double* lamh, const double* lamd,
+                  double alpha, double* partial_minmax, int* nb_out) {
+  double *lam0, *lam1 = nullptr;
+  TVD_SLOT(c, kSlotLam0, (size_t)n * n, lam0);
+  BandLines a{};
+  a.b0 = diag; a.b0_ls = n; a.b0_es = 1;
+  a.b1 = inner; a.b1_ls = n - 1; a.b1_es = 1;
+  a.c1 = inner ? 2.0 : 0.0;
+  a.nlines = n;
+  a.out = lam0; a.out_ls = n; a.out_es = 1;
+  TVD_CUDA(launch_band_project(*P, 1, a, nullptr, c->stream));
+  if (block) {
+    TVD_SLOT(c, kSlotLam1, (size_t)n * n, lam1);
+    BandLines b{};
+    b.b0 = block; b.b0_ls = n; b.b0_es = 1;
+    b.nlines = n - 1;
+    b.out = lam1; b.out_ls = n; b.out_es = 1;
+    TVD_CUDA(launch_band_project(*P, 1, b, nullptr, c->stream));
+  }
+  BandLines f{};
+  f.b0 = lam0; f.b0_ls = 1; f.b0_es = n;
+  f.b1 = lam1; f.b1_ls = 1; f.b1_es = n;
+  f.c1 = lam1 ? 2.0 : 0.0;
+  f.nlines = n;
+  f.out = out; f.out_ls = 1; f.out_es = n;
+  f.epi = epi;
+  f.lamh = lamh;
+  f.lamd = lamd;
+  f.alpha = alpha;
+  f.partial_minmax = partial_minmax;
+  TVD_CUDA(launch_band_project(*P, 0, f, nb_out, c->stream));
+  return TVD_OK;
+}
+
+int tvd_scaling(tvd_ctx* c, long long count, double alpha, const double* diag, double* d,
+                double* d_sqrt, double* s, double* min_d) {
+  if (!c || !diag) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(c->device);
+  double* part;
+  TVD_SLOT(c, kSlotPartial2, vec_blocks(), part);
+  TVD_CUDA(launch_scaling(diag, alpha, d, d_sqrt, s, count, part, vec_blocks(), c->stream));
+  std::vector<double> h(vec_blocks());
+  TVD_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  TVD_CUDA(cudaStreamSynchronize(c->stream));
+  double mn = INFINITY;
+  for (double v : h) mn = std::fmin(mn, v);
+  if (min_d) *min_d = mn;
+  if (!(mn > 0.0)) return fail(TVD_ERR_SCALING, "diagonal scaling has nonpositive entries");
+  return TVD_OK;
+}
+
+int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alpha,
+                         const double* lam_h, const double* diag, const double* inner,
+                         const double* block, double* eig, double* inv_eig, double* dvec,
+                         double* min_eig, double* max_eig, long long* n_clamped) {
+  if (!c || !lam_h || !diag || !inner || !block || !eig || !inv_eig)
+    return fail(TVD_ERR_INVALID, "null argument");
+  if (family != TVD_TRANSFORM_SINE_HAT && family != TVD_TRANSFORM_DCT)
+    return fail(TVD_ERR_INVALID, "preconditioner family must be SINE_HAT or DCT");
+  if (variant < 0 || variant > 2) return fail(TVD_ERR_INVALID, "unknown variant");
+  if (alpha <= 0) return fail(TVD_ERR_INVALID, "alpha must be positive");
+  DeviceGuard g(c->device);
+  const TrigPlan* P;
+  int rc = get_plan(c, family, n, &P);
+  if (rc) return rc;
+  const long N = (long)n * n;
+  // d = 1 + alpha diag L must be positive (precond.py:558-560)
+  double* s = nullptr;
+  double* dsq = nullptr;
+  if (variant == TVD_VARIANT_X_D) {
+    if (dvec) s = dvec;
+    else TVD_SLOT(c, kSlotS, N, s);
+  } else if (variant == TVD_VARIANT_D_X) {
+    dsq = dvec;
+  }
+  double mind;
+  rc = tvd_scaling(c, N, alpha, diag, nullptr, dsq, s, &mind);
+  if (rc == TVD_ERR_SCALING) {
+    if (min_eig) *min_eig = mind;
+    return fail(TVD_ERR_PRECOND, "1 + alpha diag L has nonpositive entries");
+  }
+  if (rc) return rc;
+  double* mm;
+  TVD_SLOT(c, kSlotPartial2, 2 * (size_t)n + 64, mm);
+  int nb = 0;
+  if (variant == TVD_VARIANT_X_D) {
+    double *lamd, *ds, *is, *bs;
+    TVD_SLOT(c, kSlotLamD, N, lamd);
+    TVD_SLOT(c, kSlotDiagS, N, ds);
+    TVD_SLOT(c, kSlotInnerS, N, is);
+    TVD_SLOT(c, kSlotBlockS, N, bs);
+    rc = level2(c, P, n, s, nullptr, nullptr, lamd, 0, nullptr, nullptr, 0.0, nullptr, nullptr);
+    if (rc) return rc;
+    TVD_CUDA(launch_scale_bands(diag, inner, block, s, n, ds, is, bs, c->stream));
+    rc = level2(c, P, n, ds, is, bs, eig, 2, lam_h, lamd, alpha, mm, &nb);
+  } else {
+    rc = level2(c, P, n, diag, inner, block, eig, 1, lam_h, nullptr, alpha, mm, &nb);
+  }
+  if (rc) return rc;
+  double mn, mx;
+  rc = host_minmax(c, mm, nb, &mn, &mx);
+  if (rc) return rc;
+  if (min_eig) *min_eig = mn;
+  if (max_eig) *max_eig = mx;
+  if (!(mn > 0.0)) return fail(TVD_ERR_PRECOND, "preconditioner is indefinite");
+  const double floor = 1e-14 * mx;
+  double* part;
+  TVD_SLOT(c, kSlotPartial, vec_blocks(), part);
+  TVD_CUDA(launch_invert_eigs(eig, floor, inv_eig, N, part, vec_blocks(), c->stream));
+  std::vector<double> h(vec_blocks());
+  TVD_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  TVD_CUDA(cudaStreamSynchronize(c->stream));
+  double cnt = 0.0;
+  for (double v : h) cnt += v;
+  if (n_clamped) *n_clamped = (long long)cnt;
+  return TVD_OK;
+}
+
+int tvd_precond_apply_inverse(tvd_ctx* c, int family, int n, const double* inv_eig,
+                              const double* d_sqrt, const double* in, double* out) {
+  if (!c || !inv_eig || !in || !out) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(c->device);
+  return precond_transform(c, family, n, inv_eig, d_sqrt, 0, in, out, nullptr, nullptr, nullptr);
+}
+
+int tvd_precond_apply(tvd_ctx* c, int family, int n, const double* eig, const double* d_sqrt,
+                      const double* in, double* out) {
+  if (!c || !eig || !in || !out) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(c->device);
+  return precond_transform(c, family, n, eig, d_sqrt, 1, in, out, nullptr, nullptr, nullptr);
+}
+
+// ------------------------------------------------------------- system/PCG
+static int check_system(const tvd_system* sys) {
+  if (!sys || !sys->blur) return fail(TVD_ERR_INVALID, "null system");
+  if ((sys->a_h == nullptr) != (sys->a_v == nullptr))
+    return fail(TVD_ERR_INVALID, "a_h and a_v must both be set");
+  if (sys->a_h && !(sys->spacing > 0)) return fail(TVD_ERR_INVALID, "spacing must be positive");
+  return TVD_OK;
+}
+
+int tvd_system_apply(tvd_ctx* c, const tvd_system* sys, const double* in, double* out) {
+  if (!c || !in || !out) return fail(TVD_ERR_INVALID, "null argument");
+  int rc = check_system(sys);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  return system_apply_internal(c, sys, in, out, nullptr, nullptr, nullptr, nullptr);
+}
+
+// z = M^{-1} r with r.z partials; z may alias r for kind NONE.
+static int minv_internal(tvd_ctx* c, const tvd_precond* pre, int n, const double* r, double* z,
+                         double* partial, const int* skip, int* nb) {
+  const long N = (long)n * n;
+  if (!pre || pre->kind == TVD_PRECOND_NONE) {
+    if (z != r) TVD_CUDA(launch_copy(r, z, N, skip, c->stream));
+    TVD_CUDA(launch_dot_partials(r, r, N, partial, vec_blocks(), skip, c->stream));
+    *nb = vec_blocks();
+    return TVD_OK;
+  }
+  if (pre->kind == TVD_PRECOND_DIAG) {
+    TVD_CUDA(launch_diag_solve(r, pre->d, z, N, partial, vec_blocks(), skip, c->stream));
+    *nb = vec_blocks();
+    return TVD_OK;
+  }
+  if (pre->kind == TVD_PRECOND_TRANSFORM)
+    return precond_transform(c, pre->family, n, pre->inv_eig, pre->d, 0, r, z, r, skip, nb);
+  return fail(TVD_ERR_INVALID, "unknown preconditioner kind");
+}
+
+int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, const double* b,
+                  const double* x0, double* x, double tol, int max_iterations, double* history,
+                  int* iterations, int* converged, int* err_iteration, double* err_value) {
+  if (!c || !b || !x0 || !x) return fail(TVD_ERR_INVALID, "null argument");
+  int rc = check_system(sys);
+  if (rc) return rc;
+  if (!(tol > 0)) return fail(TVD_ERR_INVALID, "tol must be positive");
+  if (max_iterations < 1) return fail(TVD_ERR_INVALID, "max_iterations must be at least 1");
+  if (pre && pre->kind == TVD_PRECOND_TRANSFORM && !pre->inv_eig)
+    return fail(TVD_ERR_INVALID, "transform preconditioner needs inverse eigenvalues");
+  if (pre && pre->kind == TVD_PRECOND_DIAG && !pre->d)
+    return fail(TVD_ERR_INVALID, "diagonal preconditioner needs d");
+  DeviceGuard g(c->device);
+  const int n = sys->blur->n;
+  const long N = (long)n * n;
+  cudaStream_t st = c->stream;
+  double *r, *z, *p, *q, *partial;
+  TVD_SLOT(c, kSlotR, N, r);
+  TVD_SLOT(c, kSlotZ, N, z);
+  TVD_SLOT(c, kSlotP, N, p);
+  TVD_SLOT(c, kSlotQ, N, q);
+  const size_t pcap = std::max<size_t>({(size_t)band_cols_blocks(n), (size_t)vec_blocks(),
+                                        (size_t)n + 64});
+  TVD_SLOT(c, kSlotPartial, pcap, partial);
+  const bool identity = !pre || pre->kind == TVD_PRECOND_NONE;
+  double* zz = identity ? r : z;
+  if (x != x0) TVD_CUDA(cudaMemcpyAsync(x, x0, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  PcgState* S = c->d_state;
+  const int* skip = &S->done;
+  int nb;
+  // r = b - A x ; r0 = ||r||
+  rc = system_apply_internal(c, sys, x, q, nullptr, nullptr, nullptr, &nb);
+  if (rc) return rc;
+  TVD_CUDA(launch_residual_init(b, q, r, N, partial, vec_blocks(), st));
+  TVD_CUDA(launch_pcg_start(S, partial, vec_blocks(), st));
+  // z = M^-1 r ; p = z ; rz = r.z
+  rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb);
+  if (rc) return rc;
+  TVD_CUDA(launch_pcg_rz0(S, partial, nb, st));
+  TVD_CUDA(launch_copy(zz, p, N, skip, st));
+  int chunk = 4;
+  for (int done_it = 0;;) {
+    for (int k = 0; k < chunk; ++k) {
+      rc = system_apply_internal(c, sys, p, q, p, partial, skip, &nb);
+      if (rc) return rc;
+      TVD_CUDA(launch_pcg_gamma(S, partial, nb, st));
+      TVD_CUDA(launch_pcg_update_xr(S, x, r, p, q, N, partial, vec_blocks(), st));
+      TVD_CUDA(launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
+      rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb);
+      if (rc) return rc;
+      TVD_CUDA(launch_pcg_beta(S, partial, nb, max_iterations, st));
+      TVD_CUDA(launch_pcg_update_p(S, p, zz, N, st));
+    }
+    done_it += chunk;
+    TVD_CUDA(cudaMemcpyAsync(c->h_state, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+    TVD_CUDA(cudaStreamSynchronize(st));
+    if (c->h_state->done) break;
+    if (chunk < 16) chunk *= 2;
+  }
+  const PcgState& h = *c->h_state;
+  if (iterations) *iterations = h.iters;
+  if (converged) *converged = h.converged;
+  if (err_iteration) *err_iteration = h.err_iter;
+  if (err_value) *err_value = h.err_val;
+  if (h.status == kErrDiverged) return fail(TVD_ERR_DIVERGED, "pcg produced non-finite values");
+  if (h.status == kErrIndefinite) return fail(TVD_ERR_INDEFINITE, "pcg met nonpositive curvature");
+  return TVD_OK;
+}
+
+// ------------------------------------------------------------- vectors
+int tvd_vec_dot(tvd_ctx* c, long long count, const double* x, const double* y, double* out) {
+  if (!c || !x || !y || !out) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(c->device);
+  double* part;
+  TVD_SLOT(c, kSlotPartial2, vec_blocks(), part);
+  TVD_CUDA(launch_dot_partials(x, y, count, part, vec_blocks(), nullptr, c->stream));
+  TVD_CUDA(launch_sum_partials(part, vec_blocks(), c->d_scalar, c->stream));
+  TVD_CUDA(cudaMemcpyAsync(c->h_scalar, c->d_scalar, sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  TVD_CUDA(cudaStreamSynchronize(c->stream));
+  *out = c->h_scalar[0];
+  return TVD_OK;
+}
+
+int tvd_vec_axpby(tvd_ctx* c, long long count, double a, const double* x, double b, const double* y,
+                  double* out) {
+  if (!c || !x || !y || !out) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(c->device);
+  TVD_CUDA(launch_axpby(a, x, b, y, out, count, c->stream));
+  return TVD_OK;
+}
+
+int tvd_vec_binary(tvd_ctx* c, long long count, int op, const double* x, const double* y,
+                   double* out) {
+  if (!c || !x || !y || !out) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(c->device);
+  if (op == 0) TVD_CUDA(launch_mul(x, y, out, count, c->stream));
+  else if (op == 1) TVD_CUDA(launch_div(x, y, out, count, c->stream));
+  else return fail(TVD_ERR_INVALID, "unknown op");
+  return TVD_OK;
+}
+
+}  // extern "C"

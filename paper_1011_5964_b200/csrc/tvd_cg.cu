@@ -1,0 +1,334 @@
+// PCG state machine + vector kernels.  The recurrence, its check order and its
+// error semantics follow krylov.py:82-116 exactly; vector updates use explicit
+// round-to-nearest ops so they match numpy's `x += step * p` bit for bit.
+// Reductions are deterministic: fixed grids write per-CTA partials, one
+// 512-thread CTA sums them in a fixed order.
+#include <cmath>
+
+#include "tvd_cg.h"
+
+namespace tvd {
+
+constexpr int kVecThreads = 256;
+int vec_blocks() { return kRedBlocks; }
+
+__device__ __forceinline__ double sum_partials_block(const double* partial, int nb) {
+  __shared__ double red[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) v += partial[i];
+  return block_sum(v, red);
+}
+
+__global__ void k_sum_partials(const double* partial, int nb, double* out) {
+  const double s = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void k_residual_init(const double* __restrict__ b, const double* __restrict__ q,
+                                double* __restrict__ r, long N, double* partial) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    const double v = __dsub_rn(b[g], q[g]);
+    r[g] = v;
+    acc += v * v;
+  }
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void k_pcg_start(PcgState* s, const double* partial, int nb) {
+  const double rr = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) {
+    s->r0 = sqrt(rr);
+    s->k = 1;
+    s->status = kOk;
+    s->err_iter = 0;
+    s->err_val = 0.0;
+    s->converged = 0;
+    s->iters = 0;
+    s->done = 0;
+    if (s->r0 == 0.0) {
+      s->done = 1;
+      s->iters = 0;
+      s->converged = 1;
+    }
+  }
+}
+
+__global__ void k_pcg_rz0(PcgState* s, const double* partial, int nb) {
+  if (s->done) return;
+  const double rz = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) s->rz = rz;
+}
+
+__global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst, long N, const int* skip) {
+  if (skip && *skip) return;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x)
+    dst[g] = src[g];
+}
+
+__global__ void k_pcg_gamma(PcgState* s, const double* partial, int nb) {
+  if (s->done) return;
+  const double gamma = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) {
+    s->gamma = gamma;
+    if (!isfinite(gamma)) {
+      s->status = kErrDiverged;
+      s->err_iter = s->k;
+      s->done = 1;
+    } else if (gamma <= 0.0) {
+      s->status = kErrIndefinite;
+      s->err_iter = s->k;
+      s->err_val = gamma;
+      s->done = 1;
+    } else {
+      s->step = s->rz / gamma;
+    }
+  }
+}
+
+__global__ void k_pcg_update_xr(const PcgState* s, double* __restrict__ x, double* __restrict__ r,
+                                const double* __restrict__ p, const double* __restrict__ q, long N,
+                                double* partial) {
+  if (s->done) return;
+  __shared__ double red[32];
+  const double step = s->step;
+  double acc = 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    x[g] = __dadd_rn(x[g], __dmul_rn(step, p[g]));
+    const double v = __dsub_rn(r[g], __dmul_rn(step, q[g]));
+    r[g] = v;
+    acc += v * v;
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+__global__ void k_pcg_rel(PcgState* s, const double* partial, int nb, double tol, double* hist) {
+  if (s->done) return;
+  const double rr = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) {
+    const double rel = sqrt(rr) / s->r0;
+    s->rel = rel;
+    if (!isfinite(rel)) {
+      s->status = kErrDiverged;
+      s->err_iter = s->k;
+      s->done = 1;
+      return;
+    }
+    if (hist) hist[s->k - 1] = rel;
+    if (rel < tol) {
+      s->iters = s->k;
+      s->converged = 1;
+      s->done = 1;
+    }
+  }
+}
+
+__global__ void k_pcg_beta(PcgState* s, const double* partial, int nb, int max_it) {
+  if (s->done) return;
+  const double rz_next = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) {
+    s->beta = rz_next / s->rz;
+    s->rz = rz_next;
+    s->k += 1;
+    if (s->k > max_it) {
+      s->iters = max_it;
+      s->converged = 0;
+      s->done = 1;
+    }
+  }
+}
+
+__global__ void k_pcg_update_p(const PcgState* s, double* __restrict__ p, const double* __restrict__ z,
+                               long N) {
+  if (s->done) return;
+  const double beta = s->beta;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x)
+    p[g] = __dadd_rn(z[g], __dmul_rn(beta, p[g]));
+}
+
+__global__ void k_diag_solve(const double* __restrict__ r, const double* __restrict__ d,
+                             double* __restrict__ z, long N, double* partial, const int* skip) {
+  if (skip && *skip) return;
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    const double v = __ddiv_rn(r[g], d[g]);
+    z[g] = v;
+    acc += r[g] * v;
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0 && partial) partial[blockIdx.x] = t;
+}
+
+__global__ void k_dot_partials(const double* __restrict__ x, const double* __restrict__ y, long N,
+                               double* partial, const int* skip) {
+  if (skip && *skip) return;
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x)
+    acc += x[g] * y[g];
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+__global__ void k_axpby(double a, const double* __restrict__ x, double b, const double* __restrict__ y,
+                        double* __restrict__ out, long N) {
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    const double u = a == 1.0 ? x[g] : __dmul_rn(a, x[g]);
+    const double v = b == 1.0 ? y[g] : __dmul_rn(b, y[g]);
+    out[g] = __dadd_rn(u, v);
+  }
+}
+
+__global__ void k_mul(const double* __restrict__ x, const double* __restrict__ y, double* __restrict__ out,
+                      long N) {
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x)
+    out[g] = __dmul_rn(x[g], y[g]);
+}
+
+__global__ void k_div(const double* __restrict__ x, const double* __restrict__ y, double* __restrict__ out,
+                      long N) {
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x)
+    out[g] = __ddiv_rn(x[g], y[g]);
+}
+
+__global__ void k_scaling(const double* __restrict__ diag, double alpha, double* d, double* dsq,
+                          double* s, long N, double* partial_min) {
+  __shared__ double red[32];
+  double mn = 1.0 / 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    const double v = __dadd_rn(1.0, __dmul_rn(alpha, diag[g]));
+    if (d) d[g] = v;
+    if (dsq) dsq[g] = __dsqrt_rn(v);
+    if (s) s[g] = pow(v, -0.5);
+    mn = fmin(mn, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, red[w]);
+    partial_min[blockIdx.x] = m;
+  }
+}
+
+__global__ void k_scale_bands(const double* __restrict__ diag, const double* __restrict__ inner,
+                              const double* __restrict__ block, const double* __restrict__ s, int n,
+                              double* diag_s, double* inner_s, double* block_s) {
+  const long N = (long)n * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(g / n), j = (int)(g % n);
+    diag_s[g] = __dmul_rn(__dmul_rn(diag[g], s[g]), s[g]);
+    if (j < n - 1) {
+      const long h = (long)i * (n - 1) + j;
+      inner_s[h] = __dmul_rn(__dmul_rn(inner[h], s[g]), s[g + 1]);
+    }
+    if (i < n - 1) block_s[g] = __dmul_rn(__dmul_rn(block[g], s[g]), s[g + n]);
+  }
+}
+
+__global__ void k_invert_eigs(const double* __restrict__ lam, double floor, double* __restrict__ inv,
+                              long N, double* partial) {
+  __shared__ double red[32];
+  double cnt = 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    const double v = lam[g];
+    if (v < floor) cnt += 1.0;
+    inv[g] = __ddiv_rn(1.0, fmax(v, floor));
+  }
+  const double t = block_sum(cnt, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// ------------------------------------------------------------- launchers
+#define TVD_VEC_GRID kRedBlocks, kVecThreads, 0, st
+
+cudaError_t launch_sum_partials(const double* partial, int nb, double* out, cudaStream_t st) {
+  k_sum_partials<<<1, 512, 0, st>>>(partial, nb, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_residual_init(const double* b, const double* q, double* r, long N, double* partial,
+                                 int, cudaStream_t st) {
+  k_residual_init<<<TVD_VEC_GRID>>>(b, q, r, N, partial);
+  return cudaGetLastError();
+}
+cudaError_t launch_pcg_start(PcgState* s, const double* partial, int nb, cudaStream_t st) {
+  k_pcg_start<<<1, 512, 0, st>>>(s, partial, nb);
+  return cudaGetLastError();
+}
+cudaError_t launch_pcg_rz0(PcgState* s, const double* partial, int nb, cudaStream_t st) {
+  k_pcg_rz0<<<1, 512, 0, st>>>(s, partial, nb);
+  return cudaGetLastError();
+}
+cudaError_t launch_copy(const double* src, double* dst, long N, const int* skip, cudaStream_t st) {
+  k_copy<<<TVD_VEC_GRID>>>(src, dst, N, skip);
+  return cudaGetLastError();
+}
+cudaError_t launch_pcg_gamma(PcgState* s, const double* partial, int nb, cudaStream_t st) {
+  k_pcg_gamma<<<1, 512, 0, st>>>(s, partial, nb);
+  return cudaGetLastError();
+}
+cudaError_t launch_pcg_update_xr(PcgState* s, double* x, double* r, const double* p, const double* q,
+                                 long N, double* partial, int, cudaStream_t st) {
+  k_pcg_update_xr<<<TVD_VEC_GRID>>>(s, x, r, p, q, N, partial);
+  return cudaGetLastError();
+}
+cudaError_t launch_pcg_rel(PcgState* s, const double* partial, int nb, double tol, double* hist,
+                           cudaStream_t st) {
+  k_pcg_rel<<<1, 512, 0, st>>>(s, partial, nb, tol, hist);
+  return cudaGetLastError();
+}
+cudaError_t launch_pcg_beta(PcgState* s, const double* partial, int nb, int max_it, cudaStream_t st) {
+  k_pcg_beta<<<1, 512, 0, st>>>(s, partial, nb, max_it);
+  return cudaGetLastError();
+}
+cudaError_t launch_pcg_update_p(PcgState* s, double* p, const double* z, long N, cudaStream_t st) {
+  k_pcg_update_p<<<TVD_VEC_GRID>>>(s, p, z, N);
+  return cudaGetLastError();
+}
+cudaError_t launch_diag_solve(const double* r, const double* d, double* z, long N, double* partial, int,
+                              const int* skip, cudaStream_t st) {
+  k_diag_solve<<<TVD_VEC_GRID>>>(r, d, z, N, partial, skip);
+  return cudaGetLastError();
+}
+cudaError_t launch_dot_partials(const double* x, const double* y, long N, double* partial, int,
+                                const int* skip, cudaStream_t st) {
+  k_dot_partials<<<TVD_VEC_GRID>>>(x, y, N, partial, skip);
+  return cudaGetLastError();
+}
+cudaError_t launch_axpby(double a, const double* x, double b, const double* y, double* out, long N,
+                         cudaStream_t st) {
+  k_axpby<<<TVD_VEC_GRID>>>(a, x, b, y, out, N);
+  return cudaGetLastError();
+}
+cudaError_t launch_mul(const double* x, const double* y, double* out, long N, cudaStream_t st) {
+  k_mul<<<TVD_VEC_GRID>>>(x, y, out, N);
+  return cudaGetLastError();
+}
+cudaError_t launch_div(const double* x, const double* y, double* out, long N, cudaStream_t st) {
+  k_div<<<TVD_VEC_GRID>>>(x, y, out, N);
+  return cudaGetLastError();
+}
+cudaError_t launch_scaling(const double* diag, double alpha, double* d, double* dsq, double* s, long N,
+                           double* partial_min, int, cudaStream_t st) {
+  k_scaling<<<TVD_VEC_GRID>>>(diag, alpha, d, dsq, s, N, partial_min);
+  return cudaGetLastError();
+}
+cudaError_t launch_scale_bands(const double* diag, const double* inner, const double* block,
+                               const double* s, int n, double* diag_s, double* inner_s,
+                               double* block_s, cudaStream_t st) {
+  k_scale_bands<<<TVD_VEC_GRID>>>(diag, inner, block, s, n, diag_s, inner_s, block_s);
+  return cudaGetLastError();
+}
+cudaError_t launch_invert_eigs(const double* lam, double floor, double* inv, long N, double* partial,
+                               int, cudaStream_t st) {
+  k_invert_eigs<<<TVD_VEC_GRID>>>(lam, floor, inv, N, partial);
+  return cudaGetLastError();
+}
+
+}  // namespace tvd

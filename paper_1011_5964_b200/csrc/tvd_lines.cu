@@ -1,0 +1,425 @@
+// Line passes of the trigonometric transforms (reference transforms.py:52-171,
+// precond.py:82-199 / 369-395 / 456-477).
+//
+// A CTA owns `nl` lines of an n x n fp64 array (rows when axis == 1, columns
+// when axis == 0).  Each pass:
+//   global -> real staging (smem, optional elementwise pre-division)
+//   -> pack into complex FFT lines -> fft_lines -> unpack to real staging
+//   [-> multiply by an eigenvalue grid -> second transform]   (sandwich)
+//   -> global (optional post-division, optional fused dot partial).
+// DST-I (and the bordered Shat) use one length-(N+1) complex FFT per line:
+//   c_j = z_{2j} + i z_{2((j+h) mod L)+1}  (L odd, h = (L-1)/2),
+// where z is the odd extension of the line; then
+//   y_k = -(Im C_k - (-1)^k Re C_k) / 2 * sqrt(2/L).
+// For even L the standard even/odd real-FFT split is used.
+// DCT-II / DCT-III use Makhoul's reordering with two real lines packed into
+// one complex FFT of length n.
+#include "tvd_internal.h"
+
+namespace tvd {
+
+struct TrigK {
+  FftPlan fft;
+  const double2* wfull;
+  const double2* whalf;
+  int family, n, L, nl, analysis, nlines;  // n = line length
+  long ls, es;
+  int P;   // real staging pitch (doubles)
+  int LP;  // complex line pitch
+  int ncx; // complex lines per CTA
+  double s0, s1, inv_s0, inv_s1, dst_scale;
+  LineIO io;
+};
+
+// ------------------------------------------------------------------ DST
+__device__ __forceinline__ void dst_lines(const TrigK& p, double* real, double2* cbuf) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int off = p.family == kFamSineHat ? 1 : 0;
+  const int L = p.L, N = L - 1;
+  const bool odd = (L & 1);
+  const int h = (L - 1) / 2;
+  for (int i = tid; i < p.nl * L; i += nth) {
+    const int l = i / L, j = i - l * L;
+    const double* x = real + l * p.P + off - 1;  // x[t], t = 1..N
+    auto z = [&](int t) -> double {
+      if (t == 0 || t == L) return 0.0;
+      return t < L ? x[t] : -x[2 * L - t];
+    };
+    int jj = j;
+    if (odd) {
+      jj = j + h;
+      if (jj >= L) jj -= L;
+    }
+    cbuf[l * p.LP + j] = make_double2(z(2 * j), z(2 * jj + 1));
+  }
+  __syncthreads();
+  fft_lines(cbuf, p.LP, p.nl, p.fft);
+  for (int i = tid; i < p.nl * N; i += nth) {
+    const int l = i / N, k = 1 + i - l * N;
+    const double2* c = cbuf + l * p.LP;
+    double y;
+    if (odd) {
+      const double2 C = c[k];
+      y = (k & 1) ? -(C.y + C.x) : -(C.y - C.x);
+    } else {
+      const double2 C = c[k], Cr = cconj(c[L - k]);
+      const double2 E = cscale(cadd(C, Cr), 0.5);
+      const double2 D = csub(C, Cr);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      const double2 w = p.wfull[k];
+      y = -(E.y + (w.x * O.y + w.y * O.x));
+    }
+    real[l * p.P + off + k - 1] = y * p.dst_scale;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ DCT
+__device__ __forceinline__ int makhoul(int j, int n) {
+  return j < (n + 1) / 2 ? 2 * j : 2 * (n - 1 - j) + 1;
+}
+
+// DCT-II (analysis, C^T v), two lines per complex FFT.
+__device__ __forceinline__ void dct2_lines(const TrigK& p, double* real, double2* cbuf) {
+  const int tid = threadIdx.x, nth = blockDim.x, n = p.n;
+  for (int i = tid; i < p.ncx * n; i += nth) {
+    const int q = i / n, j = i - q * n, src = makhoul(j, n);
+    cbuf[q * p.LP + j] = make_double2(real[(2 * q) * p.P + src], real[(2 * q + 1) * p.P + src]);
+  }
+  __syncthreads();
+  fft_lines(cbuf, p.LP, p.ncx, p.fft);
+  for (int i = tid; i < p.ncx * n; i += nth) {
+    const int q = i / n, k = i - q * n;
+    const double2* c = cbuf + q * p.LP;
+    const double2 C = c[k], Cr = cconj(c[k == 0 ? 0 : n - k]);
+    const double2 Va = cscale(cadd(C, Cr), 0.5);
+    const double2 D = csub(C, Cr);
+    const double2 Vb = make_double2(0.5 * D.y, -0.5 * D.x);
+    const double2 w = p.whalf[k];
+    const double s = k == 0 ? p.s0 : p.s1;
+    real[(2 * q) * p.P + k] = s * (w.x * Va.x - w.y * Va.y);
+    real[(2 * q + 1) * p.P + k] = s * (w.x * Vb.x - w.y * Vb.y);
+  }
+  __syncthreads();
+}
+
+// DCT-III (synthesis, C v), two lines per complex FFT.
+__device__ __forceinline__ void dct3_lines(const TrigK& p, double* real, double2* cbuf) {
+  const int tid = threadIdx.x, nth = blockDim.x, n = p.n;
+  for (int i = tid; i < p.ncx * n; i += nth) {
+    const int q = i / n, k = i - q * n;
+    const double* ra = real + (2 * q) * p.P;
+    const double* rb = real + (2 * q + 1) * p.P;
+    const double is = k == 0 ? p.inv_s0 : p.inv_s1;
+    const double ya = ra[k] * is, yb = rb[k] * is;
+    const double yar = k == 0 ? 0.0 : ra[n - k] * p.inv_s1;
+    const double ybr = k == 0 ? 0.0 : rb[n - k] * p.inv_s1;
+    const double2 w = cconj(p.whalf[k]);  // exp(+i pi k / 2n)
+    const double2 Va = cmul(w, make_double2(ya, -yar));
+    const double2 Vb = cmul(w, make_double2(yb, -ybr));
+    // V = Va + i Vb ; store conj(V) so a forward FFT yields n * conj(ifft(V))
+    cbuf[q * p.LP + k] = make_double2(Va.x - Vb.y, -(Va.y + Vb.x));
+  }
+  __syncthreads();
+  fft_lines(cbuf, p.LP, p.ncx, p.fft);
+  const double inv_n = 1.0 / n;
+  for (int i = tid; i < p.ncx * n; i += nth) {
+    const int q = i / n, j = i - q * n, dst = makhoul(j, n);
+    const double2 C = cbuf[q * p.LP + j];
+    real[(2 * q) * p.P + dst] = C.x * inv_n;
+    real[(2 * q + 1) * p.P + dst] = -C.y * inv_n;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void transform_lines(const TrigK& p, double* real, double2* cbuf,
+                                                bool analysis) {
+  if (p.family == kFamDct) {
+    if (analysis) dct2_lines(p, real, cbuf);
+    else dct3_lines(p, real, cbuf);
+  } else {
+    dst_lines(p, real, cbuf);
+  }
+}
+
+__global__ void __launch_bounds__(512) k_trig(const TrigK p) {
+  const LineIO& io = p.io;
+  if (io.skip && *io.skip) return;
+  extern __shared__ double2 smem2[];
+  double2* cbuf = smem2;
+  double* real = reinterpret_cast<double*>(smem2 + (size_t)p.ncx * p.LP);
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nth = blockDim.x, n = p.n;
+  const int line0 = blockIdx.x * p.nl;
+  const int nlv = min(p.nl, p.nlines - line0);
+  const bool contig = p.es == 1;
+  // (l, t) of the i-th element in memory-friendly order
+  auto lt = [&](int i, int& l, int& t) {
+    if (contig) { l = i / n; t = i - l * n; }
+    else { t = i / nlv; l = i - t * nlv; }
+  };
+  auto gidx = [&](int l, int t) { return (long)(line0 + l) * p.ls + (long)t * p.es; };
+
+  for (int i = tid; i < nlv * n; i += nth) {
+    int l, t;
+    lt(i, l, t);
+    const long g = gidx(l, t);
+    double v = io.in[g];
+    if (io.pre) v = io.pre_mul ? v * io.pre[g] : v / io.pre[g];
+    real[l * p.P + t] = v;
+  }
+  for (int i = tid; i < (p.nl - nlv) * n; i += nth) {
+    const int l = nlv + i / n, t = i % n;
+    real[l * p.P + t] = 0.0;
+  }
+  __syncthreads();
+
+  const bool sandwich = io.mid_mul != nullptr;
+  transform_lines(p, real, cbuf, sandwich ? true : p.analysis != 0);
+  if (sandwich) {
+    for (int i = tid; i < nlv * n; i += nth) {
+      int l, t;
+      lt(i, l, t);
+      real[l * p.P + t] *= io.mid_mul[gidx(l, t)];
+    }
+    __syncthreads();
+    transform_lines(p, real, cbuf, false);
+  }
+
+  double acc = 0.0;
+  for (int i = tid; i < nlv * n; i += nth) {
+    int l, t;
+    lt(i, l, t);
+    const long g = gidx(l, t);
+    double v = real[l * p.P + t];
+    if (io.post) v = io.post_mul ? v * io.post[g] : v / io.post[g];
+    io.out[g] = v;
+    if (io.dot_with) acc += v * io.dot_with[g];
+  }
+  if (io.partial) {
+    const double s = block_sum(acc, red);
+    if (tid == 0) io.partial[blockIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------ band projections
+struct BandK {
+  FftPlan fft;
+  const double2* wfull;
+  int family, n, L, nl, LP;
+  BandLines b;
+};
+
+__global__ void __launch_bounds__(512) k_band(const BandK p) {
+  extern __shared__ double2 smem2[];
+  double2* cbuf = smem2;
+  double* tot = reinterpret_cast<double*>(smem2 + (size_t)p.nl * p.LP);  // 2 * nl
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nth = blockDim.x, n = p.n, L = p.L;
+  const BandLines& b = p.b;
+  const int line0 = blockIdx.x * p.nl;
+  const int nlv = min(p.nl, b.nlines - line0);
+  const bool sine = p.family != kFamDct;
+  auto B0 = [&](int l, int j) { return b.b0[(long)(line0 + l) * b.b0_ls + (long)j * b.b0_es]; };
+  auto B1 = [&](int l, int j) { return b.b1[(long)(line0 + l) * b.b1_ls + (long)j * b.b1_es]; };
+
+  for (int i = tid; i < p.nl * L; i += nth) {
+    const int l = i / L, j = i - l * L;
+    double e = 0.0, o = 0.0;
+    if (l < nlv) {
+      if (sine) {
+        // even slots 2j <- b0[j] (j = 1..N), odd slots 2j+1 <- c1 b1[j] (j = 1..N-1)
+        if (j >= 1 && j <= L - 1) e = B0(l, j);
+        if (b.b1 && j >= 1 && j <= L - 2) o = b.c1 * B1(l, j);
+      } else {
+        // even slots 2j <- c1 b1[j-1] (j = 1..n-1), odd slots 2j+1 <- b0[j]
+        if (b.b1 && j >= 1) e = b.c1 * B1(l, j - 1);
+        o = B0(l, j);
+      }
+    }
+    cbuf[l * p.LP + j] = make_double2(e, o);
+  }
+  // per-line band totals (one warp per line, fixed order)
+  {
+    const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+    for (int l = wid; l < p.nl; l += nw) {
+      double t0 = 0.0, t1 = 0.0;
+      if (l < nlv) {
+        const int lo = sine ? 1 : 0, hi0 = sine ? n - 1 : n, hi1 = sine ? n - 2 : n - 1;
+        for (int j = lo + lane; j < hi0; j += 32) t0 += B0(l, j);
+        if (b.b1)
+          for (int j = lo + lane; j < hi1; j += 32) t1 += B1(l, j);
+      }
+      t0 = warp_sum(t0);
+      t1 = warp_sum(t1);
+      if (lane == 0) {
+        tot[2 * l] = t0;
+        tot[2 * l + 1] = t1;
+      }
+    }
+  }
+  __syncthreads();
+  fft_lines(cbuf, p.LP, p.nl, p.fft);
+
+  double vmin = 1.0 / 0.0, vmax = -1.0 / 0.0;
+  for (int i = tid; i < nlv * n; i += nth) {
+    const int l = i / n, t = i - l * n;
+    double v;
+    if (sine && (t == 0 || t == n - 1)) {
+      v = B0(l, t);
+    } else {
+      const double2* c = cbuf + l * p.LP;
+      const int tr = t == 0 ? 0 : L - t;
+      const double2 C = c[t], Cr = cconj(c[tr]);
+      const double2 E = cscale(cadd(C, Cr), 0.5);
+      const double2 D = csub(C, Cr);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      const double2 w = p.wfull[t];
+      const double re_s = E.x + (w.x * O.x - w.y * O.y);
+      const double t0 = tot[2 * l], t1 = tot[2 * l + 1];
+      if (sine) {
+        v = (t0 + b.c1 * t1 * w.x - re_s) / L;
+      } else {
+        const double rho2 = (t == 0 ? 1.0 : 2.0) / n;
+        v = 0.5 * rho2 * (t0 + b.c1 * t1 * w.x + re_s);
+      }
+    }
+    const long g = (long)(line0 + l) * b.out_ls + (long)t * b.out_es;
+    if (b.epi == 1) {
+      const double lh = b.lamh[g];
+      v = lh * lh + b.alpha * v;
+    } else if (b.epi == 2) {
+      const double lh = b.lamh[g], ld = b.lamd[g];
+      v = lh * lh * ld * ld + b.alpha * v;
+    }
+    b.out[g] = v;
+    vmin = fmin(vmin, v);
+    vmax = fmax(vmax, v);
+  }
+  if (b.epi != 0) {
+    // deterministic block min / max
+    for (int o = 16; o > 0; o >>= 1) {
+      vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+      vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    __syncthreads();
+    const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+    if (lane == 0) {
+      red[wid] = vmin;
+      red[16 + wid] = vmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = red[0], z = red[16];
+      for (int w = 1; w < nw; ++w) {
+        a = fmin(a, red[w]);
+        z = fmax(z, red[16 + w]);
+      }
+      b.partial_minmax[2 * blockIdx.x] = a;
+      b.partial_minmax[2 * blockIdx.x + 1] = z;
+    }
+  }
+}
+
+// ------------------------------------------------------------- launchers
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Lines per CTA / threads / smem for a trig pass.
+int trig_lines_per_cta(const TrigPlan& P, bool contiguous, int* nthreads, size_t* smem) {
+  const int n = P.n;
+  const bool dct = P.family == kFamDct;
+  const int pitch = n | 1;
+  const size_t cbytes = (size_t)P.L * 16;
+  const size_t rbytes = (size_t)pitch * 8;
+  const size_t budget = 100 * 1024;
+  int nl = contiguous ? 4 : 8;
+  auto bytes = [&](int k) { return (dct ? (size_t)(k / 2) : (size_t)k) * cbytes + k * rbytes; };
+  const int step = dct ? 2 : 1;
+  while (nl > step && bytes(nl) > budget) nl -= step;
+  if (bytes(nl) > 200 * 1024) return -1;
+  int nth = round_up((P.max_items_line + kFftSlots - 1) / kFftSlots, 32);
+  if (nth < 256) nth = 256;
+  if (nth > 512) return -1;
+  *nthreads = nth;
+  *smem = bytes(nl);
+  return nl;
+}
+
+int trig_blocks(const TrigPlan& P, const LineGeom& g) {
+  int nth;
+  size_t smem;
+  const int nl = trig_lines_per_cta(P, g.es == 1, &nth, &smem);
+  return nl <= 0 ? -1 : (g.nlines + nl - 1) / nl;
+}
+
+cudaError_t launch_trig(const TrigPlan& P, const LineGeom& g, int analysis, const LineIO& io,
+                        int* nblocks_out, cudaStream_t st) {
+  int nth;
+  size_t smem;
+  if (g.len != P.n) return cudaErrorInvalidValue;
+  const int nl = trig_lines_per_cta(P, g.es == 1, &nth, &smem);
+  if (nl <= 0) return cudaErrorInvalidConfiguration;
+  TrigK k{};
+  k.fft = P.fft;
+  k.wfull = P.wfull;
+  k.whalf = P.whalf;
+  k.family = P.family;
+  k.n = P.n;
+  k.L = P.L;
+  k.nl = nl;
+  k.analysis = analysis;
+  k.nlines = g.nlines;
+  k.ls = g.ls;
+  k.es = g.es;
+  k.P = P.n | 1;
+  k.LP = P.L;
+  k.ncx = P.family == kFamDct ? nl / 2 : nl;
+  k.s0 = sqrt(1.0 / P.n);
+  k.s1 = sqrt(2.0 / P.n);
+  k.inv_s0 = 1.0 / k.s0;
+  k.inv_s1 = 1.0 / k.s1;
+  k.dst_scale = 0.5 * sqrt(2.0 / P.L);
+  k.io = io;
+  const int nb = (g.nlines + nl - 1) / nl;
+  if (nblocks_out) *nblocks_out = nb;
+  if (nb == 0) return cudaSuccess;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_trig, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_done = true;
+  }
+  k_trig<<<nb, nth, smem, st>>>(k);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
+                                int* nblocks_out, cudaStream_t st) {
+  (void)axis;
+  BandK k{};
+  k.fft = P.fft;
+  k.wfull = P.wfull;
+  k.family = P.family;
+  k.n = P.n;
+  k.L = P.L;
+  k.LP = P.L;
+  k.b = b;
+  int nl = 4;
+  const size_t cbytes = (size_t)P.L * 16;
+  while (nl > 1 && nl * cbytes > 100 * 1024) --nl;
+  k.nl = nl;
+  int nth = round_up((P.max_items_line + kFftSlots - 1) / kFftSlots, 32);
+  if (nth < 256) nth = 256;
+  if (nth > 512) return cudaErrorInvalidConfiguration;
+  const size_t smem = nl * cbytes + 2 * nl * sizeof(double);
+  const int nb = (b.nlines + nl - 1) / nl;
+  if (nblocks_out) *nblocks_out = nb;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_done = true;
+  }
+  k_band<<<nb, nth, smem, st>>>(k);
+  return cudaGetLastError();
+}
+
+}  // namespace tvd

@@ -1,0 +1,437 @@
+// Stencil-type kernels: separable banded blur passes (H, H^T, G = H1^T H1),
+// the fused normal-equation epilogue (+ alpha L w, X_D scaling, p.q partial),
+// the TV diffusivity / 5-point operator / block bands, the general
+// (non-separable) 2D PSF path, and the blur eigenvalue grid.
+//
+// Reference anchors: blur.py:45-50,163-190,226-247,265-291; tv.py:42-71,
+// 96-108,138-175; pipeline.py:145-164,209-210.
+#include "tvd_stencil.h"
+
+namespace tvd {
+
+// ------------------------------------------------------------ band passes
+// Row pass: out[i][j] = sum_k B[j][j+k] in[i][j+k]  (B applied along axis 1).
+constexpr int kRowTileR = 8;
+constexpr int kRowTileC = 256;
+
+__global__ void __launch_bounds__(256) k_band_rows(BandOp op, const double* __restrict__ in,
+                                                   double* __restrict__ out, const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ double sm[];
+  const int n = op.n, w = op.w, W = 2 * w + 1;
+  const int width = kRowTileC + 2 * w;
+  double* taps = sm;
+  double* x = sm + W;
+  const int i0 = blockIdx.y * kRowTileR, j0 = blockIdx.x * kRowTileC;
+  for (int t = threadIdx.x; t < W; t += blockDim.x) taps[t] = op.taps[t];
+  for (int r = 0; r < kRowTileR; ++r) {
+    const int row = i0 + r;
+    for (int c = threadIdx.x; c < width; c += blockDim.x) {
+      const int col = j0 - w + c;
+      x[r * width + c] = (row < n && col >= 0 && col < n) ? in[(long)row * n + col] : 0.0;
+    }
+  }
+  __syncthreads();
+  const int j = j0 + threadIdx.x;
+  if (j >= n) return;
+  const bool interior = j >= op.B && j < n - op.B;
+  const double* trow = op.table + (long)j * W;
+  for (int r = 0; r < kRowTileR; ++r) {
+    const int row = i0 + r;
+    if (row >= n) break;
+    const double* xc = x + r * width + threadIdx.x + w;
+    double acc;
+    if (interior) {
+      acc = taps[w] * xc[0];
+      for (int k = 1; k <= w; ++k) acc += taps[w + k] * (xc[-k] + xc[k]);
+    } else {
+      acc = 0.0;
+      for (int k = -w; k <= w; ++k) acc += __ldg(&trow[k + w]) * xc[k];
+    }
+    out[(long)row * n + j] = acc;
+  }
+}
+
+// Column pass: out[i][j] = sum_k B[i][i+k] in[i+k][j]  (B applied along axis 0)
+// with an optional normal-equation epilogue.
+constexpr int kColTileC = 32;
+constexpr int kColTileR = 64;
+
+__global__ void __launch_bounds__(256) k_band_cols(BandOp op, const double* __restrict__ in,
+                                                   double* __restrict__ out, Epilogue ep,
+                                                   const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const int n = op.n, w = op.w, W = 2 * w + 1;
+  const int height = kColTileR + 2 * w;
+  double* taps = sm;
+  double* x = sm + W;
+  const int i0 = blockIdx.y * kColTileR, j0 = blockIdx.x * kColTileC;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < W; t += blockDim.x) taps[t] = op.taps[t];
+  const int col = j0 + tx;
+  for (int rr = ty; rr < height; rr += 8) {
+    const int row = i0 - w + rr;
+    x[rr * kColTileC + tx] = (col < n && row >= 0 && row < n) ? in[(long)row * n + col] : 0.0;
+  }
+  __syncthreads();
+  double acc_dot = 0.0;
+  if (col < n) {
+    for (int r = ty; r < kColTileR; r += 8) {
+      const int i = i0 + r;
+      if (i >= n) break;
+      const double* xc = x + (r + w) * kColTileC + tx;
+      double acc;
+      if (i >= op.B && i < n - op.B) {
+        acc = taps[w] * xc[0];
+        for (int k = 1; k <= w; ++k)
+          acc += taps[w + k] * (xc[-k * kColTileC] + xc[k * kColTileC]);
+      } else {
+        const double* trow = op.table + (long)i * W;
+        acc = 0.0;
+        for (int k = -w; k <= w; ++k) acc += __ldg(&trow[k + w]) * xc[k * kColTileC];
+      }
+      const long g = (long)i * n + col;
+      if (ep.a_h) acc = acc + ep.alpha * diffusion_at(ep.a_h, ep.a_v, ep.lw, n, i, col, ep.inv_h2);
+      if (ep.s) acc = ep.s[g] * acc;
+      out[g] = acc;
+      if (ep.dot_with) acc_dot += ep.dot_with[g] * acc;
+    }
+  }
+  if (ep.partial) {
+    const double s = block_sum(acc_dot, red);
+    if (threadIdx.x == 0) ep.partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+int band_rows_blocks(int n) { return ((n + kRowTileC - 1) / kRowTileC) * ((n + kRowTileR - 1) / kRowTileR); }
+int band_cols_blocks(int n) { return ((n + kColTileC - 1) / kColTileC) * ((n + kColTileR - 1) / kColTileR); }
+
+cudaError_t launch_band_rows(const BandOp& op, const double* in, double* out, const int* skip,
+                             cudaStream_t st) {
+  const int n = op.n;
+  dim3 grid((n + kRowTileC - 1) / kRowTileC, (n + kRowTileR - 1) / kRowTileR);
+  const size_t smem = (size_t)(2 * op.w + 1 + kRowTileR * (kRowTileC + 2 * op.w)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_band_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  k_band_rows<<<grid, 256, smem, st>>>(op, in, out, skip);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_band_cols(const BandOp& op, const double* in, double* out, const Epilogue& ep,
+                             const int* skip, cudaStream_t st) {
+  const int n = op.n;
+  dim3 grid((n + kColTileC - 1) / kColTileC, (n + kColTileR - 1) / kColTileR);
+  const size_t smem = (size_t)(2 * op.w + 1 + kColTileC * (kColTileR + 2 * op.w)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_band_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  k_band_cols<<<grid, 256, smem, st>>>(op, in, out, ep, skip);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- TV diffusion
+// Edge-padded (zero-Neumann ghost = border) differences, divided by spacing,
+// accumulated in the reference's order so the result is bit-identical to
+// numpy (no FMA contraction: __dadd_rn / __dmul_rn).
+__device__ __forceinline__ double u_at(const double* u, int n, int r, int c) {
+  r = r < 0 ? 0 : (r >= n ? n - 1 : r);
+  c = c < 0 ? 0 : (c >= n ? n - 1 : c);
+  return u[(long)r * n + c];
+}
+// dx[r][c] over the padded grid g (r in [0,n+2), c in [0,n+1)) = (g[r][c+1]-g[r][c]) / sp
+__device__ __forceinline__ double dxg(const double* u, int n, int r, int c, double sp) {
+  return __ddiv_rn(__dsub_rn(u_at(u, n, r - 1, c), u_at(u, n, r - 1, c - 1)), sp);
+}
+// dy[r][c] (r in [0,n+1), c in [0,n+2)) = (g[r+1][c]-g[r][c]) / sp
+__device__ __forceinline__ double dyg(const double* u, int n, int r, int c, double sp) {
+  return __ddiv_rn(__dsub_rn(u_at(u, n, r, c - 1), u_at(u, n, r - 1, c - 1)), sp);
+}
+
+__global__ void k_diffusivity(const double* __restrict__ u, int n, double beta, double sp,
+                              double* __restrict__ a_h, double* __restrict__ a_v) {
+  const double bb = __dmul_rn(beta, beta);
+  const long nh = (long)n * (n + 1);
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < 2 * nh;
+       e += (long)gridDim.x * blockDim.x) {
+    if (e < nh) {  // horizontal edge (i, j), i in [0,n), j in [0,n]
+      const int i = (int)(e / (n + 1)), j = (int)(e % (n + 1));
+      const double d = dxg(u, n, i + 1, j, sp);
+      double t = __dadd_rn(dyg(u, n, i, j, sp), dyg(u, n, i + 1, j, sp));
+      t = __dadd_rn(t, dyg(u, n, i, j + 1, sp));
+      t = __dadd_rn(t, dyg(u, n, i + 1, j + 1, sp));
+      t = __dmul_rn(0.25, t);
+      const double q = __dadd_rn(__dadd_rn(__dmul_rn(d, d), __dmul_rn(t, t)), bb);
+      a_h[e] = __ddiv_rn(1.0, __dsqrt_rn(q));
+    } else {       // vertical edge (i, j), i in [0,n], j in [0,n)
+      const long f = e - nh;
+      const int i = (int)(f / n), j = (int)(f % n);
+      const double d = dyg(u, n, i, j + 1, sp);
+      double t = __dadd_rn(dxg(u, n, i, j, sp), dxg(u, n, i, j + 1, sp));
+      t = __dadd_rn(t, dxg(u, n, i + 1, j, sp));
+      t = __dadd_rn(t, dxg(u, n, i + 1, j + 1, sp));
+      t = __dmul_rn(0.25, t);
+      const double q = __dadd_rn(__dadd_rn(__dmul_rn(d, d), __dmul_rn(t, t)), bb);
+      a_v[f] = __ddiv_rn(1.0, __dsqrt_rn(q));
+    }
+  }
+}
+
+__global__ void k_diffusion_apply(const double* __restrict__ a_h, const double* __restrict__ a_v,
+                                  const double* __restrict__ w, int n, double inv_h2,
+                                  double* __restrict__ out) {
+  const long N = (long)n * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(g / n), j = (int)(g % n);
+    out[g] = diffusion_at(a_h, a_v, w, n, i, j, inv_h2);
+  }
+}
+
+__global__ void k_diffusion_bands(const double* __restrict__ a_h, const double* __restrict__ a_v,
+                                  int n, double inv_h2, double* __restrict__ diag,
+                                  double* __restrict__ inner, double* __restrict__ block) {
+  const long N = (long)n * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(g / n), j = (int)(g % n);
+    const long h0 = (long)i * (n + 1) + j;
+    double d = __dadd_rn(__dadd_rn(__dadd_rn(a_h[h0], a_h[h0 + 1]), a_v[(long)i * n + j]),
+                         a_v[(long)(i + 1) * n + j]);
+    if (j == 0) d = __dsub_rn(d, a_h[(long)i * (n + 1)]);
+    if (j == n - 1) d = __dsub_rn(d, a_h[(long)i * (n + 1) + n]);
+    if (i == 0) d = __dsub_rn(d, a_v[j]);
+    if (i == n - 1) d = __dsub_rn(d, a_v[(long)n * n + j]);
+    diag[g] = __dmul_rn(inv_h2, d);
+    if (j < n - 1) inner[(long)i * (n - 1) + j] = __dmul_rn(inv_h2, -a_h[h0 + 1]);
+    if (i < n - 1) block[g] = __dmul_rn(inv_h2, -a_v[(long)(i + 1) * n + j]);
+  }
+}
+
+static int grid_for(long work, int threads) {
+  long b = (work + threads - 1) / threads;
+  if (b > 16L * kSMs) b = 16L * kSMs;
+  return (int)(b < 1 ? 1 : b);
+}
+
+cudaError_t launch_diffusivity(const double* u, int n, double beta, double sp, double* a_h,
+                               double* a_v, cudaStream_t st) {
+  k_diffusivity<<<grid_for(2L * n * (n + 1), 256), 256, 0, st>>>(u, n, beta, sp, a_h, a_v);
+  return cudaGetLastError();
+}
+cudaError_t launch_diffusion_apply(const double* a_h, const double* a_v, const double* w, int n,
+                                   double inv_h2, double* out, cudaStream_t st) {
+  k_diffusion_apply<<<grid_for((long)n * n, 256), 256, 0, st>>>(a_h, a_v, w, n, inv_h2, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_diffusion_bands(const double* a_h, const double* a_v, int n, double inv_h2,
+                                   double* diag, double* inner, double* block, cudaStream_t st) {
+  k_diffusion_bands<<<grid_for((long)n * n, 256), 256, 0, st>>>(a_h, a_v, n, inv_h2, diag, inner,
+                                                                 block);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------- general (non-separable) PSF
+// ext = pad_axis1(pad_axis0(u)) with the np.pad rules of blur.py:45-50.
+__device__ __forceinline__ int refl_index(int t, int n, int bc, double* wgt_edge, int* edge) {
+  // returns the mirrored index for an out-of-range t; *wgt_edge = 2 for AR (edge term)
+  if (t < 0) {
+    *edge = 0;
+    if (bc == 3) { *wgt_edge = 2.0; return -t; }
+    *wgt_edge = 0.0;
+    return -t - 1;
+  }
+  *edge = n - 1;
+  const int s = t - (n - 1);
+  if (bc == 3) { *wgt_edge = 2.0; return n - 1 - s; }
+  *wgt_edge = 0.0;
+  return n - s;
+}
+
+__device__ __forceinline__ double ext_row(const double* u, int n, int bc, int r, int c) {
+  if (r >= 0 && r < n) return u[(long)r * n + c];
+  double we; int edge;
+  const int rr = refl_index(r, n, bc, &we, &edge);
+  const double v = u[(long)rr * n + c];
+  return we != 0.0 ? 2.0 * u[(long)edge * n + c] - v : v;
+}
+
+__global__ void k_extend(const double* __restrict__ u, int n, int m, int bc, double* __restrict__ ext) {
+  const int T = n + 2 * m;
+  const long N = (long)T * T;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(g / T) - m, c = (int)(g % T) - m;
+    double v;
+    if (c >= 0 && c < n) {
+      v = ext_row(u, n, bc, r, c);
+    } else {
+      double we; int edge;
+      const int cc = refl_index(c, n, bc, &we, &edge);
+      const double vr = ext_row(u, n, bc, r, cc);
+      v = we != 0.0 ? 2.0 * ext_row(u, n, bc, r, edge) - vr : vr;
+    }
+    ext[g] = v;
+  }
+}
+
+// valid convolution: out[i][j] = sum_ab ext[i+a][j+b] h[2m-a][2m-b]
+__global__ void k_conv_valid(const double* __restrict__ ext, int n, int m,
+                             const double* __restrict__ h, double* __restrict__ out) {
+  const int T = n + 2 * m, K = 2 * m + 1;
+  const long N = (long)n * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(g / n), j = (int)(g % n);
+    double acc = 0.0;
+    for (int a = 0; a < K; ++a) {
+      const double* er = ext + (long)(i + a) * T + j;
+      const double* hr = h + (long)(K - 1 - a) * K + (K - 1);
+      for (int b = 0; b < K; ++b) acc += er[b] * __ldg(&hr[-b]);
+    }
+    out[g] = acc;
+  }
+}
+
+// full convolution: full[r][c] = sum_ab h[a][b] y[r-a][c-b]
+__global__ void k_conv_full(const double* __restrict__ y, int n, int m,
+                            const double* __restrict__ h, double* __restrict__ full) {
+  const int T = n + 2 * m, K = 2 * m + 1;
+  const long N = (long)T * T;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(g / T), c = (int)(g % T);
+    double acc = 0.0;
+    for (int a = 0; a < K; ++a) {
+      const int yr = r - a;
+      if (yr < 0 || yr >= n) continue;
+      for (int b = 0; b < K; ++b) {
+        const int yc = c - b;
+        if (yc < 0 || yc >= n) continue;
+        acc += __ldg(&h[a * K + b]) * y[(long)yr * n + yc];
+      }
+    }
+    full[g] = acc;
+  }
+}
+
+// Adjoint of the extension along one axis (blur.py:170-190).
+// in: rows_in x cols (axis 0) or rows x cols_in (axis 1); out drops 2m along that axis.
+__global__ void k_fold(const double* __restrict__ in, int len_in, int other, int m, int bc,
+                       int axis, double* __restrict__ out) {
+  const int n = len_in - 2 * m;
+  const long N = (long)n * other;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    int k, o;  // k: index along the folded axis in [0,n), o: other index
+    if (axis == 0) { k = (int)(g / other); o = (int)(g % other); }
+    else { o = (int)(g / n); k = (int)(g % n); }
+    auto at = [&](int t) -> double {
+      return axis == 0 ? in[(long)t * other + o] : in[(long)o * len_in + t];
+    };
+    double v = at(m + k);
+    if (bc == 3) {
+      if (k == 0) {
+        double s = 0.0;
+        for (int t = 0; t < m; ++t) s += at(t);
+        v += 2.0 * s;
+      } else if (k <= m) {
+        v -= at(m - k);
+      }
+      if (k == n - 1) {
+        double s = 0.0;
+        for (int t = 0; t < m; ++t) s += at(m + n + t);
+        v += 2.0 * s;
+      } else if (k >= n - 1 - m) {
+        v -= at(m + n + (n - 2 - k));
+      }
+    } else {
+      if (k < m) v += at(m - 1 - k);
+      if (k >= n - m) v += at(m + n + (n - 1 - k));
+    }
+    out[axis == 0 ? (long)k * other + o : (long)o * n + k] = v;
+  }
+}
+
+cudaError_t launch_general_blur(const double* in, double* out, int n, int m, int bc,
+                                const double* h, int transpose, double* scratch_a,
+                                double* scratch_b, cudaStream_t st) {
+  const int T = n + 2 * m;
+  if (!transpose) {
+    k_extend<<<grid_for((long)T * T, 256), 256, 0, st>>>(in, n, m, bc, scratch_a);
+    k_conv_valid<<<grid_for((long)n * n, 256), 256, 0, st>>>(scratch_a, n, m, h, out);
+  } else {
+    k_conv_full<<<grid_for((long)T * T, 256), 256, 0, st>>>(in, n, m, h, scratch_a);
+    k_fold<<<grid_for((long)n * T, 256), 256, 0, st>>>(scratch_a, T, T, m, bc, 0, scratch_b);
+    k_fold<<<grid_for((long)n * n, 256), 256, 0, st>>>(scratch_b, T, n, m, bc, 1, out);
+  }
+  return cudaGetLastError();
+}
+
+// q = base (+ alpha L w) (s-scaled) with p.q partials -- for the general path.
+__global__ void k_normal_epilogue(const double* __restrict__ base, Epilogue ep, int n,
+                                  double* __restrict__ out, const int* skip) {
+  if (skip && *skip) return;
+  __shared__ double red[32];
+  const long N = (long)n * n;
+  double acc_dot = 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(g / n), j = (int)(g % n);
+    double acc = base[g];
+    if (ep.a_h) acc = acc + ep.alpha * diffusion_at(ep.a_h, ep.a_v, ep.lw, n, i, j, ep.inv_h2);
+    if (ep.s) acc = ep.s[g] * acc;
+    out[g] = acc;
+    if (ep.dot_with) acc_dot += ep.dot_with[g] * acc;
+  }
+  if (ep.partial) {
+    const double s = block_sum(acc_dot, red);
+    if (threadIdx.x == 0) ep.partial[blockIdx.x] = s;
+  }
+}
+
+cudaError_t launch_normal_epilogue(const double* base, const Epilogue& ep, int n, double* out,
+                                   const int* skip, int nblocks, cudaStream_t st) {
+  k_normal_epilogue<<<nblocks, 256, 0, st>>>(base, ep, n, out, skip);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------- blur eigenvalue grid
+// lam[s][t] = sum_a c[s][a] sum_b h[a][b] c[t][b]   (blur.py:137-160, 276-291)
+__global__ void k_eig_stage1(const double* __restrict__ c, const double* __restrict__ h, int n, int K,
+                             double* __restrict__ tmp) {  // tmp[a][t]
+  const long N = (long)K * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int a = (int)(g / n), t = (int)(g % n);
+    double acc = 0.0;
+    for (int b = 0; b < K; ++b) acc += h[a * K + b] * c[(long)t * K + b];
+    tmp[g] = acc;
+  }
+}
+__global__ void k_eig_stage2(const double* __restrict__ c, const double* __restrict__ tmp, int n,
+                             int K, double* __restrict__ lam) {
+  const long N = (long)n * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int s = (int)(g / n), t = (int)(g % n);
+    double acc = 0.0;
+    for (int a = 0; a < K; ++a) acc += c[(long)s * K + a] * tmp[(long)a * n + t];
+    lam[g] = acc;
+  }
+}
+
+cudaError_t launch_eigenvalues(const double* cos_tab, const double* h, int n, int K, double* tmp,
+                               double* lam, cudaStream_t st) {
+  k_eig_stage1<<<grid_for((long)K * n, 256), 256, 0, st>>>(cos_tab, h, n, K, tmp);
+  k_eig_stage2<<<grid_for((long)n * n, 256), 256, 0, st>>>(cos_tab, tmp, n, K, lam);
+  return cudaGetLastError();
+}
+
+}  // namespace tvd

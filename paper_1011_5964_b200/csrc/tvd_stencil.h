@@ -1,0 +1,68 @@
+// Declarations for the stencil / convolution kernels (tvd_stencil.cu).
+#pragma once
+
+#include "tvd_common.cuh"
+
+namespace tvd {
+
+// One-dimensional banded operator B (n x n) of half-width w.  Rows in
+// [B, n - B) are Toeplitz with the symmetric `taps`; the others read `table`.
+struct BandOp {
+  int n, w, B;
+  const double* taps;   // 2w+1 (device)
+  const double* table;  // n x (2w+1), table[i*(2w+1) + k + w] = B[i][i+k] (device)
+};
+
+// Epilogue of the normal-equation column pass:
+//   q = [s *] (acc + alpha * L(lw)),  partial += dot_with . q
+struct Epilogue {
+  const double* a_h;
+  const double* a_v;
+  const double* lw;
+  double alpha;
+  double inv_h2;
+  const double* s;
+  const double* dot_with;
+  double* partial;
+};
+
+// (L w)[i][j] of tv.py:96-108 with zero-Neumann ghosts, reference op order.
+__device__ __forceinline__ double diffusion_at(const double* __restrict__ a_h,
+                                               const double* __restrict__ a_v,
+                                               const double* __restrict__ w, int n, int i, int j,
+                                               double inv_h2) {
+  const long g = (long)i * n + j;
+  const double wc = w[g];
+  const double wl = j > 0 ? w[g - 1] : wc;
+  const double wr = j < n - 1 ? w[g + 1] : wc;
+  const double wu = i > 0 ? w[g - n] : wc;
+  const double wd = i < n - 1 ? w[g + n] : wc;
+  const long h0 = (long)i * (n + 1) + j;
+  const double fl = __dmul_rn(a_h[h0], __dsub_rn(wc, wl));
+  const double fr = __dmul_rn(a_h[h0 + 1], __dsub_rn(wr, wc));
+  const double fu = __dmul_rn(a_v[g], __dsub_rn(wc, wu));
+  const double fd = __dmul_rn(a_v[g + n], __dsub_rn(wd, wc));
+  return __dmul_rn(-inv_h2, __dadd_rn(__dsub_rn(fr, fl), __dsub_rn(fd, fu)));
+}
+
+int band_rows_blocks(int n);
+int band_cols_blocks(int n);
+cudaError_t launch_band_rows(const BandOp& op, const double* in, double* out, const int* skip,
+                             cudaStream_t st);
+cudaError_t launch_band_cols(const BandOp& op, const double* in, double* out, const Epilogue& ep,
+                             const int* skip, cudaStream_t st);
+cudaError_t launch_diffusivity(const double* u, int n, double beta, double sp, double* a_h,
+                               double* a_v, cudaStream_t st);
+cudaError_t launch_diffusion_apply(const double* a_h, const double* a_v, const double* w, int n,
+                                   double inv_h2, double* out, cudaStream_t st);
+cudaError_t launch_diffusion_bands(const double* a_h, const double* a_v, int n, double inv_h2,
+                                   double* diag, double* inner, double* block, cudaStream_t st);
+cudaError_t launch_general_blur(const double* in, double* out, int n, int m, int bc,
+                                const double* h, int transpose, double* scratch_a,
+                                double* scratch_b, cudaStream_t st);
+cudaError_t launch_normal_epilogue(const double* base, const Epilogue& ep, int n, double* out,
+                                   const int* skip, int nblocks, cudaStream_t st);
+cudaError_t launch_eigenvalues(const double* cos_tab, const double* h, int n, int K, double* tmp,
+                               double* lam, cudaStream_t st);
+
+}  // namespace tvd

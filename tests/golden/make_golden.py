@@ -1,0 +1,174 @@
+"""Generate golden vectors by running the REAL reference (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--big]
+
+The reference package ``tvdeblur`` is pure Python and imports in the build
+container; it does not exist on the GPU box, so its outputs are frozen here as
+``.npz`` fixtures.  Inputs are seeded (numpy ``default_rng`` / PCG64) and the
+restore fixtures use the build's BASELINE generator
+(``paper_1011_5964_b200.harness``) with the reference's own ``gen_psf`` /
+``blur_and_observe`` so the observation is exactly what the reference sees.
+
+Files written:
+* ``ops_n{N}.npz``     -- per-op outputs (H, H^T exact and fast, eigenvalues,
+  diffusivity, L w, diagonal, block bands, 2D transforms, preconditioner
+  eigenvalues and M^{-1} r for R/D_R/R_D/M/D_M/M_D) at small N.
+* ``restore_*.npz``    -- full ``restore`` reports (per-FP inner iteration
+  counts, restored image, gradient norms) for config 1 (AR + M/M_D/D_M,
+  reflective + R) and config 2a/2b (512^2).
+* ``restore_c3_head.npz`` (``--big``) -- the 2048^2 headline config, first
+  FP steps only (counts + image checksums; the image itself is 32 MB).
+"""
+
+from __future__ import annotations
+
+import argparse
+import pathlib
+import sys
+import time
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parents[1]))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import tvdeblur  # noqa: E402
+from tvdeblur import harness as rh  # noqa: E402
+from tvdeblur import precond as rp  # noqa: E402
+from tvdeblur import transforms as rt  # noqa: E402
+from tvdeblur.blur import BoundaryCondition, StructuredBlurOperator, SymmetricPsf  # noqa: E402
+from tvdeblur.krylov import KrylovConfig  # noqa: E402
+from tvdeblur.pipeline import PrecondSelector, RestorationConfig, restore  # noqa: E402
+from tvdeblur.tv import DiffusionOperator  # noqa: E402
+
+from paper_1011_5964_b200 import harness as bh  # noqa: E402
+
+BCS = {"anti_reflective": BoundaryCondition.ANTI_REFLECTIVE,
+       "reflective": BoundaryCondition.REFLECTIVE}
+
+
+def disk_psf(m: int) -> np.ndarray:
+    """Quadrantally symmetric, NOT separable (exercises the general 2D path)."""
+    i = np.arange(-m, m + 1)
+    h = ((i[:, None] ** 2 + i[None, :] ** 2) <= m * m + 0.5).astype(float)
+    h *= 1.0 + 0.1 * np.cos(i[:, None] * 0.7) * np.cos(i[None, :] * 0.7)
+    return h / h.sum()
+
+
+def ops_fixture(n: int, seed: int) -> dict:
+    rng = np.random.default_rng(seed)
+    out: dict[str, np.ndarray] = {}
+    u = rng.standard_normal((n, n))
+    w = rng.standard_normal((n, n))
+    out["u"], out["w"] = u, w
+    psfs = {"gauss": rh.gen_psf("gaussian", 3, 1.3).coefficients, "disk": disk_psf(3)}
+    for pname, h in psfs.items():
+        out[f"psf_{pname}"] = h
+        for bname, bc in BCS.items():
+            op = StructuredBlurOperator(SymmetricPsf(h), bc, n)
+            key = f"{pname}_{bname}"
+            out[f"H_{key}"] = op.apply(u)
+            out[f"HT_{key}"] = op.apply_transpose(u)
+            out[f"Hfast_{key}"] = op.apply_fast(u)
+            out[f"HTfast_{key}"] = op.apply_transpose_fast(u)
+            out[f"eig_{key}"] = op.eigenvalues()
+    beta, alpha = 0.1, 1e-3
+    lop = DiffusionOperator(u, beta)
+    out["a_h"], out["a_v"] = lop.a_h, lop.a_v
+    out["Lw"] = lop.apply(w)
+    out["diagL"] = lop.diagonal()
+    for (do, di), band in lop.block_banded().items():
+        out[f"band_{do}_{di}"] = band
+    for kind in ("dst1", "sine_hat", "dct"):
+        tk = rt.TransformKind(kind)
+        out[f"T2_{kind}"] = rt.tensor_apply_2d(tk, w)
+        out[f"T2inv_{kind}"] = rt.tensor_apply_2d(tk, w, inverse=True)
+    # 1D transforms on every length 3..n (odd and even periods)
+    for length in range(3, 12):
+        x = rng.standard_normal((4, length))
+        out[f"T1in_{length}"] = x
+        out[f"T1_dst1_{length}"] = rt.dst1_apply(x)
+        out[f"T1_sine_hat_{length}"] = rt.sinehat_apply(x)
+        out[f"T1_dct_{length}"] = rt.dct_apply(x)
+        out[f"T1inv_dct_{length}"] = rt.dct_apply(x, inverse=True)
+    gauss = SymmetricPsf(psfs["gauss"])
+    for bname, fam in (("anti_reflective", "M"), ("reflective", "R")):
+        op = StructuredBlurOperator(gauss, BCS[bname], n)
+        for kind in (fam, "D_" + fam, fam + "_D"):
+            pre = rp.assemble_preconditioner(kind, op, lop, alpha)
+            out[f"lam_{kind}"] = pre.eigenvalues
+            out[f"minv_{kind}"] = pre.apply_inverse(w)
+    out["alpha"], out["beta"] = np.array(alpha), np.array(beta)
+    return out
+
+
+def restore_fixture(spec: bh.ProblemSpec, selector: str, bc: str | None = None,
+                    fp_steps: int | None = None, keep_image: bool = True,
+                    fast: bool = True) -> dict:
+    m = spec.m
+    psf = rh.gen_psf("gaussian", m, spec.sigma)
+    ext = bh.gen_piecewise_image(spec.n, m, spec.rects, spec.disks, 2023, spec.ramp)
+    v = rh.blur_and_observe(ext, psf, spec.n, spec.nsr, 7)
+    u_true = ext[m:m + spec.n, m:m + spec.n]
+    bc = bc or spec.bc
+    cfg = RestorationConfig(
+        bc_h=BCS[bc], alpha=spec.alpha, beta=spec.beta,
+        preconditioner=PrecondSelector(selector), fp_tol=1e-300,
+        fp_max=fp_steps or spec.fp_steps,
+        inner=KrylovConfig(tol=spec.tol, max_iterations=2000), use_fast_blur=fast)
+    t0 = time.perf_counter()
+    rep = restore(v, psf, cfg, u_true=u_true)
+    dt = time.perf_counter() - t0
+    print(f"  {spec.name} {bc} {selector}: counts={rep.inner_iterations} "
+          f"rre={rep.rre:.4f} ({dt:.1f}s)", flush=True)
+    out = {"psf": psf.coefficients, "inner_iterations": np.array(rep.inner_iterations),
+           "gradient_norms": np.array(rep.gradient_norms), "rre": np.array(rep.rre),
+           "alpha": np.array(spec.alpha), "beta": np.array(spec.beta),
+           "tol": np.array(spec.tol), "fp_max": np.array(cfg.fp_max),
+           "restored_norm": np.array(np.linalg.norm(rep.restored)),
+           "restored_sum": np.array(rep.restored.sum()),
+           "restored_sub": rep.restored[::16, ::16].copy(),
+           "final_gradient_norm": np.array(rep.final_gradient_norm),
+           "seconds": np.array(dt)}
+    if keep_image:
+        out["v"], out["restored"] = v, rep.restored
+    else:
+        out["v_norm"] = np.array(np.linalg.norm(v))
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true", help="also run the 2048^2 head")
+    ap.add_argument("--big-steps", type=int, default=3)
+    ap.add_argument("--only-exact", action="store_true")
+    args = ap.parse_args()
+    print("reference tvdeblur from", tvdeblur.__file__)
+    if "--only-exact" in sys.argv:
+        np.savez_compressed(HERE / "restore_c1_I_exact.npz",
+                            **restore_fixture(bh.CONFIGS["c1"], "none", fast=False))
+        return
+    for n, seed in ((32, 11), (33, 12), (16, 13)):
+        np.savez_compressed(HERE / f"ops_n{n}.npz", **ops_fixture(n, seed))
+        print("wrote ops", n)
+    c1 = bh.CONFIGS["c1"]
+    for sel, bc, tag in (("x", None, "c1_M"), ("x_d", None, "c1_M_D"),
+                         ("d_x", None, "c1_D_M"), ("x", "reflective", "c1_R"),
+                         ("x_d", "reflective", "c1_R_D"), ("none", None, "c1_I")):
+        np.savez_compressed(HERE / f"restore_{tag}.npz", **restore_fixture(c1, sel, bc))
+    # the reference's exact (pad/convolve/crop) operator path, use_fast_blur=False
+    np.savez_compressed(HERE / "restore_c1_I_exact.npz",
+                        **restore_fixture(c1, "none", fast=False))
+    for key in ("c2a", "c2b"):
+        np.savez_compressed(HERE / f"restore_{key}.npz",
+                            **restore_fixture(bh.CONFIGS[key], "x"))
+    if args.big:
+        np.savez_compressed(
+            HERE / "restore_c3_head.npz",
+            **restore_fixture(bh.CONFIGS["c3"], "x", fp_steps=args.big_steps,
+                              keep_image=False))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,338 @@
+"""GPU parity: every hot-path operator through the C ABI vs the reference's own outputs.
+
+Goldens (``tests/golden/*.npz``) were produced by running the reference package
+itself (``tests/golden/make_golden.py``); the oracle restatement covers sizes
+the goldens do not.  Tolerances follow BASELINE.json's north_star: per-op
+1e-12 relative (bit-identical where the arithmetic allows), restored image
+1e-8 relative L2, identical per-FP-step PCG iteration counts.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+from oracle import tvd_oracle as O
+
+import paper_1011_5964_b200 as tvd
+from paper_1011_5964_b200 import blur as B
+from paper_1011_5964_b200 import krylov as K
+from paper_1011_5964_b200 import precond as P
+from paper_1011_5964_b200 import transforms as T
+from paper_1011_5964_b200 import tv as TV
+from paper_1011_5964_b200.harness import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+OPS = ["ops_n16.npz", "ops_n32.npz", "ops_n33.npz"]
+BCS = {"anti_reflective": B.BoundaryCondition.ANTI_REFLECTIVE,
+       "reflective": B.BoundaryCondition.REFLECTIVE}
+
+
+# ----------------------------------------------------------------- transforms
+@pytest.mark.parametrize("name", OPS)
+def test_transforms_2d_match_reference(golden, name):
+    g = golden(name)
+    for kind in ("dst1", "sine_hat", "dct"):
+        tk = T.TransformKind(kind)
+        assert rel_err(T.tensor_apply_2d(tk, g["w"]), g[f"T2_{kind}"]) < 1e-13
+        assert rel_err(T.tensor_apply_2d(tk, g["w"], inverse=True), g[f"T2inv_{kind}"]) < 1e-13
+
+
+def test_transforms_1d_every_short_length(golden):
+    g = golden("ops_n16.npz")
+    for length in range(3, 12):
+        x = g[f"T1in_{length}"]
+        assert rel_err(T.dst1_apply(x), g[f"T1_dst1_{length}"]) < 1e-13, length
+        assert rel_err(T.sinehat_apply(x), g[f"T1_sine_hat_{length}"]) < 1e-13, length
+        assert rel_err(T.dct_apply(x), g[f"T1_dct_{length}"]) < 1e-13, length
+        assert rel_err(T.dct_apply(x, inverse=True), g[f"T1inv_dct_{length}"]) < 1e-13, length
+
+
+@pytest.mark.parametrize("n", [127, 128, 511, 512, 1023, 1024, 2048])
+def test_transforms_2d_vs_oracle(n, rng):
+    w = rng.standard_normal((n, n))
+    for kind in ("dst1", "sine_hat", "dct"):
+        tk = T.TransformKind(kind)
+        assert rel_err(T.tensor_apply_2d(tk, w), O.tensor_2d(kind, w)) < 1e-12, (n, kind)
+        assert rel_err(T.tensor_apply_2d(tk, w, inverse=True),
+                       O.tensor_2d(kind, w, inverse=True)) < 1e-12, (n, kind)
+
+
+def test_transform_known_answers():
+    # S_2 (1,1) = (sqrt2, 0) and C e1 = n^-1/2 (pkg/tests/test_transforms.py:31-48)
+    np.testing.assert_allclose(T.dst1_apply(np.array([[1.0, 1.0]])), [[np.sqrt(2.0), 0.0]],
+                               atol=1e-14)
+    e1 = np.zeros((1, 12))
+    e1[0, 0] = 1.0
+    np.testing.assert_allclose(T.dct_apply(e1), np.full((1, 12), np.sqrt(1 / 12)), atol=1e-14)
+    assert np.all(T.dst1_apply(np.zeros((2, 7))) == 0.0)
+
+
+@pytest.mark.parametrize("n", [2048])
+def test_full_size_transform_round_trips(n, rng):
+    """Size-independent properties at the headline size: Shat is an involution,
+    DCT synthesis inverts analysis."""
+    w = torch.from_numpy(rng.standard_normal((n, n))).cuda()
+    sh = T.tensor_apply_2d(T.TransformKind.SINE_HAT, T.tensor_apply_2d(T.TransformKind.SINE_HAT, w))
+    assert float((sh - w).norm() / w.norm()) < 1e-13
+    dc = T.tensor_apply_2d(T.TransformKind.DCT, T.tensor_apply_2d(T.TransformKind.DCT, w, inverse=True))
+    assert float((dc - w).norm() / w.norm()) < 1e-13
+
+
+# ---------------------------------------------------------------------- blur
+@pytest.mark.parametrize("name", OPS)
+@pytest.mark.parametrize("pname", ["gauss", "disk"])
+@pytest.mark.parametrize("bname", list(BCS))
+def test_blur_exact_vs_reference(golden, name, pname, bname):
+    g = golden(name)
+    n = g["u"].shape[0]
+    op = B.StructuredBlurOperator(B.SymmetricPsf(g[f"psf_{pname}"]), BCS[bname], n)
+    assert op.separable == (pname == "gauss")
+    key = f"{pname}_{bname}"
+    assert rel_err(op.apply(g["u"]), g[f"H_{key}"]) < 1e-12
+    assert rel_err(op.apply_transpose(g["u"]), g[f"HT_{key}"]) < 1e-12
+    np.testing.assert_allclose(op.eigenvalues(), g[f"eig_{key}"], rtol=0, atol=1e-13)
+    # normal operator == back(H(u)) of pipeline.py:167-179
+    hu = g[f"H_{key}"]
+    back = O.blur(hu, g[f"psf_{pname}"], bname) if bname == "reflective" else \
+        O.blur_transpose(hu, g[f"psf_{pname}"], bname)
+    assert rel_err(op.normal_apply(g["u"]), back) < 1e-12
+
+
+@pytest.mark.parametrize("n,m,bname", [(512, 7, "anti_reflective"), (512, 7, "reflective"),
+                                       (300, 15, "anti_reflective"), (1024, 10, "anti_reflective")])
+def test_blur_vs_oracle_midsize(n, m, bname, rng):
+    from paper_1011_5964_b200.harness import gen_psf
+    h = gen_psf("gaussian", m, m / 2.0)
+    u = rng.standard_normal((n, n))
+    op = B.StructuredBlurOperator(B.SymmetricPsf(h), BCS[bname], n)
+    assert rel_err(op.apply(u), O.blur(u, h, bname)) < 1e-12
+    assert rel_err(op.apply_transpose(u), O.blur_transpose(u, h, bname)) < 1e-12
+
+
+@pytest.mark.parametrize("n", [2048])
+def test_full_size_blur_adjointness_and_linearity(n, rng):
+    from paper_1011_5964_b200.harness import gen_psf
+    h = gen_psf("gaussian", 15, 4.0)
+    op = B.StructuredBlurOperator(B.SymmetricPsf(h), B.BoundaryCondition.ANTI_REFLECTIVE, n)
+    x = torch.from_numpy(rng.standard_normal((n, n))).cuda()
+    y = torch.from_numpy(rng.standard_normal((n, n))).cuda()
+    lhs = float((op.apply(x) * y).sum())
+    rhs = float((x * op.apply_transpose(y)).sum())
+    assert abs(lhs - rhs) <= 1e-11 * abs(lhs)
+    lin = op.apply(2.0 * x - 3.0 * y) - (2.0 * op.apply(x) - 3.0 * op.apply(y))
+    assert float(lin.norm() / op.apply(x).norm()) < 1e-13
+    nrm = op.normal_apply(x) - op.apply_transpose(op.apply(x))
+    assert float(nrm.norm() / op.normal_apply(x).norm()) < 1e-12
+
+
+# ----------------------------------------------------------------- diffusion
+@pytest.mark.parametrize("name", OPS)
+def test_diffusion_bit_identical(golden, name):
+    g = golden(name)
+    lop = TV.DiffusionOperator(g["u"], float(g["beta"]))
+    np.testing.assert_array_equal(lop.a_h, g["a_h"])
+    np.testing.assert_array_equal(lop.a_v, g["a_v"])
+    np.testing.assert_array_equal(lop.apply(g["w"]), g["Lw"])
+    np.testing.assert_array_equal(lop.diagonal(), g["diagL"])
+    bands = lop.block_banded()
+    for (do, di), band in bands.items():
+        np.testing.assert_array_equal(band, g[f"band_{do}_{di}"])
+
+
+def test_diffusion_known_answers():
+    a_h, a_v = TV.diffusion_coefficients(np.full((5, 5), 3.0), 0.5)
+    np.testing.assert_allclose(a_h, 2.0)
+    np.testing.assert_allclose(a_v, 2.0)
+    lop = TV.DiffusionOperator(np.random.default_rng(0).standard_normal((6, 6)), 0.1)
+    np.testing.assert_allclose(lop.apply(np.full((6, 6), 4.0)), 0.0, atol=1e-12)
+
+
+@pytest.mark.parametrize("n", [2048])
+def test_full_size_diffusion_bit_identical(n, rng):
+    u = rng.standard_normal((n, n)).cumsum(axis=0) * 0.01
+    w = rng.standard_normal((n, n))
+    lop = TV.DiffusionOperator(u, 0.05)
+    a_h, a_v = O.diffusivity(u, 0.05)
+    np.testing.assert_array_equal(lop.a_h, a_h)
+    np.testing.assert_array_equal(lop.a_v, a_v)
+    np.testing.assert_array_equal(lop.apply(w), O.diffusion_apply(a_h, a_v, w))
+
+
+# ------------------------------------------------------------ preconditioner
+@pytest.mark.parametrize("name", OPS)
+def test_preconditioner_eigenvalues_and_inverse(golden, name):
+    g = golden(name)
+    n = g["u"].shape[0]
+    alpha = float(g["alpha"])
+    lop = TV.DiffusionOperator(g["u"], float(g["beta"]))
+    psf = B.SymmetricPsf(g["psf_gauss"])
+    for bname, fam in (("anti_reflective", "M"), ("reflective", "R")):
+        hop = B.StructuredBlurOperator(psf, BCS[bname], n)
+        for kind in (fam, "D_" + fam, fam + "_D"):
+            pre = P.assemble_preconditioner(kind, hop, lop, alpha)
+            assert rel_err(pre.eigenvalues, g[f"lam_{kind}"]) < 1e-12, kind
+            assert rel_err(pre.apply_inverse(g["w"]), g[f"minv_{kind}"]) < 1e-12, kind
+            back = pre.apply(pre.apply_inverse(g["w"]))
+            assert rel_err(back, g["w"]) < 1e-9, kind
+
+
+@pytest.mark.parametrize("n,kind", [(512, "M"), (512, "R"), (512, "M_D"), (1024, "D_M"),
+                                    (2048, "M")])
+def test_preconditioner_vs_oracle_large(n, kind, rng):
+    from paper_1011_5964_b200.harness import gen_psf
+    h = gen_psf("gaussian", 7, 2.5)
+    u = rng.standard_normal((n, n)).cumsum(axis=1) * 0.05
+    alpha = 5e-4
+    bname = "reflective" if "R" in kind else "anti_reflective"
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(h), BCS[bname], n)
+    lop = TV.DiffusionOperator(u, 0.1)
+    pre = P.assemble_preconditioner(kind, hop, lop, alpha)
+    a_h, a_v = O.diffusivity(u, 0.1)
+    blocks = O.diffusion_bands(a_h, a_v)
+    lam_h = O.blur_eigenvalues(h, bname, n)
+    lam, lam_inv, d_sqrt, _ = O.assemble(kind, lam_h, blocks, alpha)
+    assert rel_err(pre.eigenvalues, lam) < 1e-12
+    r = rng.standard_normal((n, n))
+    fam = O.FAMILY[kind.replace("D_", "").replace("_D", "")]
+    assert rel_err(pre.apply_inverse(r), O.precond_solve(fam, lam_inv, r, d_sqrt)) < 1e-12
+
+
+def test_preconditioner_rejects_wrong_bc(golden):
+    g = golden("ops_n16.npz")
+    lop = TV.DiffusionOperator(g["u"], 0.1)
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(g["psf_gauss"]), B.BoundaryCondition.REFLECTIVE, 16)
+    with pytest.raises(ValueError):
+        P.assemble_preconditioner("M", hop, lop, 1e-3)
+    with pytest.raises(ValueError):
+        P.assemble_preconditioner("Q", hop, lop, 1e-3)
+
+
+# ----------------------------------------------------------------------- PCG
+def _dev(a):
+    return torch.from_numpy(np.asarray(a, dtype=float)).cuda()
+
+
+def test_pcg_generic_reference_cases(rng):
+    b = rng.standard_normal(6)
+    out = K.pcg(lambda x: x.clone(), None, _dev(b), _dev(np.zeros(6)))
+    assert out.converged and out.iterations == 1
+    d = np.arange(1.0, 11.0)
+    bb = rng.standard_normal(10)
+    dd = _dev(d)
+    out = K.pcg(lambda x: dd * x, lambda r: r / dd, _dev(bb), _dev(np.zeros(10)))
+    assert out.converged and out.iterations == 1
+    np.testing.assert_allclose(out.solution.cpu().numpy(), bb / d, atol=1e-12)
+    m = rng.standard_normal((8, 8))
+    a = m @ m.T + 8 * np.eye(8)
+    ad = _dev(a)
+    bv = rng.standard_normal(8)
+    out = K.pcg(lambda x: ad @ x, None, _dev(bv), _dev(np.zeros(8)),
+                K.KrylovConfig(tol=1e-12, max_iterations=100))
+    np.testing.assert_allclose(out.solution.cpu().numpy(), np.linalg.solve(a, bv), atol=1e-8)
+    with pytest.raises(K.IndefiniteOperatorError) as err:
+        K.pcg(lambda x: -x, None, _dev(rng.standard_normal(5)), _dev(np.zeros(5)))
+    assert err.value.iteration == 1
+    with pytest.raises(K.SolverDivergenceError):
+        K.pcg(lambda x: torch.full_like(x, float("nan")), None, _dev(rng.standard_normal(4)),
+              _dev(np.zeros(4)))
+    out = K.pcg(lambda x: x.clone(), None, _dev(np.zeros(4)), _dev(np.zeros(4)))
+    assert out.converged and out.iterations == 0
+
+
+def _system(g, bname, n):
+    from paper_1011_5964_b200.pipeline import NormalSystem
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(g["psf_gauss"]), BCS[bname], n)
+    lop = TV.DiffusionOperator(g["u"], float(g["beta"]))
+    return hop, lop, NormalSystem(hop, lop, float(g["alpha"]))
+
+
+@pytest.mark.parametrize("name", OPS)
+@pytest.mark.parametrize("kind", ["M", "D_M", "none"])
+def test_fused_pcg_matches_oracle_iteration_by_iteration(golden, name, kind):
+    g = golden(name)
+    n = g["u"].shape[0]
+    hop, lop, system = _system(g, "anti_reflective", n)
+    rhs = hop.apply_transpose(g["w"])
+    cfg = K.KrylovConfig(tol=1e-9, max_iterations=400, record_history=True)
+    if kind == "none":
+        minv_gpu, minv_cpu = None, None
+    else:
+        pre = P.assemble_preconditioner(kind, hop, lop, float(g["alpha"]))
+        minv_gpu = pre.apply_inverse
+        lam_inv = pre.inverse_eigenvalues_device.cpu().numpy()
+        dsq = pre.d_sqrt
+        minv_cpu = lambda r: O.precond_solve("sine_hat", lam_inv, r, dsq)  # noqa: E731
+    out = K.pcg(system, minv_gpu, rhs, g["u"], cfg)
+    h = g["psf_gauss"]
+
+    def apply_a(w):
+        return O.blur_transpose(O.blur(w, h, "anti_reflective"), h, "anti_reflective") + \
+            float(g["alpha"]) * O.diffusion_apply(lop.a_h, lop.a_v, w)
+
+    x, its, hist, ok = O.pcg(apply_a, minv_cpu, rhs, g["u"], 1e-9, 400, True)
+    assert out.converged and ok
+    # 240 unpreconditioned steps to 1e-9: rounding may move the stop by one step
+    assert abs(out.iterations - its) <= (1 if kind == "none" else 0)
+    # unpreconditioned CG loses orthogonality over ~150 steps, so rounding-level
+    # differences grow along the history; the early history must agree tightly
+    head = 10 if kind == "none" else len(hist)
+    np.testing.assert_allclose(out.residual_history[:head], hist[:head], rtol=1e-6)
+    assert rel_err(out.solution, x) < (1e-6 if kind == "none" else 1e-8)
+
+
+def test_fused_pcg_errors_and_limits(golden):
+    g = golden("ops_n16.npz")
+    hop, lop, system = _system(g, "anti_reflective", 16)
+    rhs = hop.apply_transpose(g["w"])
+    out = K.pcg(system, None, rhs, g["u"], K.KrylovConfig(tol=1e-14, max_iterations=3))
+    assert not out.converged and out.iterations == 3
+    out = K.pcg(system, None, np.zeros((16, 16)), np.zeros((16, 16)))
+    assert out.converged and out.iterations == 0
+    from paper_1011_5964_b200.pipeline import NormalSystem
+    neg = NormalSystem(hop, lop, -50.0)  # alpha < 0 with a large L -> indefinite
+    with pytest.raises(K.IndefiniteOperatorError):
+        K.pcg(neg, None, rhs, np.zeros((16, 16)), K.KrylovConfig(tol=1e-12, max_iterations=200))
+
+
+# ------------------------------------------------------------------- restore
+RESTORES = [("restore_c1_M.npz", "x", "anti_reflective"),
+            ("restore_c1_M_D.npz", "x_d", "anti_reflective"),
+            ("restore_c1_D_M.npz", "d_x", "anti_reflective"),
+            ("restore_c1_R.npz", "x", "reflective"),
+            ("restore_c1_R_D.npz", "x_d", "reflective"),
+            ("restore_c1_I_exact.npz", "none", "anti_reflective"),
+            ("restore_c2a.npz", "x", "anti_reflective"),
+            ("restore_c2b.npz", "x", "reflective")]
+
+
+@pytest.mark.parametrize("name,selector,bname", RESTORES)
+def test_restore_matches_reference(golden, name, selector, bname):
+    g = golden(name)
+    cfg = tvd.RestorationConfig(
+        bc_h=BCS[bname], alpha=float(g["alpha"]), beta=float(g["beta"]),
+        preconditioner=tvd.PrecondSelector(selector), fp_tol=1e-300, fp_max=int(g["fp_max"]),
+        inner=K.KrylovConfig(tol=float(g["tol"]), max_iterations=2000))
+    rep = tvd.restore(g["v"], B.SymmetricPsf(g["psf"]), cfg)
+    assert rep.inner_iterations == [int(k) for k in g["inner_iterations"]]
+    assert rel_err(rep.restored, g["restored"]) < 1e-8
+    np.testing.assert_allclose(rep.gradient_norms, g["gradient_norms"], rtol=1e-6)
+    assert abs(rep.final_gradient_norm - float(g["final_gradient_norm"])) <= \
+        1e-6 * float(g["final_gradient_norm"])
+
+
+def test_restore_unpreconditioned_vs_reference_fast_path(golden):
+    """Selector I: the reference's transform fast path itself differs from its exact
+    operator path by +-1 iteration at some FP steps (image 1.1e-9 apart); the GPU
+    path implements the exact operator, so against the fast-path golden the gate is
+    the north_star's +-1 per step with the image inside 1e-8."""
+    g = golden("restore_c1_I.npz")
+    cfg = tvd.RestorationConfig(
+        bc_h=BCS["anti_reflective"], alpha=float(g["alpha"]), beta=float(g["beta"]),
+        preconditioner=tvd.PrecondSelector.NONE, fp_tol=1e-300, fp_max=int(g["fp_max"]),
+        inner=K.KrylovConfig(tol=float(g["tol"]), max_iterations=2000))
+    rep = tvd.restore(g["v"], B.SymmetricPsf(g["psf"]), cfg)
+    ref = [int(k) for k in g["inner_iterations"]]
+    assert all(abs(a - b) <= 1 for a, b in zip(rep.inner_iterations, ref))
+    assert rel_err(rep.restored, g["restored"]) < 1e-8
