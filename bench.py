@@ -1,0 +1,386 @@
+"""Benchmark: PCG iterations/s of the TV-deblurring inner solve (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+
+Workload (N=1): BASELINE.json configs[2] = "c3", the 2048^2 anti-reflective
+fp64 headline case (Gaussian 31x31 sigma 4, alpha 2e-4, beta 0.05, PCG tol
+1e-5, DST-I/Shat preconditioner M).  Synthetic seeded inputs from
+``paper_1011_5964_b200.harness`` (the BASELINE generator; no dataset exists).
+
+A *step* is one inner PCG solve of one FP step: the lagged-diffusivity state
+after ``--state-fp`` FP steps is prepared untimed, then every step calls the
+public ``pcg(system, precond.apply_inverse, rhs, u, cfg)`` on device-resident
+inputs and runs to tol.  ``value`` = PCG iterations of all ranks / device
+time (CUDA events, max over ranks).  Multi-GPU: one independent problem per
+rank (batch sharding, no collective on the hot path) -> ``scaling: weak``.
+
+``e2e``: the same metric through the public API from pinned HOST buffers:
+per step H2D of (u, rhs), diffusivity, device preconditioner assembly, PCG,
+D2H of the solution.
+
+``--impl reference``: the reference algorithm's CPU path (the oracle port in
+``oracle/tvd_oracle.py``; the reference package itself is Python that cannot
+travel to the GPU box) with all host cores for its FFTs, each step a bounded
+sample of PCG iterations of the same config; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "PCG iters/sec at 2048^2 AR fp64 (config c3, DST-I/Shat preconditioner M)"
+UNIT = "PCG iters/s"
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx.append(float(f[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        finally:
+            os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -------------------------------------------------------------- reference
+def cpu_state(spec, h, v, state_fp: int):
+    """Host-side operators of the oracle port at FP state ``state_fp`` (u = v for 0)."""
+    from oracle import tvd_oracle as O
+
+    bc = spec.bc
+    lam_h = O.blur_eigenvalues(h, bc, spec.n)
+    u = v.copy()
+    a_h, a_v = O.diffusivity(u, spec.beta)
+    blocks = O.diffusion_bands(a_h, a_v)
+    _, lam_inv, _, _ = O.assemble("M" if bc == "anti_reflective" else "R", lam_h, blocks,
+                                  spec.alpha)
+    fam = "sine_hat" if bc == "anti_reflective" else "dct"
+
+    def apply_a(w):
+        hw = O.blur_fast(w, lam_h, bc)
+        back = hw if bc == "reflective" else O.blur_transpose_fast(hw, lam_h, bc)
+        return back + spec.alpha * O.diffusion_apply(a_h, a_v, w)
+
+    rhs = O.blur_transpose_fast(v, lam_h, bc) if bc == "anti_reflective" else O.blur_fast(v, lam_h, bc)
+    return apply_a, (lambda r: O.precond_solve(fam, lam_inv, r)), rhs, u
+
+
+def cpu_sample(apply_a, minv, rhs, u, iters: int) -> float:
+    """Seconds for ``iters`` PCG iterations of the oracle port (tol tiny, never converges)."""
+    from oracle import tvd_oracle as O
+
+    t0 = time.perf_counter()
+    O.pcg(apply_a, minv, rhs, u, 1e-300, iters)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    from oracle import tvd_oracle as O
+    from paper_1011_5964_b200.harness import CONFIGS, make_problem
+
+    cores = os.cpu_count() or 1
+    O.set_workers(cores)
+    spec = CONFIGS[args.config]
+    h, v, _ = make_problem(spec)
+    apply_a, minv, rhs, u = cpu_state(spec, h, v, 0)
+    per_step = args.ref_iters
+    for _ in range(args.warmup):
+        cpu_sample(apply_a, minv, rhs, u, per_step)
+    t = 0.0
+    for _ in range(args.steps):
+        t += cpu_sample(apply_a, minv, rhs, u, per_step)
+    iters = per_step * args.steps
+    value = iters / t
+    sample = (f"{per_step} PCG iterations per step of config {spec.name} ({spec.n}^2), oracle "
+              f"restatement of the reference (scipy.fft workers={cores}, numpy elementwise)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator)",
+        "config": {"workload": f"{spec.name}: {spec.n}^2 AR fp64 PCG, M preconditioner",
+                   "n": spec.n, "problems_per_gpu": 1, "l2": "inputs larger than L2"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "mpix_iter_per_s": value * spec.n ** 2 / 1e6,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- ours
+def alg_bytes_per_launch(cat: str, n: int) -> float:
+    """Algorithmic bytes one launch of a kernel category must move."""
+    px = float(n) * n
+    return {
+        "band_rows": 16.0 * px,         # read p, write t
+        "band_cols": 40.0 * px,         # read t, p, a_h, a_v; write q  (+ p.q)
+        "trig_cols": 24.0 * px,         # read t, inv_eig; write t'
+        "trig_rows": 20.0 * px,         # avg of pass 1 (16 B/px) and pass 3 (24 B/px, reads r)
+        "vector": 36.0 * px,            # avg of x/r update (48) and p update (24)
+    }.get(cat, 0.0)
+
+
+def run_ours(args, rank: int, world: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_1011_5964_b200 as tvd
+    from paper_1011_5964_b200 import _native as nat
+    from paper_1011_5964_b200.harness import CONFIGS, make_problem
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    spec = CONFIGS[args.config]
+    n = spec.n
+    bc = tvd.BoundaryCondition(spec.bc)
+    h, v, _ = make_problem(spec, index=rank)
+    kind = "M" if bc is tvd.BoundaryCondition.ANTI_REFLECTIVE else "R"
+    cfg = tvd.KrylovConfig(tol=spec.tol, max_iterations=2000)
+
+    hop = tvd.StructuredBlurOperator(tvd.SymmetricPsf(h), bc, n, device=dev)
+    v_dev = torch.from_numpy(v).to(dev)
+    back = hop.apply if bc is tvd.BoundaryCondition.REFLECTIVE else hop.apply_transpose
+    rhs = back(v_dev)
+    u = v_dev.clone()
+    for _ in range(args.state_fp):  # untimed: reach a representative lagged-diffusivity state
+        lop = tvd.DiffusionOperator(u, spec.beta, device=dev)
+        pre = tvd.assemble_preconditioner(kind, hop, lop, spec.alpha)
+        u = tvd.pcg(tvd.NormalSystem(hop, lop, spec.alpha), pre.apply_inverse, rhs, u, cfg).solution
+    lop = tvd.DiffusionOperator(u, spec.beta, device=dev)
+    pre = tvd.assemble_preconditioner(kind, hop, lop, spec.alpha)
+    system = tvd.NormalSystem(hop, lop, spec.alpha)
+
+    def step() -> int:
+        return tvd.pcg(system, pre.apply_inverse, rhs, u, cfg).iterations
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = nat.launch_count(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 0
+    with ClockSampler(local) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            iters += step()
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = nat.launch_count(dev) - l0
+    elapsed = e0.elapsed_time(e1) / 1e3
+    stats = torch.tensor([elapsed, float(iters), float(launches)], dtype=torch.float64, device=dev)
+    if world > 1:
+        t_max = stats[:1].clone()
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        sums = stats[1:].clone()
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        elapsed, iters, launches = float(t_max[0]), float(sums[0]), float(sums[1])
+    value = iters / elapsed
+
+    # ---- live per-kernel timing (CUDA events on the launch stream) for the roofline
+    nat.profile(True, dev)
+    prof_iters = step()
+    prof = nat.profile_read(dev)
+    nat.profile(False, dev)
+    cats = {k: v for k, v in prof.items() if alg_bytes_per_launch(k, n) > 0}
+    dom = max(cats, key=lambda k: cats[k][0])
+    ms_tot, cnt = cats[dom]
+    achieved = alg_bytes_per_launch(dom, n) / (ms_tot / cnt / 1e3) / 1e9
+    peaks = _peaks()
+    hbm = float(peaks["hbm_gbs"])
+    step_ms = sum(t for t, _ in prof.values())
+    kernels = {k: {"ms_total": round(t, 4), "launches": c, "share": round(t / step_ms, 4),
+                   "gbs": (round(alg_bytes_per_launch(k, n) / (t / c / 1e3) / 1e9, 1)
+                           if alg_bytes_per_launch(k, n) else None)}
+               for k, (t, c) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+
+    # ---- e2e through the public API from pinned host buffers
+    u_host = u.cpu().pin_memory()
+    rhs_host = rhs.cpu().pin_memory()
+    out_host = torch.empty_like(u_host).pin_memory()
+
+    def e2e_step() -> int:
+        ud = u_host.to(dev, non_blocking=True)
+        rd = rhs_host.to(dev, non_blocking=True)
+        l_op = tvd.DiffusionOperator(ud, spec.beta, device=dev)
+        p_op = tvd.assemble_preconditioner(kind, hop, l_op, spec.alpha)
+        res = tvd.pcg(tvd.NormalSystem(hop, l_op, spec.alpha), p_op.apply_inverse, rd, ud, cfg)
+        out_host.copy_(res.solution, non_blocking=True)
+        return res.iterations
+
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_iters = 0
+    e2e_steps = max(1, min(args.steps, 5))
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(e2e_steps):
+        e2e_iters += e2e_step()
+    s1.record()
+    torch.cuda.synchronize()
+    e2e_t = s0.elapsed_time(s1) / 1e3
+    if world > 1:
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ii = torch.tensor([float(e2e_iters)], dtype=torch.float64, device=dev)
+        dist.all_reduce(ii, op=dist.ReduceOp.SUM)
+        e2e_t, e2e_iters = float(tt[0]), float(ii[0])
+    e2e_value = e2e_iters / e2e_t
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import tvd_oracle as O
+        cores = os.cpu_count() or 1
+        O.set_workers(cores)
+        apply_a, minv, crhs, cu = cpu_state(spec, h, v, 0)
+        cpu_sample(apply_a, minv, crhs, cu, 1)  # warm (plans, page-in)
+        t = cpu_sample(apply_a, minv, crhs, cu, args.cpu_iters)
+        cpu = {"value": args.cpu_iters / t, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{args.cpu_iters} PCG iterations of config {spec.name} ({n}^2) with the "
+                         f"oracle restatement (scipy.fft workers={cores}); {t:.1f} s"}
+    clk = clocks.summary()
+    alg_iter = 128.0 * n * n
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE piecewise-constant generator, PCG64 noise)",
+        "config": {"workload": f"{spec.name}: {n}^2 AR fp64, Gaussian {2 * spec.m + 1}x"
+                               f"{2 * spec.m + 1} sigma {spec.sigma}, alpha {spec.alpha}, "
+                               f"beta {spec.beta}, tol {spec.tol}, preconditioner {kind}",
+                   "n": n, "problems_per_gpu": 1, "state_fp": args.state_fp,
+                   "pcg_iters_per_step": iters / (args.steps * world),
+                   "l2": "inputs larger than L2 (~15 n^2 fp64 arrays = 480 MB working set)"},
+        "mpix_iter_per_s": value * n * n / 1e6,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None, "kernel": dom,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"
+                     if not peaks.get("fallback") else "fallback 6650 GB/s"},
+        "pcg_roofline": {"alg_bytes_per_iter": alg_iter,
+                         "achieved_gbs": alg_iter * value / world / 1e9,
+                         "frac": alg_iter * value / world / 1e9 / hbm},
+        "kernels": kernels, "profiled_iterations": prof_iters,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * n * n,
+                "d2h_bytes_per_step": 8 * n * n, "steps": e2e_steps,
+                "includes": "H2D u,rhs; diffusivity; device assembly; PCG; D2H solution"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--state-fp", type=int, default=2)
+    ap.add_argument("--cpu-iters", type=int, default=6)
+    ap.add_argument("--ref-iters", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -89,6 +89,18 @@ int tvd_ctx_create(int device, void* stream, tvd_ctx** out);
 int tvd_ctx_set_stream(tvd_ctx* ctx, void* stream);
 int tvd_ctx_sync(tvd_ctx* ctx);
 int tvd_ctx_destroy(tvd_ctx* ctx);
+/* options: TVD_OPT_GENERIC_FFT (1) routes DST passes through the generic
+ * mixed-radix engine instead of the odd-symmetric prime-factor engine */
+#define TVD_OPT_GENERIC_FFT 1
+int tvd_ctx_set_option(tvd_ctx* ctx, int option, int value);
+/* instrumentation: kernels launched through ctx so far */
+int tvd_ctx_counters(tvd_ctx* ctx, long long* launches);
+/* enable (1) / disable (0) CUDA-event timing around every launch; resets records */
+int tvd_ctx_profile(tvd_ctx* ctx, int enable);
+/* per-category launch time (ms) and launch count since tvd_ctx_profile(ctx, 1) */
+int tvd_ctx_profile_read(tvd_ctx* ctx, int ncat, double* total_ms, long long* count);
+/* category name for id, NULL past the last */
+const char* tvd_profile_category(int id);
 
 /* ---- blur operator H  (blur.py:197-326) -------------------------------- */
 /* psf: HOST (2m+1) x (2m+1) quadrantally symmetric, normalised.

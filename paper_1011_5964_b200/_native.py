@@ -49,6 +49,11 @@ _SIGNATURES = {
     "tvd_ctx_set_stream": ([_vp, _vp], _i),
     "tvd_ctx_sync": ([_vp], _i),
     "tvd_ctx_destroy": ([_vp], _i),
+    "tvd_ctx_set_option": ([_vp, _i, _i], _i),
+    "tvd_ctx_counters": ([_vp, ctypes.POINTER(_ll)], _i),
+    "tvd_ctx_profile": ([_vp, _i], _i),
+    "tvd_ctx_profile_read": ([_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_ll)], _i),
+    "tvd_profile_category": ([_i], ctypes.c_char_p),
     "tvd_blur_create": ([_vp, _i, _vp, _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_i)], _i),
     "tvd_blur_destroy": ([_vp], _i),
     "tvd_blur_apply": ([_vp, _vp, _vp, _i], _i),
@@ -162,3 +167,34 @@ def to_device(x, device: torch.device | None = None) -> tuple[torch.Tensor, bool
 
 def to_host_like(t: torch.Tensor, was_numpy: bool):
     return t.cpu().numpy() if was_numpy else t
+
+
+# ---------------------------------------------------------- instrumentation
+def launch_count(device=None) -> int:
+    out = _ll()
+    check(load().tvd_ctx_counters(context(device), ctypes.byref(out)))
+    return out.value
+
+
+def set_generic_fft(enable: bool, device=None) -> None:
+    """Route DST passes through the generic mixed-radix FFT (parity tests of both engines)."""
+    check(load().tvd_ctx_set_option(context(device), 1, 1 if enable else 0))
+
+
+def profile(enable: bool, device=None) -> None:
+    check(load().tvd_ctx_profile(context(device), 1 if enable else 0))
+
+
+def profile_read(device=None) -> dict[str, tuple[float, int]]:
+    """``{category: (total_ms, launches)}`` recorded since ``profile(True)``."""
+    lib = load()
+    names = []
+    while True:
+        nm = lib.tvd_profile_category(len(names))
+        if nm is None:
+            break
+        names.append(nm.decode())
+    ms = (_d * len(names))()
+    cnt = (_ll * len(names))()
+    check(lib.tvd_ctx_profile_read(context(device), len(names), ms, cnt))
+    return {nm: (ms[i], cnt[i]) for i, nm in enumerate(names) if cnt[i]}

@@ -13,7 +13,7 @@ import sys
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtvdeblur_b200.so"
-SOURCES = ["tvd_lines.cu", "tvd_stencil.cu", "tvd_cg.cu", "tvd_capi.cu"]
+SOURCES = ["tvd_lines.cu", "tvd_pfa.cu", "tvd_stencil.cu", "tvd_cg.cu", "tvd_capi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17",

@@ -70,7 +70,48 @@ struct tvd_ctx {
   PcgState* h_state = nullptr;
   double* h_scalar = nullptr;  // pinned scratch for host scalars (64 doubles)
   double* d_scalar = nullptr;
+  long long launches = 0;      // kernels launched through this context
+  bool force_generic = false;  // route DST passes through the generic FFT (tests)
+  bool profiling = false;      // record CUDA events around every launch
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_marks;  // (category, first event index)
 };
+
+// kernel categories for the per-launch timer (tvd_profile_category)
+enum Cat : int {
+  kCatTrigRows = 0, kCatTrigCols, kCatBandRows, kCatBandCols, kCatVec, kCatFin,
+  kCatProject, kCatStencil, kCatGeneral, kCatCount
+};
+static const char* kCatNames[kCatCount] = {"trig_rows", "trig_cols", "band_rows", "band_cols",
+                                           "vector", "finalize", "band_project", "stencil",
+                                           "general_blur"};
+
+static void prof_begin(tvd_ctx* c, int cat) {
+  if (!c->profiling) return;
+  const size_t need = 2 * (c->ev_marks.size() + 1);
+  while (c->ev_pool.size() < need) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  const int idx = 2 * (int)c->ev_marks.size();
+  c->ev_marks.push_back({cat, idx});
+  cudaEventRecord(c->ev_pool[idx], c->stream);
+}
+static void prof_end(tvd_ctx* c) {
+  if (!c->profiling) return;
+  cudaEventRecord(c->ev_pool[c->ev_marks.back().second + 1], c->stream);
+}
+
+#define TVD_LAUNCH(c, cat, nk, call)                                                      \
+  do {                                                                                   \
+    prof_begin((c), (cat));                                                              \
+    cudaError_t e_ = (call);                                                             \
+    prof_end(c);                                                                         \
+    (c)->launches += (nk);                                                               \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(TVD_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
 
 struct tvd_blur {
   tvd_ctx* ctx = nullptr;
@@ -256,6 +297,82 @@ static int build_plan(int family, int len, std::unique_ptr<TrigPlan>& out) {
   return TVD_OK;
 }
 
+static long long modinv(long long a, long long m) {
+  long long g = m, x = 0, x1 = 1, aa = a % m;
+  while (aa) {
+    const long long qq = g / aa;
+    long long t = g - qq * aa; g = aa; aa = t;
+    t = x - qq * x1; x = x1; x1 = t;
+  }
+  return ((x % m) + m) % m;
+}
+
+// Odd-symmetric PFA plan for the DST families: L odd, <= 3 coprime prime-power
+// factors, each small enough for a direct DFT (tvd_pfa.cu).
+static bool build_pfa(TrigPlan* P) {
+  if (P->family != kFamDst1 && P->family != kFamSineHat) return false;
+  const int L = P->L;
+  if (L < 3 || (L & 1) == 0 || L - 1 > 2048) return false;
+  std::vector<int> pr = factorize(L), groups;
+  for (size_t i = 0; i < pr.size();) {
+    int g = 1;
+    const int p = pr[i];
+    while (i < pr.size() && pr[i] == p) { g *= p; ++i; }
+    groups.push_back(g);
+  }
+  if (groups.size() > 3) return false;
+  for (int g : groups)
+    if (g > 255) return false;
+  std::sort(groups.rbegin(), groups.rend());
+  PfaPlan& pl = P->pfa;
+  pl = PfaPlan{};
+  pl.L = L;
+  pl.d = (int)groups.size();
+  for (int s = 0; s < pl.d; ++s) pl.q[s] = groups[s];
+  for (int s = 0; s < pl.d; ++s) {
+    int stv = 1;
+    for (int t = s + 1; t < pl.d; ++t) stv *= pl.q[t];
+    pl.stride[s] = stv;
+    pl.rinv[s] = (int)modinv((L / pl.q[s]) % pl.q[s], pl.q[s]);
+    pl.fq[s] = make_fdiv(pl.q[s]);
+  }
+  pl.fN = make_fdiv(L - 1);
+  for (int s = 0; s < pl.d; ++s) {
+    PfaStage& S = pl.st[s];
+    S.q = pl.q[s];
+    S.H = (S.q - 1) / 2;
+    S.st = pl.stride[s];
+    std::vector<int> od;
+    for (int t = 0; t < pl.d; ++t)
+      if (t != s) od.push_back(t);
+    S.D1 = 1; S.S1 = 0; S.D2 = 1; S.S2 = 0;
+    if (od.size() == 1) { S.D2 = pl.q[od[0]]; S.S2 = pl.stride[od[0]]; }
+    if (od.size() == 2) {
+      S.D1 = pl.q[od[0]]; S.S1 = pl.stride[od[0]];
+      S.D2 = pl.q[od[1]]; S.S2 = pl.stride[od[1]];
+    }
+    S.Rcnt = (S.D1 * S.D2 + 1) / 2;
+    S.h2 = (S.D2 + 1) / 2;
+    S.kb = 4;
+    S.nch = (S.H + S.kb - 1) / S.kb;
+    S.fRcnt = make_fdiv(S.Rcnt);
+    S.fD2 = make_fdiv(S.D2);
+    S.fnch = make_fdiv(S.nch);
+    S.fH = make_fdiv(S.H);
+    std::vector<double2> M((size_t)S.H * S.H + S.kb * 2, make_double2(0.0, 0.0));
+    for (int r = 1; r <= S.H; ++r)
+      for (int k = 1; k <= S.H; ++k) {
+        double cv, sv;
+        cis_pi(2LL * r * k, S.q, &cv, &sv);
+        M[(size_t)(r - 1) * S.H + (k - 1)] = make_double2(cv, sv);
+      }
+    double2* dm;
+    if (upload(M, &dm, P->owned) != cudaSuccess) return false;
+    S.M = dm;
+  }
+  return true;
+}
+
 static int get_plan(tvd_ctx* c, int family, int len, const TrigPlan** out) {
   auto key = std::make_pair(family, len);
   auto it = c->plans.find(key);
@@ -263,6 +380,7 @@ static int get_plan(tvd_ctx* c, int family, int len, const TrigPlan** out) {
     std::unique_ptr<TrigPlan> P;
     int rc = build_plan(family, len, P);
     if (rc) return rc;
+    P->pfa_ok = build_pfa(P.get());
     it = c->plans.emplace(key, std::move(P)).first;
   }
   *out = it->second.get();
@@ -283,7 +401,12 @@ static int run_lines(tvd_ctx* c, int family, const LineGeom& g, int analysis, co
   const TrigPlan* P;
   int rc = get_plan(c, family, g.len, &P);
   if (rc) return rc;
-  TVD_CUDA(launch_trig(*P, g, analysis, io, nb, c->stream));
+  if (P->pfa_ok && !c->force_generic)
+    TVD_LAUNCH(c, g.es == 1 ? kCatTrigRows : kCatTrigCols, 1,
+               launch_pfa(P->pfa, family, g.len, g, io, nb, c->stream));
+  else
+    TVD_LAUNCH(c, g.es == 1 ? kCatTrigRows : kCatTrigCols, 1,
+               launch_trig(*P, g, analysis, io, nb, c->stream));
   return TVD_OK;
 }
 
@@ -445,7 +568,7 @@ static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double
   if (sys->s) {
     double* sp;
     TVD_SLOT(c, kSlotSP, N, sp);
-    TVD_CUDA(launch_mul(sys->s, in, sp, N, c->stream));
+    TVD_LAUNCH(c, kCatVec, 1, launch_mul(sys->s, in, sp, N, c->stream));
     w = sp;
   }
   Epilogue ep{};
@@ -462,8 +585,8 @@ static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double
   double* tmp;
   TVD_SLOT(c, kSlotTmp, N, tmp);
   if (b->separable) {
-    TVD_CUDA(launch_band_rows(b->g[1], w, tmp, skip, c->stream));
-    TVD_CUDA(launch_band_cols(b->g[0], tmp, out, ep, skip, c->stream));
+    TVD_LAUNCH(c, kCatBandRows, 1, launch_band_rows(b->g[1], w, tmp, skip, c->stream));
+    TVD_LAUNCH(c, kCatBandCols, 1, launch_band_cols(b->g[0], tmp, out, ep, skip, c->stream));
     if (nb_out) *nb_out = band_cols_blocks(n);
   } else {
     const int T = n + 2 * b->m;
@@ -471,10 +594,10 @@ static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double
     TVD_SLOT(c, kSlotExtA, (size_t)T * T, ea);
     TVD_SLOT(c, kSlotExtB, (size_t)T * T, eb);
     TVD_SLOT(c, kSlotTmp2, N, t2);
-    TVD_CUDA(launch_general_blur(w, tmp, n, b->m, b->bc, b->d_psf, 0, ea, eb, c->stream));
+    TVD_LAUNCH(c, kCatGeneral, 2, launch_general_blur(w, tmp, n, b->m, b->bc, b->d_psf, 0, ea, eb, c->stream));
     const int back_t = b->bc == TVD_BC_REFLECTIVE ? 0 : 1;
-    TVD_CUDA(launch_general_blur(tmp, t2, n, b->m, b->bc, b->d_psf, back_t, ea, eb, c->stream));
-    TVD_CUDA(launch_normal_epilogue(t2, ep, n, out, skip, vec_blocks(), c->stream));
+    TVD_LAUNCH(c, kCatGeneral, back_t ? 3 : 2, launch_general_blur(tmp, t2, n, b->m, b->bc, b->d_psf, back_t, ea, eb, c->stream));
+    TVD_LAUNCH(c, kCatVec, 1, launch_normal_epilogue(t2, ep, n, out, skip, vec_blocks(), c->stream));
     if (nb_out) *nb_out = vec_blocks();
   }
   return TVD_OK;
@@ -518,6 +641,48 @@ int tvd_ctx_sync(tvd_ctx* c) {
   return TVD_OK;
 }
 
+int tvd_ctx_set_option(tvd_ctx* c, int option, int value) {
+  if (!c) return fail(TVD_ERR_INVALID, "null context");
+  if (option == TVD_OPT_GENERIC_FFT) c->force_generic = value != 0;
+  else return fail(TVD_ERR_INVALID, "unknown option");
+  return TVD_OK;
+}
+
+int tvd_ctx_counters(tvd_ctx* c, long long* launches) {
+  if (!c || !launches) return fail(TVD_ERR_INVALID, "null argument");
+  *launches = c->launches;
+  return TVD_OK;
+}
+
+int tvd_ctx_profile(tvd_ctx* c, int enable) {
+  if (!c) return fail(TVD_ERR_INVALID, "null context");
+  c->profiling = enable != 0;
+  c->ev_marks.clear();
+  return TVD_OK;
+}
+
+const char* tvd_profile_category(int id) {
+  return (id >= 0 && id < kCatCount) ? kCatNames[id] : nullptr;
+}
+
+int tvd_ctx_profile_read(tvd_ctx* c, int ncat, double* total_ms, long long* count) {
+  if (!c || !total_ms || !count) return fail(TVD_ERR_INVALID, "null argument");
+  TVD_CUDA(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < ncat; ++i) {
+    total_ms[i] = 0.0;
+    count[i] = 0;
+  }
+  for (const auto& mk : c->ev_marks) {
+    float ms = 0.f;
+    TVD_CUDA(cudaEventElapsedTime(&ms, c->ev_pool[mk.second], c->ev_pool[mk.second + 1]));
+    if (mk.first < ncat) {
+      total_ms[mk.first] += ms;
+      count[mk.first] += 1;
+    }
+  }
+  return TVD_OK;
+}
+
 int tvd_ctx_destroy(tvd_ctx* c) {
   if (!c) return TVD_OK;
   DeviceGuard g(c->device);
@@ -529,6 +694,7 @@ int tvd_ctx_destroy(tvd_ctx* c) {
   cudaFreeHost(c->h_state);
   cudaFreeHost(c->h_scalar);
   cudaFree(c->d_scalar);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
   return TVD_OK;
 }
@@ -609,15 +775,16 @@ int tvd_blur_apply(tvd_blur* b, const double* in, double* out, int transpose) {
     TVD_SLOT(c, kSlotTmp, (size_t)n * n, tmp);
     const BandOp* ops = transpose ? b->h1t : b->h1;
     Epilogue ep{};
-    TVD_CUDA(launch_band_cols(ops[0], in, tmp, ep, nullptr, c->stream));
-    TVD_CUDA(launch_band_rows(ops[1], tmp, out, nullptr, c->stream));
+    TVD_LAUNCH(c, kCatBandCols, 1, launch_band_cols(ops[0], in, tmp, ep, nullptr, c->stream));
+    TVD_LAUNCH(c, kCatBandRows, 1, launch_band_rows(ops[1], tmp, out, nullptr, c->stream));
   } else {
     const int T = n + 2 * b->m;
     double *ea, *eb;
     TVD_SLOT(c, kSlotExtA, (size_t)T * T, ea);
     TVD_SLOT(c, kSlotExtB, (size_t)T * T, eb);
-    TVD_CUDA(launch_general_blur(in, out, n, b->m, b->bc, b->d_psf, transpose ? 1 : 0, ea, eb,
-                                 c->stream));
+    TVD_LAUNCH(c, kCatGeneral, transpose ? 3 : 2,
+               launch_general_blur(in, out, n, b->m, b->bc, b->d_psf, transpose ? 1 : 0, ea, eb,
+                                   c->stream));
   }
   return TVD_OK;
 }
@@ -646,7 +813,10 @@ int tvd_blur_eigenvalues(tvd_blur* b, double* lam) {
   std::vector<void*> owned;
   if (upload(cs, &dcs, owned) != cudaSuccess) return fail(TVD_ERR_CUDA, "upload failed");
   TVD_SLOT(c, kSlotTmp, (size_t)K * n, tmp);
+  prof_begin(c, kCatStencil);
   cudaError_t e = launch_eigenvalues(dcs, b->d_psf, n, K, tmp, lam, c->stream);
+  prof_end(c);
+  c->launches += 2;
   cudaStreamSynchronize(c->stream);
   for (void* p : owned) cudaFree(p);
   if (e != cudaSuccess) return fail(TVD_ERR_CUDA, cudaGetErrorString(e));
@@ -660,7 +830,7 @@ int tvd_diffusivity(tvd_ctx* c, int n, double beta, double spacing, const double
   if (beta <= 0) return fail(TVD_ERR_INVALID, "beta must be positive");
   if (spacing <= 0) return fail(TVD_ERR_INVALID, "spacing must be positive");
   DeviceGuard g(c->device);
-  TVD_CUDA(launch_diffusivity(u, n, beta, spacing, a_h, a_v, c->stream));
+  TVD_LAUNCH(c, kCatStencil, 1, launch_diffusivity(u, n, beta, spacing, a_h, a_v, c->stream));
   return TVD_OK;
 }
 
@@ -668,7 +838,7 @@ int tvd_diffusion_apply(tvd_ctx* c, int n, double spacing, const double* a_h, co
                         const double* w, double* out) {
   if (!c || !a_h || !a_v || !w || !out) return fail(TVD_ERR_INVALID, "null argument");
   DeviceGuard g(c->device);
-  TVD_CUDA(launch_diffusion_apply(a_h, a_v, w, n, 1.0 / (spacing * spacing), out, c->stream));
+  TVD_LAUNCH(c, kCatStencil, 1, launch_diffusion_apply(a_h, a_v, w, n, 1.0 / (spacing * spacing), out, c->stream));
   return TVD_OK;
 }
 
@@ -676,8 +846,9 @@ int tvd_diffusion_bands(tvd_ctx* c, int n, double spacing, const double* a_h, co
                         double* diag, double* inner, double* block) {
   if (!c || !a_h || !a_v || !diag || !inner || !block) return fail(TVD_ERR_INVALID, "null argument");
   DeviceGuard g(c->device);
-  TVD_CUDA(launch_diffusion_bands(a_h, a_v, n, 1.0 / (spacing * spacing), diag, inner, block,
-                                  c->stream));
+  TVD_LAUNCH(c, kCatStencil, 1,
+             launch_diffusion_bands(a_h, a_v, n, 1.0 / (spacing * spacing), diag, inner, block,
+                                    c->stream));
   return TVD_OK;
 }
 
@@ -728,14 +899,14 @@ static int level2(tvd_ctx* c, const TrigPlan* P, int n, const double* diag, cons
   a.c1 = inner ? 2.0 : 0.0;
   a.nlines = n;
   a.out = lam0; a.out_ls = n; a.out_es = 1;
-  TVD_CUDA(launch_band_project(*P, 1, a, nullptr, c->stream));
+  TVD_LAUNCH(c, kCatProject, 1, launch_band_project(*P, 1, a, nullptr, c->stream));
   if (block) {
     TVD_SLOT(c, kSlotLam1, (size_t)n * n, lam1);
     BandLines b{};
     b.b0 = block; b.b0_ls = n; b.b0_es = 1;
     b.nlines = n - 1;
     b.out = lam1; b.out_ls = n; b.out_es = 1;
-    TVD_CUDA(launch_band_project(*P, 1, b, nullptr, c->stream));
+    TVD_LAUNCH(c, kCatProject, 1, launch_band_project(*P, 1, b, nullptr, c->stream));
   }
   BandLines f{};
   f.b0 = lam0; f.b0_ls = 1; f.b0_es = n;
@@ -748,7 +919,7 @@ static int level2(tvd_ctx* c, const TrigPlan* P, int n, const double* diag, cons
   f.lamd = lamd;
   f.alpha = alpha;
   f.partial_minmax = partial_minmax;
-  TVD_CUDA(launch_band_project(*P, 0, f, nb_out, c->stream));
+  TVD_LAUNCH(c, kCatProject, 1, launch_band_project(*P, 0, f, nb_out, c->stream));
   return TVD_OK;
 }
 
@@ -758,7 +929,7 @@ int tvd_scaling(tvd_ctx* c, long long count, double alpha, const double* diag, d
   DeviceGuard g(c->device);
   double* part;
   TVD_SLOT(c, kSlotPartial2, vec_blocks(), part);
-  TVD_CUDA(launch_scaling(diag, alpha, d, d_sqrt, s, count, part, vec_blocks(), c->stream));
+  TVD_LAUNCH(c, kCatVec, 1, launch_scaling(diag, alpha, d, d_sqrt, s, count, part, vec_blocks(), c->stream));
   std::vector<double> h(vec_blocks());
   TVD_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream));
@@ -812,7 +983,7 @@ int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alph
     TVD_SLOT(c, kSlotBlockS, N, bs);
     rc = level2(c, P, n, s, nullptr, nullptr, lamd, 0, nullptr, nullptr, 0.0, nullptr, nullptr);
     if (rc) return rc;
-    TVD_CUDA(launch_scale_bands(diag, inner, block, s, n, ds, is, bs, c->stream));
+    TVD_LAUNCH(c, kCatVec, 1, launch_scale_bands(diag, inner, block, s, n, ds, is, bs, c->stream));
     rc = level2(c, P, n, ds, is, bs, eig, 2, lam_h, lamd, alpha, mm, &nb);
   } else {
     rc = level2(c, P, n, diag, inner, block, eig, 1, lam_h, nullptr, alpha, mm, &nb);
@@ -827,7 +998,7 @@ int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alph
   const double floor = 1e-14 * mx;
   double* part;
   TVD_SLOT(c, kSlotPartial, vec_blocks(), part);
-  TVD_CUDA(launch_invert_eigs(eig, floor, inv_eig, N, part, vec_blocks(), c->stream));
+  TVD_LAUNCH(c, kCatVec, 1, launch_invert_eigs(eig, floor, inv_eig, N, part, vec_blocks(), c->stream));
   std::vector<double> h(vec_blocks());
   TVD_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream));
@@ -874,13 +1045,13 @@ static int minv_internal(tvd_ctx* c, const tvd_precond* pre, int n, const double
                          double* partial, const int* skip, int* nb) {
   const long N = (long)n * n;
   if (!pre || pre->kind == TVD_PRECOND_NONE) {
-    if (z != r) TVD_CUDA(launch_copy(r, z, N, skip, c->stream));
-    TVD_CUDA(launch_dot_partials(r, r, N, partial, vec_blocks(), skip, c->stream));
+    if (z != r) TVD_LAUNCH(c, kCatVec, 1, launch_copy(r, z, N, skip, c->stream));
+    TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(r, r, N, partial, vec_blocks(), skip, c->stream));
     *nb = vec_blocks();
     return TVD_OK;
   }
   if (pre->kind == TVD_PRECOND_DIAG) {
-    TVD_CUDA(launch_diag_solve(r, pre->d, z, N, partial, vec_blocks(), skip, c->stream));
+    TVD_LAUNCH(c, kCatVec, 1, launch_diag_solve(r, pre->d, z, N, partial, vec_blocks(), skip, c->stream));
     *nb = vec_blocks();
     return TVD_OK;
   }
@@ -922,25 +1093,25 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   // r = b - A x ; r0 = ||r||
   rc = system_apply_internal(c, sys, x, q, nullptr, nullptr, nullptr, &nb);
   if (rc) return rc;
-  TVD_CUDA(launch_residual_init(b, q, r, N, partial, vec_blocks(), st));
-  TVD_CUDA(launch_pcg_start(S, partial, vec_blocks(), st));
+  TVD_LAUNCH(c, kCatVec, 1, launch_residual_init(b, q, r, N, partial, vec_blocks(), st));
+  TVD_LAUNCH(c, kCatFin, 1, launch_pcg_start(S, partial, vec_blocks(), st));
   // z = M^-1 r ; p = z ; rz = r.z
   rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb);
   if (rc) return rc;
-  TVD_CUDA(launch_pcg_rz0(S, partial, nb, st));
-  TVD_CUDA(launch_copy(zz, p, N, skip, st));
+  TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rz0(S, partial, nb, st));
+  TVD_LAUNCH(c, kCatVec, 1, launch_copy(zz, p, N, skip, st));
   int chunk = 4;
   for (int done_it = 0;;) {
     for (int k = 0; k < chunk; ++k) {
       rc = system_apply_internal(c, sys, p, q, p, partial, skip, &nb);
       if (rc) return rc;
-      TVD_CUDA(launch_pcg_gamma(S, partial, nb, st));
-      TVD_CUDA(launch_pcg_update_xr(S, x, r, p, q, N, partial, vec_blocks(), st));
-      TVD_CUDA(launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
+      TVD_LAUNCH(c, kCatFin, 1, launch_pcg_gamma(S, partial, nb, st));
+      TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, p, q, N, partial, vec_blocks(), st));
+      TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
       rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb);
       if (rc) return rc;
-      TVD_CUDA(launch_pcg_beta(S, partial, nb, max_iterations, st));
-      TVD_CUDA(launch_pcg_update_p(S, p, zz, N, st));
+      TVD_LAUNCH(c, kCatFin, 1, launch_pcg_beta(S, partial, nb, max_iterations, st));
+      TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_p(S, p, zz, N, st));
     }
     done_it += chunk;
     TVD_CUDA(cudaMemcpyAsync(c->h_state, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
@@ -964,8 +1135,8 @@ int tvd_vec_dot(tvd_ctx* c, long long count, const double* x, const double* y, d
   DeviceGuard g(c->device);
   double* part;
   TVD_SLOT(c, kSlotPartial2, vec_blocks(), part);
-  TVD_CUDA(launch_dot_partials(x, y, count, part, vec_blocks(), nullptr, c->stream));
-  TVD_CUDA(launch_sum_partials(part, vec_blocks(), c->d_scalar, c->stream));
+  TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(x, y, count, part, vec_blocks(), nullptr, c->stream));
+  TVD_LAUNCH(c, kCatFin, 1, launch_sum_partials(part, vec_blocks(), c->d_scalar, c->stream));
   TVD_CUDA(cudaMemcpyAsync(c->h_scalar, c->d_scalar, sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream));
   TVD_CUDA(cudaStreamSynchronize(c->stream));
@@ -977,7 +1148,7 @@ int tvd_vec_axpby(tvd_ctx* c, long long count, double a, const double* x, double
                   double* out) {
   if (!c || !x || !y || !out) return fail(TVD_ERR_INVALID, "null argument");
   DeviceGuard g(c->device);
-  TVD_CUDA(launch_axpby(a, x, b, y, out, count, c->stream));
+  TVD_LAUNCH(c, kCatVec, 1, launch_axpby(a, x, b, y, out, count, c->stream));
   return TVD_OK;
 }
 
@@ -985,8 +1156,8 @@ int tvd_vec_binary(tvd_ctx* c, long long count, int op, const double* x, const d
                    double* out) {
   if (!c || !x || !y || !out) return fail(TVD_ERR_INVALID, "null argument");
   DeviceGuard g(c->device);
-  if (op == 0) TVD_CUDA(launch_mul(x, y, out, count, c->stream));
-  else if (op == 1) TVD_CUDA(launch_div(x, y, out, count, c->stream));
+  if (op == 0) TVD_LAUNCH(c, kCatVec, 1, launch_mul(x, y, out, count, c->stream));
+  else if (op == 1) TVD_LAUNCH(c, kCatVec, 1, launch_div(x, y, out, count, c->stream));
   else return fail(TVD_ERR_INVALID, "unknown op");
   return TVD_OK;
 }

@@ -24,15 +24,46 @@ struct LineGeom {
   long es;
 };
 
+// ---- odd-symmetric prime-factor DST engine (tvd_pfa.cu)
+// x / d == (x * m) >> 40 exactly for 0 <= x, d < 2^20.
+struct FDiv {
+  unsigned long long m;
+  int d;
+};
+inline FDiv make_fdiv(int d) {
+  FDiv f;
+  f.d = d;
+  f.m = ((1ULL << 40) + (unsigned long long)d - 1) / (unsigned long long)d;
+  return f;
+}
+
+struct PfaStage {
+  int q, H, st;        // DFT size along this dimension, (q-1)/2, layout stride
+  int D1, D2, S1, S2;  // the other dimensions (sizes, strides); D1 = 1 when only one
+  int Rcnt, h2, nch, kb;
+  FDiv fRcnt, fD2, fnch, fH;
+  const double2* M;    // [(r-1) * H + (k-1)] = (cos, sin)(2 pi r k / q), padded
+};
+
+struct PfaPlan {
+  int L, d;
+  int q[3], stride[3], rinv[3];
+  FDiv fq[3];
+  FDiv fN;             // N = L - 1
+  PfaStage st[3];
+};
+
 // Device-resident FFT plan plus the per-length twiddle tables of one family.
 struct TrigPlan {
   int family;     // Family
-  int n;          // array side
+  int n;          // line length
   int L;          // FFT length per line
   FftPlan fft;
   const double2* wfull;  // exp(-i pi k / L), k in [0, L)
   const double2* whalf;  // DCT only: exp(-i pi k / (2n)), k in [0, n)
   int max_items_line;    // largest per-line work-item count over the stages
+  bool pfa_ok = false;   // DST family with an odd, <=3-factor coprime L
+  PfaPlan pfa;
   std::vector<void*> owned;
 };
 
@@ -65,11 +96,6 @@ struct BandLines {
   double* partial_minmax;  // per-CTA (min, max) pairs (epi != 0)
 };
 
-struct Status {
-  int code = 0;
-  std::string msg;
-};
-
 // ---- launchers (tvd_lines.cu)
 cudaError_t launch_trig(const TrigPlan& P, const LineGeom& g, int analysis, const LineIO& io,
                         int* nblocks_out, cudaStream_t st);
@@ -77,5 +103,10 @@ cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
                                 int* nblocks_out, cudaStream_t st);
 int trig_lines_per_cta(const TrigPlan& P, bool contiguous, int* nthreads, size_t* smem);
 int trig_blocks(const TrigPlan& P, const LineGeom& g);
+
+// ---- odd-symmetric PFA DST-I pass (tvd_pfa.cu), family DST1 / SINE_HAT
+cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g, const LineIO& io,
+                       int* nblocks_out, cudaStream_t st);
+int pfa_blocks(const PfaPlan& P, const LineGeom& g);
 
 }  // namespace tvd

@@ -1,0 +1,373 @@
+// Odd-symmetric prime-factor DST-I engine (the Shat / M preconditioner passes).
+//
+// A DST-I of length N = L - 1 with L odd is one complex DFT of length L of the
+// packed odd-extension sequence c'_j = z_{2j} + i z_{2((j+h) mod L)+1}
+// (tvd_lines.cu).  c' is odd (c'_{L-j} = -c'_j), so is its DFT.  With
+// L = q_1 q_2 ... q_d (pairwise coprime, d <= 3) the Good-Thomas map
+//   input  j <-> (j_s = (j mod q_s) * (L/q_s)^{-1} mod q_s)   (Ruritanian)
+//   output k <-> (k_s = k mod q_s)                            (CRT)
+// turns the DFT into a d-dimensional DFT without twiddles, computed in place
+// one dimension at a time.  Negating j negates every index, so along each
+// dimension only one DFT of every {tau, -tau} pair of "other-index" tuples is
+// computed; its partner line is written as the negated, index-reversed copy.
+// That halves the arithmetic of the generic FFT, and the self-paired line
+// (tau = 0) is odd, so its DFT needs only the sine half.  Each q-point DFT
+// folds inputs into a_r = x_r + x_{q-r}, b_r = x_r - x_{q-r} and accumulates
+// KB output pairs per work item from a (cos, sin) matrix laid out so the KB
+// coefficients of one r are contiguous (immediate-offset loads).
+// Reference semantics: transforms.py:52-81 (dst1_apply / sinehat_apply).
+#include "tvd_internal.h"
+
+namespace tvd {
+
+__device__ __forceinline__ int fdiv(int x, const FDiv& f) {
+  return (int)(((unsigned long long)(unsigned)x * f.m) >> 40);
+}
+__device__ __forceinline__ int fmodq(int x, const FDiv& f) { return x - fdiv(x, f) * f.d; }
+
+struct PfaK {
+  PfaPlan pl;
+  int n, off, N, nl, nlines;
+  long ls, es;
+  double scale;  // 0.5 * sqrt(2 / L)
+  int h;         // (L - 1) / 2
+  LineIO io;
+};
+
+// representative "other-index" tuple t -> (a, b)
+__device__ __forceinline__ void rep_tuple(int t, const PfaStage& S, int& a, int& b) {
+  if (t < S.h2) {
+    a = 0;
+    b = t;
+  } else {
+    const int u = t - S.h2;
+    const int qd = fdiv(u, S.fD2);
+    a = 1 + qd;
+    b = u - qd * S.D2;
+  }
+}
+
+template <int KB>
+__device__ __forceinline__ void pfa_stage(double2* buf, int LP, int nl, const PfaStage& S) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int q = S.q, H = S.H, st = S.st;
+  // fold x_r, x_{q-r} -> a_r, b_r for every representative line
+  const int nfold = nl * S.Rcnt * H;
+  for (int i = tid; i < nfold; i += nth) {
+    const int rest = fdiv(i, S.fRcnt);
+    const int t = i - rest * S.Rcnt;
+    const int line = fdiv(rest, S.fH);
+    const int r = 1 + rest - line * H;
+    int a, b;
+    rep_tuple(t, S, a, b);
+    double2* p = buf + line * LP + a * S.S1 + b * S.S2;
+    const double2 x1 = p[r * st], x2 = p[(q - r) * st];
+    p[r * st] = cadd(x1, x2);
+    p[(q - r) * st] = csub(x1, x2);
+  }
+  __syncthreads();
+  const int nch = S.nch;
+  const int ndft = nl * S.Rcnt;
+  const bool all_self = S.D1 * S.D2 == 1;  // prime L: the only line is odd
+  int dpr = nth / nch;  // DFTs per round (all chunks of a DFT share a round)
+  for (int d0 = 0; d0 < ndft; d0 += dpr) {
+    const int dr = min(dpr, ndft - d0);
+    const int items = dr * nch;
+    const bool active = tid < items;
+    double2 A[KB], B[KB];
+    double2 x0 = make_double2(0.0, 0.0), s0 = x0;
+    int c = 0, base = 0, neg = 0;
+    bool self = false;
+    if (active) {
+      // DFT index fastest across lanes: the chunk (coefficient rows) is warp-uniform
+      c = tid / dr;
+      const int dft = d0 + tid - c * dr;
+      const int line = fdiv(dft, S.fRcnt);
+      const int t = dft - line * S.Rcnt;
+      int a, b;
+      rep_tuple(t, S, a, b);
+      self = (t == 0);
+      base = line * LP + a * S.S1 + b * S.S2;
+      const int na = a == 0 ? 0 : S.D1 - a, nb = b == 0 ? 0 : S.D2 - b;
+      neg = line * LP + na * S.S1 + nb * S.S2;
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        A[k] = make_double2(0.0, 0.0);
+        B[k] = make_double2(0.0, 0.0);
+      }
+      const double2* p = buf + base;
+      x0 = p[0];
+      s0 = x0;
+      const double2* m = S.M + c * KB;
+      if (all_self) {  // odd line: a_r == 0, only the sine half contributes
+#pragma unroll 2
+        for (int r = 1; r <= H; ++r, m += H) {
+          const double2 bb = p[(q - r) * st];
+#pragma unroll
+          for (int k = 0; k < KB; ++k) {
+            const double sn = __ldg(&m[k].y);
+            B[k].x += bb.x * sn;
+            B[k].y += bb.y * sn;
+          }
+        }
+      } else {
+#pragma unroll 2
+        for (int r = 1; r <= H; ++r, m += H) {
+          const double2 aa = p[r * st], bb = p[(q - r) * st];
+          s0 = cadd(s0, aa);
+#pragma unroll
+          for (int k = 0; k < KB; ++k) {
+            const double2 w = __ldg(&m[k]);
+            A[k].x += aa.x * w.x;
+            A[k].y += aa.y * w.x;
+            B[k].x += bb.x * w.y;
+            B[k].y += bb.y * w.y;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (active) {
+      double2* p = buf + base;
+      double2* pn = buf + neg;
+      if (c == 0) {
+        p[0] = s0;
+        if (!self) pn[0] = make_double2(-s0.x, -s0.y);
+      }
+      const int k0 = 1 + c * KB;
+#pragma unroll
+      for (int kk = 0; kk < KB; ++kk) {
+        const int k = k0 + kk;
+        if (k <= H) {
+          const double2 vk = make_double2(x0.x + A[kk].x + B[kk].y, x0.y + A[kk].y - B[kk].x);
+          const double2 vm = make_double2(x0.x + A[kk].x - B[kk].y, x0.y + A[kk].y + B[kk].x);
+          p[k * st] = vk;
+          p[(q - k) * st] = vm;
+          if (!self) {
+            pn[(q - k) * st] = make_double2(-vk.x, -vk.y);
+            pn[k * st] = make_double2(-vm.x, -vm.y);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// position of c'_j in the PFA layout (Ruritanian input map) and of c'_{-j}
+__device__ __forceinline__ void in_pos(int j, const PfaPlan& pl, int& pos, int& npos) {
+  pos = 0;
+  npos = 0;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    if (s < pl.d) {
+      const int m = fmodq(fmodq(j, pl.fq[s]) * pl.rinv[s], pl.fq[s]);
+      pos += m * pl.stride[s];
+      npos += (m == 0 ? 0 : pl.q[s] - m) * pl.stride[s];
+    }
+  }
+}
+
+__device__ __forceinline__ int out_pos(int k, const PfaPlan& pl) {
+  int pos = 0;
+#pragma unroll
+  for (int s = 0; s < 3; ++s)
+    if (s < pl.d) pos += fmodq(k, pl.fq[s]) * pl.stride[s];
+  return pos;
+}
+
+// scatter x_t (t = 1..N) into the packed odd sequence: z_t = x_t, z_{2L-t} = -x_t
+__device__ __forceinline__ void scatter_x(double2* line, int t, double v, const PfaK& p) {
+  const int L = p.pl.L;
+  int j, comp;
+  if ((t & 1) == 0) {
+    j = t >> 1;
+    comp = 0;
+  } else {
+    j = ((t - 1) >> 1) - p.h;
+    if (j < 0) j += L;
+    comp = 1;
+  }
+  int pos, npos;
+  in_pos(j, p.pl, pos, npos);
+  double* a = reinterpret_cast<double*>(line + pos) + comp;
+  double* b = reinterpret_cast<double*>(line + npos) + comp;
+  *a = v;
+  *b = -v;
+}
+
+__device__ __forceinline__ double gather_y(const double2* line, int k, const PfaK& p) {
+  const double2 C = line[out_pos(k, p.pl)];
+  const double y = (k & 1) ? -(C.y + C.x) : -(C.y - C.x);
+  return y * p.scale;
+}
+
+__device__ __forceinline__ void pfa_transform(double2* buf, int LP, int nl, const PfaK& p) {
+  for (int s = 0; s < p.pl.d; ++s) {
+    const PfaStage& S = p.pl.st[s];
+    pfa_stage<4>(buf, LP, nl, S);
+  }
+}
+
+constexpr int kPfaMaxV = 8;   // per-thread register values in the sandwich re-pack
+constexpr int kPfaBatch = 8;  // global loads in flight per thread in the pack
+
+__global__ void __launch_bounds__(256, 3) k_pfa(const PfaK p) {
+  const LineIO& io = p.io;
+  if (io.skip && *io.skip) return;
+  extern __shared__ double2 smem2[];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int L = p.pl.L, LP = L, N = p.N, nl = p.nl;
+  const int line0 = blockIdx.x * nl;
+  const int nlv = min(nl, p.nlines - line0);
+  double2* buf = smem2;
+  auto gidx = [&](int l, int t) {  // t: 1..N interior index
+    return (long)(line0 + l) * p.ls + (long)(p.off + t - 1) * p.es;
+  };
+  // zero slot of every line (c'_0 = 0) and dead lines
+  for (int i = tid; i < nl; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
+  for (int i = tid; i < (nl - nlv) * L; i += nth) buf[nlv * LP + i] = make_double2(0.0, 0.0);
+  // element i of this CTA's lines -> (line, t), memory-friendly order
+  const bool contig = p.es == 1;
+  auto split = [&](int i, int& l, int& t) {
+    if (contig) {
+      l = fdiv(i, p.pl.fN);
+      t = 1 + i - l * N;
+    } else {
+      t = 1 + (nlv == 2 ? (i >> 1) : i / nlv);
+      l = i - (t - 1) * nlv;
+    }
+  };
+  // pack: kPfaBatch global loads in flight per thread, then the smem scatter
+  const int total = nlv * N;
+  for (int i0 = 0; i0 < total; i0 += kPfaBatch * nth) {
+    double v[kPfaBatch];
+#pragma unroll
+    for (int s = 0; s < kPfaBatch; ++s) {
+      const int i = i0 + tid + s * nth;
+      if (i < total) {
+        int l, t;
+        split(i, l, t);
+        const long g = gidx(l, t);
+        v[s] = io.in[g];
+        if (io.pre) v[s] = io.pre_mul ? v[s] * io.pre[g] : v[s] / io.pre[g];
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kPfaBatch; ++s) {
+      const int i = i0 + tid + s * nth;
+      if (i < total) {
+        int l, t;
+        split(i, l, t);
+        scatter_x(buf + l * LP, t, v[s], p);
+      }
+    }
+  }
+  __syncthreads();
+  pfa_transform(buf, LP, nl, p);
+
+  if (io.mid_mul) {
+    // y <- mid .* y, re-packed line by line through registers, then transform again
+    for (int l = 0; l < nlv; ++l) {
+      double v[kPfaMaxV];
+#pragma unroll
+      for (int s = 0; s < kPfaMaxV; ++s) {
+        const int t = 1 + tid + s * nth;
+        v[s] = t <= N ? gather_y(buf + l * LP, t, p) * io.mid_mul[gidx(l, t)] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < kPfaMaxV; ++s) {
+        const int t = 1 + tid + s * nth;
+        if (t <= N) scatter_x(buf + l * LP, t, v[s], p);
+      }
+      __syncthreads();
+    }
+    for (int l = nlv; l < nl; ++l)
+      for (int i = tid; i < L; i += nth) buf[l * LP + i] = make_double2(0.0, 0.0);
+    for (int l = tid; l < nlv; l += nth) buf[l * LP] = make_double2(0.0, 0.0);  // c'_0
+    __syncthreads();
+    pfa_transform(buf, LP, nl, p);
+  }
+
+  // unpack + store
+  double acc = 0.0;
+  auto store = [&](long g, double v) {
+    if (io.post) v = io.post_mul ? v * io.post[g] : v / io.post[g];
+    io.out[g] = v;
+    if (io.dot_with) acc += v * io.dot_with[g];
+  };
+  for (int i = tid; i < total; i += nth) {
+    int l, t;
+    split(i, l, t);
+    store(gidx(l, t), gather_y(buf + l * LP, t, p));
+  }
+  if (p.off) {  // Shat borders pass through every transform
+    for (int i = tid; i < 2 * nlv; i += nth) {
+      const int l = i >> 1;
+      const long g = (long)(line0 + l) * p.ls + (long)((i & 1) ? p.n - 1 : 0) * p.es;
+      double v = io.in[g];
+      if (io.pre) v = io.pre_mul ? v * io.pre[g] : v / io.pre[g];
+      if (io.mid_mul) v *= io.mid_mul[g];
+      store(g, v);
+    }
+  }
+  if (io.partial) {
+    const double s = block_sum(acc, red);
+    if (tid == 0) io.partial[blockIdx.x] = s;
+  }
+}
+
+static int pfa_config(const PfaPlan& P, bool contiguous, int* nl, int* nth, size_t* smem) {
+  const size_t line_bytes = (size_t)P.L * 16;
+  int k = 2;
+  (void)contiguous;
+  while (k > 1 && k * line_bytes > 150 * 1024) k >>= 1;
+  if (line_bytes * k > 200 * 1024) return -1;
+  const int t = 256;
+  // the sandwich re-pack holds kPfaMaxV values per thread
+  if ((P.L - 1) > kPfaMaxV * t) return -1;
+  *nl = k;
+  *nth = t;
+  *smem = k * line_bytes;
+  return 0;
+}
+
+int pfa_blocks(const PfaPlan& P, const LineGeom& g) {
+  int nl, nth;
+  size_t smem;
+  if (pfa_config(P, g.es == 1, &nl, &nth, &smem)) return -1;
+  return (g.nlines + nl - 1) / nl;
+}
+
+cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g, const LineIO& io,
+                       int* nblocks_out, cudaStream_t st) {
+  int nl, nth;
+  size_t smem;
+  if (pfa_config(P, g.es == 1, &nl, &nth, &smem)) return cudaErrorInvalidConfiguration;
+  PfaK k{};
+  k.pl = P;
+  k.n = len;
+  k.off = family == kFamSineHat ? 1 : 0;
+  k.N = P.L - 1;
+  k.nl = nl;
+  k.nlines = g.nlines;
+  k.ls = g.ls;
+  k.es = g.es;
+  k.scale = 0.5 * sqrt(2.0 / P.L);
+  k.h = (P.L - 1) / 2;
+  k.io = io;
+  const int nb = (g.nlines + nl - 1) / nl;
+  if (nblocks_out) *nblocks_out = nb;
+  if (nb == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pfa, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_pfa<<<nb, nth, smem, st>>>(k);
+  return cudaGetLastError();
+}
+
+}  // namespace tvd
