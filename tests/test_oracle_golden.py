@@ -1,0 +1,105 @@
+"""Pin the CPU oracle (oracle/tvd_oracle.py) to the reference's own outputs.
+
+The goldens in tests/golden/ were produced by running the reference package
+itself (tests/golden/make_golden.py).  Only after these pass is the oracle
+trusted as the checker of the GPU path at sizes the goldens do not cover.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from oracle import tvd_oracle as O
+
+OPS = ["ops_n16.npz", "ops_n32.npz", "ops_n33.npz"]
+BCS = ("anti_reflective", "reflective")
+
+
+@pytest.mark.parametrize("name", OPS)
+def test_oracle_transforms(golden, name):
+    g = golden(name)
+    for kind in ("dst1", "sine_hat", "dct"):
+        assert rel_err(O.tensor_2d(kind, g["w"]), g[f"T2_{kind}"]) < 1e-14
+        assert rel_err(O.tensor_2d(kind, g["w"], inverse=True), g[f"T2inv_{kind}"]) < 1e-14
+
+
+def test_oracle_transforms_1d_all_lengths(golden):
+    g = golden("ops_n16.npz")
+    for length in range(3, 12):
+        x = g[f"T1in_{length}"]
+        assert rel_err(O.dst1(x), g[f"T1_dst1_{length}"]) < 1e-14
+        assert rel_err(O.sinehat(x), g[f"T1_sine_hat_{length}"]) < 1e-14
+        assert rel_err(O.dct_synthesis(x), g[f"T1_dct_{length}"]) < 1e-14
+        assert rel_err(O.dct_analysis(x), g[f"T1inv_dct_{length}"]) < 1e-14
+
+
+@pytest.mark.parametrize("name", OPS)
+@pytest.mark.parametrize("pname", ["gauss", "disk"])
+@pytest.mark.parametrize("bc", BCS)
+def test_oracle_blur(golden, name, pname, bc):
+    g = golden(name)
+    h = g[f"psf_{pname}"]
+    key = f"{pname}_{bc}"
+    n = g["u"].shape[0]
+    assert rel_err(O.blur(g["u"], h, bc), g[f"H_{key}"]) < 1e-14
+    assert rel_err(O.blur_transpose(g["u"], h, bc), g[f"HT_{key}"]) < 1e-14
+    lam = O.blur_eigenvalues(h, bc, n)
+    np.testing.assert_allclose(lam, g[f"eig_{key}"], rtol=0, atol=1e-14)
+    assert rel_err(O.blur_fast(g["u"], lam, bc), g[f"Hfast_{key}"]) < 1e-13
+    assert rel_err(O.blur_transpose_fast(g["u"], lam, bc), g[f"HTfast_{key}"]) < 1e-13
+
+
+@pytest.mark.parametrize("name", OPS)
+def test_oracle_diffusion_bit_identical(golden, name):
+    g = golden(name)
+    a_h, a_v = O.diffusivity(g["u"], float(g["beta"]))
+    np.testing.assert_array_equal(a_h, g["a_h"])
+    np.testing.assert_array_equal(a_v, g["a_v"])
+    np.testing.assert_array_equal(O.diffusion_apply(a_h, a_v, g["w"]), g["Lw"])
+    bands = O.diffusion_bands(a_h, a_v)
+    for (do, di), band in bands.items():
+        np.testing.assert_array_equal(band, g[f"band_{do}_{di}"])
+
+
+@pytest.mark.parametrize("name", OPS)
+def test_oracle_preconditioners(golden, name):
+    g = golden(name)
+    n = g["u"].shape[0]
+    alpha = float(g["alpha"])
+    a_h, a_v = O.diffusivity(g["u"], float(g["beta"]))
+    blocks = O.diffusion_bands(a_h, a_v)
+    for bc, fam in (("anti_reflective", "M"), ("reflective", "R")):
+        lam_h = O.blur_eigenvalues(g["psf_gauss"], bc, n)
+        for kind in (fam, "D_" + fam, fam + "_D"):
+            lam, lam_inv, d_sqrt, clamped = O.assemble(kind, lam_h, blocks, alpha)
+            assert clamped == 0
+            assert rel_err(lam, g[f"lam_{kind}"]) < 1e-13, kind
+            z = O.precond_solve(O.FAMILY[fam], lam_inv, g["w"], d_sqrt)
+            assert rel_err(z, g[f"minv_{kind}"]) < 1e-13, kind
+
+
+RESTORES = [("restore_c1_M.npz", "x", "anti_reflective", True),
+            ("restore_c1_M_D.npz", "x_d", "anti_reflective", True),
+            ("restore_c1_D_M.npz", "d_x", "anti_reflective", True),
+            ("restore_c1_R.npz", "x", "reflective", True),
+            ("restore_c1_R_D.npz", "x_d", "reflective", True),
+            ("restore_c1_I.npz", "none", "anti_reflective", True),
+            ("restore_c1_I_exact.npz", "none", "anti_reflective", False),
+            ("restore_c2b.npz", "x", "reflective", True)]
+
+
+@pytest.mark.parametrize("name,selector,bc,fast", RESTORES)
+def test_oracle_restore_reproduces_reference(golden, name, selector, bc, fast):
+    g = golden(name)
+    rep = O.restore(g["v"], g["psf"], bc, float(g["alpha"]), float(g["beta"]), selector,
+                    fp_max=int(g["fp_max"]), tol=float(g["tol"]), fast=fast)
+    ref = [int(k) for k in g["inner_iterations"]]
+    if selector == "none":
+        # unpreconditioned CG stagnates near tol: rounding moves the stop by up to 2
+        # steps while the image stays ~1e-9 away (see test_gpu_parity)
+        assert all(abs(a - b) <= 2 for a, b in zip(rep["inner_iterations"], ref))
+        assert rel_err(rep["restored"], g["restored"]) < 1e-8
+        return
+    assert rep["inner_iterations"] == ref
+    assert rel_err(rep["restored"], g["restored"]) < 1e-10
+    np.testing.assert_allclose(rep["gradient_norms"], g["gradient_norms"], rtol=1e-9)
