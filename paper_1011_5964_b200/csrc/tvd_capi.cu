@@ -122,6 +122,7 @@ struct tvd_blur {
   // separable factors: axis 0 (rows index) and axis 1
   BandOp h1[2], h1t[2], g[2];
   std::vector<void*> owned;
+  std::vector<std::vector<double>> host_taps;  // backing store of BandOp::taps_host
 };
 
 static cudaError_t ensure(tvd_ctx* c, int slot, size_t bytes, void** out) {
@@ -369,7 +370,64 @@ static bool build_pfa(TrigPlan* P) {
     double2* dm;
     if (upload(M, &dm, P->owned) != cudaSuccess) return false;
     S.M = dm;
+    // tensor-core form for the wide radices
+    S.use_mma = S.H >= 8 ? 1 : 0;
+    S.KP = (S.H + 1 + 7) / 8 * 8;
+    S.RP = (S.H + 3) / 4 * 4;
+    std::vector<double> cm((size_t)S.KP * S.RP, 0.0), sm((size_t)S.KP * S.RP, 0.0);
+    for (int k = 0; k <= S.H; ++k)
+      for (int r = 1; r <= S.H; ++r) {
+        double cv, sv;
+        cis_pi(2LL * r * k, S.q, &cv, &sv);
+        cm[(size_t)k * S.RP + (r - 1)] = cv;
+        sm[(size_t)k * S.RP + (r - 1)] = sv;
+      }
+    double *dcm, *dsm;
+    if (upload(cm, &dcm, P->owned) != cudaSuccess || upload(sm, &dsm, P->owned) != cudaSuccess)
+      return false;
+    S.Cm = dcm;
+    S.Sm = dsm;
+    // representative line bases of this stage (line 0): base | negated base << 16
+    std::vector<unsigned> reps(S.Rcnt);
+    for (int t = 0; t < S.Rcnt; ++t) {
+      int a, b;
+      if (t < S.h2) { a = 0; b = t; }
+      else { const int u = t - S.h2; a = 1 + u / S.D2; b = u % S.D2; }
+      const int na = a == 0 ? 0 : S.D1 - a, nb = b == 0 ? 0 : S.D2 - b;
+      const unsigned base = a * S.S1 + b * S.S2, neg = na * S.S1 + nb * S.S2;
+      reps[t] = base | (neg << 16);
+    }
+    unsigned* dreps;
+    if (upload(reps, &dreps, P->owned) != cudaSuccess) return false;
+    pl.reps[s] = dreps;
   }
+  // pack scatter (Ruritanian input map) and unpack gather (CRT output map) tables
+  const int N = L - 1, h = (L - 1) / 2;
+  std::vector<unsigned> scat(N), gath(N);
+  auto pos_of = [&](int j, unsigned& pos, unsigned& npos) {
+    pos = 0;
+    npos = 0;
+    for (int s = 0; s < pl.d; ++s) {
+      const int m = (int)(((long long)(j % pl.q[s]) * pl.rinv[s]) % pl.q[s]);
+      pos += m * pl.stride[s];
+      npos += (m == 0 ? 0 : pl.q[s] - m) * pl.stride[s];
+    }
+  };
+  for (int t = 1; t <= N; ++t) {
+    int j = (t & 1) == 0 ? t / 2 : (t - 1) / 2 - h;
+    if (j < 0) j += L;
+    unsigned pos, npos;
+    pos_of(j, pos, npos);
+    scat[t - 1] = pos | (npos << 16);
+    unsigned g = 0;
+    for (int s = 0; s < pl.d; ++s) g += (t % pl.q[s]) * pl.stride[s];
+    gath[t - 1] = g;
+  }
+  unsigned *dscat, *dgath;
+  if (upload(scat, &dscat, P->owned) != cudaSuccess || upload(gath, &dgath, P->owned) != cudaSuccess)
+    return false;
+  pl.scat = dscat;
+  pl.gath = dgath;
   return true;
 }
 
@@ -553,6 +611,8 @@ static int make_bandop(tvd_blur* b, const Taps1D& t, int border, BandOp* op) {
   op->B = B;
   op->taps = dt;
   op->table = dtab;
+  b->host_taps.push_back(taps);
+  op->taps_host = b->host_taps.back().data();
   return TVD_OK;
 }
 
@@ -587,7 +647,7 @@ static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double
   if (b->separable) {
     TVD_LAUNCH(c, kCatBandRows, 1, launch_band_rows(b->g[1], w, tmp, skip, c->stream));
     TVD_LAUNCH(c, kCatBandCols, 1, launch_band_cols(b->g[0], tmp, out, ep, skip, c->stream));
-    if (nb_out) *nb_out = band_cols_blocks(n);
+    if (nb_out) *nb_out = band_cols_grid(b->g[0]);
   } else {
     const int T = n + 2 * b->m;
     double *ea, *eb, *t2;

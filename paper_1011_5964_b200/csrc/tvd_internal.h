@@ -43,6 +43,10 @@ struct PfaStage {
   int Rcnt, h2, nch, kb;
   FDiv fRcnt, fD2, fnch, fH;
   const double2* M;    // [(r-1) * H + (k-1)] = (cos, sin)(2 pi r k / q), padded
+  // tensor-core (DMMA) form: KP x RP row-major, KP = roundup(H+1, 8), RP = roundup(H, 4)
+  int use_mma, KP, RP;
+  const double* Cm;    // [k][r-1] = cos(2 pi r k / q), k = 0..H (row 0 all ones)
+  const double* Sm;    // [k][r-1] = sin(2 pi r k / q)
 };
 
 struct PfaPlan {
@@ -51,6 +55,10 @@ struct PfaPlan {
   FDiv fq[3];
   FDiv fN;             // N = L - 1
   PfaStage st[3];
+  // index tables for the compile-time specialised kernels (tvd_pfa_t.cuh)
+  const unsigned* scat;     // t = 1..N: pos(c'_j of z_t) | pos(c'_{-j}) << 16
+  const unsigned* gath;     // k = 1..N: pos(C'_k)
+  const unsigned* reps[3];  // stage s, representative t: base | negated base << 16
 };
 
 // Device-resident FFT plan plus the per-length twiddle tables of one family.

@@ -47,11 +47,10 @@ __device__ __forceinline__ void rep_tuple(int t, const PfaStage& S, int& a, int&
   }
 }
 
-template <int KB>
-__device__ __forceinline__ void pfa_stage(double2* buf, int LP, int nl, const PfaStage& S) {
+// fold x_r, x_{q-r} -> a_r = x_r + x_{q-r}, b_r = x_r - x_{q-r} for every representative line
+__device__ __forceinline__ void pfa_fold(double2* buf, int LP, int nl, const PfaStage& S) {
   const int tid = threadIdx.x, nth = blockDim.x;
   const int q = S.q, H = S.H, st = S.st;
-  // fold x_r, x_{q-r} -> a_r, b_r for every representative line
   const int nfold = nl * S.Rcnt * H;
   for (int i = tid; i < nfold; i += nth) {
     const int rest = fdiv(i, S.fRcnt);
@@ -66,6 +65,125 @@ __device__ __forceinline__ void pfa_stage(double2* buf, int LP, int nl, const Pf
     p[(q - r) * st] = csub(x1, x2);
   }
   __syncthreads();
+}
+
+// DFT index (line-major over the CTA's representative lines) -> (base, negated base, self)
+__device__ __forceinline__ void dft_lines(int dft, const PfaStage& S, int LP, int& base, int& neg,
+                                          bool& self) {
+  const int line = fdiv(dft, S.fRcnt);
+  const int t = dft - line * S.Rcnt;
+  int a, b;
+  rep_tuple(t, S, a, b);
+  self = (t == 0);
+  base = line * LP + a * S.S1 + b * S.S2;
+  const int na = a == 0 ? 0 : S.D1 - a, nb = b == 0 ? 0 : S.D2 - b;
+  neg = line * LP + na * S.S1 + nb * S.S2;
+}
+
+// D(8x8) += A(8x4) * B(4x8), fp64 tensor-core MMA (SASS DMMA.884).
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int kMmaTiles = 8;  // output tiles a warp holds across the in-place barrier
+
+// One stage as a batched GEMM on the fp64 tensor cores:
+//   A_k = sum_r cos(2 pi r k / q) a_r   (row k = 0 of the cosine matrix is all ones -> V_0)
+//   B_k = sum_r sin(2 pi r k / q) b_r
+// The columns of the data operand are (DFT, re/im) pairs of the CTA's representative lines;
+// a warp tile covers 8 output rows k x 4 DFTs and keeps both accumulators, so every lane
+// finishes with A_k, B_k (re, im) of one (k, DFT) pair and forms V_k, V_{q-k} directly.
+__device__ __forceinline__ void pfa_dft_mma(double2* buf, int LP, int nl, const PfaStage& S) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int q = S.q, H = S.H, st = S.st;
+  const int ndft = nl * S.Rcnt;
+  const int nkt = S.KP >> 3, nct = (2 * ndft + 7) >> 3, nrs = S.RP >> 2;
+  int ctr = (nw * kMmaTiles) / nkt;  // column tiles per round (all k-tiles of a column together)
+  if (ctr < 1) ctr = 1;
+  const double* bufd = reinterpret_cast<const double*>(buf);
+  for (int ct0 = 0; ct0 < nct; ct0 += ctr) {
+    const int ntile = nkt * min(ctr, nct - ct0);
+    double2 vk[kMmaTiles], vm[kMmaTiles];
+    int ob[kMmaTiles], on[kMmaTiles], oflag[kMmaTiles];
+#pragma unroll
+    for (int s = 0; s < kMmaTiles; ++s) {
+      oflag[s] = 0;
+      const int tile = warp + s * nw;
+      if (tile < ntile) {  // warp-uniform
+        const int ct = ct0 + tile / nkt, kt = tile - (tile / nkt) * nkt;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        const int colB = ct * 8 + (lane >> 2);
+        const int dB = colB >> 1;
+        const bool vB = dB < ndft;
+        int baseB = 0, negB;
+        bool selfB;
+        if (vB) dft_lines(dB, S, LP, baseB, negB, selfB);
+        const double* pb = bufd + 2 * baseB + (colB & 1);
+        const int krow = kt * 8 + (lane >> 2);
+        const double* cm = S.Cm + krow * S.RP + (lane & 3);
+        const double* sm = S.Sm + krow * S.RP + (lane & 3);
+        for (int rs = 0; rs < nrs; ++rs) {
+          const int r = 1 + rs * 4 + (lane & 3);
+          double xa = 0.0, xb = 0.0;
+          if (vB && r <= H) {
+            xa = pb[2 * r * st];
+            xb = pb[2 * (q - r) * st];
+          }
+          dmma884(a0, a1, __ldg(cm + rs * 4), xa);
+          dmma884(b0, b1, __ldg(sm + rs * 4), xb);
+        }
+        const int dO = ct * 4 + (lane & 3);
+        if (krow <= H && dO < ndft) {
+          int base, neg;
+          bool self;
+          dft_lines(dO, S, LP, base, neg, self);
+          const double2 x0 = buf[base];
+          vk[s] = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
+          vm[s] = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
+          ob[s] = base;
+          on[s] = neg;
+          oflag[s] = 1 | (self ? 2 : 0);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < kMmaTiles; ++s) {
+      if (oflag[s]) {
+        const int tile = warp + s * nw;
+        const int kt = tile - (tile / nkt) * nkt;
+        const int k = kt * 8 + (lane >> 2);
+        double2* p = buf + ob[s];
+        double2* pn = buf + on[s];
+        const bool self = oflag[s] & 2;
+        if (k == 0) {
+          p[0] = vk[s];
+          if (!self) pn[0] = make_double2(-vk[s].x, -vk[s].y);
+        } else {
+          p[k * st] = vk[s];
+          p[(q - k) * st] = vm[s];
+          if (!self) {
+            pn[(q - k) * st] = make_double2(-vk[s].x, -vk[s].y);
+            pn[k * st] = make_double2(-vm[s].x, -vm[s].y);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int KB>
+__device__ __forceinline__ void pfa_stage(double2* buf, int LP, int nl, const PfaStage& S) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int q = S.q, H = S.H, st = S.st;
+  pfa_fold(buf, LP, nl, S);
+  if (S.use_mma) {
+    pfa_dft_mma(buf, LP, nl, S);
+    return;
+  }
   const int nch = S.nch;
   const int ndft = nl * S.Rcnt;
   const bool all_self = S.D1 * S.D2 == 1;  // prime L: the only line is odd
@@ -212,7 +330,7 @@ __device__ __forceinline__ void pfa_transform(double2* buf, int LP, int nl, cons
 constexpr int kPfaMaxV = 8;   // per-thread register values in the sandwich re-pack
 constexpr int kPfaBatch = 8;  // global loads in flight per thread in the pack
 
-__global__ void __launch_bounds__(256, 3) k_pfa(const PfaK p) {
+__global__ void __launch_bounds__(256, 2) k_pfa(const PfaK p) {
   const LineIO& io = p.io;
   if (io.skip && *io.skip) return;
   extern __shared__ double2 smem2[];
@@ -319,6 +437,165 @@ __global__ void __launch_bounds__(256, 3) k_pfa(const PfaK p) {
   }
 }
 
+// ------------------------------------------------ compile-time specialised kernel
+#include "tvd_pfa_t.cuh"
+
+constexpr int kPfaLinesT = 2;  // lines per CTA of the specialised kernel
+
+template <int Q1, int Q2, int Q3>
+__device__ __forceinline__ void pfa_transform_c(double2* buf, unsigned* const* reps,
+                                                const PfaPlan& pl) {
+  using SH = PfaShape<Q1, Q2, Q3>;
+  pfa_stage_c<PfaStageC<SH, 0>, kPfaLinesT>(buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
+  if constexpr (SH::d >= 2)
+    pfa_stage_c<PfaStageC<SH, 1>, kPfaLinesT>(buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
+  if constexpr (SH::d >= 3)
+    pfa_stage_c<PfaStageC<SH, 2>, kPfaLinesT>(buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
+}
+
+template <int Q1, int Q2, int Q3>
+__global__ void __launch_bounds__(256, 2) k_pfa_t(const PfaK p) {
+  using SH = PfaShape<Q1, Q2, Q3>;
+  constexpr int L = SH::L, N = SH::N, NL = kPfaLinesT;
+  const LineIO& io = p.io;
+  if (io.skip && *io.skip) return;
+  extern __shared__ double2 smem2[];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  double2* buf = smem2;
+  unsigned* scat = reinterpret_cast<unsigned*>(buf + NL * L);
+  unsigned* gath = scat + N;
+  unsigned* reps[3];
+  reps[0] = gath + N;
+  reps[1] = reps[0] + PfaStageC<SH, 0>::Rcnt;
+  reps[2] = reps[1] + (SH::d >= 2 ? PfaStageC<SH, 1>::Rcnt : 0);
+  const int line0 = blockIdx.x * NL;
+  const int nlv = min(NL, p.nlines - line0);
+  for (int i = tid; i < N; i += nth) {
+    scat[i] = p.pl.scat[i];
+    gath[i] = p.pl.gath[i];
+  }
+  for (int s = 0; s < SH::d; ++s) {
+    const int rc = s == 0 ? PfaStageC<SH, 0>::Rcnt : (s == 1 ? PfaStageC<SH, 1>::Rcnt
+                                                              : PfaStageC<SH, 2>::Rcnt);
+    for (int i = tid; i < rc; i += nth) reps[s][i] = p.pl.reps[s][i];
+  }
+  for (int i = tid; i < NL; i += nth) buf[i * L] = make_double2(0.0, 0.0);
+  for (int i = tid; i < (NL - nlv) * L; i += nth) buf[nlv * L + i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const bool contig = p.es == 1;
+  auto gidx = [&](int l, int t) { return (long)(line0 + l) * p.ls + (long)(p.off + t - 1) * p.es; };
+  auto put = [&](int l, int t, double v) {
+    const unsigned e = scat[t - 1];
+    double* b = reinterpret_cast<double*>(buf + l * L) + (t & 1);
+    b[2 * (e & 0xffffu)] = v;
+    b[2 * (e >> 16)] = -v;
+  };
+  auto get = [&](int l, int k) {
+    const double2 C = buf[l * L + gath[k - 1]];
+    return ((k & 1) ? -(C.y + C.x) : -(C.y - C.x)) * p.scale;
+  };
+  // pack: batched global loads, then the table-driven scatter
+  const int total = nlv * N;
+  for (int i0 = 0; i0 < total; i0 += kPfaBatch * nth) {
+    double v[kPfaBatch];
+    int lt[kPfaBatch];
+#pragma unroll
+    for (int s = 0; s < kPfaBatch; ++s) {
+      const int i = i0 + tid + s * nth;
+      lt[s] = -1;
+      if (i < total) {
+        int l, t;
+        if (contig) { l = i / N; t = 1 + i - l * N; }
+        else { t = 1 + i / nlv; l = i - (t - 1) * nlv; }
+        const long g = gidx(l, t);
+        double x = io.in[g];
+        if (io.pre) x = io.pre_mul ? x * io.pre[g] : x / io.pre[g];
+        v[s] = x;
+        lt[s] = l * 65536 + t;
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kPfaBatch; ++s)
+      if (lt[s] >= 0) put(lt[s] >> 16, lt[s] & 0xffff, v[s]);
+  }
+  __syncthreads();
+  pfa_transform_c<Q1, Q2, Q3>(buf, reps, p.pl);
+  if (io.mid_mul) {
+    for (int l = 0; l < nlv; ++l) {
+      double v[kPfaMaxV];
+#pragma unroll
+      for (int s = 0; s < kPfaMaxV; ++s) {
+        const int t = 1 + tid + s * nth;
+        v[s] = t <= N ? get(l, t) * io.mid_mul[gidx(l, t)] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < kPfaMaxV; ++s) {
+        const int t = 1 + tid + s * nth;
+        if (t <= N) put(l, t, v[s]);
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < NL; i += nth) buf[i * L] = make_double2(0.0, 0.0);
+    for (int i = tid; i < (NL - nlv) * L; i += nth) buf[nlv * L + i] = make_double2(0.0, 0.0);
+    __syncthreads();
+    pfa_transform_c<Q1, Q2, Q3>(buf, reps, p.pl);
+  }
+  double acc = 0.0;
+  auto store = [&](long g, double v) {
+    if (io.post) v = io.post_mul ? v * io.post[g] : v / io.post[g];
+    io.out[g] = v;
+    if (io.dot_with) acc += v * io.dot_with[g];
+  };
+  for (int i = tid; i < total; i += nth) {
+    int l, t;
+    if (contig) { l = i / N; t = 1 + i - l * N; }
+    else { t = 1 + i / nlv; l = i - (t - 1) * nlv; }
+    store(gidx(l, t), get(l, t));
+  }
+  if (p.off) {
+    for (int i = tid; i < 2 * nlv; i += nth) {
+      const int l = i >> 1;
+      const long g = (long)(line0 + l) * p.ls + (long)((i & 1) ? p.n - 1 : 0) * p.es;
+      double v = io.in[g];
+      if (io.pre) v = io.pre_mul ? v * io.pre[g] : v / io.pre[g];
+      if (io.mid_mul) v *= io.mid_mul[g];
+      store(g, v);
+    }
+  }
+  if (io.partial) {
+    const double s = block_sum(acc, red);
+    if (tid == 0) io.partial[blockIdx.x] = s;
+  }
+}
+
+template <int Q1, int Q2, int Q3>
+static cudaError_t launch_pfa_t(const PfaK& k, int nb, cudaStream_t st) {
+  using SH = PfaShape<Q1, Q2, Q3>;
+  int reps = PfaStageC<SH, 0>::Rcnt;
+  if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
+  if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
+  const size_t smem = (size_t)kPfaLinesT * SH::L * 16 + (2 * SH::N + reps) * sizeof(unsigned);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pfa_t<Q1, Q2, Q3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  k_pfa_t<Q1, Q2, Q3><<<nb, 256, smem, st>>>(k);
+  return cudaGetLastError();
+}
+
+// specialisations: the config lengths L = n - 1 of the Shat family (n = 128, 512, 1024, 2048)
+static bool pfa_specialised(const PfaPlan& P, int* which) {
+  auto is = [&](int a, int b, int c) {
+    return P.q[0] == a && (P.d >= 2 ? P.q[1] : 1) == b && (P.d >= 3 ? P.q[2] : 1) == c;
+  };
+  *which = is(89, 23, 1) ? 1 : is(31, 11, 3) ? 2 : is(73, 7, 1) ? 3 : is(127, 1, 1) ? 4 : 0;
+  return *which != 0 && P.scat != nullptr;
+}
+
 static int pfa_config(const PfaPlan& P, bool contiguous, int* nl, int* nth, size_t* smem) {
   const size_t line_bytes = (size_t)P.L * 16;
   int k = 2;
@@ -335,17 +612,23 @@ static int pfa_config(const PfaPlan& P, bool contiguous, int* nl, int* nth, size
 }
 
 int pfa_blocks(const PfaPlan& P, const LineGeom& g) {
-  int nl, nth;
+  int nl, nth, which;
   size_t smem;
+  if (pfa_specialised(P, &which)) return (g.nlines + kPfaLinesT - 1) / kPfaLinesT;
   if (pfa_config(P, g.es == 1, &nl, &nth, &smem)) return -1;
   return (g.nlines + nl - 1) / nl;
 }
 
 cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g, const LineIO& io,
                        int* nblocks_out, cudaStream_t st) {
-  int nl, nth;
+  int nl, nth, which = 0;
   size_t smem;
-  if (pfa_config(P, g.es == 1, &nl, &nth, &smem)) return cudaErrorInvalidConfiguration;
+  const bool spec = pfa_specialised(P, &which);
+  if (spec) {
+    nl = kPfaLinesT;
+  } else if (pfa_config(P, g.es == 1, &nl, &nth, &smem)) {
+    return cudaErrorInvalidConfiguration;
+  }
   PfaK k{};
   k.pl = P;
   k.n = len;
@@ -361,6 +644,13 @@ cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g,
   const int nb = (g.nlines + nl - 1) / nl;
   if (nblocks_out) *nblocks_out = nb;
   if (nb == 0) return cudaSuccess;
+  switch (which) {
+    case 1: return launch_pfa_t<89, 23, 1>(k, nb, st);
+    case 2: return launch_pfa_t<31, 11, 3>(k, nb, st);
+    case 3: return launch_pfa_t<73, 7, 1>(k, nb, st);
+    case 4: return launch_pfa_t<127, 1, 1>(k, nb, st);
+    default: break;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_pfa, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

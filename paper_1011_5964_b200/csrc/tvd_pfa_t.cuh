@@ -1,0 +1,207 @@
+// Compile-time specialised odd-symmetric PFA DST engine (included by tvd_pfa.cu).
+//
+// Same algorithm as the runtime kernel in tvd_pfa.cu, with the factorization
+// L = Q1 * Q2 * Q3 a template parameter: every stride, representative count,
+// modular map and loop bound is a constant, the small-DFT loops unroll, and
+// the data-independent index permutations (pack scatter, unpack gather,
+// representative line bases) come from tables staged in shared memory.
+#pragma once
+
+// (included inside namespace tvd, after dmma884 / kMmaTiles)
+
+constexpr int c_modinv(int a, int m) {
+  int r = 1;
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) r = x;
+  return r;
+}
+
+template <int Q1, int Q2, int Q3>
+struct PfaShape {
+  static constexpr int L = Q1 * Q2 * Q3;
+  static constexpr int d = (Q1 > 1) + (Q2 > 1) + (Q3 > 1);
+  static constexpr int q[3] = {Q1, Q2, Q3};
+  static constexpr int stride[3] = {Q2 * Q3, Q3, 1};
+  static constexpr int h = (L - 1) / 2;
+  static constexpr int N = L - 1;
+};
+
+// Stage along dimension S of the shape.
+template <class SH, int S>
+struct PfaStageC {
+  static constexpr int q = SH::q[S];
+  static constexpr int H = (q - 1) / 2;
+  static constexpr int st = SH::stride[S];
+  // other dims in order; D1 = 1 when only one other dim
+  static constexpr int o0 = S == 0 ? 1 : 0;
+  static constexpr int o1 = S == 2 ? 1 : 2;
+  static constexpr int D1 = SH::d == 3 ? SH::q[o0] : 1;
+  static constexpr int S1 = SH::d == 3 ? SH::stride[o0] : 0;
+  static constexpr int D2 = SH::d == 3 ? SH::q[o1] : (SH::d == 2 ? SH::q[o0] : 1);
+  static constexpr int S2 = SH::d == 3 ? SH::stride[o1] : (SH::d == 2 ? SH::stride[o0] : 0);
+  static constexpr int Rcnt = (D1 * D2 + 1) / 2;
+  static constexpr int h2 = (D2 + 1) / 2;
+  static constexpr int KP = (H + 1 + 7) / 8 * 8;
+  static constexpr int RP = (H + 3) / 4 * 4;
+  static constexpr bool mma = H >= 8;
+  static constexpr int LPc = SH::L;
+};
+
+template <class ST>
+__device__ __forceinline__ void rep_ab(int t, int& a, int& b) {
+  if (t < ST::h2) {
+    a = 0;
+    b = t;
+  } else {
+    const int u = t - ST::h2;
+    a = 1 + u / ST::D2;
+    b = u - (a - 1) * ST::D2;
+  }
+}
+
+// fold + DFT of one stage.  `reps` holds (base | neg << 16) of every representative line
+// (line 0); line l adds l * LP.
+template <class ST, int NL>
+__device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
+                                            const double* Cm, const double* Sm) {
+  constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LPc;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  // fold
+  constexpr int nfold = NL * ST::Rcnt * H;
+  for (int i = tid; i < nfold; i += nth) {
+    const int t = i % ST::Rcnt;
+    const int rest = i / ST::Rcnt;
+    const int line = rest / H;
+    const int r = 1 + rest - line * H;
+    double2* p = buf + line * LP + (reps[t] & 0xffffu);
+    const double2 x1 = p[r * st], x2 = p[(q - r) * st];
+    p[r * st] = cadd(x1, x2);
+    p[(q - r) * st] = csub(x1, x2);
+  }
+  __syncthreads();
+  constexpr int ndft = NL * ST::Rcnt;
+  if constexpr (ST::mma) {
+    const int lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
+    constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;
+    const int ctr = max(1, (nw * kMmaTiles) / nkt);
+    const double* bufd = reinterpret_cast<const double*>(buf);
+    for (int ct0 = 0; ct0 < nct; ct0 += ctr) {
+      const int ntile = nkt * min(ctr, nct - ct0);
+      double2 vk[kMmaTiles], vm[kMmaTiles];
+      unsigned ob[kMmaTiles];
+      int oflag[kMmaTiles];
+#pragma unroll
+      for (int s = 0; s < kMmaTiles; ++s) {
+        oflag[s] = 0;
+        const int tile = warp + s * nw;
+        if (tile < ntile) {
+          const int ct = ct0 + tile / nkt, kt = tile - (tile / nkt) * nkt;
+          double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+          const int colB = ct * 8 + (lane >> 2);
+          const int dB = colB >> 1;
+          const bool vB = dB < ndft;
+          const int lB = vB ? dB / ST::Rcnt : 0;
+          const int tB = vB ? dB - lB * ST::Rcnt : 0;
+          const double* pb = bufd + 2 * (lB * LP + (reps[tB] & 0xffffu)) + (colB & 1);
+          const int krow = kt * 8 + (lane >> 2);
+          const double* cm = Cm + krow * ST::RP + (lane & 3);
+          const double* sm = Sm + krow * ST::RP + (lane & 3);
+#pragma unroll
+          for (int rs = 0; rs < nrs; ++rs) {
+            const int r = 1 + rs * 4 + (lane & 3);
+            double xa = 0.0, xb = 0.0;
+            if (vB && (rs * 4 + 4 <= H || r <= H)) {
+              xa = pb[2 * r * st];
+              xb = pb[2 * (q - r) * st];
+            }
+            dmma884(a0, a1, cm[rs * 4], xa);
+            dmma884(b0, b1, sm[rs * 4], xb);
+          }
+          const int dO = ct * 4 + (lane & 3);
+          if (krow <= H && dO < ndft) {
+            const int lO = dO / ST::Rcnt, tO = dO - lO * ST::Rcnt;
+            const unsigned rp = reps[tO] + (unsigned)(lO * LP) * 0x10001u;
+            const double2 x0 = buf[rp & 0xffffu];
+            vk[s] = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
+            vm[s] = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
+            ob[s] = rp;
+            oflag[s] = 1 | (tO == 0 ? 2 : 0);
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < kMmaTiles; ++s) {
+        if (oflag[s]) {
+          const int tile = warp + s * nw;
+          const int k = (tile - (tile / nkt) * nkt) * 8 + (lane >> 2);
+          double2* p = buf + (ob[s] & 0xffffu);
+          double2* pn = buf + (ob[s] >> 16);
+          const bool self = oflag[s] & 2;
+          if (k == 0) {
+            p[0] = vk[s];
+            if (!self) pn[0] = make_double2(-vk[s].x, -vk[s].y);
+          } else {
+            p[k * st] = vk[s];
+            p[(q - k) * st] = vm[s];
+            if (!self) {
+              pn[(q - k) * st] = make_double2(-vk[s].x, -vk[s].y);
+              pn[k * st] = make_double2(-vm[s].x, -vm[s].y);
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    // small radix: one thread per representative DFT, fully unrolled in registers
+    for (int d0 = 0; d0 < ndft; d0 += nth) {
+      const int dft = d0 + tid;
+      const bool act = dft < ndft;
+      double2 v[q];
+      unsigned rp = 0;
+      bool self = false;
+      if (act) {
+        const int l = dft / ST::Rcnt, t = dft - l * ST::Rcnt;
+        rp = reps[t] + (unsigned)(l * LP) * 0x10001u;
+        self = t == 0;
+        const double2* p = buf + (rp & 0xffffu);
+        const double2 x0 = p[0];
+        double2 A[H + 1], B[H + 1];
+#pragma unroll
+        for (int r = 1; r <= H; ++r) {
+          A[r] = p[r * st];
+          B[r] = p[(q - r) * st];
+        }
+        double2 s0 = x0;
+#pragma unroll
+        for (int r = 1; r <= H; ++r) s0 = cadd(s0, A[r]);
+        v[0] = s0;
+#pragma unroll
+        for (int k = 1; k <= H; ++k) {
+          double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int r = 1; r <= H; ++r) {
+            const double c = Cm[k * ST::RP + r - 1], sn = Sm[k * ST::RP + r - 1];
+            a.x += A[r].x * c; a.y += A[r].y * c;
+            b.x += B[r].x * sn; b.y += B[r].y * sn;
+          }
+          v[k] = make_double2(x0.x + a.x + b.y, x0.y + a.y - b.x);
+          v[q - k] = make_double2(x0.x + a.x - b.y, x0.y + a.y + b.x);
+        }
+      }
+      __syncthreads();
+      if (act) {
+        double2* p = buf + (rp & 0xffffu);
+        double2* pn = buf + (rp >> 16);
+#pragma unroll
+        for (int k = 0; k < q; ++k) {
+          p[k * st] = v[k];
+          if (!self) pn[((q - k) % q) * st] = make_double2(-v[k].x, -v[k].y);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+

@@ -105,11 +105,329 @@ __global__ void __launch_bounds__(256) k_band_cols(BandOp op, const double* __re
   }
 }
 
+// ------------------------------------------ register sliding-window band passes
+// One lane per row (row pass) or column (column pass) of a 32-wide tile; each
+// lane produces kSlideR consecutive outputs along the band direction from a
+// register sliding window: every loaded value feeds up to kSlideR FMAs whose
+// taps are compile-time indices into the kernel-parameter tap array (constant
+// bank operands), so the inner loop is DFMA + one conflict-free LDS per input.
+// Output positions within op.B of either end use the border table (warp-uniform).
+constexpr int kSlideR = 8;    // outputs per lane per chunk (bounded unrolled code size)
+constexpr int kSlideW = 4;    // warps per CTA
+constexpr int kSlideSpan = 32;  // outputs per warp along the band direction
+
+struct SlideTaps {
+  double t[64];  // t[k] = symmetric tap at offset +-k
+};
+
+// Asynchronous 8-byte global -> shared copy (LDGSTS); zero-fills when !valid.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::);
+}
+
+template <int W>
+__device__ __forceinline__ void slide_chunk(const double* __restrict__ x, long stride,
+                                            const SlideTaps& tp, double (&acc)[kSlideR]) {
+#pragma unroll
+  for (int r = 0; r < kSlideR; ++r) acc[r] = 0.0;
+#pragma unroll
+  for (int m = 0; m < kSlideR + 2 * W; ++m) {
+    const double xm = x[m * stride];
+#pragma unroll
+    for (int r = 0; r < kSlideR; ++r) {
+      const int k = m - W - r;
+      if (k >= -W && k <= W) acc[r] += tp.t[k < 0 ? -k : k] * xm;
+    }
+  }
+}
+
+// Output at a border position j from the band table (independent partial sums, unrolled).
+template <int W>
+__device__ __forceinline__ double border_out(const BandOp& op, int j, const double* x, long stride) {
+  const double* __restrict__ trow = op.table + (long)j * (2 * W + 1);
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < 2 * W + 1; ++k) a[k & 3] += __ldg(&trow[k]) * x[k * stride];
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Persistent double-buffered mode (grid = kSMs * kSlideCtasPerSm, next tile prefetched with
+// cp.async) halves the resident warps at W = 30 and measured slower on B200 than one tile per
+// CTA with a single buffer, so it is off: kSlidePersistent = false launches one CTA per tile.
+constexpr bool kSlidePersistent = false;
+constexpr int kSlideCtasPerSm = 2;
+constexpr int kSlideBuffers = kSlidePersistent ? 2 : 1;
+
+// Row pass: persistent CTAs walk tiles of 32 rows x (kSlideW * kSlideSpan) columns; lane = row.
+// The next tile streams in with cp.async while the current one is convolved.
+template <int W>
+__device__ __forceinline__ void slide_rows_load(double* buf, const double* __restrict__ in, int n,
+                                                int tile, int tcols) {
+  constexpr int TC = kSlideW * kSlideSpan, WIDTH = TC + 2 * W, P = WIDTH | 1;
+  const int i0 = (tile / tcols) * 32, j0 = (tile % tcols) * TC;
+  for (int e = threadIdx.x; e < 32 * WIDTH; e += blockDim.x) {
+    const int r = e / WIDTH, c = e - r * WIDTH;
+    const int row = i0 + r, col = j0 - W + c;
+    const bool ok = row < n && col >= 0 && col < n;
+    cp_async8(buf + r * P + c, ok ? in + (long)row * n + col : in, ok);
+  }
+  cp_async_commit();
+}
+
+template <int W>
+__global__ void __launch_bounds__(kSlideW * 32) k_slide_rows(BandOp op, const SlideTaps tp,
+                                                            const double* __restrict__ in,
+                                                            double* __restrict__ out,
+                                                            const int* skip) {
+  if (skip && *skip) return;
+  constexpr int TC = kSlideW * kSlideSpan, WIDTH = TC + 2 * W, P = WIDTH | 1;
+  extern __shared__ double smd[];
+  const int n = op.n;
+  const int tcols = (n + TC - 1) / TC, ntiles = tcols * ((n + 31) / 32);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int k = 0;
+  if ((int)blockIdx.x < ntiles) slide_rows_load<W>(smd, in, n, blockIdx.x, tcols);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    double* sm = smd + (k & 1) * 32 * P;
+    const int next = tile + gridDim.x;
+    if (next < ntiles) {
+      slide_rows_load<W>(smd + ((k + 1) & 1) * 32 * P, in, n, next, tcols);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int i0 = (tile / tcols) * 32, j0 = (tile % tcols) * TC;
+  double res[kSlideSpan];
+#pragma unroll
+  for (int r = 0; r < kSlideSpan; ++r) res[r] = 0.0;
+#pragma unroll 1
+  for (int ch = 0; ch < kSlideSpan / kSlideR; ++ch) {
+    const int jc = warp * kSlideSpan + ch * kSlideR;  // tile-local first output column
+    const int jg = j0 + jc;
+    const double* xr = sm + lane * P + jc;             // x of output jc sits at xr[W]
+    double acc[kSlideR];
+    slide_chunk<W>(xr, 1, tp, acc);
+    if (!(jg >= op.B && jg + kSlideR <= n - op.B)) {
+      for (int r = 0; r < kSlideR; ++r) {
+        const int j = jg + r;
+        if (j < n && (j < op.B || j >= n - op.B)) acc[r] = border_out<W>(op, j, xr + r, 1);
+      }
+    }
+    // park the chunk in the result registers (static indices: select by ch)
+#pragma unroll
+    for (int c = 0; c < kSlideSpan / kSlideR; ++c)
+      if (c == ch) {
+#pragma unroll
+        for (int r = 0; r < kSlideR; ++r) res[c * kSlideR + r] = acc[r];
+      }
+  }
+  __syncthreads();  // tile reused for the transposed write-back
+#pragma unroll
+  for (int r = 0; r < kSlideSpan; ++r) sm[lane * P + warp * kSlideSpan + r] = res[r];
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * TC; e += blockDim.x) {
+    const int r = e / TC, c = e - r * TC;
+    const int row = i0 + r, col = j0 + c;
+    if (row < n && col < n) out[(long)row * n + col] = sm[r * P + c];
+  }
+  __syncthreads();  // buffer free for the prefetch two tiles ahead
+  }
+}
+
+// Column pass: tile = (kSlideW * kSlideSpan) rows x 32 columns; lane = column.
+template <int W>
+__global__ void __launch_bounds__(kSlideW * 32) k_slide_cols(BandOp op, const SlideTaps tp,
+                                                            const double* __restrict__ in,
+                                                            double* __restrict__ out,
+                                                            Epilogue ep, const int* skip) {
+  if (skip && *skip) return;
+  constexpr int TR = kSlideW * kSlideSpan, HEIGHT = TR + 2 * W;
+  extern __shared__ double smd[];
+  __shared__ double red[32];
+  const int n = op.n;
+  const int tcols = (n + 31) / 32, ntiles = tcols * ((n + TR - 1) / TR);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto load = [&](double* buf, int tile) {
+    const int i0 = (tile / tcols) * TR, j0 = (tile % tcols) * 32;
+    for (int r = warp; r < HEIGHT; r += kSlideW) {
+      const int row = i0 - W + r, col = j0 + lane;
+      const bool ok = row >= 0 && row < n && col < n;
+      cp_async8(buf + r * 32 + lane, ok ? in + (long)row * n + col : in, ok);
+    }
+    cp_async_commit();
+  };
+  double dot = 0.0;
+  const double* __restrict__ a_h = ep.a_h;
+  const double* __restrict__ a_v = ep.a_v;
+  const double* __restrict__ lw = ep.lw;
+  const double* __restrict__ sv = ep.s;
+  const double* __restrict__ dw = ep.dot_with;
+  int k = 0;
+  if ((int)blockIdx.x < ntiles) load(smd, blockIdx.x);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    double* sm = smd + (k & 1) * HEIGHT * 32;
+    const int next = tile + gridDim.x;
+    if (next < ntiles) {
+      load(smd + ((k + 1) & 1) * HEIGHT * 32, next);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int i0 = (tile / tcols) * TR, j0 = (tile % tcols) * 32;
+    const int col = j0 + lane;
+#pragma unroll 1
+  for (int ch = 0; ch < kSlideSpan / kSlideR; ++ch) {
+    const int ic = warp * kSlideSpan + ch * kSlideR;
+    const int ig = i0 + ic;
+    const double* xc = sm + ic * 32 + lane;
+    double acc[kSlideR];
+    slide_chunk<W>(xc, 32, tp, acc);
+    if (!(ig >= op.B && ig + kSlideR <= n - op.B)) {
+      for (int r = 0; r < kSlideR; ++r) {
+        const int i = ig + r;
+        if (i < n && (i < op.B || i >= n - op.B)) acc[r] = border_out<W>(op, i, xc + r * 32, 32);
+      }
+    }
+    if (col < n) {
+      // all epilogue loads first (no store in between), then the stores
+      double v[kSlideR], dwv[kSlideR];
+#pragma unroll
+      for (int r = 0; r < kSlideR; ++r) {
+        const int i = min(ig + r, n - 1);
+        const long g = (long)i * n + col;
+        double x = acc[r];
+        if (a_h) x = x + ep.alpha * diffusion_at(a_h, a_v, lw, n, i, col, ep.inv_h2);
+        if (sv) x = sv[g] * x;
+        v[r] = x;
+        dwv[r] = dw ? dw[g] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < kSlideR; ++r) {
+        const int i = ig + r;
+        if (i < n) {
+          out[(long)i * n + col] = v[r];
+          dot += dwv[r] * v[r];
+        }
+      }
+    }
+  }
+  __syncthreads();  // buffer free for the prefetch two tiles ahead
+  }
+  if (ep.partial) {
+    const double s = block_sum(dot, red);
+    if (threadIdx.x == 0) ep.partial[blockIdx.x] = s;
+  }
+}
+
+static bool slide_taps(const BandOp& op, SlideTaps* tp) {
+  if (op.w > 63) return false;
+  for (int k = 0; k <= op.w; ++k) tp->t[k] = op.taps_host[op.w + k];
+  return op.taps_host != nullptr;
+}
+
+#define TVD_SLIDE_WIDTHS(X) X(4) X(5) X(7) X(8) X(10) X(14) X(15) X(20) X(30) X(31) X(62)
+
+static cudaError_t launch_slide_rows(const BandOp& op, const double* in, double* out,
+                                     const int* skip, cudaStream_t st, bool* done) {
+  SlideTaps tp;
+  *done = false;
+  if (!slide_taps(op, &tp)) return cudaSuccess;
+  const int n = op.n;
+  constexpr int TC = kSlideW * kSlideSpan;
+  const int ntiles = ((n + TC - 1) / TC) * ((n + 31) / 32);
+  const int grid = (kSlidePersistent && ntiles > kSMs * kSlideCtasPerSm) ? kSMs * kSlideCtasPerSm
+                                                                          : ntiles;
+  switch (op.w) {
+#define X(WW)                                                                              \
+  case WW: {                                                                               \
+    const size_t smem = kSlideBuffers * 32 * ((TC + 2 * WW) | 1) * sizeof(double);         \
+    static bool attr = false;                                                              \
+    if (!attr) {                                                                           \
+      cudaFuncSetAttribute(k_slide_rows<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                           160 * 1024);                                                    \
+      attr = true;                                                                         \
+    }                                                                                      \
+    k_slide_rows<WW><<<grid, kSlideW * 32, smem, st>>>(op, tp, in, out, skip);             \
+    *done = true;                                                                          \
+    return cudaGetLastError();                                                             \
+  }
+    TVD_SLIDE_WIDTHS(X)
+#undef X
+    default: return cudaSuccess;
+  }
+}
+
+static cudaError_t launch_slide_cols(const BandOp& op, const double* in, double* out,
+                                     const Epilogue& ep, const int* skip, cudaStream_t st,
+                                     bool* done) {
+  SlideTaps tp;
+  *done = false;
+  if (!slide_taps(op, &tp)) return cudaSuccess;
+  const int grid = band_cols_grid(op);
+  constexpr int TR = kSlideW * kSlideSpan;
+  switch (op.w) {
+#define X(WW)                                                                              \
+  case WW: {                                                                               \
+    const size_t smem = kSlideBuffers * (TR + 2 * WW) * 32 * sizeof(double);               \
+    static bool attr = false;                                                              \
+    if (!attr) {                                                                           \
+      cudaFuncSetAttribute(k_slide_cols<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                           160 * 1024);                                                    \
+      attr = true;                                                                         \
+    }                                                                                      \
+    k_slide_cols<WW><<<grid, kSlideW * 32, smem, st>>>(op, tp, in, out, ep, skip);         \
+    *done = true;                                                                          \
+    return cudaGetLastError();                                                             \
+  }
+    TVD_SLIDE_WIDTHS(X)
+#undef X
+    default: return cudaSuccess;
+  }
+}
+
 int band_rows_blocks(int n) { return ((n + kRowTileC - 1) / kRowTileC) * ((n + kRowTileR - 1) / kRowTileR); }
-int band_cols_blocks(int n) { return ((n + kColTileC - 1) / kColTileC) * ((n + kColTileR - 1) / kColTileR); }
+
+int band_cols_grid(const BandOp& op) {
+  const int n = op.n;
+  bool slide = false;
+  if (op.taps_host && op.w <= 63) {
+    switch (op.w) {
+#define X(WW) case WW: slide = true; break;
+      TVD_SLIDE_WIDTHS(X)
+#undef X
+      default: break;
+    }
+  }
+  if (slide) {
+    const int ntiles = ((n + 31) / 32) * ((n + kSlideW * kSlideSpan - 1) / (kSlideW * kSlideSpan));
+    return (kSlidePersistent && ntiles > kSMs * kSlideCtasPerSm) ? kSMs * kSlideCtasPerSm : ntiles;
+  }
+  return ((n + kColTileC - 1) / kColTileC) * ((n + kColTileR - 1) / kColTileR);
+}
+int band_cols_blocks(int n) {
+  const int a = ((n + kColTileC - 1) / kColTileC) * ((n + kColTileR - 1) / kColTileR);
+  const int b = ((n + 31) / 32) * ((n + kSlideW * kSlideSpan - 1) / (kSlideW * kSlideSpan));
+  return a > b ? a : b;
+}
 
 cudaError_t launch_band_rows(const BandOp& op, const double* in, double* out, const int* skip,
                              cudaStream_t st) {
+  bool done;
+  cudaError_t e = launch_slide_rows(op, in, out, skip, st, &done);
+  if (done || e != cudaSuccess) return e;
   const int n = op.n;
   dim3 grid((n + kRowTileC - 1) / kRowTileC, (n + kRowTileR - 1) / kRowTileR);
   const size_t smem = (size_t)(2 * op.w + 1 + kRowTileR * (kRowTileC + 2 * op.w)) * sizeof(double);
@@ -124,6 +442,9 @@ cudaError_t launch_band_rows(const BandOp& op, const double* in, double* out, co
 
 cudaError_t launch_band_cols(const BandOp& op, const double* in, double* out, const Epilogue& ep,
                              const int* skip, cudaStream_t st) {
+  bool done;
+  cudaError_t e = launch_slide_cols(op, in, out, ep, skip, st, &done);
+  if (done || e != cudaSuccess) return e;
   const int n = op.n;
   dim3 grid((n + kColTileC - 1) / kColTileC, (n + kColTileR - 1) / kColTileR);
   const size_t smem = (size_t)(2 * op.w + 1 + kColTileC * (kColTileR + 2 * op.w)) * sizeof(double);

@@ -9,8 +9,9 @@ namespace tvd {
 // [B, n - B) are Toeplitz with the symmetric `taps`; the others read `table`.
 struct BandOp {
   int n, w, B;
-  const double* taps;   // 2w+1 (device)
-  const double* table;  // n x (2w+1), table[i*(2w+1) + k + w] = B[i][i+k] (device)
+  const double* taps;       // 2w+1 (device)
+  const double* table;      // n x (2w+1), table[i*(2w+1) + k + w] = B[i][i+k] (device)
+  const double* taps_host;  // 2w+1 (host copy; becomes kernel-parameter constants)
 };
 
 // Epilogue of the normal-equation column pass:
@@ -46,7 +47,8 @@ __device__ __forceinline__ double diffusion_at(const double* __restrict__ a_h,
 }
 
 int band_rows_blocks(int n);
-int band_cols_blocks(int n);
+int band_cols_blocks(int n);          // upper bound over both column-pass variants
+int band_cols_grid(const BandOp& op);  // exact grid of launch_band_cols for this operator
 cudaError_t launch_band_rows(const BandOp& op, const double* in, double* out, const int* skip,
                              cudaStream_t st);
 cudaError_t launch_band_cols(const BandOp& op, const double* in, double* out, const Epilogue& ep,
