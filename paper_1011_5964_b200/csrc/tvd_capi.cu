@@ -53,6 +53,8 @@ enum Slot : int {
   kSlotBlockS,
   kSlotPartial,
   kSlotPartial2,
+  kSlotTmp3,
+  kSlotInvT,
   kSlotCount
 };
 
@@ -474,11 +476,66 @@ static int partial_capacity(tvd_ctx* c, size_t count, double** out) {
 }
 
 // z = X (inv .* X^T (r / d)) / d  with optional r.z partials.  Returns #partials.
+// Does the persistent TMA-pipelined DST engine handle this family / size?
+static bool pipe_ok(tvd_ctx* c, int family, int n, const TrigPlan** P) {
+  if (c->force_generic || (family != kFamSineHat && family != kFamDst1) || (n & 1)) return false;
+  if (get_plan(c, family, n, P)) return false;
+  return (*P)->pfa_ok && pipe_grid((*P)->pfa, n) > 0;
+}
+
+// z = X (inv .* X^T (r / d)) / d for the DST families through three contiguous-row passes:
+// rows -> t^T (transposed write), rows of t^T with inv^T -> t' (transposed back), rows -> z.
+static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const double* inv,
+                        const double* inv_t, const double* d, int dmul, const double* in,
+                        double* out, const double* dot_with, const int* skip, int* nb_out) {
+  double *tT, *t2, *partial = nullptr;
+  TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tT);
+  TVD_SLOT(c, kSlotTmp3, (size_t)n * n, t2);
+  if (!inv_t) {
+    double* it;
+    TVD_SLOT(c, kSlotInvT, (size_t)n * n, it);
+    TVD_LAUNCH(c, kCatVec, 1, launch_transpose(inv, it, n, c->stream));
+    inv_t = it;
+  }
+  if (dot_with) {
+    int rc = partial_capacity(c, (size_t)n + 64, &partial);
+    if (rc) return rc;
+  }
+  LineIO a{};
+  a.in = in;
+  a.out = tT;
+  a.pre = d;
+  a.pre_mul = dmul;
+  a.skip = skip;
+  int nb;
+  TVD_LAUNCH(c, kCatTrigRows, 1, launch_pipe(P->pfa, family, n, n, 1, a, &nb, c->stream));
+  LineIO b{};
+  b.in = tT;
+  b.out = t2;
+  b.mid_mul = inv_t;
+  b.skip = skip;
+  TVD_LAUNCH(c, kCatTrigCols, 1, launch_pipe(P->pfa, family, n, n, 1, b, &nb, c->stream));
+  LineIO z{};
+  z.in = t2;
+  z.out = out;
+  z.post = d;
+  z.post_mul = dmul;
+  z.dot_with = dot_with;
+  z.partial = partial;
+  z.skip = skip;
+  TVD_LAUNCH(c, kCatTrigRows, 1, launch_pipe(P->pfa, family, n, n, 0, z, &nb, c->stream));
+  if (nb_out) *nb_out = nb;
+  return TVD_OK;
+}
+
 static int precond_transform(tvd_ctx* c, int family, int n, const double* inv, const double* d,
                              int dmul, const double* in, double* out, const double* dot_with,
-                             const int* skip, int* nb_out) {
+                             const int* skip, int* nb_out, const double* inv_t = nullptr) {
   if (family != kFamSineHat && family != kFamDct && family != kFamDst1)
     return fail(TVD_ERR_INVALID, "unknown transform family");
+  const TrigPlan* PP;
+  if (pipe_ok(c, family, n, &PP))
+    return precond_pipe(c, PP, family, n, inv, inv_t, d, dmul, in, out, dot_with, skip, nb_out);
   double* tmp;
   TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tmp);
   double* partial = nullptr;
@@ -1102,7 +1159,8 @@ int tvd_system_apply(tvd_ctx* c, const tvd_system* sys, const double* in, double
 
 // z = M^{-1} r with r.z partials; z may alias r for kind NONE.
 static int minv_internal(tvd_ctx* c, const tvd_precond* pre, int n, const double* r, double* z,
-                         double* partial, const int* skip, int* nb) {
+                         double* partial, const int* skip, int* nb,
+                         const double* inv_t = nullptr) {
   const long N = (long)n * n;
   if (!pre || pre->kind == TVD_PRECOND_NONE) {
     if (z != r) TVD_LAUNCH(c, kCatVec, 1, launch_copy(r, z, N, skip, c->stream));
@@ -1116,7 +1174,8 @@ static int minv_internal(tvd_ctx* c, const tvd_precond* pre, int n, const double
     return TVD_OK;
   }
   if (pre->kind == TVD_PRECOND_TRANSFORM)
-    return precond_transform(c, pre->family, n, pre->inv_eig, pre->d, 0, r, z, r, skip, nb);
+    return precond_transform(c, pre->family, n, pre->inv_eig, pre->d, 0, r, z, r, skip, nb,
+                             inv_t);
   return fail(TVD_ERR_INVALID, "unknown preconditioner kind");
 }
 
@@ -1155,8 +1214,19 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   if (rc) return rc;
   TVD_LAUNCH(c, kCatVec, 1, launch_residual_init(b, q, r, N, partial, vec_blocks(), st));
   TVD_LAUNCH(c, kCatFin, 1, launch_pcg_start(S, partial, vec_blocks(), st));
+  // inverse eigenvalues transposed once per solve for the contiguous-row DST engine
+  const double* inv_t = nullptr;
+  if (pre && pre->kind == TVD_PRECOND_TRANSFORM) {
+    const TrigPlan* PP;
+    if (pipe_ok(c, pre->family, n, &PP)) {
+      double* it;
+      TVD_SLOT(c, kSlotInvT, N, it);
+      TVD_LAUNCH(c, kCatVec, 1, launch_transpose(pre->inv_eig, it, n, st));
+      inv_t = it;
+    }
+  }
   // z = M^-1 r ; p = z ; rz = r.z
-  rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb);
+  rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb, inv_t);
   if (rc) return rc;
   TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rz0(S, partial, nb, st));
   TVD_LAUNCH(c, kCatVec, 1, launch_copy(zz, p, N, skip, st));
@@ -1168,7 +1238,7 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
       TVD_LAUNCH(c, kCatFin, 1, launch_pcg_gamma(S, partial, nb, st));
       TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, p, q, N, partial, vec_blocks(), st));
       TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
-      rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb);
+      rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb, inv_t);
       if (rc) return rc;
       TVD_LAUNCH(c, kCatFin, 1, launch_pcg_beta(S, partial, nb, max_iterations, st));
       TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_p(S, p, zz, N, st));

@@ -116,5 +116,12 @@ int trig_blocks(const TrigPlan& P, const LineGeom& g);
 cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g, const LineIO& io,
                        int* nblocks_out, cudaStream_t st);
 int pfa_blocks(const PfaPlan& P, const LineGeom& g);
+// persistent TMA-pipelined row pass over an nlines x len row-major array (even len, PFA
+// specialised shapes); transposed != 0 writes the result transposed (len x nlines)
+cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int transposed,
+                        const LineIO& io, int* nblocks_out, cudaStream_t st);
+int pipe_grid(const PfaPlan& P, int nlines);
+// out = in^T for an n x n fp64 array (tvd_stencil.cu)
+cudaError_t launch_transpose(const double* in, double* out, int n, cudaStream_t st);
 
 }  // namespace tvd

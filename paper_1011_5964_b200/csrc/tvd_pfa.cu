@@ -16,6 +16,8 @@
 // KB output pairs per work item from a (cos, sin) matrix laid out so the KB
 // coefficients of one r are contiguous (immediate-offset loads).
 // Reference semantics: transforms.py:52-81 (dst1_apply / sinehat_apply).
+#include <cstdlib>
+
 #include "tvd_internal.h"
 
 namespace tvd {
@@ -28,6 +30,7 @@ __device__ __forceinline__ int fmodq(int x, const FDiv& f) { return x - fdiv(x, 
 struct PfaK {
   PfaPlan pl;
   int n, off, N, nl, nlines;
+  int stages;  // number of PFA stages to run (profiling knob; default = all)
   long ls, es;
   double scale;  // 0.5 * sqrt(2 / L)
   int h;         // (L - 1) / 2
@@ -444,13 +447,16 @@ constexpr int kPfaLinesT = 2;  // lines per CTA of the specialised kernel
 
 template <int Q1, int Q2, int Q3>
 __device__ __forceinline__ void pfa_transform_c(double2* buf, unsigned* const* reps,
-                                                const PfaPlan& pl) {
+                                                const PfaPlan& pl, int stages) {
   using SH = PfaShape<Q1, Q2, Q3>;
-  pfa_stage_c<PfaStageC<SH, 0>, kPfaLinesT>(buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
+  if (stages >= 1)
+    pfa_stage_c<PfaStageC<SH, 0>, kPfaLinesT, 4, 8>(buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
   if constexpr (SH::d >= 2)
-    pfa_stage_c<PfaStageC<SH, 1>, kPfaLinesT>(buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
+    if (stages >= 2)
+      pfa_stage_c<PfaStageC<SH, 1>, kPfaLinesT, 4, 8>(buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
   if constexpr (SH::d >= 3)
-    pfa_stage_c<PfaStageC<SH, 2>, kPfaLinesT>(buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
+    if (stages >= 3)
+      pfa_stage_c<PfaStageC<SH, 2>, kPfaLinesT, 4, 8>(buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
 }
 
 template <int Q1, int Q2, int Q3>
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(256, 2) k_pfa_t(const PfaK p) {
       if (lt[s] >= 0) put(lt[s] >> 16, lt[s] & 0xffff, v[s]);
   }
   __syncthreads();
-  pfa_transform_c<Q1, Q2, Q3>(buf, reps, p.pl);
+  pfa_transform_c<Q1, Q2, Q3>(buf, reps, p.pl, p.stages);
   if (io.mid_mul) {
     for (int l = 0; l < nlv; ++l) {
       double v[kPfaMaxV];
@@ -540,7 +546,7 @@ __global__ void __launch_bounds__(256, 2) k_pfa_t(const PfaK p) {
     for (int i = tid; i < NL; i += nth) buf[i * L] = make_double2(0.0, 0.0);
     for (int i = tid; i < (NL - nlv) * L; i += nth) buf[nlv * L + i] = make_double2(0.0, 0.0);
     __syncthreads();
-    pfa_transform_c<Q1, Q2, Q3>(buf, reps, p.pl);
+    pfa_transform_c<Q1, Q2, Q3>(buf, reps, p.pl, p.stages);
   }
   double acc = 0.0;
   auto store = [&](long g, double v) {
@@ -567,6 +573,322 @@ __global__ void __launch_bounds__(256, 2) k_pfa_t(const PfaK p) {
   if (io.partial) {
     const double s = block_sum(acc, red);
     if (tid == 0) io.partial[blockIdx.x] = s;
+  }
+}
+
+// ------------------------------------- persistent TMA-pipelined DST row passes
+// One CTA per SM walks batches of kPipeLines contiguous rows.  Thread 0 pulls the
+// next batch into a staging buffer with cp.async.bulk (TMA bulk copy, completion on
+// an mbarrier) as soon as the current batch has been packed, so global loads overlap
+// the FFT stages and the unpack/stores of the current batch.  The output is written
+// either row-major or transposed (column segments of kPipeLines doubles), which lets
+// the 2D preconditioner run every pass over contiguous rows.
+constexpr int kPipeLines = 2;     // lines per batch (power of two)
+constexpr int kPipeThreads = 256;
+constexpr int kPipeCtasPerSm = 2;  // two CTAs per SM overlap each other's phases
+
+static bool pfa_specialised(const PfaPlan& P, int* which);
+
+struct PipeK {
+  PfaPlan pl;
+  int n, off, nlines, transposed;
+  int stages;  // profiling knob (TVD_PFA_STAGES): 0 = pack/unpack only
+  double scale;
+  const double* in;
+  double* out;
+  const double* pre;       // input layout
+  const double* mid;       // input layout
+  const double* post;      // output layout
+  const double* dot_with;  // output layout
+  double* partial;
+  const int* skip;
+  int pre_mul, post_mul;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TVD_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TVD_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+template <int Q1, int Q2, int Q3, int NL>
+__device__ __forceinline__ void pfa_transform_nl(double2* buf, unsigned* const* reps,
+                                                 const PfaPlan& pl) {
+  using SH = PfaShape<Q1, Q2, Q3>;
+  constexpr int NW = kPipeThreads / 32;
+  pfa_stage_c<PfaStageC<SH, 0>, NL, 4, NW>(buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
+  if constexpr (SH::d >= 2)
+    pfa_stage_c<PfaStageC<SH, 1>, NL, 4, NW>(buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
+  if constexpr (SH::d >= 3)
+    pfa_stage_c<PfaStageC<SH, 2>, NL, 4, NW>(buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
+}
+
+template <int Q1, int Q2, int Q3>
+__global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const PipeK p) {
+  using SH = PfaShape<Q1, Q2, Q3>;
+  constexpr int L = SH::L, N = SH::N, B = kPipeLines;
+  constexpr int kTpt = (N + kPipeThreads - 1) / kPipeThreads;  // t-values per thread per line
+  static_assert((B & (B - 1)) == 0, "transposed store assumes power-of-two batches");
+  if (p.skip && *p.skip) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double red[32];
+  __shared__ double bord[B][2];
+  __shared__ __align__(8) unsigned long long mbar;
+  const int tid = threadIdx.x, nth = blockDim.x, n = p.n;
+  double2* buf = reinterpret_cast<double2*>(smraw);
+  double* stage = reinterpret_cast<double*>(buf + B * L);
+  unsigned* scat = reinterpret_cast<unsigned*>(stage + B * n);
+  unsigned* gath = scat + N;
+  unsigned* reps[3];
+  reps[0] = gath + N;
+  reps[1] = reps[0] + PfaStageC<SH, 0>::Rcnt;
+  reps[2] = reps[1] + (SH::d >= 2 ? PfaStageC<SH, 1>::Rcnt : 0);
+  for (int i = tid; i < N; i += nth) {
+    scat[i] = p.pl.scat[i];
+    gath[i] = p.pl.gath[i];
+  }
+  for (int s = 0; s < SH::d; ++s) {
+    const int rc = s == 0 ? PfaStageC<SH, 0>::Rcnt
+                          : (s == 1 ? PfaStageC<SH, 1>::Rcnt : PfaStageC<SH, 2>::Rcnt);
+    for (int i = tid; i < rc; i += nth) reps[s][i] = p.pl.reps[s][i];
+  }
+  const int nbatch = (p.nlines + B - 1) / B;
+  auto issue = [&](int batch) {
+    const int rows = min(B, p.nlines - batch * B);
+    mbar_expect_tx(&mbar, (unsigned)(rows * n * 8));
+    for (int l = 0; l < rows; ++l)
+      bulk_g2s(stage + l * n, p.in + (long)(batch * B + l) * n, (unsigned)(n * 8), &mbar);
+  };
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    if ((int)blockIdx.x < nbatch) issue(blockIdx.x);
+  }
+  __syncthreads();
+  auto put = [&](int l, int t, double v) {
+    const unsigned e = scat[t - 1];
+    double* b = reinterpret_cast<double*>(buf + l * L) + (t & 1);
+    b[2 * (e & 0xffffu)] = v;
+    b[2 * (e >> 16)] = -v;
+  };
+  auto get = [&](int l, int k) {
+    const double2 C = buf[l * L + gath[k - 1]];
+    return ((k & 1) ? -(C.y + C.x) : -(C.y - C.x)) * p.scale;
+  };
+  const long nl_out = p.nlines;
+  auto oidx = [&](int line, int e) {
+    return p.transposed ? (long)e * nl_out + line : (long)line * n + e;
+  };
+  double acc = 0.0;
+  unsigned phase = 0;
+  for (int b = blockIdx.x; b < nbatch; b += gridDim.x) {
+    const int line0 = b * B, nlv = min(B, p.nlines - line0);
+    for (int i = tid; i < B; i += nth) buf[i * L] = make_double2(0.0, 0.0);
+    for (int i = tid; i < (B - nlv) * L; i += nth) buf[nlv * L + i] = make_double2(0.0, 0.0);
+    mbar_wait(&mbar, phase);
+    phase ^= 1u;
+    // pack from the staging rows (+ Shat borders parked in smem): thread owns t = 1 + tid + k nth
+    for (int l = 0; l < nlv; ++l) {
+      const double* srow = stage + l * n + p.off - 1;  // srow[t] = x_t
+      const double* prow = p.pre ? p.pre + (long)(line0 + l) * n + p.off - 1 : nullptr;
+      double* bl = reinterpret_cast<double*>(buf + l * L);
+#pragma unroll
+      for (int k = 0; k < kTpt; ++k) {
+        const int t = 1 + tid + k * kPipeThreads;
+        if (k < kTpt - 1 || t <= N) {
+          double x = srow[t];
+          if (prow) x = p.pre_mul ? x * prow[t] : x / prow[t];
+          const unsigned e = scat[t - 1];
+          double* b = bl + (t & 1);
+          b[2 * (e & 0xffffu)] = x;
+          b[2 * (e >> 16)] = -x;
+        }
+      }
+    }
+    if (p.off && tid < 2 * nlv) {
+      const int l = tid >> 1, e = (tid & 1) ? n - 1 : 0;
+      double x = stage[l * n + e];
+      if (p.pre) {
+        const double q = p.pre[(long)(line0 + l) * n + e];
+        x = p.pre_mul ? x * q : x / q;
+      }
+      bord[l][tid & 1] = x;
+    }
+    __syncthreads();
+    if (tid == 0 && b + (int)gridDim.x < nbatch) {
+      fence_proxy_async();  // staging was read through the generic proxy
+      issue(b + gridDim.x);
+    }
+    if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B>(buf, reps, p.pl);
+    if (p.mid) {
+      double v[B][kTpt];
+#pragma unroll
+      for (int l = 0; l < B; ++l) {
+        const double* mrow = p.mid + (long)(line0 + min(l, nlv - 1)) * n + p.off - 1;
+#pragma unroll
+        for (int k = 0; k < kTpt; ++k) {
+          const int t = 1 + tid + k * kPipeThreads;
+          v[l][k] = (l < nlv && t <= N) ? mrow[t] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < B; ++l)
+#pragma unroll
+        for (int k = 0; k < kTpt; ++k) {
+          const int t = 1 + tid + k * kPipeThreads;
+          if (l < nlv && t <= N) v[l][k] *= get(l, t);
+        }
+      __syncthreads();
+#pragma unroll
+      for (int l = 0; l < B; ++l)
+#pragma unroll
+        for (int k = 0; k < kTpt; ++k) {
+          const int t = 1 + tid + k * kPipeThreads;
+          if (l < nlv && t <= N) put(l, t, v[l][k]);
+        }
+      for (int i = tid; i < B; i += nth) buf[i * L] = make_double2(0.0, 0.0);
+      __syncthreads();
+      if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B>(buf, reps, p.pl);
+    }
+    // unpack + store (transposed: line index fastest -> B-double column segments)
+    if (p.transposed) {
+      const int l = tid & (B - 1);
+      if (l < nlv) {
+        double* ocol = p.out + (long)(p.off - 1) * nl_out + line0 + l;  // ocol[t * nl] = y_t
+        const double* dcol = p.dot_with ? p.dot_with + (long)(p.off - 1) * nl_out + line0 + l
+                                        : nullptr;
+        const double* qcol = p.post ? p.post + (long)(p.off - 1) * nl_out + line0 + l : nullptr;
+        constexpr int TS = kPipeThreads / B;
+        for (int t = 1 + tid / B; t <= N; t += TS) {
+          const long o = (long)t * nl_out;
+          double y = get(l, t);
+          if (qcol) y = p.post_mul ? y * qcol[o] : y / qcol[o];
+          ocol[o] = y;
+          if (dcol) acc += y * dcol[o];
+        }
+      }
+    } else {
+      for (int l = 0; l < nlv; ++l) {
+        const long rowb = (long)(line0 + l) * n + p.off - 1;
+        double* orow = p.out + rowb;
+        const double* drow = p.dot_with ? p.dot_with + rowb : nullptr;
+        const double* qrow = p.post ? p.post + rowb : nullptr;
+#pragma unroll
+        for (int k = 0; k < kTpt; ++k) {
+          const int t = 1 + tid + k * kPipeThreads;
+          if (k < kTpt - 1 || t <= N) {
+            double y = get(l, t);
+            if (qrow) y = p.post_mul ? y * qrow[t] : y / qrow[t];
+            orow[t] = y;
+            if (drow) acc += y * drow[t];
+          }
+        }
+      }
+    }
+    if (p.off && tid < 2 * nlv) {
+      const int l = tid >> 1, e = (tid & 1) ? n - 1 : 0;
+      double y = bord[l][tid & 1];
+      if (p.mid) y *= p.mid[(long)(line0 + l) * n + e];
+      const long g = oidx(line0 + l, e);
+      if (p.post) y = p.post_mul ? y * p.post[g] : y / p.post[g];
+      p.out[g] = y;
+      if (p.dot_with) acc += y * p.dot_with[g];
+    }
+    __syncthreads();
+  }
+  if (p.partial) {
+    const double s = block_sum(acc, red);
+    if (tid == 0) p.partial[blockIdx.x] = s;
+  }
+}
+
+template <int Q1, int Q2, int Q3>
+static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
+  using SH = PfaShape<Q1, Q2, Q3>;
+  int reps = PfaStageC<SH, 0>::Rcnt;
+  if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
+  if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
+  const size_t smem = (size_t)kPipeLines * SH::L * 16 + (size_t)kPipeLines * k.n * 8 +
+                      (2 * SH::N + reps) * sizeof(unsigned);
+  if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    attr = true;
+  }
+  k_dst_pipe<Q1, Q2, Q3><<<grid, kPipeThreads, smem, st>>>(k);
+  return cudaGetLastError();
+}
+
+int pipe_grid(const PfaPlan& P, int nlines) {
+  int which;
+  if (!pfa_specialised(P, &which)) return -1;
+  const int nbatch = (nlines + kPipeLines - 1) / kPipeLines;
+  return nbatch < kSMs * kPipeCtasPerSm ? nbatch : kSMs * kPipeCtasPerSm;
+}
+
+cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int transposed,
+                        const LineIO& io, int* nblocks_out, cudaStream_t st) {
+  int which;
+  if (!pfa_specialised(P, &which) || (len & 1)) return cudaErrorInvalidConfiguration;
+  PipeK k{};
+  k.pl = P;
+  k.n = len;
+  k.off = family == kFamSineHat ? 1 : 0;
+  k.nlines = nlines;
+  k.transposed = transposed;
+  k.scale = 0.5 * sqrt(2.0 / P.L);
+  k.in = io.in;
+  k.out = io.out;
+  k.pre = io.pre;
+  k.pre_mul = io.pre_mul;
+  k.mid = io.mid_mul;
+  k.post = io.post;
+  k.post_mul = io.post_mul;
+  k.dot_with = io.dot_with;
+  k.partial = io.partial;
+  k.skip = io.skip;
+  static const int stages_env = [] {
+    const char* s = getenv("TVD_PFA_STAGES");
+    return s ? atoi(s) : 3;
+  }();
+  k.stages = stages_env;
+  const int grid = pipe_grid(P, nlines);
+  if (nblocks_out) *nblocks_out = grid;
+  if (grid <= 0) return cudaSuccess;
+  switch (which) {
+    case 1: return launch_pipe_t<89, 23, 1>(k, grid, st);
+    case 2: return launch_pipe_t<31, 11, 3>(k, grid, st);
+    case 3: return launch_pipe_t<73, 7, 1>(k, grid, st);
+    case 4: return launch_pipe_t<127, 1, 1>(k, grid, st);
+    default: return cudaErrorInvalidConfiguration;
   }
 }
 
@@ -640,6 +962,11 @@ cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g,
   k.es = g.es;
   k.scale = 0.5 * sqrt(2.0 / P.L);
   k.h = (P.L - 1) / 2;
+  static const int stages_env = [] {
+    const char* s = getenv("TVD_PFA_STAGES");  // profiling knob: run only the first stages
+    return s ? atoi(s) : 3;
+  }();
+  k.stages = stages_env;
   k.io = io;
   const int nb = (g.nlines + nl - 1) / nl;
   if (nblocks_out) *nblocks_out = nb;

@@ -61,12 +61,97 @@ __device__ __forceinline__ void rep_ab(int t, int& a, int& b) {
 
 // fold + DFT of one stage.  `reps` holds (base | neg << 16) of every representative line
 // (line 0); line l adds l * LP.
-template <class ST, int NL>
+template <class ST, int NL, int MT = 4, int NW = 0>
 __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
                                             const double* Cm, const double* Sm) {
+  constexpr int kMmaTiles = MT;  // output tiles a warp holds across the in-place barrier
   constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LPc;
   const int tid = threadIdx.x, nth = blockDim.x;
-  // fold
+  constexpr int ndft = NL * ST::Rcnt;
+  if constexpr (ST::mma && NW > 0) {
+    // A-stationary tensor-core stage: warp -> fixed k-tile (its cos/sin fragments for every
+    // r stay in registers) x a strided set of column tiles; the fold a/b is fused into the
+    // B-fragment load, so there is no separate fold sweep.
+    constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;
+    constexpr int G = NW / nkt >= 1 ? NW / nkt : 1;      // warps sharing one k-tile
+    constexpr int TPW = 3;                                 // column tiles per warp per round
+    constexpr int ROUND = G * TPW;                         // column tiles per round
+    const int lane = tid & 31, warp = tid >> 5;
+    const int kt = warp % nkt, g = warp / nkt;
+    const bool wact = warp < nkt * G;
+    const int krow = kt * 8 + (lane >> 2);
+    double ca[nrs], sa[nrs];
+#pragma unroll
+    for (int rs = 0; rs < nrs; ++rs) {
+      ca[rs] = Cm[krow * ST::RP + rs * 4 + (lane & 3)];
+      sa[rs] = Sm[krow * ST::RP + rs * 4 + (lane & 3)];
+    }
+    const double* bufd = reinterpret_cast<const double*>(buf);
+    for (int ct0 = 0; ct0 < nct; ct0 += ROUND) {
+    double2 vk[TPW], vm[TPW];
+    unsigned ob[TPW];
+    int oflag[TPW];
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) {
+      oflag[j] = 0;
+      const int ct = ct0 + g + j * G;
+      if (wact && ct < nct) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        const int colB = ct * 8 + (lane >> 2);
+        const int dB = colB >> 1;
+        const bool vB = dB < ndft;
+        const int lB = vB ? dB / ST::Rcnt : 0;
+        const int tB = vB ? dB - lB * ST::Rcnt : 0;
+        const double* pb = bufd + 2 * (lB * LP + (reps[tB] & 0xffffu)) + (colB & 1);
+#pragma unroll
+        for (int rs = 0; rs < nrs; ++rs) {
+          const int r = 1 + rs * 4 + (lane & 3);
+          double x1 = 0.0, x2 = 0.0;
+          if (vB && (rs * 4 + 4 <= H || r <= H)) {
+            x1 = pb[2 * r * st];
+            x2 = pb[2 * (q - r) * st];
+          }
+          dmma884(a0, a1, ca[rs], x1 + x2);
+          dmma884(b0, b1, sa[rs], x1 - x2);
+        }
+        const int dO = ct * 4 + (lane & 3);
+        if (krow <= H && dO < ndft) {
+          const int lO = dO / ST::Rcnt, tO = dO - lO * ST::Rcnt;
+          const unsigned rp = reps[tO] + (unsigned)(lO * LP) * 0x10001u;
+          const double2 x0 = buf[rp & 0xffffu];
+          vk[j] = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
+          vm[j] = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
+          ob[j] = rp;
+          oflag[j] = 1 | (tO == 0 ? 2 : 0);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) {
+      if (oflag[j]) {
+        const int k = krow;
+        double2* p = buf + (ob[j] & 0xffffu);
+        double2* pn = buf + (ob[j] >> 16);
+        const bool self = oflag[j] & 2;
+        if (k == 0) {
+          p[0] = vk[j];
+          if (!self) pn[0] = make_double2(-vk[j].x, -vk[j].y);
+        } else {
+          p[k * st] = vk[j];
+          p[(q - k) * st] = vm[j];
+          if (!self) {
+            pn[(q - k) * st] = make_double2(-vk[j].x, -vk[j].y);
+            pn[k * st] = make_double2(-vm[j].x, -vm[j].y);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    }
+    return;
+  }
+  // fold (scalar and legacy tensor-core paths)
   constexpr int nfold = NL * ST::Rcnt * H;
   for (int i = tid; i < nfold; i += nth) {
     const int t = i % ST::Rcnt;
@@ -79,7 +164,6 @@ __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
     p[(q - r) * st] = csub(x1, x2);
   }
   __syncthreads();
-  constexpr int ndft = NL * ST::Rcnt;
   if constexpr (ST::mma) {
     const int lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
     constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;

@@ -723,6 +723,29 @@ cudaError_t launch_normal_epilogue(const double* base, const Epilogue& ep, int n
   return cudaGetLastError();
 }
 
+// ----------------------------------------------------------- transpose
+__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int n) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = by + r, j = bx + threadIdx.x;
+    if (i < n && j < n) tile[r][threadIdx.x] = in[(long)i * n + j];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = bx + r, j = by + threadIdx.x;
+    if (i < n && j < n) out[(long)i * n + j] = tile[threadIdx.x][r];
+  }
+}
+}  // namespace tvd
+
+namespace tvd {
+cudaError_t launch_transpose(const double* in, double* out, int n, cudaStream_t st) {
+  dim3 grid((n + 31) / 32, (n + 31) / 32), block(32, 8);
+  k_transpose<<<grid, block, 0, st>>>(in, out, n);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------- blur eigenvalue grid
 // lam[s][t] = sum_a c[s][a] sum_b h[a][b] c[t][b]   (blur.py:137-160, 276-291)
 __global__ void k_eig_stage1(const double* __restrict__ c, const double* __restrict__ h, int n, int K,
