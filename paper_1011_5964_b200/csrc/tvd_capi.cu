@@ -339,6 +339,8 @@ static bool build_pfa(TrigPlan* P) {
     pl.rinv[s] = (int)modinv((L / pl.q[s]) % pl.q[s], pl.q[s]);
     pl.fq[s] = make_fdiv(pl.q[s]);
   }
+  if (pl.d == 2) pl.stride[0] = pfa_row_pitch(pl.q[1]);
+  pl.LP = pl.q[0] * pl.stride[0];
   pl.fN = make_fdiv(L - 1);
   for (int s = 0; s < pl.d; ++s) {
     PfaStage& S = pl.st[s];

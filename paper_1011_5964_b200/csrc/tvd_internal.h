@@ -49,8 +49,13 @@ struct PfaStage {
   const double* Sm;    // [k][r-1] = sin(2 pi r k / q)
 };
 
+// Good-Thomas line layout (row-major over the factors).  Two-factor shapes pad the
+// row pitch to pfa_row_pitch(q1) so the CRT gather and the DMMA fragment loads of a
+// warp fall on distinct shared-memory banks; LP is the padded line size.
+constexpr int pfa_row_pitch(int q1) { return q1 + ((2 - q1 % 4) + 4) % 4; }
+
 struct PfaPlan {
-  int L, d;
+  int L, d, LP;
   int q[3], stride[3], rinv[3];
   FDiv fq[3];
   FDiv fN;             // N = L - 1

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256, 2) k_pfa(const PfaK p) {
   extern __shared__ double2 smem2[];
   __shared__ double red[32];
   const int tid = threadIdx.x, nth = blockDim.x;
-  const int L = p.pl.L, LP = L, N = p.N, nl = p.nl;
+  const int LP = p.pl.LP, N = p.N, nl = p.nl;
   const int line0 = blockIdx.x * nl;
   const int nlv = min(nl, p.nlines - line0);
   double2* buf = smem2;
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(256, 2) k_pfa(const PfaK p) {
   };
   // zero slot of every line (c'_0 = 0) and dead lines
   for (int i = tid; i < nl; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
-  for (int i = tid; i < (nl - nlv) * L; i += nth) buf[nlv * LP + i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < (nl - nlv) * LP; i += nth) buf[nlv * LP + i] = make_double2(0.0, 0.0);
   // element i of this CTA's lines -> (line, t), memory-friendly order
   const bool contig = p.es == 1;
   auto split = [&](int i, int& l, int& t) {
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(256, 2) k_pfa(const PfaK p) {
       __syncthreads();
     }
     for (int l = nlv; l < nl; ++l)
-      for (int i = tid; i < L; i += nth) buf[l * LP + i] = make_double2(0.0, 0.0);
+      for (int i = tid; i < LP; i += nth) buf[l * LP + i] = make_double2(0.0, 0.0);
     for (int l = tid; l < nlv; l += nth) buf[l * LP] = make_double2(0.0, 0.0);  // c'_0
     __syncthreads();
     pfa_transform(buf, LP, nl, p);
@@ -462,14 +462,14 @@ __device__ __forceinline__ void pfa_transform_c(double2* buf, unsigned* const* r
 template <int Q1, int Q2, int Q3>
 __global__ void __launch_bounds__(256, 2) k_pfa_t(const PfaK p) {
   using SH = PfaShape<Q1, Q2, Q3>;
-  constexpr int L = SH::L, N = SH::N, NL = kPfaLinesT;
+  constexpr int LP = SH::LP, N = SH::N, NL = kPfaLinesT;
   const LineIO& io = p.io;
   if (io.skip && *io.skip) return;
   extern __shared__ double2 smem2[];
   __shared__ double red[32];
   const int tid = threadIdx.x, nth = blockDim.x;
   double2* buf = smem2;
-  unsigned* scat = reinterpret_cast<unsigned*>(buf + NL * L);
+  unsigned* scat = reinterpret_cast<unsigned*>(buf + NL * LP);
   unsigned* gath = scat + N;
   unsigned* reps[3];
   reps[0] = gath + N;
@@ -486,19 +486,19 @@ __global__ void __launch_bounds__(256, 2) k_pfa_t(const PfaK p) {
                                                               : PfaStageC<SH, 2>::Rcnt);
     for (int i = tid; i < rc; i += nth) reps[s][i] = p.pl.reps[s][i];
   }
-  for (int i = tid; i < NL; i += nth) buf[i * L] = make_double2(0.0, 0.0);
-  for (int i = tid; i < (NL - nlv) * L; i += nth) buf[nlv * L + i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < NL; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
+  for (int i = tid; i < (NL - nlv) * LP; i += nth) buf[nlv * LP + i] = make_double2(0.0, 0.0);
   __syncthreads();
   const bool contig = p.es == 1;
   auto gidx = [&](int l, int t) { return (long)(line0 + l) * p.ls + (long)(p.off + t - 1) * p.es; };
   auto put = [&](int l, int t, double v) {
     const unsigned e = scat[t - 1];
-    double* b = reinterpret_cast<double*>(buf + l * L) + (t & 1);
+    double* b = reinterpret_cast<double*>(buf + l * LP) + (t & 1);
     b[2 * (e & 0xffffu)] = v;
     b[2 * (e >> 16)] = -v;
   };
   auto get = [&](int l, int k) {
-    const double2 C = buf[l * L + gath[k - 1]];
+    const double2 C = buf[l * LP + gath[k - 1]];
     return ((k & 1) ? -(C.y + C.x) : -(C.y - C.x)) * p.scale;
   };
   // pack: batched global loads, then the table-driven scatter
@@ -543,8 +543,8 @@ __global__ void __launch_bounds__(256, 2) k_pfa_t(const PfaK p) {
       }
       __syncthreads();
     }
-    for (int i = tid; i < NL; i += nth) buf[i * L] = make_double2(0.0, 0.0);
-    for (int i = tid; i < (NL - nlv) * L; i += nth) buf[nlv * L + i] = make_double2(0.0, 0.0);
+    for (int i = tid; i < NL; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
+    for (int i = tid; i < (NL - nlv) * LP; i += nth) buf[nlv * LP + i] = make_double2(0.0, 0.0);
     __syncthreads();
     pfa_transform_c<Q1, Q2, Q3>(buf, reps, p.pl, p.stages);
   }
@@ -653,7 +653,7 @@ __device__ __forceinline__ void pfa_transform_nl(double2* buf, unsigned* const* 
 template <int Q1, int Q2, int Q3>
 __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const PipeK p) {
   using SH = PfaShape<Q1, Q2, Q3>;
-  constexpr int L = SH::L, N = SH::N, B = kPipeLines;
+  constexpr int LP = SH::LP, N = SH::N, B = kPipeLines;
   constexpr int kTpt = (N + kPipeThreads - 1) / kPipeThreads;  // t-values per thread per line
   static_assert((B & (B - 1)) == 0, "transposed store assumes power-of-two batches");
   if (p.skip && *p.skip) return;
@@ -663,17 +663,15 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
   __shared__ __align__(8) unsigned long long mbar;
   const int tid = threadIdx.x, nth = blockDim.x, n = p.n;
   double2* buf = reinterpret_cast<double2*>(smraw);
-  double* stage = reinterpret_cast<double*>(buf + B * L);
-  unsigned* scat = reinterpret_cast<unsigned*>(stage + B * n);
-  unsigned* gath = scat + N;
+  double* stage = reinterpret_cast<double*>(buf + B * LP);
+  // scatter / gather tables are read coalesced (indexed by t) through L1, leaving the
+  // shared memory to the padded lines and the staging rows
+  const unsigned* __restrict__ scat = p.pl.scat;
+  const unsigned* __restrict__ gath = p.pl.gath;
   unsigned* reps[3];
-  reps[0] = gath + N;
+  reps[0] = reinterpret_cast<unsigned*>(stage + B * n);
   reps[1] = reps[0] + PfaStageC<SH, 0>::Rcnt;
   reps[2] = reps[1] + (SH::d >= 2 ? PfaStageC<SH, 1>::Rcnt : 0);
-  for (int i = tid; i < N; i += nth) {
-    scat[i] = p.pl.scat[i];
-    gath[i] = p.pl.gath[i];
-  }
   for (int s = 0; s < SH::d; ++s) {
     const int rc = s == 0 ? PfaStageC<SH, 0>::Rcnt
                           : (s == 1 ? PfaStageC<SH, 1>::Rcnt : PfaStageC<SH, 2>::Rcnt);
@@ -691,14 +689,9 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
     if ((int)blockIdx.x < nbatch) issue(blockIdx.x);
   }
   __syncthreads();
-  auto put = [&](int l, int t, double v) {
-    const unsigned e = scat[t - 1];
-    double* b = reinterpret_cast<double*>(buf + l * L) + (t & 1);
-    b[2 * (e & 0xffffu)] = v;
-    b[2 * (e >> 16)] = -v;
-  };
-  auto get = [&](int l, int k) {
-    const double2 C = buf[l * L + gath[k - 1]];
+  // y_k from the transformed line l, gather index gi = gath[k - 1] (0 for k out of range)
+  auto unpack = [&](int l, unsigned gi, int k) {
+    const double2 C = buf[l * LP + gi];
     return ((k & 1) ? -(C.y + C.x) : -(C.y - C.x)) * p.scale;
   };
   const long nl_out = p.nlines;
@@ -709,25 +702,46 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
   unsigned phase = 0;
   for (int b = blockIdx.x; b < nbatch; b += gridDim.x) {
     const int line0 = b * B, nlv = min(B, p.nlines - line0);
-    for (int i = tid; i < B; i += nth) buf[i * L] = make_double2(0.0, 0.0);
-    for (int i = tid; i < (B - nlv) * L; i += nth) buf[nlv * L + i] = make_double2(0.0, 0.0);
+    for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
+    for (int i = tid; i < (B - nlv) * LP; i += nth) buf[nlv * LP + i] = make_double2(0.0, 0.0);
+    // pack from the staging rows (+ Shat borders parked in smem): thread owns
+    // t = 1 + tid + k nth.  The scatter indices depend on t only: one batched load
+    // serves every line of the batch and overlaps the wait for the TMA rows.
+    unsigned e[kTpt];
+#pragma unroll
+    for (int k = 0; k < kTpt; ++k) {
+      const int t = 1 + tid + k * kPipeThreads;
+      e[k] = (k < kTpt - 1 || t <= N) ? __ldg(scat + t - 1) : 0u;
+    }
     mbar_wait(&mbar, phase);
     phase ^= 1u;
-    // pack from the staging rows (+ Shat borders parked in smem): thread owns t = 1 + tid + k nth
     for (int l = 0; l < nlv; ++l) {
       const double* srow = stage + l * n + p.off - 1;  // srow[t] = x_t
-      const double* prow = p.pre ? p.pre + (long)(line0 + l) * n + p.off - 1 : nullptr;
-      double* bl = reinterpret_cast<double*>(buf + l * L);
+      double x[kTpt];
+#pragma unroll
+      for (int k = 0; k < kTpt; ++k) {
+        const int t = 1 + tid + k * kPipeThreads;
+        x[k] = (k < kTpt - 1 || t <= N) ? srow[t] : 0.0;
+      }
+      if (p.pre) {
+        const double* __restrict__ prow = p.pre + (long)(line0 + l) * n + p.off - 1;
+        double q[kTpt];
+#pragma unroll
+        for (int k = 0; k < kTpt; ++k) {
+          const int t = 1 + tid + k * kPipeThreads;
+          q[k] = (k < kTpt - 1 || t <= N) ? prow[t] : 1.0;
+        }
+#pragma unroll
+        for (int k = 0; k < kTpt; ++k) x[k] = p.pre_mul ? x[k] * q[k] : x[k] / q[k];
+      }
+      double* bl = reinterpret_cast<double*>(buf + l * LP);
 #pragma unroll
       for (int k = 0; k < kTpt; ++k) {
         const int t = 1 + tid + k * kPipeThreads;
         if (k < kTpt - 1 || t <= N) {
-          double x = srow[t];
-          if (prow) x = p.pre_mul ? x * prow[t] : x / prow[t];
-          const unsigned e = scat[t - 1];
           double* b = bl + (t & 1);
-          b[2 * (e & 0xffffu)] = x;
-          b[2 * (e >> 16)] = -x;
+          b[2 * (e[k] & 0xffffu)] = x[k];
+          b[2 * (e[k] >> 16)] = -x[k];
         }
       }
     }
@@ -746,11 +760,17 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
       issue(b + gridDim.x);
     }
     if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B>(buf, reps, p.pl);
+    unsigned g[kTpt];  // gather indices of this thread's t values
+#pragma unroll
+    for (int k = 0; k < kTpt; ++k) {
+      const int t = 1 + tid + k * kPipeThreads;
+      g[k] = (k < kTpt - 1 || t <= N) ? __ldg(gath + t - 1) : 0u;
+    }
     if (p.mid) {
       double v[B][kTpt];
 #pragma unroll
       for (int l = 0; l < B; ++l) {
-        const double* mrow = p.mid + (long)(line0 + min(l, nlv - 1)) * n + p.off - 1;
+        const double* __restrict__ mrow = p.mid + (long)(line0 + min(l, nlv - 1)) * n + p.off - 1;
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
           const int t = 1 + tid + k * kPipeThreads;
@@ -762,51 +782,107 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
           const int t = 1 + tid + k * kPipeThreads;
-          if (l < nlv && t <= N) v[l][k] *= get(l, t);
+          if (l < nlv && t <= N) v[l][k] *= unpack(l, g[k], t);
         }
       __syncthreads();
 #pragma unroll
-      for (int l = 0; l < B; ++l)
+      for (int l = 0; l < B; ++l) {
+        double* bl = reinterpret_cast<double*>(buf + l * LP);
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
           const int t = 1 + tid + k * kPipeThreads;
-          if (l < nlv && t <= N) put(l, t, v[l][k]);
+          if (l < nlv && t <= N) {
+            double* bb = bl + (t & 1);
+            bb[2 * (e[k] & 0xffffu)] = v[l][k];
+            bb[2 * (e[k] >> 16)] = -v[l][k];
+          }
         }
-      for (int i = tid; i < B; i += nth) buf[i * L] = make_double2(0.0, 0.0);
+      }
+      for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
       __syncthreads();
       if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B>(buf, reps, p.pl);
     }
-    // unpack + store (transposed: line index fastest -> B-double column segments)
+    // unpack + store (transposed: line index fastest -> B-double column segments).
+    // All global loads of a group are issued before its stores.
     if (p.transposed) {
       const int l = tid & (B - 1);
+      constexpr int TS = kPipeThreads / B;
+      constexpr int JT = (N + TS - 1) / TS;
+      constexpr int JG = 8;
       if (l < nlv) {
-        double* ocol = p.out + (long)(p.off - 1) * nl_out + line0 + l;  // ocol[t * nl] = y_t
-        const double* dcol = p.dot_with ? p.dot_with + (long)(p.off - 1) * nl_out + line0 + l
-                                        : nullptr;
-        const double* qcol = p.post ? p.post + (long)(p.off - 1) * nl_out + line0 + l : nullptr;
-        constexpr int TS = kPipeThreads / B;
-        for (int t = 1 + tid / B; t <= N; t += TS) {
-          const long o = (long)t * nl_out;
-          double y = get(l, t);
-          if (qcol) y = p.post_mul ? y * qcol[o] : y / qcol[o];
-          ocol[o] = y;
-          if (dcol) acc += y * dcol[o];
+        const long cb = (long)(p.off - 1) * nl_out + line0 + l;
+        double* __restrict__ ocol = p.out + cb;  // ocol[t * nl] = y_t
+        const double* __restrict__ dcol = p.dot_with ? p.dot_with + cb : nullptr;
+        const double* __restrict__ qcol = p.post ? p.post + cb : nullptr;
+        const int t0 = 1 + tid / B;
+#pragma unroll
+        for (int j0 = 0; j0 < JT; j0 += JG) {
+          unsigned gg[JG];
+          double y[JG];
+#pragma unroll
+          for (int j = 0; j < JG; ++j) {
+            const int t = t0 + (j0 + j) * TS;
+            gg[j] = (j0 + j < JT && t <= N) ? __ldg(gath + t - 1) : 0u;
+          }
+#pragma unroll
+          for (int j = 0; j < JG; ++j) y[j] = unpack(l, gg[j], t0 + (j0 + j) * TS);
+          if (qcol) {
+            double q[JG];
+#pragma unroll
+            for (int j = 0; j < JG; ++j) {
+              const int t = t0 + (j0 + j) * TS;
+              q[j] = (j0 + j < JT && t <= N) ? qcol[(long)t * nl_out] : 1.0;
+            }
+#pragma unroll
+            for (int j = 0; j < JG; ++j) y[j] = p.post_mul ? y[j] * q[j] : y[j] / q[j];
+          }
+          double dv[JG];
+#pragma unroll
+          for (int j = 0; j < JG; ++j) {
+            const int t = t0 + (j0 + j) * TS;
+            dv[j] = (dcol && j0 + j < JT && t <= N) ? dcol[(long)t * nl_out] : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < JG; ++j) {
+            const int t = t0 + (j0 + j) * TS;
+            if (j0 + j < JT && t <= N) {
+              ocol[(long)t * nl_out] = y[j];
+              acc += y[j] * dv[j];
+            }
+          }
         }
       }
     } else {
       for (int l = 0; l < nlv; ++l) {
         const long rowb = (long)(line0 + l) * n + p.off - 1;
-        double* orow = p.out + rowb;
-        const double* drow = p.dot_with ? p.dot_with + rowb : nullptr;
-        const double* qrow = p.post ? p.post + rowb : nullptr;
+        double* __restrict__ orow = p.out + rowb;
+        const double* __restrict__ drow = p.dot_with ? p.dot_with + rowb : nullptr;
+        const double* __restrict__ qrow = p.post ? p.post + rowb : nullptr;
+        double y[kTpt];
+#pragma unroll
+        for (int k = 0; k < kTpt; ++k) y[k] = unpack(l, g[k], 1 + tid + k * kPipeThreads);
+        if (qrow) {
+          double q[kTpt];
+#pragma unroll
+          for (int k = 0; k < kTpt; ++k) {
+            const int t = 1 + tid + k * kPipeThreads;
+            q[k] = (k < kTpt - 1 || t <= N) ? qrow[t] : 1.0;
+          }
+#pragma unroll
+          for (int k = 0; k < kTpt; ++k) y[k] = p.post_mul ? y[k] * q[k] : y[k] / q[k];
+        }
+        double dv[kTpt];
+#pragma unroll
+        for (int k = 0; k < kTpt; ++k) {
+          const int t = 1 + tid + k * kPipeThreads;
+          dv[k] = (drow && (k < kTpt - 1 || t <= N)) ? drow[t] : 0.0;
+        }
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
           const int t = 1 + tid + k * kPipeThreads;
           if (k < kTpt - 1 || t <= N) {
-            double y = get(l, t);
-            if (qrow) y = p.post_mul ? y * qrow[t] : y / qrow[t];
-            orow[t] = y;
-            if (drow) acc += y * drow[t];
+            orow[t] = y[k];
+            acc += y[k] * dv[k];
           }
         }
       }
@@ -834,8 +910,8 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   int reps = PfaStageC<SH, 0>::Rcnt;
   if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
   if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
-  const size_t smem = (size_t)kPipeLines * SH::L * 16 + (size_t)kPipeLines * k.n * 8 +
-                      (2 * SH::N + reps) * sizeof(unsigned);
+  const size_t smem = (size_t)kPipeLines * SH::LP * 16 + (size_t)kPipeLines * k.n * 8 +
+                      reps * sizeof(unsigned);
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
@@ -898,7 +974,7 @@ static cudaError_t launch_pfa_t(const PfaK& k, int nb, cudaStream_t st) {
   int reps = PfaStageC<SH, 0>::Rcnt;
   if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
   if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
-  const size_t smem = (size_t)kPfaLinesT * SH::L * 16 + (2 * SH::N + reps) * sizeof(unsigned);
+  const size_t smem = (size_t)kPfaLinesT * SH::LP * 16 + (2 * SH::N + reps) * sizeof(unsigned);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_pfa_t<Q1, Q2, Q3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -919,7 +995,7 @@ static bool pfa_specialised(const PfaPlan& P, int* which) {
 }
 
 static int pfa_config(const PfaPlan& P, bool contiguous, int* nl, int* nth, size_t* smem) {
-  const size_t line_bytes = (size_t)P.L * 16;
+  const size_t line_bytes = (size_t)P.LP * 16;
   int k = 2;
   (void)contiguous;
   while (k > 1 && k * line_bytes > 150 * 1024) k >>= 1;

@@ -21,7 +21,8 @@ struct PfaShape {
   static constexpr int L = Q1 * Q2 * Q3;
   static constexpr int d = (Q1 > 1) + (Q2 > 1) + (Q3 > 1);
   static constexpr int q[3] = {Q1, Q2, Q3};
-  static constexpr int stride[3] = {Q2 * Q3, Q3, 1};
+  static constexpr int stride[3] = {d == 2 ? pfa_row_pitch(Q2) : Q2 * Q3, Q3, 1};
+  static constexpr int LP = Q1 * stride[0];  // padded line size (tvd_internal.h)
   static constexpr int h = (L - 1) / 2;
   static constexpr int N = L - 1;
 };
@@ -44,7 +45,7 @@ struct PfaStageC {
   static constexpr int KP = (H + 1 + 7) / 8 * 8;
   static constexpr int RP = (H + 3) / 4 * 4;
   static constexpr bool mma = H >= 8;
-  static constexpr int LPc = SH::L;
+  static constexpr int LPc = SH::LP;
 };
 
 template <class ST>
