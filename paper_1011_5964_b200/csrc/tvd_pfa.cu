@@ -85,7 +85,7 @@ __device__ __forceinline__ void dft_lines(int dft, const PfaStage& S, int LP, in
 
 // D(8x8) += A(8x4) * B(4x8), fp64 tensor-core MMA (SASS DMMA.884).
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -441,6 +441,9 @@ __global__ void __launch_bounds__(256, 2) k_pfa(const PfaK p) {
 }
 
 // ------------------------------------------------ compile-time specialised kernel
+#ifdef TVD_PIPE_TIMING
+__device__ unsigned long long g_pipe_phase[8];  // profiling only
+#endif
 #include "tvd_pfa_t.cuh"
 
 constexpr int kPfaLinesT = 2;  // lines per CTA of the specialised kernel
@@ -584,8 +587,6 @@ __global__ void __launch_bounds__(256, 2) k_pfa_t(const PfaK p) {
 // either row-major or transposed (column segments of kPipeLines doubles), which lets
 // the 2D preconditioner run every pass over contiguous rows.
 constexpr int kPipeLines = 2;     // lines per batch (power of two)
-constexpr int kPipeThreads = 256;
-constexpr int kPipeCtasPerSm = 2;  // two CTAs per SM overlap each other's phases
 
 static bool pfa_specialised(const PfaPlan& P, int* which);
 
@@ -634,27 +635,60 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-template <int Q1, int Q2, int Q3, int NL>
+// Phase counters of the pipeline kernel (build with -DTVD_PIPE_TIMING; profiling only).
+#ifdef TVD_PIPE_TIMING
+#define PIPE_T_INIT long long ph_[5] = {0, 0, 0, 0, 0}, tl_ = clock64()
+#define PIPE_T(i)                   \
+  do {                              \
+    if (tid == 0) {                 \
+      const long long c_ = clock64(); \
+      ph_[i] += c_ - tl_;           \
+      tl_ = c_;                     \
+    }                               \
+  } while (0)
+#define PIPE_T_FLUSH                                                       \
+  do {                                                                     \
+    if (tid == 0)                                                          \
+      for (int i_ = 0; i_ < 5; ++i_) atomicAdd(&g_pipe_phase[i_], (unsigned long long)ph_[i_]); \
+    if (tid == 0) atomicAdd(&g_pipe_phase[7], 1ull);                       \
+  } while (0)
+#else
+#define PIPE_T_INIT
+#define PIPE_T(i) \
+  do {            \
+  } while (0)
+#define PIPE_T_FLUSH \
+  do {               \
+  } while (0)
+#endif
+
+template <int Q1, int Q2, int Q3, int NL, int NT, int TPW>
 __device__ __forceinline__ void pfa_transform_nl(double2* buf, unsigned* const* reps,
-                                                 const PfaPlan& pl) {
+                                                 const PfaPlan& pl, int stages = 3) {
   using SH = PfaShape<Q1, Q2, Q3>;
-  constexpr int NW = kPipeThreads / 32;
-  pfa_stage_c<PfaStageC<SH, 0>, NL, 4, NW>(buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
+  constexpr int NW = NT / 32;
+  if (stages >= 1)
+    pfa_stage_c<PfaStageC<SH, 0>, NL, 4, NW, TPW>(buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
   if constexpr (SH::d >= 2)
-    pfa_stage_c<PfaStageC<SH, 1>, NL, 4, NW>(buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
+    if (stages >= 2)
+      pfa_stage_c<PfaStageC<SH, 1>, NL, 4, NW, TPW>(buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
   if constexpr (SH::d >= 3)
-    pfa_stage_c<PfaStageC<SH, 2>, NL, 4, NW>(buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
+    if (stages >= 3)
+      pfa_stage_c<PfaStageC<SH, 2>, NL, 4, NW, TPW>(buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
 }
 
-template <int Q1, int Q2, int Q3>
-__global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const PipeK p) {
+template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW>
+__global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   using SH = PfaShape<Q1, Q2, Q3>;
   constexpr int LP = SH::LP, N = SH::N, B = kPipeLines;
-  constexpr int kTpt = (N + kPipeThreads - 1) / kPipeThreads;  // t-values per thread per line
+  constexpr int kTpt = (N + NT - 1) / NT;  // t-values per thread per line
   static_assert((B & (B - 1)) == 0, "transposed store assumes power-of-two batches");
   if (p.skip && *p.skip) return;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -681,8 +715,17 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
   auto issue = [&](int batch) {
     const int rows = min(B, p.nlines - batch * B);
     mbar_expect_tx(&mbar, (unsigned)(rows * n * 8));
-    for (int l = 0; l < rows; ++l)
-      bulk_g2s(stage + l * n, p.in + (long)(batch * B + l) * n, (unsigned)(n * 8), &mbar);
+    for (int l = 0; l < rows; ++l) {
+      const long r = (long)(batch * B + l) * n;
+      bulk_g2s(stage + l * n, p.in + r, (unsigned)(n * 8), &mbar);
+      // the row streams read with plain loads later in this batch: pull them into L2 now
+      if (p.pre) bulk_prefetch_l2(p.pre + r, (unsigned)(n * 8));
+      if (p.mid) bulk_prefetch_l2(p.mid + r, (unsigned)(n * 8));
+      if (!p.transposed) {
+        if (p.post) bulk_prefetch_l2(p.post + r, (unsigned)(n * 8));
+        if (p.dot_with) bulk_prefetch_l2(p.dot_with + r, (unsigned)(n * 8));
+      }
+    }
   };
   if (tid == 0) {
     mbar_init(&mbar, 1);
@@ -700,6 +743,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
   };
   double acc = 0.0;
   unsigned phase = 0;
+  PIPE_T_INIT;
   for (int b = blockIdx.x; b < nbatch; b += gridDim.x) {
     const int line0 = b * B, nlv = min(B, p.nlines - line0);
     for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
@@ -710,17 +754,18 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
     unsigned e[kTpt];
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int t = 1 + tid + k * kPipeThreads;
+      const int t = 1 + tid + k * NT;
       e[k] = (k < kTpt - 1 || t <= N) ? __ldg(scat + t - 1) : 0u;
     }
     mbar_wait(&mbar, phase);
     phase ^= 1u;
+    PIPE_T(0);
     for (int l = 0; l < nlv; ++l) {
       const double* srow = stage + l * n + p.off - 1;  // srow[t] = x_t
       double x[kTpt];
 #pragma unroll
       for (int k = 0; k < kTpt; ++k) {
-        const int t = 1 + tid + k * kPipeThreads;
+        const int t = 1 + tid + k * NT;
         x[k] = (k < kTpt - 1 || t <= N) ? srow[t] : 0.0;
       }
       if (p.pre) {
@@ -728,7 +773,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
         double q[kTpt];
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
-          const int t = 1 + tid + k * kPipeThreads;
+          const int t = 1 + tid + k * NT;
           q[k] = (k < kTpt - 1 || t <= N) ? prow[t] : 1.0;
         }
 #pragma unroll
@@ -737,7 +782,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
       double* bl = reinterpret_cast<double*>(buf + l * LP);
 #pragma unroll
       for (int k = 0; k < kTpt; ++k) {
-        const int t = 1 + tid + k * kPipeThreads;
+        const int t = 1 + tid + k * NT;
         if (k < kTpt - 1 || t <= N) {
           double* b = bl + (t & 1);
           b[2 * (e[k] & 0xffffu)] = x[k];
@@ -755,15 +800,17 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
       bord[l][tid & 1] = x;
     }
     __syncthreads();
+    PIPE_T(1);
     if (tid == 0 && b + (int)gridDim.x < nbatch) {
       fence_proxy_async();  // staging was read through the generic proxy
       issue(b + gridDim.x);
     }
-    if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B>(buf, reps, p.pl);
+    if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, reps, p.pl, p.stages);
+    PIPE_T(2);
     unsigned g[kTpt];  // gather indices of this thread's t values
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int t = 1 + tid + k * kPipeThreads;
+      const int t = 1 + tid + k * NT;
       g[k] = (k < kTpt - 1 || t <= N) ? __ldg(gath + t - 1) : 0u;
     }
     if (p.mid) {
@@ -773,7 +820,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
         const double* __restrict__ mrow = p.mid + (long)(line0 + min(l, nlv - 1)) * n + p.off - 1;
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
-          const int t = 1 + tid + k * kPipeThreads;
+          const int t = 1 + tid + k * NT;
           v[l][k] = (l < nlv && t <= N) ? mrow[t] : 0.0;
         }
       }
@@ -781,7 +828,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
       for (int l = 0; l < B; ++l)
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
-          const int t = 1 + tid + k * kPipeThreads;
+          const int t = 1 + tid + k * NT;
           if (l < nlv && t <= N) v[l][k] *= unpack(l, g[k], t);
         }
       __syncthreads();
@@ -790,7 +837,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
         double* bl = reinterpret_cast<double*>(buf + l * LP);
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
-          const int t = 1 + tid + k * kPipeThreads;
+          const int t = 1 + tid + k * NT;
           if (l < nlv && t <= N) {
             double* bb = bl + (t & 1);
             bb[2 * (e[k] & 0xffffu)] = v[l][k];
@@ -800,13 +847,14 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
       }
       for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
       __syncthreads();
-      if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B>(buf, reps, p.pl);
+      if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, reps, p.pl, p.stages);
     }
+    PIPE_T(3);
     // unpack + store (transposed: line index fastest -> B-double column segments).
     // All global loads of a group are issued before its stores.
     if (p.transposed) {
       const int l = tid & (B - 1);
-      constexpr int TS = kPipeThreads / B;
+      constexpr int TS = NT / B;
       constexpr int JT = (N + TS - 1) / TS;
       constexpr int JG = 8;
       if (l < nlv) {
@@ -860,12 +908,12 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
         const double* __restrict__ qrow = p.post ? p.post + rowb : nullptr;
         double y[kTpt];
 #pragma unroll
-        for (int k = 0; k < kTpt; ++k) y[k] = unpack(l, g[k], 1 + tid + k * kPipeThreads);
+        for (int k = 0; k < kTpt; ++k) y[k] = unpack(l, g[k], 1 + tid + k * NT);
         if (qrow) {
           double q[kTpt];
 #pragma unroll
           for (int k = 0; k < kTpt; ++k) {
-            const int t = 1 + tid + k * kPipeThreads;
+            const int t = 1 + tid + k * NT;
             q[k] = (k < kTpt - 1 || t <= N) ? qrow[t] : 1.0;
           }
 #pragma unroll
@@ -874,12 +922,12 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
         double dv[kTpt];
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
-          const int t = 1 + tid + k * kPipeThreads;
+          const int t = 1 + tid + k * NT;
           dv[k] = (drow && (k < kTpt - 1 || t <= N)) ? drow[t] : 0.0;
         }
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
-          const int t = 1 + tid + k * kPipeThreads;
+          const int t = 1 + tid + k * NT;
           if (k < kTpt - 1 || t <= N) {
             orow[t] = y[k];
             acc += y[k] * dv[k];
@@ -897,14 +945,16 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_dst_pipe(const
       if (p.dot_with) acc += y * p.dot_with[g];
     }
     __syncthreads();
+    PIPE_T(4);
   }
+  PIPE_T_FLUSH;
   if (p.partial) {
     const double s = block_sum(acc, red);
     if (tid == 0) p.partial[blockIdx.x] = s;
   }
 }
 
-template <int Q1, int Q2, int Q3>
+template <int Q1, int Q2, int Q3, int NT = 256, int MINB = 2, int TPW = 3>
 static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   using SH = PfaShape<Q1, Q2, Q3>;
   int reps = PfaStageC<SH, 0>::Rcnt;
@@ -915,19 +965,45 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          220 * 1024);
     attr = true;
   }
-  k_dst_pipe<Q1, Q2, Q3><<<grid, kPipeThreads, smem, st>>>(k);
+  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW><<<grid, NT, smem, st>>>(k);
   return cudaGetLastError();
+}
+
+// Launch shape per specialisation.  2047 = 89 * 23 runs one 12-warp CTA per SM (its
+// 6 k-tiles of the q = 89 stage split evenly over the warps and the register budget of
+// 170 keeps the DMMA chains unspilled); the smaller lengths run two 8-warp CTAs per SM.
+// TVD_PIPE_VARIANT overrides the 89 * 23 shape for experiments.
+struct PipeVariant {
+  int threads, ctas, tpw;
+};
+static int pipe_variant_id() {
+  static const int v = [] {
+    const char* s = getenv("TVD_PIPE_VARIANT");
+    return s ? atoi(s) : -1;
+  }();
+  return v;
+}
+static PipeVariant pipe_variant(int which) {
+  if (which != 1) return {256, 2, 3};
+  switch (pipe_variant_id()) {
+    case 0: return {256, 2, 3};
+    case 1: return {256, 1, 3};
+    case 2: return {384, 1, 3};
+    case 3: return {512, 1, 3};
+    default: return {384, 1, 4};
+  }
 }
 
 int pipe_grid(const PfaPlan& P, int nlines) {
   int which;
   if (!pfa_specialised(P, &which)) return -1;
   const int nbatch = (nlines + kPipeLines - 1) / kPipeLines;
-  return nbatch < kSMs * kPipeCtasPerSm ? nbatch : kSMs * kPipeCtasPerSm;
+  const int cap = kSMs * pipe_variant(which).ctas;
+  return nbatch < cap ? nbatch : cap;
 }
 
 cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int transposed,
@@ -960,7 +1036,14 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
   if (nblocks_out) *nblocks_out = grid;
   if (grid <= 0) return cudaSuccess;
   switch (which) {
-    case 1: return launch_pipe_t<89, 23, 1>(k, grid, st);
+    case 1:
+      switch (pipe_variant_id()) {
+        case 0: return launch_pipe_t<89, 23, 1, 256, 2, 3>(k, grid, st);
+        case 1: return launch_pipe_t<89, 23, 1, 256, 1, 3>(k, grid, st);
+        case 2: return launch_pipe_t<89, 23, 1, 384, 1, 3>(k, grid, st);
+        case 3: return launch_pipe_t<89, 23, 1, 512, 1, 3>(k, grid, st);
+        default: return launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
+      }
     case 2: return launch_pipe_t<31, 11, 3>(k, grid, st);
     case 3: return launch_pipe_t<73, 7, 1>(k, grid, st);
     case 4: return launch_pipe_t<127, 1, 1>(k, grid, st);
@@ -1064,3 +1147,20 @@ cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g,
 }
 
 }  // namespace tvd
+
+// profiling only: per-phase cycle sums of the pipeline kernel (-DTVD_PIPE_TIMING builds)
+extern "C" int tvd_debug_pipe_phases(unsigned long long* out8, int reset) {
+#ifdef TVD_PIPE_TIMING
+  if (out8 && cudaMemcpyFromSymbol(out8, tvd::g_pipe_phase, 8 * sizeof(unsigned long long)) != cudaSuccess)
+    return -1;
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(tvd::g_pipe_phase, z, sizeof(z));
+  }
+  return 0;
+#else
+  (void)out8;
+  (void)reset;
+  return -1;
+#endif
+}

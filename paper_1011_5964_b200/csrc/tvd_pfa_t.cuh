@@ -62,7 +62,7 @@ __device__ __forceinline__ void rep_ab(int t, int& a, int& b) {
 
 // fold + DFT of one stage.  `reps` holds (base | neg << 16) of every representative line
 // (line 0); line l adds l * LP.
-template <class ST, int NL, int MT = 4, int NW = 0>
+template <class ST, int NL, int MT = 4, int NW = 0, int TPWc = 3>
 __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
                                             const double* Cm, const double* Sm) {
   constexpr int kMmaTiles = MT;  // output tiles a warp holds across the in-place barrier
@@ -71,12 +71,16 @@ __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
   constexpr int ndft = NL * ST::Rcnt;
   if constexpr (ST::mma && NW > 0) {
     // A-stationary tensor-core stage: warp -> fixed k-tile (its cos/sin fragments for every
-    // r stay in registers) x a strided set of column tiles; the fold a/b is fused into the
-    // B-fragment load, so there is no separate fold sweep.
+    // r stay in registers) x TPW column tiles per round, sized so one round normally covers
+    // every tile.  The fold a/b is fused into the B-fragment load (no fold sweep).  The
+    // r-steps run outermost, so a warp keeps 2 TPW independent accumulator chains in flight
+    // and issues each step's loads together; padded r (> H) and clamped columns read
+    // in-range data against zero coefficients / dropped outputs, so nothing is predicated.
     constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;
-    constexpr int G = NW / nkt >= 1 ? NW / nkt : 1;      // warps sharing one k-tile
-    constexpr int TPW = 3;                                 // column tiles per warp per round
-    constexpr int ROUND = G * TPW;                         // column tiles per round
+    constexpr int G = NW / nkt >= 1 ? NW / nkt : 1;  // warps sharing one k-tile
+    constexpr int TPWn = (nct + G - 1) / G;          // tiles per warp for a single round
+    constexpr int TPW = TPWn < TPWc ? TPWn : TPWc;   // column tiles per warp per round
+    constexpr int ROUND = G * TPW;
     const int lane = tid & 31, warp = tid >> 5;
     const int kt = warp % nkt, g = warp / nkt;
     const bool wact = warp < nkt * G;
@@ -89,66 +93,87 @@ __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
     }
     const double* bufd = reinterpret_cast<const double*>(buf);
     for (int ct0 = 0; ct0 < nct; ct0 += ROUND) {
-    double2 vk[TPW], vm[TPW];
-    unsigned ob[TPW];
-    int oflag[TPW];
+      double acc[TPW][4];
+      const double* pb[TPW];
 #pragma unroll
-    for (int j = 0; j < TPW; ++j) {
-      oflag[j] = 0;
-      const int ct = ct0 + g + j * G;
-      if (wact && ct < nct) {
-        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-        const int colB = ct * 8 + (lane >> 2);
-        const int dB = colB >> 1;
-        const bool vB = dB < ndft;
-        const int lB = vB ? dB / ST::Rcnt : 0;
-        const int tB = vB ? dB - lB * ST::Rcnt : 0;
-        const double* pb = bufd + 2 * (lB * LP + (reps[tB] & 0xffffu)) + (colB & 1);
+      for (int j = 0; j < TPW; ++j) {
+        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+        const int ct = min(ct0 + g + j * G, nct - 1);
+        const int dB = min((ct * 8 + (lane >> 2)) >> 1, ndft - 1);
+        const int lB = dB / ST::Rcnt, tB = dB - lB * ST::Rcnt;
+        pb[j] = bufd + 2 * (lB * LP + (reps[tB] & 0xffffu)) + ((lane >> 2) & 1);
+      }
+#ifdef TVD_PIPE_TIMING
+      const long long tl0_ = clock64();
+#endif
+      if (wact) {
 #pragma unroll
         for (int rs = 0; rs < nrs; ++rs) {
           const int r = 1 + rs * 4 + (lane & 3);
-          double x1 = 0.0, x2 = 0.0;
-          if (vB && (rs * 4 + 4 <= H || r <= H)) {
-            x1 = pb[2 * r * st];
-            x2 = pb[2 * (q - r) * st];
+          double x1[TPW], x2[TPW];
+#pragma unroll
+          for (int j = 0; j < TPW; ++j) {
+            x1[j] = pb[j][2 * r * st];
+            x2[j] = pb[j][2 * (q - r) * st];
           }
-          dmma884(a0, a1, ca[rs], x1 + x2);
-          dmma884(b0, b1, sa[rs], x1 - x2);
+#pragma unroll
+          for (int j = 0; j < TPW; ++j) {
+            dmma884(acc[j][0], acc[j][1], ca[rs], x1[j] + x2[j]);
+            dmma884(acc[j][2], acc[j][3], sa[rs], x1[j] - x2[j]);
+          }
         }
+      }
+#ifdef TVD_PIPE_TIMING
+      if (tid == 0) {
+        // make the accumulators' completion part of the timed region
+        double z_ = 0.0;
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) z_ += acc[j][0] + acc[j][3];
+        if (z_ == 12345.678) buf[0].x = z_;
+        atomicAdd(&g_pipe_phase[q == 89 ? 5 : 6], (unsigned long long)(clock64() - tl0_));
+      }
+#endif
+      double2 vk[TPW], vm[TPW];
+      unsigned ob[TPW];
+      int oflag[TPW];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        oflag[j] = 0;
+        const int ct = ct0 + g + j * G;
         const int dO = ct * 4 + (lane & 3);
-        if (krow <= H && dO < ndft) {
+        if (wact && ct < nct && krow <= H && dO < ndft) {
           const int lO = dO / ST::Rcnt, tO = dO - lO * ST::Rcnt;
           const unsigned rp = reps[tO] + (unsigned)(lO * LP) * 0x10001u;
           const double2 x0 = buf[rp & 0xffffu];
+          const double a0 = acc[j][0], a1 = acc[j][1], b0 = acc[j][2], b1 = acc[j][3];
           vk[j] = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
           vm[j] = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
           ob[j] = rp;
           oflag[j] = 1 | (tO == 0 ? 2 : 0);
         }
       }
-    }
-    __syncthreads();
+      __syncthreads();
 #pragma unroll
-    for (int j = 0; j < TPW; ++j) {
-      if (oflag[j]) {
-        const int k = krow;
-        double2* p = buf + (ob[j] & 0xffffu);
-        double2* pn = buf + (ob[j] >> 16);
-        const bool self = oflag[j] & 2;
-        if (k == 0) {
-          p[0] = vk[j];
-          if (!self) pn[0] = make_double2(-vk[j].x, -vk[j].y);
-        } else {
-          p[k * st] = vk[j];
-          p[(q - k) * st] = vm[j];
-          if (!self) {
-            pn[(q - k) * st] = make_double2(-vk[j].x, -vk[j].y);
-            pn[k * st] = make_double2(-vm[j].x, -vm[j].y);
+      for (int j = 0; j < TPW; ++j) {
+        if (oflag[j]) {
+          const int k = krow;
+          double2* p = buf + (ob[j] & 0xffffu);
+          double2* pn = buf + (ob[j] >> 16);
+          const bool self = oflag[j] & 2;
+          if (k == 0) {
+            p[0] = vk[j];
+            if (!self) pn[0] = make_double2(-vk[j].x, -vk[j].y);
+          } else {
+            p[k * st] = vk[j];
+            p[(q - k) * st] = vm[j];
+            if (!self) {
+              pn[(q - k) * st] = make_double2(-vk[j].x, -vk[j].y);
+              pn[k * st] = make_double2(-vm[j].x, -vm[j].y);
+            }
           }
         }
       }
-    }
-    __syncthreads();
+      __syncthreads();
     }
     return;
   }

@@ -1,6 +1,6 @@
 """Attribute ncu per-SASS-instruction samples of one kernel to CUDA source lines.
 
-  python tools/sass_hot.py REPORT.ncu-rep KERNEL_SUBSTR [METRIC ...]
+  python tools/sass_hot.py REPORT.ncu-rep KERNEL_SUBSTR[@LAUNCH] [METRIC ...]
 
 Reads `ncu --page source --print-source sass`, disassembles the same kernel from
 the in-tree .so with `nvdisasm -g` (line info from -lineinfo), and prints the
@@ -20,7 +20,7 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 SO = ROOT / "paper_1011_5964_b200" / "libtvdeblur_b200.so"
 
 
-def sass_rows(rep, kname):
+def sass_rows(rep, kname, which=0):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -33,9 +33,9 @@ def sass_rows(rep, kname):
             cur["hdr"] = r
         elif cur is not None and r and r[0].startswith("0x"):
             cur["rows"].append(r)
-    for b in blocks:
-        if kname in b["name"]:
-            return b
+    hits = [b for b in blocks if kname in b["name"]]
+    if len(hits) > which:
+        return hits[which]
     raise SystemExit(f"kernel {kname} not in report")
 
 
@@ -70,9 +70,13 @@ def line_map(kname):
 
 def main():
     rep, kname = sys.argv[1], sys.argv[2]
+    which = 0
+    if "@" in kname:
+        kname, w = kname.rsplit("@", 1)
+        which = int(w)
     metrics = sys.argv[3:] or ["Warp Stall Sampling (All Samples)", "stall_long_sb", "stall_barrier",
                                "stall_short_sb", "stall_wait"]
-    b = sass_rows(rep, kname)
+    b = sass_rows(rep, kname, which)
     hdr, rows = b["hdr"], b["rows"]
     base = int(rows[0][0], 16)
     lm = line_map(kname)
