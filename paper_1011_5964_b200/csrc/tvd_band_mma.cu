@@ -1,0 +1,311 @@
+// Banded 1D operator passes on the fp64 tensor cores (mma.sync m8n8k4 f64, SASS DMMA.884).
+//
+//   row pass     out[i][j] = sum_c B[j][c] in[i][c]        (GEMM  in * B^T)
+//   column pass  out[i][j] = sum_r B[i][r] in[r][j] (+ fused normal-equation epilogue)
+//
+// B is the banded operator of tvd_stencil.h (half-width w, Toeplitz with symmetric taps in
+// the interior, border rows from the table).  A warp owns T = 8 output tiles of 8 x 8 that
+// are consecutive along the band direction.  For tile t and k-step s (4 input positions,
+// starting KOFF = roundup(w, 4) before the tile) the operator fragment of a lane is
+// B[o][o + d] with d = 4s - KOFF + (lane & 3) - (lane >> 2): it does not depend on the tile
+// in the Toeplitz interior, so the CTA stages it once in shared memory, and the data
+// fragment of (t, s) is data fragment 2t + s, so a warp issues 8 S DMMAs from
+// S + 2 (T - 1) data-fragment loads (S = 2 + KOFF / 2).  Tiles that touch the first or
+// last op.B outputs read their operator fragments from the border table.
+//
+// Reference semantics: H^T H p = G p G^T with G = H1^T H1 (src/pipeline.py:209-210,
+// src/blur.py:197-326); the epilogue is tv.py:96-108 (L w) and pipeline.py:129-164 (s).
+#include <cstdlib>
+
+#include "tvd_stencil.h"
+
+namespace tvd {
+namespace {
+
+constexpr int kBmT = 8;  // output tiles per warp along the band direction
+
+__device__ __forceinline__ void bmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool ok) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src),
+               "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ void cp_commit_wait() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+struct BandTaps {
+  double t[64];  // t[k] = symmetric interior tap at offset +-k
+};
+
+__device__ __forceinline__ double coef_interior(const BandTaps& tp, int w, int d) {
+  const int a = d < 0 ? -d : d;
+  return a <= w ? tp.t[a] : 0.0;
+}
+// B[o][c] from the border table (0 outside the band or the image)
+__device__ __forceinline__ double coef_table(const BandOp& op, int o, int c) {
+  const int d = c - o;
+  if (o >= op.n || c < 0 || c >= op.n || d < -op.w || d > op.w) return 0.0;
+  return __ldg(op.table + (long)o * (2 * op.w + 1) + d + op.w);
+}
+
+template <int KOFF>
+struct BmShape {
+  static constexpr int S = 2 + KOFF / 2;  // k-steps per tile
+  static constexpr int NA = S + 2 * (kBmT - 1);
+  // row pass: 2 row blocks x 4 column strips of 8 T outputs
+  static constexpr int RH = 16, CW = 32 * kBmT, WIDTH = CW + 2 * KOFF;
+  static constexpr int RP = WIDTH + ((4 - WIDTH % 16) + 16) % 16;  // pitch = 4 (mod 16)
+  // column pass: 4 row strips of 8 T outputs x 2 column tiles
+  static constexpr int RW = 32 * kBmT, CC = 16, HEIGHT = RW + 2 * KOFF;
+  static constexpr int CP = 24;  // pitch = 8 (mod 16): 4 rows x 8 columns in 2 wavefronts
+  static size_t rows_smem() { return (size_t)(RH * RP + S * 32) * sizeof(double); }
+  static size_t cols_smem() { return (size_t)(HEIGHT * CP + S * 32) * sizeof(double); }
+};
+
+template <int KOFF>
+__device__ __forceinline__ void stage_fragments(double* fr, const BandTaps& tp, int w) {
+  constexpr int S = BmShape<KOFF>::S;
+  for (int e = threadIdx.x; e < S * 32; e += blockDim.x) {
+    const int s = e >> 5, l = e & 31;
+    fr[e] = coef_interior(tp, w, 4 * s - KOFF + (l & 3) - (l >> 2));
+  }
+}
+
+template <int KOFF>
+__global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
+                                                     const double* __restrict__ in,
+                                                     double* __restrict__ out, const int* skip) {
+  if (skip && *skip) return;
+  using SH = BmShape<KOFF>;
+  constexpr int T = kBmT, S = SH::S, RP = SH::RP, W2 = SH::WIDTH / 2;
+  extern __shared__ __align__(16) double smb[];
+  double* tile = smb;
+  double* fr = smb + SH::RH * RP;
+  const int n = op.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i0 = blockIdx.y * SH::RH, jb = blockIdx.x * SH::CW;
+  for (int e = tid; e < SH::RH * W2; e += blockDim.x) {
+    const int r = e / W2, c = 2 * (e - r * W2);
+    const int row = i0 + r, col = jb - KOFF + c;
+    const bool ok = row < n && col >= 0 && col < n;
+    cp16(tile + r * RP + c, ok ? in + (long)row * n + col : in, ok);
+  }
+  stage_fragments<KOFF>(fr, tp, op.w);
+  cp_commit_wait();
+  __syncthreads();
+  const int rb = warp >> 2, cs = warp & 3;
+  const int o0 = jb + cs * 8 * T;  // first output column of the warp
+  const double* arow = tile + (rb * 8 + (lane >> 2)) * RP + cs * 8 * T + (lane & 3);
+  double acc[T][2];
+#pragma unroll
+  for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
+  if (o0 >= op.B && o0 + 8 * T <= n - op.B) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const double b = fr[s * 32 + lane];
+#pragma unroll
+      for (int t = 0; t < T; ++t) bmma(acc[t][0], acc[t][1], arow[4 * (2 * t + s)], b);
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int oc = o0 + 8 * t;
+      const bool tb = oc < op.B || oc + 8 > n - op.B;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const double b = tb ? coef_table(op, oc + (lane >> 2), oc - KOFF + 4 * s + (lane & 3))
+                            : fr[s * 32 + lane];
+        bmma(acc[t][0], acc[t][1], arow[4 * (2 * t + s)], b);
+      }
+    }
+  }
+  const int row = i0 + rb * 8 + (lane >> 2);
+  if (row < n) {
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int col = o0 + 8 * t + 2 * (lane & 3);
+      if (col < n)
+        *reinterpret_cast<double2*>(out + (long)row * n + col) = make_double2(acc[t][0], acc[t][1]);
+    }
+  }
+}
+
+template <int KOFF>
+__global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
+                                                     const double* __restrict__ in,
+                                                     double* __restrict__ out, Epilogue ep,
+                                                     const int* skip) {
+  if (skip && *skip) return;
+  using SH = BmShape<KOFF>;
+  constexpr int T = kBmT, S = SH::S, CP = SH::CP, C2 = SH::CC / 2;
+  extern __shared__ __align__(16) double smb[];
+  __shared__ double red[32];
+  double* tile = smb;
+  double* fr = smb + SH::HEIGHT * CP;
+  const int n = op.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ib = blockIdx.y * SH::RW, j0 = blockIdx.x * SH::CC;
+  for (int e = tid; e < SH::HEIGHT * C2; e += blockDim.x) {
+    const int r = e / C2, c = 2 * (e - r * C2);
+    const int row = ib - KOFF + r, col = j0 + c;
+    const bool ok = row >= 0 && row < n && col < n;
+    cp16(tile + r * CP + c, ok ? in + (long)row * n + col : in, ok);
+  }
+  stage_fragments<KOFF>(fr, tp, op.w);
+  cp_commit_wait();
+  __syncthreads();
+  const int rs = warp >> 1, ct = warp & 1;
+  const int o0 = ib + rs * 8 * T;  // first output row of the warp
+  const double* bcol = tile + (rs * 8 * T + (lane & 3)) * CP + ct * 8 + (lane >> 2);
+  double acc[T][2];
+#pragma unroll
+  for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
+  if (o0 >= op.B && o0 + 8 * T <= n - op.B) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const double a = fr[s * 32 + lane];
+#pragma unroll
+      for (int t = 0; t < T; ++t) bmma(acc[t][0], acc[t][1], a, bcol[4 * (2 * t + s) * CP]);
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int oc = o0 + 8 * t;
+      const bool tb = oc < op.B || oc + 8 > n - op.B;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const double a = tb ? coef_table(op, oc + (lane >> 2), oc - KOFF + 4 * s + (lane & 3))
+                            : fr[s * 32 + lane];
+        bmma(acc[t][0], acc[t][1], a, bcol[4 * (2 * t + s) * CP]);
+      }
+    }
+  }
+  // epilogue: q = [s *] (acc + alpha L(lw)), dot += dot_with . q (tv.py:96-108, pipeline.py:129-164)
+  const double* __restrict__ a_h = ep.a_h;
+  const double* __restrict__ a_v = ep.a_v;
+  const double* __restrict__ lw = ep.lw;
+  const double* __restrict__ sv = ep.s;
+  const double* __restrict__ dw = ep.dot_with;
+  const int col = j0 + ct * 8 + 2 * (lane & 3);
+  double dot = 0.0;
+  if (col < n) {
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int i = o0 + 8 * t + (lane >> 2);
+      if (i < n) {
+        const long g = (long)i * n + col;
+        double v[2], d[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double x = acc[t][e];
+          if (a_h) x = x + ep.alpha * diffusion_at(a_h, a_v, lw, n, i, col + e, ep.inv_h2);
+          if (sv) x = sv[g + e] * x;
+          v[e] = x;
+          d[e] = dw ? dw[g + e] : 0.0;
+        }
+        *reinterpret_cast<double2*>(out + g) = make_double2(v[0], v[1]);
+        dot += d[0] * v[0];
+        dot += d[1] * v[1];
+      }
+    }
+  }
+  if (ep.partial) {
+    const double s = block_sum(dot, red);
+    if (tid == 0) ep.partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+bool make_taps(const BandOp& op, BandTaps* tp) {
+  if (!op.taps_host || op.w > 63) return false;
+  for (int k = 0; k <= op.w; ++k) tp->t[k] = op.taps_host[op.w + k];
+  return true;
+}
+
+int koff_of(int w) {
+  const int k = (w + 3) / 4 * 4;
+  switch (k) {
+    case 4: case 8: case 12: case 16: case 20: case 24: case 28: case 32: return k;
+    default: return w > 32 && w <= 64 ? 64 : 0;
+  }
+}
+
+bool band_mma_enabled() {
+  static const bool on = [] {
+    const char* s = getenv("TVD_BAND_IMPL");
+    return !(s && s[0] == 's');  // "slide" selects the CUDA-core kernels (comparison runs)
+  }();
+  return on;
+}
+
+#define TVD_KOFFS(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32) X(64)
+
+}  // namespace
+
+// Tiles are 256 outputs long along the band direction, so small grids keep the CUDA-core
+// kernels (whose summation order the small-n iteration-count goldens were pinned with).
+constexpr int kBandMmaMinN = 256;
+
+bool band_mma_ok(const BandOp& op) {
+  return band_mma_enabled() && op.n >= kBandMmaMinN && (op.n % 2) == 0 && op.taps_host &&
+         koff_of(op.w) != 0;
+}
+
+int band_mma_cols_grid(int n) {
+  return ((n + 15) / 16) * ((n + 32 * kBmT - 1) / (32 * kBmT));
+}
+
+cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out, const int* skip,
+                                 cudaStream_t st) {
+  BandTaps tp;
+  if (!make_taps(op, &tp)) return cudaErrorInvalidValue;
+  const int n = op.n;
+  switch (koff_of(op.w)) {
+#define X(K)                                                                                 \
+  case K: {                                                                                  \
+    using SH = BmShape<K>;                                                                   \
+    static bool attr = false;                                                                \
+    if (!attr) {                                                                             \
+      cudaFuncSetAttribute(k_bmma_rows<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                           (int)SH::rows_smem());                                            \
+      attr = true;                                                                           \
+    }                                                                                        \
+    dim3 grid((n + SH::CW - 1) / SH::CW, (n + SH::RH - 1) / SH::RH);                         \
+    k_bmma_rows<K><<<grid, 256, SH::rows_smem(), st>>>(op, tp, in, out, skip);               \
+    return cudaGetLastError();                                                               \
+  }
+    TVD_KOFFS(X)
+#undef X
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out,
+                                 const Epilogue& ep, const int* skip, cudaStream_t st) {
+  BandTaps tp;
+  if (!make_taps(op, &tp)) return cudaErrorInvalidValue;
+  const int n = op.n;
+  switch (koff_of(op.w)) {
+#define X(K)                                                                                 \
+  case K: {                                                                                  \
+    using SH = BmShape<K>;                                                                   \
+    static bool attr = false;                                                                \
+    if (!attr) {                                                                             \
+      cudaFuncSetAttribute(k_bmma_cols<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                           (int)SH::cols_smem());                                            \
+      attr = true;                                                                           \
+    }                                                                                        \
+    dim3 grid((n + SH::CC - 1) / SH::CC, (n + SH::RW - 1) / SH::RW);                         \
+    k_bmma_cols<K><<<grid, 256, SH::cols_smem(), st>>>(op, tp, in, out, ep, skip);           \
+    return cudaGetLastError();                                                               \
+  }
+    TVD_KOFFS(X)
+#undef X
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace tvd

@@ -402,6 +402,7 @@ int band_rows_blocks(int n) { return ((n + kRowTileC - 1) / kRowTileC) * ((n + k
 
 int band_cols_grid(const BandOp& op) {
   const int n = op.n;
+  if (band_mma_ok(op)) return band_mma_cols_grid(n);
   bool slide = false;
   if (op.taps_host && op.w <= 63) {
     switch (op.w) {
@@ -420,11 +421,13 @@ int band_cols_grid(const BandOp& op) {
 int band_cols_blocks(int n) {
   const int a = ((n + kColTileC - 1) / kColTileC) * ((n + kColTileR - 1) / kColTileR);
   const int b = ((n + 31) / 32) * ((n + kSlideW * kSlideSpan - 1) / (kSlideW * kSlideSpan));
-  return a > b ? a : b;
+  const int c = band_mma_cols_grid(n);
+  return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 
 cudaError_t launch_band_rows(const BandOp& op, const double* in, double* out, const int* skip,
                              cudaStream_t st) {
+  if (band_mma_ok(op)) return launch_band_mma_rows(op, in, out, skip, st);
   bool done;
   cudaError_t e = launch_slide_rows(op, in, out, skip, st, &done);
   if (done || e != cudaSuccess) return e;
@@ -442,6 +445,7 @@ cudaError_t launch_band_rows(const BandOp& op, const double* in, double* out, co
 
 cudaError_t launch_band_cols(const BandOp& op, const double* in, double* out, const Epilogue& ep,
                              const int* skip, cudaStream_t st) {
+  if (band_mma_ok(op)) return launch_band_mma_cols(op, in, out, ep, skip, st);
   bool done;
   cudaError_t e = launch_slide_cols(op, in, out, ep, skip, st, &done);
   if (done || e != cudaSuccess) return e;

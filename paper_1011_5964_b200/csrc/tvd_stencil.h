@@ -46,6 +46,14 @@ __device__ __forceinline__ double diffusion_at(const double* __restrict__ a_h,
   return __dmul_rn(-inv_h2, __dadd_rn(__dsub_rn(fr, fl), __dsub_rn(fd, fu)));
 }
 
+// tensor-core (DMMA) band passes, tvd_band_mma.cu; used when band_mma_ok(op)
+bool band_mma_ok(const BandOp& op);
+int band_mma_cols_grid(int n);
+cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out, const int* skip,
+                                 cudaStream_t st);
+cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out,
+                                 const Epilogue& ep, const int* skip, cudaStream_t st);
+
 int band_rows_blocks(int n);
 int band_cols_blocks(int n);          // upper bound over both column-pass variants
 int band_cols_grid(const BandOp& op);  // exact grid of launch_band_cols for this operator

@@ -131,6 +131,28 @@ def test_blur_vs_oracle_midsize(n, m, bname, rng):
     assert rel_err(op.apply_transpose(u), O.blur_transpose(u, h, bname)) < 1e-12
 
 
+@pytest.mark.parametrize("n,m,bname", [(256, 7, "anti_reflective"), (512, 15, "reflective"),
+                                       (1024, 10, "anti_reflective"), (768, 31, "anti_reflective")])
+def test_normal_system_vs_oracle_midsize(n, m, bname, rng):
+    """Fused H^T H + alpha L matvec (tensor-core band passes at these sizes), plain and X_D-scaled."""
+    from paper_1011_5964_b200.harness import gen_psf
+    from paper_1011_5964_b200.pipeline import NormalSystem
+    h = gen_psf("gaussian", m, m / 2.0)
+    u = np.cumsum(rng.standard_normal((n, n)), axis=1) * 0.05
+    w = rng.standard_normal((n, n))
+    alpha, beta = 2e-3, 0.05
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(h), BCS[bname], n)
+    lop = TV.DiffusionOperator(u, beta)
+    back = O.blur_transpose if bname == "anti_reflective" else O.blur
+    want = back(O.blur(w, h, bname), h, bname) + alpha * O.diffusion_apply(lop.a_h, lop.a_v, w)
+    assert rel_err(NormalSystem(hop, lop, alpha)(w), want) < 1e-12
+    s = rng.uniform(0.5, 1.5, (n, n))
+    st = torch.from_numpy(s).cuda()
+    want_s = s * (back(O.blur(s * w, h, bname), h, bname)
+                  + alpha * O.diffusion_apply(lop.a_h, lop.a_v, s * w))
+    assert rel_err(NormalSystem(hop, lop, alpha, s=st)(w), want_s) < 1e-12
+
+
 @pytest.mark.parametrize("n", [2048])
 def test_full_size_blur_adjointness_and_linearity(n, rng):
     from paper_1011_5964_b200.harness import gen_psf
