@@ -47,17 +47,17 @@ __device__ __forceinline__ double coef_interior(const BandTaps& tp, int w, int d
   const int a = d < 0 ? -d : d;
   return a <= w ? tp.t[a] : 0.0;
 }
-// B[o][c] from the border table (0 outside the band or the image)
-__device__ __forceinline__ double coef_table(const BandOp& op, int o, int c) {
-  const int d = c - o;
-  if (o >= op.n || c < 0 || c >= op.n || d < -op.w || d > op.w) return 0.0;
-  return __ldg(op.table + (long)o * (2 * op.w + 1) + d + op.w);
+// operator fragment of border tile p (host-built, tvd_capi.cu make_bandop)
+__device__ __forceinline__ const double* border_frag(const BandOp& op, int p, int S) {
+  const int np = (op.n + 7) / 8;
+  const int idx = p < op.frag_l ? p : (p >= op.frag_r0 && p < np ? op.frag_l + p - op.frag_r0
+                                                                  : op.frag_cnt);
+  return op.frag + (size_t)idx * S * 32;
 }
 
 template <int KOFF>
 struct BmShape {
   static constexpr int S = 2 + KOFF / 2;  // k-steps per tile
-  static constexpr int NA = S + 2 * (kBmT - 1);
   // row pass: 2 row blocks x 4 column strips of 8 T outputs
   static constexpr int RH = 16, CW = 32 * kBmT, WIDTH = CW + 2 * KOFF;
   static constexpr int RP = WIDTH + ((4 - WIDTH % 16) + 16) % 16;  // pitch = 4 (mod 16)
@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
   double acc[T][2];
 #pragma unroll
   for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
-  if (o0 >= op.B && o0 + 8 * T <= n - op.B) {
+  const int p0 = o0 >> 3;  // first 8-output tile of the warp
+  if (p0 >= op.frag_l && p0 + T <= op.frag_r0) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const double b = fr[s * 32 + lane];
@@ -114,14 +115,11 @@ __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
   } else {
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      const int oc = o0 + 8 * t;
-      const bool tb = oc < op.B || oc + 8 > n - op.B;
+      const int p = p0 + t;
+      const double* bf = (p < op.frag_l || p >= op.frag_r0) ? border_frag(op, p, S) + lane
+                                                            : fr + lane;
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const double b = tb ? coef_table(op, oc + (lane >> 2), oc - KOFF + 4 * s + (lane & 3))
-                            : fr[s * 32 + lane];
-        bmma(acc[t][0], acc[t][1], arow[4 * (2 * t + s)], b);
-      }
+      for (int s = 0; s < S; ++s) bmma(acc[t][0], acc[t][1], arow[4 * (2 * t + s)], bf[s * 32]);
     }
   }
   const int row = i0 + rb * 8 + (lane >> 2);
@@ -164,7 +162,8 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
   double acc[T][2];
 #pragma unroll
   for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
-  if (o0 >= op.B && o0 + 8 * T <= n - op.B) {
+  const int p0 = o0 >> 3;  // first 8-output tile of the warp
+  if (p0 >= op.frag_l && p0 + T <= op.frag_r0) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const double a = fr[s * 32 + lane];
@@ -174,14 +173,11 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
   } else {
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      const int oc = o0 + 8 * t;
-      const bool tb = oc < op.B || oc + 8 > n - op.B;
+      const int p = p0 + t;
+      const double* af = (p < op.frag_l || p >= op.frag_r0) ? border_frag(op, p, S) + lane
+                                                            : fr + lane;
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const double a = tb ? coef_table(op, oc + (lane >> 2), oc - KOFF + 4 * s + (lane & 3))
-                            : fr[s * 32 + lane];
-        bmma(acc[t][0], acc[t][1], a, bcol[4 * (2 * t + s) * CP]);
-      }
+      for (int s = 0; s < S; ++s) bmma(acc[t][0], acc[t][1], af[s * 32], bcol[4 * (2 * t + s) * CP]);
     }
   }
   // epilogue: q = [s *] (acc + alpha L(lw)), dot += dot_with . q (tv.py:96-108, pipeline.py:129-164)
@@ -251,8 +247,10 @@ constexpr int kBandMmaMinN = 256;
 
 bool band_mma_ok(const BandOp& op) {
   return band_mma_enabled() && op.n >= kBandMmaMinN && (op.n % 2) == 0 && op.taps_host &&
-         koff_of(op.w) != 0;
+         op.frag && koff_of(op.w) != 0;
 }
+
+int band_mma_koff(int w) { return koff_of(w); }
 
 int band_mma_cols_grid(int n) {
   return ((n + 15) / 16) * ((n + 32 * kBmT - 1) / (32 * kBmT));

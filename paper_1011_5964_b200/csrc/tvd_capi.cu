@@ -672,6 +672,34 @@ static int make_bandop(tvd_blur* b, const Taps1D& t, int border, BandOp* op) {
   op->table = dtab;
   b->host_taps.push_back(taps);
   op->taps_host = b->host_taps.back().data();
+  // border-tile operator fragments of the tensor-core band passes:
+  // lane l of step s of tile p holds B[o][c], o = 8p + l / 4, c = 8p - koff + 4s + l % 4
+  op->frag = nullptr;
+  op->frag_l = op->frag_r0 = op->frag_cnt = 0;
+  const int koff = band_mma_koff(t.w);
+  if (koff > 0 && n >= 16) {
+    const int S = 2 + koff / 2, np = (n + 7) / 8;
+    const int L = std::min(np, (B + 7) / 8);
+    const int r0 = std::max(L, n - B - 8 >= 0 ? (n - B - 8) / 8 + 1 : 0);
+    const int cnt = L + (np - r0);
+    std::vector<double> fr((size_t)(cnt + 1) * S * 32, 0.0);  // + trailing zero block
+    for (int idx = 0; idx < cnt; ++idx) {
+      const int p = idx < L ? idx : r0 + (idx - L);
+      for (int s = 0; s < S; ++s)
+        for (int l = 0; l < 32; ++l) {
+          const int o = 8 * p + l / 4, cc = 8 * p - koff + 4 * s + l % 4, d = cc - o;
+          if (o < n && cc >= 0 && cc < n && d >= -t.w && d <= t.w)
+            fr[((size_t)idx * S + s) * 32 + l] = t.table[(size_t)o * W + d + t.w];
+        }
+    }
+    double* dfr;
+    if (upload(fr, &dfr, b->owned) != cudaSuccess)
+      return fail(TVD_ERR_CUDA, "band fragment upload failed");
+    op->frag = dfr;
+    op->frag_l = L;
+    op->frag_r0 = r0;
+    op->frag_cnt = cnt;
+  }
   return TVD_OK;
 }
 

@@ -12,6 +12,11 @@ struct BandOp {
   const double* taps;       // 2w+1 (device)
   const double* table;      // n x (2w+1), table[i*(2w+1) + k + w] = B[i][i+k] (device)
   const double* taps_host;  // 2w+1 (host copy; becomes kernel-parameter constants)
+  // Operator fragments of the border tiles for the tensor-core passes (tvd_band_mma.cu):
+  // 8-output tile p < frag_l is block p, frag_r0 <= p < ceil(n/8) is block frag_l + p -
+  // frag_r0, anything else the trailing zero block; block layout [S][32 lanes].
+  const double* frag;
+  int frag_l, frag_r0, frag_cnt;
 };
 
 // Epilogue of the normal-equation column pass:
@@ -48,6 +53,7 @@ __device__ __forceinline__ double diffusion_at(const double* __restrict__ a_h,
 
 // tensor-core (DMMA) band passes, tvd_band_mma.cu; used when band_mma_ok(op)
 bool band_mma_ok(const BandOp& op);
+int band_mma_koff(int w);  // k-offset of the tensor-core passes for half-width w (0: none)
 int band_mma_cols_grid(int n);
 cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out, const int* skip,
                                  cudaStream_t st);
