@@ -180,32 +180,74 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
       for (int s = 0; s < S; ++s) bmma(acc[t][0], acc[t][1], af[s * 32], bcol[4 * (2 * t + s) * CP]);
     }
   }
-  // epilogue: q = [s *] (acc + alpha L(lw)), dot += dot_with . q (tv.py:96-108, pipeline.py:129-164)
+  // epilogue: q = [s *] (acc + alpha L(lw)), dot += dot_with . q (tv.py:96-108, pipeline.py:129-164).
+  // Each lane owns the column pair (col, col + 1) of its T row tiles.  The zero-Neumann ghosts
+  // are clamped indices rather than branches, so all operands of a group of TG tiles are in
+  // flight before the first is used; per element the arithmetic is diffusion_at's, unfused.
   const double* __restrict__ a_h = ep.a_h;
   const double* __restrict__ a_v = ep.a_v;
   const double* __restrict__ lw = ep.lw;
   const double* __restrict__ sv = ep.s;
   const double* __restrict__ dw = ep.dot_with;
   const int col = j0 + ct * 8 + 2 * (lane & 3);
+  const int cl = col > 0 ? col - 1 : 0, cr = col + 2 < n ? col + 2 : n - 1;
+  auto ld2 = [](const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); };
+  constexpr int TG = 2;
   double dot = 0.0;
   if (col < n) {
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int i = o0 + 8 * t + (lane >> 2);
-      if (i < n) {
-        const long g = (long)i * n + col;
-        double v[2], d[2];
+    for (int t0 = 0; t0 < T; t0 += TG) {
+      double2 wc[TG], wu[TG], wd[TG], vu[TG], vd[TG], s2[TG], d2[TG];
+      double wl[TG], wr[TG], h0[TG], h1[TG], h2[TG];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double x = acc[t][e];
-          if (a_h) x = x + ep.alpha * diffusion_at(a_h, a_v, lw, n, i, col + e, ep.inv_h2);
-          if (sv) x = sv[g + e] * x;
-          v[e] = x;
-          d[e] = dw ? dw[g + e] : 0.0;
+      for (int k = 0; k < TG; ++k) {
+        const int i = min(o0 + 8 * (t0 + k) + (lane >> 2), n - 1);
+        const int iu = i > 0 ? i - 1 : 0, id = i < n - 1 ? i + 1 : n - 1;
+        const long r = (long)i * n;
+        if (a_h) {
+          wc[k] = ld2(lw + r + col);
+          wl[k] = __ldg(lw + r + cl);
+          wr[k] = __ldg(lw + r + cr);
+          wu[k] = ld2(lw + (long)iu * n + col);
+          wd[k] = ld2(lw + (long)id * n + col);
+          const long hb = (long)i * (n + 1) + col;
+          h0[k] = __ldg(a_h + hb);
+          h1[k] = __ldg(a_h + hb + 1);
+          h2[k] = __ldg(a_h + hb + 2);
+          vu[k] = ld2(a_v + r + col);
+          vd[k] = ld2(a_v + r + n + col);
         }
-        *reinterpret_cast<double2*>(out + g) = make_double2(v[0], v[1]);
-        dot += d[0] * v[0];
-        dot += d[1] * v[1];
+        if (sv) s2[k] = ld2(sv + r + col);
+        if (dw) d2[k] = ld2(dw + r + col);
+      }
+#pragma unroll
+      for (int k = 0; k < TG; ++k) {
+        const int i = o0 + 8 * (t0 + k) + (lane >> 2);
+        if (i >= n) continue;
+        double x0 = acc[t0 + k][0], x1 = acc[t0 + k][1];
+        if (a_h) {
+          const double fl0 = __dmul_rn(h0[k], __dsub_rn(wc[k].x, wl[k]));
+          const double fr0 = __dmul_rn(h1[k], __dsub_rn(wc[k].y, wc[k].x));
+          const double fu0 = __dmul_rn(vu[k].x, __dsub_rn(wc[k].x, wu[k].x));
+          const double fd0 = __dmul_rn(vd[k].x, __dsub_rn(wd[k].x, wc[k].x));
+          const double fl1 = fr0;  // same edge: a_h[h0 + 1] * (w[col + 1] - w[col])
+          const double fr1 = __dmul_rn(h2[k], __dsub_rn(wr[k], wc[k].y));
+          const double fu1 = __dmul_rn(vu[k].y, __dsub_rn(wc[k].y, wu[k].y));
+          const double fd1 = __dmul_rn(vd[k].y, __dsub_rn(wd[k].y, wc[k].y));
+          const double l0 = __dmul_rn(-ep.inv_h2, __dadd_rn(__dsub_rn(fr0, fl0), __dsub_rn(fd0, fu0)));
+          const double l1 = __dmul_rn(-ep.inv_h2, __dadd_rn(__dsub_rn(fr1, fl1), __dsub_rn(fd1, fu1)));
+          x0 = __dadd_rn(x0, __dmul_rn(ep.alpha, l0));
+          x1 = __dadd_rn(x1, __dmul_rn(ep.alpha, l1));
+        }
+        if (sv) {
+          x0 = __dmul_rn(s2[k].x, x0);
+          x1 = __dmul_rn(s2[k].y, x1);
+        }
+        *reinterpret_cast<double2*>(out + (long)i * n + col) = make_double2(x0, x1);
+        if (dw) {
+          dot += d2[k].x * x0;
+          dot += d2[k].y * x1;
+        }
       }
     }
   }
