@@ -442,7 +442,8 @@ __global__ void __launch_bounds__(256, 2) k_pfa(const PfaK p) {
 
 // ------------------------------------------------ compile-time specialised kernel
 #ifdef TVD_PIPE_TIMING
-__device__ unsigned long long g_pipe_phase[8];  // profiling only
+__device__ unsigned long long g_pipe_phase[8];      // profiling only
+__device__ unsigned long long g_stage_t[2 * 16 * 4];  // [stage q=89|other][warp][phase]
 #endif
 #include "tvd_pfa_t.cuh"
 
@@ -453,13 +454,13 @@ __device__ __forceinline__ void pfa_transform_c(double2* buf, unsigned* const* r
                                                 const PfaPlan& pl, int stages) {
   using SH = PfaShape<Q1, Q2, Q3>;
   if (stages >= 1)
-    pfa_stage_c<PfaStageC<SH, 0>, kPfaLinesT, 4, 8>(buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
+    pfa_stage_c<PfaStageC<SH, 0>, kPfaLinesT, 4, 8>(buf, buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
   if constexpr (SH::d >= 2)
     if (stages >= 2)
-      pfa_stage_c<PfaStageC<SH, 1>, kPfaLinesT, 4, 8>(buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
+      pfa_stage_c<PfaStageC<SH, 1>, kPfaLinesT, 4, 8>(buf, buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
   if constexpr (SH::d >= 3)
     if (stages >= 3)
-      pfa_stage_c<PfaStageC<SH, 2>, kPfaLinesT, 4, 8>(buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
+      pfa_stage_c<PfaStageC<SH, 2>, kPfaLinesT, 4, 8>(buf, buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
 }
 
 template <int Q1, int Q2, int Q3>
@@ -669,19 +670,31 @@ __device__ __forceinline__ void fence_proxy_async() {
   } while (0)
 #endif
 
+// PFA of the pipeline kernel.  kPipeOOP runs the stages out of place over two line
+// buffers (stage 0 reads `a`, writes `b`, then they swap: one barrier per stage, no
+// outputs held across barriers) -- measured no faster than in place on B200 at 2047, so
+// off.  Returns the buffer holding the result.
+constexpr bool kPipeOOP = false;
+
 template <int Q1, int Q2, int Q3, int NL, int NT, int TPW>
-__device__ __forceinline__ void pfa_transform_nl(double2* buf, unsigned* const* reps,
-                                                 const PfaPlan& pl, int stages = 3) {
+__device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, unsigned* const* reps,
+                                                     const PfaPlan& pl, int stages = 3) {
   using SH = PfaShape<Q1, Q2, Q3>;
   constexpr int NW = NT / 32;
-  if (stages >= 1)
-    pfa_stage_c<PfaStageC<SH, 0>, NL, 4, NW, TPW>(buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
-  if constexpr (SH::d >= 2)
-    if (stages >= 2)
-      pfa_stage_c<PfaStageC<SH, 1>, NL, 4, NW, TPW>(buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
-  if constexpr (SH::d >= 3)
-    if (stages >= 3)
-      pfa_stage_c<PfaStageC<SH, 2>, NL, 4, NW, TPW>(buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
+  constexpr bool O = kPipeOOP;
+  double2* x = a;
+  double2* y = O ? b : a;
+  if (stages < 1) return a;
+  pfa_stage_c<PfaStageC<SH, 0>, NL, 4, NW, TPW, O>(x, y, reps[0], pl.st[0].Cm, pl.st[0].Sm);
+  if constexpr (SH::d >= 2) {
+    if (stages < 2) return y;
+    pfa_stage_c<PfaStageC<SH, 1>, NL, 4, NW, TPW, O>(y, x, reps[1], pl.st[1].Cm, pl.st[1].Sm);
+  }
+  if constexpr (SH::d >= 3) {
+    if (stages < 3) return x;
+    pfa_stage_c<PfaStageC<SH, 2>, NL, 4, NW, TPW, O>(x, y, reps[2], pl.st[2].Cm, pl.st[2].Sm);
+  }
+  return SH::d == 2 ? x : y;
 }
 
 template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW>
@@ -696,8 +709,10 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   __shared__ double bord[B][2];
   __shared__ __align__(8) unsigned long long mbar;
   const int tid = threadIdx.x, nth = blockDim.x, n = p.n;
-  double2* buf = reinterpret_cast<double2*>(smraw);
-  double* stage = reinterpret_cast<double*>(buf + B * LP);
+  double2* buf = reinterpret_cast<double2*>(smraw);  // pack target (stage 0 input)
+  double2* buf2 = kPipeOOP ? buf + B * LP : buf;     // second buffer of out-of-place stages
+  double2* res = buf;                                 // buffer holding the transform result
+  double* stage = reinterpret_cast<double*>(buf + (kPipeOOP ? 2 : 1) * B * LP);
   // scatter / gather tables are read coalesced (indexed by t) through L1, leaving the
   // shared memory to the padded lines and the staging rows
   const unsigned* __restrict__ scat = p.pl.scat;
@@ -734,7 +749,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   __syncthreads();
   // y_k from the transformed line l, gather index gi = gath[k - 1] (0 for k out of range)
   auto unpack = [&](int l, unsigned gi, int k) {
-    const double2 C = buf[l * LP + gi];
+    const double2 C = res[l * LP + gi];
     return ((k & 1) ? -(C.y + C.x) : -(C.y - C.x)) * p.scale;
   };
   const long nl_out = p.nlines;
@@ -805,7 +820,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       fence_proxy_async();  // staging was read through the generic proxy
       issue(b + gridDim.x);
     }
-    if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, reps, p.pl, p.stages);
+    res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
     PIPE_T(2);
     unsigned g[kTpt];  // gather indices of this thread's t values
 #pragma unroll
@@ -847,7 +862,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       }
       for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
       __syncthreads();
-      if (p.stages) pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, reps, p.pl, p.stages);
+      res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
     }
     PIPE_T(3);
     // unpack + store (transposed: line index fastest -> B-double column segments).
@@ -960,7 +975,7 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   int reps = PfaStageC<SH, 0>::Rcnt;
   if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
   if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
-  const size_t smem = (size_t)kPipeLines * SH::LP * 16 + (size_t)kPipeLines * k.n * 8 +
+  const size_t smem = (size_t)(kPipeOOP ? 2 : 1) * kPipeLines * SH::LP * 16 + (size_t)kPipeLines * k.n * 8 +
                       reps * sizeof(unsigned);
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   static bool attr = false;
@@ -994,6 +1009,10 @@ static PipeVariant pipe_variant(int which) {
     case 1: return {256, 1, 3};
     case 2: return {384, 1, 3};
     case 3: return {512, 1, 3};
+    case 4: return {384, 1, 1};
+    case 5: return {384, 1, 2};
+    case 6: return {256, 1, 1};
+    case 7: return {256, 1, 2};
     default: return {384, 1, 4};
   }
 }
@@ -1042,6 +1061,10 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
         case 1: return launch_pipe_t<89, 23, 1, 256, 1, 3>(k, grid, st);
         case 2: return launch_pipe_t<89, 23, 1, 384, 1, 3>(k, grid, st);
         case 3: return launch_pipe_t<89, 23, 1, 512, 1, 3>(k, grid, st);
+        case 4: return launch_pipe_t<89, 23, 1, 384, 1, 1>(k, grid, st);
+        case 5: return launch_pipe_t<89, 23, 1, 384, 1, 2>(k, grid, st);
+        case 6: return launch_pipe_t<89, 23, 1, 256, 1, 1>(k, grid, st);
+        case 7: return launch_pipe_t<89, 23, 1, 256, 1, 2>(k, grid, st);
         default: return launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
       }
     case 2: return launch_pipe_t<31, 11, 3>(k, grid, st);
@@ -1149,6 +1172,23 @@ cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g,
 }  // namespace tvd
 
 // profiling only: per-phase cycle sums of the pipeline kernel (-DTVD_PIPE_TIMING builds)
+extern "C" int tvd_debug_stage_times(unsigned long long* out128, int reset) {
+#ifdef TVD_PIPE_TIMING
+  if (out128 && cudaMemcpyFromSymbol(out128, tvd::g_stage_t, 128 * sizeof(unsigned long long)) !=
+                    cudaSuccess)
+    return -1;
+  if (reset) {
+    unsigned long long z[128] = {};
+    cudaMemcpyToSymbol(tvd::g_stage_t, z, sizeof(z));
+  }
+  return 0;
+#else
+  (void)out128;
+  (void)reset;
+  return -1;
+#endif
+}
+
 extern "C" int tvd_debug_pipe_phases(unsigned long long* out8, int reset) {
 #ifdef TVD_PIPE_TIMING
   if (out8 && cudaMemcpyFromSymbol(out8, tvd::g_pipe_phase, 8 * sizeof(unsigned long long)) != cudaSuccess)

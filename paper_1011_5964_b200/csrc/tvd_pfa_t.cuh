@@ -61,10 +61,13 @@ __device__ __forceinline__ void rep_ab(int t, int& a, int& b) {
 }
 
 // fold + DFT of one stage.  `reps` holds (base | neg << 16) of every representative line
-// (line 0); line l adds l * LP.
-template <class ST, int NL, int MT = 4, int NW = 0, int TPWc = 3>
-__device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
+// (line 0); line l adds l * LP.  OOP: read `src`, write `dst` (a different buffer), so
+// outputs go out as soon as they are formed and the stage needs a single closing barrier;
+// otherwise src == dst and every round holds its outputs across an in-place barrier.
+template <class ST, int NL, int MT = 4, int NW = 0, int TPWc = 3, bool OOP = false>
+__device__ __forceinline__ void pfa_stage_c(const double2* src, double2* dst, const unsigned* reps,
                                             const double* Cm, const double* Sm) {
+  double2* buf = dst;  // in-place paths (src == dst)
   constexpr int kMmaTiles = MT;  // output tiles a warp holds across the in-place barrier
   constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LPc;
   const int tid = threadIdx.x, nth = blockDim.x;
@@ -91,7 +94,10 @@ __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
       ca[rs] = Cm[krow * ST::RP + rs * 4 + (lane & 3)];
       sa[rs] = Sm[krow * ST::RP + rs * 4 + (lane & 3)];
     }
-    const double* bufd = reinterpret_cast<const double*>(buf);
+#ifdef TVD_PIPE_TIMING
+    const long long ts_ = clock64();
+#endif
+    const double* bufd = reinterpret_cast<const double*>(src);
     for (int ct0 = 0; ct0 < nct; ct0 += ROUND) {
       double acc[TPW][4];
       const double* pb[TPW];
@@ -124,13 +130,13 @@ __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
         }
       }
 #ifdef TVD_PIPE_TIMING
-      if (tid == 0) {
-        // make the accumulators' completion part of the timed region
-        double z_ = 0.0;
+      long long tle_ = 0;
+      {
+        double z_ = 0.0;  // make the accumulators' completion part of the timed region
 #pragma unroll
         for (int j = 0; j < TPW; ++j) z_ += acc[j][0] + acc[j][3];
         if (z_ == 12345.678) buf[0].x = z_;
-        atomicAdd(&g_pipe_phase[q == 89 ? 5 : 6], (unsigned long long)(clock64() - tl0_));
+        tle_ = clock64();
       }
 #endif
       double2 vk[TPW], vm[TPW];
@@ -144,7 +150,7 @@ __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
         if (wact && ct < nct && krow <= H && dO < ndft) {
           const int lO = dO / ST::Rcnt, tO = dO - lO * ST::Rcnt;
           const unsigned rp = reps[tO] + (unsigned)(lO * LP) * 0x10001u;
-          const double2 x0 = buf[rp & 0xffffu];
+          const double2 x0 = src[rp & 0xffffu];
           const double a0 = acc[j][0], a1 = acc[j][1], b0 = acc[j][2], b1 = acc[j][3];
           vk[j] = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
           vm[j] = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
@@ -152,7 +158,7 @@ __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
           oflag[j] = 1 | (tO == 0 ? 2 : 0);
         }
       }
-      __syncthreads();
+      if constexpr (!OOP) __syncthreads();
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         if (oflag[j]) {
@@ -173,8 +179,73 @@ __device__ __forceinline__ void pfa_stage_c(double2* buf, const unsigned* reps,
           }
         }
       }
-      __syncthreads();
+      if constexpr (!OOP) __syncthreads();
+#ifdef TVD_PIPE_TIMING
+      if (OOP && lane == 0 && warp < 16) {
+        const long long tep_ = clock64();
+        unsigned long long* slot = g_stage_t + ((q == 89 ? 0 : 1) * 16 + warp) * 4;
+        atomicAdd(slot + 0, (unsigned long long)(tl0_ - ts_));
+        atomicAdd(slot + 1, (unsigned long long)(tle_ - tl0_));
+        atomicAdd(slot + 2, (unsigned long long)(tep_ - tle_));
+      }
+#endif
     }
+#ifdef TVD_PIPE_TIMING
+    const long long tb0_ = clock64();
+#endif
+    if constexpr (OOP) __syncthreads();
+#ifdef TVD_PIPE_TIMING
+    if (OOP && lane == 0 && warp < 16)
+      atomicAdd(g_stage_t + ((q == 89 ? 0 : 1) * 16 + warp) * 4 + 3,
+                (unsigned long long)(clock64() - tb0_));
+#endif
+    return;
+  }
+  if constexpr (OOP && !(ST::mma && NW > 0)) {
+    // small radix, out of place: one thread per representative DFT, fold in registers
+    static_assert(!ST::mma, "out-of-place stages use the A-stationary tensor-core path");
+    for (int d0 = 0; d0 < ndft; d0 += nth) {
+      const int dft = d0 + tid;
+      if (dft < ndft) {
+        const int l = dft / ST::Rcnt, t = dft - l * ST::Rcnt;
+        const unsigned rp = reps[t] + (unsigned)(l * LP) * 0x10001u;
+        const bool self = t == 0;
+        const double2* p = src + (rp & 0xffffu);
+        const double2 x0 = p[0];
+        double2 A[H + 1], Bv[H + 1];
+#pragma unroll
+        for (int r = 1; r <= H; ++r) {
+          const double2 x1 = p[r * st], x2 = p[(q - r) * st];
+          A[r] = cadd(x1, x2);
+          Bv[r] = csub(x1, x2);
+        }
+        double2 v[q];
+        double2 s0 = x0;
+#pragma unroll
+        for (int r = 1; r <= H; ++r) s0 = cadd(s0, A[r]);
+        v[0] = s0;
+#pragma unroll
+        for (int k = 1; k <= H; ++k) {
+          double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int r = 1; r <= H; ++r) {
+            const double c = Cm[k * ST::RP + r - 1], sn = Sm[k * ST::RP + r - 1];
+            a.x += A[r].x * c; a.y += A[r].y * c;
+            b.x += Bv[r].x * sn; b.y += Bv[r].y * sn;
+          }
+          v[k] = make_double2(x0.x + a.x + b.y, x0.y + a.y - b.x);
+          v[q - k] = make_double2(x0.x + a.x - b.y, x0.y + a.y + b.x);
+        }
+        double2* o = dst + (rp & 0xffffu);
+        double2* on = dst + (rp >> 16);
+#pragma unroll
+        for (int k = 0; k < q; ++k) {
+          o[k * st] = v[k];
+          if (!self) on[((q - k) % q) * st] = make_double2(-v[k].x, -v[k].y);
+        }
+      }
+    }
+    __syncthreads();
     return;
   }
   // fold (scalar and legacy tensor-core paths)

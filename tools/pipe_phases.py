@@ -27,13 +27,19 @@ lam = torch.from_numpy(rng.uniform(0.5, 2.0, (n, n))).cuda()
 pre = P.FactoredPreconditioner("M", T.TransformKind.SINE_HAT, lam, 1e-3)
 z = pre.apply_inverse(w)
 torch.cuda.synchronize()
+st_fn = lib.tvd_debug_stage_times
+st_fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+st_fn.restype = ctypes.c_int
+st_buf = (ctypes.c_ulonglong * 128)()
 buf = (ctypes.c_ulonglong * 8)()
+st_fn(st_buf, 1)
 if fn(buf, 1) != 0:
     raise SystemExit("library built without -DTVD_PIPE_TIMING")
 for _ in range(3):
     z = pre.apply_inverse(w)
 torch.cuda.synchronize()
 fn(buf, 1)
+st_fn(st_buf, 1)
 ctas = buf[7]
 names = ["wait+zero", "pack", "stages", "mid(+stages)", "unpack"]
 tot = sum(buf[i] for i in range(5))
@@ -42,3 +48,10 @@ print(f"CTAs flushed {ctas}; cycles per batch (thread 0 view), total {tot / batc
 for i, nm in enumerate(names):
     print(f"  {nm:14s} {buf[i] / batches:9.0f}  ({buf[i] / tot:.1%})")
 print(f"  warp-0 DMMA loop per batch: stage q=89 {buf[5] / batches:.0f}, other {buf[6] / batches:.0f}")
+transforms = 3 * 4 * (n // 2)  # 4 transforms per application (the sandwich pass has two)
+for si, nm in enumerate(["q=89 stage", "other stage"]):
+    print(f"{nm}: cycles per batch-transform by warp [setup, DMMA loop, epilogue, barrier]")
+    for w in range(16):
+        v = [st_buf[(si * 16 + w) * 4 + k] / transforms for k in range(4)]
+        if sum(v) > 0:
+            print(f"  warp {w:2d}: " + "  ".join(f"{x:7.0f}" for x in v))
