@@ -88,14 +88,48 @@ __global__ void k_pcg_gamma(PcgState* s, const double* partial, int nb) {
   }
 }
 
+// x += step p ; r -= step q ; partial = |r|^2.  128-bit accesses, two pairs per thread in
+// flight; odd N leaves one tail element to thread 0.
 __global__ void k_pcg_update_xr(const PcgState* s, double* __restrict__ x, double* __restrict__ r,
                                 const double* __restrict__ p, const double* __restrict__ q, long N,
                                 double* partial) {
   if (s->done) return;
   __shared__ double red[32];
   const double step = s->step;
+  const long N2 = N >> 1, stride = (long)gridDim.x * blockDim.x;
+  double2* __restrict__ x2 = reinterpret_cast<double2*>(x);
+  double2* __restrict__ r2 = reinterpret_cast<double2*>(r);
+  const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p);
+  const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q);
   double acc = 0.0;
-  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < N2; i += 2 * stride) {
+    const long j = i + stride;
+    const bool two = j < N2;
+    const double2 xa = x2[i], pa = p2[i], ra = r2[i], qa = q2[i];
+    double2 xb = make_double2(0.0, 0.0), pb = xb, rb = xb, qb = xb;
+    if (two) {
+      xb = x2[j];
+      pb = p2[j];
+      rb = r2[j];
+      qb = q2[j];
+    }
+    x2[i] = make_double2(__dadd_rn(xa.x, __dmul_rn(step, pa.x)), __dadd_rn(xa.y, __dmul_rn(step, pa.y)));
+    const double2 va = make_double2(__dsub_rn(ra.x, __dmul_rn(step, qa.x)),
+                                    __dsub_rn(ra.y, __dmul_rn(step, qa.y)));
+    r2[i] = va;
+    acc += va.x * va.x;
+    acc += va.y * va.y;
+    if (two) {
+      x2[j] = make_double2(__dadd_rn(xb.x, __dmul_rn(step, pb.x)), __dadd_rn(xb.y, __dmul_rn(step, pb.y)));
+      const double2 vb = make_double2(__dsub_rn(rb.x, __dmul_rn(step, qb.x)),
+                                      __dsub_rn(rb.y, __dmul_rn(step, qb.y)));
+      r2[j] = vb;
+      acc += vb.x * vb.x;
+      acc += vb.y * vb.y;
+    }
+  }
+  if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long g = N - 1;
     x[g] = __dadd_rn(x[g], __dmul_rn(step, p[g]));
     const double v = __dsub_rn(r[g], __dmul_rn(step, q[g]));
     r[g] = v;
@@ -141,12 +175,28 @@ __global__ void k_pcg_beta(PcgState* s, const double* partial, int nb, int max_i
   }
 }
 
+// p = z + beta p (numpy rounding); 128-bit accesses, two pairs per thread in flight.
 __global__ void k_pcg_update_p(const PcgState* s, double* __restrict__ p, const double* __restrict__ z,
                                long N) {
   if (s->done) return;
   const double beta = s->beta;
-  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x)
-    p[g] = __dadd_rn(z[g], __dmul_rn(beta, p[g]));
+  const long N2 = N >> 1, stride = (long)gridDim.x * blockDim.x;
+  double2* __restrict__ p2 = reinterpret_cast<double2*>(p);
+  const double2* __restrict__ z2 = reinterpret_cast<const double2*>(z);
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < N2; i += 2 * stride) {
+    const long j = i + stride;
+    const bool two = j < N2;
+    const double2 pa = p2[i], za = z2[i];
+    double2 pb = make_double2(0.0, 0.0), zb = pb;
+    if (two) {
+      pb = p2[j];
+      zb = z2[j];
+    }
+    p2[i] = make_double2(__dadd_rn(za.x, __dmul_rn(beta, pa.x)), __dadd_rn(za.y, __dmul_rn(beta, pa.y)));
+    if (two)
+      p2[j] = make_double2(__dadd_rn(zb.x, __dmul_rn(beta, pb.x)), __dadd_rn(zb.y, __dmul_rn(beta, pb.y)));
+  }
+  if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[N - 1] = __dadd_rn(z[N - 1], __dmul_rn(beta, p[N - 1]));
 }
 
 __global__ void k_diag_solve(const double* __restrict__ r, const double* __restrict__ d,
