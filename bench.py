@@ -335,7 +335,7 @@ def run_ours(args, rank: int, world: int) -> None:
                    "l2": "inputs larger than L2 (~15 n^2 fp64 arrays = 480 MB working set)"},
         "mpix_iter_per_s": value * n * n / 1e6,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "kernel": dom,
+                     "frac": achieved / hbm, "traffic": traffic_per_launch(dom), "kernel": dom,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"
                      if not peaks.get("fallback") else "fallback 6650 GB/s"},
         "pcg_roofline": {"alg_bytes_per_iter": alg_iter,
@@ -350,6 +350,21 @@ def run_ours(args, rank: int, world: int) -> None:
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
+
+
+def traffic_per_launch(category: str):
+    """DRAM bytes (read + write) per launch of the category's kernel, from the newest committed
+    ``ncu --set full`` capture summarised under profiles/<round>/traffic.json (or None)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                              "profiles", "r*", "traffic.json")), reverse=True):
+        try:
+            ent = json.load(open(path)).get(category)
+        except (OSError, ValueError):
+            continue
+        if ent:
+            return ent["dram_bytes"]
+    return None
 
 
 def main() -> None:

@@ -41,16 +41,29 @@ def launches(path: pathlib.Path) -> list[dict]:
             for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])]
 
 
+_BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+# bench.py kernel categories -> the kernel of a full capture whose DRAM traffic stands for it
+CATEGORY_KERNEL = {"trig_rows": "k_dst_pipe", "trig_cols": "k_dst_pipe", "band_rows": "k_bmma_rows",
+                   "band_cols": "k_bmma_cols", "vector": "k_pcg_update_xr"}
+
+
 def report(path: pathlib.Path) -> list[dict]:
     raw = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, out = rows[0], []
+    hdr, units, out = rows[0], rows[1], []
     for r in rows[2:]:
         d = {"kernel": r[hdr.index("Kernel Name")]}
         for k in KEYS:
             if k in hdr:
                 d[k] = r[hdr.index(k)]
+        rb = wb = None
+        if "dram__bytes_read.sum" in hdr and "dram__bytes_write.sum" in hdr:
+            i, j = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+            rb = float(r[i].replace(",", "")) * _BYTES.get(units[i], 1.0)
+            wb = float(r[j].replace(",", "")) * _BYTES.get(units[j], 1.0)
+            d["dram_bytes"] = rb + wb
         out.append(d)
     return out
 
@@ -58,10 +71,27 @@ def report(path: pathlib.Path) -> list[dict]:
 def main() -> None:
     rd = pathlib.Path(sys.argv[1])
     rd.mkdir(parents=True, exist_ok=True)
-    summary = {"launches": launches(pathlib.Path(sys.argv[2]))}
-    for rep in sys.argv[3:]:
+    name = "ncu_summary.json"
+    args = sys.argv[2:]
+    if args and args[0].startswith("--name="):
+        name = args.pop(0).split("=", 1)[1]
+    summary = {"launches": launches(pathlib.Path(args[0]))}
+    reps = []
+    for rep in args[1:]:
         summary[pathlib.Path(rep).stem] = report(pathlib.Path(rep))
-    (rd / "ncu_summary.json").write_text(json.dumps(summary, indent=1))
+        reps.append((pathlib.Path(rep).name, summary[pathlib.Path(rep).stem]))
+    (rd / name).write_text(json.dumps(summary, indent=1))
+    # per-launch DRAM traffic of each bench category (first capture of its kernel)
+    traffic = {}
+    for cat, kern in CATEGORY_KERNEL.items():
+        for rep_name, entries in reps:
+            hit = next((e for e in entries if kern in e["kernel"] and "dram_bytes" in e), None)
+            if hit:
+                traffic[cat] = {"kernel": hit["kernel"].split("(")[0], "dram_bytes": hit["dram_bytes"],
+                                "source": f"{rd.name}/{rep_name} (ncu --set full)"}
+                break
+    if traffic:
+        (rd / "traffic.json").write_text(json.dumps(traffic, indent=1))
     print(json.dumps(summary["launches"][:12], indent=1))
 
 
