@@ -432,6 +432,44 @@ static bool build_pfa(TrigPlan* P) {
     return false;
   pl.scat = dscat;
   pl.gath = dgath;
+  // half-line layout tables (two-factor shapes): stored b <= H1, row pitch P1h
+  pl.hscat = pl.hgath = nullptr;
+  pl.P1h = pl.LPh = 0;
+  if (pl.d == 2) {
+    const int Q0 = pl.q[0], Q1 = pl.q[1], H1 = (Q1 - 1) / 2;
+    const int P1h = H1 + 1 + ((4 - (H1 + 1) % 8) + 8) % 8;  // = 4 (mod 8): conflict-free
+    pl.P1h = P1h;
+    pl.LPh = Q0 * P1h + 1;  // + one zero pad element (stage-1 padded r reads)
+    auto stored = [&](int a, int b, unsigned* pos, unsigned* neg) {
+      if (b <= H1) {
+        *pos = (unsigned)(a * P1h + b);
+        *neg = 0;
+      } else {
+        *pos = (unsigned)(((Q0 - a) % Q0) * P1h + (Q1 - b));
+        *neg = 1;
+      }
+    };
+    std::vector<unsigned> hs(N), hg(N);
+    for (int t = 1; t <= N; ++t) {
+      int j = (t & 1) == 0 ? t / 2 : (t - 1) / 2 - h;
+      if (j < 0) j += L;
+      const int m0 = (int)(((long long)(j % Q0) * pl.rinv[0]) % Q0);
+      const int m1 = (int)(((long long)(j % Q1) * pl.rinv[1]) % Q1);
+      unsigned pa, na, e;
+      stored(m0, m1, &pa, &na);
+      e = pa | (na << 15);
+      if (m1 == 0) e |= ((unsigned)(((Q0 - m0) % Q0) * P1h) << 16) | (1u << 31);
+      hs[t - 1] = e;
+      unsigned pg, ng;
+      stored(t % Q0, t % Q1, &pg, &ng);
+      hg[t - 1] = pg | (ng << 15);
+    }
+    unsigned *dhs, *dhg;
+    if (upload(hs, &dhs, P->owned) != cudaSuccess || upload(hg, &dhg, P->owned) != cudaSuccess)
+      return false;
+    pl.hscat = dhs;
+    pl.hgath = dhg;
+  }
   return true;
 }
 

@@ -64,6 +64,11 @@ struct PfaPlan {
   const unsigned* scat;     // t = 1..N: pos(c'_j of z_t) | pos(c'_{-j}) << 16
   const unsigned* gath;     // k = 1..N: pos(C'_k)
   const unsigned* reps[3];  // stage s, representative t: base | negated base << 16
+  // Half-line layout of two-factor shapes (tvd_pfa_half.cuh): only b <= (q1 - 1) / 2 of the
+  // q0 x q1 Good-Thomas grid is stored (row pitch P1h), the rest is -(value at (-a, -b)).
+  int P1h, LPh;
+  const unsigned* hscat;  // t: posA | negA << 15 | posB << 16 | hasB << 31 (B always negated)
+  const unsigned* hgath;  // k: pos | neg << 15
 };
 
 // Device-resident FFT plan plus the per-length twiddle tables of one family.

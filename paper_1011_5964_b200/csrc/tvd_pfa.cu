@@ -697,10 +697,12 @@ __device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, uns
   return SH::d == 2 ? x : y;
 }
 
-template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW>
+template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF = false>
 __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   using SH = PfaShape<Q1, Q2, Q3>;
-  constexpr int LP = SH::LP, N = SH::N, B = kPipeLines;
+  static_assert(!HALF || SH::d == 2, "half-line layout is for two-factor lengths");
+  // HALF: half-line Good-Thomas layout (tvd_pfa_t.cuh HalfShape), signed scatter / gather
+  constexpr int LP = HALF ? HalfShape<Q1, Q2>::LPh : SH::LP, N = SH::N, B = kPipeLines;
   constexpr int kTpt = (N + NT - 1) / NT;  // t-values per thread per line
   static_assert((B & (B - 1)) == 0, "transposed store assumes power-of-two batches");
   if (p.skip && *p.skip) return;
@@ -715,8 +717,8 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   double* stage = reinterpret_cast<double*>(buf + (kPipeOOP ? 2 : 1) * B * LP);
   // scatter / gather tables are read coalesced (indexed by t) through L1, leaving the
   // shared memory to the padded lines and the staging rows
-  const unsigned* __restrict__ scat = p.pl.scat;
-  const unsigned* __restrict__ gath = p.pl.gath;
+  const unsigned* __restrict__ scat = HALF ? p.pl.hscat : p.pl.scat;
+  const unsigned* __restrict__ gath = HALF ? p.pl.hgath : p.pl.gath;
   unsigned* reps[3];
   reps[0] = reinterpret_cast<unsigned*>(stage + B * n);
   reps[1] = reps[0] + PfaStageC<SH, 0>::Rcnt;
@@ -749,8 +751,25 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   __syncthreads();
   // y_k from the transformed line l, gather index gi = gath[k - 1] (0 for k out of range)
   auto unpack = [&](int l, unsigned gi, int k) {
-    const double2 C = res[l * LP + gi];
+    double2 C;
+    if constexpr (HALF) {
+      C = res[l * LP + (gi & 0x7fffu)];
+      if (gi & 0x8000u) C = make_double2(-C.x, -C.y);
+    } else {
+      C = res[l * LP + gi];
+    }
     return ((k & 1) ? -(C.y + C.x) : -(C.y - C.x)) * p.scale;
+  };
+  // z_t -> its packed position(s) (t parity selects re / im)
+  auto scatter = [&](double* bl, int t, unsigned e, double x) {
+    double* b = bl + (t & 1);
+    if constexpr (HALF) {
+      b[2 * (e & 0x7fffu)] = (e & 0x8000u) ? -x : x;
+      if (e >> 31) b[2 * ((e >> 16) & 0x7fffu)] = -x;
+    } else {
+      b[2 * (e & 0xffffu)] = x;
+      b[2 * (e >> 16)] = -x;
+    }
   };
   const long nl_out = p.nlines;
   auto oidx = [&](int line, int e) {
@@ -761,7 +780,10 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   PIPE_T_INIT;
   for (int b = blockIdx.x; b < nbatch; b += gridDim.x) {
     const int line0 = b * B, nlv = min(B, p.nlines - line0);
-    for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
+    for (int i = tid; i < B; i += nth) {
+      buf[i * LP] = make_double2(0.0, 0.0);
+      if (HALF) buf[i * LP + LP - 1] = make_double2(0.0, 0.0);  // pad read by padded r
+    }
     for (int i = tid; i < (B - nlv) * LP; i += nth) buf[nlv * LP + i] = make_double2(0.0, 0.0);
     // pack from the staging rows (+ Shat borders parked in smem): thread owns
     // t = 1 + tid + k nth.  The scatter indices depend on t only: one batched load
@@ -798,11 +820,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 #pragma unroll
       for (int k = 0; k < kTpt; ++k) {
         const int t = 1 + tid + k * NT;
-        if (k < kTpt - 1 || t <= N) {
-          double* b = bl + (t & 1);
-          b[2 * (e[k] & 0xffffu)] = x[k];
-          b[2 * (e[k] >> 16)] = -x[k];
-        }
+        if (k < kTpt - 1 || t <= N) scatter(bl, t, e[k], x[k]);
       }
     }
     if (p.off && tid < 2 * nlv) {
@@ -820,7 +838,12 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       fence_proxy_async();  // staging was read through the generic proxy
       issue(b + gridDim.x);
     }
-    res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
+    if constexpr (HALF) {
+      half_transform<Q1, Q2, B, NT / 32, TPW>(buf, p.pl, p.stages);
+      res = buf;
+    } else {
+      res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
+    }
     PIPE_T(2);
     unsigned g[kTpt];  // gather indices of this thread's t values
 #pragma unroll
@@ -853,16 +876,17 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
           const int t = 1 + tid + k * NT;
-          if (l < nlv && t <= N) {
-            double* bb = bl + (t & 1);
-            bb[2 * (e[k] & 0xffffu)] = v[l][k];
-            bb[2 * (e[k] >> 16)] = -v[l][k];
-          }
+          if (l < nlv && t <= N) scatter(bl, t, e[k], v[l][k]);
         }
       }
       for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
       __syncthreads();
-      res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
+      if constexpr (HALF) {
+        half_transform<Q1, Q2, B, NT / 32, TPW>(buf, p.pl, p.stages);
+        res = buf;
+      } else {
+        res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
+      }
     }
     PIPE_T(3);
     // unpack + store (transposed: line index fastest -> B-double column segments).
@@ -969,22 +993,24 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   }
 }
 
-template <int Q1, int Q2, int Q3, int NT = 256, int MINB = 2, int TPW = 3>
+template <int Q1, int Q2, int Q3, int NT = 256, int MINB = 2, int TPW = 3, bool HALF = false>
 static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   using SH = PfaShape<Q1, Q2, Q3>;
   int reps = PfaStageC<SH, 0>::Rcnt;
   if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
   if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
-  const size_t smem = (size_t)(kPipeOOP ? 2 : 1) * kPipeLines * SH::LP * 16 + (size_t)kPipeLines * k.n * 8 +
-                      reps * sizeof(unsigned);
+  constexpr int LP = HALF ? HalfShape<Q1, Q2 == 1 ? 3 : Q2>::LPh : SH::LP;
+  const size_t smem = (size_t)(kPipeOOP && !HALF ? 2 : 1) * kPipeLines * LP * 16 +
+                      (size_t)kPipeLines * k.n * 8 + reps * sizeof(unsigned);
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+  if (HALF && !k.pl.hscat) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
+    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW><<<grid, NT, smem, st>>>(k);
+  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF><<<grid, NT, smem, st>>>(k);
   return cudaGetLastError();
 }
 
@@ -1001,6 +1027,14 @@ static int pipe_variant_id() {
     return s ? atoi(s) : -1;
   }();
   return v;
+}
+// half-line layout for the two-factor lengths (TVD_PIPE_HALF=0 selects the full layout)
+static bool pipe_half() {
+  static const bool on = [] {
+    const char* s = getenv("TVD_PIPE_HALF");
+    return !(s && s[0] == '0');
+  }();
+  return on;
 }
 static PipeVariant pipe_variant(int which) {
   if (which != 1) return {256, 2, 3};
@@ -1065,10 +1099,14 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
         case 5: return launch_pipe_t<89, 23, 1, 384, 1, 2>(k, grid, st);
         case 6: return launch_pipe_t<89, 23, 1, 256, 1, 1>(k, grid, st);
         case 7: return launch_pipe_t<89, 23, 1, 256, 1, 2>(k, grid, st);
-        default: return launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
+        default:
+          return pipe_half() ? launch_pipe_t<89, 23, 1, 384, 1, 4, true>(k, grid, st)
+                             : launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
       }
     case 2: return launch_pipe_t<31, 11, 3>(k, grid, st);
-    case 3: return launch_pipe_t<73, 7, 1>(k, grid, st);
+    case 3:
+      return pipe_half() ? launch_pipe_t<73, 7, 1, 256, 2, 3, true>(k, grid, st)
+                         : launch_pipe_t<73, 7, 1>(k, grid, st);
     case 4: return launch_pipe_t<127, 1, 1>(k, grid, st);
     default: return cudaErrorInvalidConfiguration;
   }

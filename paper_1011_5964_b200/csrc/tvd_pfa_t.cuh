@@ -386,3 +386,202 @@ __device__ __forceinline__ void pfa_stage_c(const double2* src, double2* dst, co
   }
 }
 
+
+// ---------------------------------------------------------------- half-line layout
+// Two-factor lengths L = Q0 * Q1.  c' is odd, so the Good-Thomas grid value at (a, b) is
+// -(value at (-a, -b)) and only b <= H1 = (Q1 - 1) / 2 is stored, row pitch P1h (= 4 mod 8,
+// which makes the q = Q0 stage's operand loads and output stores bank-conflict-free), plus
+// one zero pad element per line.  Stage 0 (along a, q = Q0) transforms the stored columns
+// b = 0..H1 and needs no partner lines; stage 1 (along b, q = Q1) transforms row a together
+// with its partner row -a: inputs x_r = S[a][r], x_{q-r} = -S[-a][r]; outputs V_k -> S[a][k],
+// V_{q-k} -> S[-a][k] = -V_{q-k}.  Every DFT reads and writes only its own positions, so
+// both stages stay in place, and no partner line is ever materialised.
+template <int Q0_, int Q1_>
+struct HalfShape {
+  static constexpr int Q0 = Q0_, Q1 = Q1_;
+  static constexpr int L = Q0 * Q1, N = L - 1;
+  static constexpr int H0 = (Q0 - 1) / 2, H1 = (Q1 - 1) / 2;
+  static constexpr int P1h = H1 + 1 + ((4 - (H1 + 1) % 8) + 8) % 8;  // tvd_capi.cu build_pfa
+  static constexpr int LPh = Q0 * P1h + 1;
+};
+
+template <class SH, int S>
+struct HalfStage {
+  static constexpr bool partnered = S == 1;
+  static constexpr int q = S == 0 ? SH::Q0 : SH::Q1;
+  static constexpr int H = (q - 1) / 2;
+  static constexpr int st = S == 0 ? SH::P1h : 1;
+  static constexpr int Rcnt = S == 0 ? SH::H1 + 1 : SH::H0 + 1;
+  static constexpr int KP = (H + 1 + 7) / 8 * 8;
+  static constexpr int RP = (H + 3) / 4 * 4;
+  static constexpr bool mma = H >= 8;
+  static constexpr int LP = SH::LPh;
+  __device__ static int base(int t) { return S == 0 ? t : t * SH::P1h; }
+  __device__ static int partner(int t) { return S == 0 ? t : ((SH::Q0 - t) % SH::Q0) * SH::P1h; }
+};
+
+template <class ST, int NL, int NW, int TPWc>
+__device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const double* Sm) {
+  constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LP;
+  constexpr bool PT = ST::partnered;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  constexpr int ndft = NL * ST::Rcnt;
+  if constexpr (ST::mma) {
+    // A-stationary tensor-core stage (see pfa_stage_c): warp -> one k-tile x TPW column tiles
+    constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;
+    constexpr int G = NW / nkt >= 1 ? NW / nkt : 1;
+    constexpr int TPWn = (nct + G - 1) / G;
+    constexpr int TPW = TPWn < TPWc ? TPWn : TPWc;
+    constexpr int ROUND = G * TPW;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int kt = warp % nkt, g = warp / nkt;
+    const bool wact = warp < nkt * G;
+    const int krow = kt * 8 + (lane >> 2);
+    double ca[nrs], sa[nrs];
+#pragma unroll
+    for (int rs = 0; rs < nrs; ++rs) {
+      ca[rs] = Cm[krow * ST::RP + rs * 4 + (lane & 3)];
+      sa[rs] = Sm[krow * ST::RP + rs * 4 + (lane & 3)];
+    }
+    const double* bufd = reinterpret_cast<const double*>(buf);
+    for (int ct0 = 0; ct0 < nct; ct0 += ROUND) {
+      double acc[TPW][4];
+      const double* p1[TPW];
+      const double* p2[TPW];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+        const int ct = min(ct0 + g + j * G, nct - 1);
+        const int dB = min((ct * 8 + (lane >> 2)) >> 1, ndft - 1);
+        const int lB = dB / ST::Rcnt, tB = dB - lB * ST::Rcnt;
+        p1[j] = bufd + 2 * (lB * LP + ST::base(tB)) + ((lane >> 2) & 1);
+        p2[j] = bufd + 2 * (lB * LP + ST::partner(tB)) + ((lane >> 2) & 1);
+      }
+      if (wact) {
+#pragma unroll
+        for (int rs = 0; rs < nrs; ++rs) {
+          const int r = 1 + rs * 4 + (lane & 3);
+          double x1[TPW], x2[TPW];
+#pragma unroll
+          for (int j = 0; j < TPW; ++j) {
+            x1[j] = p1[j][2 * r * st];
+            x2[j] = PT ? p2[j][2 * r * st] : p1[j][2 * (q - r) * st];
+          }
+#pragma unroll
+          for (int j = 0; j < TPW; ++j) {
+            // fold: a = x_r + x_{q-r}, b = x_r - x_{q-r}; partnered x_{q-r} = -S[-a][r]
+            const double fa = PT ? x1[j] - x2[j] : x1[j] + x2[j];
+            const double fb = PT ? x1[j] + x2[j] : x1[j] - x2[j];
+            dmma884(acc[j][0], acc[j][1], ca[rs], fa);
+            dmma884(acc[j][2], acc[j][3], sa[rs], fb);
+          }
+        }
+      }
+      double2 vk[TPW], vm[TPW];
+      int ob[TPW], on[TPW], oflag[TPW];
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        oflag[j] = 0;
+        const int ct = ct0 + g + j * G;
+        const int dO = ct * 4 + (lane & 3);
+        if (wact && ct < nct && krow <= H && dO < ndft) {
+          const int lO = dO / ST::Rcnt, tO = dO - lO * ST::Rcnt;
+          ob[j] = lO * LP + ST::base(tO);
+          on[j] = lO * LP + ST::partner(tO);
+          const double2 x0 = buf[ob[j]];
+          const double a0 = acc[j][0], a1 = acc[j][1], b0 = acc[j][2], b1 = acc[j][3];
+          vk[j] = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
+          vm[j] = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
+          oflag[j] = 1 | (tO == 0 ? 2 : 0);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        if (oflag[j]) {
+          const int k = krow;
+          double2* p = buf + ob[j];
+          if (!PT) {
+            if (k == 0) {
+              p[0] = vk[j];
+            } else {
+              p[k * st] = vk[j];
+              p[(q - k) * st] = vm[j];
+            }
+          } else {
+            double2* pn = buf + on[j];
+            const bool self = oflag[j] & 2;
+            p[k] = vk[j];
+            if (!self) pn[k] = k == 0 ? make_double2(-vk[j].x, -vk[j].y)
+                                      : make_double2(-vm[j].x, -vm[j].y);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    // small radix: one thread per representative DFT, fully unrolled in registers
+    for (int d0 = 0; d0 < ndft; d0 += nth) {
+      const int dft = d0 + tid;
+      const bool act = dft < ndft;
+      double2 v[q];
+      int obs = 0, ons = 0;
+      bool self = false;
+      if (act) {
+        const int l = dft / ST::Rcnt, t = dft - l * ST::Rcnt;
+        obs = l * LP + ST::base(t);
+        ons = l * LP + ST::partner(t);
+        self = t == 0;
+        const double2 x0 = buf[obs];
+        double2 A[H + 1], Bv[H + 1];
+#pragma unroll
+        for (int r = 1; r <= H; ++r) {
+          const double2 x1 = buf[obs + r * st];
+          const double2 x2 = PT ? make_double2(-buf[ons + r * st].x, -buf[ons + r * st].y)
+                                : buf[obs + (q - r) * st];
+          A[r] = cadd(x1, x2);
+          Bv[r] = csub(x1, x2);
+        }
+        double2 s0 = x0;
+#pragma unroll
+        for (int r = 1; r <= H; ++r) s0 = cadd(s0, A[r]);
+        v[0] = s0;
+#pragma unroll
+        for (int k = 1; k <= H; ++k) {
+          double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int r = 1; r <= H; ++r) {
+            const double c = Cm[k * ST::RP + r - 1], sn = Sm[k * ST::RP + r - 1];
+            a.x += A[r].x * c; a.y += A[r].y * c;
+            b.x += Bv[r].x * sn; b.y += Bv[r].y * sn;
+          }
+          v[k] = make_double2(x0.x + a.x + b.y, x0.y + a.y - b.x);
+          v[q - k] = make_double2(x0.x + a.x - b.y, x0.y + a.y + b.x);
+        }
+      }
+      __syncthreads();
+      if (act) {
+        if (!PT) {
+#pragma unroll
+          for (int k = 0; k < q; ++k) buf[obs + k * st] = v[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k <= H; ++k) buf[obs + k] = v[k];
+          if (!self) {
+            buf[ons] = make_double2(-v[0].x, -v[0].y);
+#pragma unroll
+            for (int k = 1; k <= H; ++k) buf[ons + k] = make_double2(-v[q - k].x, -v[q - k].y);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int Q0, int Q1, int NL, int NW, int TPW>
+__device__ __forceinline__ void half_transform(double2* buf, const PfaPlan& pl, int stages) {
+  using SH = HalfShape<Q0, Q1>;
+  if (stages >= 1) half_stage<HalfStage<SH, 0>, NL, NW, TPW>(buf, pl.st[0].Cm, pl.st[0].Sm);
+  if (stages >= 2) half_stage<HalfStage<SH, 1>, NL, NW, TPW>(buf, pl.st[1].Cm, pl.st[1].Sm);
+}
