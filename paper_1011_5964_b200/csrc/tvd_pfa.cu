@@ -697,12 +697,12 @@ __device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, uns
   return SH::d == 2 ? x : y;
 }
 
-template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF = false>
+template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF = false, int BL = kPipeLines>
 __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   using SH = PfaShape<Q1, Q2, Q3>;
   static_assert(!HALF || SH::d == 2, "half-line layout is for two-factor lengths");
   // HALF: half-line Good-Thomas layout (tvd_pfa_t.cuh HalfShape), signed scatter / gather
-  constexpr int LP = HALF ? HalfShape<Q1, Q2>::LPh : SH::LP, N = SH::N, B = kPipeLines;
+  constexpr int LP = HALF ? HalfShape<Q1, Q2>::LPh : SH::LP, N = SH::N, B = BL;
   constexpr int kTpt = (N + NT - 1) / NT;  // t-values per thread per line
   static_assert((B & (B - 1)) == 0, "transposed store assumes power-of-two batches");
   if (p.skip && *p.skip) return;
@@ -993,24 +993,25 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   }
 }
 
-template <int Q1, int Q2, int Q3, int NT = 256, int MINB = 2, int TPW = 3, bool HALF = false>
+template <int Q1, int Q2, int Q3, int NT = 256, int MINB = 2, int TPW = 3, bool HALF = false,
+          int BL = kPipeLines>
 static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   using SH = PfaShape<Q1, Q2, Q3>;
   int reps = PfaStageC<SH, 0>::Rcnt;
   if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
   if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
   constexpr int LP = HALF ? HalfShape<Q1, Q2 == 1 ? 3 : Q2>::LPh : SH::LP;
-  const size_t smem = (size_t)(kPipeOOP && !HALF ? 2 : 1) * kPipeLines * LP * 16 +
-                      (size_t)kPipeLines * k.n * 8 + reps * sizeof(unsigned);
+  const size_t smem = (size_t)(kPipeOOP && !HALF ? 2 : 1) * BL * LP * 16 +
+                      (size_t)BL * k.n * 8 + reps * sizeof(unsigned);
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   if (HALF && !k.pl.hscat) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF>,
+    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF><<<grid, NT, smem, st>>>(k);
+  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL><<<grid, NT, smem, st>>>(k);
   return cudaGetLastError();
 }
 
@@ -1019,7 +1020,7 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
 // 170 keeps the DMMA chains unspilled); the smaller lengths run two 8-warp CTAs per SM.
 // TVD_PIPE_VARIANT overrides the 89 * 23 shape for experiments.
 struct PipeVariant {
-  int threads, ctas, tpw;
+  int threads, ctas, tpw, lines;
 };
 static int pipe_variant_id() {
   static const int v = [] {
@@ -1037,24 +1038,28 @@ static bool pipe_half() {
   return on;
 }
 static PipeVariant pipe_variant(int which) {
-  if (which != 1) return {256, 2, 3};
+  if (which != 1) return {256, 2, 3, 2};
   switch (pipe_variant_id()) {
-    case 0: return {256, 2, 3};
-    case 1: return {256, 1, 3};
-    case 2: return {384, 1, 3};
-    case 3: return {512, 1, 3};
-    case 4: return {384, 1, 1};
-    case 5: return {384, 1, 2};
-    case 6: return {256, 1, 1};
-    case 7: return {256, 1, 2};
-    default: return {384, 1, 4};
+    case 0: return {256, 2, 3, 2};
+    case 1: return {256, 1, 3, 2};
+    case 2: return {384, 1, 3, 2};
+    case 3: return {512, 1, 3, 2};
+    case 4: return {384, 1, 1, 2};
+    case 5: return {384, 1, 2, 2};
+    case 6: return {256, 1, 1, 2};
+    case 7: return {256, 1, 2, 2};
+    case 8: return {384, 1, 4, 4};
+    case 9: return {384, 1, 2, 4};
+    case 10: return {256, 1, 2, 4};
+    default: return {384, 1, 4, 2};
   }
 }
 
 int pipe_grid(const PfaPlan& P, int nlines) {
   int which;
   if (!pfa_specialised(P, &which)) return -1;
-  const int nbatch = (nlines + kPipeLines - 1) / kPipeLines;
+  const int bl = pipe_variant(which).lines;
+  const int nbatch = (nlines + bl - 1) / bl;
   const int cap = kSMs * pipe_variant(which).ctas;
   return nbatch < cap ? nbatch : cap;
 }
@@ -1099,6 +1104,9 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
         case 5: return launch_pipe_t<89, 23, 1, 384, 1, 2>(k, grid, st);
         case 6: return launch_pipe_t<89, 23, 1, 256, 1, 1>(k, grid, st);
         case 7: return launch_pipe_t<89, 23, 1, 256, 1, 2>(k, grid, st);
+        case 8: return launch_pipe_t<89, 23, 1, 384, 1, 4, true, 4>(k, grid, st);
+        case 9: return launch_pipe_t<89, 23, 1, 384, 1, 2, true, 4>(k, grid, st);
+        case 10: return launch_pipe_t<89, 23, 1, 256, 1, 2, true, 4>(k, grid, st);
         default:
           return pipe_half() ? launch_pipe_t<89, 23, 1, 384, 1, 4, true>(k, grid, st)
                              : launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
