@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
   if (ep.partial) {
     const double s = block_sum(dot, red);
     if (tid == 0) ep.partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
+    if (ep.fin.s) pcg_fin_tail(ep.fin, ep.partial, gridDim.x * gridDim.y, red);
   }
 }
 

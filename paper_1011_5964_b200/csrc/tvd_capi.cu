@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -69,6 +70,7 @@ struct tvd_ctx {
   std::map<std::pair<int, int>, std::unique_ptr<TrigPlan>> plans;
   DevBuf slots[kSlotCount];
   PcgState* d_state = nullptr;
+  unsigned* d_fin = nullptr;  // tickets of the folded finalizers (tvd_cg.h pcg_fin_tail)
   PcgState* h_state = nullptr;
   double* h_scalar = nullptr;  // pinned scratch for host scalars (64 doubles)
   double* d_scalar = nullptr;
@@ -527,7 +529,8 @@ static bool pipe_ok(tvd_ctx* c, int family, int n, const TrigPlan** P) {
 // rows -> t^T (transposed write), rows of t^T with inv^T -> t' (transposed back), rows -> z.
 static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const double* inv,
                         const double* inv_t, const double* d, int dmul, const double* in,
-                        double* out, const double* dot_with, const int* skip, int* nb_out) {
+                        double* out, const double* dot_with, const int* skip, int* nb_out,
+                        const PcgFin* fin = nullptr, bool* fin_done = nullptr) {
   double *tT, *t2, *partial = nullptr;
   TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tT);
   TVD_SLOT(c, kSlotTmp3, (size_t)n * n, t2);
@@ -563,6 +566,10 @@ static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const 
   z.dot_with = dot_with;
   z.partial = partial;
   z.skip = skip;
+  if (fin && partial) {  // beta in the last CTA of the final row pass
+    z.fin = *fin;
+    if (fin_done) *fin_done = true;
+  }
   TVD_LAUNCH(c, kCatTrigRows, 1, launch_pipe(P->pfa, family, n, n, 0, z, &nb, c->stream));
   if (nb_out) *nb_out = nb;
   return TVD_OK;
@@ -570,12 +577,15 @@ static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const 
 
 static int precond_transform(tvd_ctx* c, int family, int n, const double* inv, const double* d,
                              int dmul, const double* in, double* out, const double* dot_with,
-                             const int* skip, int* nb_out, const double* inv_t = nullptr) {
+                             const int* skip, int* nb_out, const double* inv_t = nullptr,
+                             const PcgFin* fin = nullptr, bool* fin_done = nullptr) {
+  if (fin_done) *fin_done = false;
   if (family != kFamSineHat && family != kFamDct && family != kFamDst1)
     return fail(TVD_ERR_INVALID, "unknown transform family");
   const TrigPlan* PP;
   if (pipe_ok(c, family, n, &PP))
-    return precond_pipe(c, PP, family, n, inv, inv_t, d, dmul, in, out, dot_with, skip, nb_out);
+    return precond_pipe(c, PP, family, n, inv, inv_t, d, dmul, in, out, dot_with, skip, nb_out,
+                        fin, fin_done);
   double* tmp;
   TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tmp);
   double* partial = nullptr;
@@ -745,7 +755,9 @@ static int make_bandop(tvd_blur* b, const Taps1D& t, int border, BandOp* op) {
 // out = [s .*] (H^T H (s .* in) + alpha L (s .* in)); optional partial of dot_with . out
 static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double* in, double* out,
                                  const double* dot_with, double* partial, const int* skip,
-                                 int* nb_out) {
+                                 int* nb_out, const PcgFin* fin = nullptr,
+                                 bool* fin_done = nullptr) {
+  if (fin_done) *fin_done = false;
   tvd_blur* b = sys->blur;
   const int n = b->n;
   const long N = (long)n * n;
@@ -770,6 +782,10 @@ static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double
   double* tmp;
   TVD_SLOT(c, kSlotTmp, N, tmp);
   if (b->separable) {
+    if (fin && partial && band_mma_ok(b->g[0])) {  // gamma in the tensor-core pass's last CTA
+      ep.fin = *fin;
+      if (fin_done) *fin_done = true;
+    }
     TVD_LAUNCH(c, kCatBandRows, 1, launch_band_rows(b->g[1], w, tmp, skip, c->stream));
     TVD_LAUNCH(c, kCatBandCols, 1, launch_band_cols(b->g[0], tmp, out, ep, skip, c->stream));
     if (nb_out) *nb_out = band_cols_grid(b->g[0]);
@@ -803,7 +819,9 @@ int tvd_ctx_create(int device, void* stream, tvd_ctx** out) {
   auto* c = new tvd_ctx();
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
-  if (cudaMalloc(&c->d_state, sizeof(PcgState)) != cudaSuccess ||
+  if (cudaMalloc(&c->d_fin, 4 * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(c->d_fin, 0, 4 * sizeof(unsigned)) != cudaSuccess ||
+      cudaMalloc(&c->d_state, sizeof(PcgState)) != cudaSuccess ||
       cudaMallocHost(&c->h_state, sizeof(PcgState)) != cudaSuccess ||
       cudaMallocHost(&c->h_scalar, 64 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&c->d_scalar, 64 * sizeof(double)) != cudaSuccess) {
@@ -876,6 +894,7 @@ int tvd_ctx_destroy(tvd_ctx* c) {
   for (auto& s : c->slots)
     if (s.ptr) cudaFree(s.ptr);
   cudaFree(c->d_state);
+  cudaFree(c->d_fin);
   cudaFreeHost(c->h_state);
   cudaFreeHost(c->h_scalar);
   cudaFree(c->d_scalar);
@@ -1228,7 +1247,9 @@ int tvd_system_apply(tvd_ctx* c, const tvd_system* sys, const double* in, double
 // z = M^{-1} r with r.z partials; z may alias r for kind NONE.
 static int minv_internal(tvd_ctx* c, const tvd_precond* pre, int n, const double* r, double* z,
                          double* partial, const int* skip, int* nb,
-                         const double* inv_t = nullptr) {
+                         const double* inv_t = nullptr, const PcgFin* fin = nullptr,
+                         bool* fin_done = nullptr) {
+  if (fin_done) *fin_done = false;
   const long N = (long)n * n;
   if (!pre || pre->kind == TVD_PRECOND_NONE) {
     if (z != r) TVD_LAUNCH(c, kCatVec, 1, launch_copy(r, z, N, skip, c->stream));
@@ -1243,7 +1264,7 @@ static int minv_internal(tvd_ctx* c, const tvd_precond* pre, int n, const double
   }
   if (pre->kind == TVD_PRECOND_TRANSFORM)
     return precond_transform(c, pre->family, n, pre->inv_eig, pre->d, 0, r, z, r, skip, nb,
-                             inv_t);
+                             inv_t, fin, fin_done);
   return fail(TVD_ERR_INVALID, "unknown preconditioner kind");
 }
 
@@ -1298,17 +1319,32 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   if (rc) return rc;
   TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rz0(S, partial, nb, st));
   TVD_LAUNCH(c, kCatVec, 1, launch_copy(zz, p, N, skip, st));
+  // finalizers folded into their producers (TVD_NO_FIN_FUSION=1: separate 1-CTA launches)
+  const bool fuse_fin = !getenv("TVD_NO_FIN_FUSION");
+  const PcgFin fin_g{S, c->d_fin, kFinGamma, 0, 0.0, nullptr};
+  const PcgFin fin_r{S, c->d_fin + 1, kFinRel, 0, tol, history};
+  const PcgFin fin_b{S, c->d_fin + 2, kFinBeta, max_iterations, 0.0, nullptr};
   int chunk = 4;
   for (int done_it = 0;;) {
     for (int k = 0; k < chunk; ++k) {
-      rc = system_apply_internal(c, sys, p, q, p, partial, skip, &nb);
+      // the three scalar steps run in the last CTA of the kernel producing their partials
+      // where that kernel supports it (tvd_cg.h pcg_fin_tail), else as 1-CTA launches
+      bool fused;
+      rc = system_apply_internal(c, sys, p, q, p, partial, skip, &nb, fuse_fin ? &fin_g : nullptr,
+                                 &fused);
       if (rc) return rc;
-      TVD_LAUNCH(c, kCatFin, 1, launch_pcg_gamma(S, partial, nb, st));
-      TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, p, q, N, partial, vec_blocks(), st));
-      TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
-      rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb, inv_t);
+      if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_gamma(S, partial, nb, st));
+      if (fuse_fin) {
+        TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, p, q, N, partial, vec_blocks(), st,
+                                                       &fin_r));
+      } else {
+        TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, p, q, N, partial, vec_blocks(), st));
+        TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
+      }
+      rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb, inv_t,
+                         fuse_fin ? &fin_b : nullptr, &fused);
       if (rc) return rc;
-      TVD_LAUNCH(c, kCatFin, 1, launch_pcg_beta(S, partial, nb, max_iterations, st));
+      if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_beta(S, partial, nb, max_iterations, st));
       TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_p(S, p, zz, N, st));
     }
     done_it += chunk;

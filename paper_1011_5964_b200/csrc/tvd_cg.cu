@@ -71,28 +71,14 @@ __global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst,
 __global__ void k_pcg_gamma(PcgState* s, const double* partial, int nb) {
   if (s->done) return;
   const double gamma = sum_partials_block(partial, nb);
-  if (threadIdx.x == 0) {
-    s->gamma = gamma;
-    if (!isfinite(gamma)) {
-      s->status = kErrDiverged;
-      s->err_iter = s->k;
-      s->done = 1;
-    } else if (gamma <= 0.0) {
-      s->status = kErrIndefinite;
-      s->err_iter = s->k;
-      s->err_val = gamma;
-      s->done = 1;
-    } else {
-      s->step = s->rz / gamma;
-    }
-  }
+  if (threadIdx.x == 0) pcg_fin_gamma(s, gamma);
 }
 
 // x += step p ; r -= step q ; partial = |r|^2.  128-bit accesses, two pairs per thread in
 // flight; odd N leaves one tail element to thread 0.
 __global__ void k_pcg_update_xr(const PcgState* s, double* __restrict__ x, double* __restrict__ r,
                                 const double* __restrict__ p, const double* __restrict__ q, long N,
-                                double* partial) {
+                                double* partial, PcgFin fin) {
   if (s->done) return;
   __shared__ double red[32];
   const double step = s->step;
@@ -137,42 +123,19 @@ __global__ void k_pcg_update_xr(const PcgState* s, double* __restrict__ x, doubl
   }
   const double t = block_sum(acc, red);
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (fin.s) pcg_fin_tail(fin, partial, gridDim.x, red);  // stop test in the last CTA
 }
 
 __global__ void k_pcg_rel(PcgState* s, const double* partial, int nb, double tol, double* hist) {
   if (s->done) return;
   const double rr = sum_partials_block(partial, nb);
-  if (threadIdx.x == 0) {
-    const double rel = sqrt(rr) / s->r0;
-    s->rel = rel;
-    if (!isfinite(rel)) {
-      s->status = kErrDiverged;
-      s->err_iter = s->k;
-      s->done = 1;
-      return;
-    }
-    if (hist) hist[s->k - 1] = rel;
-    if (rel < tol) {
-      s->iters = s->k;
-      s->converged = 1;
-      s->done = 1;
-    }
-  }
+  if (threadIdx.x == 0) pcg_fin_rel(s, rr, tol, hist);
 }
 
 __global__ void k_pcg_beta(PcgState* s, const double* partial, int nb, int max_it) {
   if (s->done) return;
   const double rz_next = sum_partials_block(partial, nb);
-  if (threadIdx.x == 0) {
-    s->beta = rz_next / s->rz;
-    s->rz = rz_next;
-    s->k += 1;
-    if (s->k > max_it) {
-      s->iters = max_it;
-      s->converged = 0;
-      s->done = 1;
-    }
-  }
+  if (threadIdx.x == 0) pcg_fin_beta(s, rz_next, max_it);
 }
 
 // p = z + beta p (numpy rounding); 128-bit accesses, two pairs per thread in flight.
@@ -324,8 +287,8 @@ cudaError_t launch_pcg_gamma(PcgState* s, const double* partial, int nb, cudaStr
   return cudaGetLastError();
 }
 cudaError_t launch_pcg_update_xr(PcgState* s, double* x, double* r, const double* p, const double* q,
-                                 long N, double* partial, int, cudaStream_t st) {
-  k_pcg_update_xr<<<TVD_VEC_GRID>>>(s, x, r, p, q, N, partial);
+                                 long N, double* partial, int, cudaStream_t st, const PcgFin* fin) {
+  k_pcg_update_xr<<<TVD_VEC_GRID>>>(s, x, r, p, q, N, partial, fin ? *fin : PcgFin{});
   return cudaGetLastError();
 }
 cudaError_t launch_pcg_rel(PcgState* s, const double* partial, int nb, double tol, double* hist,

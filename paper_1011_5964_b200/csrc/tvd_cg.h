@@ -29,6 +29,84 @@ struct PcgState {
   int converged;
 };
 
+// ---- scalar steps of the recurrence (krylov.py:99-116), thread 0 of one CTA, given the
+// deterministic sum of the per-CTA partials
+__device__ __forceinline__ void pcg_fin_gamma(PcgState* s, double pq) {
+  s->gamma = pq;
+  if (!isfinite(pq)) {
+    s->status = kErrDiverged;
+    s->err_iter = s->k;
+    s->done = 1;
+  } else if (pq <= 0.0) {
+    s->status = kErrIndefinite;
+    s->err_iter = s->k;
+    s->err_val = pq;
+    s->done = 1;
+  } else {
+    s->step = s->rz / pq;
+  }
+}
+__device__ __forceinline__ void pcg_fin_rel(PcgState* s, double rr, double tol, double* hist) {
+  const double rel = sqrt(rr) / s->r0;
+  s->rel = rel;
+  if (!isfinite(rel)) {
+    s->status = kErrDiverged;
+    s->err_iter = s->k;
+    s->done = 1;
+    return;
+  }
+  if (hist) hist[s->k - 1] = rel;
+  if (rel < tol) {
+    s->iters = s->k;
+    s->converged = 1;
+    s->done = 1;
+  }
+}
+__device__ __forceinline__ void pcg_fin_beta(PcgState* s, double rz_next, int max_it) {
+  s->beta = rz_next / s->rz;
+  s->rz = rz_next;
+  s->k += 1;
+  if (s->k > max_it) {
+    s->iters = max_it;
+    s->converged = 0;
+    s->done = 1;
+  }
+}
+
+// A finalizer folded into the kernel that produces its partials: every CTA writes its
+// partial, then the last CTA to finish (threadfence + atomic ticket) sums all partials in
+// a fixed order and applies the step.  s == nullptr: the host launches the finalizer.
+enum : int { kFinGamma = 1, kFinRel = 2, kFinBeta = 3 };
+struct PcgFin {
+  PcgState* s;
+  unsigned* counter;  // zero between launches (the last CTA resets it)
+  int kind;
+  int max_it;
+  double tol;
+  double* hist;
+};
+
+// Call from every CTA after thread 0 has stored partial[blockIndex] (all threads).
+__device__ __forceinline__ void pcg_fin_tail(const PcgFin& f, const double* partial, int nb,
+                                             double* red) {
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(f.counter, 1u) == (unsigned)(nb - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) v += __ldcg(partial + i);
+  const double sum = block_sum(v, red);
+  if (threadIdx.x == 0) {
+    if (f.kind == kFinGamma) pcg_fin_gamma(f.s, sum);
+    else if (f.kind == kFinRel) pcg_fin_rel(f.s, sum, f.tol, f.hist);
+    else pcg_fin_beta(f.s, sum, f.max_it);
+    *f.counter = 0u;
+  }
+}
+
 cudaError_t launch_sum_partials(const double* partial, int nb, double* out, cudaStream_t st);
 cudaError_t launch_residual_init(const double* b, const double* q, double* r, long N, double* partial,
                                  int nb, cudaStream_t st);
@@ -37,7 +115,8 @@ cudaError_t launch_pcg_rz0(PcgState* s, const double* partial, int nb, cudaStrea
 cudaError_t launch_copy(const double* src, double* dst, long N, const int* skip, cudaStream_t st);
 cudaError_t launch_pcg_gamma(PcgState* s, const double* partial, int nb, cudaStream_t st);
 cudaError_t launch_pcg_update_xr(PcgState* s, double* x, double* r, const double* p, const double* q,
-                                 long N, double* partial, int nb, cudaStream_t st);
+                                 long N, double* partial, int nb, cudaStream_t st,
+                                 const PcgFin* fin = nullptr);
 cudaError_t launch_pcg_rel(PcgState* s, const double* partial, int nb, double tol, double* hist,
                            cudaStream_t st);
 cudaError_t launch_pcg_beta(PcgState* s, const double* partial, int nb, int max_it, cudaStream_t st);

@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "tvd_cg.h"
 #include "tvd_fft.cuh"
 
 namespace tvd {
@@ -97,6 +98,7 @@ struct LineIO {
   const int* skip;         // device flag: return immediately when *skip != 0 (nullable)
   int pre_mul;
   int post_mul;
+  PcgFin fin;  // finalizer over `partial` folded into the last CTA (pipeline pass; s == nullptr: off)
 };
 
 // Band projection of one batch of lines (preconditioner assembly).

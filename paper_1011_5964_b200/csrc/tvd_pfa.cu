@@ -605,6 +605,7 @@ struct PipeK {
   double* partial;
   const int* skip;
   int pre_mul, post_mul;
+  PcgFin fin;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -990,6 +991,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   if (p.partial) {
     const double s = block_sum(acc, red);
     if (tid == 0) p.partial[blockIdx.x] = s;
+    if (p.fin.s) pcg_fin_tail(p.fin, p.partial, gridDim.x, red);
   }
 }
 
@@ -1085,6 +1087,7 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
   k.dot_with = io.dot_with;
   k.partial = io.partial;
   k.skip = io.skip;
+  k.fin = io.fin;
   static const int stages_env = [] {
     const char* s = getenv("TVD_PFA_STAGES");
     return s ? atoi(s) : 3;

@@ -1,6 +1,7 @@
 // Declarations for the stencil / convolution kernels (tvd_stencil.cu).
 #pragma once
 
+#include "tvd_cg.h"
 #include "tvd_common.cuh"
 
 namespace tvd {
@@ -30,6 +31,7 @@ struct Epilogue {
   const double* s;
   const double* dot_with;
   double* partial;
+  PcgFin fin;  // gamma finalizer folded into the last CTA (tensor-core pass; s == nullptr: off)
 };
 
 // (L w)[i][j] of tv.py:96-108 with zero-Neumann ghosts, reference op order.
