@@ -20,7 +20,8 @@ PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtvdeblur_b200.so"
 OBJ = PKG / "_obj"
-SOURCES = ["tvd_lines.cu", "tvd_pfa.cu", "tvd_stencil.cu", "tvd_band_mma.cu", "tvd_cg.cu", "tvd_capi.cu"]
+SOURCES = ["tvd_lines.cu", "tvd_pfa.cu", "tvd_rader.cu", "tvd_stencil.cu", "tvd_band_mma.cu", "tvd_cg.cu",
+           "tvd_capi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17",

@@ -15,6 +15,7 @@
 #include "../../include/tvdeblur_b200.h"
 #include "tvd_cg.h"
 #include "tvd_internal.h"
+#include "tvd_rader.h"
 #include "tvd_stencil.h"
 
 using namespace tvd;
@@ -483,6 +484,8 @@ static int get_plan(tvd_ctx* c, int family, int len, const TrigPlan** out) {
     int rc = build_plan(family, len, P);
     if (rc) return rc;
     P->pfa_ok = build_pfa(P.get());
+    if (!P->pfa_ok && (family == kFamSineHat || family == kFamDst1))
+      P->rader_ok = build_rader_plan(P->L, &P->rader, P->owned);
     it = c->plans.emplace(key, std::move(P)).first;
   }
   *out = it->second.get();
@@ -523,6 +526,65 @@ static bool pipe_ok(tvd_ctx* c, int family, int n, const TrigPlan** P) {
   if (c->force_generic || (family != kFamSineHat && family != kFamDst1) || (n & 1)) return false;
   if (get_plan(c, family, n, P)) return false;
   return (*P)->pfa_ok && pipe_grid((*P)->pfa, n) > 0;
+}
+
+// prime odd core (config 5): the Rader row engine applies
+static bool rader_ok(tvd_ctx* c, int family, int n, const TrigPlan** P) {
+  if (c->force_generic || (family != kFamSineHat && family != kFamDst1)) return false;
+  if (get_plan(c, family, n, P)) return false;
+  return (*P)->rader_ok && rader_launchable((*P)->rader, n, family);
+}
+
+// The same three passes with the Rader row engine (one row per CTA, row-major output) and
+// explicit tiled transposes between them.
+static int precond_rader(tvd_ctx* c, const TrigPlan* P, int family, int n, const double* inv,
+                         const double* inv_t, const double* d, int dmul, const double* in,
+                         double* out, const double* dot_with, const int* skip, int* nb_out,
+                         const PcgFin* fin, bool* fin_done) {
+  double *t1, *t2, *partial = nullptr;
+  TVD_SLOT(c, kSlotTmp2, (size_t)n * n, t1);
+  TVD_SLOT(c, kSlotTmp3, (size_t)n * n, t2);
+  if (!inv_t) {
+    double* it;
+    TVD_SLOT(c, kSlotInvT, (size_t)n * n, it);
+    TVD_LAUNCH(c, kCatVec, 1, launch_transpose(inv, it, n, c->stream));
+    inv_t = it;
+  }
+  if (dot_with) {
+    int rc = partial_capacity(c, (size_t)n + 64, &partial);
+    if (rc) return rc;
+  }
+  LineIO a{};
+  a.in = in;
+  a.out = t1;
+  a.pre = d;
+  a.pre_mul = dmul;
+  a.skip = skip;
+  int nb;
+  TVD_LAUNCH(c, kCatTrigRows, 1, launch_rader_rows(P->rader, family, n, n, a, &nb, c->stream));
+  TVD_LAUNCH(c, kCatVec, 1, launch_transpose(t1, t2, n, c->stream));
+  LineIO b{};
+  b.in = t2;
+  b.out = t1;
+  b.mid_mul = inv_t;
+  b.skip = skip;
+  TVD_LAUNCH(c, kCatTrigCols, 1, launch_rader_rows(P->rader, family, n, n, b, &nb, c->stream));
+  TVD_LAUNCH(c, kCatVec, 1, launch_transpose(t1, t2, n, c->stream));
+  LineIO z{};
+  z.in = t2;
+  z.out = out;
+  z.post = d;
+  z.post_mul = dmul;
+  z.dot_with = dot_with;
+  z.partial = partial;
+  z.skip = skip;
+  if (fin && partial) {
+    z.fin = *fin;
+    if (fin_done) *fin_done = true;
+  }
+  TVD_LAUNCH(c, kCatTrigRows, 1, launch_rader_rows(P->rader, family, n, n, z, &nb, c->stream));
+  if (nb_out) *nb_out = nb;
+  return TVD_OK;
 }
 
 // z = X (inv .* X^T (r / d)) / d for the DST families through three contiguous-row passes:
@@ -586,6 +648,9 @@ static int precond_transform(tvd_ctx* c, int family, int n, const double* inv, c
   if (pipe_ok(c, family, n, &PP))
     return precond_pipe(c, PP, family, n, inv, inv_t, d, dmul, in, out, dot_with, skip, nb_out,
                         fin, fin_done);
+  if (rader_ok(c, family, n, &PP))
+    return precond_rader(c, PP, family, n, inv, inv_t, d, dmul, in, out, dot_with, skip, nb_out,
+                         fin, fin_done);
   double* tmp;
   TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tmp);
   double* partial = nullptr;
@@ -1307,7 +1372,7 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   const double* inv_t = nullptr;
   if (pre && pre->kind == TVD_PRECOND_TRANSFORM) {
     const TrigPlan* PP;
-    if (pipe_ok(c, pre->family, n, &PP)) {
+    if (pipe_ok(c, pre->family, n, &PP) || rader_ok(c, pre->family, n, &PP)) {
       double* it;
       TVD_SLOT(c, kSlotInvT, N, it);
       TVD_LAUNCH(c, kCatVec, 1, launch_transpose(pre->inv_eig, it, n, st));

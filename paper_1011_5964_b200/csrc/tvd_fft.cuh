@@ -76,6 +76,25 @@ __device__ __forceinline__ double2 odd_cs<7>(int t) {
   }
 }
 
+template <>
+__device__ __forceinline__ double2 odd_cs<13>(int t) {
+  switch (t) {
+    case 1: return make_double2(0.8854560256532099, 0.4647231720437685);
+    case 2: return make_double2(0.5680647467311559, 0.8229838658936564);
+    case 3: return make_double2(0.120536680255323, 0.992708874098054);
+    case 4: return make_double2(-0.35460488704253545, 0.9350162426854148);
+    case 5: return make_double2(-0.7485107481711012, 0.6631226582407952);
+    case 6: return make_double2(-0.970941817426052, 0.23931566428755768);
+    case 7: return make_double2(-0.9709418174260521, -0.23931566428755743);
+    case 8: return make_double2(-0.7485107481711013, -0.663122658240795);
+    case 9: return make_double2(-0.3546048870425359, -0.9350162426854147);
+    case 10: return make_double2(0.1205366802553232, -0.992708874098054);
+    case 11: return make_double2(0.5680647467311548, -0.822983865893657);
+    case 12: return make_double2(0.88545602565321, -0.4647231720437684);
+    default: return make_double2(1.0, 0.0);
+  }
+}
+
 // Forward DFT (exp(-2 pi i jk / R)) of an odd-length register vector.
 template <int R>
 __device__ __forceinline__ void dft_odd_reg(double2 (&v)[R]) {
@@ -156,6 +175,8 @@ template <>
 __device__ __forceinline__ void dft_reg<5>(double2 (&v)[5]) { dft_odd_reg<5>(v); }
 template <>
 __device__ __forceinline__ void dft_reg<7>(double2 (&v)[7]) { dft_odd_reg<7>(v); }
+template <>
+__device__ __forceinline__ void dft_reg<13>(double2 (&v)[13]) { dft_odd_reg<13>(v); }
 
 // ------------------------------------------------------------------ stages
 // Line l occupies buf[l * LP, l * LP + L).

@@ -72,6 +72,21 @@ struct PfaPlan {
   const unsigned* hgath;  // k: pos | neg << 15
 };
 
+// ---- Rader DST engine for prime odd cores (tvd_rader.cu / tvd_rader.h)
+constexpr int kRaderMaxStages = 8;
+
+// Plan of one prime length L: convolution length M = L - 1, Stockham stages of the
+// length-M FFT (radix, product of the previous radices, register items per thread).
+struct RaderPlan {
+  int L, M, g;
+  int nst;
+  int radix[kRaderMaxStages], ns[kRaderMaxStages], slots[kRaderMaxStages];
+  const unsigned* rin;   // t = 1..M: dlog_g(j(t)), the Rader position of c'_j (packing map)
+  const unsigned* rout;  // k = 1..M: (M - dlog_g(k)) mod M, where C_k lands
+  const double2* bh;     // FFT_M(b), b_q = exp(-2 pi i g^-q / L)
+  const double2* tw;     // exp(-2 pi i e / M), e in [0, M)
+};
+
 // Device-resident FFT plan plus the per-length twiddle tables of one family.
 struct TrigPlan {
   int family;     // Family
@@ -83,6 +98,8 @@ struct TrigPlan {
   int max_items_line;    // largest per-line work-item count over the stages
   bool pfa_ok = false;   // DST family with an odd, <=3-factor coprime L
   PfaPlan pfa;
+  bool rader_ok = false;  // DST family with a prime L (Rader engine)
+  RaderPlan rader;
   std::vector<void*> owned;
 };
 

@@ -698,7 +698,8 @@ __device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, uns
   return SH::d == 2 ? x : y;
 }
 
-template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF = false, int BL = kPipeLines>
+template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF = false, int BL = kPipeLines,
+          bool CSM = false>
 __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   using SH = PfaShape<Q1, Q2, Q3>;
   static_assert(!HALF || SH::d == 2, "half-line layout is for two-factor lengths");
@@ -728,6 +729,17 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     const int rc = s == 0 ? PfaStageC<SH, 0>::Rcnt
                           : (s == 1 ? PfaStageC<SH, 1>::Rcnt : PfaStageC<SH, 2>::Rcnt);
     for (int i = tid; i < rc; i += nth) reps[s][i] = p.pl.reps[s][i];
+  }
+  // CSM: the q0 stage's cos / sin tables staged in shared memory (after the reps, 8-aligned)
+  double* csm = nullptr;
+  if constexpr (CSM) {
+    using HC = HalfCoef<HalfShape<Q1, Q2>>;
+    csm = reinterpret_cast<double*>(smraw) +
+          (((reinterpret_cast<unsigned char*>(reps[2] + 64) - smraw) + 7) / 8);
+    for (int i = tid; i < HC::n0; i += nth) {
+      csm[i] = p.pl.st[0].Cm[i];
+      csm[HC::n0 + i] = p.pl.st[0].Sm[i];
+    }
   }
   const int nbatch = (p.nlines + B - 1) / B;
   auto issue = [&](int batch) {
@@ -840,7 +852,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       issue(b + gridDim.x);
     }
     if constexpr (HALF) {
-      half_transform<Q1, Q2, B, NT / 32, TPW>(buf, p.pl, p.stages);
+      half_transform<Q1, Q2, B, NT / 32, TPW, CSM>(buf, p.pl, p.stages, csm);
       res = buf;
     } else {
       res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
@@ -883,7 +895,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
       __syncthreads();
       if constexpr (HALF) {
-        half_transform<Q1, Q2, B, NT / 32, TPW>(buf, p.pl, p.stages);
+        half_transform<Q1, Q2, B, NT / 32, TPW, CSM>(buf, p.pl, p.stages, csm);
         res = buf;
       } else {
         res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
@@ -996,24 +1008,25 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 }
 
 template <int Q1, int Q2, int Q3, int NT = 256, int MINB = 2, int TPW = 3, bool HALF = false,
-          int BL = kPipeLines>
+          int BL = kPipeLines, bool CSM = false>
 static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   using SH = PfaShape<Q1, Q2, Q3>;
   int reps = PfaStageC<SH, 0>::Rcnt;
   if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
   if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
   constexpr int LP = HALF ? HalfShape<Q1, Q2 == 1 ? 3 : Q2>::LPh : SH::LP;
-  const size_t smem = (size_t)(kPipeOOP && !HALF ? 2 : 1) * BL * LP * 16 +
-                      (size_t)BL * k.n * 8 + reps * sizeof(unsigned);
+  size_t smem = (size_t)(kPipeOOP && !HALF ? 2 : 1) * BL * LP * 16 +
+                (size_t)BL * k.n * 8 + (reps + 64) * sizeof(unsigned);
+  if (CSM) smem = (smem + 7) / 8 * 8 + (size_t)HalfCoef<HalfShape<Q1, Q2 == 1 ? 3 : Q2>>::total * 8;
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   if (HALF && !k.pl.hscat) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL>,
+    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL><<<grid, NT, smem, st>>>(k);
+  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM><<<grid, NT, smem, st>>>(k);
   return cudaGetLastError();
 }
 
@@ -1053,6 +1066,9 @@ static PipeVariant pipe_variant(int which) {
     case 8: return {384, 1, 4, 4};
     case 9: return {384, 1, 2, 4};
     case 10: return {256, 1, 2, 4};
+    case 11: return {256, 2, 3, 2};
+    case 12: return {256, 2, 4, 2};
+    case 13: return {384, 1, 4, 2};
     default: return {384, 1, 4, 2};
   }
 }
@@ -1110,6 +1126,9 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
         case 8: return launch_pipe_t<89, 23, 1, 384, 1, 4, true, 4>(k, grid, st);
         case 9: return launch_pipe_t<89, 23, 1, 384, 1, 2, true, 4>(k, grid, st);
         case 10: return launch_pipe_t<89, 23, 1, 256, 1, 2, true, 4>(k, grid, st);
+        case 11: return launch_pipe_t<89, 23, 1, 256, 2, 3, true, 2, true>(k, grid, st);
+        case 12: return launch_pipe_t<89, 23, 1, 256, 2, 4, true, 2, true>(k, grid, st);
+        case 13: return launch_pipe_t<89, 23, 1, 384, 1, 4, true, 2, true>(k, grid, st);
         default:
           return pipe_half() ? launch_pipe_t<89, 23, 1, 384, 1, 4, true>(k, grid, st)
                              : launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);

@@ -420,7 +420,9 @@ struct HalfStage {
   __device__ static int partner(int t) { return S == 0 ? t : ((SH::Q0 - t) % SH::Q0) * SH::P1h; }
 };
 
-template <class ST, int NL, int NW, int TPWc>
+// CSM: Cm / Sm point to shared-memory copies and the A fragments are read per r-step
+// (frees the 2 nrs registers of the stationary fragments)
+template <class ST, int NL, int NW, int TPWc, bool CSM = false>
 __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const double* Sm) {
   constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LP;
   constexpr bool PT = ST::partnered;
@@ -437,12 +439,21 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
     const int kt = warp % nkt, g = warp / nkt;
     const bool wact = warp < nkt * G;
     const int krow = kt * 8 + (lane >> 2);
-    double ca[nrs], sa[nrs];
+    constexpr int nra = CSM ? 1 : nrs;
+    double ca[nra], sa[nra];
+    const double* cmk = Cm + krow * ST::RP + (lane & 3);
+    const double* smk = Sm + krow * ST::RP + (lane & 3);
+    if constexpr (!CSM) {
 #pragma unroll
-    for (int rs = 0; rs < nrs; ++rs) {
-      ca[rs] = Cm[krow * ST::RP + rs * 4 + (lane & 3)];
-      sa[rs] = Sm[krow * ST::RP + rs * 4 + (lane & 3)];
+      for (int rs = 0; rs < nrs; ++rs) {
+        ca[rs] = cmk[rs * 4];
+        sa[rs] = smk[rs * 4];
+      }
     }
+#ifdef TVD_PIPE_TIMING
+    const long long ts_ = clock64();
+    long long tl0_ = 0, tle_ = 0, tep_ = 0;
+#endif
     const double* bufd = reinterpret_cast<const double*>(buf);
     for (int ct0 = 0; ct0 < nct; ct0 += ROUND) {
       double acc[TPW][4];
@@ -457,6 +468,9 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
         p1[j] = bufd + 2 * (lB * LP + ST::base(tB)) + ((lane >> 2) & 1);
         p2[j] = bufd + 2 * (lB * LP + ST::partner(tB)) + ((lane >> 2) & 1);
       }
+#ifdef TVD_PIPE_TIMING
+      tl0_ = clock64();
+#endif
       if (wact) {
 #pragma unroll
         for (int rs = 0; rs < nrs; ++rs) {
@@ -467,16 +481,27 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
             x1[j] = p1[j][2 * r * st];
             x2[j] = PT ? p2[j][2 * r * st] : p1[j][2 * (q - r) * st];
           }
+          const double car = CSM ? cmk[rs * 4] : ca[CSM ? 0 : rs];
+          const double sar = CSM ? smk[rs * 4] : sa[CSM ? 0 : rs];
 #pragma unroll
           for (int j = 0; j < TPW; ++j) {
             // fold: a = x_r + x_{q-r}, b = x_r - x_{q-r}; partnered x_{q-r} = -S[-a][r]
             const double fa = PT ? x1[j] - x2[j] : x1[j] + x2[j];
             const double fb = PT ? x1[j] + x2[j] : x1[j] - x2[j];
-            dmma884(acc[j][0], acc[j][1], ca[rs], fa);
-            dmma884(acc[j][2], acc[j][3], sa[rs], fb);
+            dmma884(acc[j][0], acc[j][1], car, fa);
+            dmma884(acc[j][2], acc[j][3], sar, fb);
           }
         }
       }
+#ifdef TVD_PIPE_TIMING
+      {
+        double z_ = 0.0;
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) z_ += acc[j][0] + acc[j][3];
+        if (z_ == 12345.678) buf[0].x = z_;
+        tle_ = clock64();
+      }
+#endif
       double2 vk[TPW], vm[TPW];
       int ob[TPW], on[TPW], oflag[TPW];
 #pragma unroll
@@ -517,8 +542,20 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
           }
         }
       }
+#ifdef TVD_PIPE_TIMING
+      tep_ = clock64();
+#endif
       __syncthreads();
     }
+#ifdef TVD_PIPE_TIMING
+    if (lane == 0 && warp < 16) {
+      unsigned long long* slot = g_stage_t + ((PT ? 1 : 0) * 16 + warp) * 4;
+      atomicAdd(slot + 0, (unsigned long long)(tl0_ - ts_));
+      atomicAdd(slot + 1, (unsigned long long)(tle_ - tl0_));
+      atomicAdd(slot + 2, (unsigned long long)(tep_ - tle_));
+      atomicAdd(slot + 3, (unsigned long long)(clock64() - tep_));
+    }
+#endif
   } else {
     // small radix: one thread per representative DFT, fully unrolled in registers
     for (int d0 = 0; d0 < ndft; d0 += nth) {
@@ -579,9 +616,23 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
   }
 }
 
-template <int Q0, int Q1, int NL, int NW, int TPW>
-__device__ __forceinline__ void half_transform(double2* buf, const PfaPlan& pl, int stages) {
+// shared-memory coefficient tables of the CSM variant: [Cm0][Sm0][Cm1][Sm1], KP x RP each
+template <class SH>
+struct HalfCoef {
+  using S0 = HalfStage<SH, 0>;
+  using S1 = HalfStage<SH, 1>;
+  static constexpr int n0 = S0::KP * S0::RP, n1 = S1::KP * S1::RP;
+  static constexpr int total = 2 * (n0 + n1);
+};
+
+template <int Q0, int Q1, int NL, int NW, int TPW, bool CSM = false>
+__device__ __forceinline__ void half_transform(double2* buf, const PfaPlan& pl, int stages,
+                                               const double* cs = nullptr) {
   using SH = HalfShape<Q0, Q1>;
-  if (stages >= 1) half_stage<HalfStage<SH, 0>, NL, NW, TPW>(buf, pl.st[0].Cm, pl.st[0].Sm);
+  using HC = HalfCoef<SH>;
+  // stage 0 (the wide radix) reads its fragments from the shared copy when CSM
+  const double* c0 = CSM ? cs : pl.st[0].Cm;
+  const double* s0 = CSM ? cs + HC::n0 : pl.st[0].Sm;
+  if (stages >= 1) half_stage<HalfStage<SH, 0>, NL, NW, TPW, CSM>(buf, c0, s0);
   if (stages >= 2) half_stage<HalfStage<SH, 1>, NL, NW, TPW>(buf, pl.st[1].Cm, pl.st[1].Sm);
 }

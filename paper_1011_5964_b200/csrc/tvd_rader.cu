@@ -1,0 +1,378 @@
+// Rader DST-I engine for prime odd-core lengths (config 5: L = n - 1 = 8191).
+//
+// The DST-I of a line is the complex DFT of length L of the packed odd sequence c'
+// (tvd_pfa.cu header).  For prime L, Rader's algorithm turns the DFT into a cyclic
+// convolution of length M = L - 1 (g a generator of Z_L^*):
+//   C_{g^-m} = c'_0 + sum_n c'_{g^n} w^{g^(n - m)},   w = exp(-2 pi i / L),
+// i.e. a = (c'_{g^n})_n convolved with b = (w^{g^-q})_q.  c'_0 = 0 here (z_0 = z_L = 0).
+// One line per CTA: the pack writes c'_j straight into Rader order (discrete-log table;
+// the odd partner -j sits M/2 further), a forward Stockham FFT of length M runs in shared
+// memory, the product with B = FFT_M(b) (host-built) is conjugated so a second forward FFT
+// gives the inverse, and the unpack gathers C_k through the inverse-log table.
+// M = 8190 = 2 3 3 5 7 13 keeps every stage's items in registers (compile-time slots).
+// Reference semantics: transforms.py:52-81 (dst1_apply / sinehat_apply).
+#include <cstdlib>
+
+#include "tvd_internal.h"
+#include "tvd_rader.h"
+
+namespace tvd {
+namespace {
+
+constexpr int kRaderThreads = 512;
+
+// (cos, sin)(2 pi t / R) for t in [0, R), computed once per stage
+template <int R>
+__device__ __forceinline__ void odd_table(double2 (&cs)[R]) {
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    double s, c;
+    sincospi(2.0 * t / R, &s, &c);
+    cs[t] = make_double2(c, s);
+  }
+}
+
+// forward DFT of an odd-length register vector with a precomputed table (see dft_odd_reg)
+template <int R>
+__device__ __forceinline__ void dft_odd_cs(double2 (&v)[R], const double2 (&cs)[R]) {
+  constexpr int H = (R - 1) / 2;
+  double2 a[H + 1], b[H + 1];
+  const double2 x0 = v[0];
+  double2 s0 = x0;
+#pragma unroll
+  for (int r = 1; r <= H; ++r) {
+    a[r] = cadd(v[r], v[R - r]);
+    b[r] = csub(v[r], v[R - r]);
+    s0 = cadd(s0, a[r]);
+  }
+#pragma unroll
+  for (int k = 1; k <= H; ++k) {
+    double2 A = make_double2(0.0, 0.0), B = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 1; r <= H; ++r) {
+      const double2 w = cs[(r * k) % R];
+      A.x += a[r].x * w.x; A.y += a[r].y * w.x;
+      B.x += b[r].x * w.y; B.y += b[r].y * w.y;
+    }
+    v[k] = make_double2(x0.x + A.x + B.y, x0.y + A.y - B.x);
+    v[R - k] = make_double2(x0.x + A.x - B.y, x0.y + A.y + B.x);
+  }
+  v[0] = s0;
+}
+
+template <int R>
+__device__ __forceinline__ void dft_any(double2 (&v)[R], const double2 (&cs)[R]) {
+  if constexpr (R == 2 || R == 4 || R == 8 || R == 3 || R == 5 || R == 7 || R == 13) {
+    dft_reg<R>(v);
+  } else {
+    dft_odd_cs<R>(v, cs);
+  }
+}
+
+// One in-place Stockham stage of a single line of length M (see tvd_fft.cuh stage_reg):
+// every item of the line sits in registers across the barrier (SLOTS items per thread).
+template <int R, int SLOTS>
+__device__ __forceinline__ void rader_stage(double2* buf, int M, int ns,
+                                            const double2* __restrict__ tw) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int nb = M / R, tstride = M / (ns * R);
+  double2 cs[R];
+  if constexpr (!(R == 2 || R == 4 || R == 8 || R == 3 || R == 5 || R == 7 || R == 13)) odd_table<R>(cs);
+  double2 v[SLOTS][R];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const int j = tid + s * nth;
+    if (j < nb) {
+      const int jm = j % ns;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double2 x = buf[j + r * nb];
+        if (r > 0 && ns > 1) x = cmul(x, __ldg(&tw[r * jm * tstride]));
+        v[s][r] = x;
+      }
+      dft_any<R>(v[s], cs);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const int j = tid + s * nth;
+    if (j < nb) {
+      const int jm = j % ns;
+      const int d = (j / ns) * ns * R + jm;
+#pragma unroll
+      for (int r = 0; r < R; ++r) buf[d + r * ns] = v[s][r];
+    }
+  }
+  __syncthreads();
+}
+
+// Compile-time stage lists (radix, register items per thread at kRaderThreads) of the
+// supported convolution lengths; must match build_rader_plan's factorisation.
+template <int M>
+struct RaderStages;
+template <>
+struct RaderStages<8190> {  // 8190 = 2 3 3 5 7 13
+  // items per thread at 512 threads: 4095 / 2730 / 1638 / 1170 / 630 -> 8 / 6 / 4 / 3 / 2
+  __device__ static void fft(double2* buf, const double2* tw) {
+    rader_stage<2, 8>(buf, 8190, 1, tw);
+    rader_stage<3, 6>(buf, 8190, 2, tw);
+    rader_stage<3, 6>(buf, 8190, 6, tw);
+    rader_stage<5, 4>(buf, 8190, 18, tw);
+    rader_stage<7, 3>(buf, 8190, 90, tw);
+    rader_stage<13, 2>(buf, 8190, 630, tw);
+  }
+};
+
+// a <- conj(FFT(a) * Bh) in place, then FFT again: a_m = M conj(conv_m)
+template <int M>
+__device__ __forceinline__ void rader_convolve(double2* buf, const RaderPlan& P) {
+  RaderStages<M>::fft(buf, P.tw);
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    const double2 x = cmul(buf[m], __ldg(&P.bh[m]));
+    buf[m] = make_double2(x.x, -x.y);
+  }
+  __syncthreads();
+  RaderStages<M>::fft(buf, P.tw);
+}
+
+struct RaderK {
+  RaderPlan pl;
+  int n, off, nlines;
+  double scale;  // 0.5 sqrt(2 / L) / M  (the 1/M of the inverse FFT folded in)
+  LineIO io;
+};
+
+// One line (row) per CTA: row-major in, row-major out.
+template <int MC>
+__global__ void __launch_bounds__(kRaderThreads, 1) k_rader_rows(const RaderK p) {
+  const LineIO& io = p.io;
+  if (io.skip && *io.skip) return;
+  extern __shared__ __align__(16) double2 rbuf[];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nth = blockDim.x, n = p.n, line = blockIdx.x;
+  constexpr int M = MC;
+  const long rb = (long)line * n + p.off - 1;  // rb + t = element t (1..M) of the row
+  const int half = M / 2;
+  auto pack = [&](int t, double x) {
+    const int q = (int)__ldg(&p.pl.rin[t - 1]);
+    double* b = reinterpret_cast<double*>(rbuf) + (t & 1);
+    b[2 * q] = x;
+    int q2 = q + half;
+    if (q2 >= M) q2 -= M;
+    b[2 * q2] = -x;
+  };
+  auto unpack = [&](int k) {
+    const double2 R = rbuf[__ldg(&p.pl.rout[k - 1])];  // C = conj(R) / M, 1/M in scale
+    return ((k & 1) ? -(R.x - R.y) : -(-R.y - R.x)) * p.scale;
+  };
+  for (int t = 1 + tid; t <= M; t += nth) {
+    double x = io.in[rb + t];
+    if (io.pre) x = io.pre_mul ? x * io.pre[rb + t] : x / io.pre[rb + t];
+    pack(t, x);
+  }
+  __syncthreads();
+  rader_convolve<MC>(rbuf, p.pl);
+  if (io.mid_mul) {
+    constexpr int kV = (MC + kRaderThreads - 1) / kRaderThreads;
+    double v[kV];
+#pragma unroll
+    for (int s = 0; s < kV; ++s) {
+      const int t = 1 + tid + s * nth;
+      v[s] = t <= M ? unpack(t) * io.mid_mul[rb + t] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < kV; ++s) {
+      const int t = 1 + tid + s * nth;
+      if (t <= M) pack(t, v[s]);
+    }
+    __syncthreads();
+    rader_convolve<MC>(rbuf, p.pl);
+  }
+  double acc = 0.0;
+  for (int t = 1 + tid; t <= M; t += nth) {
+    double y = unpack(t);
+    if (io.post) y = io.post_mul ? y * io.post[rb + t] : y / io.post[rb + t];
+    io.out[rb + t] = y;
+    if (io.dot_with) acc += y * io.dot_with[rb + t];
+  }
+  if (p.off && tid < 2) {  // Shat borders pass through every transform
+    const long g = (long)line * n + (tid ? n - 1 : 0);
+    double v = io.in[g];
+    if (io.pre) v = io.pre_mul ? v * io.pre[g] : v / io.pre[g];
+    if (io.mid_mul) v *= io.mid_mul[g];
+    if (io.post) v = io.post_mul ? v * io.post[g] : v / io.post[g];
+    io.out[g] = v;
+    if (io.dot_with) acc += v * io.dot_with[g];
+  }
+  if (io.partial) {
+    const double s = block_sum(acc, red);
+    if (tid == 0) io.partial[blockIdx.x] = s;
+    if (io.fin.s) pcg_fin_tail(io.fin, io.partial, gridDim.x, red);
+  }
+}
+
+}  // namespace
+
+bool rader_launchable(const RaderPlan& P, int len, int family) {
+  return P.M == 8190 && (family == kFamSineHat ? len == P.M + 2 : len == P.M);
+}
+
+cudaError_t launch_rader_rows(const RaderPlan& P, int family, int len, int nlines,
+                              const LineIO& io, int* nblocks_out, cudaStream_t st) {
+  if (!rader_launchable(P, len, family)) return cudaErrorInvalidConfiguration;
+  RaderK k{};
+  k.pl = P;
+  k.n = len;
+  k.off = family == kFamSineHat ? 1 : 0;
+  k.nlines = nlines;
+  k.scale = 0.5 * sqrt(2.0 / (P.M + 1)) / P.M;
+  k.io = io;
+  const size_t smem = (size_t)P.M * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rader_rows<8190>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  if (nblocks_out) *nblocks_out = nlines;
+  if (nlines == 0) return cudaSuccess;
+  k_rader_rows<8190><<<nlines, kRaderThreads, smem, st>>>(k);
+  return cudaGetLastError();
+}
+
+int rader_threads() { return kRaderThreads; }
+
+}  // namespace tvd
+
+// ------------------------------------------------------------------- host plan
+#include <cmath>
+
+namespace tvd {
+namespace {
+
+long long powmod(long long b, long long e, long long m) {
+  long long r = 1 % m;
+  b %= m;
+  while (e > 0) {
+    if (e & 1) r = r * b % m;
+    b = b * b % m;
+    e >>= 1;
+  }
+  return r;
+}
+
+template <class T>
+bool upload_vec(const std::vector<T>& h, const T** out, std::vector<void*>& owned) {
+  void* d = nullptr;
+  if (cudaMalloc(&d, h.size() * sizeof(T)) != cudaSuccess) return false;
+  owned.push_back(d);
+  if (cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+    return false;
+  *out = static_cast<const T*>(d);
+  return true;
+}
+
+// (cos, sin)(2 pi e / m) with exact integer reduction, long double
+void cis_ld(long long e, long long m, long double* c, long double* s) {
+  e %= m;
+  if (e < 0) e += m;
+  const long double a = 2.0L * 3.14159265358979323846264338327950288L * (long double)e / (long double)m;
+  *c = cosl(a);
+  *s = sinl(a);
+}
+
+}  // namespace
+
+bool build_rader_plan(int L, RaderPlan* P, std::vector<void*>& owned) {
+  *P = RaderPlan{};
+  if (L < 5 || L - 1 > 8190) return false;
+  for (int d = 2; (long long)d * d <= L; ++d)
+    if (L % d == 0) return false;  // not prime
+  const int M = L - 1;
+  // stages: the length-M FFT factors into codelet radices
+  std::vector<int> rad;
+  int m = M;
+  for (int p : {8, 4, 2, 3, 5, 7, 11, 13})
+    while (m % p == 0) {
+      rad.push_back(p);
+      m /= p;
+    }
+  if (m != 1 || (int)rad.size() > kRaderMaxStages) return false;
+  const int nth = rader_threads();
+  P->L = L;
+  P->M = M;
+  P->nst = (int)rad.size();
+  int ns = 1;
+  for (int s = 0; s < P->nst; ++s) {
+    const int items = M / rad[s];
+    int sl = (items + nth - 1) / nth;
+    if (sl > 8) return false;
+    P->radix[s] = rad[s];
+    P->ns[s] = ns;
+    P->slots[s] = sl;
+    ns *= rad[s];
+  }
+  // generator of Z_L^*
+  std::vector<int> primes;
+  for (int x = M, d = 2; x > 1; ++d)
+    if (x % d == 0) {
+      primes.push_back(d);
+      while (x % d == 0) x /= d;
+    }
+  int g = 2;
+  for (;; ++g) {
+    bool ok = true;
+    for (int p : primes)
+      if (powmod(g, M / p, L) == 1) ok = false;
+    if (ok) break;
+  }
+  P->g = g;
+  std::vector<int> dlog(L, -1);
+  long long pw = 1;
+  for (int e = 0; e < M; ++e) {
+    dlog[pw] = e;
+    pw = pw * g % L;
+  }
+  const int h = (L - 1) / 2;
+  std::vector<unsigned> rin(M), rout(M);
+  for (int t = 1; t <= M; ++t) {
+    int j = (t & 1) == 0 ? t / 2 : (t - 1) / 2 - h;
+    if (j < 0) j += L;
+    rin[t - 1] = (unsigned)dlog[j];
+    rout[t - 1] = (unsigned)((M - dlog[t]) % M);
+  }
+  // b_q = w^{g^-q}; bh = FFT_M(b) (direct, long double)
+  const long long ginv = powmod(g, M - 1, L);
+  std::vector<long double> bre(M), bim(M), cm(M), sm(M);
+  pw = 1;
+  for (int q = 0; q < M; ++q) {
+    long double c, s;
+    cis_ld(pw, L, &c, &s);
+    bre[q] = c;
+    bim[q] = -s;
+    pw = pw * ginv % L;
+  }
+  for (int e = 0; e < M; ++e) cis_ld(e, M, &cm[e], &sm[e]);
+  std::vector<double2> bh(M), tw(M);
+  for (int k = 0; k < M; ++k) {
+    long double xr = 0, xi = 0;
+    int idx = 0;
+    for (int q = 0; q < M; ++q) {  // sum_q b_q exp(-2 pi i q k / M)
+      const long double c = cm[idx], s = sm[idx];
+      xr += bre[q] * c + bim[q] * s;
+      xi += bim[q] * c - bre[q] * s;
+      idx += k;
+      if (idx >= M) idx -= M;
+    }
+    bh[k] = make_double2((double)xr, (double)xi);
+    tw[k] = make_double2((double)cm[k], -(double)sm[k]);
+  }
+  if (!upload_vec(rin, &P->rin, owned) || !upload_vec(rout, &P->rout, owned) ||
+      !upload_vec(bh, &P->bh, owned) || !upload_vec(tw, &P->tw, owned))
+    return false;
+  return true;
+}
+
+}  // namespace tvd

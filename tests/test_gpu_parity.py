@@ -241,6 +241,23 @@ def test_preconditioner_vs_oracle_large(n, kind, rng):
     assert rel_err(pre.apply_inverse(r), O.precond_solve(fam, lam_inv, r, d_sqrt)) < 1e-12
 
 
+def test_prime_core_preconditioner_8192(rng):
+    """Config-5 size: odd core L = 8191 is prime -> Rader engine.  Round trip (lambda = 1 gives
+    S S = I) and the M^-1 r solve vs the oracle with random positive eigenvalues."""
+    n = 8192
+    w = rng.standard_normal((n, n))
+    wt = torch.from_numpy(w).cuda()
+    one = P.FactoredPreconditioner("M", T.TransformKind.SINE_HAT,
+                                   torch.ones(n, n, dtype=torch.float64, device="cuda"), 1e-3)
+    z = one.apply_inverse(wt)
+    assert float((z - wt).norm() / wt.norm()) < 1e-13
+    lam = rng.uniform(0.5, 2.0, (n, n))
+    pre = P.FactoredPreconditioner("M", T.TransformKind.SINE_HAT,
+                                   torch.from_numpy(lam).cuda(), 1e-3)
+    got = pre.apply_inverse(wt).cpu().numpy()
+    assert rel_err(got, O.precond_solve("sine_hat", 1.0 / lam, w)) < 1e-12
+
+
 def test_preconditioner_rejects_wrong_bc(golden):
     g = golden("ops_n16.npz")
     lop = TV.DiffusionOperator(g["u"], 0.1)
