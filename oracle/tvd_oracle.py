@@ -16,9 +16,11 @@ container has scipy 1.18.1 / numpy 2.3.5; ``tests/test_oracle_golden.py``
 pins this module against outputs of the reference itself
 (``tests/golden/``, produced by ``tests/golden/make_golden.py``).
 
-Scope: 2D, blur BCs REFLECTIVE / ANTI_REFLECTIVE, diffusion BC ZERO_NEUMANN,
-NORMAL formulation, preconditioner selectors NONE / DIAG / X / D_X / X_D
-(families R = DCT and M = SINE_HAT) -- the rows of SURVEY.md section 8.
+Scope: 2D, blur BCs REFLECTIVE / ANTI_REFLECTIVE, diffusion BCs ZERO_NEUMANN /
+ANTI_REFLECTIVE, NORMAL and REBLUR formulations, PCG and right-preconditioned
+BiCGstab, preconditioner selectors NONE / DIAG / X / D_X / X_D (families R = DCT,
+M = SINE_HAT, P = anti-reflective algebra) -- the rows of SURVEY.md section 8
+including row f2.
 """
 
 from __future__ import annotations
@@ -273,12 +275,23 @@ def blur_transpose_fast(u, lam, bc: str) -> np.ndarray:
 # total-variation diffusion  (tv.py:42-175, zero-Neumann ghosts)
 # ---------------------------------------------------------------------------
 
-def diffusivity(u: np.ndarray, beta: float, spacing: float = 1.0):
+def _ghost_pad(u: np.ndarray, bc: str) -> np.ndarray:
+    """One ghost layer (tv.py:27-39): 'zn' copies the border (``symmetric``), 'ar' is the
+    odd reflection ``u_{-1} = 2 u_0 - u_1`` (``reflect``, ``reflect_type='odd'``)."""
+    u = np.asarray(u, dtype=float)
+    if bc == "zn":
+        return np.pad(u, 1, mode="edge")
+    if bc == "ar":
+        return np.pad(u, 1, mode="reflect", reflect_type="odd")
+    raise ValueError(bc)
+
+
+def diffusivity(u: np.ndarray, beta: float, spacing: float = 1.0, bc: str = "zn"):
     """Edge coefficients ``1/sqrt(|grad u|^2 + beta^2)`` (tv.py:42-71).
 
     Returns ``(a_h, a_v)`` of shapes ``n x (n+1)`` and ``(n+1) x n``.
     """
-    g = np.pad(np.asarray(u, dtype=float), 1, mode="edge")   # ZN ghost = border
+    g = _ghost_pad(u, bc)
     dx = (g[:, 1:] - g[:, :-1]) / spacing      # (n+2) x (n+1)
     dy = (g[1:, :] - g[:-1, :]) / spacing      # (n+1) x (n+2)
     cross_x = 0.25 * (dy[:-1, :-1] + dy[1:, :-1] + dy[:-1, 1:] + dy[1:, 1:])
@@ -289,30 +302,40 @@ def diffusivity(u: np.ndarray, beta: float, spacing: float = 1.0):
     return a_h, a_v
 
 
-def diffusion_apply(a_h, a_v, w, spacing: float = 1.0) -> np.ndarray:
-    """5-point flux form ``L w`` with zero-Neumann ghosts (tv.py:96-108)."""
-    g = np.pad(np.asarray(w, dtype=float), 1, mode="edge")
+def diffusion_apply(a_h, a_v, w, spacing: float = 1.0, bc: str = "zn") -> np.ndarray:
+    """5-point flux form ``L w`` with zero-Neumann or AR ghosts (tv.py:96-108)."""
+    g = _ghost_pad(w, bc)
     fx = a_h * (g[1:-1, 1:] - g[1:-1, :-1])
     fy = a_v * (g[1:, 1:-1] - g[:-1, 1:-1])
     return -(1.0 / (spacing * spacing)) * ((fx[:, 1:] - fx[:, :-1]) + (fy[1:, :] - fy[:-1, :]))
 
 
-def diffusion_bands(a_h, a_v, spacing: float = 1.0):
-    """Block bands of L (tv.py:138-175, ZN branch).
+def diffusion_bands(a_h, a_v, spacing: float = 1.0, bc: str = "zn"):
+    """Block bands of L (tv.py:138-175).
 
     Returns ``{(block_off, inner_off): array}`` with the reference's layout:
-    (0,0) n x n, (0,+-1) n x (n-1), (+-1,0) (n-1) x n.
+    (0,0) n x n, (0,+-1) n x (n-1), (+-1,0) (n-1) x n.  With AR ghosts the border
+    cells lose twice their boundary edge and the first / last off-diagonals gain it
+    (``w_{-1} = 2 w_0 - w_1``), so the +-1 bands differ at one end.
     """
     s = 1.0 / (spacing * spacing)
     diag = a_h[:, :-1] + a_h[:, 1:] + a_v[:-1, :] + a_v[1:, :]
-    diag[:, 0] -= a_h[:, 0]
-    diag[:, -1] -= a_h[:, -1]
-    diag[0, :] -= a_v[0, :]
-    diag[-1, :] -= a_v[-1, :]
-    inner = -a_h[:, 1:-1]
-    block = -a_v[1:-1, :]
-    return {(0, 0): s * diag, (0, 1): s * inner, (0, -1): s * inner.copy(),
-            (1, 0): s * block, (-1, 0): s * block.copy()}
+    inner_up = -a_h[:, 1:-1]
+    inner_lo = -a_h[:, 1:-1]
+    block_up = -a_v[1:-1, :]
+    block_lo = -a_v[1:-1, :]
+    k = 1.0 if bc == "zn" else 2.0
+    diag[:, 0] -= k * a_h[:, 0]
+    diag[:, -1] -= k * a_h[:, -1]
+    diag[0, :] -= k * a_v[0, :]
+    diag[-1, :] -= k * a_v[-1, :]
+    if bc == "ar":
+        inner_up[:, 0] += a_h[:, 0]
+        inner_lo[:, -1] += a_h[:, -1]
+        block_up[0, :] += a_v[0, :]
+        block_lo[-1, :] += a_v[-1, :]
+    return {(0, 0): s * diag, (0, 1): s * inner_up, (0, -1): s * inner_lo,
+            (1, 0): s * block_up, (-1, 0): s * block_lo}
 
 
 # ---------------------------------------------------------------------------
@@ -376,7 +399,39 @@ def project_1d(family: str, bands: dict, n: int) -> np.ndarray:
                 inner = inner + _sine_band(sub, d, n - 2)
         out[..., 1:-1] = inner
         return out
+    if family == "ar":
+        # anti-reflective algebra (precond.py:156-165, 186-196): sine projection of the
+        # interior, its first-column representer z, border eigenvalue 2 sum(z) - z_0
+        if n < 5:
+            raise ValueError("anti-reflective projection requires n >= 5")
+        inner = np.zeros(shape + (n - 2,))
+        for d, b in bands.items():
+            sub = np.asarray(b, dtype=float)[..., 1: n - 1 - abs(d)]
+            if sub.shape[-1] > 0:
+                inner = inner + _sine_band(sub, d, n - 2)
+        z = _z_from_sine(inner)
+        border = 2.0 * z.sum(axis=-1) - z[..., 0]
+        out = np.zeros(shape + (n,))
+        out[..., 0] = border
+        out[..., 1:-1] = inner
+        out[..., -1] = border
+        return out
     raise ValueError(family)
+
+
+def _z_from_sine(lam: np.ndarray) -> np.ndarray:
+    """First-column representer of ``S diag(lam) S`` (precond.py:134-153): the first
+    column is ``S (lam * s_1)`` and equals ``z`` minus itself shifted up by two, so
+    ``z_k = col_k + z_{k+2}`` (suffix sums over each parity class)."""
+    size = lam.shape[-1]
+    t = np.arange(1, size + 1)
+    first = np.sqrt(2.0 / (size + 1)) * np.sin(t * np.pi / (size + 1))
+    col = dst1(lam * first)
+    z = col.copy()
+    for par in (size - 1, size - 2):
+        if par >= 0:
+            z[..., par::-2] = np.cumsum(col[..., par::-2], axis=-1)
+    return z
 
 
 def project_2d(family: str, blocks: dict, n: int) -> np.ndarray:
@@ -388,7 +443,7 @@ def project_2d(family: str, blocks: dict, n: int) -> np.ndarray:
     return project_1d(family, stage2, n).T
 
 
-FAMILY = {"R": "dct", "M": "sine_hat"}
+FAMILY = {"R": "dct", "M": "sine_hat", "P": "ar"}
 
 
 def scale_blocks(blocks: dict, s: np.ndarray) -> dict:
@@ -498,14 +553,81 @@ def pcg(apply_a, apply_minv, b, x0, tol: float, max_iterations: int,
     return x, max_iterations, np.array(hist), False
 
 
+class SolverBreakdown(RuntimeError):
+    def __init__(self, iteration, reason):
+        super().__init__(f"pbicgstab breakdown at iteration {iteration}: {reason}")
+        self.iteration, self.reason = iteration, reason
+
+
+def pbicgstab(apply_a, apply_minv, b, x0, tol: float, max_iterations: int,
+              record_history: bool = False):
+    """Right-preconditioned BiCGstab with the reference's checks (krylov.py:119-174).
+
+    Returns ``(x, iterations, history, converged)``.
+    """
+    minv = apply_minv or (lambda t: t)
+    dot = lambda a, c: float(np.dot(a.ravel(), c.ravel()))  # noqa: E731
+    b = np.asarray(b, dtype=float)
+    x = np.array(x0, dtype=float, copy=True)
+    r = b - apply_a(x)
+    r0 = float(np.sqrt(dot(r, r)))
+    hist: list[float] = []
+    if r0 == 0.0:
+        return x, 0, np.array(hist), True
+    rs = r.copy()
+    rho, alpha, omega = 1.0, 1.0, 1.0
+    v = np.zeros_like(r)
+    p = np.zeros_like(r)
+    for k in range(1, max_iterations + 1):
+        rho_next = dot(rs, r)
+        if abs(rho_next) < 1e-30 * r0 * r0:
+            raise SolverBreakdown(k, "rho vanished")
+        beta = (rho_next / rho) * (alpha / omega)
+        p = r + beta * (p - omega * v)
+        p_hat = minv(p)
+        v = apply_a(p_hat)
+        denom = dot(rs, v)
+        if abs(denom) < 1e-300:
+            raise SolverBreakdown(k, "shadow angle vanished")
+        alpha = rho_next / denom
+        s = r - alpha * v
+        rel = float(np.sqrt(dot(s, s))) / r0
+        if not np.isfinite(rel):
+            raise PcgDivergence(k)
+        if rel < tol:
+            x += alpha * p_hat
+            if record_history:
+                hist.append(rel)
+            return x, k, np.array(hist), True
+        s_hat = minv(s)
+        t = apply_a(s_hat)
+        tt = dot(t, t)
+        if tt == 0.0:
+            raise SolverBreakdown(k, "stabilizer direction vanished")
+        omega = dot(t, s) / tt
+        if abs(omega) < 1e-300:
+            raise SolverBreakdown(k, "omega vanished")
+        x += alpha * p_hat + omega * s_hat
+        r = s - omega * t
+        rel = float(np.sqrt(dot(r, r))) / r0
+        if not np.isfinite(rel):
+            raise PcgDivergence(k)
+        if record_history:
+            hist.append(rel)
+        if rel < tol:
+            return x, k, np.array(hist), True
+        rho = rho_next
+    return x, max_iterations, np.array(hist), False
+
+
 # ---------------------------------------------------------------------------
-# fixed-point driver  (pipeline.py:129-276, NORMAL + ZN path)
+# fixed-point driver  (pipeline.py:129-276)
 # ---------------------------------------------------------------------------
 
 def restore(v, h, bc: str, alpha: float, beta: float, selector: str = "x",
             fp_tol: float = 1e-300, fp_max: int = 10, tol: float = 1e-4,
             max_iterations: int = 2000, spacing: float = 1.0, fast: bool = True,
-            pcg_hook=None):
+            pcg_hook=None, reblur: bool = False, bc_l: str = "zn"):
     """Lagged-diffusivity loop of ``pipeline.restore`` (pipeline.py:182-251).
 
     ``selector`` in {'none', 'diag', 'x', 'd_x', 'x_d'}.  ``pcg_hook``, if
@@ -522,19 +644,22 @@ def restore(v, h, bc: str, alpha: float, beta: float, selector: str = "x",
     else:
         fwd = lambda w: blur(w, h, bc)                                # noqa: E731
         back = fwd if bc == "reflective" else (lambda w: blur_transpose(w, h, bc))
+    if reblur:  # re-blurred normal equations: H applied twice (pipeline.py:173-174)
+        back = fwd
     rhs = back(v)
-    base = "R" if bc == "reflective" else "M"
+    base = "R" if bc == "reflective" else ("P" if reblur else "M")
     fam = FAMILY[base]
-    solve = pcg_hook or pcg
+    symmetric = not reblur and bc_l == "zn"  # pipeline.py:196-198
+    solve = pcg_hook or (pcg if symmetric else pbicgstab)
     u = v.copy()
     counts, grads = [], []
     fp_converged, inner_ok = False, True
     for _ in range(fp_max):
-        a_h, a_v = diffusivity(u, beta, spacing)
-        blocks = diffusion_bands(a_h, a_v, spacing)
+        a_h, a_v = diffusivity(u, beta, spacing, bc_l)
+        blocks = diffusion_bands(a_h, a_v, spacing, bc_l)
 
         def apply_a(w, a_h=a_h, a_v=a_v):
-            return back(fwd(w)) + alpha * diffusion_apply(a_h, a_v, w, spacing)
+            return back(fwd(w)) + alpha * diffusion_apply(a_h, a_v, w, spacing, bc_l)
 
         grads.append(float(np.linalg.norm((apply_a(u) - rhs).ravel())))
         if selector == "x_d":

@@ -18,6 +18,10 @@ Files written:
   reflective + R) and config 2a/2b (512^2).
 * ``restore_c3_head.npz`` (``--big``) -- the 2048^2 headline config, first
   FP steps only (counts + image checksums; the image itself is 32 MB).
+* ``f2_ops_n{N}.npz`` / ``restore_c1_reblur_*.npz`` (``--f2``) -- row f2:
+  anti-reflective-BC diffusion, the AR transform T and its inverse / transposes, the
+  re-blurred matvec, P-family eigenvalues and solves, right-preconditioned BiCGstab, and
+  full restores of the AR+Reblur+ZN / AR+Reblur+AR configurations.
 """
 
 from __future__ import annotations
@@ -38,9 +42,9 @@ from tvdeblur import harness as rh  # noqa: E402
 from tvdeblur import precond as rp  # noqa: E402
 from tvdeblur import transforms as rt  # noqa: E402
 from tvdeblur.blur import BoundaryCondition, StructuredBlurOperator, SymmetricPsf  # noqa: E402
-from tvdeblur.krylov import KrylovConfig  # noqa: E402
-from tvdeblur.pipeline import PrecondSelector, RestorationConfig, restore  # noqa: E402
-from tvdeblur.tv import DiffusionOperator  # noqa: E402
+from tvdeblur.krylov import KrylovConfig, pbicgstab  # noqa: E402
+from tvdeblur.pipeline import Formulation, PrecondSelector, RestorationConfig, restore  # noqa: E402
+from tvdeblur.tv import DiffusionBc, DiffusionOperator  # noqa: E402
 
 from paper_1011_5964_b200 import harness as bh  # noqa: E402
 
@@ -103,9 +107,54 @@ def ops_fixture(n: int, seed: int) -> dict:
     return out
 
 
+def f2_ops_fixture(n: int, seed: int) -> dict:
+    rng = np.random.default_rng(seed)
+    out: dict[str, np.ndarray] = {}
+    u = rng.standard_normal((n, n)).cumsum(axis=1) * 0.1
+    w = rng.standard_normal((n, n))
+    out["u"], out["w"] = u, w
+    beta, alpha = 0.1, 1e-3
+    out["alpha"], out["beta"] = np.array(alpha), np.array(beta)
+    h = rh.gen_psf("gaussian", 3, 1.3).coefficients
+    out["psf"] = h
+    lops = {"zn": DiffusionOperator(u, beta), "ar": DiffusionOperator(u, beta, DiffusionBc.ANTI_REFLECTIVE)}
+    lar = lops["ar"]
+    out["a_h_ar"], out["a_v_ar"] = lar.a_h, lar.a_v
+    out["Lw_ar"] = lar.apply(w)
+    out["diagL_ar"] = lar.diagonal()
+    for (do, di), band in lar.block_banded().items():
+        out[f"band_ar_{do}_{di}"] = band
+    ark = rt.TransformKind.ANTI_REFLECTIVE
+    for inv in (False, True):
+        for tr in (False, True):
+            out[f"AR2_{int(inv)}{int(tr)}"] = rt.tensor_apply_2d(ark, w, inverse=inv, transpose=tr)
+    op = StructuredBlurOperator(SymmetricPsf(h), BoundaryCondition.ANTI_REFLECTIVE, n)
+    out["HHw"] = op.apply(op.apply(w))
+    for bcl, lop in lops.items():
+        out[f"reblur_Aw_{bcl}"] = op.apply(op.apply(w)) + alpha * lop.apply(w)
+        for kind in ("P", "D_P", "P_D"):
+            pre = rp.assemble_preconditioner(kind, op, lop, alpha)
+            out[f"lam_{kind}_{bcl}"] = pre.eigenvalues
+            out[f"minv_{kind}_{bcl}"] = pre.apply_inverse(w)
+    pre_p = rp.assemble_preconditioner("P", op, lar, alpha)
+
+    def apply_a(x):
+        return op.apply(op.apply(x)) + alpha * lar.apply(x)
+
+    b = op.apply(w)
+    out["bicg_b"] = b
+    for name, minv in (("none", None), ("P", pre_p.apply_inverse)):
+        res = pbicgstab(apply_a, minv, b, u,
+                        KrylovConfig(tol=1e-8, max_iterations=400, record_history=True))
+        out[f"bicg_{name}_x"] = res.solution
+        out[f"bicg_{name}_its"] = np.array(res.iterations)
+        out[f"bicg_{name}_hist"] = np.asarray(res.residual_history)
+    return out
+
+
 def restore_fixture(spec: bh.ProblemSpec, selector: str, bc: str | None = None,
                     fp_steps: int | None = None, keep_image: bool = True,
-                    fast: bool = True) -> dict:
+                    fast: bool = True, bc_l: str = "zn", reblur: bool = False) -> dict:
     m = spec.m
     psf = rh.gen_psf("gaussian", m, spec.sigma)
     ext = bh.gen_piecewise_image(spec.n, m, spec.rects, spec.disks, 2023, spec.ramp)
@@ -115,6 +164,8 @@ def restore_fixture(spec: bh.ProblemSpec, selector: str, bc: str | None = None,
     cfg = RestorationConfig(
         bc_h=BCS[bc], alpha=spec.alpha, beta=spec.beta,
         preconditioner=PrecondSelector(selector), fp_tol=1e-300,
+        bc_l=DiffusionBc.ANTI_REFLECTIVE if bc_l == "ar" else DiffusionBc.ZERO_NEUMANN,
+        formulation=Formulation.REBLUR if reblur else Formulation.NORMAL,
         fp_max=fp_steps or spec.fp_steps,
         inner=KrylovConfig(tol=spec.tol, max_iterations=2000), use_fast_blur=fast)
     t0 = time.perf_counter()
@@ -143,8 +194,20 @@ def main() -> None:
     ap.add_argument("--big", action="store_true", help="also run the 2048^2 head")
     ap.add_argument("--big-steps", type=int, default=3)
     ap.add_argument("--only-exact", action="store_true")
+    ap.add_argument("--f2", action="store_true", help="only the row-f2 fixtures")
     args = ap.parse_args()
     print("reference tvdeblur from", tvdeblur.__file__)
+    if args.f2:
+        for n, seed in ((32, 21), (33, 22)):
+            np.savez_compressed(HERE / f"f2_ops_n{n}.npz", **f2_ops_fixture(n, seed))
+            print("wrote f2 ops", n)
+        c1 = bh.CONFIGS["c1"]
+        for bcl in ("zn", "ar"):
+            for sel in ("none", "diag", "x", "d_x", "x_d"):
+                np.savez_compressed(HERE / f"restore_c1_reblur_{bcl}_{sel}.npz",
+                                    **restore_fixture(c1, sel, bc_l=bcl, reblur=True,
+                                                      fp_steps=4))
+        return
     if "--only-exact" in sys.argv:
         np.savez_compressed(HERE / "restore_c1_I_exact.npz",
                             **restore_fixture(bh.CONFIGS["c1"], "none", fast=False))

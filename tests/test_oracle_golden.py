@@ -103,3 +103,79 @@ def test_oracle_restore_reproduces_reference(golden, name, selector, bc, fast):
     assert rep["inner_iterations"] == ref
     assert rel_err(rep["restored"], g["restored"]) < 1e-10
     np.testing.assert_allclose(rep["gradient_norms"], g["gradient_norms"], rtol=1e-9)
+
+
+# ------------------------------------------------------------------ row f2
+F2_OPS = ["f2_ops_n32.npz", "f2_ops_n33.npz"]
+
+
+@pytest.mark.parametrize("name", F2_OPS)
+def test_oracle_f2_ar_diffusion_bit_identical(golden, name):
+    g = golden(name)
+    ah, av = O.diffusivity(g["u"], float(g["beta"]), bc="ar")
+    assert np.array_equal(ah, g["a_h_ar"]) and np.array_equal(av, g["a_v_ar"])
+    assert np.array_equal(O.diffusion_apply(ah, av, g["w"], bc="ar"), g["Lw_ar"])
+    bands = O.diffusion_bands(ah, av, bc="ar")
+    for (do, di), b in bands.items():
+        assert np.array_equal(b, g[f"band_ar_{do}_{di}"])
+    assert np.array_equal(bands[(0, 0)], g["diagL_ar"])
+
+
+@pytest.mark.parametrize("name", F2_OPS)
+def test_oracle_f2_ar_transforms_reblur_and_p_family(golden, name):
+    g = golden(name)
+    w, h, n = g["w"], g["psf"], g["w"].shape[0]
+    for inv in (0, 1):
+        for tr in (0, 1):
+            assert rel_err(O.tensor_2d("ar", w, bool(inv), bool(tr)), g[f"AR2_{inv}{tr}"]) < 1e-14
+    hh = O.blur(O.blur(w, h, "anti_reflective"), h, "anti_reflective")
+    assert rel_err(hh, g["HHw"]) < 1e-14
+    lam_h = O.blur_eigenvalues(h, "anti_reflective", n)
+    alpha = float(g["alpha"])
+    for bcl in ("zn", "ar"):
+        ah, av = O.diffusivity(g["u"], float(g["beta"]), bc=bcl)
+        blocks = O.diffusion_bands(ah, av, bc=bcl)
+        aw = hh + alpha * O.diffusion_apply(ah, av, w, bc=bcl)
+        assert rel_err(aw, g[f"reblur_Aw_{bcl}"]) < 1e-14
+        for kind in ("P", "D_P", "P_D"):
+            lam, lam_inv, d_sqrt, _ = O.assemble(kind, lam_h, blocks, alpha)
+            assert rel_err(lam, g[f"lam_{kind}_{bcl}"]) < 1e-13
+            assert rel_err(O.precond_solve("ar", lam_inv, w, d_sqrt), g[f"minv_{kind}_{bcl}"]) < 1e-13
+
+
+@pytest.mark.parametrize("name", F2_OPS)
+def test_oracle_f2_bicgstab(golden, name):
+    """P-preconditioned BiCGstab reproduces the reference iteration by iteration.  (The
+    unpreconditioned run to 1e-8 is rounding-chaotic: two exact-blur implementations
+    already stop 14 iterations apart, so it is not a parity gate.)"""
+    g = golden(name)
+    u, h, n, alpha = g["u"], g["psf"], g["u"].shape[0], float(g["alpha"])
+    ah, av = O.diffusivity(u, float(g["beta"]), bc="ar")
+    blocks = O.diffusion_bands(ah, av, bc="ar")
+    _, lam_inv, _, _ = O.assemble("P", O.blur_eigenvalues(h, "anti_reflective", n), blocks, alpha)
+
+    def apply_a(x):
+        return O.blur(O.blur(x, h, "anti_reflective"), h, "anti_reflective") + \
+            alpha * O.diffusion_apply(ah, av, x, bc="ar")
+
+    x, its, hist, ok = O.pbicgstab(apply_a, lambda r: O.precond_solve("ar", lam_inv, r),
+                                   g["bicg_b"], u, 1e-8, 400, True)
+    assert ok and its == int(g["bicg_P_its"])
+    assert rel_err(x, g["bicg_P_x"]) < 1e-12
+    assert np.allclose(hist, g["bicg_P_hist"], rtol=1e-6, atol=1e-13)
+
+
+REBLUR = [(bcl, sel) for bcl in ("zn", "ar") for sel in ("none", "diag", "x", "d_x", "x_d")]
+
+
+@pytest.mark.parametrize("bcl,sel", REBLUR)
+def test_oracle_f2_reblur_restore(golden, bcl, sel):
+    """AR+Reblur+ZN / AR+Reblur+AR (harness.py:56-59) restores: identical per-FP-step
+    BiCGstab counts; image 1e-8 (P family 1e-12), 1e-7 for the unpreconditioned and
+    diagonal selectors whose BiCGstab histories are rounding-sensitive."""
+    g = golden(f"restore_c1_reblur_{bcl}_{sel}.npz")
+    rep = O.restore(g["v"], g["psf"], "anti_reflective", float(g["alpha"]), float(g["beta"]), sel,
+                    fp_max=int(g["fp_max"]), tol=float(g["tol"]), reblur=True, bc_l=bcl)
+    assert list(rep["inner_iterations"]) == list(g["inner_iterations"])
+    tol = 1e-12 if sel in ("x", "d_x", "x_d") else 1e-7
+    assert rel_err(rep["restored"], g["restored"]) < tol
