@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TVD_ABI_VERSION 1
+#define TVD_ABI_VERSION 2
 
 /* status codes -> exception classes of the reference */
 #define TVD_OK 0
@@ -38,16 +38,23 @@ extern "C" {
 #define TVD_ERR_PRECOND 4    /* precond.IndefinitePreconditionerError (:60)   */
 #define TVD_ERR_SCALING 5    /* pipeline.InvalidScalingError (pipeline.py:60) */
 #define TVD_ERR_CUDA 6       /* CUDA runtime failure                          */
+#define TVD_ERR_BREAKDOWN 7  /* krylov.SolverBreakdownError (krylov.py:23-30) */
 
 /* blur boundary conditions (blur.py:34-38; only these two are transform-
  * diagonalisable and in scope) */
 #define TVD_BC_REFLECTIVE 2
 #define TVD_BC_ANTI_REFLECTIVE 3
 
-/* transforms (transforms.py:35-39) */
+/* transforms (transforms.py:35-39); ANTI_REFLECTIVE is T = Shat (I + U) with the rank-2
+ * border corrections (transforms.py:84-140) and also names the P preconditioner family */
 #define TVD_TRANSFORM_DST1 0
 #define TVD_TRANSFORM_SINE_HAT 1
 #define TVD_TRANSFORM_DCT 2
+#define TVD_TRANSFORM_ANTI_REFLECTIVE 3
+
+/* diffusion ghost rules (tv.py:27-39) */
+#define TVD_DBC_ZERO_NEUMANN 0
+#define TVD_DBC_ANTI_REFLECTIVE 1
 
 /* preconditioner variants of one family (precond.py:516-573) */
 #define TVD_VARIANT_X 0   /* |lam_H|^2 + alpha proj(L)                */
@@ -62,8 +69,9 @@ extern "C" {
 typedef struct tvd_ctx tvd_ctx;
 typedef struct tvd_blur tvd_blur;
 
-/* system A w = H^T H w + alpha L w   (pipeline.py:209-210), optionally the
- * diagonally scaled s .* A(s .* w)   (pipeline.py:145-164, selector X_D). */
+/* system A w = H^T H w + alpha L w   (pipeline.py:209-210), the re-blurred
+ * H H w + alpha L w (reblur = 1, pipeline.py:173-174), optionally the diagonally
+ * scaled s .* A(s .* w)   (pipeline.py:145-164, selector X_D). */
 typedef struct tvd_system {
   tvd_blur* blur;
   double alpha;
@@ -71,11 +79,13 @@ typedef struct tvd_system {
   const double* a_h; /* n x (n+1) horizontal diffusivities */
   const double* a_v; /* (n+1) x n vertical diffusivities   */
   const double* s;   /* NULL or n x n scaling              */
+  int bc_l;          /* TVD_DBC_* ghosts of L              */
+  int reblur;        /* 1: H H instead of H^T H            */
 } tvd_system;
 
 typedef struct tvd_precond {
   int kind;              /* TVD_PRECOND_*                                   */
-  int family;            /* TVD_TRANSFORM_SINE_HAT or TVD_TRANSFORM_DCT     */
+  int family;            /* TVD_TRANSFORM_SINE_HAT, _DCT or _ANTI_REFLECTIVE */
   const double* inv_eig; /* TRANSFORM: n x n inverse eigenvalues            */
   const double* d;       /* DIAG: divisor; TRANSFORM: d_sqrt (D_X) or NULL  */
 } tvd_precond;
@@ -123,6 +133,15 @@ int tvd_diffusion_apply(tvd_ctx* ctx, int n, double spacing, const double* a_h, 
 /* block bands: diag n x n, inner (0,+-1) n x (n-1), block (+-1,0) (n-1) x n */
 int tvd_diffusion_bands(tvd_ctx* ctx, int n, double spacing, const double* a_h, const double* a_v,
                         double* diag, double* inner, double* block);
+/* the same with a ghost rule TVD_DBC_* (tv.py:27-39); anti-reflective ghosts make the
+ * (0,+1)/(0,-1) and (+1,0)/(-1,0) bands differ at one end (inner_lo, block_lo: may be NULL) */
+int tvd_diffusivity_bc(tvd_ctx* ctx, int n, double beta, double spacing, int bc_l,
+                       const double* u, double* a_h, double* a_v);
+int tvd_diffusion_apply_bc(tvd_ctx* ctx, int n, double spacing, int bc_l, const double* a_h,
+                           const double* a_v, const double* w, double* out);
+int tvd_diffusion_bands_bc(tvd_ctx* ctx, int n, double spacing, int bc_l, const double* a_h,
+                           const double* a_v, double* diag, double* inner_up, double* inner_lo,
+                           double* block_up, double* block_lo);
 
 /* ---- transforms  (transforms.py:52-171) -------------------------------- */
 /* lines of length `len` (rows of a rows x len array when axis == 1, columns
@@ -163,6 +182,13 @@ int tvd_system_apply(tvd_ctx* ctx, const tvd_system* sys, const double* in, doub
 int tvd_pcg_solve(tvd_ctx* ctx, const tvd_system* sys, const tvd_precond* pre, const double* b,
                   const double* x0, double* x, double tol, int max_iterations, double* history,
                   int* iterations, int* converged, int* err_iteration, double* err_value);
+/* Device-resident right-preconditioned BiCGstab (krylov.py:119-174) for the nonsymmetric
+ * systems (re-blurred and / or anti-reflective L).  Same arguments as tvd_pcg_solve; also
+ * TVD_ERR_BREAKDOWN (*err_value: 1 rho, 2 shadow angle, 3 stabilizer, 4 omega vanished). */
+int tvd_bicgstab_solve(tvd_ctx* ctx, const tvd_system* sys, const tvd_precond* pre,
+                       const double* b, const double* x0, double* x, double tol,
+                       int max_iterations, double* history, int* iterations, int* converged,
+                       int* err_iteration, double* err_value);
 
 /* ---- vector helpers for the generic callable path ---------------------- */
 int tvd_vec_dot(tvd_ctx* ctx, long long count, const double* x, const double* y, double* out);

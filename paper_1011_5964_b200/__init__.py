@@ -9,7 +9,7 @@ fallback: operators raise when the library or a CUDA device is missing.
 """
 
 from .blur import BoundaryCondition, StructuredBlurOperator, SymmetricPsf
-from .krylov import KrylovConfig, SolveOutcome, pcg
+from .krylov import KrylovConfig, SolveOutcome, pbicgstab, pcg
 from .pipeline import (Formulation, NormalSystem, PrecondSelector, RestorationConfig,
                        RestorationReport, restore)
 from .precond import FactoredPreconditioner, assemble_preconditioner
@@ -20,5 +20,5 @@ __all__ = [
     "BoundaryCondition", "DiffusionBc", "DiffusionOperator", "FactoredPreconditioner",
     "Formulation", "KrylovConfig", "NormalSystem", "PrecondSelector", "RestorationConfig",
     "RestorationReport", "SolveOutcome", "StructuredBlurOperator", "SymmetricPsf",
-    "TransformKind", "assemble_preconditioner", "pcg", "restore",
+    "TransformKind", "assemble_preconditioner", "pbicgstab", "pcg", "restore",
 ]

@@ -21,9 +21,10 @@ _lib = None
 _lock = threading.Lock()
 
 TVD_OK, TVD_ERR_INVALID, TVD_ERR_DIVERGED, TVD_ERR_INDEFINITE = 0, 1, 2, 3
-TVD_ERR_PRECOND, TVD_ERR_SCALING, TVD_ERR_CUDA = 4, 5, 6
+TVD_ERR_PRECOND, TVD_ERR_SCALING, TVD_ERR_CUDA, TVD_ERR_BREAKDOWN = 4, 5, 6, 7
 BC_REFLECTIVE, BC_ANTI_REFLECTIVE = 2, 3
-T_DST1, T_SINE_HAT, T_DCT = 0, 1, 2
+T_DST1, T_SINE_HAT, T_DCT, T_ANTI_REFLECTIVE = 0, 1, 2, 3
+DBC_ZERO_NEUMANN, DBC_ANTI_REFLECTIVE = 0, 1
 VARIANT_X, VARIANT_D_X, VARIANT_X_D = 0, 1, 2
 PRE_NONE, PRE_DIAG, PRE_TRANSFORM = 0, 1, 2
 
@@ -35,7 +36,7 @@ _ll = ctypes.c_longlong
 
 class TvdSystem(ctypes.Structure):
     _fields_ = [("blur", _vp), ("alpha", _d), ("spacing", _d),
-                ("a_h", _vp), ("a_v", _vp), ("s", _vp)]
+                ("a_h", _vp), ("a_v", _vp), ("s", _vp), ("bc_l", _i), ("reblur", _i)]
 
 
 class TvdPrecond(ctypes.Structure):
@@ -62,6 +63,9 @@ _SIGNATURES = {
     "tvd_diffusivity": ([_vp, _i, _d, _d, _vp, _vp, _vp], _i),
     "tvd_diffusion_apply": ([_vp, _i, _d, _vp, _vp, _vp, _vp], _i),
     "tvd_diffusion_bands": ([_vp, _i, _d, _vp, _vp, _vp, _vp, _vp], _i),
+    "tvd_diffusivity_bc": ([_vp, _i, _d, _d, _i, _vp, _vp, _vp], _i),
+    "tvd_diffusion_apply_bc": ([_vp, _i, _d, _i, _vp, _vp, _vp, _vp], _i),
+    "tvd_diffusion_bands_bc": ([_vp, _i, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "tvd_transform_lines": ([_vp, _i, _i, _i, _i, _vp, _vp, _i], _i),
     "tvd_transform_2d": ([_vp, _i, _i, _vp, _vp, _i], _i),
     "tvd_precond_assemble": ([_vp, _i, _i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
@@ -73,6 +77,9 @@ _SIGNATURES = {
     "tvd_pcg_solve": ([_vp, ctypes.POINTER(TvdSystem), ctypes.POINTER(TvdPrecond), _vp, _vp, _vp,
                        _d, _i, _vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i),
                        ctypes.POINTER(_d)], _i),
+    "tvd_bicgstab_solve": ([_vp, ctypes.POINTER(TvdSystem), ctypes.POINTER(TvdPrecond), _vp, _vp,
+                            _vp, _d, _i, _vp, ctypes.POINTER(_i), ctypes.POINTER(_i),
+                            ctypes.POINTER(_i), ctypes.POINTER(_d)], _i),
     "tvd_vec_dot": ([_vp, _ll, _vp, _vp, ctypes.POINTER(_d)], _i),
     "tvd_vec_axpby": ([_vp, _ll, _d, _vp, _d, _vp, _vp], _i),
     "tvd_vec_binary": ([_vp, _ll, _i, _vp, _vp, _vp], _i),

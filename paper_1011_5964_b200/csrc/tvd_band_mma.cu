@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
   const int cl = col > 0 ? col - 1 : 0, cr = col + 2 < n ? col + 2 : n - 1;
   auto ld2 = [](const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); };
   constexpr int TG = 2;
-  double dot = 0.0;
+  const bool ar = ep.bc_l == 1;  // anti-reflective ghosts 2 w_0 - w_1 at the image border
+  double dot = 0.0, dself = 0.0;
   if (col < n) {
 #pragma unroll
     for (int t0 = 0; t0 < T; t0 += TG) {
@@ -226,6 +227,12 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
         if (i >= n) continue;
         double x0 = acc[t0 + k][0], x1 = acc[t0 + k][1];
         if (a_h) {
+          if (ar) {  // replace the clamped (zero-Neumann) ghosts by odd reflections
+            if (col == 0) wl[k] = ar_ghost(wc[k].x, wc[k].y);
+            if (col + 2 >= n) wr[k] = ar_ghost(wc[k].y, wc[k].x);
+            if (i == 0) wu[k] = make_double2(ar_ghost(wc[k].x, wd[k].x), ar_ghost(wc[k].y, wd[k].y));
+            if (i == n - 1) wd[k] = make_double2(ar_ghost(wc[k].x, wu[k].x), ar_ghost(wc[k].y, wu[k].y));
+          }
           const double fl0 = __dmul_rn(h0[k], __dsub_rn(wc[k].x, wl[k]));
           const double fr0 = __dmul_rn(h1[k], __dsub_rn(wc[k].y, wc[k].x));
           const double fu0 = __dmul_rn(vu[k].x, __dsub_rn(wc[k].x, wu[k].x));
@@ -248,6 +255,8 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
           dot += d2[k].x * x0;
           dot += d2[k].y * x1;
         }
+        dself += x0 * x0;
+        dself += x1 * x1;
       }
     }
   }
@@ -255,6 +264,10 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
     const double s = block_sum(dot, red);
     if (tid == 0) ep.partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
     if (ep.fin.s) pcg_fin_tail(ep.fin, ep.partial, gridDim.x * gridDim.y, red);
+  }
+  if (ep.partial_self) {
+    const double s = block_sum(dself, red);
+    if (tid == 0) ep.partial_self[blockIdx.y * gridDim.x + blockIdx.x] = s;
   }
 }
 

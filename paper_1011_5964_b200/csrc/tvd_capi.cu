@@ -57,6 +57,11 @@ enum Slot : int {
   kSlotPartial2,
   kSlotTmp3,
   kSlotInvT,
+  kSlotRS,     // BiCGstab shadow residual
+  kSlotBS,     // BiCGstab s
+  kSlotBSH,    // BiCGstab s_hat
+  kSlotBT,     // BiCGstab t
+  kSlotPartial3,
   kSlotCount
 };
 
@@ -72,6 +77,8 @@ struct tvd_ctx {
   DevBuf slots[kSlotCount];
   PcgState* d_state = nullptr;
   unsigned* d_fin = nullptr;  // tickets of the folded finalizers (tvd_cg.h pcg_fin_tail)
+  BicgState* d_bicg = nullptr;
+  BicgState* h_bicg = nullptr;
   PcgState* h_state = nullptr;
   double* h_scalar = nullptr;  // pinned scratch for host scalars (64 doubles)
   double* d_scalar = nullptr;
@@ -126,6 +133,7 @@ struct tvd_blur {
   double* d_psf = nullptr;   // device copy (general path)
   // separable factors: axis 0 (rows index) and axis 1
   BandOp h1[2], h1t[2], g[2];
+  BandOp rb[2];  // H1 H1 per axis: the re-blurred system H H (pipeline.py:173-174)
   std::vector<void*> owned;
   std::vector<std::vector<double>> host_taps;  // backing store of BandOp::taps_host
 };
@@ -741,6 +749,27 @@ static Taps1D transpose_table(const Taps1D& a, int n) {
   return t;
 }
 
+// A A for a banded A of half-width w -> half-width 2w (re-blurred system)
+static Taps1D square_table(const Taps1D& a, int n) {
+  const int w = a.w, W = 2 * w + 1, w2 = 2 * w, W2 = 2 * w2 + 1;
+  Taps1D t;
+  t.w = w2;
+  t.table.assign((size_t)n * W2, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int k1 = -w; k1 <= w; ++k1) {
+      const int l = i + k1;
+      if (l < 0 || l >= n) continue;
+      const double a1 = a.table[(size_t)i * W + k1 + w];
+      if (a1 == 0.0) continue;
+      for (int k2 = -w; k2 <= w; ++k2) {
+        const int c = l + k2;
+        if (c < 0 || c >= n) continue;
+        t.table[(size_t)i * W2 + (c - i) + w2] += a1 * a.table[(size_t)l * W + k2 + w];
+      }
+    }
+  return t;
+}
+
 // G = A^T A for a banded A of half-width w -> half-width 2w
 static Taps1D gram_table(const Taps1D& a, int n) {
   const int w = a.w, W = 2 * w + 1, w2 = 2 * w, W2 = 2 * w2 + 1;
@@ -821,8 +850,10 @@ static int make_bandop(tvd_blur* b, const Taps1D& t, int border, BandOp* op) {
 static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double* in, double* out,
                                  const double* dot_with, double* partial, const int* skip,
                                  int* nb_out, const PcgFin* fin = nullptr,
-                                 bool* fin_done = nullptr) {
+                                 bool* fin_done = nullptr, double* partial_self = nullptr,
+                                 bool* self_done = nullptr) {
   if (fin_done) *fin_done = false;
+  if (self_done) *self_done = false;
   tvd_blur* b = sys->blur;
   const int n = b->n;
   const long N = (long)n * n;
@@ -844,16 +875,22 @@ static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double
   ep.s = sys->s;
   ep.dot_with = dot_with;
   ep.partial = partial;
+  ep.bc_l = sys->bc_l;
   double* tmp;
   TVD_SLOT(c, kSlotTmp, N, tmp);
   if (b->separable) {
-    if (fin && partial && band_mma_ok(b->g[0])) {  // gamma in the tensor-core pass's last CTA
+    if (fin && partial && band_mma_ok(sys->reblur ? b->rb[0] : b->g[0])) {  // gamma in the last CTA
       ep.fin = *fin;
       if (fin_done) *fin_done = true;
     }
-    TVD_LAUNCH(c, kCatBandRows, 1, launch_band_rows(b->g[1], w, tmp, skip, c->stream));
-    TVD_LAUNCH(c, kCatBandCols, 1, launch_band_cols(b->g[0], tmp, out, ep, skip, c->stream));
-    if (nb_out) *nb_out = band_cols_grid(b->g[0]);
+    const BandOp* gg = sys->reblur ? b->rb : b->g;
+    if (self_done && partial_self && band_mma_ok(gg[0])) {  // t . t of BiCGstab in the epilogue
+      ep.partial_self = partial_self;
+      *self_done = true;
+    }
+    TVD_LAUNCH(c, kCatBandRows, 1, launch_band_rows(gg[1], w, tmp, skip, c->stream));
+    TVD_LAUNCH(c, kCatBandCols, 1, launch_band_cols(gg[0], tmp, out, ep, skip, c->stream));
+    if (nb_out) *nb_out = band_cols_grid(gg[0]);
   } else {
     const int T = n + 2 * b->m;
     double *ea, *eb, *t2;
@@ -861,7 +898,7 @@ static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double
     TVD_SLOT(c, kSlotExtB, (size_t)T * T, eb);
     TVD_SLOT(c, kSlotTmp2, N, t2);
     TVD_LAUNCH(c, kCatGeneral, 2, launch_general_blur(w, tmp, n, b->m, b->bc, b->d_psf, 0, ea, eb, c->stream));
-    const int back_t = b->bc == TVD_BC_REFLECTIVE ? 0 : 1;
+    const int back_t = (b->bc == TVD_BC_REFLECTIVE || sys->reblur) ? 0 : 1;
     TVD_LAUNCH(c, kCatGeneral, back_t ? 3 : 2, launch_general_blur(tmp, t2, n, b->m, b->bc, b->d_psf, back_t, ea, eb, c->stream));
     TVD_LAUNCH(c, kCatVec, 1, launch_normal_epilogue(t2, ep, n, out, skip, vec_blocks(), c->stream));
     if (nb_out) *nb_out = vec_blocks();
@@ -884,7 +921,9 @@ int tvd_ctx_create(int device, void* stream, tvd_ctx** out) {
   auto* c = new tvd_ctx();
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
-  if (cudaMalloc(&c->d_fin, 4 * sizeof(unsigned)) != cudaSuccess ||
+  if (cudaMalloc(&c->d_bicg, sizeof(BicgState)) != cudaSuccess ||
+      cudaMallocHost(&c->h_bicg, sizeof(BicgState)) != cudaSuccess ||
+      cudaMalloc(&c->d_fin, 4 * sizeof(unsigned)) != cudaSuccess ||
       cudaMemset(c->d_fin, 0, 4 * sizeof(unsigned)) != cudaSuccess ||
       cudaMalloc(&c->d_state, sizeof(PcgState)) != cudaSuccess ||
       cudaMallocHost(&c->h_state, sizeof(PcgState)) != cudaSuccess ||
@@ -960,6 +999,8 @@ int tvd_ctx_destroy(tvd_ctx* c) {
     if (s.ptr) cudaFree(s.ptr);
   cudaFree(c->d_state);
   cudaFree(c->d_fin);
+  cudaFree(c->d_bicg);
+  cudaFreeHost(c->h_bicg);
   cudaFreeHost(c->h_state);
   cudaFreeHost(c->h_scalar);
   cudaFree(c->d_scalar);
@@ -1014,6 +1055,7 @@ int tvd_blur_create(tvd_ctx* c, int n, const double* psf, int width, int bc, tvd
       int rc = make_bandop(b, h, m, &b->h1[ax]);
       if (!rc) rc = make_bandop(b, ht, 2 * m, &b->h1t[ax]);
       if (!rc) rc = make_bandop(b, gg, 2 * m, &b->g[ax]);
+      if (!rc) rc = make_bandop(b, square_table(h, n), 2 * m, &b->rb[ax]);
       if (rc) {
         tvd_blur_destroy(b);
         return rc;
@@ -1118,6 +1160,45 @@ int tvd_diffusion_bands(tvd_ctx* c, int n, double spacing, const double* a_h, co
   TVD_LAUNCH(c, kCatStencil, 1,
              launch_diffusion_bands(a_h, a_v, n, 1.0 / (spacing * spacing), diag, inner, block,
                                     c->stream));
+  return TVD_OK;
+}
+
+int tvd_diffusivity_bc(tvd_ctx* c, int n, double beta, double spacing, int bc_l,
+                       const double* u, double* a_h, double* a_v) {
+  if (!c || !u || !a_h || !a_v) return fail(TVD_ERR_INVALID, "null argument");
+  if (beta <= 0) return fail(TVD_ERR_INVALID, "beta must be positive");
+  if (spacing <= 0) return fail(TVD_ERR_INVALID, "spacing must be positive");
+  if (bc_l != TVD_DBC_ZERO_NEUMANN && bc_l != TVD_DBC_ANTI_REFLECTIVE)
+    return fail(TVD_ERR_INVALID, "unknown diffusion boundary condition");
+  if (bc_l == TVD_DBC_ANTI_REFLECTIVE && n < 2)
+    return fail(TVD_ERR_INVALID, "anti-reflective ghosts need n >= 2");
+  DeviceGuard g(c->device);
+  TVD_LAUNCH(c, kCatStencil, 1, launch_diffusivity(u, n, beta, spacing, a_h, a_v, c->stream, bc_l));
+  return TVD_OK;
+}
+
+int tvd_diffusion_apply_bc(tvd_ctx* c, int n, double spacing, int bc_l, const double* a_h,
+                           const double* a_v, const double* w, double* out) {
+  if (!c || !a_h || !a_v || !w || !out) return fail(TVD_ERR_INVALID, "null argument");
+  if (bc_l != TVD_DBC_ZERO_NEUMANN && bc_l != TVD_DBC_ANTI_REFLECTIVE)
+    return fail(TVD_ERR_INVALID, "unknown diffusion boundary condition");
+  DeviceGuard g(c->device);
+  TVD_LAUNCH(c, kCatStencil, 1, launch_diffusion_apply(a_h, a_v, w, n, 1.0 / (spacing * spacing),
+                                                       out, c->stream, bc_l));
+  return TVD_OK;
+}
+
+int tvd_diffusion_bands_bc(tvd_ctx* c, int n, double spacing, int bc_l, const double* a_h,
+                           const double* a_v, double* diag, double* inner_up, double* inner_lo,
+                           double* block_up, double* block_lo) {
+  if (!c || !a_h || !a_v || !diag || !inner_up || !block_up)
+    return fail(TVD_ERR_INVALID, "null argument");
+  if (bc_l != TVD_DBC_ZERO_NEUMANN && bc_l != TVD_DBC_ANTI_REFLECTIVE)
+    return fail(TVD_ERR_INVALID, "unknown diffusion boundary condition");
+  DeviceGuard g(c->device);
+  TVD_LAUNCH(c, kCatStencil, 1,
+             launch_diffusion_bands(a_h, a_v, n, 1.0 / (spacing * spacing), diag, inner_up,
+                                    block_up, c->stream, bc_l, inner_lo, block_lo));
   return TVD_OK;
 }
 
@@ -1295,6 +1376,10 @@ int tvd_precond_apply(tvd_ctx* c, int family, int n, const double* eig, const do
 // ------------------------------------------------------------- system/PCG
 static int check_system(const tvd_system* sys) {
   if (!sys || !sys->blur) return fail(TVD_ERR_INVALID, "null system");
+  if (sys->bc_l != TVD_DBC_ZERO_NEUMANN && sys->bc_l != TVD_DBC_ANTI_REFLECTIVE)
+    return fail(TVD_ERR_INVALID, "unknown diffusion boundary condition");
+  if (sys->reblur && sys->blur->bc != TVD_BC_ANTI_REFLECTIVE)
+    return fail(TVD_ERR_INVALID, "the re-blurred formulation requires anti-reflective blur BCs");
   if ((sys->a_h == nullptr) != (sys->a_v == nullptr))
     return fail(TVD_ERR_INVALID, "a_h and a_v must both be set");
   if (sys->a_h && !(sys->spacing > 0)) return fail(TVD_ERR_INVALID, "spacing must be positive");
@@ -1313,12 +1398,14 @@ int tvd_system_apply(tvd_ctx* c, const tvd_system* sys, const double* in, double
 static int minv_internal(tvd_ctx* c, const tvd_precond* pre, int n, const double* r, double* z,
                          double* partial, const int* skip, int* nb,
                          const double* inv_t = nullptr, const PcgFin* fin = nullptr,
-                         bool* fin_done = nullptr) {
+                         bool* fin_done = nullptr, bool want_dot = true) {
   if (fin_done) *fin_done = false;
+  if (!want_dot) partial = nullptr;
   const long N = (long)n * n;
   if (!pre || pre->kind == TVD_PRECOND_NONE) {
     if (z != r) TVD_LAUNCH(c, kCatVec, 1, launch_copy(r, z, N, skip, c->stream));
-    TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(r, r, N, partial, vec_blocks(), skip, c->stream));
+    if (partial)
+      TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(r, r, N, partial, vec_blocks(), skip, c->stream));
     *nb = vec_blocks();
     return TVD_OK;
   }
@@ -1328,9 +1415,115 @@ static int minv_internal(tvd_ctx* c, const tvd_precond* pre, int n, const double
     return TVD_OK;
   }
   if (pre->kind == TVD_PRECOND_TRANSFORM)
-    return precond_transform(c, pre->family, n, pre->inv_eig, pre->d, 0, r, z, r, skip, nb,
-                             inv_t, fin, fin_done);
+    return precond_transform(c, pre->family, n, pre->inv_eig, pre->d, 0, r, z,
+                             partial ? r : nullptr, skip, nb, inv_t, fin, fin_done);
   return fail(TVD_ERR_INVALID, "unknown preconditioner kind");
+}
+
+// Right-preconditioned BiCGstab (krylov.py:119-174), device resident like tvd_pcg_solve:
+// every kernel reads the BicgState flags, the host enqueues iterations in chunks and reads
+// the state between chunks.  Per iteration: rs.r -> beta ; p ; p_hat = M^-1 p ; v = A p_hat
+// (+ rs.v fused) -> alpha ; s, |s| -> early exit ; s_hat = M^-1 s ; t = A s_hat (+ t.s, t.t
+// fused) -> omega ; x, r, |r| -> stop test.
+int tvd_bicgstab_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre,
+                       const double* b, const double* x0, double* x, double tol,
+                       int max_iterations, double* history, int* iterations, int* converged,
+                       int* err_iteration, double* err_value) {
+  if (!c || !b || !x0 || !x) return fail(TVD_ERR_INVALID, "null argument");
+  int rc = check_system(sys);
+  if (rc) return rc;
+  if (!(tol > 0)) return fail(TVD_ERR_INVALID, "tol must be positive");
+  if (max_iterations < 1) return fail(TVD_ERR_INVALID, "max_iterations must be at least 1");
+  if (pre && pre->kind == TVD_PRECOND_TRANSFORM && !pre->inv_eig)
+    return fail(TVD_ERR_INVALID, "transform preconditioner needs inverse eigenvalues");
+  if (pre && pre->kind == TVD_PRECOND_DIAG && !pre->d)
+    return fail(TVD_ERR_INVALID, "diagonal preconditioner needs d");
+  DeviceGuard g(c->device);
+  const int n = sys->blur->n;
+  const long N = (long)n * n;
+  cudaStream_t st = c->stream;
+  double *r, *rs, *p, *v, *ph, *sv, *sh, *t, *pa, *pb, *pc;
+  TVD_SLOT(c, kSlotR, N, r);
+  TVD_SLOT(c, kSlotRS, N, rs);
+  TVD_SLOT(c, kSlotP, N, p);
+  TVD_SLOT(c, kSlotQ, N, v);
+  TVD_SLOT(c, kSlotZ, N, ph);
+  TVD_SLOT(c, kSlotBS, N, sv);
+  TVD_SLOT(c, kSlotBSH, N, sh);
+  TVD_SLOT(c, kSlotBT, N, t);
+  const size_t pcap = std::max<size_t>({(size_t)band_cols_blocks(n), (size_t)vec_blocks(),
+                                        (size_t)n + 64});
+  TVD_SLOT(c, kSlotPartial, pcap, pa);
+  TVD_SLOT(c, kSlotPartial2, pcap, pb);
+  TVD_SLOT(c, kSlotPartial3, pcap, pc);
+  if (x != x0) TVD_CUDA(cudaMemcpyAsync(x, x0, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  BicgState* S = c->d_bicg;
+  const int* halt = &S->halt;
+  int nb;
+  // r = b - A x ; r0 ; rs = r ; p = v = 0
+  rc = system_apply_internal(c, sys, x, v, nullptr, nullptr, nullptr, &nb);
+  if (rc) return rc;
+  TVD_LAUNCH(c, kCatVec, 1, launch_residual_init(b, v, r, N, pb, vec_blocks(), st));
+  TVD_LAUNCH(c, kCatFin, 1, launch_bicg_start(S, pb, vec_blocks(), st));
+  TVD_LAUNCH(c, kCatVec, 1, launch_copy(r, rs, N, nullptr, st));
+  TVD_CUDA(cudaMemsetAsync(p, 0, N * sizeof(double), st));
+  TVD_CUDA(cudaMemsetAsync(v, 0, N * sizeof(double), st));
+  const double* inv_t = nullptr;
+  if (pre && pre->kind == TVD_PRECOND_TRANSFORM) {
+    const TrigPlan* PP;
+    if (pipe_ok(c, pre->family, n, &PP) || rader_ok(c, pre->family, n, &PP)) {
+      double* it;
+      TVD_SLOT(c, kSlotInvT, N, it);
+      TVD_LAUNCH(c, kCatVec, 1, launch_transpose(pre->inv_eig, it, n, st));
+      inv_t = it;
+    }
+  }
+  int chunk = 4;
+  for (;;) {
+    for (int k = 0; k < chunk; ++k) {
+      TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(rs, r, N, pa, vec_blocks(), halt, st));
+      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_rho(S, pa, vec_blocks(), st));
+      TVD_LAUNCH(c, kCatVec, 1, launch_bicg_update_p(S, p, r, v, N, st));
+      rc = minv_internal(c, pre, n, p, ph, nullptr, halt, &nb, inv_t, nullptr, nullptr, false);
+      if (rc) return rc;
+      rc = system_apply_internal(c, sys, ph, v, rs, pa, halt, &nb);
+      if (rc) return rc;
+      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_alpha(S, pa, nb, st));
+      TVD_LAUNCH(c, kCatVec, 1, launch_bicg_s(S, sv, r, v, N, pb, st));
+      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_srel(S, pb, tol, st));
+      rc = minv_internal(c, pre, n, sv, sh, nullptr, halt, &nb, inv_t, nullptr, nullptr, false);
+      if (rc) return rc;
+      bool self_done = false;
+      rc = system_apply_internal(c, sys, sh, t, sv, pa, halt, &nb, nullptr, nullptr, pc,
+                                 &self_done);
+      if (rc) return rc;
+      int nb_tt = nb;
+      if (!self_done) {
+        TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(t, t, N, pc, vec_blocks(), halt, st));
+        nb_tt = vec_blocks();
+      }
+      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_omega(S, pa, nb, pc, nb_tt, st));
+      TVD_LAUNCH(c, kCatVec, 1, launch_bicg_update_xr(S, x, r, ph, sh, sv, t, N, pb, st));
+      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_rel(S, pb, tol, history, max_iterations, st));
+    }
+    TVD_CUDA(cudaMemcpyAsync(c->h_bicg, S, sizeof(BicgState), cudaMemcpyDeviceToHost, st));
+    TVD_CUDA(cudaStreamSynchronize(st));
+    if (c->h_bicg->done) break;
+    if (chunk < 16) chunk *= 2;
+  }
+  const BicgState& h = *c->h_bicg;
+  if (iterations) *iterations = h.iters;
+  if (converged) *converged = h.converged;
+  if (err_iteration) *err_iteration = h.err_iter;
+  if (err_value) *err_value = h.err_val;
+  if (h.status == kErrDiverged) return fail(TVD_ERR_DIVERGED, "pbicgstab produced non-finite values");
+  if (h.status == kErrBreakdown) {
+    static const char* why[] = {"", "rho vanished", "shadow angle vanished",
+                                "stabilizer direction vanished", "omega vanished"};
+    const int w = (int)h.err_val;
+    return fail(TVD_ERR_BREAKDOWN, std::string("pbicgstab breakdown: ") + why[w >= 1 && w <= 4 ? w : 0]);
+  }
+  return TVD_OK;
 }
 
 int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, const double* b,

@@ -344,4 +344,228 @@ cudaError_t launch_invert_eigs(const double* lam, double floor, double* inv, lon
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------ BiCGstab (krylov.py:119-174)
+__device__ __forceinline__ void bicg_fail(BicgState* s, int status, double val) {
+  s->status = status;
+  s->err_iter = s->k;
+  s->err_val = val;
+  s->done = 1;
+  s->halt = 1;
+}
+
+__global__ void k_bicg_start(BicgState* s, const double* partial, int nb) {
+  const double rr = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) {
+    s->r0 = sqrt(rr);
+    s->rho = s->alpha = s->omega = 1.0;
+    s->k = 1;
+    s->status = kOk;
+    s->err_iter = 0;
+    s->err_val = 0.0;
+    s->converged = 0;
+    s->iters = 0;
+    s->early = 0;
+    s->done = s->halt = 0;
+    if (s->r0 == 0.0) {
+      s->done = s->halt = 1;
+      s->converged = 1;
+    }
+  }
+}
+
+// rho_next = rs . r ; beta
+__global__ void k_bicg_rho(BicgState* s, const double* partial, int nb) {
+  if (s->halt) return;
+  const double rho_next = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) {
+    s->rho_next = rho_next;
+    if (fabs(rho_next) < 1e-30 * s->r0 * s->r0) {
+      bicg_fail(s, kErrBreakdown, 1.0);  // "rho vanished"
+      return;
+    }
+    s->beta = (rho_next / s->rho) * (s->alpha / s->omega);
+  }
+}
+
+// p = r + beta (p - omega v)
+__global__ void k_bicg_update_p(const BicgState* s, double* __restrict__ p,
+                                const double* __restrict__ r, const double* __restrict__ v,
+                                long N) {
+  if (s->halt) return;
+  const double beta = s->beta, omega = s->omega;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x)
+    p[g] = __dadd_rn(r[g], __dmul_rn(beta, __dsub_rn(p[g], __dmul_rn(omega, v[g]))));
+}
+
+// alpha = rho_next / (rs . v)
+__global__ void k_bicg_alpha(BicgState* s, const double* partial, int nb) {
+  if (s->halt) return;
+  const double denom = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) {
+    if (fabs(denom) < 1e-300) {
+      bicg_fail(s, kErrBreakdown, 2.0);  // "shadow angle vanished"
+      return;
+    }
+    s->alpha = s->rho_next / denom;
+  }
+}
+
+// s = r - alpha v ; partial |s|^2
+__global__ void k_bicg_s(const BicgState* st, double* __restrict__ sv, const double* __restrict__ r,
+                         const double* __restrict__ v, long N, double* partial) {
+  if (st->halt) return;
+  __shared__ double red[32];
+  const double alpha = st->alpha;
+  double acc = 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    const double x = __dsub_rn(r[g], __dmul_rn(alpha, v[g]));
+    sv[g] = x;
+    acc += x * x;
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// rel = |s| / r0: divergence check, early convergence (x += alpha p_hat follows)
+__global__ void k_bicg_srel(BicgState* s, const double* partial, int nb, double tol) {
+  if (s->halt) return;
+  const double ss = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) {
+    const double rel = sqrt(ss) / s->r0;
+    s->rel = rel;
+    if (!isfinite(rel)) {
+      bicg_fail(s, kErrDiverged, 0.0);
+      return;
+    }
+    if (rel < tol) {
+      s->early = 1;
+      s->halt = 1;
+    }
+  }
+}
+
+// omega = (t . s) / (t . t)
+__global__ void k_bicg_omega(BicgState* s, const double* p_ts, int nb_ts, const double* p_tt,
+                             int nb_tt) {
+  if (s->halt) return;
+  const double ts = sum_partials_block(p_ts, nb_ts);
+  __syncthreads();
+  const double tt = sum_partials_block(p_tt, nb_tt);
+  if (threadIdx.x == 0) {
+    if (tt == 0.0) {
+      bicg_fail(s, kErrBreakdown, 3.0);  // "stabilizer direction vanished"
+      return;
+    }
+    const double omega = ts / tt;
+    if (fabs(omega) < 1e-300) {
+      bicg_fail(s, kErrBreakdown, 4.0);  // "omega vanished"
+      return;
+    }
+    s->omega = omega;
+  }
+}
+
+// early: x += alpha p_hat ; else x += alpha p_hat + omega s_hat, r = s - omega t, |r|^2
+__global__ void k_bicg_update_xr(const BicgState* st, double* __restrict__ x, double* __restrict__ r,
+                                 const double* __restrict__ ph, const double* __restrict__ sh,
+                                 const double* __restrict__ sv, const double* __restrict__ t,
+                                 long N, double* partial) {
+  if (st->done) return;
+  __shared__ double red[32];
+  const double alpha = st->alpha, omega = st->omega;
+  const bool early = st->early;
+  double acc = 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    if (early) {
+      x[g] = __dadd_rn(x[g], __dmul_rn(alpha, ph[g]));
+    } else {
+      x[g] = __dadd_rn(x[g], __dadd_rn(__dmul_rn(alpha, ph[g]), __dmul_rn(omega, sh[g])));
+      const double v = __dsub_rn(sv[g], __dmul_rn(omega, t[g]));
+      r[g] = v;
+      acc += v * v;
+    }
+  }
+  const double tot = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+// end of iteration k: history, convergence / exhaustion, rho <- rho_next
+__global__ void k_bicg_rel(BicgState* s, const double* partial, int nb, double tol, double* hist,
+                           int max_it) {
+  if (s->done) return;
+  const double rr = sum_partials_block(partial, nb);
+  if (threadIdx.x == 0) {
+    if (s->early) {  // converged on the s residual
+      if (hist) hist[s->k - 1] = s->rel;
+      s->iters = s->k;
+      s->converged = 1;
+      s->done = s->halt = 1;
+      return;
+    }
+    const double rel = sqrt(rr) / s->r0;
+    s->rel = rel;
+    if (!isfinite(rel)) {
+      bicg_fail(s, kErrDiverged, 0.0);
+      return;
+    }
+    if (hist) hist[s->k - 1] = rel;
+    if (rel < tol) {
+      s->iters = s->k;
+      s->converged = 1;
+      s->done = s->halt = 1;
+      return;
+    }
+    s->rho = s->rho_next;
+    s->k += 1;
+    if (s->k > max_it) {
+      s->iters = max_it;
+      s->converged = 0;
+      s->done = s->halt = 1;
+    }
+  }
+}
+
+cudaError_t launch_bicg_start(BicgState* s, const double* partial, int nb, cudaStream_t st) {
+  k_bicg_start<<<1, 512, 0, st>>>(s, partial, nb);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_rho(BicgState* s, const double* partial, int nb, cudaStream_t st) {
+  k_bicg_rho<<<1, 512, 0, st>>>(s, partial, nb);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_update_p(BicgState* s, double* p, const double* r, const double* v, long N,
+                                 cudaStream_t st) {
+  k_bicg_update_p<<<kRedBlocks, kVecThreads, 0, st>>>(s, p, r, v, N);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_alpha(BicgState* s, const double* partial, int nb, cudaStream_t st) {
+  k_bicg_alpha<<<1, 512, 0, st>>>(s, partial, nb);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_s(BicgState* s, double* sv, const double* r, const double* v, long N,
+                          double* partial, cudaStream_t st) {
+  k_bicg_s<<<kRedBlocks, kVecThreads, 0, st>>>(s, sv, r, v, N, partial);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_srel(BicgState* s, const double* partial, double tol, cudaStream_t st) {
+  k_bicg_srel<<<1, 512, 0, st>>>(s, partial, kRedBlocks, tol);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_omega(BicgState* s, const double* p_ts, int nb_ts, const double* p_tt,
+                              int nb_tt, cudaStream_t st) {
+  k_bicg_omega<<<1, 512, 0, st>>>(s, p_ts, nb_ts, p_tt, nb_tt);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_update_xr(BicgState* s, double* x, double* r, const double* p_hat,
+                                  const double* s_hat, const double* sv, const double* t, long N,
+                                  double* partial, cudaStream_t st) {
+  k_bicg_update_xr<<<kRedBlocks, kVecThreads, 0, st>>>(s, x, r, p_hat, s_hat, sv, t, N, partial);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicg_rel(BicgState* s, const double* partial, double tol, double* hist,
+                            int max_it, cudaStream_t st) {
+  k_bicg_rel<<<1, 512, 0, st>>>(s, partial, kRedBlocks, tol, hist, max_it);
+  return cudaGetLastError();
+}
+
 }  // namespace tvd

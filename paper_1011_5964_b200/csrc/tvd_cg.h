@@ -107,6 +107,32 @@ __device__ __forceinline__ void pcg_fin_tail(const PcgFin& f, const double* part
   }
 }
 
+// ---- right-preconditioned BiCGstab (krylov.py:119-174).  `halt` = done or the early exit
+// after the s-residual test; the kernels of the second half-step skip on it, the x / r
+// update and the final check only on `done`.
+enum : int { kErrBreakdown = 7 };
+struct BicgState {
+  double rho, alpha, omega, rho_next, beta, r0, rel;
+  int k, done, halt, early, status, err_iter;
+  double err_val;
+  int iters, converged;
+};
+cudaError_t launch_bicg_start(BicgState* s, const double* partial, int nb, cudaStream_t st);
+cudaError_t launch_bicg_rho(BicgState* s, const double* partial, int nb, cudaStream_t st);
+cudaError_t launch_bicg_update_p(BicgState* s, double* p, const double* r, const double* v, long N,
+                                 cudaStream_t st);
+cudaError_t launch_bicg_alpha(BicgState* s, const double* partial, int nb, cudaStream_t st);
+cudaError_t launch_bicg_s(BicgState* s, double* sv, const double* r, const double* v, long N,
+                          double* partial, cudaStream_t st);
+cudaError_t launch_bicg_srel(BicgState* s, const double* partial, double tol, cudaStream_t st);
+cudaError_t launch_bicg_omega(BicgState* s, const double* p_ts, int nb_ts, const double* p_tt,
+                              int nb_tt, cudaStream_t st);
+cudaError_t launch_bicg_update_xr(BicgState* s, double* x, double* r, const double* p_hat,
+                                  const double* s_hat, const double* sv, const double* t, long N,
+                                  double* partial, cudaStream_t st);
+cudaError_t launch_bicg_rel(BicgState* s, const double* partial, double tol, double* hist,
+                            int max_it, cudaStream_t st);
+
 cudaError_t launch_sum_partials(const double* partial, int nb, double* out, cudaStream_t st);
 cudaError_t launch_residual_init(const double* b, const double* q, double* r, long N, double* partial,
                                  int nb, cudaStream_t st);

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) k_band_cols(BandOp op, const double* __re
         for (int k = -w; k <= w; ++k) acc += __ldg(&trow[k + w]) * xc[k * kColTileC];
       }
       const long g = (long)i * n + col;
-      if (ep.a_h) acc = acc + ep.alpha * diffusion_at(ep.a_h, ep.a_v, ep.lw, n, i, col, ep.inv_h2);
+      if (ep.a_h) acc = acc + ep.alpha * diffusion_at(ep.a_h, ep.a_v, ep.lw, n, i, col, ep.inv_h2, ep.bc_l);
       if (ep.s) acc = ep.s[g] * acc;
       out[g] = acc;
       if (ep.dot_with) acc_dot += ep.dot_with[g] * acc;
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kSlideW * 32) k_slide_cols(BandOp op, const Sl
         const int i = min(ig + r, n - 1);
         const long g = (long)i * n + col;
         double x = acc[r];
-        if (a_h) x = x + ep.alpha * diffusion_at(a_h, a_v, lw, n, i, col, ep.inv_h2);
+        if (a_h) x = x + ep.alpha * diffusion_at(a_h, a_v, lw, n, i, col, ep.inv_h2, ep.bc_l);
         if (sv) x = sv[g] * x;
         v[r] = x;
         dwv[r] = dw ? dw[g] : 0.0;
@@ -465,42 +465,56 @@ cudaError_t launch_band_cols(const BandOp& op, const double* in, double* out, co
 // Edge-padded (zero-Neumann ghost = border) differences, divided by spacing,
 // accumulated in the reference's order so the result is bit-identical to
 // numpy (no FMA contraction: __dadd_rn / __dmul_rn).
-__device__ __forceinline__ double u_at(const double* u, int n, int r, int c) {
+// Ghost layer of width 1 (tv.py:27-39): bc 0 = zero Neumann (np.pad "symmetric": copy the
+// border), bc 1 = anti-reflective (np.pad "reflect" / "odd": 2 u_0 - u_1).  numpy pads axis 0
+// first and axis 1 from the row-padded array, so AR corners compose the two rules; every
+// ghost is one 2 e - m rounding as in numpy.
+__device__ __forceinline__ double ar_row(const double* u, int n, int r, int c) {
+  if (r < 0) return __dsub_rn(__dmul_rn(2.0, u[c]), u[(long)n + c]);
+  if (r >= n) return __dsub_rn(__dmul_rn(2.0, u[(long)(n - 1) * n + c]), u[(long)(n - 2) * n + c]);
+  return u[(long)r * n + c];
+}
+__device__ __forceinline__ double u_at(const double* u, int n, int r, int c, int bc) {
+  if (bc == 1) {
+    if (c < 0) return __dsub_rn(__dmul_rn(2.0, ar_row(u, n, r, 0)), ar_row(u, n, r, 1));
+    if (c >= n) return __dsub_rn(__dmul_rn(2.0, ar_row(u, n, r, n - 1)), ar_row(u, n, r, n - 2));
+    return ar_row(u, n, r, c);
+  }
   r = r < 0 ? 0 : (r >= n ? n - 1 : r);
   c = c < 0 ? 0 : (c >= n ? n - 1 : c);
   return u[(long)r * n + c];
 }
 // dx[r][c] over the padded grid g (r in [0,n+2), c in [0,n+1)) = (g[r][c+1]-g[r][c]) / sp
-__device__ __forceinline__ double dxg(const double* u, int n, int r, int c, double sp) {
-  return __ddiv_rn(__dsub_rn(u_at(u, n, r - 1, c), u_at(u, n, r - 1, c - 1)), sp);
+__device__ __forceinline__ double dxg(const double* u, int n, int r, int c, double sp, int bc) {
+  return __ddiv_rn(__dsub_rn(u_at(u, n, r - 1, c, bc), u_at(u, n, r - 1, c - 1, bc)), sp);
 }
 // dy[r][c] (r in [0,n+1), c in [0,n+2)) = (g[r+1][c]-g[r][c]) / sp
-__device__ __forceinline__ double dyg(const double* u, int n, int r, int c, double sp) {
-  return __ddiv_rn(__dsub_rn(u_at(u, n, r, c - 1), u_at(u, n, r - 1, c - 1)), sp);
+__device__ __forceinline__ double dyg(const double* u, int n, int r, int c, double sp, int bc) {
+  return __ddiv_rn(__dsub_rn(u_at(u, n, r, c - 1, bc), u_at(u, n, r - 1, c - 1, bc)), sp);
 }
 
 __global__ void k_diffusivity(const double* __restrict__ u, int n, double beta, double sp,
-                              double* __restrict__ a_h, double* __restrict__ a_v) {
+                              double* __restrict__ a_h, double* __restrict__ a_v, int bc) {
   const double bb = __dmul_rn(beta, beta);
   const long nh = (long)n * (n + 1);
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < 2 * nh;
        e += (long)gridDim.x * blockDim.x) {
     if (e < nh) {  // horizontal edge (i, j), i in [0,n), j in [0,n]
       const int i = (int)(e / (n + 1)), j = (int)(e % (n + 1));
-      const double d = dxg(u, n, i + 1, j, sp);
-      double t = __dadd_rn(dyg(u, n, i, j, sp), dyg(u, n, i + 1, j, sp));
-      t = __dadd_rn(t, dyg(u, n, i, j + 1, sp));
-      t = __dadd_rn(t, dyg(u, n, i + 1, j + 1, sp));
+      const double d = dxg(u, n, i + 1, j, sp, bc);
+      double t = __dadd_rn(dyg(u, n, i, j, sp, bc), dyg(u, n, i + 1, j, sp, bc));
+      t = __dadd_rn(t, dyg(u, n, i, j + 1, sp, bc));
+      t = __dadd_rn(t, dyg(u, n, i + 1, j + 1, sp, bc));
       t = __dmul_rn(0.25, t);
       const double q = __dadd_rn(__dadd_rn(__dmul_rn(d, d), __dmul_rn(t, t)), bb);
       a_h[e] = __ddiv_rn(1.0, __dsqrt_rn(q));
     } else {       // vertical edge (i, j), i in [0,n], j in [0,n)
       const long f = e - nh;
       const int i = (int)(f / n), j = (int)(f % n);
-      const double d = dyg(u, n, i, j + 1, sp);
-      double t = __dadd_rn(dxg(u, n, i, j, sp), dxg(u, n, i, j + 1, sp));
-      t = __dadd_rn(t, dxg(u, n, i + 1, j, sp));
-      t = __dadd_rn(t, dxg(u, n, i + 1, j + 1, sp));
+      const double d = dyg(u, n, i, j + 1, sp, bc);
+      double t = __dadd_rn(dxg(u, n, i, j, sp, bc), dxg(u, n, i, j + 1, sp, bc));
+      t = __dadd_rn(t, dxg(u, n, i + 1, j, sp, bc));
+      t = __dadd_rn(t, dxg(u, n, i + 1, j + 1, sp, bc));
       t = __dmul_rn(0.25, t);
       const double q = __dadd_rn(__dadd_rn(__dmul_rn(d, d), __dmul_rn(t, t)), bb);
       a_v[f] = __ddiv_rn(1.0, __dsqrt_rn(q));
@@ -510,18 +524,22 @@ __global__ void k_diffusivity(const double* __restrict__ u, int n, double beta, 
 
 __global__ void k_diffusion_apply(const double* __restrict__ a_h, const double* __restrict__ a_v,
                                   const double* __restrict__ w, int n, double inv_h2,
-                                  double* __restrict__ out) {
+                                  double* __restrict__ out, int bc) {
   const long N = (long)n * n;
   for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
        g += (long)gridDim.x * blockDim.x) {
     const int i = (int)(g / n), j = (int)(g % n);
-    out[g] = diffusion_at(a_h, a_v, w, n, i, j, inv_h2);
+    out[g] = diffusion_at(a_h, a_v, w, n, i, j, inv_h2, bc);
   }
 }
 
+// Block bands (tv.py:138-175).  AR ghosts (bc 1) subtract the boundary edge twice from the
+// border diagonal and add it to the first / last off-diagonal, so up and low bands differ
+// at one end; inner_lo / block_lo may be null (zero Neumann: equal to up).
 __global__ void k_diffusion_bands(const double* __restrict__ a_h, const double* __restrict__ a_v,
                                   int n, double inv_h2, double* __restrict__ diag,
-                                  double* __restrict__ inner, double* __restrict__ block) {
+                                  double* __restrict__ inner, double* __restrict__ block, int bc,
+                                  double* __restrict__ inner_lo, double* __restrict__ block_lo) {
   const long N = (long)n * n;
   for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
        g += (long)gridDim.x * blockDim.x) {
@@ -529,13 +547,30 @@ __global__ void k_diffusion_bands(const double* __restrict__ a_h, const double* 
     const long h0 = (long)i * (n + 1) + j;
     double d = __dadd_rn(__dadd_rn(__dadd_rn(a_h[h0], a_h[h0 + 1]), a_v[(long)i * n + j]),
                          a_v[(long)(i + 1) * n + j]);
-    if (j == 0) d = __dsub_rn(d, a_h[(long)i * (n + 1)]);
-    if (j == n - 1) d = __dsub_rn(d, a_h[(long)i * (n + 1) + n]);
-    if (i == 0) d = __dsub_rn(d, a_v[j]);
-    if (i == n - 1) d = __dsub_rn(d, a_v[(long)n * n + j]);
+    auto edge = [&](double a) { return bc == 1 ? __dmul_rn(2.0, a) : a; };
+    if (j == 0) d = __dsub_rn(d, edge(a_h[(long)i * (n + 1)]));
+    if (j == n - 1) d = __dsub_rn(d, edge(a_h[(long)i * (n + 1) + n]));
+    if (i == 0) d = __dsub_rn(d, edge(a_v[j]));
+    if (i == n - 1) d = __dsub_rn(d, edge(a_v[(long)n * n + j]));
     diag[g] = __dmul_rn(inv_h2, d);
-    if (j < n - 1) inner[(long)i * (n - 1) + j] = __dmul_rn(inv_h2, -a_h[h0 + 1]);
-    if (i < n - 1) block[g] = __dmul_rn(inv_h2, -a_v[(long)(i + 1) * n + j]);
+    if (j < n - 1) {
+      const double b = -a_h[h0 + 1];
+      const double up = (bc == 1 && j == 0) ? __dadd_rn(b, a_h[h0]) : b;
+      inner[(long)i * (n - 1) + j] = __dmul_rn(inv_h2, up);
+      if (inner_lo) {
+        const double lo = (bc == 1 && j == n - 2) ? __dadd_rn(b, a_h[h0 + 2]) : b;
+        inner_lo[(long)i * (n - 1) + j] = __dmul_rn(inv_h2, lo);
+      }
+    }
+    if (i < n - 1) {
+      const double b = -a_v[(long)(i + 1) * n + j];
+      const double up = (bc == 1 && i == 0) ? __dadd_rn(b, a_v[j]) : b;
+      block[g] = __dmul_rn(inv_h2, up);
+      if (block_lo) {
+        const double lo = (bc == 1 && i == n - 2) ? __dadd_rn(b, a_v[(long)n * n + j]) : b;
+        block_lo[g] = __dmul_rn(inv_h2, lo);
+      }
+    }
   }
 }
 
@@ -546,19 +581,20 @@ static int grid_for(long work, int threads) {
 }
 
 cudaError_t launch_diffusivity(const double* u, int n, double beta, double sp, double* a_h,
-                               double* a_v, cudaStream_t st) {
-  k_diffusivity<<<grid_for(2L * n * (n + 1), 256), 256, 0, st>>>(u, n, beta, sp, a_h, a_v);
+                               double* a_v, cudaStream_t st, int bc) {
+  k_diffusivity<<<grid_for(2L * n * (n + 1), 256), 256, 0, st>>>(u, n, beta, sp, a_h, a_v, bc);
   return cudaGetLastError();
 }
 cudaError_t launch_diffusion_apply(const double* a_h, const double* a_v, const double* w, int n,
-                                   double inv_h2, double* out, cudaStream_t st) {
-  k_diffusion_apply<<<grid_for((long)n * n, 256), 256, 0, st>>>(a_h, a_v, w, n, inv_h2, out);
+                                   double inv_h2, double* out, cudaStream_t st, int bc) {
+  k_diffusion_apply<<<grid_for((long)n * n, 256), 256, 0, st>>>(a_h, a_v, w, n, inv_h2, out, bc);
   return cudaGetLastError();
 }
 cudaError_t launch_diffusion_bands(const double* a_h, const double* a_v, int n, double inv_h2,
-                                   double* diag, double* inner, double* block, cudaStream_t st) {
+                                   double* diag, double* inner, double* block, cudaStream_t st,
+                                   int bc, double* inner_lo, double* block_lo) {
   k_diffusion_bands<<<grid_for((long)n * n, 256), 256, 0, st>>>(a_h, a_v, n, inv_h2, diag, inner,
-                                                                 block);
+                                                                 block, bc, inner_lo, block_lo);
   return cudaGetLastError();
 }
 
@@ -710,7 +746,7 @@ __global__ void k_normal_epilogue(const double* __restrict__ base, Epilogue ep, 
        g += (long)gridDim.x * blockDim.x) {
     const int i = (int)(g / n), j = (int)(g % n);
     double acc = base[g];
-    if (ep.a_h) acc = acc + ep.alpha * diffusion_at(ep.a_h, ep.a_v, ep.lw, n, i, j, ep.inv_h2);
+    if (ep.a_h) acc = acc + ep.alpha * diffusion_at(ep.a_h, ep.a_v, ep.lw, n, i, j, ep.inv_h2, ep.bc_l);
     if (ep.s) acc = ep.s[g] * acc;
     out[g] = acc;
     if (ep.dot_with) acc_dot += ep.dot_with[g] * acc;

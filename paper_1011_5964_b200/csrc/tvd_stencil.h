@@ -31,20 +31,26 @@ struct Epilogue {
   const double* s;
   const double* dot_with;
   double* partial;
-  PcgFin fin;  // gamma finalizer folded into the last CTA (tensor-core pass; s == nullptr: off)
+  PcgFin fin;
+  int bc_l;              // diffusion ghosts: 0 zero Neumann, 1 anti-reflective
+  double* partial_self;  // optional per-CTA partials of q . q (BiCGstab t . t)  // gamma finalizer folded into the last CTA (tensor-core pass; s == nullptr: off)
 };
 
-// (L w)[i][j] of tv.py:96-108 with zero-Neumann ghosts, reference op order.
+// (L w)[i][j] of tv.py:96-108, reference op order.  Ghosts: bc 0 zero Neumann (w_{-1} =
+// w_0), bc 1 anti-reflective (w_{-1} = 2 w_0 - w_1, one rounding as numpy's odd reflection).
+__device__ __forceinline__ double ar_ghost(double w0, double w1) {
+  return __dsub_rn(__dmul_rn(2.0, w0), w1);
+}
 __device__ __forceinline__ double diffusion_at(const double* __restrict__ a_h,
                                                const double* __restrict__ a_v,
                                                const double* __restrict__ w, int n, int i, int j,
-                                               double inv_h2) {
+                                               double inv_h2, int bc = 0) {
   const long g = (long)i * n + j;
   const double wc = w[g];
-  const double wl = j > 0 ? w[g - 1] : wc;
-  const double wr = j < n - 1 ? w[g + 1] : wc;
-  const double wu = i > 0 ? w[g - n] : wc;
-  const double wd = i < n - 1 ? w[g + n] : wc;
+  const double wl = j > 0 ? w[g - 1] : (bc ? ar_ghost(wc, w[g + 1]) : wc);
+  const double wr = j < n - 1 ? w[g + 1] : (bc ? ar_ghost(wc, w[g - 1]) : wc);
+  const double wu = i > 0 ? w[g - n] : (bc ? ar_ghost(wc, w[g + n]) : wc);
+  const double wd = i < n - 1 ? w[g + n] : (bc ? ar_ghost(wc, w[g - n]) : wc);
   const long h0 = (long)i * (n + 1) + j;
   const double fl = __dmul_rn(a_h[h0], __dsub_rn(wc, wl));
   const double fr = __dmul_rn(a_h[h0 + 1], __dsub_rn(wr, wc));
@@ -70,11 +76,13 @@ cudaError_t launch_band_rows(const BandOp& op, const double* in, double* out, co
 cudaError_t launch_band_cols(const BandOp& op, const double* in, double* out, const Epilogue& ep,
                              const int* skip, cudaStream_t st);
 cudaError_t launch_diffusivity(const double* u, int n, double beta, double sp, double* a_h,
-                               double* a_v, cudaStream_t st);
+                               double* a_v, cudaStream_t st, int bc = 0);
 cudaError_t launch_diffusion_apply(const double* a_h, const double* a_v, const double* w, int n,
-                                   double inv_h2, double* out, cudaStream_t st);
+                                   double inv_h2, double* out, cudaStream_t st, int bc = 0);
 cudaError_t launch_diffusion_bands(const double* a_h, const double* a_v, int n, double inv_h2,
-                                   double* diag, double* inner, double* block, cudaStream_t st);
+                                   double* diag, double* inner, double* block, cudaStream_t st,
+                                   int bc = 0, double* inner_lo = nullptr,
+                                   double* block_lo = nullptr);
 cudaError_t launch_general_blur(const double* in, double* out, int n, int m, int bc,
                                 const double* h, int transpose, double* scratch_a,
                                 double* scratch_b, cudaStream_t st);

@@ -126,15 +126,21 @@ class NormalSystem:
     """
 
     def __init__(self, h_op: StructuredBlurOperator, l_op: DiffusionOperator, alpha: float,
-                 s: torch.Tensor | None = None) -> None:
+                 s: torch.Tensor | None = None, reblur: bool = False) -> None:
         self.h_op, self.l_op, self.alpha, self.s = h_op, l_op, float(alpha), s
+        self.reblur = bool(reblur)
         self.device = h_op.device
         self.n = h_op.n
+
+    @property
+    def symmetric(self) -> bool:
+        """PCG applies (pipeline.py:196-198); otherwise BiCGstab."""
+        return not self.reblur and self.l_op.symmetric
 
     def c_struct(self) -> nat.TvdSystem:
         return nat.TvdSystem(self.h_op.handle, self.alpha, self.l_op.spacing,
                              self.l_op.a_h_device.data_ptr(), self.l_op.a_v_device.data_ptr(),
-                             nat.ptr(self.s))
+                             nat.ptr(self.s), self.l_op.bc_code, int(self.reblur))
 
     def __call__(self, w):
         t, was_np = nat.to_device(w, self.device)
@@ -211,7 +217,7 @@ def scale_system(system: NormalSystem, rhs, l_op: DiffusionOperator, alpha: floa
         raise ConfigurationError(f"alpha must be positive, got {alpha}")
     d, s = _scaling(l_op, alpha, "s")
     rt = nat.to_device(rhs, system.device)[0]
-    scaled = NormalSystem(system.h_op, system.l_op, system.alpha, s=s)
+    scaled = NormalSystem(system.h_op, system.l_op, system.alpha, s=s, reblur=system.reblur)
     return ScaledSystem(d=d, d_inv_sqrt=s, apply=scaled, rhs=_binary(s, rt, 0))
 
 

@@ -155,7 +155,8 @@ def assemble_preconditioner(kind: str, h_op, l_op, alpha: float) -> FactoredPrec
     n = h_op.n
     dev = h_op.device
     lam_h = h_op.eigenvalues_device()
-    diag, inner, block = l_op.bands_device()
+    # the projections read interior bands only, where up == low even for AR ghosts
+    diag, inner, _, block, _ = l_op.bands_device()
     eig = torch.empty((n, n), dtype=torch.float64, device=dev)
     inv = torch.empty_like(eig)
     dvec = torch.empty_like(eig) if variant != nat.VARIANT_X else None

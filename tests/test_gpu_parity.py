@@ -424,3 +424,82 @@ def test_headline_c3_restore_matches_reference():
     assert abs(np.linalg.norm(r) - float(g["restored_norm"])) <= 1e-8 * float(g["restored_norm"])
     assert rel_err(r[::16, ::16], g["restored_sub"]) < 1e-8
     assert abs(rep.rre - float(g["rre"])) < 1e-8
+
+
+# ------------------------------------------------------------------ row f2
+F2_OPS = ["f2_ops_n32.npz", "f2_ops_n33.npz"]
+
+
+@pytest.mark.parametrize("name", F2_OPS)
+def test_f2_ar_diffusion_bit_identical(golden, name):
+    g = golden(name)
+    lop = TV.DiffusionOperator(g["u"], float(g["beta"]), TV.DiffusionBc.ANTI_REFLECTIVE)
+    assert np.array_equal(lop.a_h, g["a_h_ar"]) and np.array_equal(lop.a_v, g["a_v_ar"])
+    assert np.array_equal(lop.apply(g["w"]), g["Lw_ar"])
+    for (do, di), b in lop.block_banded().items():
+        assert np.array_equal(b, g[f"band_ar_{do}_{di}"]), (do, di)
+
+
+@pytest.mark.parametrize("name", F2_OPS)
+def test_f2_reblur_matvec(golden, name):
+    from paper_1011_5964_b200.pipeline import NormalSystem
+    g = golden(name)
+    n = g["u"].shape[0]
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(g["psf"]), B.BoundaryCondition.ANTI_REFLECTIVE, n)
+    for bcl, bc in (("zn", TV.DiffusionBc.ZERO_NEUMANN), ("ar", TV.DiffusionBc.ANTI_REFLECTIVE)):
+        lop = TV.DiffusionOperator(g["u"], float(g["beta"]), bc)
+        sysr = NormalSystem(hop, lop, float(g["alpha"]), reblur=True)
+        assert rel_err(sysr(g["w"]), g[f"reblur_Aw_{bcl}"]) < 1e-12
+
+
+@pytest.mark.parametrize("n,m", [(256, 7), (512, 15)])
+def test_f2_reblur_ar_matvec_tensor_core_sizes(n, m, rng):
+    """Re-blurred H H + alpha L_AR at sizes that run the DMMA band passes, vs the oracle."""
+    from paper_1011_5964_b200.harness import gen_psf
+    from paper_1011_5964_b200.pipeline import NormalSystem
+    h = gen_psf("gaussian", m, m / 2.0)
+    u = np.cumsum(rng.standard_normal((n, n)), axis=1) * 0.05
+    w = rng.standard_normal((n, n))
+    alpha, beta = 2e-3, 0.05
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(h), B.BoundaryCondition.ANTI_REFLECTIVE, n)
+    lop = TV.DiffusionOperator(u, beta, TV.DiffusionBc.ANTI_REFLECTIVE)
+    ah, av = O.diffusivity(u, beta, bc="ar")
+    want = O.blur(O.blur(w, h, "anti_reflective"), h, "anti_reflective") + \
+        alpha * O.diffusion_apply(ah, av, w, bc="ar")
+    assert rel_err(NormalSystem(hop, lop, alpha, reblur=True)(w), want) < 1e-12
+
+
+@pytest.mark.parametrize("name", F2_OPS)
+def test_f2_bicgstab_device_loop(golden, name):
+    """Fused device BiCGstab (tvd_bicgstab_solve) vs the generic path and the oracle on the
+    re-blurred + anti-reflective-L system with the diagonal preconditioner."""
+    from paper_1011_5964_b200.pipeline import NormalSystem
+    g = golden(name)
+    n, alpha, beta = g["u"].shape[0], float(g["alpha"]), float(g["beta"])
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(g["psf"]), B.BoundaryCondition.ANTI_REFLECTIVE, n)
+    lop = TV.DiffusionOperator(g["u"], beta, TV.DiffusionBc.ANTI_REFLECTIVE)
+    system = NormalSystem(hop, lop, alpha, reblur=True)
+    assert not system.symmetric
+    b = hop.apply(g["w"])
+    d = 1.0 + alpha * lop.diagonal()
+    minv = K.DiagonalInverse(torch.from_numpy(d).cuda())
+    cfg = K.KrylovConfig(tol=1e-6, max_iterations=400, record_history=True)
+    fused = K.pbicgstab(system, minv, b, g["u"], cfg)
+    generic = K.pbicgstab(lambda w: system(w), minv, b, g["u"], cfg)
+    ah, av = O.diffusivity(g["u"], beta, bc="ar")
+    h = g["psf"]
+
+    def apply_a(x):
+        return O.blur(O.blur(x, h, "anti_reflective"), h, "anti_reflective") + \
+            alpha * O.diffusion_apply(ah, av, x, bc="ar")
+
+    x, its, hist, ok = O.pbicgstab(apply_a, lambda r: r / d, b, g["u"], 1e-6, 400, True)
+    assert fused.converged and generic.converged and ok
+    assert abs(fused.iterations - its) <= 1 and abs(generic.iterations - its) <= 1
+    head = min(8, len(hist))
+    np.testing.assert_allclose(fused.residual_history[:head], hist[:head], rtol=1e-7)
+    np.testing.assert_allclose(generic.residual_history[:head], hist[:head], rtol=1e-7)
+    assert rel_err(fused.solution, x) < 1e-5 and rel_err(generic.solution, x) < 1e-5
+    # zero residual: zero iterations, converged (krylov.py:127-128)
+    exact = K.pbicgstab(system, minv, system(g["u"]), g["u"], cfg)
+    assert exact.iterations == 0 and exact.converged
