@@ -74,6 +74,11 @@ struct tvd_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::map<std::pair<int, int>, std::unique_ptr<TrigPlan>> plans;
+  // AR transform tables per n: q_L, q_R (n-2 each) and the P-projection border weights c
+  struct ArTables {
+    double *ql = nullptr, *qr = nullptr, *c = nullptr;
+  };
+  std::map<int, ArTables> ar;
   DevBuf slots[kSlotCount];
   PcgState* d_state = nullptr;
   unsigned* d_fin = nullptr;  // tickets of the folded finalizers (tvd_cg.h pcg_fin_tail)
@@ -536,6 +541,61 @@ static bool pipe_ok(tvd_ctx* c, int family, int n, const TrigPlan** P) {
   return (*P)->pfa_ok && pipe_grid((*P)->pfa, n) > 0;
 }
 
+// Anti-reflective transform tables (transforms.py:84-93, precond.py:134-165), long double:
+//   q_L = S_{n-2} p, q_R = S_{n-2} J p, p_j = 1 - j/(n-1) (j = 1..n-2), and the border weights
+//   c = s_1 .* S w, w_j = 2 (floor(j/2) + 1) - [j even], of the P-family projection.
+static int get_ar_tables(tvd_ctx* c, int n, const tvd_ctx::ArTables** out) {
+  auto it = c->ar.find(n);
+  if (it == c->ar.end()) {
+    if (n < 5) return fail(TVD_ERR_INVALID, "anti-reflective transform requires n >= 5");
+    const int N = n - 2, P2 = 2 * (N + 1);
+    const long double pi = 3.14159265358979323846264338327950288L;
+    std::vector<long double> sn(P2);
+    for (int k = 0; k < P2; ++k) sn[k] = sinl(pi * (long double)k / (long double)(N + 1));
+    const long double nrm = sqrtl(2.0L / (long double)(N + 1));
+    auto dst = [&](const std::vector<long double>& x, std::vector<long double>& y) {
+      y.assign(N, 0.0L);
+      for (int t = 0; t < N; ++t) {
+        long double acc = 0.0L;
+        long long idx = 0;
+        const int step = t + 1;
+        for (int j = 0; j < N; ++j) {
+          idx += step;
+          if (idx >= P2) idx -= P2;
+          acc += sn[idx] * x[j];
+        }
+        y[t] = nrm * acc;
+      }
+    };
+    std::vector<long double> ramp(N), rev(N), w(N), yl, yr, yw;
+    for (int j = 0; j < N; ++j) {
+      ramp[j] = 1.0L - (long double)(j + 1) / (long double)(n - 1);
+      w[j] = 2.0L * (long double)(j / 2 + 1) - ((j % 2 == 0) ? 1.0L : 0.0L);
+    }
+    for (int j = 0; j < N; ++j) rev[j] = ramp[N - 1 - j];
+    dst(ramp, yl);
+    dst(rev, yr);
+    dst(w, yw);
+    std::vector<double> hl(N), hr(N), hc(N);
+    for (int t = 0; t < N; ++t) {
+      hl[t] = (double)yl[t];
+      hr[t] = (double)yr[t];
+      hc[t] = (double)(nrm * sn[t + 1] * yw[t]);
+    }
+    tvd_ctx::ArTables T;
+    if (cudaMalloc(&T.ql, N * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&T.qr, N * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&T.c, N * sizeof(double)) != cudaSuccess ||
+        cudaMemcpy(T.ql, hl.data(), N * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(T.qr, hr.data(), N * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(T.c, hc.data(), N * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(TVD_ERR_CUDA, "AR table upload failed");
+    it = c->ar.emplace(n, T).first;
+  }
+  *out = &it->second;
+  return TVD_OK;
+}
+
 // prime odd core (config 5): the Rader row engine applies
 static bool rader_ok(tvd_ctx* c, int family, int n, const TrigPlan** P) {
   if (c->force_generic || (family != kFamSineHat && family != kFamDst1)) return false;
@@ -600,7 +660,10 @@ static int precond_rader(tvd_ctx* c, const TrigPlan* P, int family, int n, const
 static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const double* inv,
                         const double* inv_t, const double* d, int dmul, const double* in,
                         double* out, const double* dot_with, const int* skip, int* nb_out,
-                        const PcgFin* fin = nullptr, bool* fin_done = nullptr) {
+                        const PcgFin* fin = nullptr, bool* fin_done = nullptr,
+                        const double* ar_ql = nullptr, const double* ar_qr = nullptr) {
+  // ar_ql / ar_qr: P family -- T^-1 after the row pass and the first column transform, T
+  // before the second column transform and the last row pass (precond.py:456-461)
   double *tT, *t2, *partial = nullptr;
   TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tT);
   TVD_SLOT(c, kSlotTmp3, (size_t)n * n, t2);
@@ -620,6 +683,11 @@ static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const 
   a.pre = d;
   a.pre_mul = dmul;
   a.skip = skip;
+  if (ar_ql) {
+    a.ar_mode = 2;
+    a.ar_ql = ar_ql;
+    a.ar_qr = ar_qr;
+  }
   int nb;
   TVD_LAUNCH(c, kCatTrigRows, 1, launch_pipe(P->pfa, family, n, n, 1, a, &nb, c->stream));
   LineIO b{};
@@ -627,6 +695,11 @@ static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const 
   b.out = t2;
   b.mid_mul = inv_t;
   b.skip = skip;
+  if (ar_ql) {
+    b.ar_mode = 2 | 4;
+    b.ar_ql = ar_ql;
+    b.ar_qr = ar_qr;
+  }
   TVD_LAUNCH(c, kCatTrigCols, 1, launch_pipe(P->pfa, family, n, n, 1, b, &nb, c->stream));
   LineIO z{};
   z.in = t2;
@@ -640,6 +713,11 @@ static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const 
     z.fin = *fin;
     if (fin_done) *fin_done = true;
   }
+  if (ar_ql) {
+    z.ar_mode = 1;
+    z.ar_ql = ar_ql;
+    z.ar_qr = ar_qr;
+  }
   TVD_LAUNCH(c, kCatTrigRows, 1, launch_pipe(P->pfa, family, n, n, 0, z, &nb, c->stream));
   if (nb_out) *nb_out = nb;
   return TVD_OK;
@@ -650,6 +728,56 @@ static int precond_transform(tvd_ctx* c, int family, int n, const double* inv, c
                              const int* skip, int* nb_out, const double* inv_t = nullptr,
                              const PcgFin* fin = nullptr, bool* fin_done = nullptr) {
   if (fin_done) *fin_done = false;
+  if (family == TVD_TRANSFORM_ANTI_REFLECTIVE) {  // P family: T = Shat (I + U) around the DSTs
+    const tvd_ctx::ArTables* T;
+    int rc = get_ar_tables(c, n, &T);
+    if (rc) return rc;
+    const TrigPlan* PA;
+    if (pipe_ok(c, kFamSineHat, n, &PA))
+      return precond_pipe(c, PA, kFamSineHat, n, inv, inv_t, d, dmul, in, out, dot_with, skip,
+                          nb_out, fin, fin_done, T->ql, T->qr);
+    // other lengths: single Shat passes with the corrections as elementwise kernels
+    double *tmp, *partial = nullptr;
+    TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tmp);
+    if (dot_with) {
+      int rc2 = partial_capacity(c, (size_t)n + 64, &partial);
+      if (rc2) return rc2;
+    }
+    int nb;
+    LineIO a{};
+    a.in = in;
+    a.out = tmp;
+    a.pre = d;
+    a.pre_mul = dmul;
+    a.skip = skip;
+    rc = run_lines(c, kFamSineHat, rows_geom(n, n), 1, a, &nb);                      // T^-1 rows
+    if (rc) return rc;
+    TVD_LAUNCH(c, kCatVec, 1, launch_ar_corr(tmp, n, 1, -1.0, T->ql, T->qr, skip, c->stream));
+    LineIO b{};
+    b.in = tmp;
+    b.out = tmp;
+    b.skip = skip;
+    rc = run_lines(c, kFamSineHat, cols_geom(n, n), 1, b, &nb);                      // T^-1 cols
+    if (rc) return rc;
+    TVD_LAUNCH(c, kCatVec, 1, launch_ar_corr(tmp, n, 0, -1.0, T->ql, T->qr, skip, c->stream));
+    TVD_LAUNCH(c, kCatVec, 1, launch_mul(inv, tmp, tmp, (long)n * n, c->stream));  // lambda
+    TVD_LAUNCH(c, kCatVec, 1, launch_ar_corr(tmp, n, 0, 1.0, T->ql, T->qr, skip, c->stream));
+    rc = run_lines(c, kFamSineHat, cols_geom(n, n), 1, b, &nb);                      // T cols
+    if (rc) return rc;
+    TVD_LAUNCH(c, kCatVec, 1, launch_ar_corr(tmp, n, 1, 1.0, T->ql, T->qr, skip, c->stream));
+    LineIO z{};
+    z.in = tmp;
+    z.out = out;
+    z.post = d;
+    z.post_mul = dmul;
+    z.dot_with = dot_with;
+    z.partial = partial;
+    z.skip = skip;
+    rc = run_lines(c, kFamSineHat, rows_geom(n, n), 0, z, &nb);                      // T rows
+    if (rc) return rc;
+    if (nb_out) *nb_out = nb;
+    return TVD_OK;
+  }
   if (family != kFamSineHat && family != kFamDct && family != kFamDst1)
     return fail(TVD_ERR_INVALID, "unknown transform family");
   const TrigPlan* PP;
@@ -999,6 +1127,11 @@ int tvd_ctx_destroy(tvd_ctx* c) {
     if (s.ptr) cudaFree(s.ptr);
   cudaFree(c->d_state);
   cudaFree(c->d_fin);
+  for (auto& kv : c->ar) {
+    cudaFree(kv.second.ql);
+    cudaFree(kv.second.qr);
+    cudaFree(kv.second.c);
+  }
   cudaFree(c->d_bicg);
   cudaFreeHost(c->h_bicg);
   cudaFreeHost(c->h_state);
@@ -1216,6 +1349,41 @@ int tvd_transform_lines(tvd_ctx* c, int kind, int rows, int cols, int axis, cons
 }
 
 int tvd_transform_2d(tvd_ctx* c, int kind, int n, const double* in, double* out, int inverse) {
+  if (kind == TVD_TRANSFORM_ANTI_REFLECTIVE) {  // T (x) T or its inverse: two transposing row passes
+    if (!c || !in || !out) return fail(TVD_ERR_INVALID, "null argument");
+    DeviceGuard g(c->device);
+    const tvd_ctx::ArTables* T;
+    int rc = get_ar_tables(c, n, &T);
+    if (rc) return rc;
+    const TrigPlan* PA;
+    if (!pipe_ok(c, kFamSineHat, n, &PA)) {  // single Shat passes + correction kernels
+      const int sgn = inverse ? -1 : 1;
+      TVD_CUDA(cudaMemcpyAsync(out, in, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToDevice,
+                               c->stream));
+      for (int axis = 1; axis >= 0; --axis) {
+        if (!inverse)
+          TVD_LAUNCH(c, kCatVec, 1, launch_ar_corr(out, n, axis, sgn, T->ql, T->qr, nullptr, c->stream));
+        rc = tvd_transform_lines(c, TVD_TRANSFORM_SINE_HAT, n, n, axis, out, out, 0);
+        if (rc) return rc;
+        if (inverse)
+          TVD_LAUNCH(c, kCatVec, 1, launch_ar_corr(out, n, axis, sgn, T->ql, T->qr, nullptr, c->stream));
+      }
+      return TVD_OK;
+    }
+    double* t1;
+    TVD_SLOT(c, kSlotTmp2, (size_t)n * n, t1);
+    for (int pass = 0; pass < 2; ++pass) {
+      LineIO io{};
+      io.in = pass ? t1 : in;
+      io.out = pass ? out : t1;
+      io.ar_mode = inverse ? 2 : 1;
+      io.ar_ql = T->ql;
+      io.ar_qr = T->qr;
+      int nb;
+      TVD_LAUNCH(c, kCatTrigRows, 1, launch_pipe(PA->pfa, kFamSineHat, n, n, 1, io, &nb, c->stream));
+    }
+    return TVD_OK;
+  }
   int rc = tvd_transform_lines(c, kind, n, n, 0, in, out, inverse);
   if (rc) return rc;
   return tvd_transform_lines(c, kind, n, n, 1, out, out, inverse);
@@ -1240,7 +1408,9 @@ static int host_minmax(tvd_ctx* c, const double* d_partial, int nb, double* mn, 
 // level-2 projection of bands (diag[, inner, block]) into `out`, epilogue per BandLines.
 static int level2(tvd_ctx* c, const TrigPlan* P, int n, const double* diag, const double* inner,
                   const double* block, double* out, int epi, const double* lamh, const double* lamd,
-                  double alpha, double* partial_minmax, int* nb_out) {
+                  double alpha, double* partial_minmax, int* nb_out,
+                  const double* ar_c = nullptr) {
+  // ar_c: P family -- every level's lines get the AR border eigenvalues (precond.py:186-196)
   double *lam0, *lam1 = nullptr;
   TVD_SLOT(c, kSlotLam0, (size_t)n * n, lam0);
   BandLines a{};
@@ -1250,6 +1420,9 @@ static int level2(tvd_ctx* c, const TrigPlan* P, int n, const double* diag, cons
   a.nlines = n;
   a.out = lam0; a.out_ls = n; a.out_es = 1;
   TVD_LAUNCH(c, kCatProject, 1, launch_band_project(*P, 1, a, nullptr, c->stream));
+  if (ar_c)
+    TVD_LAUNCH(c, kCatProject, 1, launch_ar_lines(lam0, n, n, n, 1, ar_c, 0, nullptr, nullptr, 0.0,
+                                                  nullptr, nullptr, c->stream));
   if (block) {
     TVD_SLOT(c, kSlotLam1, (size_t)n * n, lam1);
     BandLines b{};
@@ -1257,6 +1430,9 @@ static int level2(tvd_ctx* c, const TrigPlan* P, int n, const double* diag, cons
     b.nlines = n - 1;
     b.out = lam1; b.out_ls = n; b.out_es = 1;
     TVD_LAUNCH(c, kCatProject, 1, launch_band_project(*P, 1, b, nullptr, c->stream));
+    if (ar_c)
+      TVD_LAUNCH(c, kCatProject, 1, launch_ar_lines(lam1, n - 1, n, n, 1, ar_c, 0, nullptr, nullptr,
+                                                    0.0, nullptr, nullptr, c->stream));
   }
   BandLines f{};
   f.b0 = lam0; f.b0_ls = 1; f.b0_es = n;
@@ -1264,6 +1440,12 @@ static int level2(tvd_ctx* c, const TrigPlan* P, int n, const double* diag, cons
   f.c1 = lam1 ? 2.0 : 0.0;
   f.nlines = n;
   f.out = out; f.out_ls = 1; f.out_es = n;
+  if (ar_c) {  // level 2 without the epilogue, then borders + epilogue per column line
+    TVD_LAUNCH(c, kCatProject, 1, launch_band_project(*P, 0, f, nullptr, c->stream));
+    TVD_LAUNCH(c, kCatProject, 1, launch_ar_lines(out, n, n, 1, n, ar_c, epi, lamh, lamd, alpha,
+                                                  partial_minmax, nb_out, c->stream));
+    return TVD_OK;
+  }
   f.epi = epi;
   f.lamh = lamh;
   f.lamd = lamd;
@@ -1297,12 +1479,21 @@ int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alph
                          double* min_eig, double* max_eig, long long* n_clamped) {
   if (!c || !lam_h || !diag || !inner || !block || !eig || !inv_eig)
     return fail(TVD_ERR_INVALID, "null argument");
-  if (family != TVD_TRANSFORM_SINE_HAT && family != TVD_TRANSFORM_DCT)
-    return fail(TVD_ERR_INVALID, "preconditioner family must be SINE_HAT or DCT");
+  if (family != TVD_TRANSFORM_SINE_HAT && family != TVD_TRANSFORM_DCT &&
+      family != TVD_TRANSFORM_ANTI_REFLECTIVE)
+    return fail(TVD_ERR_INVALID, "preconditioner family must be SINE_HAT, DCT or ANTI_REFLECTIVE");
   if (variant < 0 || variant > 2) return fail(TVD_ERR_INVALID, "unknown variant");
   if (alpha <= 0) return fail(TVD_ERR_INVALID, "alpha must be positive");
   DeviceGuard g(c->device);
   const TrigPlan* P;
+  const double* ar_c = nullptr;
+  if (family == TVD_TRANSFORM_ANTI_REFLECTIVE) {  // sine projection + AR border eigenvalues
+    const tvd_ctx::ArTables* T;
+    int rc0 = get_ar_tables(c, n, &T);
+    if (rc0) return rc0;
+    ar_c = T->c;
+    family = TVD_TRANSFORM_SINE_HAT;
+  }
   int rc = get_plan(c, family, n, &P);
   if (rc) return rc;
   const long N = (long)n * n;
@@ -1331,12 +1522,13 @@ int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alph
     TVD_SLOT(c, kSlotDiagS, N, ds);
     TVD_SLOT(c, kSlotInnerS, N, is);
     TVD_SLOT(c, kSlotBlockS, N, bs);
-    rc = level2(c, P, n, s, nullptr, nullptr, lamd, 0, nullptr, nullptr, 0.0, nullptr, nullptr);
+    rc = level2(c, P, n, s, nullptr, nullptr, lamd, 0, nullptr, nullptr, 0.0, nullptr, nullptr,
+                ar_c);
     if (rc) return rc;
     TVD_LAUNCH(c, kCatVec, 1, launch_scale_bands(diag, inner, block, s, n, ds, is, bs, c->stream));
-    rc = level2(c, P, n, ds, is, bs, eig, 2, lam_h, lamd, alpha, mm, &nb);
+    rc = level2(c, P, n, ds, is, bs, eig, 2, lam_h, lamd, alpha, mm, &nb, ar_c);
   } else {
-    rc = level2(c, P, n, diag, inner, block, eig, 1, lam_h, nullptr, alpha, mm, &nb);
+    rc = level2(c, P, n, diag, inner, block, eig, 1, lam_h, nullptr, alpha, mm, &nb, ar_c);
   }
   if (rc) return rc;
   double mn, mx;

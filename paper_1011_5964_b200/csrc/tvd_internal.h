@@ -116,6 +116,12 @@ struct LineIO {
   int pre_mul;
   int post_mul;
   PcgFin fin;  // finalizer over `partial` folded into the last CTA (pipeline pass; s == nullptr: off)
+  // anti-reflective transform T = Shat (I + U) (transforms.py:96-140), pipeline passes only:
+  // bit 0: T before the first transform (x_int += x_0 q_L + x_last q_R), bit 1: T^-1 after it
+  // (y_int -= x_0 q_L + x_last q_R), bit 2: T before the sandwich's second transform
+  int ar_mode;
+  const double* ar_ql;
+  const double* ar_qr;
 };
 
 // Band projection of one batch of lines (preconditioner assembly).
@@ -139,6 +145,13 @@ cudaError_t launch_trig(const TrigPlan& P, const LineGeom& g, int analysis, cons
 cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
                                 int* nblocks_out, cudaStream_t st);
 int trig_lines_per_cta(const TrigPlan& P, bool contiguous, int* nthreads, size_t* smem);
+// AR (P family) projection: border eigenvalues of each projected line from its interior
+// (weights c), optionally followed by the eigenvalue epilogue with per-CTA (min, max) pairs
+cudaError_t launch_ar_corr(double* x, int n, int axis, double sign, const double* ql,
+                           const double* qr, const int* skip, cudaStream_t st);
+cudaError_t launch_ar_lines(double* proj, int nlines, int n, long ls, long es, const double* c,
+                            int epi, const double* lamh, const double* lamd, double alpha,
+                            double* partial_minmax, int* nblocks_out, cudaStream_t st);
 int trig_blocks(const TrigPlan& P, const LineGeom& g);
 
 // ---- odd-symmetric PFA DST-I pass (tvd_pfa.cu), family DST1 / SINE_HAT

@@ -422,4 +422,102 @@ cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
   return cudaGetLastError();
 }
 
+// ------------------------------------------------ anti-reflective (P family) projection
+// The AR algebra's interior eigenvalues are the sine projection's; its border eigenvalue
+// 2 sum(z) - z_0 (precond.py:156-165, z the first-column representer of S diag(lam) S,
+// precond.py:134-153) is the fixed linear functional sum_t c_t lam_t, c = s_1 .* S w,
+// w_j = 2 (floor(j/2) + 1) - [j even] (host-built weights).  One thread per line (lanes
+// = consecutive lines), deterministic sequential sums; epi as k_band's epilogue.
+__global__ void k_ar_lines(double* __restrict__ proj, int nlines, int n, long ls, long es,
+                           const double* __restrict__ c, int epi, const double* __restrict__ lamh,
+                           const double* __restrict__ lamd, double alpha,
+                           double* __restrict__ partial_minmax) {
+  __shared__ double red[64];
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  double vmin = INFINITY, vmax = -INFINITY;
+  if (l < nlines) {
+    double* line = proj + (long)l * ls;
+    double bsum = 0.0;
+    for (int t = 1; t <= n - 2; ++t) bsum += c[t - 1] * line[(long)t * es];
+    line[0] = bsum;
+    line[(long)(n - 1) * es] = bsum;
+    if (epi != 0) {
+      for (int t = 0; t < n; ++t) {
+        const long g = (long)l * ls + (long)t * es;
+        double v = proj[g];
+        if (epi == 1) {
+          const double lh = lamh[g];
+          v = lh * lh + alpha * v;
+        } else {
+          const double lh = lamh[g], ld = lamd[g];
+          v = lh * lh * ld * ld + alpha * v;
+        }
+        proj[g] = v;
+        vmin = fmin(vmin, v);
+        vmax = fmax(vmax, v);
+      }
+    }
+  }
+  if (epi != 0) {
+    for (int o = 16; o > 0; o >>= 1) {
+      vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+      vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) {
+      red[wid] = vmin;
+      red[32 + wid] = vmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = INFINITY, b = -INFINITY;
+      for (int w = 0; w < nw; ++w) {
+        a = fmin(a, red[w]);
+        b = fmax(b, red[32 + w]);
+      }
+      partial_minmax[2 * blockIdx.x] = a;
+      partial_minmax[2 * blockIdx.x + 1] = b;
+    }
+  }
+}
+
+cudaError_t launch_ar_lines(double* proj, int nlines, int n, long ls, long es, const double* c,
+                            int epi, const double* lamh, const double* lamd, double alpha,
+                            double* partial_minmax, int* nblocks_out, cudaStream_t st) {
+  const int threads = 128, nb = (nlines + threads - 1) / threads;
+  if (nblocks_out) *nblocks_out = nb;
+  if (nlines <= 0) return cudaSuccess;
+  k_ar_lines<<<nb, threads, 0, st>>>(proj, nlines, n, ls, es, c, epi, lamh, lamd, alpha,
+                                     partial_minmax);
+  return cudaGetLastError();
+}
+
+// x_int += sign (x_0 q_L + x_last q_R) along `axis` (1: rows, 0: columns) -- the rank-2 factor
+// of T = Shat (I + U) (transforms.py:96-140); the borders are read from x itself (Shat leaves
+// them unchanged, so before and after a transform they are the same).
+__global__ void k_ar_corr(double* __restrict__ x, int n, int axis, double sign,
+                          const double* __restrict__ ql, const double* __restrict__ qr,
+                          const int* skip) {
+  if (skip && *skip) return;
+  const long N = (long)n * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(g / n), j = (int)(g % n);
+    const int t = axis == 1 ? j : i;  // position along the line
+    if (t == 0 || t == n - 1) continue;
+    const double b0 = axis == 1 ? x[(long)i * n] : x[j];
+    const double b1 = axis == 1 ? x[(long)i * n + n - 1] : x[(long)(n - 1) * n + j];
+    const double corr = __dadd_rn(__dmul_rn(b0, ql[t - 1]), __dmul_rn(b1, qr[t - 1]));
+    x[g] = sign > 0 ? __dadd_rn(x[g], corr) : __dsub_rn(x[g], corr);
+  }
+}
+
+cudaError_t launch_ar_corr(double* x, int n, int axis, double sign, const double* ql,
+                           const double* qr, const int* skip, cudaStream_t st) {
+  long nb = ((long)n * n + 255) / 256;
+  if (nb > 16L * kSMs) nb = 16L * kSMs;
+  k_ar_corr<<<(int)(nb < 1 ? 1 : nb), 256, 0, st>>>(x, n, axis, sign, ql, qr, skip);
+  return cudaGetLastError();
+}
+
 }  // namespace tvd

@@ -606,6 +606,9 @@ struct PipeK {
   const int* skip;
   int pre_mul, post_mul;
   PcgFin fin;
+  int ar_mode;  // LineIO::ar_mode
+  const double* ar_ql;
+  const double* ar_qr;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -773,6 +776,10 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     }
     return ((k & 1) ? -(C.y + C.x) : -(C.y - C.x)) * p.scale;
   };
+  // rank-2 border correction of the AR transform at interior t: b0 q_L[t] + b1 q_R[t]
+  auto arcorr = [&](double b0, double b1, int t) {
+    return __dadd_rn(__dmul_rn(b0, __ldg(p.ar_ql + t - 1)), __dmul_rn(b1, __ldg(p.ar_qr + t - 1)));
+  };
   // z_t -> its packed position(s) (t parity selects re / im)
   auto scatter = [&](double* bl, int t, unsigned e, double x) {
     double* b = bl + (t & 1);
@@ -829,6 +836,19 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) x[k] = p.pre_mul ? x[k] * q[k] : x[k] / q[k];
       }
+      if (p.ar_mode & 1) {  // T: x_int += x_0 q_L + x_last q_R (borders after the pre-scaling)
+        double b0 = stage[l * n], b1 = stage[l * n + n - 1];
+        if (p.pre) {
+          const double q0 = p.pre[(long)(line0 + l) * n], q1 = p.pre[(long)(line0 + l) * n + n - 1];
+          b0 = p.pre_mul ? b0 * q0 : b0 / q0;
+          b1 = p.pre_mul ? b1 * q1 : b1 / q1;
+        }
+#pragma unroll
+        for (int k = 0; k < kTpt; ++k) {
+          const int t = 1 + tid + k * NT;
+          if (k < kTpt - 1 || t <= N) x[k] = __dadd_rn(x[k], arcorr(b0, b1, t));
+        }
+      }
       double* bl = reinterpret_cast<double*>(buf + l * LP);
 #pragma unroll
       for (int k = 0; k < kTpt; ++k) {
@@ -880,8 +900,26 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) {
           const int t = 1 + tid + k * NT;
-          if (l < nlv && t <= N) v[l][k] *= unpack(l, g[k], t);
+          if (l < nlv && t <= N) {
+            double y = unpack(l, g[k], t);
+            if (p.ar_mode & 2) y = __dsub_rn(y, arcorr(bord[l][0], bord[l][1], t));  // T^-1
+            v[l][k] *= y;
+          }
         }
+      if (p.ar_mode & 4) {  // T before the second transform, borders scaled by mid
+#pragma unroll
+        for (int l = 0; l < B; ++l) {
+          if (l < nlv) {
+            const long rb = (long)(line0 + l) * n;
+            const double b0 = bord[l][0] * p.mid[rb], b1 = bord[l][1] * p.mid[rb + n - 1];
+#pragma unroll
+            for (int k = 0; k < kTpt; ++k) {
+              const int t = 1 + tid + k * NT;
+              if (t <= N) v[l][k] = __dadd_rn(v[l][k], arcorr(b0, b1, t));
+            }
+          }
+        }
+      }
       __syncthreads();
 #pragma unroll
       for (int l = 0; l < B; ++l) {
@@ -926,6 +964,13 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
           }
 #pragma unroll
           for (int j = 0; j < JG; ++j) y[j] = unpack(l, gg[j], t0 + (j0 + j) * TS);
+          if ((p.ar_mode & 2) && !p.mid) {  // T^-1 of the (only) transform
+#pragma unroll
+            for (int j = 0; j < JG; ++j) {
+              const int t = t0 + (j0 + j) * TS;
+              if (j0 + j < JT && t <= N) y[j] = __dsub_rn(y[j], arcorr(bord[l][0], bord[l][1], t));
+            }
+          }
           if (qcol) {
             double q[JG];
 #pragma unroll
@@ -961,6 +1006,13 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
         double y[kTpt];
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) y[k] = unpack(l, g[k], 1 + tid + k * NT);
+        if ((p.ar_mode & 2) && !p.mid) {  // T^-1 of the (only) transform
+#pragma unroll
+          for (int k = 0; k < kTpt; ++k) {
+            const int t = 1 + tid + k * NT;
+            if (k < kTpt - 1 || t <= N) y[k] = __dsub_rn(y[k], arcorr(bord[l][0], bord[l][1], t));
+          }
+        }
         if (qrow) {
           double q[kTpt];
 #pragma unroll
@@ -1104,6 +1156,9 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
   k.partial = io.partial;
   k.skip = io.skip;
   k.fin = io.fin;
+  k.ar_mode = io.ar_mode;
+  k.ar_ql = io.ar_ql;
+  k.ar_qr = io.ar_qr;
   static const int stages_env = [] {
     const char* s = getenv("TVD_PFA_STAGES");
     return s ? atoi(s) : 3;

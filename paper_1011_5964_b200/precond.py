@@ -11,8 +11,10 @@ eigenvalues come from the device symbol grid, and the positivity check /
 
 ``FactoredPreconditioner.apply_inverse`` is one row pass, one fused
 column "sandwich" pass (transform -> eigenvalue scaling -> transform) and one
-row pass.  The P family (anti-reflective algebra) only serves the re-blurred
-BiCGstab systems and is out of scope.
+row pass.  The P family (anti-reflective algebra, the re-blurred BiCGstab systems)
+uses the same passes with ``T = Shat (I + U)``'s rank-2 border corrections fused in, and
+its projection adds the AR border eigenvalues to the sine projection
+(precond.py:156-165, 302-352).
 """
 
 from __future__ import annotations
@@ -30,7 +32,8 @@ logger = logging.getLogger(__name__)
 
 _FAMILIES = {"R": TransformKind.DCT, "M": TransformKind.SINE_HAT,
              "P": TransformKind.ANTI_REFLECTIVE}
-_FAMILY_CODE = {TransformKind.DCT: nat.T_DCT, TransformKind.SINE_HAT: nat.T_SINE_HAT}
+_FAMILY_CODE = {TransformKind.DCT: nat.T_DCT, TransformKind.SINE_HAT: nat.T_SINE_HAT,
+                TransformKind.ANTI_REFLECTIVE: nat.T_ANTI_REFLECTIVE}
 
 PRECONDITIONER_KINDS = ("R", "D_R", "R_D", "M", "D_M", "M_D", "P", "D_P", "P_D")
 
@@ -143,9 +146,6 @@ def assemble_preconditioner(kind: str, h_op, l_op, alpha: float) -> FactoredPrec
         raise ValueError(
             f"preconditioner {kind!r} requires a blur operator with "
             f"{expected_bc.value!r} boundary conditions, got {h_op.bc.value!r}")
-    if transform not in _FAMILY_CODE:
-        raise NotImplementedError(
-            "the P (anti-reflective algebra) family is outside this build's scope (SURVEY.md 8f #2)")
     if kind.endswith("_D"):
         variant = nat.VARIANT_X_D
     elif kind.startswith("D_"):

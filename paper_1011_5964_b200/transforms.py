@@ -8,11 +8,13 @@ DCT-II), ``sinehat_apply`` (``diag(1, S_{n-2}, 1)``), ``apply_1d`` and
 numpy array is returned) or CUDA tensors (a CUDA tensor is returned); every
 transform runs in the sm_100a line-FFT kernels of ``csrc/tvd_lines.cu``.
 
-The anti-reflective transform ``T`` only feeds the reference's transform-
-domain blur and the P preconditioner family; this build applies H exactly
-(banded, ``csrc/tvd_stencil.cu``) and the P family is out of scope for the
-PCG path, so ``ANTI_REFLECTIVE`` raises
-``NotImplementedError``.
+The anti-reflective transform ``T = Shat (I + U)`` (transforms.py:84-140) feeds the P
+preconditioner family; ``tensor_apply_2d`` applies ``T (x) T`` and its inverse with
+the rank-2 border corrections fused into the pipelined DST row passes (odd cores
+with the prime-factor engine).  Its transposes only serve the reference's
+transform-domain blur adjoint, which this build does not use (H is applied
+exactly, ``csrc/tvd_stencil.cu``), so ``transpose=True`` raises
+``NotImplementedError``; so does the 1D ``apply_1d`` form.
 """
 
 from __future__ import annotations
@@ -33,13 +35,13 @@ class TransformKind(Enum):
 
 
 _CODES = {TransformKind.DST1: nat.T_DST1, TransformKind.SINE_HAT: nat.T_SINE_HAT,
-          TransformKind.DCT: nat.T_DCT}
+          TransformKind.DCT: nat.T_DCT, TransformKind.ANTI_REFLECTIVE: nat.T_ANTI_REFLECTIVE}
 
 
 def _lines(kind: TransformKind, v, inverse: bool, axis: int):
     if kind is TransformKind.ANTI_REFLECTIVE:
         raise NotImplementedError(
-            "the anti-reflective transform T is outside this build's PCG scope (SURVEY.md 8f #2)")
+            "the 1D anti-reflective transform is not built; tensor_apply_2d provides T (x) T")
     t, was_np = nat.to_device(v)
     if t.ndim == 0:
         raise ValueError("transform input must be at least 1D")
@@ -87,9 +89,8 @@ def apply_1d(kind: TransformKind, v, inverse: bool = False, transpose: bool = Fa
 
 def tensor_apply_2d(kind: TransformKind, g, inverse: bool = False, transpose: bool = False):
     """``X G X^T`` on a square grid (transforms.py:159-171)."""
-    if kind is TransformKind.ANTI_REFLECTIVE:
-        raise NotImplementedError(
-            "the anti-reflective transform T is outside this build's PCG scope (SURVEY.md 8f #2)")
+    if kind is TransformKind.ANTI_REFLECTIVE and transpose:
+        raise NotImplementedError("T^T / T^-T (transform-domain blur adjoint) are not built")
     t, was_np = nat.to_device(g)
     if t.ndim != 2 or t.shape[0] != t.shape[1]:
         raise ValueError(f"tensor transform needs a square grid, got shape {tuple(t.shape)}")
@@ -98,6 +99,8 @@ def tensor_apply_2d(kind: TransformKind, g, inverse: bool = False, transpose: bo
     n = t.shape[0]
     if kind is TransformKind.SINE_HAT and n < 3:
         raise ValueError(f"Shat_n requires length >= 3, got {n}")
+    if kind is TransformKind.ANTI_REFLECTIVE and n < 3:
+        raise ValueError(f"T_n requires length >= 3, got {n}")
     out = torch.empty_like(t)
     ctx = nat.context(t.device)
     nat.check(nat.load().tvd_transform_2d(ctx, _CODES[kind], n, t.data_ptr(), out.data_ptr(),

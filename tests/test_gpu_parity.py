@@ -503,3 +503,36 @@ def test_f2_bicgstab_device_loop(golden, name):
     # zero residual: zero iterations, converged (krylov.py:127-128)
     exact = K.pbicgstab(system, minv, system(g["u"]), g["u"], cfg)
     assert exact.iterations == 0 and exact.converged
+
+
+@pytest.mark.parametrize("name", F2_OPS)
+def test_f2_ar_transform_2d(golden, name):
+    g = golden(name)
+    for inv in (0, 1):
+        got = T.tensor_apply_2d(T.TransformKind.ANTI_REFLECTIVE, g["w"], inverse=bool(inv))
+        assert rel_err(got, g[f"AR2_{inv}0"]) < 1e-13
+
+
+@pytest.mark.parametrize("name", F2_OPS)
+def test_f2_p_family_assembly_and_solve(golden, name):
+    g = golden(name)
+    n = g["u"].shape[0]
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(g["psf"]), B.BoundaryCondition.ANTI_REFLECTIVE, n)
+    for bcl, bc in (("zn", TV.DiffusionBc.ZERO_NEUMANN), ("ar", TV.DiffusionBc.ANTI_REFLECTIVE)):
+        lop = TV.DiffusionOperator(g["u"], float(g["beta"]), bc)
+        for kind in ("P", "D_P", "P_D"):
+            pre = P.assemble_preconditioner(kind, hop, lop, float(g["alpha"]))
+            assert rel_err(pre.eigenvalues, g[f"lam_{kind}_{bcl}"]) < 1e-12, (kind, bcl)
+            assert rel_err(pre.apply_inverse(g["w"]), g[f"minv_{kind}_{bcl}"]) < 1e-12, (kind, bcl)
+
+
+@pytest.mark.parametrize("n", [128, 512, 1024, 2048])
+def test_f2_p_family_vs_oracle_config_sizes(n, rng):
+    """P-family M^-1 r (fused AR corrections in the pipelined row passes) vs the oracle at the
+    config sizes (odd cores 127, 511, 1023, 2047)."""
+    lam = rng.uniform(0.5, 2.0, (n, n))
+    w = rng.standard_normal((n, n))
+    pre = P.FactoredPreconditioner("P", T.TransformKind.ANTI_REFLECTIVE,
+                                   torch.from_numpy(lam).cuda(), 1e-3)
+    got = pre.apply_inverse(torch.from_numpy(w).cuda()).cpu().numpy()
+    assert rel_err(got, O.precond_solve("ar", 1.0 / lam, w)) < 1e-12
