@@ -28,7 +28,7 @@ import torch
 
 from . import _native as nat
 from .blur import BoundaryCondition, StructuredBlurOperator, SymmetricPsf
-from .krylov import DiagonalInverse, KrylovConfig, SolveOutcome, pcg
+from .krylov import DiagonalInverse, KrylovConfig, SolveOutcome, pbicgstab, pcg
 from .precond import assemble_preconditioner
 from .tv import DiffusionBc, DiffusionOperator
 
@@ -221,11 +221,11 @@ def scale_system(system: NormalSystem, rhs, l_op: DiffusionOperator, alpha: floa
     return ScaledSystem(d=d, d_inv_sqrt=s, apply=scaled, rhs=_binary(s, rt, 0))
 
 
-def _timed_pcg(apply_a, apply_minv, b, x0, cfg, acc: list[float]) -> SolveOutcome:
+def _timed_solve(solver, apply_a, apply_minv, b, x0, cfg, acc: list[float]) -> SolveOutcome:
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     start.record()
-    out = pcg(apply_a, apply_minv, b, x0, cfg)
+    out = solver(apply_a, apply_minv, b, x0, cfg)
     stop.record()
     stop.synchronize()
     acc[0] += start.elapsed_time(stop) / 1e3
@@ -238,17 +238,17 @@ def restore(v, psf: SymmetricPsf, config: RestorationConfig, u_true=None) -> Res
     vt, was_np = nat.to_device(v)
     if not bool(torch.isfinite(vt).all()):
         raise ConfigurationError("observed data must be finite")
-    if config.formulation is not Formulation.NORMAL or config.bc_l is not DiffusionBc.ZERO_NEUMANN:
-        raise NotImplementedError(
-            "re-blurred / anti-reflective-diffusion (BiCGstab) systems are outside this build's "
-            "scope (SURVEY.md 8f #2)")
     torch.cuda.synchronize(vt.device)
     started = time.perf_counter()
     if not isinstance(psf, SymmetricPsf):
         psf = SymmetricPsf(psf)
     n = vt.shape[0]
     h_op = StructuredBlurOperator(psf, config.bc_h, n, device=vt.device)
-    back = h_op.apply if config.bc_h is BoundaryCondition.REFLECTIVE else h_op.apply_transpose
+    reblur = config.formulation is Formulation.REBLUR
+    # back operator (pipeline.py:166-179): H for the re-blurred and the (symmetric) reflective
+    # systems, H^T otherwise
+    back = h_op.apply if (reblur or config.bc_h is BoundaryCondition.REFLECTIVE) \
+        else h_op.apply_transpose
     alpha = config.alpha
     rhs = back(vt)
     u = vt.clone()
@@ -260,14 +260,15 @@ def restore(v, psf: SymmetricPsf, config: RestorationConfig, u_true=None) -> Res
     pcg_time = [0.0]
     for _ in range(config.fp_max):
         l_op = DiffusionOperator(u, config.beta, config.bc_l, config.spacing, device=vt.device)
-        system = NormalSystem(h_op, l_op, alpha)
+        system = NormalSystem(h_op, l_op, alpha, reblur=reblur)
+        solver = pcg if system.symmetric else pbicgstab  # pipeline.py:196-198
         gradient_norms.append(_norm(_sub(system(u), rhs)))
         selector = config.preconditioner
         if selector is PrecondSelector.X_D:
             bundle = scale_system(system, rhs, l_op, alpha)
             precond = assemble_preconditioner(f"{config.base_kind()}_D", h_op, l_op, alpha)
-            outcome = _timed_pcg(bundle.apply, precond.apply_inverse, bundle.rhs,
-                                 bundle.scale_iterate(u), config.inner, pcg_time)
+            outcome = _timed_solve(solver, bundle.apply, precond.apply_inverse, bundle.rhs,
+                                   bundle.scale_iterate(u), config.inner, pcg_time)
             u_next = bundle.unscale(outcome.solution)
         else:
             if selector is PrecondSelector.NONE:
@@ -280,7 +281,7 @@ def restore(v, psf: SymmetricPsf, config: RestorationConfig, u_true=None) -> Res
                     else f"D_{config.base_kind()}"
                 precond = assemble_preconditioner(kind, h_op, l_op, alpha)
                 apply_minv = precond.apply_inverse
-            outcome = _timed_pcg(system, apply_minv, rhs, u, config.inner, pcg_time)
+            outcome = _timed_solve(solver, system, apply_minv, rhs, u, config.inner, pcg_time)
             u_next = outcome.solution
         steps += 1
         inner_iterations.append(outcome.iterations)
@@ -291,10 +292,10 @@ def restore(v, psf: SymmetricPsf, config: RestorationConfig, u_true=None) -> Res
         if scale > 0 and change / scale < config.fp_tol:
             fp_converged = True
             break
-    # el_residual (tv.py:190-204): H^T (H u - v) + alpha L(u) u
+    # el_residual (tv.py:190-204): H* (H u - v) + alpha L(u) u, H* = H for the re-blurred form
     residual = _sub(h_op.apply(u), vt)
     l_fin = DiffusionOperator(u, config.beta, config.bc_l, config.spacing, device=vt.device)
-    grad = h_op.apply_transpose(residual)
+    grad = h_op.reblur_apply(residual) if reblur else h_op.apply_transpose(residual)
     lu = l_fin.apply(u)
     ctx = nat.context(vt.device)
     g_out = torch.empty_like(grad)

@@ -536,3 +536,27 @@ def test_f2_p_family_vs_oracle_config_sizes(n, rng):
                                    torch.from_numpy(lam).cuda(), 1e-3)
     got = pre.apply_inverse(torch.from_numpy(w).cuda()).cpu().numpy()
     assert rel_err(got, O.precond_solve("ar", 1.0 / lam, w)) < 1e-12
+
+
+REBLUR = [(bcl, sel) for bcl in ("zn", "ar") for sel in ("none", "diag", "x", "d_x", "x_d")]
+
+
+@pytest.mark.parametrize("bcl,sel", REBLUR)
+def test_f2_reblur_restore_matches_reference(golden, bcl, sel):
+    """AR+Reblur+ZN / AR+Reblur+AR (harness.py:56-59) through restore: BiCGstab per FP step with
+    the P family (x, d_x, x_d), the diagonal or no preconditioner.  Identical per-FP-step
+    counts; image 1e-8 (P family) / 1e-7 (none, diag: rounding-sensitive BiCGstab histories)."""
+    g = golden(f"restore_c1_reblur_{bcl}_{sel}.npz")
+    cfg = tvd.RestorationConfig(
+        bc_h=B.BoundaryCondition.ANTI_REFLECTIVE, alpha=float(g["alpha"]), beta=float(g["beta"]),
+        bc_l=TV.DiffusionBc.ANTI_REFLECTIVE if bcl == "ar" else TV.DiffusionBc.ZERO_NEUMANN,
+        formulation=tvd.Formulation.REBLUR, preconditioner=tvd.PrecondSelector(sel),
+        fp_tol=1e-300, fp_max=int(g["fp_max"]),
+        inner=K.KrylovConfig(tol=float(g["tol"]), max_iterations=2000))
+    rep = tvd.restore(g["v"], B.SymmetricPsf(g["psf"]), cfg)
+    assert rep.inner_iterations == [int(k) for k in g["inner_iterations"]]
+    tol = 1e-8 if sel in ("x", "d_x", "x_d") else 1e-7
+    assert rel_err(rep.restored, g["restored"]) < tol
+    np.testing.assert_allclose(rep.gradient_norms, g["gradient_norms"], rtol=1e-6)
+    assert abs(rep.final_gradient_norm - float(g["final_gradient_norm"])) <= \
+        1e-6 * float(g["final_gradient_norm"])
