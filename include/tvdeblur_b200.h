@@ -191,6 +191,58 @@ int tvd_bicgstab_solve(tvd_ctx* ctx, const tvd_system* sys, const tvd_precond* p
                        int* err_iteration, double* err_value);
 
 /* ---- vector helpers for the generic callable path ---------------------- */
+/* ---- row-slab decomposition of one large problem over nranks ranks (config 5).
+ * Rank `rank` owns the global rows [rank R, rank R + R), R = n / nranks.  The library runs the
+ * kernels of each phase on the context stream; the caller runs the collectives between the
+ * phases on the buffers tvd_slab_buffer exposes (paper_1011_5964_b200/slab.py):
+ *   start:  MATVEC_ROWS, halo(T_EXT, khalo rows; P_EXT, 1 row), MATVEC_COLS, RESIDUAL,
+ *           allgather(CONTRIB -> GATHER), START, precond, allgather, RZ0
+ *   iter:   MATVEC_ROWS, halo, MATVEC_COLS, allgather, GAMMA_UPDATE, allgather, REL,
+ *           precond, allgather, BETA_P
+ *   precond (transform): PREC_ROWS, all-to-all(SEND -> RECV), PREC_COLS, all-to-all,
+ *           PREC_FINAL;  (none / diagonal): PREC_ROWS only
+ * sys: a_h = the slab's R x (n+1) rows of a_h, a_v = its R+1 rows [rank R, rank R + R] of a_v,
+ * s = NULL, reblur = 0, separable PSF (tensor-core band passes, n >= 256).
+ * pre: NONE; DIAG (d = slab of the divisor); TRANSFORM (family DST1 / SINE_HAT, inv_eig = rows
+ * [rank R, rank R + R) of the TRANSPOSED inverse eigenvalue grid, d = slab of d_sqrt or NULL).
+ * Replaces the inner solve krylov.pcg (krylov.py:82-116) for an image split across GPUs. */
+typedef struct tvd_slab tvd_slab;
+#define TVD_SLAB_MATVEC_ROWS 0
+#define TVD_SLAB_MATVEC_COLS 1
+#define TVD_SLAB_RESIDUAL 2
+#define TVD_SLAB_START 3
+#define TVD_SLAB_GAMMA_UPDATE 4
+#define TVD_SLAB_REL 5
+#define TVD_SLAB_PREC_ROWS 6
+#define TVD_SLAB_PREC_COLS 7
+#define TVD_SLAB_PREC_FINAL 8
+#define TVD_SLAB_RZ0 9
+#define TVD_SLAB_BETA_P 10
+#define TVD_SLAB_BUF_X 0      /* R x n solution slab                                   */
+#define TVD_SLAB_BUF_R 1
+#define TVD_SLAB_BUF_Z 2
+#define TVD_SLAB_BUF_Q 3
+#define TVD_SLAB_BUF_P_EXT 4  /* (R + 2) x n: halo row, p slab, halo row               */
+#define TVD_SLAB_BUF_T_EXT 5  /* (R + 2 khalo) x n: halo, t = p G_1^T slab, halo        */
+#define TVD_SLAB_BUF_SEND 6   /* n x R all-to-all send blocks (block j -> rank j)      */
+#define TVD_SLAB_BUF_RECV 7   /* n x R all-to-all receive blocks (block i <- rank i)   */
+#define TVD_SLAB_BUF_CONTRIB 8 /* 1 double: this rank's partial of the current dot     */
+#define TVD_SLAB_BUF_GATHER 9 /* nranks doubles: every rank's contribution, rank order */
+int tvd_slab_create(tvd_ctx* ctx, const tvd_system* sys, const tvd_precond* pre, int nranks,
+                    int rank, tvd_slab** out);
+int tvd_slab_destroy(tvd_slab* slab);
+/* info[8]: n, R, row_lo, khalo, p halo rows, nranks, rank, preconditioner exchanges (0/1) */
+int tvd_slab_info(tvd_slab* slab, int* info);
+int tvd_slab_buffer(tvd_slab* slab, int which, double** ptr, long long* count);
+/* b, x0: this rank's R x n slabs (b must stay valid during the solve); history: NULL or
+ * max_iterations doubles */
+int tvd_slab_start(tvd_slab* slab, const double* b, const double* x0, double tol,
+                   int max_iterations, double* history);
+int tvd_slab_phase(tvd_slab* slab, int phase);
+/* synchronises; TVD_ERR_DIVERGED / TVD_ERR_INDEFINITE once a failure ended the solve */
+int tvd_slab_status(tvd_slab* slab, int* done, int* iterations, int* converged,
+                    int* err_iteration, double* err_value);
+
 int tvd_vec_dot(tvd_ctx* ctx, long long count, const double* x, const double* y, double* out);
 /* out = a x + b y */
 int tvd_vec_axpby(tvd_ctx* ctx, long long count, double a, const double* x, double b,

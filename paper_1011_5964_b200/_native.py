@@ -80,6 +80,15 @@ _SIGNATURES = {
     "tvd_bicgstab_solve": ([_vp, ctypes.POINTER(TvdSystem), ctypes.POINTER(TvdPrecond), _vp, _vp,
                             _vp, _d, _i, _vp, ctypes.POINTER(_i), ctypes.POINTER(_i),
                             ctypes.POINTER(_i), ctypes.POINTER(_d)], _i),
+    "tvd_slab_create": ([_vp, ctypes.POINTER(TvdSystem), ctypes.POINTER(TvdPrecond), _i, _i,
+                         ctypes.POINTER(_vp)], _i),
+    "tvd_slab_destroy": ([_vp], _i),
+    "tvd_slab_info": ([_vp, ctypes.POINTER(_i)], _i),
+    "tvd_slab_buffer": ([_vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_ll)], _i),
+    "tvd_slab_start": ([_vp, _vp, _vp, _d, _i, _vp], _i),
+    "tvd_slab_phase": ([_vp, _i], _i),
+    "tvd_slab_status": ([_vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i),
+                         ctypes.POINTER(_i), ctypes.POINTER(_d)], _i),
     "tvd_vec_dot": ([_vp, _ll, _vp, _vp, ctypes.POINTER(_d)], _i),
     "tvd_vec_axpby": ([_vp, _ll, _d, _vp, _d, _vp, _vp], _i),
     "tvd_vec_binary": ([_vp, _ll, _i, _vp, _vp, _vp], _i),

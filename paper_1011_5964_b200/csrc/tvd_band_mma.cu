@@ -80,7 +80,8 @@ __device__ __forceinline__ void stage_fragments(double* fr, const BandTaps& tp, 
 template <int KOFF>
 __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
                                                      const double* __restrict__ in,
-                                                     double* __restrict__ out, const int* skip) {
+                                                     double* __restrict__ out, const int* skip,
+                                                     int row_lo, int row_hi) {
   if (skip && *skip) return;
   using SH = BmShape<KOFF>;
   constexpr int T = kBmT, S = SH::S, RP = SH::RP, W2 = SH::WIDTH / 2;
@@ -88,12 +89,12 @@ __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
   double* tile = smb;
   double* fr = smb + SH::RH * RP;
   const int n = op.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int i0 = blockIdx.y * SH::RH, jb = blockIdx.x * SH::CW;
+  const int i0 = row_lo + blockIdx.y * SH::RH, jb = blockIdx.x * SH::CW;
   for (int e = tid; e < SH::RH * W2; e += blockDim.x) {
     const int r = e / W2, c = 2 * (e - r * W2);
     const int row = i0 + r, col = jb - KOFF + c;
-    const bool ok = row < n && col >= 0 && col < n;
-    cp16(tile + r * RP + c, ok ? in + (long)row * n + col : in, ok);
+    const bool ok = row < row_hi && col >= 0 && col < n;
+    cp16(tile + r * RP + c, ok ? in + (long)row * n + col : in + (long)i0 * n, ok);
   }
   stage_fragments<KOFF>(fr, tp, op.w);
   cp_commit_wait();
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
     }
   }
   const int row = i0 + rb * 8 + (lane >> 2);
-  if (row < n) {
+  if (row < row_hi) {
 #pragma unroll
     for (int t = 0; t < T; ++t) {
       const int col = o0 + 8 * t + 2 * (lane & 3);
@@ -137,7 +138,7 @@ template <int KOFF>
 __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
                                                      const double* __restrict__ in,
                                                      double* __restrict__ out, Epilogue ep,
-                                                     const int* skip) {
+                                                     const int* skip, int row_lo, int row_hi) {
   if (skip && *skip) return;
   using SH = BmShape<KOFF>;
   constexpr int T = kBmT, S = SH::S, CP = SH::CP, C2 = SH::CC / 2;
@@ -146,12 +147,12 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
   double* tile = smb;
   double* fr = smb + SH::HEIGHT * CP;
   const int n = op.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ib = blockIdx.y * SH::RW, j0 = blockIdx.x * SH::CC;
+  const int ib = row_lo + blockIdx.y * SH::RW, j0 = blockIdx.x * SH::CC;
   for (int e = tid; e < SH::HEIGHT * C2; e += blockDim.x) {
     const int r = e / C2, c = 2 * (e - r * C2);
     const int row = ib - KOFF + r, col = j0 + c;
     const bool ok = row >= 0 && row < n && col < n;
-    cp16(tile + r * CP + c, ok ? in + (long)row * n + col : in, ok);
+    cp16(tile + r * CP + c, ok ? in + (long)row * n + col : in + (long)ib * n, ok);
   }
   stage_fragments<KOFF>(fr, tp, op.w);
   cp_commit_wait();
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
       double wl[TG], wr[TG], h0[TG], h1[TG], h2[TG];
 #pragma unroll
       for (int k = 0; k < TG; ++k) {
-        const int i = min(o0 + 8 * (t0 + k) + (lane >> 2), n - 1);
+        const int i = min(o0 + 8 * (t0 + k) + (lane >> 2), row_hi - 1);
         const int iu = i > 0 ? i - 1 : 0, id = i < n - 1 ? i + 1 : n - 1;
         const long r = (long)i * n;
         if (a_h) {
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
 #pragma unroll
       for (int k = 0; k < TG; ++k) {
         const int i = o0 + 8 * (t0 + k) + (lane >> 2);
-        if (i >= n) continue;
+        if (i >= row_hi) continue;
         double x0 = acc[t0 + k][0], x1 = acc[t0 + k][1];
         if (a_h) {
           if (ar) {  // replace the clamped (zero-Neumann) ghosts by odd reflections
@@ -308,15 +309,21 @@ bool band_mma_ok(const BandOp& op) {
 
 int band_mma_koff(int w) { return koff_of(w); }
 
-int band_mma_cols_grid(int n) {
-  return ((n + 15) / 16) * ((n + 32 * kBmT - 1) / (32 * kBmT));
+int band_mma_cols_grid(int n, int rows) {
+  if (rows < 0) rows = n;
+  return ((n + 15) / 16) * ((rows + 32 * kBmT - 1) / (32 * kBmT));
 }
+int band_mma_row_tile() { return 32 * kBmT; }
 
 cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out, const int* skip,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int row_lo, int row_hi) {
   BandTaps tp;
   if (!make_taps(op, &tp)) return cudaErrorInvalidValue;
   const int n = op.n;
+  if (row_hi < 0) row_hi = n;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > n) return cudaErrorInvalidValue;
+  const int nr = row_hi - row_lo;
+  if (nr == 0) return cudaSuccess;
   switch (koff_of(op.w)) {
 #define X(K)                                                                                 \
   case K: {                                                                                  \
@@ -327,8 +334,8 @@ cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out
                            (int)SH::rows_smem());                                            \
       attr = true;                                                                           \
     }                                                                                        \
-    dim3 grid((n + SH::CW - 1) / SH::CW, (n + SH::RH - 1) / SH::RH);                         \
-    k_bmma_rows<K><<<grid, 256, SH::rows_smem(), st>>>(op, tp, in, out, skip);               \
+    dim3 grid((n + SH::CW - 1) / SH::CW, (nr + SH::RH - 1) / SH::RH);                        \
+    k_bmma_rows<K><<<grid, 256, SH::rows_smem(), st>>>(op, tp, in, out, skip, row_lo, row_hi); \
     return cudaGetLastError();                                                               \
   }
     TVD_KOFFS(X)
@@ -338,10 +345,15 @@ cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out
 }
 
 cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out,
-                                 const Epilogue& ep, const int* skip, cudaStream_t st) {
+                                 const Epilogue& ep, const int* skip, cudaStream_t st, int row_lo,
+                                 int row_hi) {
   BandTaps tp;
   if (!make_taps(op, &tp)) return cudaErrorInvalidValue;
   const int n = op.n;
+  if (row_hi < 0) row_hi = n;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > n) return cudaErrorInvalidValue;
+  const int nr = row_hi - row_lo;
+  if (nr == 0) return cudaSuccess;
   switch (koff_of(op.w)) {
 #define X(K)                                                                                 \
   case K: {                                                                                  \
@@ -352,8 +364,9 @@ cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out
                            (int)SH::cols_smem());                                            \
       attr = true;                                                                           \
     }                                                                                        \
-    dim3 grid((n + SH::CC - 1) / SH::CC, (n + SH::RW - 1) / SH::RW);                         \
-    k_bmma_cols<K><<<grid, 256, SH::cols_smem(), st>>>(op, tp, in, out, ep, skip);           \
+    dim3 grid((n + SH::CC - 1) / SH::CC, (nr + SH::RW - 1) / SH::RW);                        \
+    k_bmma_cols<K><<<grid, 256, SH::cols_smem(), st>>>(op, tp, in, out, ep, skip, row_lo,     \
+                                                       row_hi);                               \
     return cudaGetLastError();                                                               \
   }
     TVD_KOFFS(X)

@@ -1847,3 +1847,5 @@ int tvd_vec_binary(tvd_ctx* c, long long count, int op, const double* x, const d
 }
 
 }  // extern "C"
+
+#include "tvd_slab.cuh"

@@ -122,6 +122,11 @@ struct LineIO {
   int ar_mode;
   const double* ar_ql;
   const double* ar_qr;
+  // segmented input rows (row-slab decomposition, pipeline and Rader passes): when in_seg > 0,
+  // element e of line l is in[(e / in_seg) * in_seg_stride + l * in_seg + e % in_seg] -- the
+  // layout an all-to-all of per-rank blocks leaves behind; 0 = row-major (l * len + e)
+  int in_seg;
+  long in_seg_stride;
 };
 
 // Band projection of one batch of lines (preconditioner assembly).
@@ -165,5 +170,8 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
 int pipe_grid(const PfaPlan& P, int nlines);
 // out = in^T for an n x n fp64 array (tvd_stencil.cu)
 cudaError_t launch_transpose(const double* in, double* out, int n, cudaStream_t st);
+// out (cols x rows) = in^T for a rows x cols fp64 array
+cudaError_t launch_transpose_rect(const double* in, double* out, int rows, int cols,
+                                  const int* skip, cudaStream_t st);
 
 }  // namespace tvd

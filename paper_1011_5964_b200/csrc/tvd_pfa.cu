@@ -609,6 +609,8 @@ struct PipeK {
   int ar_mode;  // LineIO::ar_mode
   const double* ar_ql;
   const double* ar_qr;
+  int in_seg;          // LineIO::in_seg (0: row-major input)
+  long in_seg_stride;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -750,7 +752,14 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     mbar_expect_tx(&mbar, (unsigned)(rows * n * 8));
     for (int l = 0; l < rows; ++l) {
       const long r = (long)(batch * B + l) * n;
-      bulk_g2s(stage + l * n, p.in + r, (unsigned)(n * 8), &mbar);
+      if (p.in_seg) {  // one bulk copy per all-to-all block of the row
+        const long base = (long)(batch * B + l) * p.in_seg;
+        for (int s0 = 0; s0 < n; s0 += p.in_seg)
+          bulk_g2s(stage + l * n + s0, p.in + (s0 / p.in_seg) * p.in_seg_stride + base,
+                   (unsigned)(p.in_seg * 8), &mbar);
+      } else {
+        bulk_g2s(stage + l * n, p.in + r, (unsigned)(n * 8), &mbar);
+      }
       // the row streams read with plain loads later in this batch: pull them into L2 now
       if (p.pre) bulk_prefetch_l2(p.pre + r, (unsigned)(n * 8));
       if (p.mid) bulk_prefetch_l2(p.mid + r, (unsigned)(n * 8));
@@ -1159,6 +1168,9 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
   k.ar_mode = io.ar_mode;
   k.ar_ql = io.ar_ql;
   k.ar_qr = io.ar_qr;
+  if (io.in_seg && (io.in_seg % 2 || len % io.in_seg)) return cudaErrorInvalidValue;
+  k.in_seg = io.in_seg;
+  k.in_seg_stride = io.in_seg_stride;
   static const int stages_env = [] {
     const char* s = getenv("TVD_PFA_STAGES");
     return s ? atoi(s) : 3;

@@ -166,8 +166,13 @@ __global__ void __launch_bounds__(kRaderThreads, 1) k_rader_rows(const RaderK p)
     const double2 R = rbuf[__ldg(&p.pl.rout[k - 1])];  // C = conj(R) / M, 1/M in scale
     return ((k & 1) ? -(R.x - R.y) : -(-R.y - R.x)) * p.scale;
   };
+  // element e of this line in the input (row-major or all-to-all segmented, LineIO::in_seg)
+  auto in_at = [&](int e) {
+    if (!io.in_seg) return io.in[(long)line * n + e];
+    return io.in[(long)(e / io.in_seg) * io.in_seg_stride + (long)line * io.in_seg + e % io.in_seg];
+  };
   for (int t = 1 + tid; t <= M; t += nth) {
-    double x = io.in[rb + t];
+    double x = in_at(p.off - 1 + t);
     if (io.pre) x = io.pre_mul ? x * io.pre[rb + t] : x / io.pre[rb + t];
     pack(t, x);
   }
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(kRaderThreads, 1) k_rader_rows(const RaderK p)
   }
   if (p.off && tid < 2) {  // Shat borders pass through every transform
     const long g = (long)line * n + (tid ? n - 1 : 0);
-    double v = io.in[g];
+    double v = in_at(tid ? n - 1 : 0);
     if (io.pre) v = io.pre_mul ? v * io.pre[g] : v / io.pre[g];
     if (io.mid_mul) v *= io.mid_mul[g];
     if (io.post) v = io.post_mul ? v * io.post[g] : v / io.post[g];

@@ -764,26 +764,32 @@ cudaError_t launch_normal_epilogue(const double* base, const Epilogue& ep, int n
 }
 
 // ----------------------------------------------------------- transpose
-__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int n) {
+__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int rows,
+                            int cols, const int* skip) {
+  if (skip && *skip) return;
   __shared__ double tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int i = by + r, j = bx + threadIdx.x;
-    if (i < n && j < n) tile[r][threadIdx.x] = in[(long)i * n + j];
+    if (i < rows && j < cols) tile[r][threadIdx.x] = in[(long)i * cols + j];
   }
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int i = bx + r, j = by + threadIdx.x;
-    if (i < n && j < n) out[(long)i * n + j] = tile[threadIdx.x][r];
+    if (i < cols && j < rows) out[(long)i * rows + j] = tile[threadIdx.x][r];
   }
 }
 }  // namespace tvd
 
 namespace tvd {
-cudaError_t launch_transpose(const double* in, double* out, int n, cudaStream_t st) {
-  dim3 grid((n + 31) / 32, (n + 31) / 32), block(32, 8);
-  k_transpose<<<grid, block, 0, st>>>(in, out, n);
+cudaError_t launch_transpose_rect(const double* in, double* out, int rows, int cols,
+                                  const int* skip, cudaStream_t st) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+  k_transpose<<<grid, block, 0, st>>>(in, out, rows, cols, skip);
   return cudaGetLastError();
+}
+cudaError_t launch_transpose(const double* in, double* out, int n, cudaStream_t st) {
+  return launch_transpose_rect(in, out, n, n, nullptr, st);
 }
 
 // ------------------------------------------------- blur eigenvalue grid

@@ -62,11 +62,17 @@ __device__ __forceinline__ double diffusion_at(const double* __restrict__ a_h,
 // tensor-core (DMMA) band passes, tvd_band_mma.cu; used when band_mma_ok(op)
 bool band_mma_ok(const BandOp& op);
 int band_mma_koff(int w);  // k-offset of the tensor-core passes for half-width w (0: none)
-int band_mma_cols_grid(int n);
+int band_mma_cols_grid(int n, int rows = -1);
+int band_mma_row_tile();  // output rows per column-pass CTA (row windows align to it)
+// row_lo / row_hi: output rows [row_lo, row_hi) only (row-slab decomposition; -1 = all).
+// Pointers index global rows (in + row * n); the column pass reads `in` rows
+// [row_lo - KOFF, row_hi + KOFF) and the epilogue's lw rows row_lo - 1 .. row_hi (clipped to
+// the image), a_v rows row_lo .. row_hi.
 cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out, const int* skip,
-                                 cudaStream_t st);
+                                 cudaStream_t st, int row_lo = 0, int row_hi = -1);
 cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out,
-                                 const Epilogue& ep, const int* skip, cudaStream_t st);
+                                 const Epilogue& ep, const int* skip, cudaStream_t st,
+                                 int row_lo = 0, int row_hi = -1);
 
 int band_rows_blocks(int n);
 int band_cols_blocks(int n);          // upper bound over both column-pass variants

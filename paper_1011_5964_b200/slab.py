@@ -1,0 +1,317 @@
+"""Row-slab decomposition of one large inner solve across ranks.
+
+The reference solves one image on one CPU (krylov.py:82-116).  For an 8192^2 problem this
+build splits the image into row slabs, one per GPU: rank ``rho`` of ``P`` owns the global
+rows ``[rho R, rho R + R)``, ``R = n / P``, of every ``n x n`` array.  The kernels of one PCG
+iteration run in the native library (``tvd_slab_phase``, ``csrc/tvd_slab.cuh``); between the
+phases this module runs the collectives:
+
+* **halo exchange** of ``t = p G_1^T`` (``khalo`` rows) and of ``p`` (one row, the ``L``
+  stencil) with the two neighbouring slabs -- the column band pass ``G_0 t`` and ``L p`` are
+  local otherwise;
+* **all-to-all** twice inside the preconditioner: the row DST writes its output transposed,
+  so block ``j`` of the send buffer already holds the columns of rank ``j``; after the
+  exchange every column is a line of ``P`` contiguous segments (one TMA bulk copy each) for
+  the column "sandwich" pass (DST, ``lambda^-1``, DST), and the second exchange brings the
+  rows back for the last row DST;
+* **allgather** of one double per dot product (``p.q``, ``r.r``, ``r.z``); every rank sums the
+  ``P`` contributions in rank order, so every rank computes bit-identical scalars and takes
+  the same branch (stop test, exceptions) without a broadcast.
+
+The same schedule runs over three communicators: :class:`TorchComm` (``torch.distributed``,
+NCCL over NVLink on the GPU box, gloo in the CPU tests), and :class:`LoopbackComm`, which
+drives ``P`` slabs of one process on one device with local copies (single-GPU parity tests of
+the slab kernels; nothing waits on another kernel).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .krylov import IndefiniteOperatorError, KrylovConfig, SolveOutcome, SolverDivergenceError
+
+# phases and buffers (include/tvdeblur_b200.h TVD_SLAB_*)
+MATVEC_ROWS, MATVEC_COLS, RESIDUAL, START, GAMMA_UPDATE, REL = 0, 1, 2, 3, 4, 5
+PREC_ROWS, PREC_COLS, PREC_FINAL, RZ0, BETA_P = 6, 7, 8, 9, 10
+BUF_X, BUF_R, BUF_Z, BUF_Q, BUF_P_EXT, BUF_T_EXT = 0, 1, 2, 3, 4, 5
+BUF_SEND, BUF_RECV, BUF_CONTRIB, BUF_GATHER = 6, 7, 8, 9
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    """Host-side geometry of one rank's slab (shared by every communicator)."""
+
+    n: int
+    nranks: int
+    rank: int
+    khalo: int
+    exchanges: bool = True  # the preconditioner needs the two all-to-alls
+
+    @property
+    def rows(self) -> int:
+        return self.n // self.nranks
+
+    @property
+    def row_lo(self) -> int:
+        return self.rank * self.rows
+
+    def ext_shape(self, halo: int) -> tuple[int, int]:
+        return (self.rows + 2 * halo, self.n)
+
+    def halo_plan(self, halo: int):
+        """``[(peer, send_rows, recv_rows)]`` of an extended buffer with ``halo`` rows per side:
+        my first interior rows become the bottom halo of rank - 1, my last ones the top halo
+        of rank + 1 (no neighbour beyond the image border)."""
+        R, h = self.rows, halo
+        plan = []
+        if self.rank > 0:
+            plan.append((self.rank - 1, slice(h, 2 * h), slice(0, h)))
+        if self.rank < self.nranks - 1:
+            plan.append((self.rank + 1, slice(R, R + h), slice(R + h, R + 2 * h)))
+        return plan
+
+    def block(self, j: int) -> slice:
+        """Flat range of all-to-all block ``j`` (``R x R`` doubles) of the send / recv buffers."""
+        bs = self.rows * self.rows
+        return slice(j * bs, (j + 1) * bs)
+
+
+class _DeviceArray:
+    """``__cuda_array_interface__`` over a library-owned device buffer."""
+
+    def __init__(self, ptr: int, count: int) -> None:
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class Slab:
+    """One rank's slab solver (``tvd_slab``): buffers, phases and status."""
+
+    def __init__(self, system, precond, nranks: int, rank: int) -> None:
+        """``system``: a full-size :class:`~.pipeline.NormalSystem` (its diffusivities are
+        sliced here); ``precond``: ``None``, a :class:`~.krylov.DiagonalInverse` or a
+        ``FactoredPreconditioner.apply_inverse`` of the full problem."""
+        from .krylov import _fused_precond
+
+        n = system.n
+        if n % nranks:
+            raise ValueError(f"n = {n} is not divisible by {nranks} ranks")
+        R = n // nranks
+        lo = rank * R
+        self.device = system.device
+        self.n, self.nranks, self.rank = n, nranks, rank
+        lop = system.l_op
+        # slab operands (kept alive for the handle's lifetime)
+        self._a_h = lop.a_h_device[lo:lo + R].contiguous()
+        self._a_v = lop.a_v_device[lo:lo + R + 1].contiguous()
+        fused = _fused_precond(precond)
+        if fused is None:
+            raise ValueError("slab solves take None, a DiagonalInverse or "
+                             "FactoredPreconditioner.apply_inverse")
+        kind, family, inv, d = fused
+        self._inv_t = None if inv is None else inv.t()[lo:lo + R].contiguous()
+        self._d = None if d is None else d[lo:lo + R].contiguous()
+        if system.s is not None or system.reblur:
+            raise ValueError("slab solves support the X / D_X systems H^T H + alpha L")
+        self._csys = nat.TvdSystem(system.h_op.handle, system.alpha, lop.spacing,
+                                   self._a_h.data_ptr(), self._a_v.data_ptr(), None,
+                                   lop.bc_code, 0)
+        self._cpre = nat.TvdPrecond(kind, family, nat.ptr(self._inv_t), nat.ptr(self._d))
+        self._h_op = system.h_op  # the blur handle must outlive the slab
+        lib = nat.load()
+        ctx = nat.context(self.device)
+        out = ctypes.c_void_p()
+        nat.check(lib.tvd_slab_create(ctx, ctypes.byref(self._csys), ctypes.byref(self._cpre),
+                                      nranks, rank, ctypes.byref(out)))
+        self.handle = out.value
+        info = (ctypes.c_int * 8)()
+        nat.check(lib.tvd_slab_info(self.handle, info))
+        self.layout = SlabLayout(n, nranks, rank, info[3], bool(info[7]))
+        self._bufs: dict[int, torch.Tensor] = {}
+
+    def __del__(self) -> None:
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                nat.load().tvd_slab_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.handle = None
+
+    def buf(self, which: int) -> torch.Tensor:
+        t = self._bufs.get(which)
+        if t is None:
+            p, cnt = ctypes.c_void_p(), ctypes.c_longlong()
+            nat.check(nat.load().tvd_slab_buffer(self.handle, which, ctypes.byref(p),
+                                                 ctypes.byref(cnt)))
+            t = torch.as_tensor(_DeviceArray(p.value, cnt.value), device=self.device)
+            self._bufs[which] = t
+        return t
+
+    def start(self, b: torch.Tensor, x0: torch.Tensor, config: KrylovConfig, history) -> None:
+        self._b = b  # the library keeps the pointer for the whole solve
+        nat.context(self.device)
+        nat.check(nat.load().tvd_slab_start(self.handle, b.data_ptr(), x0.data_ptr(),
+                                            float(config.tol), int(config.max_iterations),
+                                            nat.ptr(history)))
+
+    def phase(self, ph: int) -> None:
+        nat.check(nat.load().tvd_slab_phase(self.handle, ph))
+
+    def status(self) -> tuple[int, int, int, int, float]:
+        """``(rc, done, iterations, converged, err_iteration, err_value)`` (synchronises)."""
+        done, it, conv, eit = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        ev = ctypes.c_double()
+        rc = nat.load().tvd_slab_status(self.handle, ctypes.byref(done), ctypes.byref(it),
+                                        ctypes.byref(conv), ctypes.byref(eit), ctypes.byref(ev))
+        return rc, done.value, it.value, conv.value, eit.value, ev.value
+
+
+# ------------------------------------------------------------------ communicators
+class TorchComm:
+    """Collectives of one rank over ``torch.distributed`` (NCCL on GPUs, gloo on CPUs)."""
+
+    def __init__(self, group=None) -> None:
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+
+    def halo(self, slabs) -> None:
+        dist = self.dist
+        (s,) = slabs
+        lay = s.layout
+        ops = []
+        for which, h in ((BUF_T_EXT, lay.khalo), (BUF_P_EXT, 1)):
+            ext = s.buf(which).view(lay.ext_shape(h))
+            for peer, snd, rcv in lay.halo_plan(h):
+                ops.append(dist.P2POp(dist.isend, ext[snd], peer, self.group))
+                ops.append(dist.P2POp(dist.irecv, ext[rcv], peer, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def all_to_all(self, slabs) -> None:
+        (s,) = slabs
+        self.dist.all_to_all_single(s.buf(BUF_RECV), s.buf(BUF_SEND), group=self.group)
+
+    def allgather(self, slabs) -> None:
+        (s,) = slabs
+        src, dst = s.buf(BUF_CONTRIB), s.buf(BUF_GATHER)
+        if dst.is_cuda:
+            self.dist.all_gather_into_tensor(dst, src, group=self.group)
+        else:  # gloo has no all_gather_into_tensor
+            parts = list(dst.split(1))
+            self.dist.all_gather(parts, src, group=self.group)
+
+
+class LoopbackComm:
+    """The same collectives over ``P`` slabs held by one process (local copies, in order)."""
+
+    def halo(self, slabs) -> None:
+        for s in slabs:
+            lay = s.layout
+            for which, h in ((BUF_T_EXT, lay.khalo), (BUF_P_EXT, 1)):
+                mine = s.buf(which).view(lay.ext_shape(h))
+                for peer, _, rcv in lay.halo_plan(h):
+                    other = slabs[peer]
+                    theirs = other.buf(which).view(other.layout.ext_shape(h))
+                    snd = next(sl for p2, sl, _ in other.layout.halo_plan(h) if p2 == s.layout.rank)
+                    mine[rcv].copy_(theirs[snd])
+
+    def all_to_all(self, slabs) -> None:
+        sends = [s.buf(BUF_SEND) for s in slabs]
+        for s in slabs:
+            recv, lay = s.buf(BUF_RECV), s.layout
+            for i, snd in enumerate(sends):
+                recv[lay.block(i)].copy_(snd[lay.block(lay.rank)])
+
+    def allgather(self, slabs) -> None:
+        vals = torch.cat([s.buf(BUF_CONTRIB)[:1] for s in slabs])
+        for s in slabs:
+            s.buf(BUF_GATHER)[: len(slabs)].copy_(vals)
+
+
+# ------------------------------------------------------------------ the schedule
+def _run(slabs, ph: int) -> None:
+    for s in slabs:
+        s.phase(ph)
+
+
+def _precond(slabs, comm) -> None:
+    _run(slabs, PREC_ROWS)
+    if slabs[0].layout.exchanges:
+        comm.all_to_all(slabs)
+        _run(slabs, PREC_COLS)
+        comm.all_to_all(slabs)
+        _run(slabs, PREC_FINAL)
+
+
+def _matvec(slabs, comm) -> None:
+    _run(slabs, MATVEC_ROWS)
+    comm.halo(slabs)
+    _run(slabs, MATVEC_COLS)
+
+
+def iteration(slabs, comm) -> None:
+    """One PCG iteration (krylov.py:99-116) of every local slab."""
+    _matvec(slabs, comm)
+    comm.allgather(slabs)
+    _run(slabs, GAMMA_UPDATE)
+    comm.allgather(slabs)
+    _run(slabs, REL)
+    _precond(slabs, comm)
+    comm.allgather(slabs)
+    _run(slabs, BETA_P)
+
+
+def slab_pcg(slabs, comm, b_slabs, x0_slabs, config: KrylovConfig = KrylovConfig(),
+             chunk: int = 4) -> list[SolveOutcome]:
+    """Device-resident PCG over row slabs; same recurrence, stop test and exceptions as
+    :func:`~.krylov.pcg`.  ``slabs`` are this process's :class:`Slab` objects (one per rank
+    under ``torch.distributed``; all ``P`` under :class:`LoopbackComm`)."""
+    hists = []
+    for s, b, x0 in zip(slabs, b_slabs, x0_slabs):
+        h = (torch.empty(config.max_iterations, dtype=torch.float64, device=s.device)
+             if config.record_history else None)
+        hists.append(h)
+        s.start(b, x0, config, h)
+    _matvec(slabs, comm)
+    _run(slabs, RESIDUAL)
+    comm.allgather(slabs)
+    _run(slabs, START)
+    _precond(slabs, comm)
+    comm.allgather(slabs)
+    _run(slabs, RZ0)
+    done_it = 0
+    while True:
+        for _ in range(chunk):
+            iteration(slabs, comm)
+        done_it += chunk
+        sts = [s.status() for s in slabs]
+        if sts[0][1] or done_it >= config.max_iterations + chunk:
+            break
+        chunk = min(chunk * 2, 16)
+    outs = []
+    for s, st, h in zip(slabs, sts, hists):
+        rc, done, it, conv, eit, ev = st
+        if rc == nat.TVD_ERR_DIVERGED:
+            raise SolverDivergenceError("pcg", eit)
+        if rc == nat.TVD_ERR_INDEFINITE:
+            raise IndefiniteOperatorError(eit, ev)
+        nat.check(rc)
+        hist = h[:it].cpu().numpy() if h is not None else np.array([])
+        outs.append(SolveOutcome(s.buf(BUF_X).view(s.layout.rows, s.n).clone(), it, hist,
+                                 bool(conv)))
+    return outs
+
+
+def split_rows(a: torch.Tensor, nranks: int, rank: int) -> torch.Tensor:
+    """Rank ``rank``'s slab of an ``n x n`` array (contiguous copy)."""
+    R = a.shape[0] // nranks
+    return a[rank * R:(rank + 1) * R].contiguous()

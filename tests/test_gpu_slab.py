@@ -1,0 +1,136 @@
+"""GPU parity of the row-slab decomposition (SURVEY.md 8e, config 5 path).
+
+The slab kernels (row-window band passes, all-to-all-segmented DST passes, the PCG phases)
+run through the C ABI for P slabs of one device, driven by the same schedule as the
+multi-GPU run with :class:`~paper_1011_5964_b200.slab.LoopbackComm` standing in for NCCL
+(local copies between the slabs' buffers, in stream order; no kernel waits on another).
+Reference: the single-GPU fused PCG on the same system (itself pinned to the oracle and the
+reference goldens in test_gpu_parity.py) and, at small n, the oracle PCG.  Gates: identical
+iteration counts (the dot products are summed per slab, then over slabs: a different
+rounding order, which the tolerances of BASELINE.json's north_star absorb -- counts +-1) and
+the solution within 1e-10 relative.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+from oracle import tvd_oracle as O
+
+import paper_1011_5964_b200 as tvd
+from paper_1011_5964_b200 import slab as SL
+from paper_1011_5964_b200.harness import CONFIGS, gen_psf, make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(n, m, sigma, alpha, beta, kind="M", seed=0):
+    """A lagged-diffusivity state of a seeded piecewise-constant image blurred on the GPU."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    u = torch.rand(n // 64 + 1, n // 64 + 1, generator=g, dtype=torch.float64)
+    u = torch.nn.functional.interpolate(u[None, None], size=(n, n), mode="nearest")[0, 0]
+    u = u.cuda()
+    hop = tvd.StructuredBlurOperator(tvd.SymmetricPsf(gen_psf("gaussian", m, sigma)),
+                                     tvd.BoundaryCondition.ANTI_REFLECTIVE, n)
+    v = hop.apply(u)
+    v = v + 0.01 * v.norm() / n * torch.randn(n, n, generator=g, dtype=torch.float64).cuda()
+    lop = tvd.DiffusionOperator(v, beta)
+    system = tvd.NormalSystem(hop, lop, alpha)
+    pre = None if kind == "I" else tvd.assemble_preconditioner(kind, hop, lop, alpha)
+    rhs = hop.apply_transpose(v)
+    return system, pre, rhs, v
+
+
+def _solve_both(system, pre, rhs, x0, nranks, tol, max_it=400):
+    cfg = tvd.KrylovConfig(tol=tol, max_iterations=max_it, record_history=True)
+    minv = None if pre is None else pre.apply_inverse
+    ref = tvd.pcg(system, minv, rhs, x0, cfg)
+    slabs = [SL.Slab(system, minv, nranks, r) for r in range(nranks)]
+    outs = SL.slab_pcg(slabs, SL.LoopbackComm(),
+                       [SL.split_rows(rhs, nranks, r) for r in range(nranks)],
+                       [SL.split_rows(x0, nranks, r) for r in range(nranks)], cfg)
+    x = torch.cat([o.solution for o in outs])
+    its = {o.iterations for o in outs}
+    assert len(its) == 1, its  # every slab took the same branch
+    return ref, outs[0], x
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4, 8])
+@pytest.mark.parametrize("kind", ["M", "D_M", "I"])
+def test_slab_pcg_matches_single_gpu_512(nranks, kind):
+    spec = CONFIGS["c2a"]
+    system, pre, rhs, v = _problem(512, spec.m, spec.sigma, spec.alpha, spec.beta, kind)
+    ref, out, x = _solve_both(system, pre, rhs, v, nranks, spec.tol)
+    assert ref.converged and out.converged
+    if kind == "I":
+        # unpreconditioned CG is rounding-sensitive near tol (the reference's own
+        # two operator paths disagree by +-1 there): the gate is the image, counts within 2
+        assert abs(out.iterations - ref.iterations) <= (0 if nranks == 1 else 2)
+        assert rel_err(x.cpu().numpy(), ref.solution.cpu().numpy()) < 1e-8
+        return
+    assert abs(out.iterations - ref.iterations) <= (0 if nranks == 1 else 1)
+    if out.iterations == ref.iterations:
+        assert rel_err(out.residual_history, ref.residual_history) < 1e-9
+    assert rel_err(x.cpu().numpy(), ref.solution.cpu().numpy()) < 1e-10
+
+
+def test_slab_pcg_matches_oracle_c2a():
+    """Config 2a through 4 slabs vs the oracle's PCG on the reference's own operators."""
+    spec = CONFIGS["c2a"]
+    h, v, _ = make_problem(spec)
+    n = spec.n
+    hop = tvd.StructuredBlurOperator(tvd.SymmetricPsf(h), tvd.BoundaryCondition.ANTI_REFLECTIVE, n)
+    lop = tvd.DiffusionOperator(v, spec.beta)
+    pre = tvd.assemble_preconditioner("M", hop, lop, spec.alpha)
+    system = tvd.NormalSystem(hop, lop, spec.alpha)
+    vt = torch.from_numpy(v).cuda()
+    rhs = hop.apply_transpose(vt)
+    cfg = tvd.KrylovConfig(tol=spec.tol, max_iterations=400)
+    slabs = [SL.Slab(system, pre.apply_inverse, 4, r) for r in range(4)]
+    outs = SL.slab_pcg(slabs, SL.LoopbackComm(), [SL.split_rows(rhs, 4, r) for r in range(4)],
+                       [SL.split_rows(vt, 4, r) for r in range(4)], cfg)
+    x = torch.cat([o.solution for o in outs]).cpu().numpy()
+    a_h, a_v = O.diffusivity(v, spec.beta)
+    lam_h = O.blur_eigenvalues(h, "anti_reflective", n)
+    _, lam_inv, _, _ = O.assemble("M", lam_h, O.diffusion_bands(a_h, a_v), spec.alpha)
+
+    def apply_a(w):
+        return O.blur_transpose(O.blur(w, h, "anti_reflective"), h, "anti_reflective") + \
+            spec.alpha * O.diffusion_apply(a_h, a_v, w)
+
+    xo, its, _, ok = O.pcg(apply_a, lambda r: O.precond_solve("sine_hat", lam_inv, r),
+                           O.blur_transpose(v, h, "anti_reflective"), v, spec.tol, 400)
+    assert ok and outs[0].converged
+    assert abs(outs[0].iterations - its) <= 1
+    assert rel_err(x, xo) < 1e-8
+
+
+@pytest.mark.parametrize("nranks", [2, 8])
+def test_slab_pcg_matches_single_gpu_2048(nranks):
+    spec = CONFIGS["c3"]
+    system, pre, rhs, v = _problem(2048, spec.m, spec.sigma, spec.alpha, spec.beta)
+    ref, out, x = _solve_both(system, pre, rhs, v, nranks, spec.tol)
+    assert ref.converged and out.converged
+    assert abs(out.iterations - ref.iterations) <= 1
+    assert rel_err(x.cpu().numpy(), ref.solution.cpu().numpy()) < 1e-10
+
+
+def test_slab_pcg_rader_8192_eight_slabs():
+    """Config 5 geometry: 8192^2, Gaussian 63x63 (band halo 64 rows), prime odd core 8191
+    (Rader engine with segmented input + rectangular transposes), 8 slabs of 1024 rows."""
+    spec = CONFIGS["c5"]
+    system, pre, rhs, v = _problem(8192, spec.m, spec.sigma, spec.alpha, spec.beta)
+    ref, out, x = _solve_both(system, pre, rhs, v, 8, spec.tol)
+    assert ref.converged and out.converged
+    assert abs(out.iterations - ref.iterations) <= 1
+    assert float((x - ref.solution).norm() / ref.solution.norm()) < 1e-10
+
+
+def test_slab_rejects_bad_geometry():
+    spec = CONFIGS["c2a"]
+    system, pre, rhs, v = _problem(512, spec.m, spec.sigma, spec.alpha, spec.beta)
+    with pytest.raises(ValueError):
+        SL.Slab(system, pre.apply_inverse, 3, 0)  # 512 not divisible by 3
+    with pytest.raises(tvd._native.NativeError):
+        SL.Slab(system, pre.apply_inverse, 64, 0)  # 8-row slabs: below the band halo
