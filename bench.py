@@ -352,6 +352,319 @@ def run_ours(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def _time_region(step, args, world: int, local: int, dev):
+    """Warm-up, then K timed steps bracketed by barrier + synchronize, CUDA events on the
+    launching stream; returns (elapsed_s max over ranks, local work sum, launches, clocks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1011_5964_b200 import _native as nat
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = nat.launch_count(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    work = 0
+    with ClockSampler(local) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            work += step()
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = nat.launch_count(dev) - l0
+    elapsed = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t[0])
+    return elapsed, work, launches, clocks.summary()
+
+
+def _sum_over_ranks(vals, world: int, dev):
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return [float(v) for v in vals]
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t]
+
+
+def _profile_kernels(step, n, dev):
+    """Per-category live CUDA-event timing of one step (tvd_ctx_profile) and the dominant
+    HBM-streaming category's roofline entry."""
+    from paper_1011_5964_b200 import _native as nat
+
+    nat.profile(True, dev)
+    work = step()
+    prof = nat.profile_read(dev)
+    nat.profile(False, dev)
+    cats = {k: v for k, v in prof.items() if alg_bytes_per_launch(k, n) > 0}
+    dom = max(cats, key=lambda k: cats[k][0])
+    ms_tot, cnt = cats[dom]
+    achieved = alg_bytes_per_launch(dom, n) / (ms_tot / cnt / 1e3) / 1e9
+    step_ms = sum(t for t, _ in prof.values())
+    kernels = {k: {"ms_total": round(t, 4), "launches": c, "share": round(t / step_ms, 4),
+                   "gbs": (round(alg_bytes_per_launch(k, n) / (t / c / 1e3) / 1e9, 1)
+                           if alg_bytes_per_launch(k, n) else None)}
+               for k, (t, c) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    peaks = _peaks()
+    hbm = float(peaks["hbm_gbs"])
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic_per_launch(dom), "kernel": dom,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("fallback")
+            else "fallback 6650 GB/s"}
+    return roof, kernels, work, hbm
+
+
+def run_slab(args, rank: int, world: int) -> None:
+    """Config 5: one 8192^2 problem.  N = 1: the single-GPU fused PCG.  N > 1: row slabs of
+    n / N rows per rank (slab.py): halo exchanges, two all-to-alls per preconditioner solve
+    and one 8-byte allgather per dot product over NCCL; strong scaling (fixed total work)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1011_5964_b200 as tvd
+    from paper_1011_5964_b200 import slab as SL
+    from paper_1011_5964_b200.harness import CONFIGS, make_problem
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    spec = CONFIGS[args.config]
+    n = spec.n
+    bc = tvd.BoundaryCondition(spec.bc)
+    # every rank generates the same seeded problem (the blur of the truth runs on its GPU)
+    h, v_np, _ = make_problem(spec, exact=False, device=dev)
+    cfg = tvd.KrylovConfig(tol=spec.tol, max_iterations=2000)
+    hop = tvd.StructuredBlurOperator(tvd.SymmetricPsf(h), bc, n, device=dev)
+    v = torch.from_numpy(v_np).to(dev)
+    del v_np
+    rhs = hop.apply_transpose(v)
+    comm = SL.TorchComm() if world > 1 else None
+
+    def operators(u_full):
+        lop = tvd.DiffusionOperator(u_full, spec.beta, device=dev)
+        pre = tvd.assemble_preconditioner("M", hop, lop, spec.alpha)
+        return tvd.NormalSystem(hop, lop, spec.alpha), pre
+
+    def solve(system, pre, x0_full):
+        """(iterations, full solution) of one inner solve"""
+        if world == 1:
+            out = tvd.pcg(system, pre.apply_inverse, rhs, x0_full, cfg)
+            return out.iterations, out.solution
+        s = SL.Slab(system, pre.apply_inverse, world, rank)
+        (o,) = SL.slab_pcg([s], comm, [SL.split_rows(rhs, world, rank)],
+                           [SL.split_rows(x0_full, world, rank)], cfg)
+        full = torch.empty(n, n, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(full, o.solution)
+        return o.iterations, full
+
+    u = v.clone()
+    for _ in range(args.state_fp):  # untimed: a representative lagged-diffusivity state
+        system, pre = operators(u)
+        u = solve(system, pre, u)[1]
+    system, pre = operators(u)
+    if world == 1:
+        def step() -> int:
+            return tvd.pcg(system, pre.apply_inverse, rhs, u, cfg).iterations
+    else:
+        slab = SL.Slab(system, pre.apply_inverse, world, rank)
+        b_s, x_s = SL.split_rows(rhs, world, rank), SL.split_rows(u, world, rank)
+
+        def step() -> int:
+            (o,) = SL.slab_pcg([slab], comm, [b_s], [x_s], cfg)
+            return o.iterations
+
+    elapsed, iters, launches, clk = _time_region(step, args, world, local, dev)
+    (launches,) = _sum_over_ranks([launches], world, dev)
+    value = iters / elapsed  # iterations of the one global problem (identical on every rank)
+    roof, kernels, prof_iters, hbm = _profile_kernels(step, n if world == 1 else n, dev)
+    if world > 1:  # per-rank kernels move 1/N of the bytes of a full-size launch
+        R = n // world
+        for k in kernels.values():
+            if k["gbs"]:
+                k["gbs"] = round(k["gbs"] * R / n, 1)
+        roof["achieved"] *= R / n
+        roof["frac"] = roof["achieved"] / hbm
+
+    # e2e: this rank's slabs of (u, rhs) from pinned host memory, allgather of u, diffusivity
+    # and assembly, the slab solve, D2H of the solution slab
+    R = n // world
+    u_host = SL.split_rows(u, world, rank).cpu().pin_memory()
+    rhs_host = SL.split_rows(rhs, world, rank).cpu().pin_memory()
+    out_host = torch.empty_like(u_host).pin_memory()
+
+    def e2e_step() -> int:
+        us = u_host.to(dev, non_blocking=True)
+        rs = rhs_host.to(dev, non_blocking=True)
+        if world == 1:
+            sysm, p_op = operators(us)
+            res = tvd.pcg(sysm, p_op.apply_inverse, rs, us, cfg)
+            out_host.copy_(res.solution, non_blocking=True)
+            return res.iterations
+        full = torch.empty(n, n, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(full, us)
+        sysm, p_op = operators(full)
+        s = SL.Slab(sysm, p_op.apply_inverse, world, rank)
+        (o,) = SL.slab_pcg([s], comm, [rs], [us], cfg)
+        out_host.copy_(o.solution, non_blocking=True)
+        return o.iterations
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e2e_steps = max(1, min(args.steps, 3))
+    if world > 1:
+        dist.barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    e2e_iters = sum(e2e_step() for _ in range(e2e_steps))
+    s1.record()
+    torch.cuda.synchronize()
+    e2e_t = s0.elapsed_time(s1) / 1e3
+    if world > 1:
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt[0])
+    if rank != 0:
+        return
+    line = {
+        "metric": f"PCG iters/sec at {n}^2 AR fp64 (config {spec.name}, one image, "
+                  f"{'row slabs' if world > 1 else 'single GPU'})",
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE piecewise-constant generator, PCG64 noise)",
+        "config": {"workload": f"{spec.name}: {n}^2 AR fp64, Gaussian {2 * spec.m + 1}x"
+                               f"{2 * spec.m + 1} sigma {spec.sigma}, alpha {spec.alpha}, "
+                               f"beta {spec.beta}, tol {spec.tol}, preconditioner M",
+                   "n": n, "slab_rows": R, "parallelism": f"row slabs x{world}",
+                   "state_fp": args.state_fp, "pcg_iters_per_step": iters / args.steps,
+                   "l2": "inputs larger than L2"},
+        "mpix_iter_per_s": value * n * n / 1e6,
+        "roofline": roof,
+        "pcg_roofline": {"alg_bytes_per_iter": 128.0 * n * n,
+                         "achieved_gbs": 128.0 * n * n * value / world / 1e9,
+                         "frac": 128.0 * n * n * value / world / 1e9 / hbm},
+        "kernels": kernels, "profiled_iterations": prof_iters,
+        "cpu_baseline": None,
+        "e2e": {"value": e2e_iters / e2e_t, "unit": UNIT, "h2d_bytes_per_step": 16 * R * n,
+                "d2h_bytes_per_step": 8 * R * n, "steps": e2e_steps,
+                "includes": "H2D u,rhs slabs; allgather u; diffusivity; device assembly; "
+                            "slab PCG; D2H solution slab"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_batch(args, rank: int, world: int) -> None:
+    """Config 4: 64 independent 1024^2 problems (Gaussian 21x21 / box 11x11 alternating),
+    dealt to the ranks in Gaussian/box pairs (sharding.py); a step is one inner PCG solve of
+    every problem of the rank, ``--streams`` host threads each driving its own stream over
+    its share.  Strong scaling (fixed 64 problems); no collective on the hot path."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
+    import paper_1011_5964_b200 as tvd
+    from paper_1011_5964_b200 import _native as nat
+    from paper_1011_5964_b200.harness import CONFIGS, make_problem
+    from paper_1011_5964_b200.sharding import shard_problems
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    spec = CONFIGS[args.config]
+    n = spec.n
+    bc = tvd.BoundaryCondition(spec.bc)
+    mine = shard_problems(spec.problems, world, rank)
+    cfg = tvd.KrylovConfig(tol=spec.tol, max_iterations=2000)
+    probs = []
+    for i in mine:  # untimed: a representative lagged-diffusivity state per problem
+        h, v_np, _ = make_problem(spec, index=i)
+        hop = tvd.StructuredBlurOperator(tvd.SymmetricPsf(h), bc, n, device=dev)
+        v = torch.from_numpy(v_np).to(dev)
+        rhs = hop.apply_transpose(v)
+        u = v.clone()
+        for _ in range(args.state_fp):
+            lop = tvd.DiffusionOperator(u, spec.beta, device=dev)
+            pre = tvd.assemble_preconditioner("M", hop, lop, spec.alpha)
+            u = tvd.pcg(tvd.NormalSystem(hop, lop, spec.alpha), pre.apply_inverse, rhs, u,
+                        cfg).solution
+        lop = tvd.DiffusionOperator(u, spec.beta, device=dev)
+        pre = tvd.assemble_preconditioner("M", hop, lop, spec.alpha)
+        probs.append((tvd.NormalSystem(hop, lop, spec.alpha), pre, rhs, u))
+    nstreams = max(1, min(args.streams, len(probs)))
+    streams = [torch.cuda.Stream(dev) for _ in range(nstreams)]
+    groups = [probs[k::nstreams] for k in range(nstreams)]
+    # persistent workers: each keeps its thread-local native context (stream, plans, scratch)
+    pool = ThreadPoolExecutor(max_workers=nstreams)
+
+    def solve_group(k):
+        torch.cuda.set_device(local)
+        with torch.cuda.stream(streams[k]):
+            return sum(tvd.pcg(s, p.apply_inverse, b, x0, cfg).iterations
+                       for s, p, b, x0 in groups[k])
+
+    def step() -> int:
+        cur = torch.cuda.current_stream(dev)
+        for st in streams:
+            st.wait_stream(cur)
+        its = sum(pool.map(solve_group, range(nstreams)))
+        for st in streams:
+            cur.wait_stream(st)
+        return its
+
+    def solve_all() -> int:  # main thread, one stream (launch counting, kernel profile)
+        return sum(tvd.pcg(s, p.apply_inverse, b, x0, cfg).iterations for s, p, b, x0 in probs)
+
+    elapsed, iters, _, clk = _time_region(step, args, world, local, dev)
+    pool.shutdown()
+    l0 = nat.launch_count(dev)
+    solve_all()
+    launches = (nat.launch_count(dev) - l0) * args.steps  # the contexts of the workers
+    iters, launches = _sum_over_ranks([iters, launches], world, dev)
+    value = iters / elapsed
+    roof, kernels, prof_iters, hbm = _profile_kernels(solve_all, n, dev)
+    if rank != 0:
+        return
+    line = {
+        "metric": f"PCG iters/sec, batch of {spec.problems} x {n}^2 AR fp64 (config {spec.name})",
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE piecewise-constant generator, PCG64 noise)",
+        "config": {"workload": f"{spec.name}: {spec.problems} x {n}^2 AR fp64, Gaussian 21x21 "
+                               f"sigma 3 / box 11x11 alternating, alpha {spec.alpha}, beta "
+                               f"{spec.beta}, tol {spec.tol}, preconditioner M",
+                   "n": n, "problems_per_gpu": len(mine), "streams": nstreams,
+                   "parallelism": f"problem sharding x{world}", "state_fp": args.state_fp,
+                   "pcg_iters_per_step": iters / args.steps, "l2": "inputs larger than L2"},
+        "mpix_iter_per_s": value * n * n / 1e6,
+        "roofline": roof,
+        "pcg_roofline": {"alg_bytes_per_iter": 128.0 * n * n,
+                         "achieved_gbs": 128.0 * n * n * value / world / 1e9,
+                         "frac": 128.0 * n * n * value / world / 1e9 / hbm},
+        "kernels": kernels, "profiled_iterations": prof_iters,
+        "cpu_baseline": None,
+        "e2e": None,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def traffic_per_launch(category: str):
     """DRAM bytes (read + write) per launch of the category's kernel, from the newest committed
     ``ncu --set full`` capture summarised under profiles/<round>/traffic.json (or None)."""
@@ -378,6 +691,7 @@ def main() -> None:
     ap.add_argument("--cpu-iters", type=int, default=6)
     ap.add_argument("--ref-iters", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=4, help="c4: host threads / CUDA streams")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -390,7 +704,12 @@ def main() -> None:
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
     try:
-        run_ours(args, rank, world)
+        if args.config == "c5":
+            run_slab(args, rank, world)
+        elif args.config == "c4":
+            run_batch(args, rank, world)
+        else:
+            run_ours(args, rank, world)
     finally:
         if world > 1:
             import torch.distributed as dist

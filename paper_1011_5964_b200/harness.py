@@ -52,14 +52,14 @@ def gen_piecewise_image(n: int, m: int, rects: int, disks: int, seed: int,
         r0, c0 = rng.integers(0, total, size=2)
         h, w = rng.integers(lo, hi + 1, size=2)
         img[r0:r0 + h, c0:c0 + w] = rng.uniform()
-    yy, xx = np.mgrid[0:total, 0:total]
     for _ in range(disks):
         cy, cx = rng.uniform(0, total, size=2)
         rad = rng.uniform(total / 32, total / 8)
         val = rng.uniform()
         r0, r1 = max(0, int(cy - rad) - 1), min(total, int(cy + rad) + 2)
         c0, c1 = max(0, int(cx - rad) - 1), min(total, int(cx + rad) + 2)
-        sub = (yy[r0:r1, c0:c1] - cy) ** 2 + (xx[r0:r1, c0:c1] - cx) ** 2 <= rad * rad
+        yy, xx = np.ogrid[r0:r1, c0:c1]
+        sub = (yy - cy) ** 2 + (xx - cx) ** 2 <= rad * rad
         img[r0:r1, c0:c1][sub] = val
     if ramp:
         coord = np.arange(total) / max(1, total - 1)
@@ -77,7 +77,25 @@ def _separable_factors(h: np.ndarray):
     return None
 
 
-def valid_convolve(ext: np.ndarray, h: np.ndarray, exact: bool = True) -> np.ndarray:
+def _valid_convolve_device(ext: np.ndarray, g1: np.ndarray, g2: np.ndarray, device):
+    """The separable shifted-slice sum of :func:`valid_convolve` (same operation order) on a
+    torch device -- data generation for the 8192^2 config, not part of the solver."""
+    import torch
+
+    k = len(g1)
+    n = ext.shape[0] - k + 1
+    e = torch.from_numpy(np.ascontiguousarray(ext)).to(device)
+    rows = torch.zeros((ext.shape[0], n), dtype=torch.float64, device=device)
+    for b in range(k):
+        rows += float(g2[k - 1 - b]) * e[:, b:b + n]
+    out = torch.zeros((n, n), dtype=torch.float64, device=device)
+    for a in range(k):
+        out += float(g1[k - 1 - a]) * rows[a:a + n, :]
+    return out.cpu().numpy()
+
+
+def valid_convolve(ext: np.ndarray, h: np.ndarray, exact: bool = True,
+                   device=None) -> np.ndarray:
     """``convolve2d(ext, h, 'valid')`` for a symmetric PSF.
 
     ``exact`` uses ``scipy.signal.convolve2d`` -- the very routine the
@@ -94,6 +112,8 @@ def valid_convolve(ext: np.ndarray, h: np.ndarray, exact: bool = True) -> np.nda
     k = h.shape[0]
     n = ext.shape[0] - k + 1
     sep = _separable_factors(h)
+    if sep is not None and device is not None:
+        return _valid_convolve_device(ext, sep[0], sep[1], device)
     if sep is not None:
         g1, g2 = sep
         rows = np.zeros((ext.shape[0], n))
@@ -112,11 +132,11 @@ def valid_convolve(ext: np.ndarray, h: np.ndarray, exact: bool = True) -> np.nda
 
 
 def blur_and_observe(ext: np.ndarray, h: np.ndarray, n: int, nsr: float,
-                     seed: int, exact: bool = True) -> np.ndarray:
+                     seed: int, exact: bool = True, device=None) -> np.ndarray:
     """Exact blur of the extended truth plus seeded noise at an exact NSR (harness.py:170-198)."""
     if nsr < 0:
         raise ValueError("noise-to-signal ratio must be >= 0")
-    clean = valid_convolve(np.asarray(ext, dtype=float), h, exact)
+    clean = valid_convolve(np.asarray(ext, dtype=float), h, exact, device)
     if clean.shape != (n, n):
         raise ValueError(f"extended input {ext.shape} does not crop to {(n, n)}")
     if nsr == 0:
@@ -157,11 +177,12 @@ CONFIGS = {
 }
 
 
-def make_problem(spec: ProblemSpec, index: int = 0, exact: bool | None = None):
+def make_problem(spec: ProblemSpec, index: int = 0, exact: bool | None = None, device=None):
     """``(psf, v, u_true)`` for problem ``index`` (seeds 2023+i / 7+i).
 
     Config 4 alternates Gaussian 21x21 (even i) and the 11x11 box (odd i).
-    ``exact`` (default: n <= 2048) selects the reference's own convolve2d.
+    ``exact`` (default: n <= 2048) selects the reference's own convolve2d; otherwise
+    ``device`` (a torch device) runs the separable shifted-slice sum there.
     """
     if spec.name == "c4" and index % 2 == 1:
         h, m = gen_psf("box", 5), 5
@@ -170,5 +191,6 @@ def make_problem(spec: ProblemSpec, index: int = 0, exact: bool | None = None):
     if exact is None:
         exact = spec.n <= 2048
     ext = gen_piecewise_image(spec.n, m, spec.rects, spec.disks, 2023 + index, spec.ramp)
-    v = blur_and_observe(ext, h, spec.n, spec.nsr, 7 + index, exact)
+    v = blur_and_observe(ext, h, spec.n, spec.nsr, 7 + index, exact,
+                         None if exact else device)
     return h, v, ext[m:m + spec.n, m:m + spec.n].copy()
