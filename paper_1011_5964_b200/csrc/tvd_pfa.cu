@@ -746,14 +746,24 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       csm[HC::n0 + i] = p.pl.st[0].Sm[i];
     }
   }
-  const int nbatch = (p.nlines + B - 1) / B;
-  auto issue = [&](int batch) {
-    const int rows = min(B, p.nlines - batch * B);
+  // Batches: F full rounds in which CTA c takes lines (j G + c) B .. +B (concurrent CTAs
+  // work on adjacent lines: their transposed column stores share sectors), then one
+  // balanced round that spreads the remaining rem < B G lines evenly (at most B per CTA,
+  // sizes differ by one), so the tail is not a partial wave of full batches.
+  const int G = gridDim.x, c = blockIdx.x;
+  const int F = p.nlines / (B * G), rem = p.nlines - F * B * G;
+  const int tl0 = F * B * G + (int)((long)c * rem / G);
+  const int tl1 = F * B * G + (int)((long)(c + 1) * rem / G);
+  const int nb_cta = F + (tl1 > tl0 ? 1 : 0);
+  auto first_of = [&](int j) { return j < F ? (j * G + c) * B : tl0; };
+  auto rows_of = [&](int j) { return j < F ? B : tl1 - tl0; };
+  auto issue = [&](int j) {
+    const int first = first_of(j), rows = rows_of(j);
     mbar_expect_tx(&mbar, (unsigned)(rows * n * 8));
     for (int l = 0; l < rows; ++l) {
-      const long r = (long)(batch * B + l) * n;
+      const long r = (long)(first + l) * n;
       if (p.in_seg) {  // one bulk copy per all-to-all block of the row
-        const long base = (long)(batch * B + l) * p.in_seg;
+        const long base = (long)(first + l) * p.in_seg;
         for (int s0 = 0; s0 < n; s0 += p.in_seg)
           bulk_g2s(stage + l * n + s0, p.in + (s0 / p.in_seg) * p.in_seg_stride + base,
                    (unsigned)(p.in_seg * 8), &mbar);
@@ -771,7 +781,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   };
   if (tid == 0) {
     mbar_init(&mbar, 1);
-    if ((int)blockIdx.x < nbatch) issue(blockIdx.x);
+    if (nb_cta > 0) issue(0);
   }
   __syncthreads();
   // y_k from the transformed line l, gather index gi = gath[k - 1] (0 for k out of range)
@@ -807,8 +817,8 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   double acc = 0.0;
   unsigned phase = 0;
   PIPE_T_INIT;
-  for (int b = blockIdx.x; b < nbatch; b += gridDim.x) {
-    const int line0 = b * B, nlv = min(B, p.nlines - line0);
+  for (int jb = 0; jb < nb_cta; ++jb) {
+    const int line0 = first_of(jb), nlv = rows_of(jb);
     for (int i = tid; i < B; i += nth) {
       buf[i * LP] = make_double2(0.0, 0.0);
       if (HALF) buf[i * LP + LP - 1] = make_double2(0.0, 0.0);  // pad read by padded r
@@ -876,9 +886,9 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     }
     __syncthreads();
     PIPE_T(1);
-    if (tid == 0 && b + (int)gridDim.x < nbatch) {
+    if (tid == 0 && jb + 1 < nb_cta) {
       fence_proxy_async();  // staging was read through the generic proxy
-      issue(b + gridDim.x);
+      issue(jb + 1);
     }
     if constexpr (HALF) {
       half_transform<Q1, Q2, B, NT / 32, TPW, CSM>(buf, p.pl, p.stages, csm);
@@ -1091,9 +1101,11 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Launch shape per specialisation.  2047 = 89 * 23 runs one 12-warp CTA per SM (its
-// 6 k-tiles of the q = 89 stage split evenly over the warps and the register budget of
-// 170 keeps the DMMA chains unspilled); the smaller lengths run two 8-warp CTAs per SM.
+// Launch shape per specialisation.  2047 = 89 * 23 runs two 6-warp CTAs per SM (one warp
+// per k-tile of the q = 89 stage, one column tile per warp and round; the register budget
+// of 170 keeps the DMMA chains unspilled, and the two independent CTAs overlap one batch's
+// pack / unpack with the other's DFT stages: 273 us vs 291 us per M^-1 for one 12-warp CTA,
+// tools/pipe_variants.py); the smaller lengths run two 8-warp CTAs per SM.
 // TVD_PIPE_VARIANT overrides the 89 * 23 shape for experiments.
 struct PipeVariant {
   int threads, ctas, tpw, lines;
@@ -1130,7 +1142,14 @@ static PipeVariant pipe_variant(int which) {
     case 11: return {256, 2, 3, 2};
     case 12: return {256, 2, 4, 2};
     case 13: return {384, 1, 4, 2};
-    default: return {384, 1, 4, 2};
+    case 14: return {192, 2, 3, 2};
+    case 15: return {192, 2, 4, 2};
+    case 16: return {192, 2, 2, 2};
+    case 17: return {192, 2, 2, 2};
+    case 18: return {192, 2, 1, 2};
+    case 19: return {192, 3, 2, 2};
+    case 20: return {192, 3, 1, 2};
+    default: return pipe_half() ? PipeVariant{192, 2, 1, 2} : PipeVariant{384, 1, 4, 2};
   }
 }
 
@@ -1196,8 +1215,15 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
         case 11: return launch_pipe_t<89, 23, 1, 256, 2, 3, true, 2, true>(k, grid, st);
         case 12: return launch_pipe_t<89, 23, 1, 256, 2, 4, true, 2, true>(k, grid, st);
         case 13: return launch_pipe_t<89, 23, 1, 384, 1, 4, true, 2, true>(k, grid, st);
+        case 14: return launch_pipe_t<89, 23, 1, 192, 2, 3, true>(k, grid, st);
+        case 15: return launch_pipe_t<89, 23, 1, 192, 2, 4, true>(k, grid, st);
+        case 16: return launch_pipe_t<89, 23, 1, 192, 2, 2, true>(k, grid, st);
+        case 17: return launch_pipe_t<89, 23, 1, 192, 2, 2, true, 2, true>(k, grid, st);
+        case 18: return launch_pipe_t<89, 23, 1, 192, 2, 1, true>(k, grid, st);
+        case 19: return launch_pipe_t<89, 23, 1, 192, 3, 2, true>(k, grid, st);
+        case 20: return launch_pipe_t<89, 23, 1, 192, 3, 1, true>(k, grid, st);
         default:
-          return pipe_half() ? launch_pipe_t<89, 23, 1, 384, 1, 4, true>(k, grid, st)
+          return pipe_half() ? launch_pipe_t<89, 23, 1, 192, 2, 1, true>(k, grid, st)
                              : launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
       }
     case 2: return launch_pipe_t<31, 11, 3>(k, grid, st);
