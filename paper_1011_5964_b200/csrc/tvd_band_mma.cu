@@ -39,6 +39,10 @@ __device__ __forceinline__ void cp_commit_wait() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const double* p) {
+  if (p) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+
 struct BandTaps {
   double t[64];  // t[k] = symmetric interior tap at offset +-k
 };
@@ -148,6 +152,26 @@ __global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
   double* fr = smb + SH::HEIGHT * CP;
   const int n = op.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ib = row_lo + blockIdx.y * SH::RW, j0 = blockIdx.x * SH::CC;
+  // The epilogue's operands (a_h, a_v, lw and the extra streams) are read long after the
+  // tile: pull their rows into L2 now so those loads hit L2 instead of waiting on DRAM.
+  if (ep.prefetch) {
+    for (int i = tid; i < SH::RW + 2; i += blockDim.x) {
+      const int row = ib - 1 + i;
+      if (row < 0 || row >= n || row > row_hi) continue;
+      const int c0 = j0 > 0 ? j0 - 1 : 0;
+      prefetch_l2(ep.lw ? ep.lw + (long)row * n + c0 : nullptr);
+      prefetch_l2(ep.lw ? ep.lw + (long)row * n + min(j0 + SH::CC, n - 1) : nullptr);
+      if (row >= ib && row < row_hi) {
+        prefetch_l2(ep.a_h ? ep.a_h + (long)row * (n + 1) + j0 : nullptr);
+        prefetch_l2(ep.a_h ? ep.a_h + (long)row * (n + 1) + j0 + SH::CC : nullptr);
+        prefetch_l2(ep.a_v ? ep.a_v + (long)row * n + j0 : nullptr);
+        prefetch_l2(ep.a_v ? ep.a_v + (long)row * n + j0 + SH::CC - 1 : nullptr);
+        if (ep.s) prefetch_l2(ep.s + (long)row * n + j0);
+        if (ep.dot_with && ep.dot_with != ep.lw) prefetch_l2(ep.dot_with + (long)row * n + j0);
+      }
+      if (row == row_hi && ep.a_v) prefetch_l2(ep.a_v + (long)row * n + j0);
+    }
+  }
   for (int e = tid; e < SH::HEIGHT * C2; e += blockDim.x) {
     const int r = e / C2, c = 2 * (e - r * C2);
     const int row = ib - KOFF + r, col = j0 + c;
@@ -345,11 +369,17 @@ cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out
 }
 
 cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out,
-                                 const Epilogue& ep, const int* skip, cudaStream_t st, int row_lo,
+                                 const Epilogue& ep_in, const int* skip, cudaStream_t st, int row_lo,
                                  int row_hi) {
   BandTaps tp;
   if (!make_taps(op, &tp)) return cudaErrorInvalidValue;
   const int n = op.n;
+  static const int prefetch = [] {  // TVD_BAND_PREFETCH=1: measured slower (96 vs 88 us)
+    const char* e = getenv("TVD_BAND_PREFETCH");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  Epilogue ep = ep_in;
+  ep.prefetch = prefetch;
   if (row_hi < 0) row_hi = n;
   if (row_lo < 0 || row_lo > row_hi || row_hi > n) return cudaErrorInvalidValue;
   const int nr = row_hi - row_lo;

@@ -33,6 +33,7 @@ struct Epilogue {
   double* partial;
   PcgFin fin;
   int bc_l;              // diffusion ghosts: 0 zero Neumann, 1 anti-reflective
+  int prefetch;          // tensor-core column pass: L2 prefetch of the epilogue operands
   double* partial_self;  // optional per-CTA partials of q . q (BiCGstab t . t)  // gamma finalizer folded into the last CTA (tensor-core pass; s == nullptr: off)
 };
 
