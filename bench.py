@@ -273,29 +273,62 @@ def run_ours(args, rank: int, world: int) -> None:
                            if alg_bytes_per_launch(k, n) else None)}
                for k, (t, c) in sorted(prof.items(), key=lambda kv: -kv[1][0])}
 
-    # ---- e2e through the public API from pinned host buffers
+    # ---- e2e through the public API from pinned host buffers.  Every step copies its inputs
+    # (u, rhs) host -> device and its solution device -> host inside the timed region; the
+    # copies run on two copy streams, double-buffered, so step s + 1's upload and step s - 1's
+    # download overlap step s's compute (as a streaming deployment would run it).
     u_host = u.cpu().pin_memory()
     rhs_host = rhs.cpu().pin_memory()
-    out_host = torch.empty_like(u_host).pin_memory()
+    outs_host = [torch.empty_like(u_host).pin_memory() for _ in range(2)]
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    dbuf = [(torch.empty_like(u), torch.empty_like(rhs)) for _ in range(2)]
+    h2d_done = [torch.cuda.Event() for _ in range(2)]
+    comp_done = [torch.cuda.Event() for _ in range(2)]
+    d2h_done = [torch.cuda.Event() for _ in range(2)]
 
-    def e2e_step() -> int:
-        ud = u_host.to(dev, non_blocking=True)
-        rd = rhs_host.to(dev, non_blocking=True)
-        l_op = tvd.DiffusionOperator(ud, spec.beta, device=dev)
-        p_op = tvd.assemble_preconditioner(kind, hop, l_op, spec.alpha)
-        res = tvd.pcg(tvd.NormalSystem(hop, l_op, spec.alpha), p_op.apply_inverse, rd, ud, cfg)
-        out_host.copy_(res.solution, non_blocking=True)
-        return res.iterations
+    def upload(k):
+        with torch.cuda.stream(h2d):
+            h2d.wait_event(comp_done[k % 2])  # step k - 2 has finished with this buffer
+            dbuf[k % 2][0].copy_(u_host, non_blocking=True)
+            dbuf[k % 2][1].copy_(rhs_host, non_blocking=True)
+            h2d_done[k % 2].record(h2d)
 
-    e2e_step()
+    def run_steps(nsteps: int) -> int:
+        cur = torch.cuda.current_stream(dev)
+        for e in comp_done + d2h_done:
+            e.record(cur)
+        h2d.wait_stream(cur)
+        d2h.wait_stream(cur)
+        its = 0
+        upload(0)
+        for k in range(nsteps):
+            if k + 1 < nsteps:
+                upload(k + 1)
+            cur.wait_event(h2d_done[k % 2])
+            cur.wait_event(d2h_done[k % 2])  # outs_host[k % 2] drained (its step k - 2)
+            ud, rd = dbuf[k % 2]
+            l_op = tvd.DiffusionOperator(ud, spec.beta, device=dev)
+            p_op = tvd.assemble_preconditioner(kind, hop, l_op, spec.alpha)
+            res = tvd.pcg(tvd.NormalSystem(hop, l_op, spec.alpha), p_op.apply_inverse, rd, ud,
+                          cfg)
+            comp_done[k % 2].record(cur)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(comp_done[k % 2])
+                outs_host[k % 2].copy_(res.solution, non_blocking=True)
+                res.solution.record_stream(d2h)  # not recycled before the copy has read it
+                d2h_done[k % 2].record(d2h)
+            its += res.iterations
+        cur.wait_stream(h2d)
+        cur.wait_stream(d2h)
+        return its
+
+    run_steps(2)
     torch.cuda.synchronize()
     barrier()
-    e2e_iters = 0
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(2, min(args.steps, 5))
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
-    for _ in range(e2e_steps):
-        e2e_iters += e2e_step()
+    e2e_iters = run_steps(e2e_steps)
     s1.record()
     torch.cuda.synchronize()
     e2e_t = s0.elapsed_time(s1) / 1e3
@@ -345,7 +378,9 @@ def run_ours(args, rank: int, world: int) -> None:
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * n * n,
                 "d2h_bytes_per_step": 8 * n * n, "steps": e2e_steps,
-                "includes": "H2D u,rhs; diffusivity; device assembly; PCG; D2H solution"},
+                "includes": "H2D u,rhs; diffusivity; device assembly; PCG; D2H solution "
+                            "(copies double-buffered on two copy streams, overlapping the "
+                            "neighbouring steps' compute)"},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
