@@ -1101,6 +1101,33 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+#include "tvd_pfa_ws.cuh"
+
+template <int Q1, int Q2, int NP, int NC, int TPW, int MINB = 1>
+static cudaError_t launch_ws_t(const PipeK& k, int grid, cudaStream_t st) {
+  constexpr int LPh = HalfShape<Q1, Q2>::LPh;
+  const size_t smem = (size_t)2 * 2 * LPh * 16 + (size_t)2 * k.n * 8;
+  if (smem > 220 * 1024 || !k.pl.hscat) return cudaErrorInvalidConfiguration;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dst_ws<Q1, Q2, NP, NC, TPW, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  k_dst_ws<Q1, Q2, NP, NC, TPW, MINB><<<grid, (NP + NC) * 32, smem, st>>>(k);
+  return cudaGetLastError();
+}
+// TVD_PIPE_WS selects the warp-specialised pass (tvd_pfa_ws.cuh; 0 = off, the lock-step
+// k_dst_pipe).  Measured at 2048^2 per M^-1: 272-288 us for 4-6 producer + 6-8 consumer warps
+// vs 275 us lock step (bit-identical results): the phases do not overlap profitably, so off.
+static int pipe_ws_id() {
+  static const int v = [] {
+    const char* s = getenv("TVD_PIPE_WS");
+    return s ? atoi(s) : 0;
+  }();
+  return v;
+}
+
 // Launch shape per specialisation.  2047 = 89 * 23 runs two 6-warp CTAs per SM (one warp
 // per k-tile of the q = 89 stage, one column tile per warp and round; the register budget
 // of 170 keeps the DMMA chains unspilled, and the two independent CTAs overlap one batch's
@@ -1195,6 +1222,21 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
     return s ? atoi(s) : 3;
   }();
   k.stages = stages_env;
+  if (pipe_ws_id() > 0 && io.ar_mode == 0 && pipe_half() && (which == 1 || which == 3)) {
+    const int nbatch = (nlines + 1) / 2;
+    const int grid = nbatch < kSMs ? nbatch : kSMs;
+    if (nblocks_out) *nblocks_out = grid;
+    if (grid <= 0) return cudaSuccess;
+    if (which == 3) return launch_ws_t<73, 7, 4, 8, 1>(k, grid, st);
+    switch (pipe_ws_id()) {
+      case 2: return launch_ws_t<89, 23, 4, 8, 2>(k, grid, st);
+      case 3: return launch_ws_t<89, 23, 6, 6, 1>(k, grid, st);
+      case 4: return launch_ws_t<89, 23, 2, 8, 1>(k, grid, st);
+      case 5: return launch_ws_t<89, 23, 4, 6, 1>(k, grid, st);
+      case 6: return launch_ws_t<89, 23, 6, 6, 2>(k, grid, st);
+      default: return launch_ws_t<89, 23, 4, 8, 1>(k, grid, st);
+    }
+  }
   const int grid = pipe_grid(P, nlines);
   if (nblocks_out) *nblocks_out = grid;
   if (grid <= 0) return cudaSuccess;

@@ -33,7 +33,12 @@ n = int(sys.argv[1])
 import numpy as np  # noqa: E402
 base = None
 for v in sys.argv[2:]:
-    env = dict(os.environ, TVD_PIPE_VARIANT=v)
+    # a token is a TVD_PIPE_VARIANT id or a comma list of NAME=value environment settings
+    if "=" in v:
+        env = dict(os.environ, **dict(kv.split("=", 1) for kv in v.split(",")))
+        v = v.replace("=", "").replace(",", "_")
+    else:
+        env = dict(os.environ, TVD_PIPE_VARIANT=v)
     out = subprocess.run([sys.executable, "-c", CHILD % (root, n, v)], env=env,
                          capture_output=True, text=True)
     if out.returncode:
