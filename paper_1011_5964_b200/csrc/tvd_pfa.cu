@@ -1152,7 +1152,32 @@ static bool pipe_half() {
   }();
   return on;
 }
+// TVD_PIPE_VARIANT2: launch shapes of the 1023 = 31 * 11 * 3 pass (config 4) for experiments
+static int pipe_variant2_id() {
+  static const int v = [] {
+    const char* s = getenv("TVD_PIPE_VARIANT2");
+    return s ? atoi(s) : -1;
+  }();
+  return v;
+}
 static PipeVariant pipe_variant(int which) {
+  if (which == 2) {
+    switch (pipe_variant2_id()) {
+      case 1: return {192, 2, 1, 2};
+      case 2: return {192, 2, 2, 2};
+      case 3: return {384, 1, 3, 2};
+      case 4: return {128, 3, 3, 2};
+      case 5: return {256, 2, 1, 2};
+      case 6: return {128, 4, 2, 2};
+      case 7: return {128, 4, 1, 2};
+      case 8: return {128, 4, 3, 2};
+      case 9: return {96, 4, 2, 2};
+      case 10: return {64, 4, 2, 2};
+      case 11: return {160, 4, 2, 2};
+      case 0: return {256, 2, 3, 2};
+      default: return {64, 4, 2, 2};
+    }
+  }
   if (which != 1) return {256, 2, 3, 2};
   switch (pipe_variant_id()) {
     case 0: return {256, 2, 3, 2};
@@ -1268,7 +1293,23 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
           return pipe_half() ? launch_pipe_t<89, 23, 1, 192, 2, 1, true>(k, grid, st)
                              : launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
       }
-    case 2: return launch_pipe_t<31, 11, 3>(k, grid, st);
+    case 2:
+      switch (pipe_variant2_id()) {
+        case 1: return launch_pipe_t<31, 11, 3, 192, 2, 1>(k, grid, st);
+        case 2: return launch_pipe_t<31, 11, 3, 192, 2, 2>(k, grid, st);
+        case 3: return launch_pipe_t<31, 11, 3, 384, 1, 3>(k, grid, st);
+        case 4: return launch_pipe_t<31, 11, 3, 128, 3, 3>(k, grid, st);
+        case 5: return launch_pipe_t<31, 11, 3, 256, 2, 1>(k, grid, st);
+        case 6: return launch_pipe_t<31, 11, 3, 128, 4, 2>(k, grid, st);
+        case 7: return launch_pipe_t<31, 11, 3, 128, 4, 1>(k, grid, st);
+        case 8: return launch_pipe_t<31, 11, 3, 128, 4, 3>(k, grid, st);
+        case 9: return launch_pipe_t<31, 11, 3, 96, 4, 2>(k, grid, st);
+        case 10: return launch_pipe_t<31, 11, 3, 64, 4, 2>(k, grid, st);
+        case 11: return launch_pipe_t<31, 11, 3, 160, 4, 2>(k, grid, st);
+        case 0: return launch_pipe_t<31, 11, 3>(k, grid, st);
+        // four 2-warp CTAs per SM: 99 us per M^-1 at 1024^2 vs 127 us for two 8-warp CTAs
+        default: return launch_pipe_t<31, 11, 3, 64, 4, 2>(k, grid, st);
+      }
     case 3:
       return pipe_half() ? launch_pipe_t<73, 7, 1, 256, 2, 3, true>(k, grid, st)
                          : launch_pipe_t<73, 7, 1>(k, grid, st);
