@@ -59,14 +59,14 @@ __device__ __forceinline__ const double* border_frag(const BandOp& op, int p, in
   return op.frag + (size_t)idx * S * 32;
 }
 
-template <int KOFF>
+template <int KOFF, int TC = kBmT>
 struct BmShape {
   static constexpr int S = 2 + KOFF / 2;  // k-steps per tile
   // row pass: 2 row blocks x 4 column strips of 8 T outputs
   static constexpr int RH = 16, CW = 32 * kBmT, WIDTH = CW + 2 * KOFF;
   static constexpr int RP = WIDTH + ((4 - WIDTH % 16) + 16) % 16;  // pitch = 4 (mod 16)
   // column pass: 4 row strips of 8 T outputs x 2 column tiles
-  static constexpr int RW = 32 * kBmT, CC = 16, HEIGHT = RW + 2 * KOFF;
+  static constexpr int RW = 4 * 8 * TC, CC = 16, HEIGHT = RW + 2 * KOFF;  // TC tiles per warp
   static constexpr int CP = 24;  // pitch = 8 (mod 16): 4 rows x 8 columns in 2 wavefronts
   static size_t rows_smem() { return (size_t)(RH * RP + S * 32) * sizeof(double); }
   static size_t cols_smem() { return (size_t)(HEIGHT * CP + S * 32) * sizeof(double); }
@@ -138,14 +138,14 @@ __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
   }
 }
 
-template <int KOFF>
-__global__ void __launch_bounds__(256, 2) k_bmma_cols(BandOp op, BandTaps tp,
+template <int KOFF, int TC, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_bmma_cols(BandOp op, BandTaps tp,
                                                      const double* __restrict__ in,
                                                      double* __restrict__ out, Epilogue ep,
                                                      const int* skip, int row_lo, int row_hi) {
   if (skip && *skip) return;
-  using SH = BmShape<KOFF>;
-  constexpr int T = kBmT, S = SH::S, CP = SH::CP, C2 = SH::CC / 2;
+  using SH = BmShape<KOFF, TC>;
+  constexpr int T = TC, S = SH::S, CP = SH::CP, C2 = SH::CC / 2;
   extern __shared__ __align__(16) double smb[];
   __shared__ double red[32];
   double* tile = smb;
@@ -333,11 +333,26 @@ bool band_mma_ok(const BandOp& op) {
 
 int band_mma_koff(int w) { return koff_of(w); }
 
+// column-pass shape: TVD_BAND_COLS_VARIANT 0 = 8 tiles per warp (256-row CTAs) x 2 CTAs/SM,
+// 1 = 4 tiles (128 rows) x 3 CTAs, 2 = 4 tiles x 2 CTAs (default: matvec 81.5 us vs 87.7 us
+// for variant 0 at 2048^2; 3 CTAs spill), 3 / 4 = 2 tiles x 2 / 3 CTAs (88 / 96 us)
+static int cols_variant() {
+  static const int v = [] {
+    const char* s = getenv("TVD_BAND_COLS_VARIANT");
+    return s ? atoi(s) : 2;
+  }();
+  return v;
+}
+static int cols_tiles() {
+  const int v = cols_variant();
+  return v == 0 ? 8 : (v <= 2 ? 4 : 2);
+}
 int band_mma_cols_grid(int n, int rows) {
   if (rows < 0) rows = n;
-  return ((n + 15) / 16) * ((rows + 32 * kBmT - 1) / (32 * kBmT));
+  const int rw = 32 * cols_tiles();
+  return ((n + 15) / 16) * ((rows + rw - 1) / rw);
 }
-int band_mma_row_tile() { return 32 * kBmT; }
+int band_mma_row_tile() { return 32 * cols_tiles(); }
 
 cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out, const int* skip,
                                  cudaStream_t st, int row_lo, int row_hi) {
@@ -368,6 +383,24 @@ cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out
   }
 }
 
+template <int K, int TC, int MINB>
+static cudaError_t launch_cols_t(const BandOp& op, const BandTaps& tp, const double* in,
+                                 double* out, const Epilogue& ep, const int* skip, cudaStream_t st,
+                                 int row_lo, int row_hi) {
+  using SH = BmShape<K, TC>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bmma_cols<K, TC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SH::cols_smem());
+    attr = true;
+  }
+  const int n = op.n, nr = row_hi - row_lo;
+  dim3 grid((n + SH::CC - 1) / SH::CC, (nr + SH::RW - 1) / SH::RW);
+  k_bmma_cols<K, TC, MINB><<<grid, 256, SH::cols_smem(), st>>>(op, tp, in, out, ep, skip, row_lo,
+                                                                row_hi);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out,
                                  const Epilogue& ep_in, const int* skip, cudaStream_t st, int row_lo,
                                  int row_hi) {
@@ -386,19 +419,14 @@ cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out
   if (nr == 0) return cudaSuccess;
   switch (koff_of(op.w)) {
 #define X(K)                                                                                 \
-  case K: {                                                                                  \
-    using SH = BmShape<K>;                                                                   \
-    static bool attr = false;                                                                \
-    if (!attr) {                                                                             \
-      cudaFuncSetAttribute(k_bmma_cols<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                           (int)SH::cols_smem());                                            \
-      attr = true;                                                                           \
-    }                                                                                        \
-    dim3 grid((n + SH::CC - 1) / SH::CC, (nr + SH::RW - 1) / SH::RW);                        \
-    k_bmma_cols<K><<<grid, 256, SH::cols_smem(), st>>>(op, tp, in, out, ep, skip, row_lo,     \
-                                                       row_hi);                               \
-    return cudaGetLastError();                                                               \
-  }
+  case K:                                                                                    \
+    switch (cols_variant()) {                                                                \
+      case 1: return launch_cols_t<K, 4, 3>(op, tp, in, out, ep, skip, st, row_lo, row_hi);  \
+      case 2: return launch_cols_t<K, 4, 2>(op, tp, in, out, ep, skip, st, row_lo, row_hi);  \
+      case 3: return launch_cols_t<K, 2, 2>(op, tp, in, out, ep, skip, st, row_lo, row_hi);  \
+      case 4: return launch_cols_t<K, 2, 3>(op, tp, in, out, ep, skip, st, row_lo, row_hi);  \
+      default: return launch_cols_t<K, 8, 2>(op, tp, in, out, ep, skip, st, row_lo, row_hi); \
+    }
     TVD_KOFFS(X)
 #undef X
     default: return cudaErrorInvalidValue;
