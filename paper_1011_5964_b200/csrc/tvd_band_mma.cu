@@ -81,28 +81,58 @@ __device__ __forceinline__ void stage_fragments(double* fr, const BandTaps& tp, 
   }
 }
 
+// Fused CG direction update (PCG iterations >= 2): the pass reads z and the previous
+// direction p_old, forms p = z + beta p_old (numpy rounding, k_pcg_update_p) for its tile
+// including the halo columns, stores its interior columns to p_new (a different buffer:
+// neighbouring CTAs still read p_old halos) and multiplies the formed tile -- the separate
+// p-update pass and one read of p disappear.
+struct PFuse {
+  const double* z;     // nullptr: plain pass over `in`
+  double* p_new;
+  const PcgState* st;  // beta
+};
+
 template <int KOFF>
 __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
                                                      const double* __restrict__ in,
                                                      double* __restrict__ out, const int* skip,
-                                                     int row_lo, int row_hi) {
+                                                     int row_lo, int row_hi, PFuse fz) {
   if (skip && *skip) return;
   using SH = BmShape<KOFF>;
   constexpr int T = kBmT, S = SH::S, RP = SH::RP, W2 = SH::WIDTH / 2;
   extern __shared__ __align__(16) double smb[];
   double* tile = smb;
   double* fr = smb + SH::RH * RP;
+  double* tile2 = fr + S * 32;  // fused: p_old tile (tile holds z)
   const int n = op.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = row_lo + blockIdx.y * SH::RH, jb = blockIdx.x * SH::CW;
+  const double* src = fz.z ? fz.z : in;
   for (int e = tid; e < SH::RH * W2; e += blockDim.x) {
     const int r = e / W2, c = 2 * (e - r * W2);
     const int row = i0 + r, col = jb - KOFF + c;
     const bool ok = row < row_hi && col >= 0 && col < n;
-    cp16(tile + r * RP + c, ok ? in + (long)row * n + col : in + (long)i0 * n, ok);
+    cp16(tile + r * RP + c, ok ? src + (long)row * n + col : src + (long)i0 * n, ok);
+    if (fz.z) cp16(tile2 + r * RP + c, ok ? in + (long)row * n + col : in + (long)i0 * n, ok);
   }
   stage_fragments<KOFF>(fr, tp, op.w);
   cp_commit_wait();
   __syncthreads();
+  if (fz.z) {
+    const double beta = fz.st->beta;
+    for (int e = tid; e < SH::RH * W2; e += blockDim.x) {
+      const int r = e / W2, c = 2 * (e - r * W2);
+      const int row = i0 + r, col = jb - KOFF + c;
+      double2* tz = reinterpret_cast<double2*>(tile + r * RP + c);
+      const double2 po = *reinterpret_cast<const double2*>(tile2 + r * RP + c);
+      const double2 zz = *tz;
+      const double2 pv = make_double2(__dadd_rn(zz.x, __dmul_rn(beta, po.x)),
+                                      __dadd_rn(zz.y, __dmul_rn(beta, po.y)));
+      *tz = pv;  // zero-filled out-of-range elements stay zero
+      if (row < row_hi && col >= jb && col < jb + SH::CW && col < n)
+        *reinterpret_cast<double2*>(fz.p_new + (long)row * n + col) = pv;
+    }
+    __syncthreads();
+  }
   const int rb = warp >> 2, cs = warp & 3;
   const int o0 = jb + cs * 8 * T;  // first output column of the warp
   const double* arow = tile + (rb * 8 + (lane >> 2)) * RP + cs * 8 * T + (lane & 3);
@@ -356,6 +386,15 @@ int band_mma_row_tile() { return 32 * cols_tiles(); }
 
 cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out, const int* skip,
                                  cudaStream_t st, int row_lo, int row_hi) {
+  return launch_band_mma_rows_fused(op, in, out, skip, st, nullptr, nullptr, nullptr, row_lo,
+                                    row_hi);
+}
+
+cudaError_t launch_band_mma_rows_fused(const BandOp& op, const double* in, double* out,
+                                       const int* skip, cudaStream_t st, const double* z,
+                                       double* p_new, const PcgState* pst, int row_lo,
+                                       int row_hi) {
+  const PFuse fz{z, p_new, pst};
   BandTaps tp;
   if (!make_taps(op, &tp)) return cudaErrorInvalidValue;
   const int n = op.n;
@@ -370,11 +409,12 @@ cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out
     static bool attr = false;                                                                \
     if (!attr) {                                                                             \
       cudaFuncSetAttribute(k_bmma_rows<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                           (int)SH::rows_smem());                                            \
+                           (int)(SH::rows_smem() + SH::RH * SH::RP * sizeof(double)));       \
       attr = true;                                                                           \
     }                                                                                        \
     dim3 grid((n + SH::CW - 1) / SH::CW, (nr + SH::RH - 1) / SH::RH);                        \
-    k_bmma_rows<K><<<grid, 256, SH::rows_smem(), st>>>(op, tp, in, out, skip, row_lo, row_hi); \
+    const size_t sm = SH::rows_smem() + (z ? SH::RH * SH::RP * sizeof(double) : 0);           \
+    k_bmma_rows<K><<<grid, 256, sm, st>>>(op, tp, in, out, skip, row_lo, row_hi, fz);        \
     return cudaGetLastError();                                                               \
   }
     TVD_KOFFS(X)

@@ -62,6 +62,7 @@ enum Slot : int {
   kSlotBSH,    // BiCGstab s_hat
   kSlotBT,     // BiCGstab t
   kSlotPartial3,
+  kSlotP2,     // second PCG direction buffer (fused direction update)
   kSlotCount
 };
 
@@ -1034,6 +1035,46 @@ static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double
   return TVD_OK;
 }
 
+// PCG iterations >= 2 with the direction update fused into the row band pass:
+// p_new = z + beta p_old, q = A p_new, partial of p_new . q (gamma folded into the column
+// pass when fin).  Separable X / D_X systems on the tensor-core passes only (pcg_p_fusable).
+static bool pcg_p_fusable(const tvd_system* sys) {
+  static const bool off = getenv("TVD_NO_P_FUSION") != nullptr;
+  const tvd_blur* b = sys->blur;
+  return !off && b->separable && !sys->s && !sys->reblur && band_mma_ok(b->g[0]) &&
+         band_mma_ok(b->g[1]);
+}
+static int system_apply_pfused(tvd_ctx* c, const tvd_system* sys, const double* z,
+                               const double* p_old, double* p_new, double* q, double* partial,
+                               const PcgState* S, const int* skip, int* nb_out, const PcgFin* fin,
+                               bool* fin_done) {
+  tvd_blur* b = sys->blur;
+  const int n = b->n;
+  double* tmp;
+  TVD_SLOT(c, kSlotTmp, (long)n * n, tmp);
+  Epilogue ep{};
+  if (sys->a_h) {
+    ep.a_h = sys->a_h;
+    ep.a_v = sys->a_v;
+    ep.lw = p_new;
+    ep.alpha = sys->alpha;
+    ep.inv_h2 = 1.0 / (sys->spacing * sys->spacing);
+  }
+  ep.dot_with = p_new;
+  ep.partial = partial;
+  ep.bc_l = sys->bc_l;
+  if (fin_done) *fin_done = false;
+  if (fin && partial) {
+    ep.fin = *fin;
+    if (fin_done) *fin_done = true;
+  }
+  TVD_LAUNCH(c, kCatBandRows, 1,
+             launch_band_mma_rows_fused(b->g[1], p_old, tmp, skip, c->stream, z, p_new, S));
+  TVD_LAUNCH(c, kCatBandCols, 1, launch_band_cols(b->g[0], tmp, q, ep, skip, c->stream));
+  if (nb_out) *nb_out = band_cols_grid(b->g[0]);
+  return TVD_OK;
+}
+
 // ================================================================== ABI
 extern "C" {
 
@@ -1774,28 +1815,40 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   const PcgFin fin_g{S, c->d_fin, kFinGamma, 0, 0.0, nullptr};
   const PcgFin fin_r{S, c->d_fin + 1, kFinRel, 0, tol, history};
   const PcgFin fin_b{S, c->d_fin + 2, kFinBeta, max_iterations, 0.0, nullptr};
+  // direction update fused into the next iteration's row band pass, p ping-ponging between
+  // two buffers (the pass reads p_old halos of its neighbours while writing p_new)
+  const bool pfuse = pcg_p_fusable(sys);
+  double* pb[2] = {p, nullptr};
+  if (pfuse) TVD_SLOT(c, kSlotP2, N, pb[1]);
+  int it = 0;
   int chunk = 4;
   for (int done_it = 0;;) {
-    for (int k = 0; k < chunk; ++k) {
+    for (int k = 0; k < chunk; ++k, ++it) {
       // the three scalar steps run in the last CTA of the kernel producing their partials
       // where that kernel supports it (tvd_cg.h pcg_fin_tail), else as 1-CTA launches
       bool fused;
-      rc = system_apply_internal(c, sys, p, q, p, partial, skip, &nb, fuse_fin ? &fin_g : nullptr,
-                                 &fused);
+      double* pc = pfuse ? pb[it & 1] : p;
+      if (pfuse && it > 0) {
+        rc = system_apply_pfused(c, sys, zz, pb[(it - 1) & 1], pc, q, partial, S, skip, &nb,
+                                 fuse_fin ? &fin_g : nullptr, &fused);
+      } else {
+        rc = system_apply_internal(c, sys, pc, q, pc, partial, skip, &nb,
+                                   fuse_fin ? &fin_g : nullptr, &fused);
+      }
       if (rc) return rc;
       if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_gamma(S, partial, nb, st));
       if (fuse_fin) {
-        TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, p, q, N, partial, vec_blocks(), st,
+        TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, pc, q, N, partial, vec_blocks(), st,
                                                        &fin_r));
       } else {
-        TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, p, q, N, partial, vec_blocks(), st));
+        TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, pc, q, N, partial, vec_blocks(), st));
         TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
       }
       rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb, inv_t,
                          fuse_fin ? &fin_b : nullptr, &fused);
       if (rc) return rc;
       if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_beta(S, partial, nb, max_iterations, st));
-      TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_p(S, p, zz, N, st));
+      if (!pfuse) TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_p(S, p, zz, N, st));
     }
     done_it += chunk;
     TVD_CUDA(cudaMemcpyAsync(c->h_state, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));

@@ -74,6 +74,12 @@ cudaError_t launch_band_mma_rows(const BandOp& op, const double* in, double* out
 cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out,
                                  const Epilogue& ep, const int* skip, cudaStream_t st,
                                  int row_lo = 0, int row_hi = -1);
+// row pass fused with the PCG direction update: p_new = z + beta p_old (in = p_old), out = p_new
+// G^T; z == nullptr is the plain pass
+cudaError_t launch_band_mma_rows_fused(const BandOp& op, const double* in, double* out,
+                                       const int* skip, cudaStream_t st, const double* z,
+                                       double* p_new, const PcgState* pst, int row_lo = 0,
+                                       int row_hi = -1);
 
 int band_rows_blocks(int n);
 int band_cols_blocks(int n);          // upper bound over both column-pass variants
