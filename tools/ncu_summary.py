@@ -85,7 +85,15 @@ def main() -> None:
     traffic = {}
     for cat, kern in CATEGORY_KERNEL.items():
         for rep_name, entries in reps:
-            hit = next((e for e in entries if kern in e["kernel"] and "dram_bytes" in e), None)
+            cand = [e for e in entries if kern in e["kernel"] and "dram_bytes" in e]
+            # the column (sandwich) DST pass is the longest pipeline launch of a capture
+            if cat == "trig_cols" and cand:
+                cand = [max(cand, key=lambda e: float(e.get("gpu__time_duration.sum", "0")
+                                                       .replace(",", "")))]
+            elif cat == "trig_rows" and cand:
+                cand = [min(cand, key=lambda e: float(e.get("gpu__time_duration.sum", "0")
+                                                       .replace(",", "")))]
+            hit = cand[0] if cand else None
             if hit:
                 traffic[cat] = {"kernel": hit["kernel"].split("(")[0], "dram_bytes": hit["dram_bytes"],
                                 "source": f"{rd.name}/{rep_name} (ncu --set full)"}
