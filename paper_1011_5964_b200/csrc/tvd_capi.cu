@@ -93,6 +93,11 @@ struct tvd_ctx {
   bool profiling = false;      // record CUDA events around every launch
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> ev_marks;  // (category, first event index)
+  // captured PCG iterations (tvd_pcg_solve graph replay) and the operands they were built for
+  cudaGraphExec_t pcg_graph = nullptr;
+  cudaStream_t cap_stream = nullptr;  // private stream for graph capture
+  std::vector<uintptr_t> pcg_graph_key;
+  long long pcg_graph_launches = 0;
 };
 
 // kernel categories for the per-launch timer (tvd_profile_category)
@@ -1179,6 +1184,8 @@ int tvd_ctx_destroy(tvd_ctx* c) {
   cudaFreeHost(c->h_scalar);
   cudaFree(c->d_scalar);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->pcg_graph) cudaGraphExecDestroy(c->pcg_graph);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
   return TVD_OK;
 }
@@ -1820,41 +1827,138 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   const bool pfuse = pcg_p_fusable(sys);
   double* pb[2] = {p, nullptr};
   if (pfuse) TVD_SLOT(c, kSlotP2, N, pb[1]);
-  int it = 0;
-  int chunk = 4;
-  for (int done_it = 0;;) {
-    for (int k = 0; k < chunk; ++k, ++it) {
-      // the three scalar steps run in the last CTA of the kernel producing their partials
-      // where that kernel supports it (tvd_cg.h pcg_fin_tail), else as 1-CTA launches
-      bool fused;
-      double* pc = pfuse ? pb[it & 1] : p;
-      if (pfuse && it > 0) {
-        rc = system_apply_pfused(c, sys, zz, pb[(it - 1) & 1], pc, q, partial, S, skip, &nb,
-                                 fuse_fin ? &fin_g : nullptr, &fused);
-      } else {
-        rc = system_apply_internal(c, sys, pc, q, pc, partial, skip, &nb,
-                                   fuse_fin ? &fin_g : nullptr, &fused);
-      }
-      if (rc) return rc;
-      if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_gamma(S, partial, nb, st));
-      if (fuse_fin) {
-        TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, pc, q, N, partial, vec_blocks(), st,
-                                                       &fin_r));
-      } else {
-        TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, pc, q, N, partial, vec_blocks(), st));
-        TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
-      }
-      rc = minv_internal(c, pre, n, r, zz, partial, skip, &nb, inv_t,
-                         fuse_fin ? &fin_b : nullptr, &fused);
-      if (rc) return rc;
-      if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_beta(S, partial, nb, max_iterations, st));
-      if (!pfuse) TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_p(S, p, zz, N, st));
+  // one PCG iteration (krylov.py:99-116) enqueued on the stream; every kernel skips once the
+  // device state is done, so iterations can be enqueued ahead of the host's checks
+  auto enqueue_iter = [&](int it) -> int {
+    // the three scalar steps run in the last CTA of the kernel producing their partials
+    // where that kernel supports it (tvd_cg.h pcg_fin_tail), else as 1-CTA launches
+    bool fused;
+    int nbl;
+    double* pc = pfuse ? pb[it & 1] : p;
+    int rc2;
+    if (pfuse && it > 0) {
+      rc2 = system_apply_pfused(c, sys, zz, pb[(it - 1) & 1], pc, q, partial, S, skip, &nbl,
+                                fuse_fin ? &fin_g : nullptr, &fused);
+    } else {
+      rc2 = system_apply_internal(c, sys, pc, q, pc, partial, skip, &nbl,
+                                  fuse_fin ? &fin_g : nullptr, &fused);
     }
-    done_it += chunk;
+    if (rc2) return rc2;
+    if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_gamma(S, partial, nbl, st));
+    if (fuse_fin) {
+      TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, pc, q, N, partial, vec_blocks(), st,
+                                                     &fin_r));
+    } else {
+      TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, pc, q, N, partial, vec_blocks(), st));
+      TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
+    }
+    rc2 = minv_internal(c, pre, n, r, zz, partial, skip, &nbl, inv_t,
+                        fuse_fin ? &fin_b : nullptr, &fused);
+    if (rc2) return rc2;
+    if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_beta(S, partial, nbl, max_iterations, st));
+    if (!pfuse) TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_p(S, p, zz, N, st));
+    return TVD_OK;
+  };
+  auto check_done = [&](bool* done) -> int {
     TVD_CUDA(cudaMemcpyAsync(c->h_state, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
     TVD_CUDA(cudaStreamSynchronize(st));
-    if (c->h_state->done) break;
-    if (chunk < 16) chunk *= 2;
+    *done = c->h_state->done != 0;
+    return TVD_OK;
+  };
+  // CUDA-graph replay (TVD_PCG_GRAPH, default on): iteration 0 runs eagerly, then a graph of
+  // kGraphIters iterations (an even count, so the p ping-pong parity repeats) is captured once
+  // per operand set and replayed -- the launch gaps between the ~5 kernels of an iteration
+  // shrink to the graph's.  Profiling runs (per-launch events) stay eager.
+  static const bool graph_on = [] {
+    const char* e = getenv("TVD_PCG_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  constexpr int kGraphIters = 4;
+  bool done = false;
+  if (graph_on && !c->profiling) {
+    rc = enqueue_iter(0);
+    if (rc) return rc;
+    const void* key[] = {sys->blur, sys->a_h, sys->a_v, sys->s, pre, pre ? pre->inv_eig : nullptr,
+                         pre ? pre->d : nullptr, x, r, zz, pb[0], pb[1], q, partial, inv_t,
+                         history, S};
+    std::vector<uintptr_t> k2;
+    for (const void* v : key) k2.push_back(reinterpret_cast<uintptr_t>(v));
+    k2.push_back((uintptr_t)max_iterations);
+    uint64_t tolbits;
+    memcpy(&tolbits, &tol, sizeof(tol));
+    k2.push_back((uintptr_t)tolbits);
+    k2.push_back((uintptr_t)(pre ? pre->kind * 16 + pre->family : -1));
+    k2.push_back((uintptr_t)(sys->alpha * 1e12));
+    for (const DevBuf& sl : c->slots) k2.push_back(reinterpret_cast<uintptr_t>(sl.ptr));
+    k2.push_back((uintptr_t)c->force_generic);
+    if (!c->pcg_graph || c->pcg_graph_key != k2) {
+      const long long l0 = c->launches;
+      // capture on a private stream (the legacy default stream cannot capture); the
+      // graph is launched on the context stream
+      if (!c->cap_stream) TVD_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+      cudaStream_t saved = c->stream;
+      c->stream = c->cap_stream;
+      st = c->cap_stream;
+      TVD_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      int rcc = TVD_OK;
+      for (int i = 1; i <= kGraphIters && !rcc; ++i) rcc = enqueue_iter(i);
+      cudaGraph_t gph = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(st, &gph);
+      c->stream = saved;
+      st = saved;
+      if (rcc) {
+        if (gph) cudaGraphDestroy(gph);
+        return rcc;
+      }
+      if (ec != cudaSuccess) return fail(TVD_ERR_CUDA, "pcg graph capture failed");
+      // same topology with new operands (the next FP step's diffusivities, eigenvalues,
+      // buffers): update the executable graph in place instead of instantiating again
+      bool updated = false;
+      if (c->pcg_graph) {
+        cudaGraphExecUpdateResultInfo info;
+        updated = cudaGraphExecUpdate(c->pcg_graph, gph, &info) == cudaSuccess;
+        if (!updated) {
+          cudaGetLastError();
+          cudaGraphExecDestroy(c->pcg_graph);
+          c->pcg_graph = nullptr;
+        }
+      }
+      if (!updated) {
+        const cudaError_t ei = cudaGraphInstantiate(&c->pcg_graph, gph, 0);
+        if (ei != cudaSuccess) {
+          cudaGraphDestroy(gph);
+          c->pcg_graph = nullptr;
+          return fail(TVD_ERR_CUDA, "pcg graph instantiation failed");
+        }
+      }
+      cudaGraphDestroy(gph);
+      c->pcg_graph_launches = c->launches - l0;
+      c->launches = l0;
+      c->pcg_graph_key = k2;
+    }
+    int reps = 1;  // graph replays between host checks: 4, 8, 16 iterations
+    for (int done_it = 1; !done && done_it <= max_iterations + kGraphIters;) {
+      for (int k = 0; k < reps; ++k) {
+        TVD_CUDA(cudaGraphLaunch(c->pcg_graph, st));
+        c->launches += c->pcg_graph_launches;
+      }
+      done_it += reps * kGraphIters;
+      rc = check_done(&done);
+      if (rc) return rc;
+      if (reps < 4) reps *= 2;
+    }
+  } else {
+    int it = 0;
+    int chunk = 4;
+    while (!done) {
+      for (int k = 0; k < chunk; ++k, ++it) {
+        rc = enqueue_iter(it);
+        if (rc) return rc;
+      }
+      rc = check_done(&done);
+      if (rc) return rc;
+      if (chunk < 16) chunk *= 2;
+    }
   }
   const PcgState& h = *c->h_state;
   if (iterations) *iterations = h.iters;
