@@ -85,6 +85,7 @@ struct RaderPlan {
   const unsigned* rout;  // k = 1..M: (M - dlog_g(k)) mod M, where C_k lands
   const double2* bh;     // FFT_M(b), b_q = exp(-2 pi i g^-q / L)
   const double2* tw;     // exp(-2 pi i e / M), e in [0, M)
+  const unsigned* dlg;   // m = 1..M: dlog_g(m), the Rader position of input m (plain DFT)
 };
 
 // Device-resident FFT plan plus the per-length twiddle tables of one family.

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Line passes of the trigonometric transforms (reference transforms.py:52-171,
 // precond.py:82-199 / 369-395 / 456-477).
 //
@@ -15,6 +16,7 @@
 // DCT-II / DCT-III use Makhoul's reordering with two real lines packed into
 // one complex FFT of length n.
 #include "tvd_internal.h"
+#include "tvd_rader.h"
 
 namespace tvd {
 
@@ -395,6 +397,10 @@ cudaError_t launch_trig(const TrigPlan& P, const LineGeom& g, int analysis, cons
 cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
                                 int* nblocks_out, cudaStream_t st) {
   (void)axis;
+  // prime odd core (config 5, L = 8191): the length-L DFTs run on the Rader engine instead of
+  // the generic engine's O(L) per point odd-radix stage (808 ms -> a few ms per assembly)
+  if (P.family != kFamDct && P.rader_ok && P.rader.L == P.L && !getenv("TVD_BAND_GENERIC"))
+    return launch_band_rader(P.rader, P.n, P.wfull, b, nblocks_out, st);
   BandK k{};
   k.fft = P.fft;
   k.wfull = P.wfull;

@@ -251,7 +251,120 @@ __global__ void __launch_bounds__(kRaderThreads, 1) k_rader_rows(const RaderK p)
   }
 }
 
+// Band projection of one line (sine family, k_band in tvd_lines.cu): the even slots carry b0,
+// the odd slots c1 b1, packed as one complex sequence c_j = (b0_j, c1 b1_j), j = 1..L-1
+// (c_0 = 0), whose length-L DFT the Rader convolution computes; the real FFT of length 2L is
+// recombined per output t with w_t = exp(-i pi t / L).  One line per CTA.
+struct BandRaderK {
+  RaderPlan pl;
+  int n, L;
+  const double2* wfull;
+  BandLines b;
+};
+
+template <int MC>
+__global__ void __launch_bounds__(kRaderThreads, 1) k_band_rader(const BandRaderK p) {
+  extern __shared__ __align__(16) double2 rbuf[];
+  __shared__ double red[32];
+  __shared__ double tots[2];
+  const int tid = threadIdx.x, nth = blockDim.x, n = p.n, L = p.L, line = blockIdx.x;
+  constexpr int M = MC;
+  const BandLines& b = p.b;
+  auto B0 = [&](int j) { return b.b0[(long)line * b.b0_ls + (long)j * b.b0_es]; };
+  auto B1 = [&](int j) { return b.b1[(long)line * b.b1_ls + (long)j * b.b1_es]; };
+  double t0 = 0.0, t1 = 0.0;
+  for (int m = 1 + tid; m <= M; m += nth) {
+    const double e = B0(m);  // m <= L - 1 = n - 2
+    const double o = (b.b1 && m <= L - 2) ? b.c1 * B1(m) : 0.0;
+    rbuf[__ldg(&p.pl.dlg[m - 1])] = make_double2(e, o);
+    t0 += e;
+    if (b.b1 && m <= L - 2) t1 += B1(m);
+  }
+  t0 = block_sum(t0, red);
+  if (tid == 0) tots[0] = t0;
+  t1 = block_sum(t1, red);
+  if (tid == 0) tots[1] = t1;
+  __syncthreads();
+  rader_convolve<MC>(rbuf, p.pl);
+  const double inv_m = 1.0 / M;
+  auto Ck = [&](int k) {  // forward DFT coefficient k = 1..M: conj(R) / M
+    const double2 R = rbuf[__ldg(&p.pl.rout[k - 1])];
+    return make_double2(R.x * inv_m, -R.y * inv_m);
+  };
+  double vmin = 1.0 / 0.0, vmax = -1.0 / 0.0;
+  const double T0 = tots[0], T1 = tots[1];
+  for (int t = tid; t < n; t += nth) {
+    double v;
+    if (t == 0 || t == n - 1) {
+      v = B0(t);
+    } else {
+      const double2 C = Ck(t), Cr = cconj(Ck(L - t));
+      const double2 E = cscale(cadd(C, Cr), 0.5);
+      const double2 D = csub(C, Cr);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      const double2 w = p.wfull[t];
+      const double re_s = E.x + (w.x * O.x - w.y * O.y);
+      v = (T0 + b.c1 * T1 * w.x - re_s) / L;
+    }
+    const long g = (long)line * b.out_ls + (long)t * b.out_es;
+    if (b.epi == 1) {
+      const double lh = b.lamh[g];
+      v = lh * lh + b.alpha * v;
+    } else if (b.epi == 2) {
+      const double lh = b.lamh[g], ld = b.lamd[g];
+      v = lh * lh * ld * ld + b.alpha * v;
+    }
+    b.out[g] = v;
+    vmin = fmin(vmin, v);
+    vmax = fmax(vmax, v);
+  }
+  if (b.epi != 0) {
+    for (int o = 16; o > 0; o >>= 1) {
+      vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+      vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    __syncthreads();
+    const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+    if (lane == 0) {
+      red[wid] = vmin;
+      red[16 + wid] = vmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = red[0], z = red[16];
+      for (int w = 1; w < nw; ++w) {
+        a = fmin(a, red[w]);
+        z = fmax(z, red[16 + w]);
+      }
+      b.partial_minmax[2 * blockIdx.x] = a;
+      b.partial_minmax[2 * blockIdx.x + 1] = z;
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_band_rader(const RaderPlan& P, int n, const double2* wfull, const BandLines& b,
+                              int* nblocks_out, cudaStream_t st) {
+  if (P.M != 8190 || n != P.L + 1 || !P.dlg) return cudaErrorInvalidConfiguration;
+  BandRaderK k{};
+  k.pl = P;
+  k.n = n;
+  k.L = P.L;
+  k.wfull = wfull;
+  k.b = b;
+  const size_t smem = (size_t)(P.M + RaderStages<8190>::kScratch) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_band_rader<8190>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  if (nblocks_out) *nblocks_out = b.nlines;
+  if (b.nlines == 0) return cudaSuccess;
+  k_band_rader<8190><<<b.nlines, kRaderThreads, smem, st>>>(k);
+  return cudaGetLastError();
+}
 
 bool rader_launchable(const RaderPlan& P, int len, int family) {
   return P.M == 8190 && (family == kFamSineHat ? len == P.M + 2 : len == P.M);
@@ -374,7 +487,8 @@ bool build_rader_plan(int L, RaderPlan* P, std::vector<void*>& owned) {
     pw = pw * g % L;
   }
   const int h = (L - 1) / 2;
-  std::vector<unsigned> rin(M), rout(M);
+  std::vector<unsigned> rin(M), rout(M), dlg(M);
+  for (int m = 1; m <= M; ++m) dlg[m - 1] = (unsigned)dlog[m];
   for (int t = 1; t <= M; ++t) {
     int j = (t & 1) == 0 ? t / 2 : (t - 1) / 2 - h;
     if (j < 0) j += L;
@@ -408,7 +522,8 @@ bool build_rader_plan(int L, RaderPlan* P, std::vector<void*>& owned) {
     tw[k] = make_double2((double)cm[k], -(double)sm[k]);
   }
   if (!upload_vec(rin, &P->rin, owned) || !upload_vec(rout, &P->rout, owned) ||
-      !upload_vec(bh, &P->bh, owned) || !upload_vec(tw, &P->tw, owned))
+      !upload_vec(bh, &P->bh, owned) || !upload_vec(tw, &P->tw, owned) ||
+      !upload_vec(dlg, &P->dlg, owned))
     return false;
   return true;
 }

@@ -18,5 +18,9 @@ bool rader_launchable(const RaderPlan& P, int len, int family);
 cudaError_t launch_rader_rows(const RaderPlan& P, int family, int len, int nlines,
                               const LineIO& io, int* nblocks_out, cudaStream_t st);
 int rader_threads();
+// band projection (preconditioner assembly, k_band's math) of every line with the length-L DFT
+// computed by the Rader engine: one line per CTA; *nblocks_out = nlines (min / max partials)
+cudaError_t launch_band_rader(const RaderPlan& P, int n, const double2* wfull, const BandLines& b,
+                              int* nblocks_out, cudaStream_t st);
 
 }  // namespace tvd
