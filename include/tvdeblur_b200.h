@@ -191,6 +191,15 @@ int tvd_bicgstab_solve(tvd_ctx* ctx, const tvd_system* sys, const tvd_precond* p
                        int* err_iteration, double* err_value);
 
 /* ---- vector helpers for the generic callable path ---------------------- */
+/* valid 2D convolution of an extended T x T device array with a width x width HOST psf
+ * (harness.py:170-198, blur_and_observe's convolve2d(u_extended, h, 'valid')); out: device
+ * (T-width+1)^2.  Rank-1 PSFs (or caller factors f1 (axis 0), f2 (axis 1), host, both
+ * non-NULL) run as two 1D passes, bit-identical to the separable shifted-slice sums
+ * sum_b f2[w-1-b] ext[:, b:] then sum_a f1[w-1-a] rows[a:, :]; others as a direct 2D
+ * convolution.  Synchronises. */
+int tvd_valid_convolve(tvd_ctx* ctx, const double* ext, int T, const double* psf, int width,
+                       const double* f1, const double* f2, double* out);
+
 /* ---- row-slab decomposition of one large problem over nranks ranks (config 5).
  * Rank `rank` owns the global rows [rank R, rank R + R), R = n / nranks.  The library runs the
  * kernels of each phase on the context stream; the caller runs the collectives between the

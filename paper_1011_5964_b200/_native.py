@@ -80,6 +80,7 @@ _SIGNATURES = {
     "tvd_bicgstab_solve": ([_vp, ctypes.POINTER(TvdSystem), ctypes.POINTER(TvdPrecond), _vp, _vp,
                             _vp, _d, _i, _vp, ctypes.POINTER(_i), ctypes.POINTER(_i),
                             ctypes.POINTER(_i), ctypes.POINTER(_d)], _i),
+    "tvd_valid_convolve": ([_vp, _vp, _i, _vp, _i, _vp, _vp, _vp], _i),
     "tvd_slab_create": ([_vp, ctypes.POINTER(TvdSystem), ctypes.POINTER(TvdPrecond), _i, _i,
                          ctypes.POINTER(_vp)], _i),
     "tvd_slab_destroy": ([_vp], _i),

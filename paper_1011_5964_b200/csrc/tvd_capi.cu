@@ -63,6 +63,7 @@ enum Slot : int {
   kSlotBT,     // BiCGstab t
   kSlotPartial3,
   kSlotP2,     // second PCG direction buffer (fused direction update)
+  kSlotPsf,    // PSF / factor vectors of tvd_valid_convolve
   kSlotCount
 };
 
@@ -1967,6 +1968,60 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   if (err_value) *err_value = h.err_val;
   if (h.status == kErrDiverged) return fail(TVD_ERR_DIVERGED, "pcg produced non-finite values");
   if (h.status == kErrIndefinite) return fail(TVD_ERR_INDEFINITE, "pcg met nonpositive curvature");
+  return TVD_OK;
+}
+
+// ------------------------------------------------------ observation pipeline
+// Valid convolution of an extended T x T array (harness.py:170-198 blur_and_observe's
+// convolve2d(..., 'valid')): rank-1 PSFs (outer(g1, g2) / sum within 1e-14, the harness's
+// _separable_factors test) as two 1D passes bit-identical to the harness's shifted-slice sums,
+// others as a direct 2D convolution.
+int tvd_valid_convolve(tvd_ctx* c, const double* ext, int T, const double* psf, int width,
+                       const double* f1, const double* f2, double* out) {
+  if (!c || !ext || !psf || !out) return fail(TVD_ERR_INVALID, "null argument");
+  if (width < 1 || width % 2 == 0 || width > T) return fail(TVD_ERR_INVALID, "bad psf width");
+  DeviceGuard g(c->device);
+  const int K = width, n = T - K + 1;
+  std::vector<double> g1(K, 0.0), g2(K, 0.0);
+  double total = 0.0, hmax = 0.0;
+  for (int a = 0; a < K; ++a)
+    for (int b = 0; b < K; ++b) {
+      const double v = psf[a * K + b];
+      g1[a] += v;
+      g2[b] += v;
+      hmax = std::max(hmax, std::fabs(v));
+    }
+  for (int a = 0; a < K; ++a) total += g1[a];
+  bool sep = total != 0.0;
+  for (int a = 0; a < K && sep; ++a)
+    for (int b = 0; b < K && sep; ++b)
+      if (std::fabs(g1[a] * g2[b] / total - psf[a * K + b]) > 1e-14 * hmax) sep = false;
+  double* dps;
+  TVD_SLOT(c, kSlotPsf, (size_t)K * K + 2 * K, dps);
+  if (f1 && f2) {  // the caller's factors (the harness's own, for bit-identical fixtures)
+    sep = true;
+    g1.assign(f1, f1 + K);
+    g2.assign(f2, f2 + K);
+  } else if (sep) {
+    for (int a = 0; a < K; ++a) g1[a] /= total;
+  }
+  if (sep) {
+    std::vector<double> fac(g1);
+    fac.insert(fac.end(), g2.begin(), g2.end());
+    TVD_CUDA(cudaMemcpyAsync(dps, fac.data(), fac.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             c->stream));
+    double* rows;
+    TVD_SLOT(c, kSlotExtA, (size_t)T * n, rows);
+    TVD_LAUNCH(c, kCatGeneral, 2, launch_valid_convolve(ext, T, K, dps, dps + K, nullptr, rows,
+                                                        out, c->stream));
+  } else {
+    TVD_CUDA(cudaMemcpyAsync(dps, psf, (size_t)K * K * sizeof(double), cudaMemcpyHostToDevice,
+                             c->stream));
+    TVD_LAUNCH(c, kCatGeneral, 1, launch_valid_convolve(ext, T, K, nullptr, nullptr, dps, nullptr,
+                                                        out, c->stream));
+  }
+  // the host PSF buffers must outlive the copies
+  TVD_CUDA(cudaStreamSynchronize(c->stream));
   return TVD_OK;
 }
 

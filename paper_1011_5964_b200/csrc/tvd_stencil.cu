@@ -660,6 +660,51 @@ __global__ void k_conv_valid(const double* __restrict__ ext, int n, int m,
   }
 }
 
+// Separable valid convolution of an extended T x T array (observation pipeline at scale,
+// harness.py:170-198 / paper_1011_5964_b200.harness.valid_convolve): pass 1 along axis 1,
+// rows[r][j] = sum_b g2[K-1-b] ext[r][j+b]; pass 2 along axis 0, out[i][j] = sum_a
+// g1[K-1-a] rows[i+a][j] -- the harness's shifted-slice sums in the same order and with the
+// same two roundings per term (no FMA contraction), so the results are bit-identical.
+__global__ void k_valid_rows(const double* __restrict__ ext, int T, int K,
+                             const double* __restrict__ g2, double* __restrict__ rows) {
+  const int n = T - K + 1;
+  const long N = (long)T * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(g / n), j = (int)(g % n);
+    const double* er = ext + (long)r * T + j;
+    double acc = 0.0;
+    for (int b = 0; b < K; ++b) acc = __dadd_rn(acc, __dmul_rn(__ldg(&g2[K - 1 - b]), er[b]));
+    rows[g] = acc;
+  }
+}
+__global__ void k_valid_cols(const double* __restrict__ rows, int T, int K,
+                             const double* __restrict__ g1, double* __restrict__ out) {
+  const int n = T - K + 1;
+  const long N = (long)n * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(g / n), j = (int)(g % n);
+    double acc = 0.0;
+    for (int a = 0; a < K; ++a)
+      acc = __dadd_rn(acc, __dmul_rn(__ldg(&g1[K - 1 - a]), rows[(long)(i + a) * n + j]));
+    out[g] = acc;
+  }
+}
+
+cudaError_t launch_valid_convolve(const double* ext, int T, int K, const double* g1,
+                                  const double* g2, const double* h, double* scratch,
+                                  double* out, cudaStream_t st) {
+  const int n = T - K + 1;
+  if (h) {  // general PSF: direct 2D valid convolution
+    k_conv_valid<<<grid_for((long)n * n, 256), 256, 0, st>>>(ext, n, (K - 1) / 2, h, out);
+    return cudaGetLastError();
+  }
+  k_valid_rows<<<grid_for((long)T * n, 256), 256, 0, st>>>(ext, T, K, g2, scratch);
+  k_valid_cols<<<grid_for((long)n * n, 256), 256, 0, st>>>(scratch, T, K, g1, out);
+  return cudaGetLastError();
+}
+
 // full convolution: full[r][c] = sum_ab h[a][b] y[r-a][c-b]
 __global__ void k_conv_full(const double* __restrict__ y, int n, int m,
                             const double* __restrict__ h, double* __restrict__ full) {

@@ -99,6 +99,11 @@ cudaError_t launch_diffusion_bands(const double* a_h, const double* a_v, int n, 
 cudaError_t launch_general_blur(const double* in, double* out, int n, int m, int bc,
                                 const double* h, int transpose, double* scratch_a,
                                 double* scratch_b, cudaStream_t st);
+// valid convolution of an extended T x T array with a K x K PSF: separable (h == nullptr:
+// factors g1 along axis 0, g2 along axis 1, scratch T x (T-K+1)) or direct 2D (h)
+cudaError_t launch_valid_convolve(const double* ext, int T, int K, const double* g1,
+                                  const double* g2, const double* h, double* scratch,
+                                  double* out, cudaStream_t st);
 cudaError_t launch_normal_epilogue(const double* base, const Epilogue& ep, int n, double* out,
                                    const int* skip, int nblocks, cudaStream_t st);
 cudaError_t launch_eigenvalues(const double* cos_tab, const double* h, int n, int K, double* tmp,

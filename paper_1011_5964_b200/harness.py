@@ -77,20 +77,32 @@ def _separable_factors(h: np.ndarray):
     return None
 
 
-def _valid_convolve_device(ext: np.ndarray, g1: np.ndarray, g2: np.ndarray, device):
-    """The separable shifted-slice sum of :func:`valid_convolve` (same operation order) on a
-    torch device -- data generation for the 8192^2 config, not part of the solver."""
+def _valid_convolve_device(ext: np.ndarray, h: np.ndarray, factors, device):
+    """The valid convolution on a CUDA device through the library (``tvd_valid_convolve``):
+    with ``factors`` (the separable pair of :func:`_separable_factors`) it runs the same
+    shifted-slice sums in the same order and rounding as the host path below (bit-identical);
+    otherwise a direct 2D convolution."""
+    import ctypes
+
     import torch
 
-    k = len(g1)
+    from . import _native as nat
+
+    dev = torch.device(device)
+    e = torch.from_numpy(np.ascontiguousarray(ext, dtype=float)).to(dev)
+    k = h.shape[0]
     n = ext.shape[0] - k + 1
-    e = torch.from_numpy(np.ascontiguousarray(ext)).to(device)
-    rows = torch.zeros((ext.shape[0], n), dtype=torch.float64, device=device)
-    for b in range(k):
-        rows += float(g2[k - 1 - b]) * e[:, b:b + n]
-    out = torch.zeros((n, n), dtype=torch.float64, device=device)
-    for a in range(k):
-        out += float(g1[k - 1 - a]) * rows[a:a + n, :]
+    out = torch.empty((n, n), dtype=torch.float64, device=dev)
+    hc = np.ascontiguousarray(h, dtype=float)
+    f1 = f2 = None
+    if factors is not None:
+        f1 = np.ascontiguousarray(factors[0], dtype=float)
+        f2 = np.ascontiguousarray(factors[1], dtype=float)
+    ctx = nat.context(dev)
+    nat.check(nat.load().tvd_valid_convolve(
+        ctx, e.data_ptr(), ext.shape[0], hc.ctypes.data, k,
+        None if f1 is None else f1.ctypes.data, None if f2 is None else f2.ctypes.data,
+        out.data_ptr()))
     return out.cpu().numpy()
 
 
@@ -112,8 +124,8 @@ def valid_convolve(ext: np.ndarray, h: np.ndarray, exact: bool = True,
     k = h.shape[0]
     n = ext.shape[0] - k + 1
     sep = _separable_factors(h)
-    if sep is not None and device is not None:
-        return _valid_convolve_device(ext, sep[0], sep[1], device)
+    if device is not None:
+        return _valid_convolve_device(ext, h, sep, device)
     if sep is not None:
         g1, g2 = sep
         rows = np.zeros((ext.shape[0], n))

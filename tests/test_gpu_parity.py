@@ -586,3 +586,36 @@ def test_prime_core_assembly_rader_matches_generic_8192():
 def O_gauss(m, sigma):
     from paper_1011_5964_b200.harness import gen_psf
     return gen_psf("gaussian", m, sigma)
+
+
+# ------------------------------------------------- observation pipeline
+def test_valid_convolve_device_matches_host(rng):
+    """tvd_valid_convolve: separable PSFs bit-identical to the harness's shifted-slice sums;
+    a non-separable PSF (direct 2D path) within rounding of scipy's convolve2d (the routine
+    the reference's blur_and_observe calls, harness.py:186)."""
+    from scipy.signal import convolve2d
+    from paper_1011_5964_b200.harness import gen_psf, valid_convolve
+    ext = rng.uniform(size=(300, 300))
+    for h in (gen_psf("gaussian", 10, 3.0), gen_psf("box", 5)):
+        dev = valid_convolve(ext, h, exact=False, device="cuda")
+        host = valid_convolve(ext, h, exact=False)
+        assert np.array_equal(dev, host)
+        assert rel_err(dev, convolve2d(ext, h, mode="valid")) < 1e-14
+    h = rng.uniform(size=(9, 9))
+    h = (h + h[::-1, ::-1]) / 2  # symmetric, not rank 1
+    dev = valid_convolve(ext, h, exact=False, device="cuda")
+    assert rel_err(dev, convolve2d(ext, h, mode="valid")) < 1e-13
+
+
+def test_observation_at_config5_scale_on_device():
+    """8192^2 observation (config 5: 63 x 63 Gaussian over the 8254^2 extended truth) on the
+    GPU: spot rows against the host shifted-slice sums."""
+    from paper_1011_5964_b200.harness import gen_psf, valid_convolve
+    g = np.random.default_rng(1)
+    ext = g.uniform(size=(8254, 8254))
+    h = gen_psf("gaussian", 31, 8.0)
+    dev = valid_convolve(ext, h, exact=False, device="cuda")
+    assert dev.shape == (8192, 8192)
+    for r0, c0 in ((0, 0), (4000, 7000), (8064, 8064)):  # 128 x 128 blocks need 190 x 190
+        host = valid_convolve(ext[r0:r0 + 190, c0:c0 + 190], h, exact=False)
+        assert np.array_equal(dev[r0:r0 + 128, c0:c0 + 128], host)
