@@ -619,3 +619,30 @@ def test_observation_at_config5_scale_on_device():
     for r0, c0 in ((0, 0), (4000, 7000), (8064, 8064)):  # 128 x 128 blocks need 190 x 190
         host = valid_convolve(ext[r0:r0 + 190, c0:c0 + 190], h, exact=False)
         assert np.array_equal(dev[r0:r0 + 128, c0:c0 + 128], host)
+
+
+# ------------------------------------------------------------ sweeps
+def test_sweep_matches_reference_files(tmp_path):
+    """The reference's own 2D sweep (tests/golden/make_sweep_golden.py: R / AR+Sine+ZN /
+    AR+Reblur+ZN x alpha 1e-3, 1e-2 x preconditioners x, d_x at n = 48) against the same
+    spec on the device path: identical cells, FP step counts and file set; average inner
+    counts within one iteration, RRE within 1e-8, restored PGM bytes within one grey level."""
+    import pathlib
+    from paper_1011_5964_b200 import sweep as SW
+    ref = pathlib.Path(__file__).resolve().parent / "golden" / "sweep_ref"
+    spec = SW.BenchmarkSpec(ns=(48,), alphas=(1e-3, 1e-2), betas=(0.1,),
+                            configurations=("R", "AR+Sine+ZN", "AR+Reblur+ZN"),
+                            preconditioners=("x", "d_x"), fp_max=40)
+    res = SW.run_sweep(spec, out_dir=tmp_path)
+    assert sorted(p.name for p in res.files) == sorted(p.name for p in ref.iterdir())
+    hdr, rows = SW.read_csv(tmp_path / "iterations.csv")
+    rhdr, rrows = SW.read_csv(ref / "iterations.csv")
+    assert hdr == rhdr and len(rows) == len(rrows)
+    for a, b in zip(rows, rrows):
+        assert a[:5] == b[:5], (a, b)  # label, alpha, beta, n, fp_steps
+        assert abs(float(a[5]) - float(b[5])) <= 1.0, (a, b)
+        assert abs(float(a[6]) - float(b[6])) <= 1e-8 * float(b[6]), (a, b)
+    for f in ref.glob("*.pgm"):
+        mine, theirs = SW.read_pgm(tmp_path / f.name), SW.read_pgm(f)
+        assert mine.shape == theirs.shape
+        assert int(np.abs(mine.astype(int) - theirs.astype(int)).max()) <= 1, f.name
