@@ -703,9 +703,14 @@ __device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, uns
   return SH::d == 2 ? x : y;
 }
 
+// PM: pass mode known at compile time (bit 0: sandwich with mid, bit 1: transposed output),
+// -1: read both from the parameters.  The specialised instances carry only their pass's code
+// (smaller kernels, fewer live registers, no dead branches).
 template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF = false, int BL = kPipeLines,
-          bool CSM = false>
+          bool CSM = false, int PM = -1>
 __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
+  const bool has_mid = PM < 0 ? p.mid != nullptr : (PM & 1) != 0;
+  const bool trans = PM < 0 ? p.transposed != 0 : (PM & 2) != 0;
   using SH = PfaShape<Q1, Q2, Q3>;
   static_assert(!HALF || SH::d == 2, "half-line layout is for two-factor lengths");
   // HALF: half-line Good-Thomas layout (tvd_pfa_t.cuh HalfShape), signed scatter / gather
@@ -772,8 +777,8 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       }
       // the row streams read with plain loads later in this batch: pull them into L2 now
       if (p.pre) bulk_prefetch_l2(p.pre + r, (unsigned)(n * 8));
-      if (p.mid) bulk_prefetch_l2(p.mid + r, (unsigned)(n * 8));
-      if (!p.transposed) {
+      if (has_mid) bulk_prefetch_l2(p.mid + r, (unsigned)(n * 8));
+      if (!trans) {
         if (p.post) bulk_prefetch_l2(p.post + r, (unsigned)(n * 8));
         if (p.dot_with) bulk_prefetch_l2(p.dot_with + r, (unsigned)(n * 8));
       }
@@ -812,7 +817,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   };
   const long nl_out = p.nlines;
   auto oidx = [&](int line, int e) {
-    return p.transposed ? (long)e * nl_out + line : (long)line * n + e;
+    return trans ? (long)e * nl_out + line : (long)line * n + e;
   };
   double acc = 0.0;
   unsigned phase = 0;
@@ -903,7 +908,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       const int t = 1 + tid + k * NT;
       g[k] = (k < kTpt - 1 || t <= N) ? __ldg(gath + t - 1) : 0u;
     }
-    if (p.mid) {
+    if (has_mid) {
       double v[B][kTpt];
 #pragma unroll
       for (int l = 0; l < B; ++l) {
@@ -961,7 +966,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     PIPE_T(3);
     // unpack + store (transposed: line index fastest -> B-double column segments).
     // All global loads of a group are issued before its stores.
-    if (p.transposed) {
+    if (trans) {
       const int l = tid & (B - 1);
       constexpr int TS = NT / B;
       constexpr int JT = (N + TS - 1) / TS;
@@ -983,7 +988,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
           }
 #pragma unroll
           for (int j = 0; j < JG; ++j) y[j] = unpack(l, gg[j], t0 + (j0 + j) * TS);
-          if ((p.ar_mode & 2) && !p.mid) {  // T^-1 of the (only) transform
+          if ((p.ar_mode & 2) && !has_mid) {  // T^-1 of the (only) transform
 #pragma unroll
             for (int j = 0; j < JG; ++j) {
               const int t = t0 + (j0 + j) * TS;
@@ -1025,7 +1030,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
         double y[kTpt];
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) y[k] = unpack(l, g[k], 1 + tid + k * NT);
-        if ((p.ar_mode & 2) && !p.mid) {  // T^-1 of the (only) transform
+        if ((p.ar_mode & 2) && !has_mid) {  // T^-1 of the (only) transform
 #pragma unroll
           for (int k = 0; k < kTpt; ++k) {
             const int t = 1 + tid + k * NT;
@@ -1061,7 +1066,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     if (p.off && tid < 2 * nlv) {
       const int l = tid >> 1, e = (tid & 1) ? n - 1 : 0;
       double y = bord[l][tid & 1];
-      if (p.mid) y *= p.mid[(long)(line0 + l) * n + e];
+      if (has_mid) y *= p.mid[(long)(line0 + l) * n + e];
       const long g = oidx(line0 + l, e);
       if (p.post) y = p.post_mul ? y * p.post[g] : y / p.post[g];
       p.out[g] = y;
@@ -1079,7 +1084,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 }
 
 template <int Q1, int Q2, int Q3, int NT = 256, int MINB = 2, int TPW = 3, bool HALF = false,
-          int BL = kPipeLines, bool CSM = false>
+          int BL = kPipeLines, bool CSM = false, int PM = -1>
 static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   using SH = PfaShape<Q1, Q2, Q3>;
   int reps = PfaStageC<SH, 0>::Rcnt;
@@ -1093,12 +1098,29 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   if (HALF && !k.pl.hscat) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM>,
+    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM><<<grid, NT, smem, st>>>(k);
+  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM><<<grid, NT, smem, st>>>(k);
   return cudaGetLastError();
+}
+
+// the four pass-specialised instances of one launch shape
+template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF>
+static cudaError_t launch_pipe_pm(const PipeK& k, int grid, cudaStream_t st) {
+  static const bool generic = [] {  // TVD_PIPE_PM=0: one kernel for every pass (A/B runs)
+    const char* e = getenv("TVD_PIPE_PM");
+    return e && e[0] == '0';
+  }();
+  if (generic) return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF>(k, grid, st);
+  const int pm = (k.mid ? 1 : 0) | (k.transposed ? 2 : 0);
+  switch (pm) {
+    case 0: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 0>(k, grid, st);
+    case 1: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 1>(k, grid, st);
+    case 2: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 2>(k, grid, st);
+    default: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 3>(k, grid, st);
+  }
 }
 
 #include "tvd_pfa_ws.cuh"
@@ -1290,7 +1312,7 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
         case 19: return launch_pipe_t<89, 23, 1, 192, 3, 2, true>(k, grid, st);
         case 20: return launch_pipe_t<89, 23, 1, 192, 3, 1, true>(k, grid, st);
         default:
-          return pipe_half() ? launch_pipe_t<89, 23, 1, 192, 2, 1, true>(k, grid, st)
+          return pipe_half() ? launch_pipe_pm<89, 23, 1, 192, 2, 1, true>(k, grid, st)
                              : launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
       }
     case 2:
@@ -1308,10 +1330,10 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
         case 11: return launch_pipe_t<31, 11, 3, 160, 4, 2>(k, grid, st);
         case 0: return launch_pipe_t<31, 11, 3>(k, grid, st);
         // four 2-warp CTAs per SM: 99 us per M^-1 at 1024^2 vs 127 us for two 8-warp CTAs
-        default: return launch_pipe_t<31, 11, 3, 64, 4, 2>(k, grid, st);
+        default: return launch_pipe_pm<31, 11, 3, 64, 4, 2, false>(k, grid, st);
       }
     case 3:
-      return pipe_half() ? launch_pipe_t<73, 7, 1, 256, 2, 3, true>(k, grid, st)
+      return pipe_half() ? launch_pipe_pm<73, 7, 1, 256, 2, 3, true>(k, grid, st)
                          : launch_pipe_t<73, 7, 1>(k, grid, st);
     case 4: return launch_pipe_t<127, 1, 1>(k, grid, st);
     default: return cudaErrorInvalidConfiguration;
