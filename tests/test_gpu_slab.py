@@ -134,3 +134,30 @@ def test_slab_rejects_bad_geometry():
         SL.Slab(system, pre.apply_inverse, 3, 0)  # 512 not divisible by 3
     with pytest.raises(tvd._native.NativeError):
         SL.Slab(system, pre.apply_inverse, 64, 0)  # 8-row slabs: below the band halo
+
+
+def test_slab_pcg_over_nccl_single_rank():
+    """The TorchComm collectives on the library's device buffers through a real NCCL process
+    group (world size 1 on the one GPU of the test box: all-to-all and allgather run, the halo
+    plan is empty), against the single-GPU PCG."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        spec = CONFIGS["c2a"]
+        system, pre, rhs, v = _problem(512, spec.m, spec.sigma, spec.alpha, spec.beta)
+        cfg = tvd.KrylovConfig(tol=spec.tol, max_iterations=400)
+        ref = tvd.pcg(system, pre.apply_inverse, rhs, v, cfg)
+        (out,) = SL.slab_pcg([SL.Slab(system, pre.apply_inverse, 1, 0)], SL.TorchComm(),
+                             [rhs.contiguous()], [v.contiguous()], cfg)
+        assert out.converged and out.iterations == ref.iterations
+        assert rel_err(out.solution.cpu().numpy(), ref.solution.cpu().numpy()) < 1e-12
+    finally:
+        dist.destroy_process_group()
