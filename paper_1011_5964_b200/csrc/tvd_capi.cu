@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -95,10 +96,13 @@ struct tvd_ctx {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> ev_marks;  // (category, first event index)
   // captured PCG iterations (tvd_pcg_solve graph replay) and the operands they were built for
-  cudaGraphExec_t pcg_graph = nullptr;
+  struct GraphCache {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<uintptr_t> key;  // operand pointers / scalars / scratch slots baked in
+    long long launches = 0;      // kernels per replay
+  };
+  GraphCache pcg_graph, bicg_graph;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
-  std::vector<uintptr_t> pcg_graph_key;
-  long long pcg_graph_launches = 0;
 };
 
 // kernel categories for the per-launch timer (tvd_profile_category)
@@ -1041,6 +1045,69 @@ static int system_apply_internal(tvd_ctx* c, const tvd_system* sys, const double
   return TVD_OK;
 }
 
+// Solver-loop graphs.  `body` enqueues a fixed number of iterations on c->stream; when `key`
+// differs from the cached one it is captured on a private stream (the legacy default stream
+// cannot capture) and applied to the cached executable graph with cudaGraphExecUpdate (same
+// topology, new operands), else instantiated.  The graph is launched on the context stream.
+static int graph_prepare(tvd_ctx* c, tvd_ctx::GraphCache& g, const std::vector<uintptr_t>& key,
+                         const std::function<int()>& body) {
+  if (g.exec && g.key == key) return TVD_OK;
+  const long long l0 = c->launches;
+  if (!c->cap_stream) TVD_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t saved = c->stream;
+  c->stream = c->cap_stream;
+  TVD_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const int rcc = body();
+  cudaGraph_t gph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(c->stream, &gph);
+  c->stream = saved;
+  if (rcc) {
+    if (gph) cudaGraphDestroy(gph);
+    return rcc;
+  }
+  if (ec != cudaSuccess) return fail(TVD_ERR_CUDA, "solver graph capture failed");
+  bool updated = false;
+  if (g.exec) {
+    cudaGraphExecUpdateResultInfo info;
+    updated = cudaGraphExecUpdate(g.exec, gph, &info) == cudaSuccess;
+    if (!updated) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+  }
+  if (!updated && cudaGraphInstantiate(&g.exec, gph, 0) != cudaSuccess) {
+    cudaGraphDestroy(gph);
+    g.exec = nullptr;
+    return fail(TVD_ERR_CUDA, "solver graph instantiation failed");
+  }
+  cudaGraphDestroy(gph);
+  g.launches = c->launches - l0;
+  c->launches = l0;
+  g.key = key;
+  return TVD_OK;
+}
+static void key_push(std::vector<uintptr_t>& k, const void* p) {
+  k.push_back(reinterpret_cast<uintptr_t>(p));
+}
+static void key_push(std::vector<uintptr_t>& k, double v) {
+  uint64_t b;
+  memcpy(&b, &v, sizeof(v));
+  k.push_back((uintptr_t)b);
+}
+static void key_slots(std::vector<uintptr_t>& k, const tvd_ctx* c) {
+  for (const DevBuf& sl : c->slots) k.push_back(reinterpret_cast<uintptr_t>(sl.ptr));
+  k.push_back((uintptr_t)c->force_generic);
+}
+static bool graphs_enabled() {
+  static const bool on = [] {  // TVD_SOLVER_GRAPH=0 (or the older TVD_PCG_GRAPH=0): eager
+    const char* e = getenv("TVD_SOLVER_GRAPH");
+    const char* f = getenv("TVD_PCG_GRAPH");
+    return !((e && e[0] == '0') || (f && f[0] == '0'));
+  }();
+  return on;
+}
+
 // PCG iterations >= 2 with the direction update fused into the row band pass:
 // p_new = z + beta p_old, q = A p_new, partial of p_new . q (gamma folded into the column
 // pass when fin).  Separable X / D_X systems on the tensor-core passes only (pcg_p_fusable).
@@ -1185,7 +1252,8 @@ int tvd_ctx_destroy(tvd_ctx* c) {
   cudaFreeHost(c->h_scalar);
   cudaFree(c->d_scalar);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-  if (c->pcg_graph) cudaGraphExecDestroy(c->pcg_graph);
+  if (c->pcg_graph.exec) cudaGraphExecDestroy(c->pcg_graph.exec);
+  if (c->bicg_graph.exec) cudaGraphExecDestroy(c->bicg_graph.exec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
   return TVD_OK;
@@ -1719,38 +1787,90 @@ int tvd_bicgstab_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre
       inv_t = it;
     }
   }
-  int chunk = 4;
-  for (;;) {
-    for (int k = 0; k < chunk; ++k) {
-      TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(rs, r, N, pa, vec_blocks(), halt, st));
-      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_rho(S, pa, vec_blocks(), st));
-      TVD_LAUNCH(c, kCatVec, 1, launch_bicg_update_p(S, p, r, v, N, st));
-      rc = minv_internal(c, pre, n, p, ph, nullptr, halt, &nb, inv_t, nullptr, nullptr, false);
-      if (rc) return rc;
-      rc = system_apply_internal(c, sys, ph, v, rs, pa, halt, &nb);
-      if (rc) return rc;
-      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_alpha(S, pa, nb, st));
-      TVD_LAUNCH(c, kCatVec, 1, launch_bicg_s(S, sv, r, v, N, pb, st));
-      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_srel(S, pb, tol, st));
-      rc = minv_internal(c, pre, n, sv, sh, nullptr, halt, &nb, inv_t, nullptr, nullptr, false);
-      if (rc) return rc;
-      bool self_done = false;
-      rc = system_apply_internal(c, sys, sh, t, sv, pa, halt, &nb, nullptr, nullptr, pc,
-                                 &self_done);
-      if (rc) return rc;
-      int nb_tt = nb;
-      if (!self_done) {
-        TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(t, t, N, pc, vec_blocks(), halt, st));
-        nb_tt = vec_blocks();
-      }
-      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_omega(S, pa, nb, pc, nb_tt, st));
-      TVD_LAUNCH(c, kCatVec, 1, launch_bicg_update_xr(S, x, r, ph, sh, sv, t, N, pb, st));
-      TVD_LAUNCH(c, kCatFin, 1, launch_bicg_rel(S, pb, tol, history, max_iterations, st));
+  // one BiCGstab iteration (krylov.py:131-174); every kernel reads the state flags
+  auto enqueue_iter = [&]() -> int {
+    int nbl;
+    TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(rs, r, N, pa, vec_blocks(), halt, st));
+    TVD_LAUNCH(c, kCatFin, 1, launch_bicg_rho(S, pa, vec_blocks(), st));
+    TVD_LAUNCH(c, kCatVec, 1, launch_bicg_update_p(S, p, r, v, N, st));
+    int rc2 = minv_internal(c, pre, n, p, ph, nullptr, halt, &nbl, inv_t, nullptr, nullptr, false);
+    if (rc2) return rc2;
+    rc2 = system_apply_internal(c, sys, ph, v, rs, pa, halt, &nbl);
+    if (rc2) return rc2;
+    TVD_LAUNCH(c, kCatFin, 1, launch_bicg_alpha(S, pa, nbl, st));
+    TVD_LAUNCH(c, kCatVec, 1, launch_bicg_s(S, sv, r, v, N, pb, st));
+    TVD_LAUNCH(c, kCatFin, 1, launch_bicg_srel(S, pb, tol, st));
+    rc2 = minv_internal(c, pre, n, sv, sh, nullptr, halt, &nbl, inv_t, nullptr, nullptr, false);
+    if (rc2) return rc2;
+    bool self_done = false;
+    rc2 = system_apply_internal(c, sys, sh, t, sv, pa, halt, &nbl, nullptr, nullptr, pc,
+                                &self_done);
+    if (rc2) return rc2;
+    int nb_tt = nbl;
+    if (!self_done) {
+      TVD_LAUNCH(c, kCatVec, 1, launch_dot_partials(t, t, N, pc, vec_blocks(), halt, st));
+      nb_tt = vec_blocks();
     }
+    TVD_LAUNCH(c, kCatFin, 1, launch_bicg_omega(S, pa, nbl, pc, nb_tt, st));
+    TVD_LAUNCH(c, kCatVec, 1, launch_bicg_update_xr(S, x, r, ph, sh, sv, t, N, pb, st));
+    TVD_LAUNCH(c, kCatFin, 1, launch_bicg_rel(S, pb, tol, history, max_iterations, st));
+    return TVD_OK;
+  };
+  auto check_done = [&](bool* done) -> int {
     TVD_CUDA(cudaMemcpyAsync(c->h_bicg, S, sizeof(BicgState), cudaMemcpyDeviceToHost, st));
     TVD_CUDA(cudaStreamSynchronize(st));
-    if (c->h_bicg->done) break;
-    if (chunk < 16) chunk *= 2;
+    *done = c->h_bicg->done != 0;
+    return TVD_OK;
+  };
+  constexpr int kGraphIters = 4;
+  bool done = false;
+  if (graphs_enabled() && !c->profiling) {  // graph replay as in tvd_pcg_solve
+    std::vector<uintptr_t> key;
+    for (const void* vp : {(const void*)sys->blur, (const void*)sys->a_h, (const void*)sys->a_v,
+                           (const void*)sys->s, (const void*)(pre ? pre->inv_eig : nullptr),
+                           (const void*)(pre ? pre->d : nullptr), (const void*)x,
+                           (const void*)r, (const void*)rs, (const void*)p, (const void*)v,
+                           (const void*)ph, (const void*)sv, (const void*)sh, (const void*)t,
+                           (const void*)pa, (const void*)pb, (const void*)pc,
+                           (const void*)inv_t, (const void*)history, (const void*)S})
+      key_push(key, vp);
+    key_push(key, tol);
+    key_push(key, sys->alpha);
+    key_push(key, sys->spacing);
+    key.push_back((uintptr_t)max_iterations);
+    key.push_back((uintptr_t)(pre ? pre->kind * 16 + pre->family : 255));
+    key.push_back((uintptr_t)(sys->bc_l * 2 + sys->reblur));
+    key_slots(key, c);
+    rc = graph_prepare(c, c->bicg_graph, key, [&]() -> int {
+      st = c->stream;
+      int rc2 = TVD_OK;
+      for (int i = 0; i < kGraphIters && !rc2; ++i) rc2 = enqueue_iter();
+      return rc2;
+    });
+    st = c->stream;
+    if (rc) return rc;
+    int reps = 1;
+    for (int done_it = 0; !done && done_it <= max_iterations + kGraphIters;) {
+      for (int k = 0; k < reps; ++k) {
+        TVD_CUDA(cudaGraphLaunch(c->bicg_graph.exec, st));
+        c->launches += c->bicg_graph.launches;
+      }
+      done_it += reps * kGraphIters;
+      rc = check_done(&done);
+      if (rc) return rc;
+      if (reps < 4) reps *= 2;
+    }
+  } else {
+    int chunk = 4;
+    while (!done) {
+      for (int k = 0; k < chunk; ++k) {
+        rc = enqueue_iter();
+        if (rc) return rc;
+      }
+      rc = check_done(&done);
+      if (rc) return rc;
+      if (chunk < 16) chunk *= 2;
+    }
   }
   const BicgState& h = *c->h_bicg;
   if (iterations) *iterations = h.iters;
@@ -1870,78 +1990,39 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   // kGraphIters iterations (an even count, so the p ping-pong parity repeats) is captured once
   // per operand set and replayed -- the launch gaps between the ~5 kernels of an iteration
   // shrink to the graph's.  Profiling runs (per-launch events) stay eager.
-  static const bool graph_on = [] {
-    const char* e = getenv("TVD_PCG_GRAPH");
-    return !(e && e[0] == '0');
-  }();
   constexpr int kGraphIters = 4;
   bool done = false;
-  if (graph_on && !c->profiling) {
+  if (graphs_enabled() && !c->profiling) {
     rc = enqueue_iter(0);
     if (rc) return rc;
-    const void* key[] = {sys->blur, sys->a_h, sys->a_v, sys->s, pre, pre ? pre->inv_eig : nullptr,
-                         pre ? pre->d : nullptr, x, r, zz, pb[0], pb[1], q, partial, inv_t,
-                         history, S};
-    std::vector<uintptr_t> k2;
-    for (const void* v : key) k2.push_back(reinterpret_cast<uintptr_t>(v));
-    k2.push_back((uintptr_t)max_iterations);
-    uint64_t tolbits;
-    memcpy(&tolbits, &tol, sizeof(tol));
-    k2.push_back((uintptr_t)tolbits);
-    k2.push_back((uintptr_t)(pre ? pre->kind * 16 + pre->family : -1));
-    k2.push_back((uintptr_t)(sys->alpha * 1e12));
-    for (const DevBuf& sl : c->slots) k2.push_back(reinterpret_cast<uintptr_t>(sl.ptr));
-    k2.push_back((uintptr_t)c->force_generic);
-    if (!c->pcg_graph || c->pcg_graph_key != k2) {
-      const long long l0 = c->launches;
-      // capture on a private stream (the legacy default stream cannot capture); the
-      // graph is launched on the context stream
-      if (!c->cap_stream) TVD_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-      cudaStream_t saved = c->stream;
-      c->stream = c->cap_stream;
-      st = c->cap_stream;
-      TVD_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      int rcc = TVD_OK;
-      for (int i = 1; i <= kGraphIters && !rcc; ++i) rcc = enqueue_iter(i);
-      cudaGraph_t gph = nullptr;
-      const cudaError_t ec = cudaStreamEndCapture(st, &gph);
-      c->stream = saved;
-      st = saved;
-      if (rcc) {
-        if (gph) cudaGraphDestroy(gph);
-        return rcc;
-      }
-      if (ec != cudaSuccess) return fail(TVD_ERR_CUDA, "pcg graph capture failed");
-      // same topology with new operands (the next FP step's diffusivities, eigenvalues,
-      // buffers): update the executable graph in place instead of instantiating again
-      bool updated = false;
-      if (c->pcg_graph) {
-        cudaGraphExecUpdateResultInfo info;
-        updated = cudaGraphExecUpdate(c->pcg_graph, gph, &info) == cudaSuccess;
-        if (!updated) {
-          cudaGetLastError();
-          cudaGraphExecDestroy(c->pcg_graph);
-          c->pcg_graph = nullptr;
-        }
-      }
-      if (!updated) {
-        const cudaError_t ei = cudaGraphInstantiate(&c->pcg_graph, gph, 0);
-        if (ei != cudaSuccess) {
-          cudaGraphDestroy(gph);
-          c->pcg_graph = nullptr;
-          return fail(TVD_ERR_CUDA, "pcg graph instantiation failed");
-        }
-      }
-      cudaGraphDestroy(gph);
-      c->pcg_graph_launches = c->launches - l0;
-      c->launches = l0;
-      c->pcg_graph_key = k2;
-    }
+    std::vector<uintptr_t> key;
+    for (const void* v : {(const void*)sys->blur, (const void*)sys->a_h, (const void*)sys->a_v,
+                          (const void*)sys->s, (const void*)(pre ? pre->inv_eig : nullptr),
+                          (const void*)(pre ? pre->d : nullptr), (const void*)x,
+                          (const void*)r, (const void*)zz, (const void*)pb[0], (const void*)pb[1],
+                          (const void*)q, (const void*)partial, (const void*)inv_t,
+                          (const void*)history, (const void*)S})
+      key_push(key, v);
+    key_push(key, tol);
+    key_push(key, sys->alpha);
+    key_push(key, sys->spacing);
+    key.push_back((uintptr_t)max_iterations);
+    key.push_back((uintptr_t)(pre ? pre->kind * 16 + pre->family : 255));
+    key.push_back((uintptr_t)(sys->bc_l * 2 + sys->reblur));
+    key_slots(key, c);
+    rc = graph_prepare(c, c->pcg_graph, key, [&]() -> int {
+      st = c->stream;
+      int rc2 = TVD_OK;
+      for (int i = 1; i <= kGraphIters && !rc2; ++i) rc2 = enqueue_iter(i);
+      return rc2;
+    });
+    st = c->stream;
+    if (rc) return rc;
     int reps = 1;  // graph replays between host checks: 4, 8, 16 iterations
     for (int done_it = 1; !done && done_it <= max_iterations + kGraphIters;) {
       for (int k = 0; k < reps; ++k) {
-        TVD_CUDA(cudaGraphLaunch(c->pcg_graph, st));
-        c->launches += c->pcg_graph_launches;
+        TVD_CUDA(cudaGraphLaunch(c->pcg_graph.exec, st));
+        c->launches += c->pcg_graph.launches;
       }
       done_it += reps * kGraphIters;
       rc = check_done(&done);
