@@ -485,39 +485,50 @@ __device__ __forceinline__ double u_at(const double* u, int n, int r, int c, int
   return u[(long)r * n + c];
 }
 // dx[r][c] over the padded grid g (r in [0,n+2), c in [0,n+1)) = (g[r][c+1]-g[r][c]) / sp
+// (x / sp with sp == 1 is x exactly: the unit-spacing instance skips the divisions)
+template <bool UNIT = false>
 __device__ __forceinline__ double dxg(const double* u, int n, int r, int c, double sp, int bc) {
-  return __ddiv_rn(__dsub_rn(u_at(u, n, r - 1, c, bc), u_at(u, n, r - 1, c - 1, bc)), sp);
+  const double d = __dsub_rn(u_at(u, n, r - 1, c, bc), u_at(u, n, r - 1, c - 1, bc));
+  return UNIT ? d : __ddiv_rn(d, sp);
 }
 // dy[r][c] (r in [0,n+1), c in [0,n+2)) = (g[r+1][c]-g[r][c]) / sp
+template <bool UNIT = false>
 __device__ __forceinline__ double dyg(const double* u, int n, int r, int c, double sp, int bc) {
-  return __ddiv_rn(__dsub_rn(u_at(u, n, r, c - 1, bc), u_at(u, n, r - 1, c - 1, bc)), sp);
+  const double d = __dsub_rn(u_at(u, n, r, c - 1, bc), u_at(u, n, r - 1, c - 1, bc));
+  return UNIT ? d : __ddiv_rn(d, sp);
 }
 
+template <bool UNIT>
 __global__ void k_diffusivity(const double* __restrict__ u, int n, double beta, double sp,
                               double* __restrict__ a_h, double* __restrict__ a_v, int bc) {
   const double bb = __dmul_rn(beta, beta);
   const long nh = (long)n * (n + 1);
+  // 32-bit index arithmetic (the host launches this kernel for 2 n (n + 1) < 2^32 only):
+  // 64-bit integer division per edge dominated the kernel
+  const unsigned np1 = (unsigned)n + 1u, nu = (unsigned)n;
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < 2 * nh;
        e += (long)gridDim.x * blockDim.x) {
     if (e < nh) {  // horizontal edge (i, j), i in [0,n), j in [0,n]
-      const int i = (int)(e / (n + 1)), j = (int)(e % (n + 1));
-      const double d = dxg(u, n, i + 1, j, sp, bc);
-      double t = __dadd_rn(dyg(u, n, i, j, sp, bc), dyg(u, n, i + 1, j, sp, bc));
-      t = __dadd_rn(t, dyg(u, n, i, j + 1, sp, bc));
-      t = __dadd_rn(t, dyg(u, n, i + 1, j + 1, sp, bc));
+      const unsigned eu = (unsigned)e;
+      const int i = (int)(eu / np1), j = (int)(eu - (unsigned)i * np1);
+      const double d = dxg<UNIT>(u, n, i + 1, j, sp, bc);
+      double t = __dadd_rn(dyg<UNIT>(u, n, i, j, sp, bc), dyg<UNIT>(u, n, i + 1, j, sp, bc));
+      t = __dadd_rn(t, dyg<UNIT>(u, n, i, j + 1, sp, bc));
+      t = __dadd_rn(t, dyg<UNIT>(u, n, i + 1, j + 1, sp, bc));
       t = __dmul_rn(0.25, t);
       const double q = __dadd_rn(__dadd_rn(__dmul_rn(d, d), __dmul_rn(t, t)), bb);
       a_h[e] = __ddiv_rn(1.0, __dsqrt_rn(q));
     } else {       // vertical edge (i, j), i in [0,n], j in [0,n)
-      const long f = e - nh;
-      const int i = (int)(f / n), j = (int)(f % n);
-      const double d = dyg(u, n, i, j + 1, sp, bc);
-      double t = __dadd_rn(dxg(u, n, i, j, sp, bc), dxg(u, n, i, j + 1, sp, bc));
-      t = __dadd_rn(t, dxg(u, n, i + 1, j, sp, bc));
-      t = __dadd_rn(t, dxg(u, n, i + 1, j + 1, sp, bc));
+      const unsigned f = (unsigned)(e - nh);
+      const int i = (int)(f / nu), j = (int)(f - (unsigned)i * nu);
+      const double d = dyg<UNIT>(u, n, i, j + 1, sp, bc);
+      const long fo = (long)f;
+      double t = __dadd_rn(dxg<UNIT>(u, n, i, j, sp, bc), dxg<UNIT>(u, n, i, j + 1, sp, bc));
+      t = __dadd_rn(t, dxg<UNIT>(u, n, i + 1, j, sp, bc));
+      t = __dadd_rn(t, dxg<UNIT>(u, n, i + 1, j + 1, sp, bc));
       t = __dmul_rn(0.25, t);
       const double q = __dadd_rn(__dadd_rn(__dmul_rn(d, d), __dmul_rn(t, t)), bb);
-      a_v[f] = __ddiv_rn(1.0, __dsqrt_rn(q));
+      a_v[fo] = __ddiv_rn(1.0, __dsqrt_rn(q));
     }
   }
 }
@@ -543,7 +554,7 @@ __global__ void k_diffusion_bands(const double* __restrict__ a_h, const double* 
   const long N = (long)n * n;
   for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
        g += (long)gridDim.x * blockDim.x) {
-    const int i = (int)(g / n), j = (int)(g % n);
+    const int i = (int)((unsigned long long)g / (unsigned)n), j = (int)(g - (long)i * n);
     const long h0 = (long)i * (n + 1) + j;
     double d = __dadd_rn(__dadd_rn(__dadd_rn(a_h[h0], a_h[h0 + 1]), a_v[(long)i * n + j]),
                          a_v[(long)(i + 1) * n + j]);
@@ -582,7 +593,11 @@ static int grid_for(long work, int threads) {
 
 cudaError_t launch_diffusivity(const double* u, int n, double beta, double sp, double* a_h,
                                double* a_v, cudaStream_t st, int bc) {
-  k_diffusivity<<<grid_for(2L * n * (n + 1), 256), 256, 0, st>>>(u, n, beta, sp, a_h, a_v, bc);
+  if (2L * n * (n + 1) >= (1L << 32)) return cudaErrorInvalidValue;  // 32-bit edge indices
+  if (sp == 1.0)
+    k_diffusivity<true><<<grid_for(2L * n * (n + 1), 256), 256, 0, st>>>(u, n, beta, sp, a_h, a_v, bc);
+  else
+    k_diffusivity<false><<<grid_for(2L * n * (n + 1), 256), 256, 0, st>>>(u, n, beta, sp, a_h, a_v, bc);
   return cudaGetLastError();
 }
 cudaError_t launch_diffusion_apply(const double* a_h, const double* a_v, const double* w, int n,
