@@ -183,11 +183,11 @@ def alg_bytes_per_launch(cat: str, n: int) -> float:
     """Algorithmic bytes one launch of a kernel category must move."""
     px = float(n) * n
     return {
-        "band_rows": 16.0 * px,         # read p, write t
+        "band_rows": 32.0 * px,         # read z, p_old; write p_new, t (fused p = z + beta p)
         "band_cols": 40.0 * px,         # read t, p, a_h, a_v; write q  (+ p.q)
         "trig_cols": 24.0 * px,         # read t, inv_eig; write t'
         "trig_rows": 20.0 * px,         # avg of pass 1 (16 B/px) and pass 3 (24 B/px, reads r)
-        "vector": 36.0 * px,            # avg of x/r update (48) and p update (24)
+        "vector": 48.0 * px,            # x / r update (the p update is fused into band_rows)
     }.get(cat, 0.0)
 
 
