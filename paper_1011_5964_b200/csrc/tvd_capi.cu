@@ -734,6 +734,67 @@ static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const 
   return TVD_OK;
 }
 
+// The DCT family (R preconditioners) on the generic engine over contiguous rows only: row pass
+// written transposed, sandwich over the rows of the transpose (with the transposed inverse
+// eigenvalues) written transposed back, row pass with the dot and the beta finalizer --
+// instead of a strided column sandwich.
+static bool trig_trans_ok(tvd_ctx* c, int family) {
+  static const bool off = getenv("TVD_TRIG_STRIDED") != nullptr;
+  return family == kFamDct && !c->force_generic && !off;
+}
+static int precond_trig_trans(tvd_ctx* c, int family, int n, const double* inv,
+                              const double* inv_t, const double* d, int dmul, const double* in,
+                              double* out, const double* dot_with, const int* skip, int* nb_out,
+                              const PcgFin* fin, bool* fin_done) {
+  double *tT, *t2, *partial = nullptr;
+  TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tT);
+  TVD_SLOT(c, kSlotTmp3, (size_t)n * n, t2);
+  if (!inv_t) {
+    double* it;
+    TVD_SLOT(c, kSlotInvT, (size_t)n * n, it);
+    TVD_LAUNCH(c, kCatVec, 1, launch_transpose(inv, it, n, c->stream));
+    inv_t = it;
+  }
+  if (dot_with) {
+    int rc = partial_capacity(c, (size_t)n + 64, &partial);
+    if (rc) return rc;
+  }
+  int nb;
+  LineIO a{};
+  a.in = in;
+  a.out = tT;
+  a.pre = d;
+  a.pre_mul = dmul;
+  a.skip = skip;
+  a.out_trans = 1;
+  int rc = run_lines(c, family, rows_geom(n, n), 1, a, &nb);
+  if (rc) return rc;
+  LineIO b{};
+  b.in = tT;
+  b.out = t2;
+  b.mid_mul = inv_t;
+  b.skip = skip;
+  b.out_trans = 1;
+  rc = run_lines(c, family, rows_geom(n, n), 1, b, &nb);
+  if (rc) return rc;
+  LineIO z{};
+  z.in = t2;
+  z.out = out;
+  z.post = d;
+  z.post_mul = dmul;
+  z.dot_with = dot_with;
+  z.partial = partial;
+  z.skip = skip;
+  if (fin && partial) {
+    z.fin = *fin;
+    if (fin_done) *fin_done = true;
+  }
+  rc = run_lines(c, family, rows_geom(n, n), 0, z, &nb);
+  if (rc) return rc;
+  if (nb_out) *nb_out = nb;
+  return TVD_OK;
+}
+
 static int precond_transform(tvd_ctx* c, int family, int n, const double* inv, const double* d,
                              int dmul, const double* in, double* out, const double* dot_with,
                              const int* skip, int* nb_out, const double* inv_t = nullptr,
@@ -798,6 +859,9 @@ static int precond_transform(tvd_ctx* c, int family, int n, const double* inv, c
   if (rader_ok(c, family, n, &PP))
     return precond_rader(c, PP, family, n, inv, inv_t, d, dmul, in, out, dot_with, skip, nb_out,
                          fin, fin_done);
+  if (trig_trans_ok(c, family))
+    return precond_trig_trans(c, family, n, inv, inv_t, d, dmul, in, out, dot_with, skip, nb_out,
+                              fin, fin_done);
   double* tmp;
   TVD_SLOT(c, kSlotTmp2, (size_t)n * n, tmp);
   double* partial = nullptr;
@@ -1926,7 +1990,8 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   const double* inv_t = nullptr;
   if (pre && pre->kind == TVD_PRECOND_TRANSFORM) {
     const TrigPlan* PP;
-    if (pipe_ok(c, pre->family, n, &PP) || rader_ok(c, pre->family, n, &PP)) {
+    if (pipe_ok(c, pre->family, n, &PP) || rader_ok(c, pre->family, n, &PP) ||
+        trig_trans_ok(c, pre->family)) {
       double* it;
       TVD_SLOT(c, kSlotInvT, N, it);
       TVD_LAUNCH(c, kCatVec, 1, launch_transpose(pre->inv_eig, it, n, st));

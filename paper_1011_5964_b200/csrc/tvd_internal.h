@@ -128,6 +128,9 @@ struct LineIO {
   // layout an all-to-all of per-rank blocks leaves behind; 0 = row-major (l * len + e)
   int in_seg;
   long in_seg_stride;
+  // generic engine (k_trig): element t of line l is written to out[t * nlines + l] (the pass
+  // output transposed, so the next pass runs over contiguous rows); post / dot_with unused
+  int out_trans;
 };
 
 // Band projection of one batch of lines (preconditioner assembly).

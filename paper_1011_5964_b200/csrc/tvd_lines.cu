@@ -189,18 +189,26 @@ __global__ void __launch_bounds__(512) k_trig(const TrigK p) {
   }
 
   double acc = 0.0;
-  for (int i = tid; i < nlv * n; i += nth) {
-    int l, t;
-    lt(i, l, t);
-    const long g = gidx(l, t);
-    double v = real[l * p.P + t];
-    if (io.post) v = io.post_mul ? v * io.post[g] : v / io.post[g];
-    io.out[g] = v;
-    if (io.dot_with) acc += v * io.dot_with[g];
+  if (io.out_trans) {  // t-major: consecutive threads write the nlv adjacent lines of one t
+    for (int i = tid; i < nlv * n; i += nth) {
+      const int t = i / nlv, l = i - t * nlv;
+      io.out[(long)t * p.nlines + line0 + l] = real[l * p.P + t];
+    }
+  } else {
+    for (int i = tid; i < nlv * n; i += nth) {
+      int l, t;
+      lt(i, l, t);
+      const long g = gidx(l, t);
+      double v = real[l * p.P + t];
+      if (io.post) v = io.post_mul ? v * io.post[g] : v / io.post[g];
+      io.out[g] = v;
+      if (io.dot_with) acc += v * io.dot_with[g];
+    }
   }
   if (io.partial) {
     const double s = block_sum(acc, red);
     if (tid == 0) io.partial[blockIdx.x] = s;
+    if (io.fin.s) pcg_fin_tail(io.fin, io.partial, gridDim.x, red);
   }
 }
 
