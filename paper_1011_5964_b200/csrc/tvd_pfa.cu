@@ -1182,7 +1182,26 @@ static int pipe_variant2_id() {
   }();
   return v;
 }
+// TVD_PIPE_VARIANT3: launch shapes of the 511 = 73 * 7 pass (config 2a) for experiments
+static int pipe_variant3_id() {
+  static const int v = [] {
+    const char* s = getenv("TVD_PIPE_VARIANT3");
+    return s ? atoi(s) : -1;
+  }();
+  return v;
+}
 static PipeVariant pipe_variant(int which) {
+  if (which == 3) {
+    switch (pipe_variant3_id()) {
+      case 1: return {192, 2, 1, 2};
+      case 2: return {192, 2, 2, 2};
+      case 3: return {160, 3, 1, 2};
+      case 4: return {160, 3, 2, 2};
+      case 5: return {256, 2, 1, 2};
+      case 0: return {256, 2, 3, 2};
+      default: return {192, 2, 1, 2};  // 38.3 vs 40.4 us per M^-1 at 512^2
+    }
+  }
   if (which == 2) {
     switch (pipe_variant2_id()) {
       case 1: return {192, 2, 1, 2};
@@ -1333,7 +1352,18 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
         default: return launch_pipe_pm<31, 11, 3, 64, 4, 2, false>(k, grid, st);
       }
     case 3:
-      return pipe_half() ? launch_pipe_pm<73, 7, 1, 256, 2, 3, true>(k, grid, st)
+      if (pipe_half()) {
+        switch (pipe_variant3_id()) {
+          case 1: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st);
+          case 2: return launch_pipe_pm<73, 7, 1, 192, 2, 2, true>(k, grid, st);
+          case 3: return launch_pipe_pm<73, 7, 1, 160, 3, 1, true>(k, grid, st);
+          case 4: return launch_pipe_pm<73, 7, 1, 160, 3, 2, true>(k, grid, st);
+          case 5: return launch_pipe_pm<73, 7, 1, 256, 2, 1, true>(k, grid, st);
+          case 0: return launch_pipe_pm<73, 7, 1, 256, 2, 3, true>(k, grid, st);
+          default: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st);
+        }
+      }
+      return pipe_half() ? launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st)
                          : launch_pipe_t<73, 7, 1>(k, grid, st);
     case 4: return launch_pipe_t<127, 1, 1>(k, grid, st);
     default: return cudaErrorInvalidConfiguration;
