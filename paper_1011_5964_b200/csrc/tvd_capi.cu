@@ -100,6 +100,7 @@ struct tvd_ctx {
     cudaGraphExec_t exec = nullptr;
     std::vector<uintptr_t> key;  // operand pointers / scalars / scratch slots baked in
     long long launches = 0;      // kernels per replay
+    std::vector<uintptr_t> pending;  // last operand set solved eagerly (graph_worth)
   };
   GraphCache pcg_graph, bicg_graph;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
@@ -1151,6 +1152,17 @@ static int graph_prepare(tvd_ctx* c, tvd_ctx::GraphCache& g, const std::vector<u
   g.key = key;
   return TVD_OK;
 }
+// Whether a solve with operand set `key` should run from a graph: always when the cached graph
+// matches (replay only); for a new operand set only on large grids (n >= 2048: the capture +
+// update, ~0.3 ms of host work, is repaid within one solve) or when the same set was just
+// solved eagerly (a repeated system).  Small problems with fresh operands every solve (the
+// config-4 batch) stay eager.
+static bool graph_worth(tvd_ctx::GraphCache& g, const std::vector<uintptr_t>& key, int n) {
+  if (g.exec && g.key == key) return true;
+  if (n >= 2048 || g.pending == key) return true;
+  g.pending = key;
+  return false;
+}
 static void key_push(std::vector<uintptr_t>& k, const void* p) {
   k.push_back(reinterpret_cast<uintptr_t>(p));
 }
@@ -1888,8 +1900,9 @@ int tvd_bicgstab_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre
   };
   constexpr int kGraphIters = 4;
   bool done = false;
-  if (graphs_enabled() && !c->profiling) {  // graph replay as in tvd_pcg_solve
-    std::vector<uintptr_t> key;
+  std::vector<uintptr_t> key;
+  bool use_graph = graphs_enabled() && !c->profiling;
+  if (use_graph) {  // graph replay as in tvd_pcg_solve
     for (const void* vp : {(const void*)sys->blur, (const void*)sys->a_h, (const void*)sys->a_v,
                            (const void*)sys->s, (const void*)(pre ? pre->inv_eig : nullptr),
                            (const void*)(pre ? pre->d : nullptr), (const void*)x,
@@ -1905,6 +1918,9 @@ int tvd_bicgstab_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre
     key.push_back((uintptr_t)(pre ? pre->kind * 16 + pre->family : 255));
     key.push_back((uintptr_t)(sys->bc_l * 2 + sys->reblur));
     key_slots(key, c);
+    use_graph = graph_worth(c->bicg_graph, key, n);
+  }
+  if (use_graph) {
     rc = graph_prepare(c, c->bicg_graph, key, [&]() -> int {
       st = c->stream;
       int rc2 = TVD_OK;
@@ -2057,10 +2073,9 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   // shrink to the graph's.  Profiling runs (per-launch events) stay eager.
   constexpr int kGraphIters = 4;
   bool done = false;
-  if (graphs_enabled() && !c->profiling) {
-    rc = enqueue_iter(0);
-    if (rc) return rc;
-    std::vector<uintptr_t> key;
+  std::vector<uintptr_t> key;
+  bool use_graph = graphs_enabled() && !c->profiling;
+  if (use_graph) {
     for (const void* v : {(const void*)sys->blur, (const void*)sys->a_h, (const void*)sys->a_v,
                           (const void*)sys->s, (const void*)(pre ? pre->inv_eig : nullptr),
                           (const void*)(pre ? pre->d : nullptr), (const void*)x,
@@ -2075,6 +2090,11 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
     key.push_back((uintptr_t)(pre ? pre->kind * 16 + pre->family : 255));
     key.push_back((uintptr_t)(sys->bc_l * 2 + sys->reblur));
     key_slots(key, c);
+    use_graph = graph_worth(c->pcg_graph, key, n);
+  }
+  if (use_graph) {
+    rc = enqueue_iter(0);
+    if (rc) return rc;
     rc = graph_prepare(c, c->pcg_graph, key, [&]() -> int {
       st = c->stream;
       int rc2 = TVD_OK;
