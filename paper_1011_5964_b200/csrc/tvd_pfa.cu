@@ -707,7 +707,7 @@ __device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, uns
 // -1: read both from the parameters.  The specialised instances carry only their pass's code
 // (smaller kernels, fewer live registers, no dead branches).
 template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF = false, int BL = kPipeLines,
-          bool CSM = false, int PM = -1>
+          bool CSM = false, int PM = -1, bool HO = false>
 __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   const bool has_mid = PM < 0 ? p.mid != nullptr : (PM & 1) != 0;
   const bool trans = PM < 0 ? p.transposed != 0 : (PM & 2) != 0;
@@ -724,9 +724,10 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   __shared__ __align__(8) unsigned long long mbar;
   const int tid = threadIdx.x, nth = blockDim.x, n = p.n;
   double2* buf = reinterpret_cast<double2*>(smraw);  // pack target (stage 0 input)
-  double2* buf2 = kPipeOOP ? buf + B * LP : buf;     // second buffer of out-of-place stages
+  constexpr bool OOPB = kPipeOOP || (HALF && HO);     // a second line buffer
+  double2* buf2 = OOPB ? buf + B * LP : buf;          // second buffer of out-of-place stages
   double2* res = buf;                                 // buffer holding the transform result
-  double* stage = reinterpret_cast<double*>(buf + (kPipeOOP ? 2 : 1) * B * LP);
+  double* stage = reinterpret_cast<double*>(buf + (OOPB ? 2 : 1) * B * LP);
   // scatter / gather tables are read coalesced (indexed by t) through L1, leaving the
   // shared memory to the padded lines and the staging rows
   const unsigned* __restrict__ scat = HALF ? p.pl.hscat : p.pl.scat;
@@ -739,6 +740,9 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     const int rc = s == 0 ? PfaStageC<SH, 0>::Rcnt
                           : (s == 1 ? PfaStageC<SH, 1>::Rcnt : PfaStageC<SH, 2>::Rcnt);
     for (int i = tid; i < rc; i += nth) reps[s][i] = p.pl.reps[s][i];
+  }
+  if constexpr (HALF && HO) {  // out-of-place stages: the second buffer's pads read as zero
+    for (int i = tid; i < B * LP; i += nth) buf2[i] = make_double2(0.0, 0.0);
   }
   // CSM: the q0 stage's cos / sin tables staged in shared memory (after the reps, 8-aligned)
   double* csm = nullptr;
@@ -896,7 +900,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       issue(jb + 1);
     }
     if constexpr (HALF) {
-      half_transform<Q1, Q2, B, NT / 32, TPW, CSM>(buf, p.pl, p.stages, csm);
+      half_transform<Q1, Q2, B, NT / 32, TPW, CSM, HO>(buf, p.pl, p.stages, csm, buf2);
       res = buf;
     } else {
       res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
@@ -957,7 +961,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
       __syncthreads();
       if constexpr (HALF) {
-        half_transform<Q1, Q2, B, NT / 32, TPW, CSM>(buf, p.pl, p.stages, csm);
+        half_transform<Q1, Q2, B, NT / 32, TPW, CSM, HO>(buf, p.pl, p.stages, csm, buf2);
         res = buf;
       } else {
         res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
@@ -1084,42 +1088,42 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 }
 
 template <int Q1, int Q2, int Q3, int NT = 256, int MINB = 2, int TPW = 3, bool HALF = false,
-          int BL = kPipeLines, bool CSM = false, int PM = -1>
+          int BL = kPipeLines, bool CSM = false, int PM = -1, bool HO = false>
 static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   using SH = PfaShape<Q1, Q2, Q3>;
   int reps = PfaStageC<SH, 0>::Rcnt;
   if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
   if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
   constexpr int LP = HALF ? HalfShape<Q1, Q2 == 1 ? 3 : Q2>::LPh : SH::LP;
-  size_t smem = (size_t)(kPipeOOP && !HALF ? 2 : 1) * BL * LP * 16 +
+  size_t smem = (size_t)((kPipeOOP && !HALF) || (HALF && HO) ? 2 : 1) * BL * LP * 16 +
                 (size_t)BL * k.n * 8 + (reps + 64) * sizeof(unsigned);
   if (CSM) smem = (smem + 7) / 8 * 8 + (size_t)HalfCoef<HalfShape<Q1, Q2 == 1 ? 3 : Q2>>::total * 8;
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   if (HALF && !k.pl.hscat) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM>,
+    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM, HO>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM><<<grid, NT, smem, st>>>(k);
+  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM, HO><<<grid, NT, smem, st>>>(k);
   return cudaGetLastError();
 }
 
 // the four pass-specialised instances of one launch shape
-template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF>
+template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF, bool HO = false>
 static cudaError_t launch_pipe_pm(const PipeK& k, int grid, cudaStream_t st) {
   static const bool generic = [] {  // TVD_PIPE_PM=0: one kernel for every pass (A/B runs)
     const char* e = getenv("TVD_PIPE_PM");
     return e && e[0] == '0';
   }();
-  if (generic) return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF>(k, grid, st);
+  if (generic) return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, -1, HO>(k, grid, st);
   const int pm = (k.mid ? 1 : 0) | (k.transposed ? 2 : 0);
   switch (pm) {
-    case 0: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 0>(k, grid, st);
-    case 1: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 1>(k, grid, st);
-    case 2: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 2>(k, grid, st);
-    default: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 3>(k, grid, st);
+    case 0: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 0, HO>(k, grid, st);
+    case 1: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 1, HO>(k, grid, st);
+    case 2: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 2, HO>(k, grid, st);
+    default: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 3, HO>(k, grid, st);
   }
 }
 
@@ -1150,7 +1154,8 @@ static int pipe_ws_id() {
   return v;
 }
 
-// Launch shape per specialisation.  2047 = 89 * 23 runs two 6-warp CTAs per SM (one warp
+// Launch shape per specialisation (the 2047 default runs its two stages out of place over a
+// second line buffer, HO).  2047 = 89 * 23 runs two 6-warp CTAs per SM (one warp
 // per k-tile of the q = 89 stage, one column tile per warp and round; the register budget
 // of 170 keeps the DMMA chains unspilled, and the two independent CTAs overlap one batch's
 // pack / unpack with the other's DFT stages: 273 us vs 291 us per M^-1 for one 12-warp CTA,
@@ -1198,6 +1203,7 @@ static PipeVariant pipe_variant(int which) {
       case 3: return {160, 3, 1, 2};
       case 4: return {160, 3, 2, 2};
       case 5: return {256, 2, 1, 2};
+      case 6: return {192, 2, 1, 2};
       case 0: return {256, 2, 3, 2};
       default: return {192, 2, 1, 2};  // 38.3 vs 40.4 us per M^-1 at 512^2
     }
@@ -1242,6 +1248,8 @@ static PipeVariant pipe_variant(int which) {
     case 18: return {192, 2, 1, 2};
     case 19: return {192, 3, 2, 2};
     case 20: return {192, 3, 1, 2};
+    case 21: return {192, 2, 1, 2};
+    case 22: return {192, 2, 2, 2};
     default: return pipe_half() ? PipeVariant{192, 2, 1, 2} : PipeVariant{384, 1, 4, 2};
   }
 }
@@ -1330,8 +1338,11 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
         case 18: return launch_pipe_t<89, 23, 1, 192, 2, 1, true>(k, grid, st);
         case 19: return launch_pipe_t<89, 23, 1, 192, 3, 2, true>(k, grid, st);
         case 20: return launch_pipe_t<89, 23, 1, 192, 3, 1, true>(k, grid, st);
+        case 21: return launch_pipe_pm<89, 23, 1, 192, 2, 1, true, true>(k, grid, st);
+        case 22: return launch_pipe_pm<89, 23, 1, 192, 2, 2, true, true>(k, grid, st);
         default:
-          return pipe_half() ? launch_pipe_pm<89, 23, 1, 192, 2, 1, true>(k, grid, st)
+          // out-of-place stages over two line buffers: 262.8 vs 272.1 us per M^-1
+          return pipe_half() ? launch_pipe_pm<89, 23, 1, 192, 2, 1, true, true>(k, grid, st)
                              : launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
       }
     case 2:
@@ -1359,6 +1370,7 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
           case 3: return launch_pipe_pm<73, 7, 1, 160, 3, 1, true>(k, grid, st);
           case 4: return launch_pipe_pm<73, 7, 1, 160, 3, 2, true>(k, grid, st);
           case 5: return launch_pipe_pm<73, 7, 1, 256, 2, 1, true>(k, grid, st);
+          case 6: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true, true>(k, grid, st);
           case 0: return launch_pipe_pm<73, 7, 1, 256, 2, 3, true>(k, grid, st);
           default: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st);
         }

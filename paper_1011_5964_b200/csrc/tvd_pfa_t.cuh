@@ -422,12 +422,16 @@ struct HalfStage {
 
 // CSM: Cm / Sm point to shared-memory copies and the A fragments are read per r-step
 // (frees the 2 nrs registers of the stationary fragments)
-template <class ST, int NL, int NW, int TPWc, bool CSM = false>
-__device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const double* Sm) {
+// OOP: read `buf`, write `dst` (a second line buffer): no in-place hazard, so the warps run
+// their rounds back to back without the two barriers per round, one barrier at the end.
+template <class ST, int NL, int NW, int TPWc, bool CSM = false, bool OOP = false>
+__device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const double* Sm,
+                                           double2* dst = nullptr) {
   constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LP;
   constexpr bool PT = ST::partnered;
   const int tid = threadIdx.x, nth = blockDim.x;
   constexpr int ndft = NL * ST::Rcnt;
+  double2* const out = OOP ? dst : buf;
   if constexpr (ST::mma) {
     // A-stationary tensor-core stage (see pfa_stage_c): warp -> one k-tile x TPW column tiles
     constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;
@@ -520,12 +524,12 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
           oflag[j] = 1 | (tO == 0 ? 2 : 0);
         }
       }
-      __syncthreads();
+      if constexpr (!OOP) __syncthreads();
 #pragma unroll
       for (int j = 0; j < TPW; ++j) {
         if (oflag[j]) {
           const int k = krow;
-          double2* p = buf + ob[j];
+          double2* p = out + ob[j];
           if (!PT) {
             if (k == 0) {
               p[0] = vk[j];
@@ -534,7 +538,7 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
               p[(q - k) * st] = vm[j];
             }
           } else {
-            double2* pn = buf + on[j];
+            double2* pn = out + on[j];
             const bool self = oflag[j] & 2;
             p[k] = vk[j];
             if (!self) pn[k] = k == 0 ? make_double2(-vk[j].x, -vk[j].y)
@@ -545,8 +549,9 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
 #ifdef TVD_PIPE_TIMING
       tep_ = clock64();
 #endif
-      __syncthreads();
+      if constexpr (!OOP) __syncthreads();
     }
+    if constexpr (OOP) __syncthreads();
 #ifdef TVD_PIPE_TIMING
     if (lane == 0 && warp < 16) {
       unsigned long long* slot = g_stage_t + ((PT ? 1 : 0) * 16 + warp) * 4;
@@ -600,14 +605,14 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
       if (act) {
         if (!PT) {
 #pragma unroll
-          for (int k = 0; k < q; ++k) buf[obs + k * st] = v[k];
+          for (int k = 0; k < q; ++k) out[obs + k * st] = v[k];
         } else {
 #pragma unroll
-          for (int k = 0; k <= H; ++k) buf[obs + k] = v[k];
+          for (int k = 0; k <= H; ++k) out[obs + k] = v[k];
           if (!self) {
-            buf[ons] = make_double2(-v[0].x, -v[0].y);
+            out[ons] = make_double2(-v[0].x, -v[0].y);
 #pragma unroll
-            for (int k = 1; k <= H; ++k) buf[ons + k] = make_double2(-v[q - k].x, -v[q - k].y);
+            for (int k = 1; k <= H; ++k) out[ons + k] = make_double2(-v[q - k].x, -v[q - k].y);
           }
         }
       }
@@ -625,14 +630,21 @@ struct HalfCoef {
   static constexpr int total = 2 * (n0 + n1);
 };
 
-template <int Q0, int Q1, int NL, int NW, int TPW, bool CSM = false>
+template <int Q0, int Q1, int NL, int NW, int TPW, bool CSM = false, bool OOP = false>
 __device__ __forceinline__ void half_transform(double2* buf, const PfaPlan& pl, int stages,
-                                               const double* cs = nullptr) {
+                                               const double* cs = nullptr,
+                                               double2* buf2 = nullptr) {
   using SH = HalfShape<Q0, Q1>;
   using HC = HalfCoef<SH>;
   // stage 0 (the wide radix) reads its fragments from the shared copy when CSM
   const double* c0 = CSM ? cs : pl.st[0].Cm;
   const double* s0 = CSM ? cs + HC::n0 : pl.st[0].Sm;
-  if (stages >= 1) half_stage<HalfStage<SH, 0>, NL, NW, TPW, CSM>(buf, c0, s0);
-  if (stages >= 2) half_stage<HalfStage<SH, 1>, NL, NW, TPW>(buf, pl.st[1].Cm, pl.st[1].Sm);
+  // OOP: stage 0 buf -> buf2, stage 1 buf2 -> buf (the result lands in buf either way)
+  if (stages >= 1) half_stage<HalfStage<SH, 0>, NL, NW, TPW, CSM, OOP>(buf, c0, s0, buf2);
+  if (stages >= 2) {
+    if constexpr (OOP)
+      half_stage<HalfStage<SH, 1>, NL, NW, TPW, false, true>(buf2, pl.st[1].Cm, pl.st[1].Sm, buf);
+    else
+      half_stage<HalfStage<SH, 1>, NL, NW, TPW>(buf, pl.st[1].Cm, pl.st[1].Sm);
+  }
 }
