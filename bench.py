@@ -67,12 +67,12 @@ class ClockSampler:
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
+        self.out = os.fdopen(fd, "w")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                stdout=self.out, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
         time.sleep(0.3)
@@ -85,6 +85,7 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        self.out.close()
 
     def summary(self) -> dict:
         sm, mx, reasons = [], [], set()
