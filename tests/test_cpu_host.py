@@ -52,7 +52,9 @@ def test_library_loads_and_exports_every_declared_symbol():
 
 def test_library_is_built_for_sm_100a():
     so = ROOT / "paper_1011_5964_b200" / "libtvdeblur_b200.so"
-    out = os.popen(f"cuobjdump --list-elf {so} 2>&1").read()
+    import subprocess
+    res = subprocess.run(["cuobjdump", "--list-elf", str(so)], capture_output=True, text=True)
+    out = res.stdout + res.stderr
     assert "sm_100a" in out
 
 
