@@ -417,12 +417,20 @@ cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
   k.L = P.L;
   k.LP = P.L;
   k.b = b;
-  int nl = 4;
+  static const int nl_env = [] {  // TVD_BAND_NL: lines per CTA (experiments)
+    const char* e = getenv("TVD_BAND_NL");
+    return e ? atoi(e) : 0;
+  }();
+  static const int nth_min = [] {  // TVD_BAND_NTH_MIN: minimum threads per CTA
+    const char* e = getenv("TVD_BAND_NTH_MIN");
+    return e ? atoi(e) : 256;
+  }();
+  int nl = nl_env > 0 ? nl_env : 2;  // 2 lines: 792 vs 866 us per 2048^2 assembly for 4
   const size_t cbytes = (size_t)P.L * 16;
   while (nl > 1 && nl * cbytes > 100 * 1024) --nl;
   k.nl = nl;
   int nth = round_up((P.max_items_line + kFftSlots - 1) / kFftSlots, 32);
-  if (nth < 256) nth = 256;
+  if (nth < nth_min) nth = nth_min;
   if (nth > 512) return cudaErrorInvalidConfiguration;
   const size_t smem = nl * cbytes + 2 * nl * sizeof(double);
   const int nb = (b.nlines + nl - 1) / nl;
