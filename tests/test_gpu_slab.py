@@ -161,3 +161,23 @@ def test_slab_pcg_over_nccl_single_rank():
         assert rel_err(out.solution.cpu().numpy(), ref.solution.cpu().numpy()) < 1e-12
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_slab_pcg_graph_replay_matches_eager(nranks):
+    """The slab iteration captured as a CUDA graph (phases + loopback copies) replays to the
+    same iterates as the eager schedule, bit for bit."""
+    spec = CONFIGS["c2a"]
+    system, pre, rhs, v = _problem(512, spec.m, spec.sigma, spec.alpha, spec.beta)
+    cfg = tvd.KrylovConfig(tol=spec.tol, max_iterations=400, record_history=True)
+    outs = {}
+    for graph in (False, True):
+        slabs = [SL.Slab(system, pre.apply_inverse, nranks, r) for r in range(nranks)]
+        outs[graph] = SL.slab_pcg(slabs, SL.LoopbackComm(),
+                                  [SL.split_rows(rhs, nranks, r) for r in range(nranks)],
+                                  [SL.split_rows(v, nranks, r) for r in range(nranks)], cfg,
+                                  graph=graph)
+    for a, b in zip(outs[False], outs[True]):
+        assert a.iterations == b.iterations and a.converged and b.converged
+        assert torch.equal(a.solution, b.solution)
+        assert np.array_equal(a.residual_history, b.residual_history)
