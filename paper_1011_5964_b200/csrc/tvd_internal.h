@@ -86,6 +86,11 @@ struct RaderPlan {
   const double2* bh;     // FFT_M(b), b_q = exp(-2 pi i g^-q / L)
   const double2* tw;     // exp(-2 pi i e / M), e in [0, M)
   const unsigned* dlg;   // m = 1..M: dlog_g(m), the Rader position of input m (plain DFT)
+  // negacyclic half-length form for the odd DST input (a_{n+H} = -a_n, H = M / 2):
+  int H;
+  const double2* psi;    // n < H: exp(i pi n / H)
+  const double2* twh;    // e < H: exp(-2 pi i e / H)
+  const double2* bhh;    // FFT_H of beta~, beta_n = b_n - b_{n+H}, beta~_n = beta_n psi^n
 };
 
 // Device-resident FFT plan plus the per-length twiddle tables of one family.

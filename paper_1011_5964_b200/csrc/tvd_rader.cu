@@ -169,6 +169,39 @@ __device__ __forceinline__ void rader_convolve(double2* buf, const RaderPlan& P)
   RaderStages<M>::fft(buf, P.tw, scratch);
 }
 
+// Half-length stage list: 4095 = 3 3 5 7 13 at kRaderNegThreads = 256 threads; butterflies
+// 1365 / 1365 / 819 / 585 / 315 -> register slots 6 / 6 / 4 / 2 (+ 73 stashed) / 1 (+ 59)
+constexpr int kRaderNegThreads = 256;
+template <>
+struct RaderStages<4095> {
+  __device__ static void fft(double2* buf, const double2* tw, double2* scratch) {
+    rader_stage<3, 6>(buf, 4095, 1, tw);
+    rader_stage<3, 6>(buf, 4095, 3, tw);
+    rader_stage<5, 4>(buf, 4095, 9, tw);
+    rader_stage<7, 2, true>(buf, 4095, 45, tw, scratch);
+    rader_stage<13, 1, true>(buf, 4095, 315, tw, scratch);
+  }
+  static constexpr int kScratch = 59 * 13;  // max(73 * 7, 59 * 13)
+};
+
+// DST input is odd (c'_{L-j} = -c'_j), so in Rader order a_{n+H} = -a_n (H = M / 2) and the
+// length-M cyclic convolution folds into a length-H negacyclic one: with psi = exp(i pi / H),
+// y_m = psi^-m (a psi^n (*) beta psi^n)_m for m < H and y_{m+H} = -y_m.  Half the FFT length,
+// half the shared memory (two CTAs per SM).
+template <int H>
+__device__ __forceinline__ void rader_convolve_neg(double2* buf, const RaderPlan& P) {
+  double2* scratch = buf + H;
+  for (int m = threadIdx.x; m < H; m += blockDim.x) buf[m] = cmul(buf[m], __ldg(&P.psi[m]));
+  __syncthreads();
+  RaderStages<H>::fft(buf, P.twh, scratch);
+  for (int m = threadIdx.x; m < H; m += blockDim.x) {
+    const double2 x = cmul(buf[m], __ldg(&P.bhh[m]));
+    buf[m] = make_double2(x.x, -x.y);
+  }
+  __syncthreads();
+  RaderStages<H>::fft(buf, P.twh, scratch);
+}
+
 struct RaderK {
   RaderPlan pl;
   int n, off, nlines;
@@ -227,6 +260,86 @@ __global__ void __launch_bounds__(kRaderThreads, 1) k_rader_rows(const RaderK p)
     }
     __syncthreads();
     rader_convolve<MC>(rbuf, p.pl);
+  }
+  double acc = 0.0;
+  for (int t = 1 + tid; t <= M; t += nth) {
+    double y = unpack(t);
+    if (io.post) y = io.post_mul ? y * io.post[rb + t] : y / io.post[rb + t];
+    io.out[rb + t] = y;
+    if (io.dot_with) acc += y * io.dot_with[rb + t];
+  }
+  if (p.off && tid < 2) {  // Shat borders pass through every transform
+    const long g = (long)line * n + (tid ? n - 1 : 0);
+    double v = in_at(tid ? n - 1 : 0);
+    if (io.pre) v = io.pre_mul ? v * io.pre[g] : v / io.pre[g];
+    if (io.mid_mul) v *= io.mid_mul[g];
+    if (io.post) v = io.post_mul ? v * io.post[g] : v / io.post[g];
+    io.out[g] = v;
+    if (io.dot_with) acc += v * io.dot_with[g];
+  }
+  if (io.partial) {
+    const double s = block_sum(acc, red);
+    if (tid == 0) io.partial[blockIdx.x] = s;
+    if (io.fin.s) pcg_fin_tail(io.fin, io.partial, gridDim.x, red);
+  }
+}
+
+// The row pass on the negacyclic half-length convolution (HC = H); same I/O as k_rader_rows.
+template <int HC>
+__global__ void __launch_bounds__(kRaderNegThreads, 2) k_rader_rows_neg(const RaderK p) {
+  const LineIO& io = p.io;
+  if (io.skip && *io.skip) return;
+  extern __shared__ __align__(16) double2 rbuf[];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nth = blockDim.x, n = p.n, line = blockIdx.x;
+  constexpr int H = HC, M = 2 * HC;  // M = L - 1 DST outputs per line
+  const long rb = (long)line * n + p.off - 1;
+  auto pack = [&](int t, double x) {  // position q >= H holds -a_{q-H}
+    int q = (int)__ldg(&p.pl.rin[t - 1]);
+    if (q >= H) {
+      q -= H;
+      x = -x;
+    }
+    reinterpret_cast<double*>(rbuf)[2 * q + (t & 1)] = x;
+  };
+  auto unpack = [&](int k) {  // C_k = sgn conj(psi^m' R_m') / H, 1/H in scale
+    int m = (int)__ldg(&p.pl.rout[k - 1]);
+    double sgn = 1.0;
+    if (m >= H) {
+      m -= H;
+      sgn = -1.0;
+    }
+    const double2 P = cmul(__ldg(&p.pl.psi[m]), rbuf[m]);
+    const double cx = sgn * P.x, cy = -sgn * P.y;
+    return ((k & 1) ? -(cy + cx) : -(cy - cx)) * p.scale;
+  };
+  auto in_at = [&](int e) {
+    if (!io.in_seg) return io.in[(long)line * n + e];
+    return io.in[(long)(e / io.in_seg) * io.in_seg_stride + (long)line * io.in_seg + e % io.in_seg];
+  };
+  for (int t = 1 + tid; t <= M; t += nth) {
+    double x = in_at(p.off - 1 + t);
+    if (io.pre) x = io.pre_mul ? x * io.pre[rb + t] : x / io.pre[rb + t];
+    pack(t, x);
+  }
+  __syncthreads();
+  rader_convolve_neg<HC>(rbuf, p.pl);
+  if (io.mid_mul) {
+    constexpr int kV = (M + kRaderNegThreads - 1) / kRaderNegThreads;
+    double v[kV];
+#pragma unroll
+    for (int s = 0; s < kV; ++s) {
+      const int t = 1 + tid + s * nth;
+      v[s] = t <= M ? unpack(t) * io.mid_mul[rb + t] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < kV; ++s) {
+      const int t = 1 + tid + s * nth;
+      if (t <= M) pack(t, v[s]);
+    }
+    __syncthreads();
+    rader_convolve_neg<HC>(rbuf, p.pl);
   }
   double acc = 0.0;
   for (int t = 1 + tid; t <= M; t += nth) {
@@ -389,6 +502,19 @@ cudaError_t launch_rader_rows(const RaderPlan& P, int family, int len, int nline
   }
   if (nblocks_out) *nblocks_out = nlines;
   if (nlines == 0) return cudaSuccess;
+  static const bool full = getenv("TVD_RADER_FULL") != nullptr;  // A/B: full-length engine
+  if (!full && P.H == 4095 && P.psi) {
+    k.scale = 0.5 * sqrt(2.0 / (P.M + 1)) / P.H;
+    const size_t smem_h = (size_t)(P.H + RaderStages<4095>::kScratch) * sizeof(double2);
+    static bool attr_h = false;
+    if (!attr_h) {
+      cudaFuncSetAttribute(k_rader_rows_neg<4095>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_h);
+      attr_h = true;
+    }
+    k_rader_rows_neg<4095><<<nlines, kRaderNegThreads, smem_h, st>>>(k);
+    return cudaGetLastError();
+  }
   k_rader_rows<8190><<<nlines, kRaderThreads, smem, st>>>(k);
   return cudaGetLastError();
 }
@@ -521,9 +647,35 @@ bool build_rader_plan(int L, RaderPlan* P, std::vector<void*>& owned) {
     bh[k] = make_double2((double)xr, (double)xi);
     tw[k] = make_double2((double)cm[k], -(double)sm[k]);
   }
+  // negacyclic half-length tables: beta_n = b_n - b_{n+H}, beta~ = beta psi^n, bhh = FFT_H
+  const int H = M / 2;
+  std::vector<double2> psi(H), twh(H), bhh(H);
+  std::vector<long double> tr(H), ti(H), ch(H), sh(H);
+  for (int e = 0; e < H; ++e) {
+    long double c, s;
+    cis_ld(e, 2LL * H, &c, &s);  // exp(i pi e / H)
+    psi[e] = make_double2((double)c, (double)s);
+    tr[e] = (bre[e] - bre[e + H]) * c - (bim[e] - bim[e + H]) * s;
+    ti[e] = (bre[e] - bre[e + H]) * s + (bim[e] - bim[e + H]) * c;
+    cis_ld(e, H, &ch[e], &sh[e]);
+    twh[e] = make_double2((double)ch[e], -(double)sh[e]);
+  }
+  for (int k = 0; k < H; ++k) {
+    long double xr = 0, xi = 0;
+    int idx = 0;
+    for (int q = 0; q < H; ++q) {  // sum_q beta~_q exp(-2 pi i q k / H)
+      xr += tr[q] * ch[idx] + ti[q] * sh[idx];
+      xi += ti[q] * ch[idx] - tr[q] * sh[idx];
+      idx += k;
+      if (idx >= H) idx -= H;
+    }
+    bhh[k] = make_double2((double)xr, (double)xi);
+  }
+  P->H = H;
   if (!upload_vec(rin, &P->rin, owned) || !upload_vec(rout, &P->rout, owned) ||
       !upload_vec(bh, &P->bh, owned) || !upload_vec(tw, &P->tw, owned) ||
-      !upload_vec(dlg, &P->dlg, owned))
+      !upload_vec(dlg, &P->dlg, owned) || !upload_vec(psi, &P->psi, owned) ||
+      !upload_vec(twh, &P->twh, owned) || !upload_vec(bhh, &P->bhh, owned))
     return false;
   return true;
 }
