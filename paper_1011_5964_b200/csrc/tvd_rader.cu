@@ -98,10 +98,18 @@ __device__ __forceinline__ void rader_stage(double2* buf, int M, int ns,
     const int j = tid + s * nth;
     if (j < nb) {
       const int jm = j % ns;
+      // twiddles w^(r e0), e0 = jm tstride: one table load per butterfly, the powers by
+      // recurrence (R - 2 complex products; ~R ulp, far inside the 1e-12 parity bound) --
+      // the per-element twiddle loads were the kernel's dominant long-scoreboard stall
+      const double2 w1 = ns > 1 ? __ldg(&tw[jm * tstride]) : make_double2(1.0, 0.0);
+      double2 wr = w1;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double2 x = buf[j + r * nb];
-        if (r > 0 && ns > 1) x = cmul(x, __ldg(&tw[r * jm * tstride]));
+        if (r > 0 && ns > 1) {
+          x = cmul(x, wr);
+          if (r + 1 < R) wr = cmul(wr, w1);
+        }
         v[s][r] = x;
       }
       dft_any<R>(v[s], cs);
@@ -122,10 +130,15 @@ __device__ __forceinline__ void rader_stage(double2* buf, int M, int ns,
     for (int j = jr + tid; j < nb; j += nth) {
       const int jm = j % ns;
       double2 w[R];
+      const double2 w1 = ns > 1 ? __ldg(&tw[jm * tstride]) : make_double2(1.0, 0.0);
+      double2 wr = w1;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double2 x = scratch[r * (nb - jr) + j - jr];
-        if (r > 0 && ns > 1) x = cmul(x, __ldg(&tw[r * jm * tstride]));
+        if (r > 0 && ns > 1) {
+          x = cmul(x, wr);
+          if (r + 1 < R) wr = cmul(wr, w1);
+        }
         w[r] = x;
       }
       dft_any<R>(w, cs);
