@@ -197,10 +197,16 @@ __device__ __forceinline__ void stage_reg(double2* buf, int LP, int nl, int L, i
       if (i < items) {
         const int line = l0 + i / nb, j = i % nb, jm = j % ns;
         const double2* base = buf + line * LP;
+        // one twiddle load per butterfly, the powers w^(r e0) by recurrence (~R ulp)
+        const double2 w1 = ns > 1 ? __ldg(&tw[jm * tstride]) : make_double2(1.0, 0.0);
+        double2 wr = w1;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           double2 x = base[j + r * nb];
-          if (r > 0 && ns > 1) x = cmul(x, __ldg(&tw[r * jm * tstride]));
+          if (r > 0 && ns > 1) {
+            x = cmul(x, wr);
+            if (r + 1 < R) wr = cmul(wr, w1);
+          }
           v[s][r] = x;
         }
         dft_reg<R>(v[s]);
