@@ -666,6 +666,41 @@ def run_batch(args, rank: int, world: int) -> None:
         return sum(tvd.pcg(s, p.apply_inverse, b, x0, cfg).iterations for s, p, b, x0 in probs)
 
     elapsed, iters, _, clk = _time_region(step, args, world, local, dev)
+
+    # e2e through the public API: every problem's (u, rhs) host -> device from pinned memory
+    # and its solution device -> host, on the problem's worker stream; the streams overlap
+    # one another's copies with their solves
+    hosts = [(x0.cpu().pin_memory(), b.cpu().pin_memory(), torch.empty(x0.shape, dtype=x0.dtype, pin_memory=True))
+             for _, _, b, x0 in probs]
+    hgroups = [hosts[k::nstreams] for k in range(nstreams)]
+    dbufs = [(torch.empty_like(probs[0][3]), torch.empty_like(probs[0][2]))
+             for _ in range(nstreams)]
+
+    def e2e_group(k):
+        torch.cuda.set_device(local)
+        ud, bd = dbufs[k]
+        its = 0
+        with torch.cuda.stream(streams[k]):
+            for (s, p, _, _), (uh, bh, oh) in zip(groups[k], hgroups[k]):
+                ud.copy_(uh, non_blocking=True)
+                bd.copy_(bh, non_blocking=True)
+                res = tvd.pcg(s, p.apply_inverse, bd, ud, cfg)
+                oh.copy_(res.solution, non_blocking=True)
+                its += res.iterations
+        return its
+
+    def e2e_step() -> int:
+        cur = torch.cuda.current_stream(dev)
+        for st in streams:
+            st.wait_stream(cur)
+        its = sum(pool.map(e2e_group, range(nstreams)))
+        for st in streams:
+            cur.wait_stream(st)
+        return its
+
+    e2e_args = argparse.Namespace(warmup=1, steps=max(1, min(args.steps, 3)))
+    e2e_t, e2e_iters, _, _ = _time_region(e2e_step, e2e_args, world, local, dev)
+    (e2e_iters,) = _sum_over_ranks([e2e_iters], world, dev)
     pool.shutdown()
     l0 = nat.launch_count(dev)
     solve_all()
@@ -694,7 +729,11 @@ def run_batch(args, rank: int, world: int) -> None:
                          "frac": 128.0 * n * n * value / world / 1e9 / hbm},
         "kernels": kernels, "profiled_iterations": prof_iters,
         "cpu_baseline": None,
-        "e2e": None,
+        "e2e": {"value": e2e_iters / e2e_t, "unit": UNIT,
+                "h2d_bytes_per_step": 16 * n * n * len(mine),
+                "d2h_bytes_per_step": 8 * n * n * len(mine), "steps": e2e_args.steps,
+                "path": "per problem: pinned H2D of (u, rhs), tvd.pcg, D2H of the solution, "
+                        "on the problem's worker stream"},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
