@@ -144,7 +144,8 @@ __device__ __forceinline__ void transform_lines(const TrigK& p, double* real, do
   }
 }
 
-__global__ void __launch_bounds__(512) k_trig(const TrigK p) {
+template <int NTH, int MINB>
+__global__ void __launch_bounds__(NTH, MINB) k_trig(const TrigK p) {
   const LineIO& io = p.io;
   if (io.skip && *io.skip) return;
   extern __shared__ double2 smem2[];
@@ -395,10 +396,17 @@ cudaError_t launch_trig(const TrigPlan& P, const LineGeom& g, int analysis, cons
   if (nb == 0) return cudaSuccess;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(k_trig, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_trig<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_trig<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
-  k_trig<<<nb, nth, smem, st>>>(k);
+  // 256-thread CTAs take the 255-register instance (the 512-thread bound caps the engine at
+  // 128 registers and spills; c2b 10831 -> 10980 it/s); TVD_LINES_CAP128=1 keeps the capped one
+  static const bool wide = !getenv("TVD_LINES_CAP128");
+  if (nth <= 256 && wide)
+    k_trig<256, 1><<<nb, nth, smem, st>>>(k);
+  else
+    k_trig<512, 1><<<nb, nth, smem, st>>>(k);
   return cudaGetLastError();
 }
 
@@ -440,6 +448,8 @@ cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
     cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
+  // (a 255-register instance for 256-thread CTAs measured slower here: 1164 vs 805 us per
+  // 2048^2 assembly -- occupancy, not the rarely executed spills, bounds this kernel)
   k_band<<<nb, nth, smem, st>>>(k);
   return cudaGetLastError();
 }
