@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
                                                      const double* __restrict__ in,
                                                      double* __restrict__ out, const int* skip,
                                                      int row_lo, int row_hi, PFuse fz) {
+  pdl_enter();
   if (skip && *skip) return;
   using SH = BmShape<KOFF>;
   constexpr int T = kBmT, S = SH::S, RP = SH::RP, W2 = SH::WIDTH / 2;
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(256, MINB) k_bmma_cols(BandOp op, BandTaps tp,
                                                      const double* __restrict__ in,
                                                      double* __restrict__ out, Epilogue ep,
                                                      const int* skip, int row_lo, int row_hi) {
+  pdl_enter();
   if (skip && *skip) return;
   using SH = BmShape<KOFF, TC>;
   constexpr int T = TC, S = SH::S, CP = SH::CP, C2 = SH::CC / 2;
@@ -414,8 +416,8 @@ cudaError_t launch_band_mma_rows_fused(const BandOp& op, const double* in, doubl
     }                                                                                        \
     dim3 grid((n + SH::CW - 1) / SH::CW, (nr + SH::RH - 1) / SH::RH);                        \
     const size_t sm = SH::rows_smem() + (z ? SH::RH * SH::RP * sizeof(double) : 0);           \
-    k_bmma_rows<K><<<grid, 256, sm, st>>>(op, tp, in, out, skip, row_lo, row_hi, fz);        \
-    return cudaGetLastError();                                                               \
+    return launch_pdl(k_bmma_rows<K>, grid, 256, sm, st, op, tp, in, out, skip, row_lo, row_hi, \
+                      fz);                                                                   \
   }
     TVD_KOFFS(X)
 #undef X
@@ -436,9 +438,8 @@ static cudaError_t launch_cols_t(const BandOp& op, const BandTaps& tp, const dou
   }
   const int n = op.n, nr = row_hi - row_lo;
   dim3 grid((n + SH::CC - 1) / SH::CC, (nr + SH::RW - 1) / SH::RW);
-  k_bmma_cols<K, TC, MINB><<<grid, 256, SH::cols_smem(), st>>>(op, tp, in, out, ep, skip, row_lo,
-                                                                row_hi);
-  return cudaGetLastError();
+  return launch_pdl(k_bmma_cols<K, TC, MINB>, grid, 256, SH::cols_smem(), st, op, tp, in, out, ep,
+                    skip, row_lo, row_hi);
 }
 
 cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out,

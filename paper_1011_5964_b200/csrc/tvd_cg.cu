@@ -69,6 +69,7 @@ __global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst,
 }
 
 __global__ void k_pcg_gamma(PcgState* s, const double* partial, int nb) {
+  pdl_enter();
   if (s->done) return;
   const double gamma = sum_partials_block(partial, nb);
   if (threadIdx.x == 0) pcg_fin_gamma(s, gamma);
@@ -79,6 +80,7 @@ __global__ void k_pcg_gamma(PcgState* s, const double* partial, int nb) {
 __global__ void k_pcg_update_xr(const PcgState* s, double* __restrict__ x, double* __restrict__ r,
                                 const double* __restrict__ p, const double* __restrict__ q, long N,
                                 double* partial, PcgFin fin) {
+  pdl_enter();
   if (s->done) return;
   __shared__ double red[32];
   const double step = s->step;
@@ -127,12 +129,14 @@ __global__ void k_pcg_update_xr(const PcgState* s, double* __restrict__ x, doubl
 }
 
 __global__ void k_pcg_rel(PcgState* s, const double* partial, int nb, double tol, double* hist) {
+  pdl_enter();
   if (s->done) return;
   const double rr = sum_partials_block(partial, nb);
   if (threadIdx.x == 0) pcg_fin_rel(s, rr, tol, hist);
 }
 
 __global__ void k_pcg_beta(PcgState* s, const double* partial, int nb, int max_it) {
+  pdl_enter();
   if (s->done) return;
   const double rz_next = sum_partials_block(partial, nb);
   if (threadIdx.x == 0) pcg_fin_beta(s, rz_next, max_it);
@@ -141,6 +145,7 @@ __global__ void k_pcg_beta(PcgState* s, const double* partial, int nb, int max_i
 // p = z + beta p (numpy rounding); 128-bit accesses, two pairs per thread in flight.
 __global__ void k_pcg_update_p(const PcgState* s, double* __restrict__ p, const double* __restrict__ z,
                                long N) {
+  pdl_enter();
   if (s->done) return;
   const double beta = s->beta;
   const long N2 = N >> 1, stride = (long)gridDim.x * blockDim.x;
@@ -283,26 +288,22 @@ cudaError_t launch_copy(const double* src, double* dst, long N, const int* skip,
   return cudaGetLastError();
 }
 cudaError_t launch_pcg_gamma(PcgState* s, const double* partial, int nb, cudaStream_t st) {
-  k_pcg_gamma<<<1, 512, 0, st>>>(s, partial, nb);
-  return cudaGetLastError();
+  return launch_pdl(k_pcg_gamma, 1, 512, 0, st, s, partial, nb);
 }
 cudaError_t launch_pcg_update_xr(PcgState* s, double* x, double* r, const double* p, const double* q,
                                  long N, double* partial, int, cudaStream_t st, const PcgFin* fin) {
-  k_pcg_update_xr<<<TVD_VEC_GRID>>>(s, x, r, p, q, N, partial, fin ? *fin : PcgFin{});
-  return cudaGetLastError();
+  return launch_pdl(k_pcg_update_xr, kRedBlocks, kVecThreads, 0, st, s, x, r, p, q, N, partial,
+                    fin ? *fin : PcgFin{});
 }
 cudaError_t launch_pcg_rel(PcgState* s, const double* partial, int nb, double tol, double* hist,
                            cudaStream_t st) {
-  k_pcg_rel<<<1, 512, 0, st>>>(s, partial, nb, tol, hist);
-  return cudaGetLastError();
+  return launch_pdl(k_pcg_rel, 1, 512, 0, st, s, partial, nb, tol, hist);
 }
 cudaError_t launch_pcg_beta(PcgState* s, const double* partial, int nb, int max_it, cudaStream_t st) {
-  k_pcg_beta<<<1, 512, 0, st>>>(s, partial, nb, max_it);
-  return cudaGetLastError();
+  return launch_pdl(k_pcg_beta, 1, 512, 0, st, s, partial, nb, max_it);
 }
 cudaError_t launch_pcg_update_p(PcgState* s, double* p, const double* z, long N, cudaStream_t st) {
-  k_pcg_update_p<<<TVD_VEC_GRID>>>(s, p, z, N);
-  return cudaGetLastError();
+  return launch_pdl(k_pcg_update_p, kRedBlocks, kVecThreads, 0, st, s, p, z, N);
 }
 cudaError_t launch_diag_solve(const double* r, const double* d, double* z, long N, double* partial, int,
                               const int* skip, cudaStream_t st) {

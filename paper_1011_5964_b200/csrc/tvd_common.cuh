@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 namespace tvd {
 
@@ -38,6 +40,45 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
     t = warp_sum(t);
   }
   return t;
+}
+
+// Programmatic dependent launch (PDL).  The PCG iteration kernels are launched with the
+// programmatic-stream-serialization attribute (`launch_pdl`), so the next kernel's CTAs are
+// scheduled onto the SMs while this one drains its last wave and the launch latency between
+// the ~5 kernels of an iteration overlaps the tail.  Every kernel launched that way calls
+// `pdl_enter()` FIRST, unconditionally (also before its done / skip test, which reads state
+// the previous kernel wrote): griddepcontrol.wait blocks until the previous grid has completed
+// and its memory is visible, so completion stays transitive along the stream.  The dependents
+// trigger comes after the wait, so at most two grids of the stream are resident at a time.
+// Both instructions are no-ops for a grid launched without the attribute.  TVD_NO_PDL=1
+// launches everything plainly (A/B switch).
+#ifndef TVD_PDL_EARLY_TRIGGER
+#define TVD_PDL_EARLY_TRIGGER 1
+#endif
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (TVD_PDL_EARLY_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = getenv("TVD_NO_PDL") == nullptr;
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace tvd

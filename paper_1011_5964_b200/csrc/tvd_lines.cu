@@ -146,6 +146,7 @@ __device__ __forceinline__ void transform_lines(const TrigK& p, double* real, do
 
 template <int NTH, int MINB>
 __global__ void __launch_bounds__(NTH, MINB) k_trig(const TrigK p) {
+  pdl_enter();
   const LineIO& io = p.io;
   if (io.skip && *io.skip) return;
   extern __shared__ double2 smem2[];
@@ -403,11 +404,8 @@ cudaError_t launch_trig(const TrigPlan& P, const LineGeom& g, int analysis, cons
   // 256-thread CTAs take the 255-register instance (the 512-thread bound caps the engine at
   // 128 registers and spills; c2b 10831 -> 10980 it/s); TVD_LINES_CAP128=1 keeps the capped one
   static const bool wide = !getenv("TVD_LINES_CAP128");
-  if (nth <= 256 && wide)
-    k_trig<256, 1><<<nb, nth, smem, st>>>(k);
-  else
-    k_trig<512, 1><<<nb, nth, smem, st>>>(k);
-  return cudaGetLastError();
+  if (nth <= 256 && wide) return launch_pdl(k_trig<256, 1>, nb, nth, smem, st, k);
+  return launch_pdl(k_trig<512, 1>, nb, nth, smem, st, k);
 }
 
 cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,

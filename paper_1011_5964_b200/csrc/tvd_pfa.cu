@@ -709,6 +709,7 @@ __device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, uns
 template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF = false, int BL = kPipeLines,
           bool CSM = false, int PM = -1, bool HO = false>
 __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
+  pdl_enter();
   const bool has_mid = PM < 0 ? p.mid != nullptr : (PM & 1) != 0;
   const bool trans = PM < 0 ? p.transposed != 0 : (PM & 2) != 0;
   using SH = PfaShape<Q1, Q2, Q3>;
@@ -1106,8 +1107,8 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM, HO><<<grid, NT, smem, st>>>(k);
-  return cudaGetLastError();
+  return launch_pdl(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM, HO>, grid, NT, smem,
+                    st, k);
 }
 
 // the four pass-specialised instances of one launch shape

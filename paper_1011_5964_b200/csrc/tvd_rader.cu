@@ -225,6 +225,7 @@ struct RaderK {
 // One line (row) per CTA: row-major in, row-major out.
 template <int MC>
 __global__ void __launch_bounds__(kRaderThreads, 1) k_rader_rows(const RaderK p) {
+  pdl_enter();
   const LineIO& io = p.io;
   if (io.skip && *io.skip) return;
   extern __shared__ __align__(16) double2 rbuf[];
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(kRaderThreads, 1) k_rader_rows(const RaderK p)
 // The row pass on the negacyclic half-length convolution (HC = H); same I/O as k_rader_rows.
 template <int HC>
 __global__ void __launch_bounds__(kRaderNegThreads, 2) k_rader_rows_neg(const RaderK p) {
+  pdl_enter();
   const LineIO& io = p.io;
   if (io.skip && *io.skip) return;
   extern __shared__ __align__(16) double2 rbuf[];
@@ -525,11 +527,9 @@ cudaError_t launch_rader_rows(const RaderPlan& P, int family, int len, int nline
                            (int)smem_h);
       attr_h = true;
     }
-    k_rader_rows_neg<4095><<<nlines, kRaderNegThreads, smem_h, st>>>(k);
-    return cudaGetLastError();
+    return launch_pdl(k_rader_rows_neg<4095>, nlines, kRaderNegThreads, smem_h, st, k);
   }
-  k_rader_rows<8190><<<nlines, kRaderThreads, smem, st>>>(k);
-  return cudaGetLastError();
+  return launch_pdl(k_rader_rows<8190>, nlines, kRaderThreads, smem, st, k);
 }
 
 int rader_threads() { return kRaderThreads; }
