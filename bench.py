@@ -340,7 +340,7 @@ def run_ours(args, rank: int, world: int) -> None:
     run_steps(2)
     torch.cuda.synchronize()
     barrier()
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(2, min(args.steps, 10))
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
     e2e_iters = run_steps(e2e_steps)

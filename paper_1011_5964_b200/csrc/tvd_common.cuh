@@ -42,18 +42,21 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
   return t;
 }
 
-// Programmatic dependent launch (PDL).  The PCG iteration kernels are launched with the
-// programmatic-stream-serialization attribute (`launch_pdl`), so the next kernel's CTAs are
-// scheduled onto the SMs while this one drains its last wave and the launch latency between
-// the ~5 kernels of an iteration overlaps the tail.  Every kernel launched that way calls
-// `pdl_enter()` FIRST, unconditionally (also before its done / skip test, which reads state
-// the previous kernel wrote): griddepcontrol.wait blocks until the previous grid has completed
-// and its memory is visible, so completion stays transitive along the stream.  The dependents
-// trigger comes after the wait, so at most two grids of the stream are resident at a time.
-// Both instructions are no-ops for a grid launched without the attribute.  TVD_NO_PDL=1
-// launches everything plainly (A/B switch).
+// Programmatic dependent launch (PDL).  The PCG iteration kernels (DST / Rader / generic line
+// passes, both band passes, the vector updates and finalizers) are launched with the
+// programmatic-stream-serialization attribute (`launch_pdl`): a kernel's grid is launched as
+// soon as every CTA of the previous one has exited, before that grid's completion and memory
+// flush, so the launch latency overlaps the previous kernel's drain.  Every kernel launched
+// that way calls `pdl_enter()` FIRST, unconditionally (also before its done / skip test, which
+// reads state the previous kernel wrote): griddepcontrol.wait blocks until the previous grid
+// has completed and its memory is visible, so completion stays transitive along the stream.
+// An explicit early trigger (griddepcontrol.launch_dependents right after the wait, so the
+// next grid's CTAs become resident during this one's last wave) measured 8 % SLOWER on c3
+// (2330 vs 2532 it/s) and is off by default (-DTVD_PDL_EARLY_TRIGGER=1 builds it).  Both
+// instructions are no-ops for a grid launched without the attribute; TVD_NO_PDL=1 launches
+// everything plainly (A/B switch: c3 2532 vs 2531 it/s, c4 8609 vs 8486).
 #ifndef TVD_PDL_EARLY_TRIGGER
-#define TVD_PDL_EARLY_TRIGGER 1
+#define TVD_PDL_EARLY_TRIGGER 0
 #endif
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
