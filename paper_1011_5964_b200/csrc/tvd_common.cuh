@@ -53,8 +53,10 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
 // An explicit early trigger (griddepcontrol.launch_dependents right after the wait, so the
 // next grid's CTAs become resident during this one's last wave) measured 8 % SLOWER on c3
 // (2330 vs 2532 it/s) and is off by default (-DTVD_PDL_EARLY_TRIGGER=1 builds it).  Both
-// instructions are no-ops for a grid launched without the attribute; TVD_NO_PDL=1 launches
-// everything plainly (A/B switch: c3 2532 vs 2531 it/s, c4 8609 vs 8486).
+// instructions are no-ops for a grid launched without the attribute.  Wait-only PDL measured
+// neutral (c3 2541 / 2537 vs 2541 it/s, c4 8626 vs 8676, c5 102.5 vs 102.5, c2b 11413 vs
+// 11409: the replayed graphs already hide the launch gaps), so the attribute is opt-in:
+// TVD_PDL=1 sets it.
 #ifndef TVD_PDL_EARLY_TRIGGER
 #define TVD_PDL_EARLY_TRIGGER 0
 #endif
@@ -64,7 +66,7 @@ __device__ __forceinline__ void pdl_enter() {
 }
 
 inline bool pdl_enabled() {
-  static const bool on = getenv("TVD_NO_PDL") == nullptr;
+  static const bool on = getenv("TVD_PDL") != nullptr;
   return on;
 }
 
