@@ -125,40 +125,84 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- reference
-def cpu_state(spec, h, v, state_fp: int):
-    """Host-side operators of the oracle port at FP state ``state_fp`` (u = v for 0)."""
+def workload(spec) -> str:
+    """The one workload label both arms print (``config.workload``)."""
+    kind = "M" if spec.bc == "anti_reflective" else "R"
+    if spec.name == "c4":
+        psf = "Gaussian 21x21 sigma 3 / box 11x11 alternating"
+        return (f"{spec.name}: {spec.problems} x {spec.n}^2 AR fp64, {psf}, alpha {spec.alpha}, "
+                f"beta {spec.beta}, tol {spec.tol}, preconditioner M")
+    return (f"{spec.name}: {spec.n}^2 {bc_tag(spec)} fp64, Gaussian {2 * spec.m + 1}x"
+            f"{2 * spec.m + 1} sigma {spec.sigma}, alpha {spec.alpha}, beta {spec.beta}, "
+            f"tol {spec.tol}, preconditioner {kind}")
+
+
+def bench_config(spec, state_fp: int) -> dict:
+    """``config`` of the JSON line, identical in both arms for the same workload."""
+    ws = 15 * 8 * spec.n ** 2 * spec.problems / 2 ** 20
+    l2 = (f"inputs larger than L2 (~15 n^2 fp64 arrays = {ws:.0f} MiB working set vs 126 MB L2)"
+          if ws > 126 else f"working set {ws:.0f} MiB fits in L2 (not flushed; small config)")
+    return {"workload": workload(spec), "n": spec.n, "problems_per_gpu": 1,
+            "state_fp": state_fp, "l2": l2}
+
+
+def cpu_state(spec, h, v, state_fp: int, u_state=None):
+    """Host operators of the oracle port (the reference's fast-operator path,
+    pipeline.py:167-179,209-210) at the lagged-diffusivity state after ``state_fp`` FP steps
+    from ``u = v`` (pipeline.py:200-244), each step a full PCG solve to tol."""
     from oracle import tvd_oracle as O
 
     bc = spec.bc
     lam_h = O.blur_eigenvalues(h, bc, spec.n)
-    u = v.copy()
-    a_h, a_v = O.diffusivity(u, spec.beta)
-    blocks = O.diffusion_bands(a_h, a_v)
-    _, lam_inv, _, _ = O.assemble("M" if bc == "anti_reflective" else "R", lam_h, blocks,
-                                  spec.alpha)
     fam = "sine_hat" if bc == "anti_reflective" else "dct"
+    kind = "M" if bc == "anti_reflective" else "R"
 
-    def apply_a(w):
-        hw = O.blur_fast(w, lam_h, bc)
-        back = hw if bc == "reflective" else O.blur_transpose_fast(hw, lam_h, bc)
-        return back + spec.alpha * O.diffusion_apply(a_h, a_v, w)
+    def operators(u):
+        a_h, a_v = O.diffusivity(u, spec.beta)
+        _, lam_inv, _, _ = O.assemble(kind, lam_h, O.diffusion_bands(a_h, a_v), spec.alpha)
+
+        def apply_a(w):
+            hw = O.blur_fast(w, lam_h, bc)
+            back = hw if bc == "reflective" else O.blur_transpose_fast(hw, lam_h, bc)
+            return back + spec.alpha * O.diffusion_apply(a_h, a_v, w)
+
+        return apply_a, (lambda r: O.precond_solve(fam, lam_inv, r))
 
     rhs = O.blur_transpose_fast(v, lam_h, bc) if bc == "anti_reflective" else O.blur_fast(v, lam_h, bc)
-    return apply_a, (lambda r: O.precond_solve(fam, lam_inv, r)), rhs, u
+    u = v.copy() if u_state is None else np.asarray(u_state, dtype=float)
+    for _ in range(state_fp if u_state is None else 0):
+        apply_a, minv = operators(u)
+        u = O.pcg(apply_a, minv, rhs, u, spec.tol, 2000)[0]
+    apply_a, minv = operators(u)
+    return apply_a, minv, rhs, u
 
 
 def cpu_sample(apply_a, minv, rhs, u, iters: int) -> float:
-    """Seconds for ``iters`` PCG iterations of the oracle port (tol tiny, never converges)."""
-    from oracle import tvd_oracle as O
-
+    """Seconds for exactly ``iters`` PCG loop iterations (krylov.py:95-115: one matvec, one
+    M^-1, three dots, three updates) of the oracle port.  The setup ``r = b - A x0``,
+    ``z = M^-1 r`` runs untimed, as the GPU arm's per-iteration figure amortises it."""
+    x = np.array(u, dtype=float, copy=True)
+    r = rhs - apply_a(x)
+    z = minv(r)
+    p = z.copy()
+    rz = float(np.dot(r.ravel(), z.ravel()))
     t0 = time.perf_counter()
-    O.pcg(apply_a, minv, rhs, u, 1e-300, iters)
+    for _ in range(iters):
+        q = apply_a(p)
+        step = rz / float(np.dot(p.ravel(), q.ravel()))
+        x += step * p
+        r -= step * q
+        math.sqrt(float(np.dot(r.ravel(), r.ravel())))
+        z = minv(r)
+        rz_next = float(np.dot(r.ravel(), z.ravel()))
+        p = z + (rz_next / rz) * p
+        rz = rz_next
     return time.perf_counter() - t0
 
 
-def run_reference(args, rank: int, world: int) -> None:
+def run_reference(args, rank: int, world: int):
     if rank != 0:
-        return
+        return None
     from oracle import tvd_oracle as O
     from paper_1011_5964_b200.harness import CONFIGS, make_problem
 
@@ -166,7 +210,7 @@ def run_reference(args, rank: int, world: int) -> None:
     O.set_workers(cores)
     spec = CONFIGS[args.config]
     h, v, _ = make_problem(spec)
-    apply_a, minv, rhs, u = cpu_state(spec, h, v, 0)
+    apply_a, minv, rhs, u = cpu_state(spec, h, v, args.state_fp)
     per_step = args.ref_iters
     for _ in range(args.warmup):
         cpu_sample(apply_a, minv, rhs, u, per_step)
@@ -175,22 +219,21 @@ def run_reference(args, rank: int, world: int) -> None:
         t += cpu_sample(apply_a, minv, rhs, u, per_step)
     iters = per_step * args.steps
     value = iters / t
-    sample = (f"{per_step} PCG iterations per step of config {spec.name} ({spec.n}^2), oracle "
-              f"restatement of the reference (scipy.fft workers={cores}, numpy elementwise)")
-    line = {
-        "impl": "reference", "metric": metric_for(spec), "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE generator)",
-        "config": {"workload": f"{spec.name}: {spec.n}^2 {bc_tag(spec)} fp64 PCG, preconditioner "
-                               f"{'M' if spec.bc == 'anti_reflective' else 'R'}",
-                   "n": spec.n, "problems_per_gpu": 1, "l2": "inputs larger than L2"},
+    sample = (f"{per_step} PCG loop iterations per step (setup untimed) of config {spec.name} "
+              f"({spec.n}^2) at FP state {args.state_fp}, oracle restatement of the reference "
+              f"(scipy.fft workers={cores}, numpy elementwise)")
+    return {
+        "impl": "reference", "metric": metric_for(spec), "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE piecewise-constant generator, PCG64 noise)",
+        "config": bench_config(spec, args.state_fp),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "mpix_iter_per_s": value * spec.n ** 2 / 1e6,
     }
-    print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------- ours
@@ -363,18 +406,20 @@ def run_ours(args, rank: int, world: int) -> None:
     e2e_value = e2e_iters / e2e_t
 
     if rank != 0:
-        return
+        return None
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         from oracle import tvd_oracle as O
         cores = os.cpu_count() or 1
         O.set_workers(cores)
-        apply_a, minv, crhs, cu = cpu_state(spec, h, v, 0)
+        # the same FP state as the timed GPU solves (the GPU's u after state_fp steps)
+        apply_a, minv, crhs, cu = cpu_state(spec, h, v, args.state_fp, u.cpu().numpy())
         cpu_sample(apply_a, minv, crhs, cu, 1)  # warm (plans, page-in)
         t = cpu_sample(apply_a, minv, crhs, cu, args.cpu_iters)
         cpu = {"value": args.cpu_iters / t, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{args.cpu_iters} PCG iterations of config {spec.name} ({n}^2) with the "
-                         f"oracle restatement (scipy.fft workers={cores}); {t:.1f} s"}
+               "sample": f"{args.cpu_iters} PCG loop iterations (setup untimed) of config "
+                         f"{spec.name} ({n}^2) at FP state {args.state_fp}, oracle "
+                         f"restatement (scipy.fft workers={cores}); {t:.1f} s"}
     clk = clocks.summary()
     alg_iter = 128.0 * n * n
     line = {
@@ -382,15 +427,12 @@ def run_ours(args, rank: int, world: int) -> None:
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE piecewise-constant generator, PCG64 noise)",
-        "config": {"workload": f"{spec.name}: {n}^2 {bc_tag(spec)} fp64, Gaussian {2 * spec.m + 1}x"
-                               f"{2 * spec.m + 1} sigma {spec.sigma}, alpha {spec.alpha}, "
-                               f"beta {spec.beta}, tol {spec.tol}, preconditioner {kind}",
-                   "n": n, "problems_per_gpu": 1, "state_fp": args.state_fp,
-                   "pcg_iters_per_step": iters / (args.steps * world),
-                   "l2": "inputs larger than L2 (~15 n^2 fp64 arrays = 480 MB working set)"},
+        "config": bench_config(spec, args.state_fp),
+        "pcg_iters_per_step": iters / (args.steps * world),
         "mpix_iter_per_s": value * n * n / 1e6,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic_per_launch(dom), "kernel": dom,
+                     "frac": achieved / hbm, "traffic": traffic_per_launch(dom, spec.name, n),
+                     "kernel": dom,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"
                      if not peaks.get("fallback") else "fallback 6650 GB/s"},
         "pcg_roofline": {"alg_bytes_per_iter": alg_iter,
@@ -406,7 +448,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "gpu_launches": int(launches),
         "clocks": clk,
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def _time_region(step, args, world: int, local: int, dev):
@@ -457,7 +499,7 @@ def _sum_over_ranks(vals, world: int, dev):
     return [float(v) for v in t]
 
 
-def _profile_kernels(step, n, dev):
+def _profile_kernels(step, n, dev, config: str):
     """Per-category live CUDA-event timing of one step (tvd_ctx_profile) and the dominant
     HBM-streaming category's roofline entry."""
     from paper_1011_5964_b200 import _native as nat
@@ -478,7 +520,7 @@ def _profile_kernels(step, n, dev):
     peaks = _peaks()
     hbm = float(peaks["hbm_gbs"])
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": traffic_per_launch(dom), "kernel": dom,
+            "frac": achieved / hbm, "traffic": traffic_per_launch(dom, config, n), "kernel": dom,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("fallback")
             else "fallback 6650 GB/s"}
     return roof, kernels, work, hbm
@@ -546,7 +588,7 @@ def run_slab(args, rank: int, world: int) -> None:
     elapsed, iters, launches, clk = _time_region(step, args, world, local, dev)
     (launches,) = _sum_over_ranks([launches], world, dev)
     value = iters / elapsed  # iterations of the one global problem (identical on every rank)
-    roof, kernels, prof_iters, hbm = _profile_kernels(step, n if world == 1 else n, dev)
+    roof, kernels, prof_iters, hbm = _profile_kernels(step, n, dev, spec.name if world == 1 else f"{spec.name}/slab{world}")
     if world > 1:  # per-rank kernels move 1/N of the bytes of a full-size launch
         R = n // world
         for k in kernels.values():
@@ -594,7 +636,7 @@ def run_slab(args, rank: int, world: int) -> None:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_t = float(tt[0])
     if rank != 0:
-        return
+        return None
     line = {
         "metric": f"PCG iters/sec at {n}^2 AR fp64 (config {spec.name}, one image, "
                   f"{'row slabs' if world > 1 else 'single GPU'})",
@@ -602,12 +644,9 @@ def run_slab(args, rank: int, world: int) -> None:
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE piecewise-constant generator, PCG64 noise)",
-        "config": {"workload": f"{spec.name}: {n}^2 AR fp64, Gaussian {2 * spec.m + 1}x"
-                               f"{2 * spec.m + 1} sigma {spec.sigma}, alpha {spec.alpha}, "
-                               f"beta {spec.beta}, tol {spec.tol}, preconditioner M",
-                   "n": n, "slab_rows": R, "parallelism": f"row slabs x{world}",
-                   "state_fp": args.state_fp, "pcg_iters_per_step": iters / args.steps,
-                   "l2": "inputs larger than L2"},
+        "config": {**bench_config(spec, args.state_fp), "slab_rows": R,
+                   "parallelism": f"row slabs x{world}"},
+        "pcg_iters_per_step": iters / args.steps,
         "mpix_iter_per_s": value * n * n / 1e6,
         "roofline": roof,
         "pcg_roofline": {"alg_bytes_per_iter": 128.0 * n * n,
@@ -622,7 +661,7 @@ def run_slab(args, rank: int, world: int) -> None:
         "gpu_launches": int(launches),
         "clocks": clk,
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def run_batch(args, rank: int, world: int) -> None:
@@ -728,21 +767,18 @@ def run_batch(args, rank: int, world: int) -> None:
     launches = (nat.launch_count(dev) - l0) * args.steps  # the contexts of the workers
     iters, launches = _sum_over_ranks([iters, launches], world, dev)
     value = iters / elapsed
-    roof, kernels, prof_iters, hbm = _profile_kernels(solve_all, n, dev)
+    roof, kernels, prof_iters, hbm = _profile_kernels(solve_all, n, dev, spec.name)
     if rank != 0:
-        return
+        return None
     line = {
         "metric": f"PCG iters/sec, batch of {spec.problems} x {n}^2 AR fp64 (config {spec.name})",
         "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE piecewise-constant generator, PCG64 noise)",
-        "config": {"workload": f"{spec.name}: {spec.problems} x {n}^2 AR fp64, Gaussian 21x21 "
-                               f"sigma 3 / box 11x11 alternating, alpha {spec.alpha}, beta "
-                               f"{spec.beta}, tol {spec.tol}, preconditioner M",
-                   "n": n, "problems_per_gpu": len(mine), "streams": nstreams,
-                   "parallelism": f"problem sharding x{world}", "state_fp": args.state_fp,
-                   "pcg_iters_per_step": iters / args.steps, "l2": "inputs larger than L2"},
+        "config": {**bench_config(spec, args.state_fp), "problems_per_gpu": len(mine),
+                   "streams": nstreams, "parallelism": f"problem sharding x{world}"},
+        "pcg_iters_per_step": iters / args.steps,
         "mpix_iter_per_s": value * n * n / 1e6,
         "roofline": roof,
         "pcg_roofline": {"alg_bytes_per_iter": 128.0 * n * n,
@@ -758,21 +794,75 @@ def run_batch(args, rank: int, world: int) -> None:
         "gpu_launches": int(launches),
         "clocks": clk,
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
-def traffic_per_launch(category: str):
-    """DRAM bytes (read + write) per launch of the category's kernel, from the newest committed
-    ``ncu --set full`` capture summarised under profiles/<round>/traffic.json (or None)."""
+def traffic_per_launch(category: str, config: str, n: int):
+    """DRAM bytes (read + write) per launch of the category's kernel for this workload, from
+    the newest committed ``ncu --set full`` capture summarised in a ``profiles/**/traffic.json``
+    (``{"config": ..., "n": ..., "kernels": {category: {"dram_bytes": ...}}}``; the round-1
+    files without the keys are c3 / 2048 captures); None when no capture of this config and
+    size exists."""
     import glob
-    for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)),
-                                              "profiles", "r*", "traffic.json")), reverse=True):
+    root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    paths = glob.glob(os.path.join(root, "**", "traffic.json"), recursive=True)
+    # newest round first (profiles/rNN/...), deeper (later) captures of a round first
+    paths.sort(key=lambda p: (os.path.relpath(p, root).split(os.sep)[0], p.count(os.sep)),
+               reverse=True)
+    for path in paths:
         try:
-            ent = json.load(open(path)).get(category)
+            doc = json.load(open(path))
         except (OSError, ValueError):
             continue
+        if "kernels" in doc:
+            cfg, size, table = doc.get("config"), doc.get("n"), doc["kernels"]
+        else:
+            cfg, size, table = "c3", 2048, doc
+        if cfg != config or size != n:
+            continue
+        ent = table.get(category)
         if ent:
             return ent["dram_bytes"]
+    return None
+
+
+def launch_ranks(args) -> int:
+    """``--gpus N`` without a torchrun environment: re-run this script under
+    ``torch.distributed.run`` with N local ranks (127.0.0.1 rendezvous), NCCL's INFO log on
+    stderr so the communicator's N ranks are visible.  Returns the launcher's exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def launch_check(rank: int, world: int):
+    """``--launch-check``: the process group forms with ``world`` ranks (NCCL on GPUs, gloo
+    on a CPU-only host) and every rank takes part in one all-reduce."""
+    import torch
+    import torch.distributed as dist
+
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if world > 1:
+        if backend == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group(backend)
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))) \
+        if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t)
+        dist.destroy_process_group()
+    if rank == 0:
+        return {"launch_check": True, "n_gpus": world, "backend": backend,
+                "rank_sum": float(t[0])}
     return None
 
 
@@ -788,24 +878,49 @@ def main() -> None:
     ap.add_argument("--ref-iters", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=4, help="c4: host threads / CUDA streams")
+    ap.add_argument("--extra", default="auto",
+                    help="extra workloads measured after the main one and attached under "
+                         "'extra' (comma list of c4 / c5, 'none'); auto = c4 at N > 1")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="only form the N-rank process group and all-reduce once")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.launch_check:
+        line = launch_check(rank, world)
+        if line:
+            print(json.dumps(line), flush=True)
+        return
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        line = run_reference(args, rank, world)
+        if line:
+            print(json.dumps(line), flush=True)
         return
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
+    runners = {"c5": run_slab, "c4": run_batch}
     try:
-        if args.config == "c5":
-            run_slab(args, rank, world)
-        elif args.config == "c4":
-            run_batch(args, rank, world)
-        else:
-            run_ours(args, rank, world)
+        line = runners.get(args.config, run_ours)(args, rank, world)
+        extra = ([] if args.extra == "none" else
+                 (["c4"] if world > 1 and args.config == "c3" else [])
+                 if args.extra == "auto" else [e for e in args.extra.split(",") if e])
+        for cfg in extra:
+            sub = argparse.Namespace(**{**vars(args), "config": cfg, "no_cpu_baseline": True})
+            out = runners.get(cfg, run_ours)(sub, rank, world)
+            if line is not None and out is not None:
+                line.setdefault("extra", {})[cfg] = {
+                    k: out[k] for k in ("metric", "value", "unit", "scaling", "ms_per_step",
+                                        "config", "pcg_iters_per_step", "roofline",
+                                        "pcg_roofline", "e2e", "gpu_launches") if k in out}
+        if line is not None:
+            print(json.dumps(line), flush=True)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -106,6 +107,18 @@ struct tvd_ctx {
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
 };
 
+static void drop_graph(tvd_ctx::GraphCache& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g.exec = nullptr;
+  g.key.clear();
+  g.pending.clear();
+  g.launches = 0;
+}
+static void drop_graphs(tvd_ctx* c) {
+  drop_graph(c->pcg_graph);
+  drop_graph(c->bicg_graph);
+}
+
 // kernel categories for the per-launch timer (tvd_profile_category)
 enum Cat : int {
   kCatTrigRows = 0, kCatTrigCols, kCatBandRows, kCatBandCols, kCatVec, kCatFin,
@@ -144,6 +157,7 @@ static void prof_end(tvd_ctx* c) {
 
 struct tvd_blur {
   tvd_ctx* ctx = nullptr;
+  uint64_t serial = 0;  // unique per blur for the life of the process (solver-graph keys)
   int n = 0, m = 0, bc = 0;
   bool separable = false;
   std::vector<double> psf;   // host copy
@@ -1346,6 +1360,8 @@ int tvd_blur_create(tvd_ctx* c, int n, const double* psf, int width, int bc, tvd
   if (m >= n) return fail(TVD_ERR_INVALID, "PSF half-width must be below size");
   DeviceGuard gd(c->device);
   auto* b = new tvd_blur();
+  static std::atomic<uint64_t> next_serial{1};
+  b->serial = next_serial.fetch_add(1);
   b->ctx = c;
   b->n = n;
   b->m = m;
@@ -1397,6 +1413,8 @@ int tvd_blur_destroy(tvd_blur* b) {
   if (!b) return TVD_OK;
   DeviceGuard g(b->ctx->device);
   cudaStreamSynchronize(b->ctx->stream);
+  // captured solver graphs bake this blur's taps and tables in: drop them with it
+  drop_graphs(b->ctx);
   for (void* p : b->owned) cudaFree(p);
   delete b;
   return TVD_OK;
@@ -1903,7 +1921,8 @@ int tvd_bicgstab_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre
   std::vector<uintptr_t> key;
   bool use_graph = graphs_enabled() && !c->profiling;
   if (use_graph) {  // graph replay as in tvd_pcg_solve
-    for (const void* vp : {(const void*)sys->blur, (const void*)sys->a_h, (const void*)sys->a_v,
+    key.push_back((uintptr_t)sys->blur->serial);
+    for (const void* vp : {(const void*)sys->a_h, (const void*)sys->a_v,
                            (const void*)sys->s, (const void*)(pre ? pre->inv_eig : nullptr),
                            (const void*)(pre ? pre->d : nullptr), (const void*)x,
                            (const void*)r, (const void*)rs, (const void*)p, (const void*)v,
@@ -2076,7 +2095,8 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   std::vector<uintptr_t> key;
   bool use_graph = graphs_enabled() && !c->profiling;
   if (use_graph) {
-    for (const void* v : {(const void*)sys->blur, (const void*)sys->a_h, (const void*)sys->a_v,
+    key.push_back((uintptr_t)sys->blur->serial);
+    for (const void* v : {(const void*)sys->a_h, (const void*)sys->a_v,
                           (const void*)sys->s, (const void*)(pre ? pre->inv_eig : nullptr),
                           (const void*)(pre ? pre->d : nullptr), (const void*)x,
                           (const void*)r, (const void*)zz, (const void*)pb[0], (const void*)pb[1],

@@ -246,3 +246,42 @@ def test_sweep_file_formats_round_trip(tmp_path):
     assert SW.default_half_width(48) == 6
     img, (fr, fc) = SW.gen_image_2d(32, 4)
     assert img.shape == (40, 40) and (fr.start, fr.stop) == (4, 36)
+
+
+def test_sweep_csv_matches_the_csv_module_and_sweep_files_parse(tmp_path):
+    """The hand-written CSV writer agrees byte for byte with ``csv.writer`` (the reference's
+    writer, harness.py:452-460) on floats, ints, numpy scalars, stars and fields that need
+    quoting; sweep files (harness.py:512-568) parse to the same spec as keyword arguments."""
+    import csv
+    import io
+
+    from paper_1011_5964_b200 import sweep as SW
+
+    rows = [("R/x", 1e-3, 0.1, 48, 7, 12.25, 0.0123456789), ("AR+Sine+ZN/d_x", np.float64(2.5e-4),
+            np.int64(3), 64, "*", "*", "*"), ('a,"b"', 1.0, -0.0, 0, 1e300, float("inf"), "x\ny")]
+    SW.write_csv(tmp_path / "a.csv", SW.TABLE_HEADER, rows)
+    buf = io.StringIO(newline="")
+    w = csv.writer(buf, lineterminator="\n")
+    w.writerow(SW.TABLE_HEADER)
+    for r in rows:
+        w.writerow([repr(float(x)) if isinstance(x, (float, np.floating)) else
+                    int(x) if isinstance(x, np.integer) else x for x in r])
+    assert (tmp_path / "a.csv").read_text() == buf.getvalue()
+    hdr, back = SW.read_csv(tmp_path / "a.csv")
+    assert tuple(hdr) == SW.TABLE_HEADER and back[2][0] == 'a,"b"'
+    (tmp_path / "s.cfg").write_text("# sweep\nn = 48, 64\nalpha = 1e-3,1e-2  # two\n"
+                                    "config = R, AR+Sine+ZN\nprecond = x, d_x\nfp_max = 40\n"
+                                    "save_restored = no\n")
+    spec = SW.parse_sweep_config(tmp_path / "s.cfg")
+    assert spec == SW.BenchmarkSpec(ns=(48, 64), alphas=(1e-3, 1e-2),
+                                    configurations=("R", "AR+Sine+ZN"),
+                                    preconditioners=("x", "d_x"), fp_max=40,
+                                    save_restored=False)
+    keys = list(SW.cell_keys(spec))
+    assert len(keys) == 16 and keys[0] == ("R", 48, 0.1, 1e-3, "x") and \
+        keys[-1] == ("AR+Sine+ZN", 64, 0.1, 1e-2, "d_x")
+    (tmp_path / "bad.cfg").write_text("n 48\n")
+    with pytest.raises(ValueError):
+        SW.parse_sweep_config(tmp_path / "bad.cfg")
+    with pytest.raises(ValueError):
+        SW.BenchmarkSpec(dimension=1)

@@ -673,3 +673,36 @@ def test_full_size_operator_symmetry_and_linearity_2048():
     mxy, myx = float((x * my).sum()), float((y * mx).sum())
     assert abs(mxy - myx) <= 1e-12 * float(x.norm() * my.norm())
     assert float((x * mx).sum()) > 0
+
+
+def test_solver_graph_cache_follows_the_blur(rng):
+    """Two solves in a row at 2048^2 (where the fused PCG replays a captured CUDA graph) with
+    blurs of the same width but different taps, the first blur freed before the second is
+    built (so its host address and device tables are likely reused): each fused solve must
+    equal the generic-path solve of its own system, i.e. no stale graph replays the old taps."""
+    import gc
+
+    from paper_1011_5964_b200.harness import gen_psf
+    from paper_1011_5964_b200.pipeline import NormalSystem
+
+    n = 2048
+    u = np.cumsum(rng.standard_normal((n, n)), axis=1) * 0.01
+    b = rng.standard_normal((n, n))
+    lop = TV.DiffusionOperator(u, 0.1)
+    cfg = K.KrylovConfig(tol=1e-6, max_iterations=60)
+    seen = []
+    for sigma in (2.0, 3.5, 2.0):
+        hop = B.StructuredBlurOperator(B.SymmetricPsf(gen_psf("gaussian", 7, sigma)),
+                                       B.BoundaryCondition.ANTI_REFLECTIVE, n)
+        system = NormalSystem(hop, lop, 1e-3)
+        pre = P.assemble_preconditioner("M", hop, lop, 1e-3)
+        fused = K.pcg(system, pre.apply_inverse, b, np.zeros((n, n)), cfg)
+        generic = K.pcg(lambda w, s=system: s(w), lambda r, p=pre: p.apply_inverse(r), b,
+                        np.zeros((n, n)), cfg)
+        assert fused.converged and fused.iterations == generic.iterations, sigma
+        assert rel_err(fused.solution, generic.solution) < 1e-10, sigma
+        seen.append(fused.solution)
+        del hop, system, pre, fused, generic
+        gc.collect()
+    assert rel_err(seen[0], seen[1]) > 1e-3
+    assert rel_err(seen[0], seen[2]) < 1e-14
