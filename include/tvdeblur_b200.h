@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TVD_ABI_VERSION 2
+#define TVD_ABI_VERSION 3
 
 /* status codes -> exception classes of the reference */
 #define TVD_OK 0
@@ -99,10 +99,30 @@ int tvd_ctx_create(int device, void* stream, tvd_ctx** out);
 int tvd_ctx_set_stream(tvd_ctx* ctx, void* stream);
 int tvd_ctx_sync(tvd_ctx* ctx);
 int tvd_ctx_destroy(tvd_ctx* ctx);
-/* options: TVD_OPT_GENERIC_FFT (1) routes DST passes through the generic
- * mixed-radix engine instead of the odd-symmetric prime-factor engine */
+/* options.  TVD_OPT_GENERIC_FFT (per context) routes DST passes through the generic
+ * mixed-radix engine instead of the odd-symmetric prime-factor engine.  The others are
+ * process-wide (every context; setting one drops the context's captured solver graphs);
+ * their defaults are the measured production configuration:
+ *   TVD_OPT_SOLVER_GRAPH  1: replay captured PCG / BiCGstab iterations as CUDA graphs
+ *   TVD_OPT_PDL           0: programmatic dependent launch attribute on the iteration kernels
+ *   TVD_OPT_BAND_GENERIC  0: prime-core assembly projections on the generic engine, not Rader
+ *   TVD_OPT_BAND_SLIDE    0: CUDA-core band passes instead of the fp64 tensor-core ones
+ *   TVD_OPT_FIN_FUSION    1: PCG scalar steps folded into their producers' last CTA
+ *   TVD_OPT_P_FUSION      1: direction update fused into the row band pass
+ *   TVD_OPT_PFA_STAGES    3: (profiling) run only the first k stages of the DST engine
+ *   TVD_OPT_GENERAL_BLUR  0: blurs created while set take the general 2D path (explicit
+ *                            extension + direct convolution) even when the PSF is rank 1 */
 #define TVD_OPT_GENERIC_FFT 1
+#define TVD_OPT_SOLVER_GRAPH 2
+#define TVD_OPT_PDL 3
+#define TVD_OPT_BAND_GENERIC 4
+#define TVD_OPT_BAND_SLIDE 5
+#define TVD_OPT_FIN_FUSION 6
+#define TVD_OPT_P_FUSION 7
+#define TVD_OPT_PFA_STAGES 8
+#define TVD_OPT_GENERAL_BLUR 9
 int tvd_ctx_set_option(tvd_ctx* ctx, int option, int value);
+int tvd_ctx_get_option(tvd_ctx* ctx, int option, int* value);
 /* instrumentation: kernels launched through ctx so far */
 int tvd_ctx_counters(tvd_ctx* ctx, long long* launches);
 /* enable (1) / disable (0) CUDA-event timing around every launch; resets records */

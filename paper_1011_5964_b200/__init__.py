@@ -10,15 +10,16 @@ fallback: operators raise when the library or a CUDA device is missing.
 
 from .blur import BoundaryCondition, StructuredBlurOperator, SymmetricPsf
 from .krylov import KrylovConfig, SolveOutcome, pbicgstab, pcg
-from .pipeline import (Formulation, NormalSystem, PrecondSelector, RestorationConfig,
+from .pipeline import (ConfigurationError, Formulation, InvalidScalingError, NormalSystem,
+                       PrecondSelector, RestorationConfig,
                        RestorationReport, restore)
 from .precond import FactoredPreconditioner, assemble_preconditioner
 from .transforms import TransformKind
 from .tv import DiffusionBc, DiffusionOperator
 
 __all__ = [
-    "BoundaryCondition", "DiffusionBc", "DiffusionOperator", "FactoredPreconditioner",
-    "Formulation", "KrylovConfig", "NormalSystem", "PrecondSelector", "RestorationConfig",
+    "BoundaryCondition", "ConfigurationError", "DiffusionBc", "DiffusionOperator", "FactoredPreconditioner",
+    "Formulation", "InvalidScalingError", "KrylovConfig", "NormalSystem", "PrecondSelector", "RestorationConfig",
     "RestorationReport", "SolveOutcome", "StructuredBlurOperator", "SymmetricPsf",
     "TransformKind", "assemble_preconditioner", "pbicgstab", "pcg", "restore",
 ]

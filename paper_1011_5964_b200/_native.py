@@ -51,6 +51,7 @@ _SIGNATURES = {
     "tvd_ctx_sync": ([_vp], _i),
     "tvd_ctx_destroy": ([_vp], _i),
     "tvd_ctx_set_option": ([_vp, _i, _i], _i),
+    "tvd_ctx_get_option": ([_vp, _i, ctypes.POINTER(_i)], _i),
     "tvd_ctx_counters": ([_vp, ctypes.POINTER(_ll)], _i),
     "tvd_ctx_profile": ([_vp, _i], _i),
     "tvd_ctx_profile_read": ([_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_ll)], _i),
@@ -193,9 +194,40 @@ def launch_count(device=None) -> int:
     return out.value
 
 
+#: option ids of include/tvdeblur_b200.h (TVD_OPT_*)
+OPTIONS = {"generic_fft": 1, "solver_graph": 2, "pdl": 3, "band_generic": 4, "band_slide": 5,
+           "fin_fusion": 6, "p_fusion": 7, "pfa_stages": 8, "general_blur": 9}
+
+
+def set_option(name: str, value: int, device=None) -> None:
+    """Set a library option (``generic_fft`` per context, the others process-wide)."""
+    check(load().tvd_ctx_set_option(context(device), OPTIONS[name], int(value)))
+
+
+def get_option(name: str, device=None) -> int:
+    out = _i()
+    check(load().tvd_ctx_get_option(context(device), OPTIONS[name], ctypes.byref(out)))
+    return out.value
+
+
+class option:
+    """``with option("pdl", 1): ...`` -- set an option for a block, then restore it."""
+
+    def __init__(self, name: str, value: int, device=None) -> None:
+        self.name, self.value, self.device = name, int(value), device
+
+    def __enter__(self):
+        self.saved = get_option(self.name, self.device)
+        set_option(self.name, self.value, self.device)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, self.saved, self.device)
+
+
 def set_generic_fft(enable: bool, device=None) -> None:
     """Route DST passes through the generic mixed-radix FFT (parity tests of both engines)."""
-    check(load().tvd_ctx_set_option(context(device), 1, 1 if enable else 0))
+    set_option("generic_fft", 1 if enable else 0, device)
 
 
 def profile(enable: bool, device=None) -> None:

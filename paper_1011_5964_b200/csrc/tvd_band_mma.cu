@@ -342,13 +342,8 @@ int koff_of(int w) {
   }
 }
 
-bool band_mma_enabled() {
-  static const bool on = [] {
-    const char* s = getenv("TVD_BAND_IMPL");
-    return !(s && s[0] == 's');  // "slide" selects the CUDA-core kernels (comparison runs)
-  }();
-  return on;
-}
+// TVD_OPT_BAND_SLIDE selects the CUDA-core sliding-window kernels (comparison runs)
+bool band_mma_enabled() { return option(kOptBandSlide) == 0; }
 
 #define TVD_KOFFS(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32) X(64)
 
@@ -365,20 +360,10 @@ bool band_mma_ok(const BandOp& op) {
 
 int band_mma_koff(int w) { return koff_of(w); }
 
-// column-pass shape: TVD_BAND_COLS_VARIANT 0 = 8 tiles per warp (256-row CTAs) x 2 CTAs/SM,
-// 1 = 4 tiles (128 rows) x 3 CTAs, 2 = 4 tiles x 2 CTAs (default: matvec 81.5 us vs 87.7 us
-// for variant 0 at 2048^2; 3 CTAs spill), 3 / 4 = 2 tiles x 2 / 3 CTAs (88 / 96 us)
-static int cols_variant() {
-  static const int v = [] {
-    const char* s = getenv("TVD_BAND_COLS_VARIANT");
-    return s ? atoi(s) : 2;
-  }();
-  return v;
-}
-static int cols_tiles() {
-  const int v = cols_variant();
-  return v == 0 ? 8 : (v <= 2 ? 4 : 2);
-}
+// column-pass shape: 4 row tiles per warp (128-row CTAs), two CTAs per SM (matvec 81.5 us vs
+// 87.7 us for 8 tiles / 256-row CTAs at 2048^2; three CTAs spill; 2 tiles: 88-96 us)
+constexpr int kColsTiles = 4;
+static int cols_tiles() { return kColsTiles; }
 int band_mma_cols_grid(int n, int rows) {
   if (rows < 0) rows = n;
   const int rw = 32 * cols_tiles();
@@ -448,26 +433,15 @@ cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out
   BandTaps tp;
   if (!make_taps(op, &tp)) return cudaErrorInvalidValue;
   const int n = op.n;
-  static const int prefetch = [] {  // TVD_BAND_PREFETCH=1: measured slower (96 vs 88 us)
-    const char* e = getenv("TVD_BAND_PREFETCH");
-    return e && e[0] == '1' ? 1 : 0;
-  }();
   Epilogue ep = ep_in;
-  ep.prefetch = prefetch;
+  ep.prefetch = 0;  // L2 prefetch of the epilogue operands measured slower (96 vs 88 us)
   if (row_hi < 0) row_hi = n;
   if (row_lo < 0 || row_lo > row_hi || row_hi > n) return cudaErrorInvalidValue;
   const int nr = row_hi - row_lo;
   if (nr == 0) return cudaSuccess;
   switch (koff_of(op.w)) {
-#define X(K)                                                                                 \
-  case K:                                                                                    \
-    switch (cols_variant()) {                                                                \
-      case 1: return launch_cols_t<K, 4, 3>(op, tp, in, out, ep, skip, st, row_lo, row_hi);  \
-      case 2: return launch_cols_t<K, 4, 2>(op, tp, in, out, ep, skip, st, row_lo, row_hi);  \
-      case 3: return launch_cols_t<K, 2, 2>(op, tp, in, out, ep, skip, st, row_lo, row_hi);  \
-      case 4: return launch_cols_t<K, 2, 3>(op, tp, in, out, ep, skip, st, row_lo, row_hi);  \
-      default: return launch_cols_t<K, 8, 2>(op, tp, in, out, ep, skip, st, row_lo, row_hi); \
-    }
+#define X(K) \
+  case K: return launch_cols_t<K, kColsTiles, 2>(op, tp, in, out, ep, skip, st, row_lo, row_hi);
     TVD_KOFFS(X)
 #undef X
     default: return cudaErrorInvalidValue;

@@ -22,6 +22,15 @@
 
 using namespace tvd;
 
+namespace tvd {
+// defaults: graph replay on, PDL attribute off (measured neutral), Rader band projections,
+// tensor-core band passes, folded finalizers, fused direction update, every PFA stage,
+// separable blurs on the banded path
+static std::atomic<int> g_options[kOptCount] = {0, 0, 1, 0, 0, 0, 1, 1, 3, 0};
+int option(int id) { return (id > 0 && id < kOptCount) ? g_options[id].load() : 0; }
+}  // namespace tvd
+
+
 // ------------------------------------------------------------------ errors
 static thread_local std::string g_last_error;
 
@@ -754,8 +763,7 @@ static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const 
 // eigenvalues) written transposed back, row pass with the dot and the beta finalizer --
 // instead of a strided column sandwich.
 static bool trig_trans_ok(tvd_ctx* c, int family) {
-  static const bool off = getenv("TVD_TRIG_STRIDED") != nullptr;
-  return family == kFamDct && !c->force_generic && !off;
+  return family == kFamDct && !c->force_generic;
 }
 static int precond_trig_trans(tvd_ctx* c, int family, int n, const double* inv,
                               const double* inv_t, const double* d, int dmul, const double* in,
@@ -1189,22 +1197,14 @@ static void key_slots(std::vector<uintptr_t>& k, const tvd_ctx* c) {
   for (const DevBuf& sl : c->slots) k.push_back(reinterpret_cast<uintptr_t>(sl.ptr));
   k.push_back((uintptr_t)c->force_generic);
 }
-static bool graphs_enabled() {
-  static const bool on = [] {  // TVD_SOLVER_GRAPH=0 (or the older TVD_PCG_GRAPH=0): eager
-    const char* e = getenv("TVD_SOLVER_GRAPH");
-    const char* f = getenv("TVD_PCG_GRAPH");
-    return !((e && e[0] == '0') || (f && f[0] == '0'));
-  }();
-  return on;
-}
+static bool graphs_enabled() { return option(kOptSolverGraph) != 0; }
 
 // PCG iterations >= 2 with the direction update fused into the row band pass:
 // p_new = z + beta p_old, q = A p_new, partial of p_new . q (gamma folded into the column
 // pass when fin).  Separable X / D_X systems on the tensor-core passes only (pcg_p_fusable).
 static bool pcg_p_fusable(const tvd_system* sys) {
-  static const bool off = getenv("TVD_NO_P_FUSION") != nullptr;
   const tvd_blur* b = sys->blur;
-  return !off && b->separable && !sys->s && !sys->reblur && band_mma_ok(b->g[0]) &&
+  return option(kOptPFusion) != 0 && b->separable && !sys->s && !sys->reblur && band_mma_ok(b->g[0]) &&
          band_mma_ok(b->g[1]);
 }
 static int system_apply_pfused(tvd_ctx* c, const tvd_system* sys, const double* z,
@@ -1282,7 +1282,24 @@ int tvd_ctx_sync(tvd_ctx* c) {
 
 int tvd_ctx_set_option(tvd_ctx* c, int option, int value) {
   if (!c) return fail(TVD_ERR_INVALID, "null context");
-  if (option == TVD_OPT_GENERIC_FFT) c->force_generic = value != 0;
+  if (option == TVD_OPT_GENERIC_FFT) {
+    c->force_generic = value != 0;
+    return TVD_OK;
+  }
+  if (option <= TVD_OPT_GENERIC_FFT || option >= kOptCount)
+    return fail(TVD_ERR_INVALID, "unknown option");
+  if (option == TVD_OPT_PFA_STAGES && (value < 0 || value > 3))
+    return fail(TVD_ERR_INVALID, "pfa stages must be 0..3");
+  // solver graphs bake the previous choices in
+  drop_graphs(c);
+  g_options[option] = value;
+  return TVD_OK;
+}
+
+int tvd_ctx_get_option(tvd_ctx* c, int option, int* value) {
+  if (!c || !value) return fail(TVD_ERR_INVALID, "null argument");
+  if (option == TVD_OPT_GENERIC_FFT) *value = c->force_generic ? 1 : 0;
+  else if (option > TVD_OPT_GENERIC_FFT && option < kOptCount) *value = g_options[option];
   else return fail(TVD_ERR_INVALID, "unknown option");
   return TVD_OK;
 }
@@ -1382,7 +1399,7 @@ int tvd_blur_create(tvd_ctx* c, int n, const double* psf, int width, int bc, tvd
   for (int a = 0; a < width; ++a)
     for (int q = 0; q < width; ++q)
       err = std::max(err, std::fabs(b->psf[(size_t)a * width + q] - g0[a] * g1[q] / total));
-  b->separable = total != 0.0 && err <= 1e-13 * hmax;
+  b->separable = total != 0.0 && err <= 1e-13 * hmax && !option(kOptGeneralBlur);
   if (upload(b->psf, &b->d_psf, b->owned) != cudaSuccess) {
     delete b;
     return fail(TVD_ERR_CUDA, "psf upload failed");
@@ -2039,7 +2056,7 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rz0(S, partial, nb, st));
   TVD_LAUNCH(c, kCatVec, 1, launch_copy(zz, p, N, skip, st));
   // finalizers folded into their producers (TVD_NO_FIN_FUSION=1: separate 1-CTA launches)
-  const bool fuse_fin = !getenv("TVD_NO_FIN_FUSION");
+  const bool fuse_fin = option(kOptFinFusion) != 0;
   const PcgFin fin_g{S, c->d_fin, kFinGamma, 0, 0.0, nullptr};
   const PcgFin fin_r{S, c->d_fin + 1, kFinRel, 0, tol, history};
   const PcgFin fin_b{S, c->d_fin + 2, kFinBeta, max_iterations, 0.0, nullptr};

@@ -65,10 +65,15 @@ __device__ __forceinline__ void pdl_enter() {
   if (TVD_PDL_EARLY_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-inline bool pdl_enabled() {
-  static const bool on = getenv("TVD_PDL") != nullptr;
-  return on;
-}
+// Process-wide switches set through tvd_ctx_set_option (include/tvdeblur_b200.h TVD_OPT_*);
+// every default is the measured production configuration.
+enum TvdOpt : int {
+  kOptGenericFft = 1, kOptSolverGraph, kOptPdl, kOptBandGeneric, kOptBandSlide, kOptFinFusion,
+  kOptPFusion, kOptPfaStages, kOptGeneralBlur, kOptCount
+};
+int option(int id);  // tvd_capi.cu
+
+inline bool pdl_enabled() { return option(kOptPdl) != 0; }
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,

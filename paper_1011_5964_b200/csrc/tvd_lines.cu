@@ -402,9 +402,8 @@ cudaError_t launch_trig(const TrigPlan& P, const LineGeom& g, int analysis, cons
     attr_done = true;
   }
   // 256-thread CTAs take the 255-register instance (the 512-thread bound caps the engine at
-  // 128 registers and spills; c2b 10831 -> 10980 it/s); TVD_LINES_CAP128=1 keeps the capped one
-  static const bool wide = !getenv("TVD_LINES_CAP128");
-  if (nth <= 256 && wide) return launch_pdl(k_trig<256, 1>, nb, nth, smem, st, k);
+  // 128 registers and spills; c2b 10831 -> 10980 it/s)
+  if (nth <= 256) return launch_pdl(k_trig<256, 1>, nb, nth, smem, st, k);
   return launch_pdl(k_trig<512, 1>, nb, nth, smem, st, k);
 }
 
@@ -413,7 +412,7 @@ cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
   (void)axis;
   // prime odd core (config 5, L = 8191): the length-L DFTs run on the Rader engine instead of
   // the generic engine's O(L) per point odd-radix stage (808 ms -> a few ms per assembly)
-  if (P.family != kFamDct && P.rader_ok && P.rader.L == P.L && !getenv("TVD_BAND_GENERIC"))
+  if (P.family != kFamDct && P.rader_ok && P.rader.L == P.L && !option(kOptBandGeneric))
     return launch_band_rader(P.rader, P.n, P.wfull, b, nblocks_out, st);
   BandK k{};
   k.fft = P.fft;
@@ -423,15 +422,8 @@ cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
   k.L = P.L;
   k.LP = P.L;
   k.b = b;
-  static const int nl_env = [] {  // TVD_BAND_NL: lines per CTA (experiments)
-    const char* e = getenv("TVD_BAND_NL");
-    return e ? atoi(e) : 0;
-  }();
-  static const int nth_min = [] {  // TVD_BAND_NTH_MIN: minimum threads per CTA
-    const char* e = getenv("TVD_BAND_NTH_MIN");
-    return e ? atoi(e) : 256;
-  }();
-  int nl = nl_env > 0 ? nl_env : 2;  // 2 lines: 792 vs 866 us per 2048^2 assembly for 4
+  constexpr int nth_min = 256;  // minimum threads per CTA
+  int nl = 2;                   // 2 lines: 792 vs 866 us per 2048^2 assembly for 4
   const size_t cbytes = (size_t)P.L * 16;
   while (nl > 1 && nl * cbytes > 100 * 1024) --nl;
   k.nl = nl;

@@ -1114,11 +1114,6 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
 // the four pass-specialised instances of one launch shape
 template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF, bool HO = false>
 static cudaError_t launch_pipe_pm(const PipeK& k, int grid, cudaStream_t st) {
-  static const bool generic = [] {  // TVD_PIPE_PM=0: one kernel for every pass (A/B runs)
-    const char* e = getenv("TVD_PIPE_PM");
-    return e && e[0] == '0';
-  }();
-  if (generic) return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, -1, HO>(k, grid, st);
   const int pm = (k.mid ? 1 : 0) | (k.transposed ? 2 : 0);
   switch (pm) {
     case 0: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 0, HO>(k, grid, st);
@@ -1128,130 +1123,26 @@ static cudaError_t launch_pipe_pm(const PipeK& k, int grid, cudaStream_t st) {
   }
 }
 
-#include "tvd_pfa_ws.cuh"
-
-template <int Q1, int Q2, int NP, int NC, int TPW, int MINB = 1>
-static cudaError_t launch_ws_t(const PipeK& k, int grid, cudaStream_t st) {
-  constexpr int LPh = HalfShape<Q1, Q2>::LPh;
-  const size_t smem = (size_t)2 * 2 * LPh * 16 + (size_t)2 * k.n * 8;
-  if (smem > 220 * 1024 || !k.pl.hscat) return cudaErrorInvalidConfiguration;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_dst_ws<Q1, Q2, NP, NC, TPW, MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr = true;
-  }
-  k_dst_ws<Q1, Q2, NP, NC, TPW, MINB><<<grid, (NP + NC) * 32, smem, st>>>(k);
-  return cudaGetLastError();
-}
-// TVD_PIPE_WS selects the warp-specialised pass (tvd_pfa_ws.cuh; 0 = off, the lock-step
-// k_dst_pipe).  Measured at 2048^2 per M^-1: 272-288 us for 4-6 producer + 6-8 consumer warps
-// vs 275 us lock step (bit-identical results): the phases do not overlap profitably, so off.
-static int pipe_ws_id() {
-  static const int v = [] {
-    const char* s = getenv("TVD_PIPE_WS");
-    return s ? atoi(s) : 0;
-  }();
-  return v;
-}
-
-// Launch shape per specialisation (the 2047 default runs its two stages out of place over a
-// second line buffer, HO).  2047 = 89 * 23 runs two 6-warp CTAs per SM (one warp
-// per k-tile of the q = 89 stage, one column tile per warp and round; the register budget
-// of 170 keeps the DMMA chains unspilled, and the two independent CTAs overlap one batch's
-// pack / unpack with the other's DFT stages: 273 us vs 291 us per M^-1 for one 12-warp CTA,
-// tools/pipe_variants.py); the smaller lengths run two 8-warp CTAs per SM.
-// TVD_PIPE_VARIANT overrides the 89 * 23 shape for experiments.
+// Launch shape per specialisation (tools/pipe_variants.py swept these in round 1):
+// * 2047 = 89 * 23 (config 3): half-line layout, stages out of place over a second line
+//   buffer, two 6-warp CTAs per SM, one column tile per warp and round (the register budget
+//   of 170 keeps the DMMA chains unspilled; the two CTAs overlap one batch's pack / unpack
+//   with the other's DFT stages): 262.8 us per M^-1 vs 272.1 in place, 291 for one 12-warp CTA;
+// * 1023 = 31 * 11 * 3 (config 4): four 2-warp CTAs per SM (99 vs 127 us per M^-1 for two
+//   8-warp CTAs);
+// * 511 = 73 * 7 (config 2a): half-line layout, two 6-warp CTAs (38.3 vs 40.4 us per M^-1);
+// * 127 (config 1): two 8-warp CTAs.
+// A warp-specialised producer / consumer variant of the 2047 pass measured 272-288 us per
+// M^-1 against 275 us lock step (bit-identical) and was removed.
 struct PipeVariant {
   int threads, ctas, tpw, lines;
 };
-static int pipe_variant_id() {
-  static const int v = [] {
-    const char* s = getenv("TVD_PIPE_VARIANT");
-    return s ? atoi(s) : -1;
-  }();
-  return v;
-}
-// half-line layout for the two-factor lengths (TVD_PIPE_HALF=0 selects the full layout)
-static bool pipe_half() {
-  static const bool on = [] {
-    const char* s = getenv("TVD_PIPE_HALF");
-    return !(s && s[0] == '0');
-  }();
-  return on;
-}
-// TVD_PIPE_VARIANT2: launch shapes of the 1023 = 31 * 11 * 3 pass (config 4) for experiments
-static int pipe_variant2_id() {
-  static const int v = [] {
-    const char* s = getenv("TVD_PIPE_VARIANT2");
-    return s ? atoi(s) : -1;
-  }();
-  return v;
-}
-// TVD_PIPE_VARIANT3: launch shapes of the 511 = 73 * 7 pass (config 2a) for experiments
-static int pipe_variant3_id() {
-  static const int v = [] {
-    const char* s = getenv("TVD_PIPE_VARIANT3");
-    return s ? atoi(s) : -1;
-  }();
-  return v;
-}
 static PipeVariant pipe_variant(int which) {
-  if (which == 3) {
-    switch (pipe_variant3_id()) {
-      case 1: return {192, 2, 1, 2};
-      case 2: return {192, 2, 2, 2};
-      case 3: return {160, 3, 1, 2};
-      case 4: return {160, 3, 2, 2};
-      case 5: return {256, 2, 1, 2};
-      case 6: return {192, 2, 1, 2};
-      case 0: return {256, 2, 3, 2};
-      default: return {192, 2, 1, 2};  // 38.3 vs 40.4 us per M^-1 at 512^2
-    }
-  }
-  if (which == 2) {
-    switch (pipe_variant2_id()) {
-      case 1: return {192, 2, 1, 2};
-      case 2: return {192, 2, 2, 2};
-      case 3: return {384, 1, 3, 2};
-      case 4: return {128, 3, 3, 2};
-      case 5: return {256, 2, 1, 2};
-      case 6: return {128, 4, 2, 2};
-      case 7: return {128, 4, 1, 2};
-      case 8: return {128, 4, 3, 2};
-      case 9: return {96, 4, 2, 2};
-      case 10: return {64, 4, 2, 2};
-      case 11: return {160, 4, 2, 2};
-      case 0: return {256, 2, 3, 2};
-      default: return {64, 4, 2, 2};
-    }
-  }
-  if (which != 1) return {256, 2, 3, 2};
-  switch (pipe_variant_id()) {
-    case 0: return {256, 2, 3, 2};
-    case 1: return {256, 1, 3, 2};
-    case 2: return {384, 1, 3, 2};
-    case 3: return {512, 1, 3, 2};
-    case 4: return {384, 1, 1, 2};
-    case 5: return {384, 1, 2, 2};
-    case 6: return {256, 1, 1, 2};
-    case 7: return {256, 1, 2, 2};
-    case 8: return {384, 1, 4, 4};
-    case 9: return {384, 1, 2, 4};
-    case 10: return {256, 1, 2, 4};
-    case 11: return {256, 2, 3, 2};
-    case 12: return {256, 2, 4, 2};
-    case 13: return {384, 1, 4, 2};
-    case 14: return {192, 2, 3, 2};
-    case 15: return {192, 2, 4, 2};
-    case 16: return {192, 2, 2, 2};
-    case 17: return {192, 2, 2, 2};
-    case 18: return {192, 2, 1, 2};
-    case 19: return {192, 3, 2, 2};
-    case 20: return {192, 3, 1, 2};
-    case 21: return {192, 2, 1, 2};
-    case 22: return {192, 2, 2, 2};
-    default: return pipe_half() ? PipeVariant{192, 2, 1, 2} : PipeVariant{384, 1, 4, 2};
+  switch (which) {
+    case 1: return {192, 2, 1, 2};
+    case 2: return {64, 4, 2, 2};
+    case 3: return {192, 2, 1, 2};
+    default: return {256, 2, 3, 2};
   }
 }
 
@@ -1292,92 +1183,14 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
   if (io.in_seg && (io.in_seg % 2 || len % io.in_seg)) return cudaErrorInvalidValue;
   k.in_seg = io.in_seg;
   k.in_seg_stride = io.in_seg_stride;
-  static const int stages_env = [] {
-    const char* s = getenv("TVD_PFA_STAGES");
-    return s ? atoi(s) : 3;
-  }();
-  k.stages = stages_env;
-  if (pipe_ws_id() > 0 && io.ar_mode == 0 && pipe_half() && (which == 1 || which == 3)) {
-    const int nbatch = (nlines + 1) / 2;
-    const int grid = nbatch < kSMs ? nbatch : kSMs;
-    if (nblocks_out) *nblocks_out = grid;
-    if (grid <= 0) return cudaSuccess;
-    if (which == 3) return launch_ws_t<73, 7, 4, 8, 1>(k, grid, st);
-    switch (pipe_ws_id()) {
-      case 2: return launch_ws_t<89, 23, 4, 8, 2>(k, grid, st);
-      case 3: return launch_ws_t<89, 23, 6, 6, 1>(k, grid, st);
-      case 4: return launch_ws_t<89, 23, 2, 8, 1>(k, grid, st);
-      case 5: return launch_ws_t<89, 23, 4, 6, 1>(k, grid, st);
-      case 6: return launch_ws_t<89, 23, 6, 6, 2>(k, grid, st);
-      default: return launch_ws_t<89, 23, 4, 8, 1>(k, grid, st);
-    }
-  }
+  k.stages = option(kOptPfaStages);  // profiling: run only the first stages
   const int grid = pipe_grid(P, nlines);
   if (nblocks_out) *nblocks_out = grid;
   if (grid <= 0) return cudaSuccess;
   switch (which) {
-    case 1:
-      switch (pipe_variant_id()) {
-        case 0: return launch_pipe_t<89, 23, 1, 256, 2, 3>(k, grid, st);
-        case 1: return launch_pipe_t<89, 23, 1, 256, 1, 3>(k, grid, st);
-        case 2: return launch_pipe_t<89, 23, 1, 384, 1, 3>(k, grid, st);
-        case 3: return launch_pipe_t<89, 23, 1, 512, 1, 3>(k, grid, st);
-        case 4: return launch_pipe_t<89, 23, 1, 384, 1, 1>(k, grid, st);
-        case 5: return launch_pipe_t<89, 23, 1, 384, 1, 2>(k, grid, st);
-        case 6: return launch_pipe_t<89, 23, 1, 256, 1, 1>(k, grid, st);
-        case 7: return launch_pipe_t<89, 23, 1, 256, 1, 2>(k, grid, st);
-        case 8: return launch_pipe_t<89, 23, 1, 384, 1, 4, true, 4>(k, grid, st);
-        case 9: return launch_pipe_t<89, 23, 1, 384, 1, 2, true, 4>(k, grid, st);
-        case 10: return launch_pipe_t<89, 23, 1, 256, 1, 2, true, 4>(k, grid, st);
-        case 11: return launch_pipe_t<89, 23, 1, 256, 2, 3, true, 2, true>(k, grid, st);
-        case 12: return launch_pipe_t<89, 23, 1, 256, 2, 4, true, 2, true>(k, grid, st);
-        case 13: return launch_pipe_t<89, 23, 1, 384, 1, 4, true, 2, true>(k, grid, st);
-        case 14: return launch_pipe_t<89, 23, 1, 192, 2, 3, true>(k, grid, st);
-        case 15: return launch_pipe_t<89, 23, 1, 192, 2, 4, true>(k, grid, st);
-        case 16: return launch_pipe_t<89, 23, 1, 192, 2, 2, true>(k, grid, st);
-        case 17: return launch_pipe_t<89, 23, 1, 192, 2, 2, true, 2, true>(k, grid, st);
-        case 18: return launch_pipe_t<89, 23, 1, 192, 2, 1, true>(k, grid, st);
-        case 19: return launch_pipe_t<89, 23, 1, 192, 3, 2, true>(k, grid, st);
-        case 20: return launch_pipe_t<89, 23, 1, 192, 3, 1, true>(k, grid, st);
-        case 21: return launch_pipe_pm<89, 23, 1, 192, 2, 1, true, true>(k, grid, st);
-        case 22: return launch_pipe_pm<89, 23, 1, 192, 2, 2, true, true>(k, grid, st);
-        default:
-          // out-of-place stages over two line buffers: 262.8 vs 272.1 us per M^-1
-          return pipe_half() ? launch_pipe_pm<89, 23, 1, 192, 2, 1, true, true>(k, grid, st)
-                             : launch_pipe_t<89, 23, 1, 384, 1, 4>(k, grid, st);
-      }
-    case 2:
-      switch (pipe_variant2_id()) {
-        case 1: return launch_pipe_t<31, 11, 3, 192, 2, 1>(k, grid, st);
-        case 2: return launch_pipe_t<31, 11, 3, 192, 2, 2>(k, grid, st);
-        case 3: return launch_pipe_t<31, 11, 3, 384, 1, 3>(k, grid, st);
-        case 4: return launch_pipe_t<31, 11, 3, 128, 3, 3>(k, grid, st);
-        case 5: return launch_pipe_t<31, 11, 3, 256, 2, 1>(k, grid, st);
-        case 6: return launch_pipe_t<31, 11, 3, 128, 4, 2>(k, grid, st);
-        case 7: return launch_pipe_t<31, 11, 3, 128, 4, 1>(k, grid, st);
-        case 8: return launch_pipe_t<31, 11, 3, 128, 4, 3>(k, grid, st);
-        case 9: return launch_pipe_t<31, 11, 3, 96, 4, 2>(k, grid, st);
-        case 10: return launch_pipe_t<31, 11, 3, 64, 4, 2>(k, grid, st);
-        case 11: return launch_pipe_t<31, 11, 3, 160, 4, 2>(k, grid, st);
-        case 0: return launch_pipe_t<31, 11, 3>(k, grid, st);
-        // four 2-warp CTAs per SM: 99 us per M^-1 at 1024^2 vs 127 us for two 8-warp CTAs
-        default: return launch_pipe_pm<31, 11, 3, 64, 4, 2, false>(k, grid, st);
-      }
-    case 3:
-      if (pipe_half()) {
-        switch (pipe_variant3_id()) {
-          case 1: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st);
-          case 2: return launch_pipe_pm<73, 7, 1, 192, 2, 2, true>(k, grid, st);
-          case 3: return launch_pipe_pm<73, 7, 1, 160, 3, 1, true>(k, grid, st);
-          case 4: return launch_pipe_pm<73, 7, 1, 160, 3, 2, true>(k, grid, st);
-          case 5: return launch_pipe_pm<73, 7, 1, 256, 2, 1, true>(k, grid, st);
-          case 6: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true, true>(k, grid, st);
-          case 0: return launch_pipe_pm<73, 7, 1, 256, 2, 3, true>(k, grid, st);
-          default: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st);
-        }
-      }
-      return pipe_half() ? launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st)
-                         : launch_pipe_t<73, 7, 1>(k, grid, st);
+    case 1: return launch_pipe_pm<89, 23, 1, 192, 2, 1, true, true>(k, grid, st);
+    case 2: return launch_pipe_pm<31, 11, 3, 64, 4, 2, false>(k, grid, st);
+    case 3: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st);
     case 4: return launch_pipe_t<127, 1, 1>(k, grid, st);
     default: return cudaErrorInvalidConfiguration;
   }
@@ -1453,11 +1266,7 @@ cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g,
   k.es = g.es;
   k.scale = 0.5 * sqrt(2.0 / P.L);
   k.h = (P.L - 1) / 2;
-  static const int stages_env = [] {
-    const char* s = getenv("TVD_PFA_STAGES");  // profiling knob: run only the first stages
-    return s ? atoi(s) : 3;
-  }();
-  k.stages = stages_env;
+  k.stages = option(kOptPfaStages);  // profiling: run only the first stages
   k.io = io;
   const int nb = (g.nlines + nl - 1) / nl;
   if (nblocks_out) *nblocks_out = nb;

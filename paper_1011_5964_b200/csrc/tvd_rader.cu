@@ -517,8 +517,7 @@ cudaError_t launch_rader_rows(const RaderPlan& P, int family, int len, int nline
   }
   if (nblocks_out) *nblocks_out = nlines;
   if (nlines == 0) return cudaSuccess;
-  static const bool full = getenv("TVD_RADER_FULL") != nullptr;  // A/B: full-length engine
-  if (!full && P.H == 4095 && P.psi) {
+  if (P.H == 4095 && P.psi) {  // negacyclic half-length engine (the full one: 11.5 vs 7.75 ms)
     k.scale = 0.5 * sqrt(2.0 / (P.M + 1)) / P.H;
     const size_t smem_h = (size_t)(P.H + RaderStages<4095>::kScratch) * sizeof(double2);
     static bool attr_h = false;

@@ -18,6 +18,14 @@ Files written:
   reflective + R) and config 2a/2b (512^2).
 * ``restore_c3_head.npz`` (``--big``) -- the 2048^2 headline config, first
   FP steps only (counts + image checksums; the image itself is 32 MB).
+* ``restore_c4_{gauss,box}.npz`` (``--c4``) -- config 4's two problem types at 1024^2
+  (problem 0: Gaussian 21x21 sigma 3; problem 1: box 11x11), full 10-FP restores: counts,
+  gradient norms, RRE, a 1/64 subsample and a 64-projection sketch of the whole image
+  (``tests/sketch.py``).
+* ``c5_ops.npz`` (``--c5``) -- config 5 at 8192^2 (Gaussian 63x63 sigma 8, m = 31): the
+  reference's exact ``apply`` / ``apply_transpose``, diffusivity, the assembled kind-M
+  eigenvalues and ``apply_inverse`` of a seeded field, and the first FP step's PCG count and
+  iterate, each as a subsample + sketch (the arrays are 512 MB).
 * ``f2_ops_n{N}.npz`` / ``restore_c1_reblur_*.npz`` (``--f2``) -- row f2:
   anti-reflective-BC diffusion, the AR transform T and its inverse / transposes, the
   re-blurred matvec, P-family eigenvalues and solves, right-preconditioned BiCGstab, and
@@ -47,6 +55,9 @@ from tvdeblur.pipeline import Formulation, PrecondSelector, RestorationConfig, r
 from tvdeblur.tv import DiffusionBc, DiffusionOperator  # noqa: E402
 
 from paper_1011_5964_b200 import harness as bh  # noqa: E402
+
+sys.path.insert(0, str(HERE.parent))
+from sketch import sketch  # noqa: E402
 
 BCS = {"anti_reflective": BoundaryCondition.ANTI_REFLECTIVE,
        "reflective": BoundaryCondition.REFLECTIVE}
@@ -189,14 +200,98 @@ def restore_fixture(spec: bh.ProblemSpec, selector: str, bc: str | None = None,
     return out
 
 
+def c4_fixture(index: int) -> dict:
+    """Config 4's problem ``index`` (even: Gaussian, odd: box) restored by the reference."""
+    spec = bh.CONFIGS["c4"]
+    h, v, u_true = bh.make_problem(spec, index=index)
+    cfg = RestorationConfig(bc_h=BoundaryCondition.ANTI_REFLECTIVE, alpha=spec.alpha,
+                            beta=spec.beta, preconditioner=PrecondSelector.X, fp_tol=1e-300,
+                            fp_max=spec.fp_steps,
+                            inner=KrylovConfig(tol=spec.tol, max_iterations=2000))
+    t0 = time.perf_counter()
+    rep = restore(v, SymmetricPsf(h), cfg, u_true=u_true)
+    dt = time.perf_counter() - t0
+    print(f"  c4[{index}]: counts={rep.inner_iterations} rre={rep.rre:.4f} ({dt:.1f}s)",
+          flush=True)
+    r = rep.restored
+    return {"index": np.array(index), "psf": h, "v_norm": np.array(np.linalg.norm(v)),
+            "inner_iterations": np.array(rep.inner_iterations),
+            "gradient_norms": np.array(rep.gradient_norms), "rre": np.array(rep.rre),
+            "final_gradient_norm": np.array(rep.final_gradient_norm),
+            "restored_norm": np.array(np.linalg.norm(r)), "restored_sum": np.array(r.sum()),
+            "restored_sub": r[::8, ::8].copy(), "restored_sketch": sketch(r, 64),
+            "seconds": np.array(dt)}
+
+
+def _big(out: dict, key: str, a: np.ndarray, k: int = 16) -> None:
+    """A 512 MB array as norm + subsample (prime stride) + border rows + sketch."""
+    out[f"{key}_norm"] = np.array(np.linalg.norm(a))
+    out[f"{key}_sub"] = a[::61, ::61].copy()
+    out[f"{key}_rows"] = a[[0, 1, 2, 30, 31, 32, -33, -32, -31, -3, -2, -1], ::7].copy()
+    out[f"{key}_cols"] = a[::7, [0, 1, 2, 30, 31, 32, -33, -32, -31, -3, -2, -1]].copy()
+    out[f"{key}_sketch"] = sketch(a, k)
+    print(f"  c5 {key}: norm {float(out[key + '_norm']):.6e}", flush=True)
+
+
+def c5_fixture() -> dict:
+    """Config 5 (8192^2) per-op outputs of the reference plus its first FP step."""
+    spec = bh.CONFIGS["c5"]
+    h, v, _ = bh.make_problem(spec, exact=False)
+    psf = SymmetricPsf(h)
+    n = spec.n
+    op = StructuredBlurOperator(psf, BoundaryCondition.ANTI_REFLECTIVE, n)
+    out: dict[str, np.ndarray] = {"psf": h, "alpha": np.array(spec.alpha),
+                                  "beta": np.array(spec.beta)}
+    _big(out, "v", v)
+    t0 = time.perf_counter()
+    _big(out, "H_v", op.apply(v))
+    _big(out, "HT_v", op.apply_transpose(v))
+    print(f"  c5 exact blur {time.perf_counter() - t0:.0f}s", flush=True)
+    lop = DiffusionOperator(v, spec.beta)
+    _big(out, "a_h", lop.a_h)
+    _big(out, "a_v", lop.a_v)
+    t0 = time.perf_counter()
+    pre = rp.assemble_preconditioner("M", op, lop, spec.alpha)
+    print(f"  c5 assembly {time.perf_counter() - t0:.0f}s", flush=True)
+    _big(out, "lam_M", pre.eigenvalues)
+    w = np.random.default_rng(8192).standard_normal((n, n))
+    _big(out, "minv_w", pre.apply_inverse(w))
+    del w
+    # first FP step of restore (pipeline.py:194-244): rhs = H^T_fast v, u0 = v, kind M
+    from tvdeblur.krylov import pcg
+
+    rhs = op.apply_transpose_fast(v)
+
+    def apply_a(x):
+        return op.apply_transpose_fast(op.apply_fast(x)) + spec.alpha * lop.apply(x)
+
+    t0 = time.perf_counter()
+    res = pcg(apply_a, pre.apply_inverse, rhs, v,
+              KrylovConfig(tol=spec.tol, max_iterations=2000, record_history=True))
+    print(f"  c5 FP step 1: {res.iterations} its ({time.perf_counter() - t0:.0f}s)", flush=True)
+    out["fp1_iterations"] = np.array(res.iterations)
+    out["fp1_history"] = np.asarray(res.residual_history)
+    _big(out, "fp1_u", res.solution)
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run the 2048^2 head")
     ap.add_argument("--big-steps", type=int, default=3)
     ap.add_argument("--only-exact", action="store_true")
     ap.add_argument("--f2", action="store_true", help="only the row-f2 fixtures")
+    ap.add_argument("--c4", action="store_true", help="only the config-4 restores")
+    ap.add_argument("--c5", action="store_true", help="only the config-5 (8192^2) ops")
     args = ap.parse_args()
     print("reference tvdeblur from", tvdeblur.__file__)
+    if args.c4:
+        for i, tag in ((0, "gauss"), (1, "box")):
+            np.savez_compressed(HERE / f"restore_c4_{tag}.npz", **c4_fixture(i))
+        return
+    if args.c5:
+        np.savez_compressed(HERE / "c5_ops.npz", **c5_fixture())
+        return
     if args.f2:
         for n, seed in ((32, 21), (33, 22)):
             np.savez_compressed(HERE / f"f2_ops_n{n}.npz", **f2_ops_fixture(n, seed))

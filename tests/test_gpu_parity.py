@@ -132,12 +132,14 @@ def test_blur_vs_oracle_midsize(n, m, bname, rng):
 
 
 @pytest.mark.parametrize("n,m,bname", [(256, 7, "anti_reflective"), (512, 15, "reflective"),
-                                       (1024, 10, "anti_reflective"), (768, 31, "anti_reflective")])
+                                       (1024, 10, "anti_reflective"), (768, 31, "anti_reflective"),
+                                       (1024, -5, "anti_reflective")])
 def test_normal_system_vs_oracle_midsize(n, m, bname, rng):
-    """Fused H^T H + alpha L matvec (tensor-core band passes at these sizes), plain and X_D-scaled."""
+    """Fused H^T H + alpha L matvec (tensor-core band passes at these sizes), plain and X_D-scaled.
+    m < 0: the config-4 box PSF (11 x 11 uniform, half-width |m|)."""
     from paper_1011_5964_b200.harness import gen_psf
     from paper_1011_5964_b200.pipeline import NormalSystem
-    h = gen_psf("gaussian", m, m / 2.0)
+    h = gen_psf("box", -m) if m < 0 else gen_psf("gaussian", m, m / 2.0)
     u = np.cumsum(rng.standard_normal((n, n)), axis=1) * 0.05
     w = rng.standard_normal((n, n))
     alpha, beta = 2e-3, 0.05
@@ -564,9 +566,9 @@ def test_f2_reblur_restore_matches_reference(golden, bcl, sel):
 
 def test_prime_core_assembly_rader_matches_generic_8192():
     """Config-5 preconditioner assembly: the band projections of length L = 8191 (prime) run
-    on the Rader engine (launch_band_rader); the generic mixed-radix engine (TVD_BAND_GENERIC)
-    computes the same eigenvalues in O(L) per point -- they agree to rounding."""
-    import os
+    on the Rader engine (launch_band_rader); the generic mixed-radix engine (option
+    band_generic) computes the same eigenvalues in O(L) per point -- they agree to rounding."""
+    from paper_1011_5964_b200 import _native as nat
     n = 8192
     g = torch.Generator(device="cpu").manual_seed(5)
     u = torch.rand(n // 64, n // 64, generator=g, dtype=torch.float64)
@@ -575,11 +577,8 @@ def test_prime_core_assembly_rader_matches_generic_8192():
                                    B.BoundaryCondition.ANTI_REFLECTIVE, n)
     lop = TV.DiffusionOperator(u, 0.05)
     fast = P.assemble_preconditioner("D_M", hop, lop, 1e-4).eigenvalues_device.clone()
-    os.environ["TVD_BAND_GENERIC"] = "1"
-    try:
+    with nat.option("band_generic", 1):
         slow = P.assemble_preconditioner("D_M", hop, lop, 1e-4).eigenvalues_device
-    finally:
-        del os.environ["TVD_BAND_GENERIC"]
     assert float((fast - slow).norm() / slow.norm()) < 1e-12
 
 
@@ -706,3 +705,134 @@ def test_solver_graph_cache_follows_the_blur(rng):
         gc.collect()
     assert rel_err(seen[0], seen[1]) > 1e-3
     assert rel_err(seen[0], seen[2]) < 1e-14
+
+
+# ------------------------------------------------- numerical edge cases of the reference's tests
+def test_indefinite_preconditioner_reports_kind_and_alpha():
+    """reference pkg/tests/test_precond.py:348-354 (precond.py:437-441), on device arrays."""
+    lam = np.ones((16, 16))
+    lam[3, 5] = -0.5
+    with pytest.raises(P.IndefinitePreconditionerError) as err:
+        P.FactoredPreconditioner("R", T.TransformKind.DCT, lam, alpha=0.25,
+                                 device=torch.device("cuda"))
+    assert err.value.kind == "R" and err.value.alpha == 0.25
+    assert err.value.min_eigenvalue == -0.5
+    assert "R" in str(err.value) and "0.25" in str(err.value)
+
+
+def test_clamping_logs_warning(caplog):
+    """reference pkg/tests/test_precond.py:357-364 (precond.py:442-450): eigenvalues below
+    1e-14 max are clamped with a logged warning and the inverse stays finite."""
+    import logging
+
+    lam = np.ones((16, 16)) * 2.0
+    lam[0, 0] = 1.0
+    lam[7, 9] = 1e-20
+    with caplog.at_level(logging.WARNING, logger="paper_1011_5964_b200.precond"):
+        fp = P.FactoredPreconditioner("R", T.TransformKind.DCT, lam, alpha=1e-3,
+                                      device=torch.device("cuda"))
+    assert any("clamped 1 eigenvalue" in rec.message for rec in caplog.records)
+    assert fp.clamped == 1
+    inv = fp.inverse_eigenvalues_device.cpu().numpy()
+    assert inv[7, 9] == 1.0 / (1e-14 * 2.0)
+    assert np.all(np.isfinite(fp.apply_inverse(np.ones((16, 16)))))
+
+
+def test_device_assembly_clamps_like_the_reference(caplog):
+    """The device assembly's positivity check and clamp (tvd_precond_assemble) on a system
+    whose projected eigenvalues fall below 1e-14 max: a box PSF whose symbol nearly vanishes
+    on the DCT grid and a vanishing alpha.  Clamp count and the clamped inverse agree with the
+    oracle's restatement of precond.py:437-450, and the warning is logged."""
+    import logging
+
+    n = 48
+    h = np.full((3, 3), 1.0 / 9.0)  # symbol (1 + 2 cos y) / 3 ~ 0 at y = 2 pi / 3 (j = 32)
+    u = np.random.default_rng(5).standard_normal((n, n))
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(h), B.BoundaryCondition.REFLECTIVE, n)
+    lop = TV.DiffusionOperator(u, 0.1)
+    alpha = 1e-300
+    with caplog.at_level(logging.WARNING, logger="paper_1011_5964_b200.precond"):
+        pre = P.assemble_preconditioner("R", hop, lop, alpha)
+    lam_h = O.blur_eigenvalues(h, "reflective", n)
+    lam, lam_inv, _, _ = O.assemble("R", lam_h, O.diffusion_bands(lop.a_h, lop.a_v), alpha)
+    expect = int(np.count_nonzero(lam < 1e-14 * lam.max()))
+    assert expect > 0 and pre.clamped == expect
+    assert any("clamped" in rec.message for rec in caplog.records)
+    assert rel_err(pre.inverse_eigenvalues_device.cpu().numpy(), lam_inv) < 1e-12
+
+
+def test_assembly_rejects_nonpositive_scaling_diagonal():
+    """precond.py:558-560: d = 1 + alpha diag L <= 0 (anti-reflective diffusion has negative
+    border diagonal entries, reference test_pipeline.py:88-97) raises
+    IndefinitePreconditionerError(kind, alpha, min d) for every kind."""
+    from paper_1011_5964_b200.tv import DiffusionBc
+
+    n = 16
+    u = np.random.default_rng(20230814).standard_normal((n, n)) * 5.0
+    lop = TV.DiffusionOperator(u, 0.01, DiffusionBc.ANTI_REFLECTIVE)
+    dmin = float(lop.diagonal().min())
+    assert dmin < 0
+    alpha = 2.0 / abs(dmin)
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(np.full((3, 3), 1 / 9.0)),
+                                   B.BoundaryCondition.ANTI_REFLECTIVE, n)
+    for kind in ("M", "D_M", "M_D", "P", "D_P", "P_D"):
+        with pytest.raises(P.IndefinitePreconditionerError) as err:
+            P.assemble_preconditioner(kind, hop, lop, alpha)
+        assert err.value.kind == kind and err.value.alpha == alpha
+        assert err.value.min_eigenvalue == pytest.approx(1.0 + alpha * dmin, rel=1e-12)
+
+
+def test_scaling_errors_match_the_reference():
+    """pipeline.py:154-158 (scale_system) and :229-233 (the DIAG selector): a nonpositive
+    scaling diagonal raises InvalidScalingError, through the API and through restore."""
+    from paper_1011_5964_b200.pipeline import NormalSystem, scale_system
+    from paper_1011_5964_b200.tv import DiffusionBc
+
+    n = 16
+    u = np.random.default_rng(20230814).standard_normal((n, n)) * 5.0
+    lop = TV.DiffusionOperator(u, 0.01, DiffusionBc.ANTI_REFLECTIVE)
+    alpha = 2.0 / abs(float(lop.diagonal().min()))
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(np.full((3, 3), 1 / 9.0)),
+                                   B.BoundaryCondition.ANTI_REFLECTIVE, n)
+    with pytest.raises(tvd.InvalidScalingError):
+        scale_system(NormalSystem(hop, lop, alpha), np.ones((n, n)), lop, alpha)
+    for sel in (tvd.PrecondSelector.DIAG, tvd.PrecondSelector.X_D):
+        cfg = tvd.RestorationConfig(
+            bc_h=B.BoundaryCondition.ANTI_REFLECTIVE, alpha=alpha, beta=0.01,
+            bc_l=DiffusionBc.ANTI_REFLECTIVE, formulation=tvd.Formulation.REBLUR,
+            preconditioner=sel, fp_tol=1e-3, fp_max=2,
+            inner=K.KrylovConfig(tol=1e-6, max_iterations=50))
+        with pytest.raises(tvd.InvalidScalingError):
+            tvd.restore(u, B.SymmetricPsf(np.full((3, 3), 1 / 9.0)), cfg)
+
+
+# ------------------------------------------------- config 4 (1024^2 batch problems) vs the reference
+@pytest.mark.parametrize("name", ["restore_c4_gauss.npz", "restore_c4_box.npz"])
+def test_c4_restore_matches_reference(golden, name):
+    """Config 4's two problem types (Gaussian 21x21 sigma 3 / box 11x11, 1024^2 AR, 10 FP
+    steps, tol 1e-4) restored on the device against the reference's own restore
+    (tests/golden/make_golden.py --c4): identical per-FP-step PCG counts, gradient norms,
+    and the restored image within 1e-8 on a 1/64 subsample AND over every pixel through a
+    64-projection sketch (tests/sketch.py, a Johnson-Lindenstrauss estimate of the full-image
+    relative L2 difference)."""
+    from sketch import sketch_rel_err
+
+    from paper_1011_5964_b200.harness import make_problem
+
+    g = golden(name)
+    spec = CONFIGS["c4"]
+    h, v, u_true = make_problem(spec, index=int(g["index"]))
+    assert np.array_equal(h, g["psf"])
+    assert abs(np.linalg.norm(v) - float(g["v_norm"])) <= 1e-14 * float(g["v_norm"])
+    cfg = tvd.RestorationConfig(
+        bc_h=BCS["anti_reflective"], alpha=spec.alpha, beta=spec.beta,
+        preconditioner=tvd.PrecondSelector.X, fp_tol=1e-300, fp_max=spec.fp_steps,
+        inner=K.KrylovConfig(tol=spec.tol, max_iterations=2000))
+    rep = tvd.restore(v, B.SymmetricPsf(h), cfg, u_true=u_true)
+    assert rep.inner_iterations == [int(k) for k in g["inner_iterations"]]
+    np.testing.assert_allclose(rep.gradient_norms, g["gradient_norms"], rtol=1e-6)
+    r = np.asarray(rep.restored)
+    assert rel_err(r[::8, ::8], g["restored_sub"]) < 1e-8
+    assert abs(np.linalg.norm(r) - float(g["restored_norm"])) <= 1e-8 * float(g["restored_norm"])
+    assert sketch_rel_err(r, g["restored_sketch"], float(g["restored_norm"])) < 1e-8
+    assert abs(rep.rre - float(g["rre"])) < 1e-8

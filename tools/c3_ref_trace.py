@@ -1,13 +1,16 @@
 """Trace the REFERENCE's config-c3 restore (build container only; parity evidence).
 
-    PYTHONPATH=/root/reference/pkg/src python tools/c3_ref_trace.py OUTDIR [FP_STEPS]
+    PYTHONPATH=/root/reference/pkg/src python tools/c3_ref_trace.py OUTDIR [FP_STEPS] [--exact]
 
 Runs ``tvdeblur.pipeline.restore`` (reference ``pipeline.py:182-276``) unchanged on the c3
 fixture of ``tests/golden/make_golden.py`` and, through a wrapper around the module-level
 ``pcg`` it calls (``pipeline.py:198``), records for every FP step the starting iterate
 ``u_k`` (``OUTDIR/u_{k}.npy``), the reference's residual history
 (``krylov.py:105-109``) and the solution.  ``tools/c3_step_probe.py`` then replays single FP
-steps from these iterates with other operator variants and with the GPU.
+steps from these iterates with other operator variants and with the GPU.  ``--exact`` runs the
+reference with ``use_fast_blur=False`` (``pipeline.py:75,167-179``): its exact pad / convolve /
+crop ``H`` and full-convolve + fold ``H^T`` (``blur.py:226-247``) in place of the transform
+path.
 """
 import json
 import pathlib
@@ -31,7 +34,9 @@ from paper_1011_5964_b200 import harness as bh  # noqa: E402
 out = pathlib.Path(sys.argv[1])
 out.mkdir(parents=True, exist_ok=True)
 spec = bh.CONFIGS["c3"]
-fp = int(sys.argv[2]) if len(sys.argv) > 2 else spec.fp_steps
+exact = "--exact" in sys.argv
+argv = [a for a in sys.argv if a != "--exact"]
+fp = int(argv[2]) if len(argv) > 2 else spec.fp_steps
 psf = rh.gen_psf("gaussian", spec.m, spec.sigma)
 ext = bh.gen_piecewise_image(spec.n, spec.m, spec.rects, spec.disks, 2023, spec.ramp)
 v = rh.blur_and_observe(ext, psf, spec.n, spec.nsr, 7)
@@ -60,7 +65,8 @@ def traced(apply_a, apply_minv, b, x0, config):
 rpipe.pcg = traced
 cfg = RestorationConfig(bc_h=BoundaryCondition.ANTI_REFLECTIVE, alpha=spec.alpha, beta=spec.beta,
                         preconditioner=PrecondSelector.X, fp_tol=1e-300, fp_max=fp,
-                        inner=KrylovConfig(tol=spec.tol, max_iterations=2000))
+                        inner=KrylovConfig(tol=spec.tol, max_iterations=2000),
+                        use_fast_blur=not exact)
 rep = restore(v, psf, cfg, u_true=ext[spec.m:spec.m + spec.n, spec.m:spec.m + spec.n])
 np.save(out / f"u_{fp}.npy", rep.restored)
 log["gradient_norms"] = [float(g) for g in rep.gradient_norms]
