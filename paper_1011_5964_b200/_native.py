@@ -196,7 +196,8 @@ def launch_count(device=None) -> int:
 
 #: option ids of include/tvdeblur_b200.h (TVD_OPT_*)
 OPTIONS = {"generic_fft": 1, "solver_graph": 2, "pdl": 3, "band_generic": 4, "band_slide": 5,
-           "fin_fusion": 6, "p_fusion": 7, "pfa_stages": 8, "general_blur": 9}
+           "fin_fusion": 6, "p_fusion": 7, "pfa_stages": 8, "general_blur": 9,
+           "band_prefetch": 10}
 
 
 def set_option(name: str, value: int, device=None) -> None:

@@ -42,6 +42,9 @@ __device__ __forceinline__ void cp_commit_wait() {
 __device__ __forceinline__ void prefetch_l2(const double* p) {
   if (p) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
+__device__ __forceinline__ void prefetch_l1(const double* p) {
+  if (p) asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p));
+}
 
 struct BandTaps {
   double t[64];  // t[k] = symmetric interior tap at offset +-k
@@ -185,23 +188,28 @@ __global__ void __launch_bounds__(256, MINB) k_bmma_cols(BandOp op, BandTaps tp,
   const int n = op.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ib = row_lo + blockIdx.y * SH::RW, j0 = blockIdx.x * SH::CC;
   // The epilogue's operands (a_h, a_v, lw and the extra streams) are read long after the
-  // tile: pull their rows into L2 now so those loads hit L2 instead of waiting on DRAM.
+  // tile: option band_prefetch pulls their lines into L2 (1) or L1 (2) before the tile load.
   if (ep.prefetch) {
+    auto pf = [&](const double* q) {
+      if (ep.prefetch == 2) prefetch_l1(q);
+      else prefetch_l2(q);
+    };
     for (int i = tid; i < SH::RW + 2; i += blockDim.x) {
       const int row = ib - 1 + i;
       if (row < 0 || row >= n || row > row_hi) continue;
       const int c0 = j0 > 0 ? j0 - 1 : 0;
-      prefetch_l2(ep.lw ? ep.lw + (long)row * n + c0 : nullptr);
-      prefetch_l2(ep.lw ? ep.lw + (long)row * n + min(j0 + SH::CC, n - 1) : nullptr);
+      pf(ep.lw ? ep.lw + (long)row * n + c0 : nullptr);
+      pf(ep.lw ? ep.lw + (long)row * n + j0 : nullptr);
+      pf(ep.lw ? ep.lw + (long)row * n + min(j0 + SH::CC, n - 1) : nullptr);
       if (row >= ib && row < row_hi) {
-        prefetch_l2(ep.a_h ? ep.a_h + (long)row * (n + 1) + j0 : nullptr);
-        prefetch_l2(ep.a_h ? ep.a_h + (long)row * (n + 1) + j0 + SH::CC : nullptr);
-        prefetch_l2(ep.a_v ? ep.a_v + (long)row * n + j0 : nullptr);
-        prefetch_l2(ep.a_v ? ep.a_v + (long)row * n + j0 + SH::CC - 1 : nullptr);
-        if (ep.s) prefetch_l2(ep.s + (long)row * n + j0);
-        if (ep.dot_with && ep.dot_with != ep.lw) prefetch_l2(ep.dot_with + (long)row * n + j0);
+        pf(ep.a_h ? ep.a_h + (long)row * (n + 1) + j0 : nullptr);
+        pf(ep.a_h ? ep.a_h + (long)row * (n + 1) + j0 + SH::CC : nullptr);
+        pf(ep.a_v ? ep.a_v + (long)row * n + j0 : nullptr);
+        pf(ep.a_v ? ep.a_v + (long)row * n + j0 + SH::CC - 1 : nullptr);
+        if (ep.s) pf(ep.s + (long)row * n + j0);
+        if (ep.dot_with && ep.dot_with != ep.lw) pf(ep.dot_with + (long)row * n + j0);
       }
-      if (row == row_hi && ep.a_v) prefetch_l2(ep.a_v + (long)row * n + j0);
+      if (row == row_hi && ep.a_v) pf(ep.a_v + (long)row * n + j0);
     }
   }
   for (int e = tid; e < SH::HEIGHT * C2; e += blockDim.x) {
@@ -434,7 +442,7 @@ cudaError_t launch_band_mma_cols(const BandOp& op, const double* in, double* out
   if (!make_taps(op, &tp)) return cudaErrorInvalidValue;
   const int n = op.n;
   Epilogue ep = ep_in;
-  ep.prefetch = 0;  // L2 prefetch of the epilogue operands measured slower (96 vs 88 us)
+  ep.prefetch = option(kOptBandPrefetch);  // 1: L2 (measured slower, 96 vs 88 us), 2: L1
   if (row_hi < 0) row_hi = n;
   if (row_lo < 0 || row_lo > row_hi || row_hi > n) return cudaErrorInvalidValue;
   const int nr = row_hi - row_lo;

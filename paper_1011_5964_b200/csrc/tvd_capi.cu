@@ -26,7 +26,7 @@ namespace tvd {
 // defaults: graph replay on, PDL attribute off (measured neutral), Rader band projections,
 // tensor-core band passes, folded finalizers, fused direction update, every PFA stage,
 // separable blurs on the banded path
-static std::atomic<int> g_options[kOptCount] = {0, 0, 1, 0, 0, 0, 1, 1, 3, 0};
+static std::atomic<int> g_options[kOptCount] = {0, 0, 1, 0, 0, 0, 1, 1, 3, 0, 0};
 int option(int id) { return (id > 0 && id < kOptCount) ? g_options[id].load() : 0; }
 }  // namespace tvd
 

@@ -707,7 +707,7 @@ __device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, uns
 // -1: read both from the parameters.  The specialised instances carry only their pass's code
 // (smaller kernels, fewer live registers, no dead branches).
 template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF = false, int BL = kPipeLines,
-          bool CSM = false, int PM = -1, bool HO = false>
+          bool CSM = false, int PM = -1, bool HO = false, int CO = 0>
 __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   pdl_enter();
   const bool has_mid = PM < 0 ? p.mid != nullptr : (PM & 1) != 0;
@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       issue(jb + 1);
     }
     if constexpr (HALF) {
-      half_transform<Q1, Q2, B, NT / 32, TPW, CSM, HO>(buf, p.pl, p.stages, csm, buf2);
+      half_transform<Q1, Q2, B, NT / 32, TPW, CSM, HO, CO>(buf, p.pl, p.stages, csm, buf2);
       res = buf;
     } else {
       res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
@@ -962,7 +962,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       for (int i = tid; i < B; i += nth) buf[i * LP] = make_double2(0.0, 0.0);
       __syncthreads();
       if constexpr (HALF) {
-        half_transform<Q1, Q2, B, NT / 32, TPW, CSM, HO>(buf, p.pl, p.stages, csm, buf2);
+        half_transform<Q1, Q2, B, NT / 32, TPW, CSM, HO, CO>(buf, p.pl, p.stages, csm, buf2);
         res = buf;
       } else {
         res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
@@ -1089,7 +1089,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 }
 
 template <int Q1, int Q2, int Q3, int NT = 256, int MINB = 2, int TPW = 3, bool HALF = false,
-          int BL = kPipeLines, bool CSM = false, int PM = -1, bool HO = false>
+          int BL = kPipeLines, bool CSM = false, int PM = -1, bool HO = false, int CO = 0>
 static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   using SH = PfaShape<Q1, Q2, Q3>;
   int reps = PfaStageC<SH, 0>::Rcnt;
@@ -1103,31 +1103,33 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   if (HALF && !k.pl.hscat) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM, HO>,
+    cudaFuncSetAttribute(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM, HO, CO>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  return launch_pdl(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM, HO>, grid, NT, smem,
+  return launch_pdl(k_dst_pipe<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, PM, HO, CO>, grid, NT, smem,
                     st, k);
 }
 
 // the four pass-specialised instances of one launch shape
-template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF, bool HO = false>
+template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF, bool HO = false,
+          int BL = kPipeLines, int CO = 0>
 static cudaError_t launch_pipe_pm(const PipeK& k, int grid, cudaStream_t st) {
   const int pm = (k.mid ? 1 : 0) | (k.transposed ? 2 : 0);
   switch (pm) {
-    case 0: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 0, HO>(k, grid, st);
-    case 1: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 1, HO>(k, grid, st);
-    case 2: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 2, HO>(k, grid, st);
-    default: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, kPipeLines, false, 3, HO>(k, grid, st);
+    case 0: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 0, HO, CO>(k, grid, st);
+    case 1: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 1, HO, CO>(k, grid, st);
+    case 2: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 2, HO, CO>(k, grid, st);
+    default: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 3, HO, CO>(k, grid, st);
   }
 }
 
 // Launch shape per specialisation (tools/pipe_variants.py swept these in round 1):
 // * 2047 = 89 * 23 (config 3): half-line layout, stages out of place over a second line
-//   buffer, two 6-warp CTAs per SM, one column tile per warp and round (the register budget
-//   of 170 keeps the DMMA chains unspilled; the two CTAs overlap one batch's pack / unpack
-//   with the other's DFT stages): 262.8 us per M^-1 vs 272.1 in place, 291 for one 12-warp CTA;
+//   buffer, two 6-warp CTAs per SM (the two CTAs overlap one batch's pack / unpack with the
+//   other's DFT stages), column-owner tensor-core stages (tvd_pfa_t.cuh half_stage_co):
+//   243.3 us per M^-1 vs 263.9 with k-tile-owner stages (bit-identical), 272.1 in place, 291
+//   for one 12-warp CTA; one line per batch or three CTAs per SM (spilling) measured slower;
 // * 1023 = 31 * 11 * 3 (config 4): four 2-warp CTAs per SM (99 vs 127 us per M^-1 for two
 //   8-warp CTAs);
 // * 511 = 73 * 7 (config 2a): half-line layout, two 6-warp CTAs (38.3 vs 40.4 us per M^-1);
@@ -1188,7 +1190,7 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
   if (nblocks_out) *nblocks_out = grid;
   if (grid <= 0) return cudaSuccess;
   switch (which) {
-    case 1: return launch_pipe_pm<89, 23, 1, 192, 2, 1, true, true>(k, grid, st);
+    case 1: return launch_pipe_pm<89, 23, 1, 192, 2, 1, true, true, 2, 2>(k, grid, st);
     case 2: return launch_pipe_pm<31, 11, 3, 64, 4, 2, false>(k, grid, st);
     case 3: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st);
     case 4: return launch_pipe_t<127, 1, 1>(k, grid, st);

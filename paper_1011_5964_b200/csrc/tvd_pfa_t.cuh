@@ -424,7 +424,79 @@ struct HalfStage {
 // (frees the 2 nrs registers of the stationary fragments)
 // OOP: read `buf`, write `dst` (a second line buffer): no in-place hazard, so the warps run
 // their rounds back to back without the two barriers per round, one barrier at the end.
-template <class ST, int NL, int NW, int TPWc, bool CSM = false, bool OOP = false>
+// CO: column-owner tensor-core stage (out of place only).  A warp owns one column tile (8
+// columns = 4 DFTs x re / im) and accumulates EVERY k-tile of it: per r-step it loads the data
+// fragment once, folds it, and issues 2 nkt DMMAs on nkt independent accumulator pairs with
+// the cos / sin fragments read through L1 -- the accumulator chains of a warp are independent,
+// so the DMMA latency (29 cycles) is hidden by the warp itself instead of by more warps, at
+// ~60 registers.  Every output's DMMA sequence (fragments, k-step order) is the k-tile-owner
+// stage's, so the results are bit-identical.
+template <class ST, int NL, int NW>
+__device__ __forceinline__ void half_stage_co(const double2* buf, const double* __restrict__ Cm,
+                                              const double* __restrict__ Sm, double2* out) {
+  constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LP;
+  constexpr bool PT = ST::partnered;
+  constexpr int ndft = NL * ST::Rcnt;
+  constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* bufd = reinterpret_cast<const double*>(buf);
+  const int coff = (lane >> 2) * ST::RP + (lane & 3);
+  for (int ct = warp; ct < nct; ct += NW) {
+    const int dB = min((ct * 8 + (lane >> 2)) >> 1, ndft - 1);
+    const int lB = dB / ST::Rcnt, tB = dB - lB * ST::Rcnt;
+    const double* p1 = bufd + 2 * (lB * LP + ST::base(tB)) + ((lane >> 2) & 1);
+    const double* p2 = bufd + 2 * (lB * LP + ST::partner(tB)) + ((lane >> 2) & 1);
+    double acc[nkt][4];
+#pragma unroll
+    for (int kt = 0; kt < nkt; ++kt) acc[kt][0] = acc[kt][1] = acc[kt][2] = acc[kt][3] = 0.0;
+#pragma unroll
+    for (int rs = 0; rs < nrs; ++rs) {
+      const int r = 1 + rs * 4 + (lane & 3);
+      const double x1 = p1[2 * r * st];
+      const double x2 = PT ? p2[2 * r * st] : p1[2 * (q - r) * st];
+      const double fa = PT ? x1 - x2 : x1 + x2;
+      const double fb = PT ? x1 + x2 : x1 - x2;
+#pragma unroll
+      for (int kt = 0; kt < nkt; ++kt) {
+        const int o = kt * 8 * ST::RP + coff + rs * 4;
+        dmma884(acc[kt][0], acc[kt][1], __ldg(Cm + o), fa);
+        dmma884(acc[kt][2], acc[kt][3], __ldg(Sm + o), fb);
+      }
+    }
+    const int dO = ct * 4 + (lane & 3);
+    if (dO < ndft) {
+      const int lO = dO / ST::Rcnt, tO = dO - lO * ST::Rcnt;
+      const int ob = lO * LP + ST::base(tO), on = lO * LP + ST::partner(tO);
+      const bool self = tO == 0;
+      const double2 x0 = buf[ob];
+      double2* p = out + ob;
+      double2* pn = out + on;
+#pragma unroll
+      for (int kt = 0; kt < nkt; ++kt) {
+        const int k = kt * 8 + (lane >> 2);
+        if (k <= H) {
+          const double a0 = acc[kt][0], a1 = acc[kt][1], b0 = acc[kt][2], b1 = acc[kt][3];
+          const double2 vk = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
+          const double2 vm = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
+          if (!PT) {
+            if (k == 0) {
+              p[0] = vk;
+            } else {
+              p[k * st] = vk;
+              p[(q - k) * st] = vm;
+            }
+          } else {
+            p[k] = vk;
+            if (!self) pn[k] = k == 0 ? make_double2(-vk.x, -vk.y) : make_double2(-vm.x, -vm.y);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <class ST, int NL, int NW, int TPWc, bool CSM = false, bool OOP = false, bool CO = false>
 __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const double* Sm,
                                            double2* dst = nullptr) {
   constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LP;
@@ -432,6 +504,10 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
   const int tid = threadIdx.x, nth = blockDim.x;
   constexpr int ndft = NL * ST::Rcnt;
   double2* const out = OOP ? dst : buf;
+  if constexpr (ST::mma && CO && OOP) {
+    half_stage_co<ST, NL, NW>(buf, Cm, Sm, dst);
+    return;
+  }
   if constexpr (ST::mma) {
     // A-stationary tensor-core stage (see pfa_stage_c): warp -> one k-tile x TPW column tiles
     constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;
@@ -630,7 +706,8 @@ struct HalfCoef {
   static constexpr int total = 2 * (n0 + n1);
 };
 
-template <int Q0, int Q1, int NL, int NW, int TPW, bool CSM = false, bool OOP = false>
+// CO: 0 = k-tile-owner tensor-core stages, 1 = column-owner wide stage (q = Q0), 2 = both
+template <int Q0, int Q1, int NL, int NW, int TPW, bool CSM = false, bool OOP = false, int CO = 0>
 __device__ __forceinline__ void half_transform(double2* buf, const PfaPlan& pl, int stages,
                                                const double* cs = nullptr,
                                                double2* buf2 = nullptr) {
@@ -640,10 +717,12 @@ __device__ __forceinline__ void half_transform(double2* buf, const PfaPlan& pl, 
   const double* c0 = CSM ? cs : pl.st[0].Cm;
   const double* s0 = CSM ? cs + HC::n0 : pl.st[0].Sm;
   // OOP: stage 0 buf -> buf2, stage 1 buf2 -> buf (the result lands in buf either way)
-  if (stages >= 1) half_stage<HalfStage<SH, 0>, NL, NW, TPW, CSM, OOP>(buf, c0, s0, buf2);
+  if (stages >= 1)
+    half_stage<HalfStage<SH, 0>, NL, NW, TPW, CSM, OOP, (CO >= 1)>(buf, c0, s0, buf2);
   if (stages >= 2) {
     if constexpr (OOP)
-      half_stage<HalfStage<SH, 1>, NL, NW, TPW, false, true>(buf2, pl.st[1].Cm, pl.st[1].Sm, buf);
+      half_stage<HalfStage<SH, 1>, NL, NW, TPW, false, true, (CO >= 2)>(buf2, pl.st[1].Cm,
+                                                                        pl.st[1].Sm, buf);
     else
       half_stage<HalfStage<SH, 1>, NL, NW, TPW>(buf, pl.st[1].Cm, pl.st[1].Sm);
   }
