@@ -369,9 +369,11 @@ def run_ours(args, rank: int, world: int) -> None:
             cur.wait_event(d2h_done[k % 2])  # outs_host[k % 2] drained (its step k - 2)
             ud, rd = dbuf[k % 2]
             l_op = tvd.DiffusionOperator(ud, spec.beta, device=dev)
-            p_op = tvd.assemble_preconditioner(kind, hop, l_op, spec.alpha)
+            # the assembly's checks stay on the device until the solve has synchronised
+            p_op = tvd.assemble_preconditioner(kind, hop, l_op, spec.alpha, defer_checks=True)
             res = tvd.pcg(tvd.NormalSystem(hop, l_op, spec.alpha), p_op.apply_inverse, rd, ud,
                           cfg)
+            p_op.check()
             comp_done[k % 2].record(cur)
             step_ev.append(torch.cuda.Event(enable_timing=True))
             step_ev[-1].record(cur)

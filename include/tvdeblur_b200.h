@@ -111,7 +111,10 @@ int tvd_ctx_destroy(tvd_ctx* ctx);
  *   TVD_OPT_P_FUSION      1: direction update fused into the row band pass
  *   TVD_OPT_PFA_STAGES    3: (profiling) run only the first k stages of the DST engine
  *   TVD_OPT_GENERAL_BLUR  0: blurs created while set take the general 2D path (explicit
- *                            extension + direct convolution) even when the PSF is rank 1 */
+ *                            extension + direct convolution) even when the PSF is rank 1
+ *   TVD_OPT_BAND_PREFETCH 0: column band pass prefetches its epilogue operands to L2 (1) / L1 (2)
+ *   TVD_OPT_SPLIT_X       0: PCG x update on a second stream, overlapping the M^-1 passes
+ *                            (bit-identical; measured no gain) */
 #define TVD_OPT_GENERIC_FFT 1
 #define TVD_OPT_SOLVER_GRAPH 2
 #define TVD_OPT_PDL 3
@@ -121,6 +124,8 @@ int tvd_ctx_destroy(tvd_ctx* ctx);
 #define TVD_OPT_P_FUSION 7
 #define TVD_OPT_PFA_STAGES 8
 #define TVD_OPT_GENERAL_BLUR 9
+#define TVD_OPT_BAND_PREFETCH 10
+#define TVD_OPT_SPLIT_X 11
 int tvd_ctx_set_option(tvd_ctx* ctx, int option, int value);
 int tvd_ctx_get_option(tvd_ctx* ctx, int option, int* value);
 /* instrumentation: kernels launched through ctx so far */
@@ -182,6 +187,15 @@ int tvd_precond_assemble(tvd_ctx* ctx, int family, int variant, int n, double al
                          const double* lam_h, const double* diag, const double* inner,
                          const double* block, double* eig, double* inv_eig, double* dvec,
                          double* min_eig, double* max_eig, long long* n_clamped);
+/* the same assembly with its checks left on the device (no host synchronisation): d_check
+ * (4 device doubles) receives [min(1 + alpha diag L), min eigenvalue, max eigenvalue, clamped
+ * count] in stream order; the caller reads it when it next synchronises (e.g. after the
+ * solve) and raises IndefinitePreconditionerError / logs the clamp warning then.  The
+ * eigenvalues and their clamped inverse are those of tvd_precond_assemble (same kernels). */
+int tvd_precond_assemble_async(tvd_ctx* ctx, int family, int variant, int n, double alpha,
+                               const double* lam_h, const double* diag, const double* inner,
+                               const double* block, double* eig, double* inv_eig, double* dvec,
+                               double* d_check);
 /* z = X (inv_eig .* X^T (r / d_sqrt)) / d_sqrt   (precond.py:456-477) */
 int tvd_precond_apply_inverse(tvd_ctx* ctx, int family, int n, const double* inv_eig,
                               const double* d_sqrt, const double* in, double* out);

@@ -71,6 +71,8 @@ _SIGNATURES = {
     "tvd_transform_2d": ([_vp, _i, _i, _vp, _vp, _i], _i),
     "tvd_precond_assemble": ([_vp, _i, _i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               ctypes.POINTER(_d), ctypes.POINTER(_d), ctypes.POINTER(_ll)], _i),
+    "tvd_precond_assemble_async": ([_vp, _i, _i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _vp], _i),
     "tvd_precond_apply_inverse": ([_vp, _i, _i, _vp, _vp, _vp, _vp], _i),
     "tvd_precond_apply": ([_vp, _i, _i, _vp, _vp, _vp, _vp], _i),
     "tvd_scaling": ([_vp, _ll, _d, _vp, _vp, _vp, _vp, ctypes.POINTER(_d)], _i),
@@ -197,7 +199,7 @@ def launch_count(device=None) -> int:
 #: option ids of include/tvdeblur_b200.h (TVD_OPT_*)
 OPTIONS = {"generic_fft": 1, "solver_graph": 2, "pdl": 3, "band_generic": 4, "band_slide": 5,
            "fin_fusion": 6, "p_fusion": 7, "pfa_stages": 8, "general_blur": 9,
-           "band_prefetch": 10}
+           "band_prefetch": 10, "split_x": 11}
 
 
 def set_option(name: str, value: int, device=None) -> None:

@@ -26,7 +26,7 @@ namespace tvd {
 // defaults: graph replay on, PDL attribute off (measured neutral), Rader band projections,
 // tensor-core band passes, folded finalizers, fused direction update, every PFA stage,
 // separable blurs on the banded path
-static std::atomic<int> g_options[kOptCount] = {0, 0, 1, 0, 0, 0, 1, 1, 3, 0, 0};
+static std::atomic<int> g_options[kOptCount] = {0, 0, 1, 0, 0, 0, 1, 1, 3, 0, 0, 0};
 int option(int id) { return (id > 0 && id < kOptCount) ? g_options[id].load() : 0; }
 }  // namespace tvd
 
@@ -114,6 +114,9 @@ struct tvd_ctx {
   };
   GraphCache pcg_graph, bicg_graph;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
+  // split PCG update: x += step p runs on `side`, forked after gamma, joined at iteration end
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 static void drop_graph(tvd_ctx::GraphCache& g) {
@@ -1362,6 +1365,9 @@ int tvd_ctx_destroy(tvd_ctx* c) {
   if (c->pcg_graph.exec) cudaGraphExecDestroy(c->pcg_graph.exec);
   if (c->bicg_graph.exec) cudaGraphExecDestroy(c->bicg_graph.exec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
   return TVD_OK;
 }
@@ -1701,10 +1707,15 @@ int tvd_scaling(tvd_ctx* c, long long count, double alpha, const double* diag, d
   return TVD_OK;
 }
 
-int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alpha,
-                         const double* lam_h, const double* diag, const double* inner,
-                         const double* block, double* eig, double* inv_eig, double* dvec,
-                         double* min_eig, double* max_eig, long long* n_clamped) {
+// The assembly (precond.py:516-573) with its checks either on the host (sync: min / max /
+// clamp count read back, errors returned) or on the device (d_check != nullptr: four
+// doubles [min(1 + alpha diag L), min lambda, max lambda, clamp count] written in stream
+// order, no host synchronisation; the caller reads them after its solve and raises there).
+static int precond_assemble_impl(tvd_ctx* c, int family, int variant, int n, double alpha,
+                                 const double* lam_h, const double* diag, const double* inner,
+                                 const double* block, double* eig, double* inv_eig, double* dvec,
+                                 double* min_eig, double* max_eig, long long* n_clamped,
+                                 double* d_check) {
   if (!c || !lam_h || !diag || !inner || !block || !eig || !inv_eig)
     return fail(TVD_ERR_INVALID, "null argument");
   if (family != TVD_TRANSFORM_SINE_HAT && family != TVD_TRANSFORM_DCT &&
@@ -1734,15 +1745,22 @@ int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alph
   } else if (variant == TVD_VARIANT_D_X) {
     dsq = dvec;
   }
-  double mind;
-  rc = tvd_scaling(c, N, alpha, diag, nullptr, dsq, s, &mind);
-  if (rc == TVD_ERR_SCALING) {
-    if (min_eig) *min_eig = mind;
-    return fail(TVD_ERR_PRECOND, "1 + alpha diag L has nonpositive entries");
+  if (d_check) {
+    double* part;
+    TVD_SLOT(c, kSlotPartial2, 2 * (size_t)n + 64 + vec_blocks(), part);
+    TVD_LAUNCH(c, kCatVec, 1, launch_scaling(diag, alpha, nullptr, dsq, s, N, part, vec_blocks(), c->stream));
+    TVD_LAUNCH(c, kCatFin, 1, launch_reduce_min(part, vec_blocks(), d_check, c->stream));
+  } else {
+    double mind;
+    rc = tvd_scaling(c, N, alpha, diag, nullptr, dsq, s, &mind);
+    if (rc == TVD_ERR_SCALING) {
+      if (min_eig) *min_eig = mind;
+      return fail(TVD_ERR_PRECOND, "1 + alpha diag L has nonpositive entries");
+    }
+    if (rc) return rc;
   }
-  if (rc) return rc;
   double* mm;
-  TVD_SLOT(c, kSlotPartial2, 2 * (size_t)n + 64, mm);
+  TVD_SLOT(c, kSlotPartial2, 2 * (size_t)n + 64 + vec_blocks(), mm);
   int nb = 0;
   if (variant == TVD_VARIANT_X_D) {
     double *lamd, *ds, *is, *bs;
@@ -1759,6 +1777,14 @@ int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alph
     rc = level2(c, P, n, diag, inner, block, eig, 1, lam_h, nullptr, alpha, mm, &nb, ar_c);
   }
   if (rc) return rc;
+  double* part;
+  TVD_SLOT(c, kSlotPartial, vec_blocks(), part);
+  if (d_check) {
+    TVD_LAUNCH(c, kCatFin, 1, launch_reduce_minmax(mm, nb, d_check + 1, d_check + 2, c->stream));
+    TVD_LAUNCH(c, kCatVec, 1, launch_invert_eigs_dev(eig, d_check + 2, inv_eig, N, part, c->stream));
+    TVD_LAUNCH(c, kCatFin, 1, launch_sum_partials(part, vec_blocks(), d_check + 3, c->stream));
+    return TVD_OK;
+  }
   double mn, mx;
   rc = host_minmax(c, mm, nb, &mn, &mx);
   if (rc) return rc;
@@ -1766,8 +1792,6 @@ int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alph
   if (max_eig) *max_eig = mx;
   if (!(mn > 0.0)) return fail(TVD_ERR_PRECOND, "preconditioner is indefinite");
   const double floor = 1e-14 * mx;
-  double* part;
-  TVD_SLOT(c, kSlotPartial, vec_blocks(), part);
   TVD_LAUNCH(c, kCatVec, 1, launch_invert_eigs(eig, floor, inv_eig, N, part, vec_blocks(), c->stream));
   std::vector<double> h(vec_blocks());
   TVD_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1777,6 +1801,23 @@ int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alph
   for (double v : h) cnt += v;
   if (n_clamped) *n_clamped = (long long)cnt;
   return TVD_OK;
+}
+
+int tvd_precond_assemble(tvd_ctx* c, int family, int variant, int n, double alpha,
+                         const double* lam_h, const double* diag, const double* inner,
+                         const double* block, double* eig, double* inv_eig, double* dvec,
+                         double* min_eig, double* max_eig, long long* n_clamped) {
+  return precond_assemble_impl(c, family, variant, n, alpha, lam_h, diag, inner, block, eig,
+                               inv_eig, dvec, min_eig, max_eig, n_clamped, nullptr);
+}
+
+int tvd_precond_assemble_async(tvd_ctx* c, int family, int variant, int n, double alpha,
+                               const double* lam_h, const double* diag, const double* inner,
+                               const double* block, double* eig, double* inv_eig, double* dvec,
+                               double* d_check) {
+  if (!d_check) return fail(TVD_ERR_INVALID, "null check buffer");
+  return precond_assemble_impl(c, family, variant, n, alpha, lam_h, diag, inner, block, eig,
+                               inv_eig, dvec, nullptr, nullptr, nullptr, d_check);
 }
 
 int tvd_precond_apply_inverse(tvd_ctx* c, int family, int n, const double* inv_eig,
@@ -2063,6 +2104,17 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
   // direction update fused into the next iteration's row band pass, p ping-ponging between
   // two buffers (the pass reads p_old halos of its neighbours while writing p_new)
   const bool pfuse = pcg_p_fusable(sys);
+  // option split_x: x += step p off the critical path, forked to a side stream once gamma is
+  // known and joined before the iteration's end (before the p update, which overwrites the p
+  // it reads).  Bit-identical, but measured 2650 vs 2673 PCG it/s at c3: the DST passes hold
+  // the whole register file (2 x 192 threads x 168 registers per SM), so the side kernel
+  // finds no room to run alongside them.  Off by default.
+  const bool split = option(kOptSplitX) != 0;
+  if (split && !c->side) {
+    TVD_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    TVD_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    TVD_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
   double* pb[2] = {p, nullptr};
   if (pfuse) TVD_SLOT(c, kSlotP2, N, pb[1]);
   // one PCG iteration (krylov.py:99-116) enqueued on the stream; every kernel skips once the
@@ -2083,7 +2135,16 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
     }
     if (rc2) return rc2;
     if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_gamma(S, partial, nbl, st));
-    if (fuse_fin) {
+    if (split) {
+      TVD_CUDA(cudaEventRecord(c->ev_fork, st));
+      TVD_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+      const cudaError_t ex = launch_pcg_update_x(S, x, pc, N, c->d_fin + 3, c->side);
+      if (ex != cudaSuccess) return fail(TVD_ERR_CUDA, std::string("pcg x update: ") + cudaGetErrorString(ex));
+      c->launches += 1;
+      TVD_CUDA(cudaEventRecord(c->ev_join, c->side));
+      TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_r(S, r, q, N, partial, st, fuse_fin ? &fin_r : nullptr));
+      if (!fuse_fin) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_rel(S, partial, vec_blocks(), tol, history, st));
+    } else if (fuse_fin) {
       TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_xr(S, x, r, pc, q, N, partial, vec_blocks(), st,
                                                      &fin_r));
     } else {
@@ -2094,6 +2155,7 @@ int tvd_pcg_solve(tvd_ctx* c, const tvd_system* sys, const tvd_precond* pre, con
                         fuse_fin ? &fin_b : nullptr, &fused);
     if (rc2) return rc2;
     if (!fused) TVD_LAUNCH(c, kCatFin, 1, launch_pcg_beta(S, partial, nbl, max_iterations, st));
+    if (split) TVD_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
     if (!pfuse) TVD_LAUNCH(c, kCatVec, 1, launch_pcg_update_p(S, p, zz, N, st));
     return TVD_OK;
   };

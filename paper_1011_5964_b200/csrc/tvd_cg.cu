@@ -48,6 +48,7 @@ __global__ void k_pcg_start(PcgState* s, const double* partial, int nb) {
     s->converged = 0;
     s->iters = 0;
     s->done = 0;
+    s->x_pending = 0;
     if (s->r0 == 0.0) {
       s->done = 1;
       s->iters = 0;
@@ -126,6 +127,83 @@ __global__ void k_pcg_update_xr(const PcgState* s, double* __restrict__ x, doubl
   const double t = block_sum(acc, red);
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
   if (fin.s) pcg_fin_tail(fin, partial, gridDim.x, red);  // stop test in the last CTA
+}
+
+__global__ void k_pcg_update_r(const PcgState* s, double* __restrict__ r,
+                               const double* __restrict__ q, long N, double* partial, PcgFin fin) {
+  pdl_enter();
+  if (s->done) return;
+  __shared__ double red[32];
+  const double step = s->step;
+  const long N2 = N >> 1, stride = (long)gridDim.x * blockDim.x;
+  double2* __restrict__ r2 = reinterpret_cast<double2*>(r);
+  const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q);
+  double acc = 0.0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < N2; i += 2 * stride) {
+    const long j = i + stride;
+    const bool two = j < N2;
+    const double2 ra = r2[i], qa = q2[i];
+    double2 rb = make_double2(0.0, 0.0), qb = rb;
+    if (two) {
+      rb = r2[j];
+      qb = q2[j];
+    }
+    const double2 va = make_double2(__dsub_rn(ra.x, __dmul_rn(step, qa.x)),
+                                    __dsub_rn(ra.y, __dmul_rn(step, qa.y)));
+    r2[i] = va;
+    acc += va.x * va.x;
+    acc += va.y * va.y;
+    if (two) {
+      const double2 vb = make_double2(__dsub_rn(rb.x, __dmul_rn(step, qb.x)),
+                                      __dsub_rn(rb.y, __dmul_rn(step, qb.y)));
+      r2[j] = vb;
+      acc += vb.x * vb.x;
+      acc += vb.y * vb.y;
+    }
+  }
+  if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long g = N - 1;
+    const double v = __dsub_rn(r[g], __dmul_rn(step, q[g]));
+    r[g] = v;
+    acc += v * v;
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  if (fin.s) pcg_fin_tail(fin, partial, gridDim.x, red);  // stop test in the last CTA
+}
+
+__global__ void k_pcg_update_x(PcgState* s, double* __restrict__ x, const double* __restrict__ p,
+                               long N, unsigned* counter) {
+  pdl_enter();
+  if (!s->x_pending) return;
+  const double step = s->step;
+  const long N2 = N >> 1, stride = (long)gridDim.x * blockDim.x;
+  double2* __restrict__ x2 = reinterpret_cast<double2*>(x);
+  const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p);
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < N2; i += 2 * stride) {
+    const long j = i + stride;
+    const bool two = j < N2;
+    const double2 xa = x2[i], pa = p2[i];
+    double2 xb = make_double2(0.0, 0.0), pb = xb;
+    if (two) {
+      xb = x2[j];
+      pb = p2[j];
+    }
+    x2[i] = make_double2(__dadd_rn(xa.x, __dmul_rn(step, pa.x)), __dadd_rn(xa.y, __dmul_rn(step, pa.y)));
+    if (two)
+      x2[j] = make_double2(__dadd_rn(xb.x, __dmul_rn(step, pb.x)), __dadd_rn(xb.y, __dmul_rn(step, pb.y)));
+  }
+  if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) x[N - 1] = __dadd_rn(x[N - 1], __dmul_rn(step, p[N - 1]));
+  // the last CTA to finish (every CTA has read x_pending) clears it
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    s->x_pending = 0;
+    *counter = 0u;
+  }
 }
 
 __global__ void k_pcg_rel(PcgState* s, const double* partial, int nb, double tol, double* hist) {
@@ -263,6 +341,60 @@ __global__ void k_invert_eigs(const double* __restrict__ lam, double floor, doub
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
 
+// device-side checks of the deferred assembly (tvd_precond_assemble_async): the scaling
+// diagonal's minimum, the eigenvalues' min / max (per-CTA pairs), the clamp floor read back
+// from device memory, and the clamp count
+__global__ void k_reduce_min(const double* partial_min, int nb, double* out) {
+  __shared__ double red[32];
+  double mn = 1.0 / 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) mn = fmin(mn, partial_min[i]);
+  for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mn = fmin(mn, red[w]);
+    *out = mn;
+  }
+}
+__global__ void k_reduce_minmax(const double* partial_mm, int nb, double* out_min, double* out_max) {
+  __shared__ double rmn[32], rmx[32];
+  double mn = 1.0 / 0.0, mx = -1.0 / 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    mn = fmin(mn, partial_mm[2 * i]);
+    mx = fmax(mx, partial_mm[2 * i + 1]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    rmn[threadIdx.x >> 5] = mn;
+    rmx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mn = fmin(mn, rmn[w]);
+      mx = fmax(mx, rmx[w]);
+    }
+    *out_min = mn;
+    *out_max = mx;
+  }
+}
+__global__ void k_invert_eigs_dev(const double* __restrict__ lam, const double* max_lam,
+                                  double* __restrict__ inv, long N, double* partial) {
+  __shared__ double red[32];
+  const double floor = 1e-14 * *max_lam;  // precond.py:442 (same rounding as the host's)
+  double cnt = 0.0;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N; g += (long)gridDim.x * blockDim.x) {
+    const double v = lam[g];
+    if (v < floor) cnt += 1.0;
+    inv[g] = __ddiv_rn(1.0, fmax(v, floor));
+  }
+  const double t = block_sum(cnt, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
 // ------------------------------------------------------------- launchers
 #define TVD_VEC_GRID kRedBlocks, kVecThreads, 0, st
 
@@ -294,6 +426,15 @@ cudaError_t launch_pcg_update_xr(PcgState* s, double* x, double* r, const double
                                  long N, double* partial, int, cudaStream_t st, const PcgFin* fin) {
   return launch_pdl(k_pcg_update_xr, kRedBlocks, kVecThreads, 0, st, s, x, r, p, q, N, partial,
                     fin ? *fin : PcgFin{});
+}
+cudaError_t launch_pcg_update_r(PcgState* s, double* r, const double* q, long N, double* partial,
+                                cudaStream_t st, const PcgFin* fin) {
+  return launch_pdl(k_pcg_update_r, kRedBlocks, kVecThreads, 0, st, s, r, q, N, partial,
+                    fin ? *fin : PcgFin{});
+}
+cudaError_t launch_pcg_update_x(PcgState* s, double* x, const double* p, long N, unsigned* counter,
+                                cudaStream_t st) {
+  return launch_pdl(k_pcg_update_x, kRedBlocks, kVecThreads, 0, st, s, x, p, N, counter);
 }
 cudaError_t launch_pcg_rel(PcgState* s, const double* partial, int nb, double tol, double* hist,
                            cudaStream_t st) {
@@ -342,6 +483,20 @@ cudaError_t launch_scale_bands(const double* diag, const double* inner, const do
 cudaError_t launch_invert_eigs(const double* lam, double floor, double* inv, long N, double* partial,
                                int, cudaStream_t st) {
   k_invert_eigs<<<TVD_VEC_GRID>>>(lam, floor, inv, N, partial);
+  return cudaGetLastError();
+}
+cudaError_t launch_invert_eigs_dev(const double* lam, const double* max_lam, double* inv, long N,
+                                   double* partial, cudaStream_t st) {
+  k_invert_eigs_dev<<<TVD_VEC_GRID>>>(lam, max_lam, inv, N, partial);
+  return cudaGetLastError();
+}
+cudaError_t launch_reduce_min(const double* partial_min, int nb, double* out, cudaStream_t st) {
+  k_reduce_min<<<1, 512, 0, st>>>(partial_min, nb, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_reduce_minmax(const double* partial_mm, int nb, double* out_min, double* out_max,
+                                 cudaStream_t st) {
+  k_reduce_minmax<<<1, 512, 0, st>>>(partial_mm, nb, out_min, out_max);
   return cudaGetLastError();
 }
 

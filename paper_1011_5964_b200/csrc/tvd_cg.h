@@ -27,6 +27,7 @@ struct PcgState {
   double err_val;
   int iters;
   int converged;
+  int x_pending;  // gamma of iteration k accepted, x += step p not yet applied (split update)
 };
 
 // ---- scalar steps of the recurrence (krylov.py:99-116), thread 0 of one CTA, given the
@@ -44,6 +45,7 @@ __device__ __forceinline__ void pcg_fin_gamma(PcgState* s, double pq) {
     s->done = 1;
   } else {
     s->step = s->rz / pq;
+    s->x_pending = 1;
   }
 }
 __device__ __forceinline__ void pcg_fin_rel(PcgState* s, double rr, double tol, double* hist) {
@@ -147,6 +149,14 @@ cudaError_t launch_pcg_rel(PcgState* s, const double* partial, int nb, double to
                            cudaStream_t st);
 cudaError_t launch_pcg_beta(PcgState* s, const double* partial, int nb, int max_it, cudaStream_t st);
 cudaError_t launch_pcg_update_p(PcgState* s, double* p, const double* z, long N, cudaStream_t st);
+// split x / r update: r -= step q with r.r and the stop test (critical path), and
+// x += step p (off the critical path: another stream overlaps it with the preconditioner
+// passes; it applies iff iteration k's gamma was accepted, x_pending, which its last CTA
+// clears through `counter`).  Same arithmetic and r.r partials as k_pcg_update_xr.
+cudaError_t launch_pcg_update_r(PcgState* s, double* r, const double* q, long N, double* partial,
+                                cudaStream_t st, const PcgFin* fin);
+cudaError_t launch_pcg_update_x(PcgState* s, double* x, const double* p, long N, unsigned* counter,
+                                cudaStream_t st);
 cudaError_t launch_diag_solve(const double* r, const double* d, double* z, long N, double* partial,
                               int nb, const int* skip, cudaStream_t st);
 cudaError_t launch_dot_partials(const double* x, const double* y, long N, double* partial, int nb,
@@ -166,6 +176,11 @@ cudaError_t launch_scale_bands(const double* diag, const double* inner, const do
 // inv = 1 / max(lam, floor); partial counts of lam < floor
 cudaError_t launch_invert_eigs(const double* lam, double floor, double* inv, long N, double* partial,
                                int nb, cudaStream_t st);
+cudaError_t launch_invert_eigs_dev(const double* lam, const double* max_lam, double* inv, long N,
+                                   double* partial, cudaStream_t st);
+cudaError_t launch_reduce_min(const double* partial_min, int nb, double* out, cudaStream_t st);
+cudaError_t launch_reduce_minmax(const double* partial_mm, int nb, double* out_min, double* out_max,
+                                 cudaStream_t st);
 int vec_blocks();
 
 }  // namespace tvd

@@ -7,12 +7,14 @@ of the restored image stays resident in HBM: per FP step the diffusivity
 kernel, the device preconditioner assembly and the device PCG
 (``tvd_pcg_solve``) run back to back on the current torch stream.
 
-In scope (BASELINE.json north_star): NORMAL formulation with zero-Neumann
-diffusion, i.e. the symmetric systems solved by PCG, for reflective (R
-family) and anti-reflective (M family) blur, selectors NONE / DIAG / X /
-D_X / X_D.  REBLUR and the anti-reflective diffusion BC (BiCGstab systems)
-are validated like the reference and then rejected with
-``NotImplementedError``.
+Systems: the NORMAL formulation with zero-Neumann diffusion (symmetric, solved by the
+device PCG) for reflective (R family) and anti-reflective (M family) blur -- the BASELINE
+hot path -- and, as the reference does (pipeline.py:196-198), the REBLUR formulation and the
+anti-reflective diffusion BC (nonsymmetric, solved by the device BiCGstab with the P family,
+SURVEY.md 8f #2); selectors NONE / DIAG / X / D_X / X_D.  Preconditioners are assembled with
+their positivity checks left on the device and resolved after each solve
+(``FactoredPreconditioner.check``), so an FP step synchronises the host only where the
+reference's report needs a scalar (gradient norm, FP change).
 """
 
 from __future__ import annotations
@@ -221,11 +223,23 @@ def scale_system(system: NormalSystem, rhs, l_op: DiffusionOperator, alpha: floa
     return ScaledSystem(d=d, d_inv_sqrt=s, apply=scaled, rhs=_binary(s, rt, 0))
 
 
-def _timed_solve(solver, apply_a, apply_minv, b, x0, cfg, acc: list[float]) -> SolveOutcome:
+def _timed_solve(solver, apply_a, apply_minv, b, x0, cfg, acc: list[float],
+                 precond=None) -> SolveOutcome:
+    """One inner solve, timed with CUDA events.  ``precond``: a preconditioner assembled with
+    deferred checks -- resolved after the solve (which synchronises anyway), and first when
+    the solve raises, since the reference fails at assembly (precond.py:437-441, 558-560)
+    before it would ever reach the solver."""
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     start.record()
-    out = solver(apply_a, apply_minv, b, x0, cfg)
+    try:
+        out = solver(apply_a, apply_minv, b, x0, cfg)
+    except Exception:
+        if precond is not None:
+            precond.check()
+        raise
+    if precond is not None:
+        precond.check()
     stop.record()
     stop.synchronize()
     acc[0] += start.elapsed_time(stop) / 1e3
@@ -266,11 +280,13 @@ def restore(v, psf: SymmetricPsf, config: RestorationConfig, u_true=None) -> Res
         selector = config.preconditioner
         if selector is PrecondSelector.X_D:
             bundle = scale_system(system, rhs, l_op, alpha)
-            precond = assemble_preconditioner(f"{config.base_kind()}_D", h_op, l_op, alpha)
+            precond = assemble_preconditioner(f"{config.base_kind()}_D", h_op, l_op, alpha,
+                                              defer_checks=True)
             outcome = _timed_solve(solver, bundle.apply, precond.apply_inverse, bundle.rhs,
-                                   bundle.scale_iterate(u), config.inner, pcg_time)
+                                   bundle.scale_iterate(u), config.inner, pcg_time, precond)
             u_next = bundle.unscale(outcome.solution)
         else:
+            precond = None
             if selector is PrecondSelector.NONE:
                 apply_minv = None
             elif selector is PrecondSelector.DIAG:
@@ -279,9 +295,10 @@ def restore(v, psf: SymmetricPsf, config: RestorationConfig, u_true=None) -> Res
             else:
                 kind = config.base_kind() if selector is PrecondSelector.X \
                     else f"D_{config.base_kind()}"
-                precond = assemble_preconditioner(kind, h_op, l_op, alpha)
+                precond = assemble_preconditioner(kind, h_op, l_op, alpha, defer_checks=True)
                 apply_minv = precond.apply_inverse
-            outcome = _timed_solve(solver, system, apply_minv, rhs, u, config.inner, pcg_time)
+            outcome = _timed_solve(solver, system, apply_minv, rhs, u, config.inner, pcg_time,
+                                   precond)
             u_next = outcome.solution
         steps += 1
         inner_iterations.append(outcome.iterations)

@@ -55,7 +55,8 @@ class FactoredPreconditioner:
 
     def __init__(self, kind: str, transform: TransformKind, eigenvalues, alpha: float,
                  d_sqrt=None, *, inverse_eigenvalues=None, clamped: int | None = None,
-                 scaling=None, device: torch.device | None = None) -> None:
+                 scaling=None, device: torch.device | None = None,
+                 pending: torch.Tensor | None = None) -> None:
         if transform not in _FAMILY_CODE:
             raise NotImplementedError(f"{transform.value} preconditioners are outside this build's scope")
         self.kind = kind
@@ -74,11 +75,36 @@ class FactoredPreconditioner:
             floor = 1e-14 * float(lam.max())
             clamped = int((lam < floor).sum())
             inverse_eigenvalues = 1.0 / torch.clamp(lam, min=floor)
-        if clamped:
+        self._inv = inverse_eigenvalues
+        #: deferred device-side checks (tvd_precond_assemble_async), resolved by check()
+        self._pending = pending
+        self._clamped = int(clamped or 0)
+        if pending is None and clamped:
             logger.warning("preconditioner %s: clamped %d eigenvalue(s) below %.3e",
                            kind, clamped, 1e-14 * float(lam.max()))
-        self._inv = inverse_eigenvalues
-        self.clamped = int(clamped or 0)
+
+    def check(self) -> None:
+        """Resolve the construction checks of a deferred assembly (precond.py:437-450,
+        558-560): raise :class:`IndefinitePreconditionerError` for a nonpositive scaling
+        diagonal or eigenvalue, log the clamp warning.  Reads four device doubles (one
+        synchronisation); a no-op for an eagerly checked preconditioner."""
+        if self._pending is None:
+            return
+        min_d, mn, mx, cnt = (float(x) for x in self._pending.cpu())
+        self._pending = None
+        if not min_d > 0.0:
+            raise IndefinitePreconditionerError(self.kind, self.alpha, min_d)
+        if not mn > 0.0:
+            raise IndefinitePreconditionerError(self.kind, self.alpha, mn)
+        self._clamped = int(cnt)
+        if self._clamped:
+            logger.warning("preconditioner %s: clamped %d eigenvalue(s) below %.3e",
+                           self.kind, self._clamped, 1e-14 * mx)
+
+    @property
+    def clamped(self) -> int:
+        self.check()
+        return self._clamped
 
     @property
     def ndim(self) -> int:
@@ -130,8 +156,14 @@ class FactoredPreconditioner:
         return self._run(b, True)
 
 
-def assemble_preconditioner(kind: str, h_op, l_op, alpha: float) -> FactoredPreconditioner:
-    """Build one factored preconditioner on the device (precond.py:516-573)."""
+def assemble_preconditioner(kind: str, h_op, l_op, alpha: float, *,
+                            defer_checks: bool = False) -> FactoredPreconditioner:
+    """Build one factored preconditioner on the device (precond.py:516-573).
+
+    ``defer_checks``: leave the positivity checks and the clamp count on the device (no host
+    synchronisation; ``tvd_precond_assemble_async``); the returned preconditioner raises /
+    warns from :meth:`FactoredPreconditioner.check`, which the caller runs after its solve
+    (``restore`` does).  The eigenvalues are identical either way."""
     from .blur import BoundaryCondition
 
     if kind not in PRECONDITIONER_KINDS:
@@ -164,6 +196,17 @@ def assemble_preconditioner(kind: str, h_op, l_op, alpha: float) -> FactoredPrec
     ctx = nat.context(dev)
     inner_c = inner.contiguous()
     block_c = block.contiguous()
+    if defer_checks:
+        chk = torch.empty(4, dtype=torch.float64, device=dev)
+        nat.check(nat.load().tvd_precond_assemble_async(
+            ctx, _FAMILY_CODE[transform], variant, n, float(alpha), lam_h.data_ptr(),
+            diag.data_ptr(), inner_c.data_ptr(), block_c.data_ptr(), eig.data_ptr(),
+            inv.data_ptr(), nat.ptr(dvec), chk.data_ptr()))
+        if variant == nat.VARIANT_X_D:
+            return FactoredPreconditioner(kind, transform, eig, alpha, inverse_eigenvalues=inv,
+                                          scaling=dvec, device=dev, pending=chk)
+        return FactoredPreconditioner(kind, transform, eig, alpha, d_sqrt=dvec,
+                                      inverse_eigenvalues=inv, device=dev, pending=chk)
     rc = nat.load().tvd_precond_assemble(
         ctx, _FAMILY_CODE[transform], variant, n, float(alpha), lam_h.data_ptr(),
         diag.data_ptr(), inner_c.data_ptr(), block_c.data_ptr(), eig.data_ptr(), inv.data_ptr(),

@@ -41,3 +41,35 @@ def sketch_rel_err(u, ref_sketch: np.ndarray, ref_norm: float) -> float:
     """JL estimate of ``||u - ref|| / ||ref||`` from the reference's sketch and norm."""
     s = sketch(u, len(ref_sketch))
     return float(np.linalg.norm(s - ref_sketch) / np.sqrt(len(ref_sketch)) / ref_norm)
+
+
+def _signs_torch(idx, j: int):
+    """``_signs`` on int64 torch tensors (same bit patterns: multiplication wraps mod 2^64,
+    logical right shifts by masking)."""
+    import torch
+
+    def srl(z, s):
+        return (z >> s) & ((1 << (64 - s)) - 1)
+
+    def c64(v: int) -> int:  # a uint64 constant as the int64 with the same bits
+        return v - (1 << 64) if v >= 1 << 63 else v
+
+    z = idx + c64(((j + 1) * int(_GOLD)) % (1 << 64))
+    z = (z ^ srl(z, 30)) * c64(int(_M1))
+    z = (z ^ srl(z, 27)) * c64(int(_M2))
+    z = z ^ srl(z, 31)
+    return 1.0 - 2.0 * (z < 0).to(torch.float64)
+
+
+def sketch_torch(t, k: int = 32, chunk: int = 1 << 24) -> np.ndarray:
+    """:func:`sketch` of a torch tensor on its own device (the same projections)."""
+    import torch
+
+    flat = t.reshape(-1).to(torch.float64)
+    out = np.zeros(k)
+    for c0 in range(0, flat.numel(), chunk):
+        part = flat[c0:c0 + chunk]
+        idx = torch.arange(c0, c0 + part.numel(), dtype=torch.int64, device=part.device)
+        for j in range(k):
+            out[j] += float(torch.dot(_signs_torch(idx, j), part))
+    return out

@@ -836,3 +836,62 @@ def test_c4_restore_matches_reference(golden, name):
     assert abs(np.linalg.norm(r) - float(g["restored_norm"])) <= 1e-8 * float(g["restored_norm"])
     assert sketch_rel_err(r, g["restored_sketch"], float(g["restored_norm"])) < 1e-8
     assert abs(rep.rre - float(g["rre"])) < 1e-8
+
+
+# ------------------------------------------------- config 5 (8192^2) vs the reference
+def _big_check(g, key, t, tol):
+    """``t`` (device tensor) against the reference's 512 MB array ``key`` frozen as norm,
+    prime-stride subsample, border rows / columns and a 16-projection sketch."""
+    from sketch import sketch_torch
+
+    ref_norm = float(g[f"{key}_norm"])
+    assert abs(float(torch.linalg.norm(t)) - ref_norm) <= tol * ref_norm, key
+    a = t.cpu().numpy() if t.numel() <= (1 << 27) else None
+    sub = t[::61, ::61].cpu().numpy()
+    assert rel_err(sub, g[f"{key}_sub"]) < tol, key
+    rows = t[[0, 1, 2, 30, 31, 32, -33, -32, -31, -3, -2, -1], ::7].cpu().numpy()
+    cols = t[::7, [0, 1, 2, 30, 31, 32, -33, -32, -31, -3, -2, -1]].cpu().numpy()
+    assert rel_err(rows, g[f"{key}_rows"]) < tol, key
+    assert rel_err(cols, g[f"{key}_cols"]) < tol, key
+    sk = g[f"{key}_sketch"]
+    est = np.linalg.norm(sketch_torch(t, len(sk)) - sk) / np.sqrt(len(sk)) / ref_norm
+    assert est < tol, (key, est)
+    del a
+
+
+def test_c5_ops_and_first_fp_step_match_reference(golden):
+    """Config 5 (8192^2 AR, Gaussian 63 x 63 sigma 8, m = 31) against the reference's own
+    outputs (tests/golden/make_golden.py --c5, ~1 h of CPU): the observation, exact H v and
+    H^T v, the diffusivities, the assembled kind-M eigenvalues (Rader band projections at the
+    prime core 8191), M^-1 of a seeded field, and the first FP step's PCG solve (count within
+    one, iterate within 1e-8).  Every array is gated over all of its 67M entries through a
+    sketch plus subsample / border rows (tests/sketch.py)."""
+    from paper_1011_5964_b200.harness import make_problem
+
+    g = golden("c5_ops.npz")
+    spec = CONFIGS["c5"]
+    n = spec.n
+    dev = torch.device("cuda")
+    h, v, _ = make_problem(spec, exact=False, device=dev)
+    assert np.array_equal(h, g["psf"])
+    vd = torch.from_numpy(v).to(dev)
+    del v
+    _big_check(g, "v", vd, 1e-14)
+    hop = B.StructuredBlurOperator(B.SymmetricPsf(h), B.BoundaryCondition.ANTI_REFLECTIVE, n,
+                                   device=dev)
+    _big_check(g, "H_v", hop.apply(vd), 1e-12)
+    rhs = hop.apply_transpose(vd)
+    _big_check(g, "HT_v", rhs, 1e-12)
+    lop = TV.DiffusionOperator(vd, spec.beta, device=dev)
+    _big_check(g, "a_h", lop.a_h_device, 1e-14)
+    _big_check(g, "a_v", lop.a_v_device, 1e-14)
+    pre = P.assemble_preconditioner("M", hop, lop, spec.alpha)
+    _big_check(g, "lam_M", pre.eigenvalues_device, 1e-12)
+    w = torch.from_numpy(np.random.default_rng(8192).standard_normal((n, n))).to(dev)
+    _big_check(g, "minv_w", pre.apply_inverse(w), 1e-12)
+    del w
+    from paper_1011_5964_b200.pipeline import NormalSystem
+    out = K.pcg(NormalSystem(hop, lop, spec.alpha), pre.apply_inverse, rhs, vd,
+                K.KrylovConfig(tol=spec.tol, max_iterations=2000, record_history=True))
+    assert abs(out.iterations - int(g["fp1_iterations"])) <= 1
+    _big_check(g, "fp1_u", out.solution, 1e-8)
