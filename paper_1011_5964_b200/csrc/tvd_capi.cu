@@ -727,9 +727,11 @@ static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const 
     a.ar_qr = ar_qr;
   }
   int nb;
-  TVD_LAUNCH(c, kCatTrigRows, 1, launch_pipe(P->pfa, family, n, n, 1, a, &nb, c->stream));
+  // the intermediates in the pair-blocked layout (tvd_pfa.cu launch_pipe_pm)
+  TVD_LAUNCH(c, kCatTrigRows, 1, launch_pipe(P->pfa, family, n, n, 2, a, &nb, c->stream));
   LineIO b{};
   b.in = tT;
+  b.in_blocked = 1;
   b.out = t2;
   b.mid_mul = inv_t;
   b.skip = skip;
@@ -738,9 +740,10 @@ static int precond_pipe(tvd_ctx* c, const TrigPlan* P, int family, int n, const 
     b.ar_ql = ar_ql;
     b.ar_qr = ar_qr;
   }
-  TVD_LAUNCH(c, kCatTrigCols, 1, launch_pipe(P->pfa, family, n, n, 1, b, &nb, c->stream));
+  TVD_LAUNCH(c, kCatTrigCols, 1, launch_pipe(P->pfa, family, n, n, 2, b, &nb, c->stream));
   LineIO z{};
   z.in = t2;
+  z.in_blocked = 1;
   z.out = out;
   z.post = d;
   z.post_mul = dmul;

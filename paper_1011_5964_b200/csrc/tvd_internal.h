@@ -136,6 +136,9 @@ struct LineIO {
   // generic engine (k_trig): element t of line l is written to out[t * nlines + l] (the pass
   // output transposed, so the next pass runs over contiguous rows); post / dot_with unused
   int out_trans;
+  // pipeline passes: input in the pair-blocked layout of a pass launched with transposed = 2
+  // (element e of line l at ((l >> 1) len + e) 2 + (l & 1)); row-major input otherwise
+  int in_blocked;
 };
 
 // Band projection of one batch of lines (preconditioner assembly).

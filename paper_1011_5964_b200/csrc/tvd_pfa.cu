@@ -611,6 +611,7 @@ struct PipeK {
   const double* ar_qr;
   int in_seg;          // LineIO::in_seg (0: row-major input)
   long in_seg_stride;
+  int in_blocked;      // LineIO::in_blocked (dispatch only: PM bit 3)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -712,6 +713,12 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   pdl_enter();
   const bool has_mid = PM < 0 ? p.mid != nullptr : (PM & 1) != 0;
   const bool trans = PM < 0 ? p.transposed != 0 : (PM & 2) != 0;
+  // pair-blocked layouts (PM bits 2 / 3): element e of line l lives at ((l >> 1) n + e) 2 +
+  // (l & 1), so a 2-line batch writes 2 n contiguous doubles and the next pass, whose lines
+  // are the columns, reads one 16-byte pair per (block, line) -- instead of 16-byte column
+  // segments written at a stride of n doubles
+  constexpr bool BOUT = PM >= 0 && (PM & 4) != 0;
+  constexpr bool BIN = PM >= 0 && (PM & 8) != 0;
   using SH = PfaShape<Q1, Q2, Q3>;
   static_assert(!HALF || SH::d == 2, "half-line layout is for two-factor lengths");
   // HALF: half-line Good-Thomas layout (tvd_pfa_t.cuh HalfShape), signed scatter / gather
@@ -767,6 +774,30 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   const int nb_cta = F + (tl1 > tl0 ? 1 : 0);
   auto first_of = [&](int j) { return j < F ? (j * G + c) * B : tl0; };
   auto rows_of = [&](int j) { return j < F ? B : tl1 - tl0; };
+  // blocked input: every thread copies 16-byte pairs with cp.async (the staging row of line
+  // t gets pair (2 b, 2 b + 1) from block b), completion by wait_group + the pack barrier
+  auto issue_blocked = [&](int j) {
+    const int first = first_of(j), rows = rows_of(j);
+    const int nh = n >> 1;
+    for (int i = tid; i < rows * nh; i += nth) {
+      const int l = i / nh, b = i - l * nh;
+      const double* src = p.in + ((long)b * n + first + l) * 2;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(stage + l * n + 2 * b);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    if (tid == 0) {
+      for (int l = 0; l < rows; ++l) {
+        const long r = (long)(first + l) * n;
+        if (p.pre) bulk_prefetch_l2(p.pre + r, (unsigned)(n * 8));
+        if (has_mid) bulk_prefetch_l2(p.mid + r, (unsigned)(n * 8));
+        if (!trans) {
+          if (p.post) bulk_prefetch_l2(p.post + r, (unsigned)(n * 8));
+          if (p.dot_with) bulk_prefetch_l2(p.dot_with + r, (unsigned)(n * 8));
+        }
+      }
+    }
+  };
   auto issue = [&](int j) {
     const int first = first_of(j), rows = rows_of(j);
     mbar_expect_tx(&mbar, (unsigned)(rows * n * 8));
@@ -791,8 +822,9 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   };
   if (tid == 0) {
     mbar_init(&mbar, 1);
-    if (nb_cta > 0) issue(0);
+    if (!BIN && nb_cta > 0) issue(0);
   }
+  if (BIN && nb_cta > 0) issue_blocked(0);
   __syncthreads();
   // y_k from the transformed line l, gather index gi = gath[k - 1] (0 for k out of range)
   auto unpack = [&](int l, unsigned gi, int k) {
@@ -822,6 +854,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   };
   const long nl_out = p.nlines;
   auto oidx = [&](int line, int e) {
+    if (BOUT) return ((long)(line >> 1) * n + e) * 2 + (line & 1);
     return trans ? (long)e * nl_out + line : (long)line * n + e;
   };
   double acc = 0.0;
@@ -843,8 +876,13 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       const int t = 1 + tid + k * NT;
       e[k] = (k < kTpt - 1 || t <= N) ? __ldg(scat + t - 1) : 0u;
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1u;
+    if constexpr (BIN) {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+    } else {
+      mbar_wait(&mbar, phase);
+      phase ^= 1u;
+    }
     PIPE_T(0);
     for (int l = 0; l < nlv; ++l) {
       const double* srow = stage + l * n + p.off - 1;  // srow[t] = x_t
@@ -896,7 +934,9 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     }
     __syncthreads();
     PIPE_T(1);
-    if (tid == 0 && jb + 1 < nb_cta) {
+    if (BIN) {
+      if (jb + 1 < nb_cta) issue_blocked(jb + 1);
+    } else if (tid == 0 && jb + 1 < nb_cta) {
       fence_proxy_async();  // staging was read through the generic proxy
       issue(jb + 1);
     }
@@ -977,8 +1017,10 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       constexpr int JT = (N + TS - 1) / TS;
       constexpr int JG = 8;
       if (l < nlv) {
-        const long cb = (long)(p.off - 1) * nl_out + line0 + l;
-        double* __restrict__ ocol = p.out + cb;  // ocol[t * nl] = y_t
+        // ocol[t * ostr] = y_t: column segments (stride nl) or the pair-blocked layout (2)
+        const long ostr = BOUT ? 2 : nl_out;
+        const long cb = BOUT ? oidx(line0 + l, p.off - 1) : (long)(p.off - 1) * nl_out + line0 + l;
+        double* __restrict__ ocol = p.out + cb;
         const double* __restrict__ dcol = p.dot_with ? p.dot_with + cb : nullptr;
         const double* __restrict__ qcol = p.post ? p.post + cb : nullptr;
         const int t0 = 1 + tid / B;
@@ -1005,7 +1047,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 #pragma unroll
             for (int j = 0; j < JG; ++j) {
               const int t = t0 + (j0 + j) * TS;
-              q[j] = (j0 + j < JT && t <= N) ? qcol[(long)t * nl_out] : 1.0;
+              q[j] = (j0 + j < JT && t <= N) ? qcol[(long)t * ostr] : 1.0;
             }
 #pragma unroll
             for (int j = 0; j < JG; ++j) y[j] = p.post_mul ? y[j] * q[j] : y[j] / q[j];
@@ -1014,13 +1056,13 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
 #pragma unroll
           for (int j = 0; j < JG; ++j) {
             const int t = t0 + (j0 + j) * TS;
-            dv[j] = (dcol && j0 + j < JT && t <= N) ? dcol[(long)t * nl_out] : 0.0;
+            dv[j] = (dcol && j0 + j < JT && t <= N) ? dcol[(long)t * ostr] : 0.0;
           }
 #pragma unroll
           for (int j = 0; j < JG; ++j) {
             const int t = t0 + (j0 + j) * TS;
             if (j0 + j < JT && t <= N) {
-              ocol[(long)t * nl_out] = y[j];
+              ocol[(long)t * ostr] = y[j];
               acc += y[j] * dv[j];
             }
           }
@@ -1112,15 +1154,23 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
 }
 
 // the four pass-specialised instances of one launch shape
+// pass modes: bit 0 sandwich, bit 1 transposed output, bit 2 pair-blocked output (with bit 1),
+// bit 3 pair-blocked input.  The single-GPU M^-1 runs 6 -> 15 -> 8 (row pass into the blocked
+// layout, sandwich blocked to blocked, row pass out of it); the row-slab passes 0..3.
 template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF, bool HO = false,
           int BL = kPipeLines, int CO = 0>
 static cudaError_t launch_pipe_pm(const PipeK& k, int grid, cudaStream_t st) {
-  const int pm = (k.mid ? 1 : 0) | (k.transposed ? 2 : 0);
+  const int pm = (k.mid ? 1 : 0) | (k.transposed ? 2 : 0) | (k.transposed == 2 ? 4 : 0) |
+                 (k.in_blocked ? 8 : 0);
   switch (pm) {
     case 0: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 0, HO, CO>(k, grid, st);
     case 1: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 1, HO, CO>(k, grid, st);
     case 2: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 2, HO, CO>(k, grid, st);
-    default: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 3, HO, CO>(k, grid, st);
+    case 3: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 3, HO, CO>(k, grid, st);
+    case 6: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 6, HO, CO>(k, grid, st);
+    case 8: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 8, HO, CO>(k, grid, st);
+    case 15: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 15, HO, CO>(k, grid, st);
+    default: return cudaErrorInvalidConfiguration;
   }
 }
 
@@ -1183,8 +1233,10 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
   k.ar_ql = io.ar_ql;
   k.ar_qr = io.ar_qr;
   if (io.in_seg && (io.in_seg % 2 || len % io.in_seg)) return cudaErrorInvalidValue;
+  if (io.in_blocked && (io.in_seg || (len & 1) || nlines != len)) return cudaErrorInvalidValue;
   k.in_seg = io.in_seg;
   k.in_seg_stride = io.in_seg_stride;
+  k.in_blocked = io.in_blocked;
   k.stages = option(kOptPfaStages);  // profiling: run only the first stages
   const int grid = pipe_grid(P, nlines);
   if (nblocks_out) *nblocks_out = grid;
@@ -1193,7 +1245,7 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
     case 1: return launch_pipe_pm<89, 23, 1, 192, 2, 1, true, true, 2, 2>(k, grid, st);
     case 2: return launch_pipe_pm<31, 11, 3, 64, 4, 2, false>(k, grid, st);
     case 3: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st);
-    case 4: return launch_pipe_t<127, 1, 1>(k, grid, st);
+    case 4: return launch_pipe_pm<127, 1, 1, 256, 2, 3, false>(k, grid, st);
     default: return cudaErrorInvalidConfiguration;
   }
 }
