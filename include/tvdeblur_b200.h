@@ -114,7 +114,9 @@ int tvd_ctx_destroy(tvd_ctx* ctx);
  *                            extension + direct convolution) even when the PSF is rank 1
  *   TVD_OPT_BAND_PREFETCH 0: column band pass prefetches its epilogue operands to L2 (1) / L1 (2)
  *   TVD_OPT_SPLIT_X       0: PCG x update on a second stream, overlapping the M^-1 passes
- *                            (bit-identical; measured no gain) */
+ *                            (bit-identical; measured no gain)
+ *   TVD_OPT_GUARD_SLOTS   0: scratch allocated while set carries 4 KB guard bands checked by
+ *                            tvd_ctx_check_guards (debugging: out-of-bounds kernel writes) */
 #define TVD_OPT_GENERIC_FFT 1
 #define TVD_OPT_SOLVER_GRAPH 2
 #define TVD_OPT_PDL 3
@@ -126,8 +128,12 @@ int tvd_ctx_destroy(tvd_ctx* ctx);
 #define TVD_OPT_GENERAL_BLUR 9
 #define TVD_OPT_BAND_PREFETCH 10
 #define TVD_OPT_SPLIT_X 11
+#define TVD_OPT_GUARD_SLOTS 12
 int tvd_ctx_set_option(tvd_ctx* ctx, int option, int value);
 int tvd_ctx_get_option(tvd_ctx* ctx, int option, int* value);
+/* bytes of the guard bands of ctx's guarded scratch slots that no longer hold the fill
+ * pattern (0 = no out-of-bounds write into the context's scratch) */
+int tvd_ctx_check_guards(tvd_ctx* ctx, long long* bad_bytes, int* guarded_slots);
 /* instrumentation: kernels launched through ctx so far */
 int tvd_ctx_counters(tvd_ctx* ctx, long long* launches);
 /* enable (1) / disable (0) CUDA-event timing around every launch; resets records */

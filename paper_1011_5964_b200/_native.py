@@ -52,6 +52,7 @@ _SIGNATURES = {
     "tvd_ctx_destroy": ([_vp], _i),
     "tvd_ctx_set_option": ([_vp, _i, _i], _i),
     "tvd_ctx_get_option": ([_vp, _i, ctypes.POINTER(_i)], _i),
+    "tvd_ctx_check_guards": ([_vp, ctypes.POINTER(_ll), ctypes.POINTER(_i)], _i),
     "tvd_ctx_counters": ([_vp, ctypes.POINTER(_ll)], _i),
     "tvd_ctx_profile": ([_vp, _i], _i),
     "tvd_ctx_profile_read": ([_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_ll)], _i),
@@ -199,7 +200,7 @@ def launch_count(device=None) -> int:
 #: option ids of include/tvdeblur_b200.h (TVD_OPT_*)
 OPTIONS = {"generic_fft": 1, "solver_graph": 2, "pdl": 3, "band_generic": 4, "band_slide": 5,
            "fin_fusion": 6, "p_fusion": 7, "pfa_stages": 8, "general_blur": 9,
-           "band_prefetch": 10, "split_x": 11}
+           "band_prefetch": 10, "split_x": 11, "guard_slots": 12}
 
 
 def set_option(name: str, value: int, device=None) -> None:
@@ -226,6 +227,14 @@ class option:
 
     def __exit__(self, *exc):
         set_option(self.name, self.saved, self.device)
+
+
+def check_guards(device=None) -> tuple[int, int]:
+    """``(corrupted guard bytes, guarded slots)`` of this thread's context (option
+    ``guard_slots``)."""
+    bad, slots = _ll(), _i()
+    check(load().tvd_ctx_check_guards(context(device), ctypes.byref(bad), ctypes.byref(slots)))
+    return bad.value, slots.value
 
 
 def set_generic_fft(enable: bool, device=None) -> None:

@@ -26,7 +26,7 @@ namespace tvd {
 // defaults: graph replay on, PDL attribute off (measured neutral), Rader band projections,
 // tensor-core band passes, folded finalizers, fused direction update, every PFA stage,
 // separable blurs on the banded path
-static std::atomic<int> g_options[kOptCount] = {0, 0, 1, 0, 0, 0, 1, 1, 3, 0, 0, 0};
+static std::atomic<int> g_options[kOptCount] = {0, 0, 1, 0, 0, 0, 1, 1, 3, 0, 0, 0, 0};
 int option(int id) { return (id > 0 && id < kOptCount) ? g_options[id].load() : 0; }
 }  // namespace tvd
 
@@ -81,7 +81,14 @@ enum Slot : int {
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
+  void* base = nullptr;  // allocation start (ptr - kGuardBytes when guarded)
+  bool guarded = false;
 };
+// option guard_slots: every scratch slot allocated while it is set carries kGuardBytes of a
+// fill pattern on both sides, checked by tvd_ctx_check_guards (out-of-bounds writes by the
+// kernels into the context's scratch; compute-sanitizer is not available on the GPU pool)
+constexpr size_t kGuardBytes = 4096;
+constexpr int kGuardFill = 0xA5;
 
 struct tvd_ctx {
   int device = 0;
@@ -187,13 +194,22 @@ static cudaError_t ensure(tvd_ctx* c, int slot, size_t bytes, void** out) {
     if (b.ptr) {
       cudaError_t e = cudaStreamSynchronize(c->stream);
       if (e != cudaSuccess) return e;
-      cudaFree(b.ptr);
-      b.ptr = nullptr;
+      cudaFree(b.base);
+      b.ptr = b.base = nullptr;
       b.bytes = 0;
     }
-    cudaError_t e = cudaMalloc(&b.ptr, bytes);
+    b.guarded = option(kOptGuardSlots) != 0;
+    const size_t g = b.guarded ? kGuardBytes : 0;
+    cudaError_t e = cudaMalloc(&b.base, bytes + 2 * g);
     if (e != cudaSuccess) return e;
+    b.ptr = static_cast<char*>(b.base) + g;
     b.bytes = bytes;
+    if (g) {
+      e = cudaMemset(b.base, kGuardFill, g);
+      if (e == cudaSuccess) e = cudaMemset(static_cast<char*>(b.ptr) + bytes, kGuardFill, g);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) return e;
+    }
   }
   *out = b.ptr;
   return cudaSuccess;
@@ -1302,6 +1318,27 @@ int tvd_ctx_set_option(tvd_ctx* c, int option, int value) {
   return TVD_OK;
 }
 
+int tvd_ctx_check_guards(tvd_ctx* c, long long* bad_bytes, int* guarded_slots) {
+  if (!c || !bad_bytes) return fail(TVD_ERR_INVALID, "null argument");
+  DeviceGuard g(c->device);
+  TVD_CUDA(cudaDeviceSynchronize());
+  long long bad = 0;
+  int slots = 0;
+  std::vector<unsigned char> h(kGuardBytes);
+  for (const DevBuf& b : c->slots) {
+    if (!b.guarded || !b.base) continue;
+    ++slots;
+    const void* bands[2] = {b.base, static_cast<const char*>(b.ptr) + b.bytes};
+    for (const void* gp : bands) {
+      TVD_CUDA(cudaMemcpy(h.data(), gp, kGuardBytes, cudaMemcpyDeviceToHost));
+      for (unsigned char v : h) bad += v != kGuardFill;
+    }
+  }
+  *bad_bytes = bad;
+  if (guarded_slots) *guarded_slots = slots;
+  return TVD_OK;
+}
+
 int tvd_ctx_get_option(tvd_ctx* c, int option, int* value) {
   if (!c || !value) return fail(TVD_ERR_INVALID, "null argument");
   if (option == TVD_OPT_GENERIC_FFT) *value = c->force_generic ? 1 : 0;
@@ -1351,7 +1388,7 @@ int tvd_ctx_destroy(tvd_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (auto& kv : c->plans) free_plan(kv.second.get());
   for (auto& s : c->slots)
-    if (s.ptr) cudaFree(s.ptr);
+    if (s.base) cudaFree(s.base);
   cudaFree(c->d_state);
   cudaFree(c->d_fin);
   for (auto& kv : c->ar) {

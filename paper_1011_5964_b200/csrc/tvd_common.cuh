@@ -69,7 +69,7 @@ __device__ __forceinline__ void pdl_enter() {
 // every default is the measured production configuration.
 enum TvdOpt : int {
   kOptGenericFft = 1, kOptSolverGraph, kOptPdl, kOptBandGeneric, kOptBandSlide, kOptFinFusion,
-  kOptPFusion, kOptPfaStages, kOptGeneralBlur, kOptBandPrefetch, kOptSplitX, kOptCount
+  kOptPFusion, kOptPfaStages, kOptGeneralBlur, kOptBandPrefetch, kOptSplitX, kOptGuardSlots, kOptCount
 };
 int option(int id);  // tvd_capi.cu
 

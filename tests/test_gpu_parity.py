@@ -402,30 +402,49 @@ def test_restore_unpreconditioned(golden, name):
 
 
 def test_headline_c3_restore_matches_reference():
-    """Config 3 (2048^2 AR, 20 FP steps, tol 1e-5) end to end vs the reference's own
-    28-minute CPU run (tests/golden/restore_c3_head.npz): identical per-FP-step PCG
-    counts, restored image checksums within 1e-8."""
+    """Config 3 (2048^2 AR, 20 FP steps, tol 1e-5) end to end against the reference's own
+    CPU runs (tests/golden/c3_parity.json, made by tests/golden/make_c3_parity.py from four
+    ~30-120-minute runs of the unmodified reference on identical inputs).
+
+    Counts: at tol 1e-5 the stopping iteration is not a property of the algorithm.  The
+    reference disagrees with ITSELF by up to 3 iterations per FP step between runs that
+    differ only in the BLAS thread count of its dot products (krylov.py:70-75) or in its
+    fast vs exact H^T (blur.py:236-247 vs 302-314); replays of single FP steps from the
+    reference's own iterates (same file) show the relative residual sitting within a few
+    percent of tol, followed by a non-monotone bump, where rounding picks the iteration.
+    The gate is the reference's own envelope: each device count within [min, max] of the
+    reference runs, widened by one.  The image is gated over every pixel (sketch) and on the
+    subsample against each reference run at 1e-8 -- the runs agree with each other to ~1e-10.
+    """
+    import json
+
+    from sketch import sketch
+
     from paper_1011_5964_b200.harness import make_problem
-    g = golden_c3 = __import__("conftest").load_golden("restore_c3_head.npz")
+    ev = json.loads((__import__("pathlib").Path(__file__).parent / "golden" /
+                     "c3_parity.json").read_text())
     spec = CONFIGS["c3"]
     h, v, u_true = make_problem(spec)
-    assert abs(np.linalg.norm(v) - float(g["v_norm"])) <= 1e-14 * float(g["v_norm"])
+    assert abs(np.linalg.norm(v) - ev["v_norm"]) <= 1e-14 * ev["v_norm"]
     cfg = tvd.RestorationConfig(
         bc_h=BCS["anti_reflective"], alpha=spec.alpha, beta=spec.beta,
-        preconditioner=tvd.PrecondSelector.X, fp_tol=1e-300, fp_max=int(g["fp_max"]),
+        preconditioner=tvd.PrecondSelector.X, fp_tol=1e-300, fp_max=spec.fp_steps,
         inner=K.KrylovConfig(tol=spec.tol, max_iterations=2000))
     rep = tvd.restore(v, B.SymmetricPsf(h), cfg, u_true=u_true)
-    # The c3 stopping decisions are rounding-sensitive: the reference algorithm restated
-    # with a different FFT (oracle fast path) or with the exact operator lands +3 off the
-    # reference's own count at FP step 7 (tests/golden/c3_count_spread.json), while every
-    # image stays within 1e-8.  Gate: the images; counts within that measured spread.
-    ref = [int(k) for k in golden_c3["inner_iterations"]]
-    assert rep.inner_iterations[:6] == ref[:6]
-    assert all(abs(a - b) <= 3 for a, b in zip(rep.inner_iterations, ref))
+    runs = list(ev["reference_runs"].values())
+    lo = [min(r["counts"][k] for r in runs) for k in range(spec.fp_steps)]
+    hi = [max(r["counts"][k] for r in runs) for k in range(spec.fp_steps)]
+    got = rep.inner_iterations
+    assert all(lo[k] - 1 <= got[k] <= hi[k] + 1 for k in range(spec.fp_steps)), (got, lo, hi)
     r = np.asarray(rep.restored)
-    assert abs(np.linalg.norm(r) - float(g["restored_norm"])) <= 1e-8 * float(g["restored_norm"])
-    assert rel_err(r[::16, ::16], g["restored_sub"]) < 1e-8
-    assert abs(rep.rre - float(g["rre"])) < 1e-8
+    s = sketch(r, 64)
+    for name, run in ev["reference_runs"].items():
+        img = run["image"]
+        assert abs(np.linalg.norm(r) - img["norm"]) <= 1e-8 * img["norm"], name
+        est = np.linalg.norm(s - np.asarray(img["sketch"])) / 8.0 / img["norm"]
+        assert est < 1e-8, (name, est)
+        assert rel_err(r[::16, ::16], np.asarray(img["sub"])) < 1e-8, name
+        assert abs(rep.rre - run["rre"]) < 1e-8, name
 
 
 # ------------------------------------------------------------------ row f2 (SURVEY.md 8f #2)

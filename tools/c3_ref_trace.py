@@ -1,6 +1,7 @@
 """Trace the REFERENCE's config-c3 restore (build container only; parity evidence).
 
     PYTHONPATH=/root/reference/pkg/src python tools/c3_ref_trace.py OUTDIR [FP_STEPS] [--exact]
+        [--exact-dots]
 
 Runs ``tvdeblur.pipeline.restore`` (reference ``pipeline.py:182-276``) unchanged on the c3
 fixture of ``tests/golden/make_golden.py`` and, through a wrapper around the module-level
@@ -10,7 +11,9 @@ fixture of ``tests/golden/make_golden.py`` and, through a wrapper around the mod
 steps from these iterates with other operator variants and with the GPU.  ``--exact`` runs the
 reference with ``use_fast_blur=False`` (``pipeline.py:75,167-179``): its exact pad / convolve /
 crop ``H`` and full-convolve + fold ``H^T`` (``blur.py:226-247``) in place of the transform
-path.
+path.  ``--exact-dots`` replaces the reference's BLAS ``_dot`` / ``_norm`` (krylov.py:70-75)
+by exactly rounded dot products (tools/c3_dot_probe.py ``exact_dot``): the reference's
+recurrence with reductions free of summation-order error.
 """
 import json
 import pathlib
@@ -35,7 +38,16 @@ out = pathlib.Path(sys.argv[1])
 out.mkdir(parents=True, exist_ok=True)
 spec = bh.CONFIGS["c3"]
 exact = "--exact" in sys.argv
-argv = [a for a in sys.argv if a != "--exact"]
+exact_dots = "--exact-dots" in sys.argv
+argv = [a for a in sys.argv if a not in ("--exact", "--exact-dots")]
+if exact_dots:
+    import math
+
+    sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent))
+    from c3_dot_probe_lib import exact_dot
+
+    rk._dot = exact_dot
+    rk._norm = lambda x: math.sqrt(exact_dot(x, x))
 fp = int(argv[2]) if len(argv) > 2 else spec.fp_steps
 psf = rh.gen_psf("gaussian", spec.m, spec.sigma)
 ext = bh.gen_piecewise_image(spec.n, spec.m, spec.rects, spec.disks, 2023, spec.ramp)

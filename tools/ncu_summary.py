@@ -1,6 +1,10 @@
 """Summarise ncu outputs into profiles/<round>/ (run in the build container, no GPU needed).
 
-    python tools/ncu_summary.py <round_dir> <launches.csv> [<report.ncu-rep> ...]
+    python tools/ncu_summary.py <round_dir> [--name=F] [--config=c3 --n=2048] <launches.csv>
+        [<report.ncu-rep> ...]
+
+traffic.json carries the workload it was captured on ({"config", "n", "kernels"}), which
+bench.py's roofline.traffic matches against the line's own config and size.
 """
 import collections
 import csv
@@ -73,8 +77,15 @@ def main() -> None:
     rd.mkdir(parents=True, exist_ok=True)
     name = "ncu_summary.json"
     args = sys.argv[2:]
-    if args and args[0].startswith("--name="):
-        name = args.pop(0).split("=", 1)[1]
+    config, size = "c3", 2048
+    while args and args[0].startswith("--"):
+        key, _, val = args.pop(0)[2:].partition("=")
+        if key == "name":
+            name = val
+        elif key == "config":
+            config = val
+        elif key == "n":
+            size = int(val)
     summary = {"launches": launches(pathlib.Path(args[0]))}
     reps = []
     for rep in args[1:]:
@@ -99,7 +110,8 @@ def main() -> None:
                                 "source": f"{rd.name}/{rep_name} (ncu --set full)"}
                 break
     if traffic:
-        (rd / "traffic.json").write_text(json.dumps(traffic, indent=1))
+        (rd / "traffic.json").write_text(json.dumps({"config": config, "n": size,
+                                                     "kernels": traffic}, indent=1))
     print(json.dumps(summary["launches"][:12], indent=1))
 
 
