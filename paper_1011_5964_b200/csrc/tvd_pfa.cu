@@ -779,11 +779,13 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   auto issue_blocked = [&](int j) {
     const int first = first_of(j), rows = rows_of(j);
     const int nh = n >> 1;
-    for (int i = tid; i < rows * nh; i += nth) {
-      const int l = i / nh, b = i - l * nh;
-      const double* src = p.in + ((long)b * n + first + l) * 2;
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(stage + l * n + 2 * b);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+    // one thread per block: the batch's lines are adjacent 16-byte pairs of one sector
+    for (int b = tid; b < nh; b += nth) {
+      const double* src = p.in + ((long)b * n + first) * 2;
+      for (int l = 0; l < rows; ++l) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(stage + l * n + 2 * b);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + 2 * l));
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::);
     if (tid == 0) {
