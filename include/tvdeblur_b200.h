@@ -104,7 +104,7 @@ int tvd_ctx_destroy(tvd_ctx* ctx);
  * process-wide (every context; setting one drops the context's captured solver graphs);
  * their defaults are the measured production configuration:
  *   TVD_OPT_SOLVER_GRAPH  1: replay captured PCG / BiCGstab iterations as CUDA graphs
- *   TVD_OPT_PDL           0: programmatic dependent launch attribute on the iteration kernels
+ *   TVD_OPT_PDL           1: programmatic dependent launch attribute on the iteration kernels
  *   TVD_OPT_BAND_GENERIC  0: prime-core assembly projections on the generic engine, not Rader
  *   TVD_OPT_BAND_SLIDE    0: CUDA-core band passes instead of the fp64 tensor-core ones
  *   TVD_OPT_FIN_FUSION    1: PCG scalar steps folded into their producers' last CTA

@@ -23,10 +23,11 @@
 using namespace tvd;
 
 namespace tvd {
-// defaults: graph replay on, PDL attribute off (measured neutral), Rader band projections,
+// defaults: graph replay on, PDL attribute on (c1 / c2a / c2b / single-stream c4 solves
+// +17 / +31 / +24 / +20 %, c3 neutral; bit-identical), Rader band projections,
 // tensor-core band passes, folded finalizers, fused direction update, every PFA stage,
 // separable blurs on the banded path
-static std::atomic<int> g_options[kOptCount] = {0, 0, 1, 0, 0, 0, 1, 1, 3, 0, 0, 0, 0};
+static std::atomic<int> g_options[kOptCount] = {0, 0, 1, 1, 0, 0, 1, 1, 3, 0, 0, 0, 0};
 int option(int id) { return (id > 0 && id < kOptCount) ? g_options[id].load() : 0; }
 }  // namespace tvd
 

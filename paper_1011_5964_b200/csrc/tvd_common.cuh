@@ -53,10 +53,10 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
 // An explicit early trigger (griddepcontrol.launch_dependents right after the wait, so the
 // next grid's CTAs become resident during this one's last wave) measured 8 % SLOWER on c3
 // (2330 vs 2532 it/s) and is off by default (-DTVD_PDL_EARLY_TRIGGER=1 builds it).  Both
-// instructions are no-ops for a grid launched without the attribute.  Wait-only PDL measured
-// neutral (c3 2541 / 2537 vs 2541 it/s, c4 8626 vs 8676, c5 102.5 vs 102.5, c2b 11413 vs
-// 11409: the replayed graphs already hide the launch gaps), so the attribute is opt-in:
-// TVD_PDL=1 sets it.
+// instructions are no-ops for a grid launched without the attribute.  Wait-only PDL: neutral
+// at c3 (2787 vs 2782 it/s), and +17 / +31 / +24 / +20 % on single-stream c1 / c2a / c2b / c4
+// solves (round 2, tools/pcg_ab.py pdl 0,1 CONFIG), whose short kernels leave the launch
+// latency exposed; on by default, option TVD_OPT_PDL.
 #ifndef TVD_PDL_EARLY_TRIGGER
 #define TVD_PDL_EARLY_TRIGGER 0
 #endif

@@ -42,10 +42,10 @@ def _solves() -> list[tuple]:
 def test_pdl_bit_identical():
     from paper_1011_5964_b200 import _native as nat
 
-    assert nat.get_option("pdl") == 0
-    plain = _solves()
-    with nat.option("pdl", 1):
-        assert nat.get_option("pdl") == 1
-        pdl = _solves()
-    assert nat.get_option("pdl") == 0
+    assert nat.get_option("pdl") == 1  # the default
+    with nat.option("pdl", 0):
+        assert nat.get_option("pdl") == 0
+        plain = _solves()
+    assert nat.get_option("pdl") == 1
+    pdl = _solves()
     assert len(plain) == 4 and plain == pdl, (plain, pdl)

@@ -1,7 +1,7 @@
-"""A/B of one c3 inner PCG solve (2048^2, FP state 2 as in bench.py) under a library option:
-iterations/s over repeated solves and bit-identity of the solutions.  Profiling aid.
+"""A/B of one inner PCG solve (FP state 2 as in bench.py; default config c3) under a library
+option: iterations/s over repeated solves and bit-identity of the solutions.  Profiling aid.
 
-    python tools/pcg_ab.py OPTION v1,v2,...
+    python tools/pcg_ab.py OPTION v1,v2,... [CONFIG]
 """
 import json
 import pathlib
@@ -16,21 +16,22 @@ from paper_1011_5964_b200.harness import CONFIGS, make_problem  # noqa: E402
 
 name = sys.argv[1]
 vals = [int(v) for v in sys.argv[2].split(",")]
-spec = CONFIGS["c3"]
+spec = CONFIGS[sys.argv[3] if len(sys.argv) > 3 else "c3"]
 dev = torch.device("cuda", 0)
 h, v, _ = make_problem(spec)
-hop = tvd.StructuredBlurOperator(tvd.SymmetricPsf(h), tvd.BoundaryCondition.ANTI_REFLECTIVE, spec.n,
-                                 device=dev)
+bc = tvd.BoundaryCondition(spec.bc)
+kind = "M" if bc is tvd.BoundaryCondition.ANTI_REFLECTIVE else "R"
+hop = tvd.StructuredBlurOperator(tvd.SymmetricPsf(h), bc, spec.n, device=dev)
 v = torch.from_numpy(v).to(dev)
-rhs = hop.apply_transpose(v)
+rhs = hop.apply(v) if kind == "R" else hop.apply_transpose(v)
 cfg = tvd.KrylovConfig(tol=spec.tol, max_iterations=2000)
 u = v.clone()
 for _ in range(2):
     lop = tvd.DiffusionOperator(u, spec.beta, device=dev)
-    pre = tvd.assemble_preconditioner("M", hop, lop, spec.alpha)
+    pre = tvd.assemble_preconditioner(kind, hop, lop, spec.alpha)
     u = tvd.pcg(tvd.NormalSystem(hop, lop, spec.alpha), pre.apply_inverse, rhs, u, cfg).solution
 lop = tvd.DiffusionOperator(u, spec.beta, device=dev)
-pre = tvd.assemble_preconditioner("M", hop, lop, spec.alpha)
+pre = tvd.assemble_preconditioner(kind, hop, lop, spec.alpha)
 system = tvd.NormalSystem(hop, lop, spec.alpha)
 saved = nat.get_option(name)
 out, ref = {}, None
@@ -42,7 +43,7 @@ for val in vals:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     its = 0
     e0.record()
-    for _ in range(10):
+    for _ in range(10 if spec.n >= 2048 else 50):
         res = tvd.pcg(system, pre.apply_inverse, rhs, u, cfg)
         its += res.iterations
     e1.record()
