@@ -559,29 +559,32 @@ def run_slab(args, rank: int, world: int) -> None:
         pre = tvd.assemble_preconditioner("M", hop, lop, spec.alpha)
         return tvd.NormalSystem(hop, lop, spec.alpha), pre
 
-    def solve(system, pre, x0_full):
-        """(iterations, full solution) of one inner solve"""
-        if world == 1:
-            out = tvd.pcg(system, pre.apply_inverse, rhs, x0_full, cfg)
-            return out.iterations, out.solution
-        s = SL.Slab(system, pre.apply_inverse, world, rank)
-        (o,) = SL.slab_pcg([s], comm, [SL.split_rows(rhs, world, rank)],
-                           [SL.split_rows(x0_full, world, rank)], cfg)
-        full = torch.empty(n, n, dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(full, o.solution)
-        return o.iterations, full
+    layout = SL.SlabLayout(n, world, rank, 1)
 
-    u = v.clone()
-    for _ in range(args.state_fp):  # untimed: a representative lagged-diffusivity state
-        system, pre = operators(u)
-        u = solve(system, pre, u)[1]
-    system, pre = operators(u)
+    def slab_of(u_slab):
+        """This rank's slab solver for the FP state u: diffusivity and assembly of its own
+        rows only (slab.slab_operators: a one-row u halo, one all-to-all, a min / max
+        allreduce) -- no rank rebuilds the full image's operators."""
+        (ops,) = SL.slab_operators(hop, [u_slab], [layout], comm, spec.beta, spec.alpha, "M")
+        return SL.Slab.from_operands(hop, spec.alpha, ops, world, rank)
+
     if world == 1:
+        u = v.clone()
+        for _ in range(args.state_fp):  # untimed: a representative lagged-diffusivity state
+            system, pre = operators(u)
+            u = tvd.pcg(system, pre.apply_inverse, rhs, u, cfg).solution
+        system, pre = operators(u)
+
         def step() -> int:
             return tvd.pcg(system, pre.apply_inverse, rhs, u, cfg).iterations
     else:
-        slab = SL.Slab(system, pre.apply_inverse, world, rank)
-        b_s, x_s = SL.split_rows(rhs, world, rank), SL.split_rows(u, world, rank)
+        b_s = SL.split_rows(rhs, world, rank)
+        x_s = SL.split_rows(v, world, rank)
+        for _ in range(args.state_fp):
+            (o,) = SL.slab_pcg([slab_of(x_s)], comm, [b_s], [x_s], cfg)
+            x_s = o.solution
+        slab = slab_of(x_s)
+        u = None
 
         def step() -> int:
             (o,) = SL.slab_pcg([slab], comm, [b_s], [x_s], cfg)
@@ -599,10 +602,11 @@ def run_slab(args, rank: int, world: int) -> None:
         roof["achieved"] *= R / n
         roof["frac"] = roof["achieved"] / hbm
 
-    # e2e: this rank's slabs of (u, rhs) from pinned host memory, allgather of u, diffusivity
-    # and assembly, the slab solve, D2H of the solution slab
+    # e2e: this rank's slabs of (u, rhs) from pinned host memory, the FP-step setup of its
+    # rows (u halo, diffusivity, assembly with one all-to-all), the slab solve, D2H of the
+    # solution slab
     R = n // world
-    u_host = SL.split_rows(u, world, rank).cpu().pin_memory()
+    u_host = (u if world == 1 else x_s).cpu().pin_memory()
     rhs_host = SL.split_rows(rhs, world, rank).cpu().pin_memory()
     out_host = torch.empty_like(u_host).pin_memory()
 
@@ -614,11 +618,7 @@ def run_slab(args, rank: int, world: int) -> None:
             res = tvd.pcg(sysm, p_op.apply_inverse, rs, us, cfg)
             out_host.copy_(res.solution, non_blocking=True)
             return res.iterations
-        full = torch.empty(n, n, dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(full, us)
-        sysm, p_op = operators(full)
-        s = SL.Slab(sysm, p_op.apply_inverse, world, rank)
-        (o,) = SL.slab_pcg([s], comm, [rs], [us], cfg)
+        (o,) = SL.slab_pcg([slab_of(us)], comm, [rs], [us], cfg)
         out_host.copy_(o.solution, non_blocking=True)
         return o.iterations
 
@@ -658,8 +658,8 @@ def run_slab(args, rank: int, world: int) -> None:
         "cpu_baseline": None,
         "e2e": {"value": e2e_iters / e2e_t, "unit": UNIT, "h2d_bytes_per_step": 16 * R * n,
                 "d2h_bytes_per_step": 8 * R * n, "steps": e2e_steps,
-                "includes": "H2D u,rhs slabs; allgather u; diffusivity; device assembly; "
-                            "slab PCG; D2H solution slab"},
+                "includes": "H2D u,rhs slabs; u halo rows; slab diffusivity and assembly "
+                            "(one all-to-all); slab PCG; D2H solution slab"},
         "gpu_launches": int(launches),
         "clocks": clk,
     }

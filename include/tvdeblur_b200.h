@@ -182,6 +182,27 @@ int tvd_transform_lines(tvd_ctx* ctx, int kind, int rows, int cols, int axis, co
 /* X G X^T on a square n x n grid: axis 0 then axis 1 (tensor_apply_2d) */
 int tvd_transform_2d(tvd_ctx* ctx, int kind, int n, const double* in, double* out, int inverse);
 
+/* ---- row windows: the FP-step setup of a row slab (slab.slab_operators) ---
+ * Diffusivity of the global rows [row_lo, row_hi) of an n x n image (zero-Neumann ghosts):
+ * a_h rows [row_lo, row_hi) ((row_hi-row_lo) x (n+1)), a_v rows [row_lo, row_hi]
+ * ((row_hi-row_lo+1) x n), from a window u_win of the global rows [win_lo, win_lo+win_rows)
+ * that holds the one-row halo.  Bit-identical to the rows of tvd_diffusivity. */
+int tvd_diffusivity_rows(tvd_ctx* ctx, int n, double beta, double spacing, const double* u_win,
+                         int win_lo, int win_rows, int row_lo, int row_hi, double* a_h,
+                         double* a_v);
+/* block bands (diag n, inner n-1, block n per row) of the global rows [row_lo, row_hi) from
+ * the window's a_h / a_v (as written by tvd_diffusivity_rows); rows of tvd_diffusion_bands */
+int tvd_diffusion_bands_rows(tvd_ctx* ctx, int n, double spacing, const double* a_h,
+                             const double* a_v, int row_lo, int row_hi, double* diag,
+                             double* inner, double* block);
+/* one level of the band projection (precond.py:82-199) over nlines contiguous lines of n:
+ * b0 the d = 0 band, b1 (nullable; line stride b1_stride, multiplicity c1) the |d| = 1
+ * band; epi 0 stores the projection, epi 1 stores lamh^2 + alpha * projection and returns
+ * its min / max (host) */
+int tvd_band_project_lines(tvd_ctx* ctx, int family, int n, int nlines, const double* b0,
+                           const double* b1, int b1_stride, double c1, int epi,
+                           const double* lamh, double alpha, double* out, double* min_max);
+
 /* ---- preconditioner  (precond.py:369-573) ------------------------------ */
 /* Assemble eigenvalues of kind {R,D_R,R_D} (family DCT) or {M,D_M,M_D}
  * (family SINE_HAT) from the blur eigenvalues and the diffusion bands.

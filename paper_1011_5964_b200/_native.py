@@ -53,6 +53,10 @@ _SIGNATURES = {
     "tvd_ctx_set_option": ([_vp, _i, _i], _i),
     "tvd_ctx_get_option": ([_vp, _i, ctypes.POINTER(_i)], _i),
     "tvd_ctx_check_guards": ([_vp, ctypes.POINTER(_ll), ctypes.POINTER(_i)], _i),
+    "tvd_diffusivity_rows": ([_vp, _i, _d, _d, _vp, _i, _i, _i, _i, _vp, _vp], _i),
+    "tvd_diffusion_bands_rows": ([_vp, _i, _d, _vp, _vp, _i, _i, _vp, _vp, _vp], _i),
+    "tvd_band_project_lines": ([_vp, _i, _i, _i, _vp, _vp, _i, _d, _i, _vp, _d, _vp,
+                                ctypes.POINTER(_d)], _i),
     "tvd_ctx_counters": ([_vp, ctypes.POINTER(_ll)], _i),
     "tvd_ctx_profile": ([_vp, _i], _i),
     "tvd_ctx_profile_read": ([_vp, _i, ctypes.POINTER(_d), ctypes.POINTER(_ll)], _i),

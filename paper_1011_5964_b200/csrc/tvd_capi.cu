@@ -1610,6 +1610,79 @@ int tvd_diffusion_bands_bc(tvd_ctx* c, int n, double spacing, int bc_l, const do
   return TVD_OK;
 }
 
+// ------------------------------------------- row windows (the row-slab FP-step setup)
+static int host_minmax(tvd_ctx* c, const double* d_partial, int nb, double* mn, double* mx);
+
+int tvd_diffusivity_rows(tvd_ctx* c, int n, double beta, double spacing, const double* u_win,
+                         int win_lo, int win_rows, int row_lo, int row_hi, double* a_h,
+                         double* a_v) {
+  if (!c || !u_win || !a_h || !a_v) return fail(TVD_ERR_INVALID, "null argument");
+  if (beta <= 0 || spacing <= 0) return fail(TVD_ERR_INVALID, "beta and spacing must be positive");
+  if (row_lo < 0 || row_hi > n || row_lo >= row_hi)
+    return fail(TVD_ERR_INVALID, "row window outside the image");
+  // the edge stencils read rows row_lo - 1 .. row_hi (clamped to the image)
+  const int need_lo = row_lo > 0 ? row_lo - 1 : 0, need_hi = row_hi < n ? row_hi : n - 1;
+  if (need_lo < win_lo || need_hi >= win_lo + win_rows)
+    return fail(TVD_ERR_INVALID, "u window lacks the one-row halo of the row window");
+  DeviceGuard g(c->device);
+  TVD_LAUNCH(c, kCatStencil, 1, launch_diffusivity_rows(u_win, win_lo, n, beta, spacing, a_h, a_v,
+                                                        c->stream, TVD_DBC_ZERO_NEUMANN, row_lo,
+                                                        row_hi));
+  return TVD_OK;
+}
+
+int tvd_diffusion_bands_rows(tvd_ctx* c, int n, double spacing, const double* a_h,
+                             const double* a_v, int row_lo, int row_hi, double* diag,
+                             double* inner, double* block) {
+  if (!c || !a_h || !a_v || !diag || !inner || !block) return fail(TVD_ERR_INVALID, "null argument");
+  if (row_lo < 0 || row_hi > n || row_lo >= row_hi)
+    return fail(TVD_ERR_INVALID, "row window outside the image");
+  DeviceGuard g(c->device);
+  TVD_LAUNCH(c, kCatStencil, 1, launch_diffusion_bands_rows(a_h, a_v, n, 1.0 / (spacing * spacing),
+                                                            diag, inner, block, row_lo, row_hi,
+                                                            c->stream));
+  return TVD_OK;
+}
+
+int tvd_band_project_lines(tvd_ctx* c, int family, int n, int nlines, const double* b0,
+                           const double* b1, int b1_stride, double c1, int epi,
+                           const double* lamh, double alpha, double* out, double* min_max) {
+  if (!c || !b0 || !out) return fail(TVD_ERR_INVALID, "null argument");
+  if (family != TVD_TRANSFORM_SINE_HAT && family != TVD_TRANSFORM_DCT)
+    return fail(TVD_ERR_INVALID, "line projections support the SINE_HAT and DCT families");
+  if (epi != 0 && epi != 1) return fail(TVD_ERR_INVALID, "epilogue must be 0 or 1");
+  if (epi == 1 && (!lamh || !min_max)) return fail(TVD_ERR_INVALID, "epilogue needs lamh / min_max");
+  if (nlines < 1 || nlines > n) return fail(TVD_ERR_INVALID, "bad line count");
+  DeviceGuard g(c->device);
+  const TrigPlan* P;
+  int rc = get_plan(c, family, n, &P);
+  if (rc) return rc;
+  BandLines f{};
+  f.b0 = b0; f.b0_ls = n; f.b0_es = 1;
+  f.b1 = b1; f.b1_ls = b1_stride; f.b1_es = 1;
+  f.c1 = b1 ? c1 : 0.0;
+  f.nlines = nlines;
+  f.out = out; f.out_ls = n; f.out_es = 1;
+  f.epi = epi;
+  f.lamh = lamh;
+  f.alpha = alpha;
+  double* mm = nullptr;
+  if (epi) {
+    TVD_SLOT(c, kSlotPartial2, 2 * (size_t)n + 64 + vec_blocks(), mm);
+    f.partial_minmax = mm;
+  }
+  int nb = 0;
+  TVD_LAUNCH(c, kCatProject, 1, launch_band_project(*P, 0, f, &nb, c->stream));
+  if (epi) {
+    double mn, mx;
+    rc = host_minmax(c, mm, nb, &mn, &mx);
+    if (rc) return rc;
+    min_max[0] = mn;
+    min_max[1] = mx;
+  }
+  return TVD_OK;
+}
+
 // ------------------------------------------------------------ transforms
 int tvd_transform_lines(tvd_ctx* c, int kind, int rows, int cols, int axis, const double* in,
                         double* out, int inverse) {

@@ -533,6 +533,46 @@ __global__ void k_diffusivity(const double* __restrict__ u, int n, double beta, 
   }
 }
 
+// Row window of the diffusivity (the row-slab setup): edges of the global rows
+// [row_lo, row_hi) -- a_h rows [row_lo, row_hi), a_v rows [row_lo, row_hi] -- from a window of
+// u that holds the global rows [win_lo, win_lo + rows) with row_lo - 1 >= win_lo and
+// row_hi <= win_lo + rows - 1 (or the image border).  Same edge arithmetic as k_diffusivity
+// (dxg / dyg over a base pointer shifted to global row 0: bit-identical outputs).
+template <bool UNIT>
+__global__ void k_diffusivity_rows(const double* __restrict__ u_win, int win_lo, int n,
+                                   double beta, double sp, double* __restrict__ a_h,
+                                   double* __restrict__ a_v, int bc, int row_lo, int row_hi) {
+  const double bb = __dmul_rn(beta, beta);
+  const double* u = u_win - (long)win_lo * n;  // dereferenced only inside the window
+  const unsigned np1 = (unsigned)n + 1u, nu = (unsigned)n;
+  const long nh = (long)(row_hi - row_lo) * (n + 1);
+  const long nv = (long)(row_hi - row_lo + 1) * n;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < nh + nv;
+       e += (long)gridDim.x * blockDim.x) {
+    if (e < nh) {
+      const unsigned eu = (unsigned)e;
+      const int i = row_lo + (int)(eu / np1), j = (int)(eu - (unsigned)(i - row_lo) * np1);
+      const double d = dxg<UNIT>(u, n, i + 1, j, sp, bc);
+      double t = __dadd_rn(dyg<UNIT>(u, n, i, j, sp, bc), dyg<UNIT>(u, n, i + 1, j, sp, bc));
+      t = __dadd_rn(t, dyg<UNIT>(u, n, i, j + 1, sp, bc));
+      t = __dadd_rn(t, dyg<UNIT>(u, n, i + 1, j + 1, sp, bc));
+      t = __dmul_rn(0.25, t);
+      const double q = __dadd_rn(__dadd_rn(__dmul_rn(d, d), __dmul_rn(t, t)), bb);
+      a_h[e] = __ddiv_rn(1.0, __dsqrt_rn(q));
+    } else {
+      const unsigned f = (unsigned)(e - nh);
+      const int i = row_lo + (int)(f / nu), j = (int)(f - (unsigned)(i - row_lo) * nu);
+      const double d = dyg<UNIT>(u, n, i, j + 1, sp, bc);
+      double t = __dadd_rn(dxg<UNIT>(u, n, i, j, sp, bc), dxg<UNIT>(u, n, i, j + 1, sp, bc));
+      t = __dadd_rn(t, dxg<UNIT>(u, n, i + 1, j, sp, bc));
+      t = __dadd_rn(t, dxg<UNIT>(u, n, i + 1, j + 1, sp, bc));
+      t = __dmul_rn(0.25, t);
+      const double q = __dadd_rn(__dadd_rn(__dmul_rn(d, d), __dmul_rn(t, t)), bb);
+      a_v[(long)f] = __ddiv_rn(1.0, __dsqrt_rn(q));
+    }
+  }
+}
+
 __global__ void k_diffusion_apply(const double* __restrict__ a_h, const double* __restrict__ a_v,
                                   const double* __restrict__ w, int n, double inv_h2,
                                   double* __restrict__ out, int bc) {
@@ -585,6 +625,31 @@ __global__ void k_diffusion_bands(const double* __restrict__ a_h, const double* 
   }
 }
 
+// Block bands of the global rows [row_lo, row_hi) from a_h rows [row_lo, row_hi) and a_v rows
+// [row_lo, row_hi] (k_diffusion_bands restricted to a row window, zero-Neumann ghosts; the
+// outputs are the window's rows of diag / inner / block, block row i = rows (i, i + 1))
+__global__ void k_diffusion_bands_rows(const double* __restrict__ a_h_win,
+                                       const double* __restrict__ a_v_win, int n, double inv_h2,
+                                       double* __restrict__ diag, double* __restrict__ inner,
+                                       double* __restrict__ block, int row_lo, int row_hi) {
+  const long W = (long)(row_hi - row_lo) * n;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < W;
+       g += (long)gridDim.x * blockDim.x) {
+    const int il = (int)((unsigned long long)g / (unsigned)n), j = (int)(g - (long)il * n);
+    const int i = row_lo + il;
+    const double* a_h = a_h_win + (long)il * (n + 1);
+    const double* a_v = a_v_win + (long)il * n;  // a_v[0] = global row i, a_v[n] = row i + 1
+    double d = __dadd_rn(__dadd_rn(__dadd_rn(a_h[j], a_h[j + 1]), a_v[j]), a_v[n + j]);
+    if (j == 0) d = __dsub_rn(d, a_h[0]);
+    if (j == n - 1) d = __dsub_rn(d, a_h[n]);
+    if (i == 0) d = __dsub_rn(d, a_v[j]);
+    if (i == n - 1) d = __dsub_rn(d, a_v[n + j]);
+    diag[g] = __dmul_rn(inv_h2, d);
+    if (j < n - 1) inner[(long)il * (n - 1) + j] = __dmul_rn(inv_h2, -a_h[j + 1]);
+    if (i < n - 1) block[g] = __dmul_rn(inv_h2, -a_v[n + j]);
+  }
+}
+
 static int grid_for(long work, int threads) {
   long b = (work + threads - 1) / threads;
   if (b > 16L * kSMs) b = 16L * kSMs;
@@ -598,6 +663,26 @@ cudaError_t launch_diffusivity(const double* u, int n, double beta, double sp, d
     k_diffusivity<true><<<grid_for(2L * n * (n + 1), 256), 256, 0, st>>>(u, n, beta, sp, a_h, a_v, bc);
   else
     k_diffusivity<false><<<grid_for(2L * n * (n + 1), 256), 256, 0, st>>>(u, n, beta, sp, a_h, a_v, bc);
+  return cudaGetLastError();
+}
+cudaError_t launch_diffusivity_rows(const double* u_win, int win_lo, int n, double beta, double sp,
+                                    double* a_h, double* a_v, cudaStream_t st, int bc, int row_lo,
+                                    int row_hi) {
+  const long work = (long)(row_hi - row_lo) * (n + 1) + (long)(row_hi - row_lo + 1) * n;
+  if (work >= (1L << 32)) return cudaErrorInvalidValue;
+  if (sp == 1.0)
+    k_diffusivity_rows<true><<<grid_for(work, 256), 256, 0, st>>>(u_win, win_lo, n, beta, sp, a_h,
+                                                                  a_v, bc, row_lo, row_hi);
+  else
+    k_diffusivity_rows<false><<<grid_for(work, 256), 256, 0, st>>>(u_win, win_lo, n, beta, sp, a_h,
+                                                                   a_v, bc, row_lo, row_hi);
+  return cudaGetLastError();
+}
+cudaError_t launch_diffusion_bands_rows(const double* a_h, const double* a_v, int n, double inv_h2,
+                                        double* diag, double* inner, double* block, int row_lo,
+                                        int row_hi, cudaStream_t st) {
+  k_diffusion_bands_rows<<<grid_for((long)(row_hi - row_lo) * n, 256), 256, 0, st>>>(
+      a_h, a_v, n, inv_h2, diag, inner, block, row_lo, row_hi);
   return cudaGetLastError();
 }
 cudaError_t launch_diffusion_apply(const double* a_h, const double* a_v, const double* w, int n,

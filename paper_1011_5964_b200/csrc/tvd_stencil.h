@@ -92,6 +92,12 @@ cudaError_t launch_diffusivity(const double* u, int n, double beta, double sp, d
                                double* a_v, cudaStream_t st, int bc = 0);
 cudaError_t launch_diffusion_apply(const double* a_h, const double* a_v, const double* w, int n,
                                    double inv_h2, double* out, cudaStream_t st, int bc = 0);
+cudaError_t launch_diffusivity_rows(const double* u_win, int win_lo, int n, double beta, double sp,
+                                    double* a_h, double* a_v, cudaStream_t st, int bc, int row_lo,
+                                    int row_hi);
+cudaError_t launch_diffusion_bands_rows(const double* a_h, const double* a_v, int n, double inv_h2,
+                                        double* diag, double* inner, double* block, int row_lo,
+                                        int row_hi, cudaStream_t st);
 cudaError_t launch_diffusion_bands(const double* a_h, const double* a_v, int n, double inv_h2,
                                    double* diag, double* inner, double* block, cudaStream_t st,
                                    int bc = 0, double* inner_lo = nullptr,

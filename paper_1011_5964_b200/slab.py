@@ -89,6 +89,25 @@ class _DeviceArray:
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
+@dataclass
+class SlabOperands:
+    """One rank's share of an FP step's operators: diffusivities of its rows (``a_h``
+    ``R x (n+1)``, ``a_v`` ``(R+1) x n``), its rows of the transposed inverse eigenvalues
+    (``inv_t`` = columns ``[lo, lo+R)`` of ``lambda^-1``, the layout of the preconditioner's
+    column pass), ``d`` = ``sqrt(1 + alpha diag L)`` rows for D_X kinds, the native
+    preconditioner kind / family codes, the global eigenvalue range and clamp count."""
+
+    a_h: torch.Tensor
+    a_v: torch.Tensor
+    inv_t: torch.Tensor | None
+    d: torch.Tensor | None
+    kind: int
+    family: int
+    min_eig: float = float("nan")
+    max_eig: float = float("nan")
+    clamped: int = 0
+
+
 class Slab:
     """One rank's slab solver (``tvd_slab``): buffers, phases and status."""
 
@@ -103,26 +122,39 @@ class Slab:
             raise ValueError(f"n = {n} is not divisible by {nranks} ranks")
         R = n // nranks
         lo = rank * R
-        self.device = system.device
-        self.n, self.nranks, self.rank = n, nranks, rank
         lop = system.l_op
-        # slab operands (kept alive for the handle's lifetime)
-        self._a_h = lop.a_h_device[lo:lo + R].contiguous()
-        self._a_v = lop.a_v_device[lo:lo + R + 1].contiguous()
         fused = _fused_precond(precond)
         if fused is None:
             raise ValueError("slab solves take None, a DiagonalInverse or "
                              "FactoredPreconditioner.apply_inverse")
         kind, family, inv, d = fused
-        self._inv_t = None if inv is None else inv.t()[lo:lo + R].contiguous()
-        self._d = None if d is None else d[lo:lo + R].contiguous()
         if system.s is not None or system.reblur:
             raise ValueError("slab solves support the X / D_X systems H^T H + alpha L")
-        self._csys = nat.TvdSystem(system.h_op.handle, system.alpha, lop.spacing,
-                                   self._a_h.data_ptr(), self._a_v.data_ptr(), None,
-                                   lop.bc_code, 0)
-        self._cpre = nat.TvdPrecond(kind, family, nat.ptr(self._inv_t), nat.ptr(self._d))
-        self._h_op = system.h_op  # the blur handle must outlive the slab
+        ops = SlabOperands(lop.a_h_device[lo:lo + R].contiguous(),
+                           lop.a_v_device[lo:lo + R + 1].contiguous(),
+                           None if inv is None else inv.t()[lo:lo + R].contiguous(),
+                           None if d is None else d[lo:lo + R].contiguous(), kind, family)
+        self._init(system.h_op, system.alpha, lop.spacing, lop.bc_code, ops, nranks, rank)
+
+    @classmethod
+    def from_operands(cls, h_op, alpha: float, ops: "SlabOperands", nranks: int, rank: int,
+                      spacing: float = 1.0) -> "Slab":
+        """A slab from this rank's own operands (:func:`slab_operators`) -- no full-size
+        system or preconditioner exists anywhere."""
+        self = cls.__new__(cls)
+        self._init(h_op, alpha, spacing, 0, ops, nranks, rank)
+        return self
+
+    def _init(self, h_op, alpha, spacing, bc_code, ops: "SlabOperands", nranks, rank) -> None:
+        n = h_op.n
+        self.device = h_op.device
+        self.n, self.nranks, self.rank = n, nranks, rank
+        # slab operands (kept alive for the handle's lifetime)
+        self._a_h, self._a_v, self._inv_t, self._d = ops.a_h, ops.a_v, ops.inv_t, ops.d
+        self._csys = nat.TvdSystem(h_op.handle, float(alpha), float(spacing),
+                                   self._a_h.data_ptr(), self._a_v.data_ptr(), None, bc_code, 0)
+        self._cpre = nat.TvdPrecond(ops.kind, ops.family, nat.ptr(self._inv_t), nat.ptr(self._d))
+        self._h_op = h_op  # the blur handle must outlive the slab
         lib = nat.load()
         ctx = nat.context(self.device)
         out = ctypes.c_void_p()
@@ -209,6 +241,32 @@ class TorchComm:
             parts = list(dst.split(1))
             self.dist.all_gather(parts, src, group=self.group)
 
+    # -- tensor collectives of the FP-step setup (slab_operators) --------------------
+    def halo_rows(self, exts, layouts, h: int = 1) -> None:
+        dist = self.dist
+        ((ext,), (lay,)) = (exts, layouts)
+        ops = []
+        for peer, snd, rcv in lay.halo_plan(h):
+            ops.append(dist.P2POp(dist.isend, ext[snd], peer, self.group))
+            ops.append(dist.P2POp(dist.irecv, ext[rcv], peer, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def all_to_all_blocks(self, sends):
+        (send,) = sends
+        recv = torch.empty_like(send)
+        self.dist.all_to_all_single(recv, send, group=self.group)
+        return [recv]
+
+    def allreduce_min_max(self, pairs):
+        ((mn, mx),) = pairs
+        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
+            else torch.device("cpu")
+        t = torch.tensor([-mn, mx], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return -float(t[0]), float(t[1])
+
 
 class LoopbackComm:
     """The same collectives over ``P`` slabs held by one process (local copies, in order)."""
@@ -235,6 +293,18 @@ class LoopbackComm:
         vals = torch.cat([s.buf(BUF_CONTRIB)[:1] for s in slabs])
         for s in slabs:
             s.buf(BUF_GATHER)[: len(slabs)].copy_(vals)
+
+    def halo_rows(self, exts, layouts, h: int = 1) -> None:
+        for ext, lay in zip(exts, layouts):
+            for peer, _, rcv in lay.halo_plan(h):
+                snd = next(sl for p2, sl, _ in layouts[peer].halo_plan(h) if p2 == lay.rank)
+                ext[rcv].copy_(exts[peer][snd])
+
+    def all_to_all_blocks(self, sends):
+        return [torch.stack([s[r] for s in sends]) for r in range(len(sends))]
+
+    def allreduce_min_max(self, pairs):
+        return min(p[0] for p in pairs), max(p[1] for p in pairs)
 
 
 # ------------------------------------------------------------------ the schedule
@@ -332,6 +402,103 @@ def slab_pcg(slabs, comm, b_slabs, x0_slabs, config: KrylovConfig = KrylovConfig
         outs.append(SolveOutcome(s.buf(BUF_X).view(s.layout.rows, s.n).clone(), it, hist,
                                  bool(conv)))
     return outs
+
+
+# ------------------------------------------------------------------ the FP-step setup
+def slab_operators(h_op, u_slabs, layouts, comm, beta: float, alpha: float, kind: str = "M",
+                   spacing: float = 1.0) -> list[SlabOperands]:
+    """Each rank's operators of one FP step from its own rows of ``u`` -- no
+    rank holds or recomputes the full image:
+
+    * a one-row halo of ``u`` from each neighbour (``comm.halo_rows``), then the diffusivity
+      of the rank's rows (``tvd_diffusivity_rows``, tv.py:42-71) and their block bands
+      (``tvd_diffusion_bands_rows``, tv.py:138-175);
+    * ``level2_project`` (precond.py:369-395) split at its transpose: the axis-1 band
+      projections of the rank's rows (``tvd_band_project_lines``), ONE all-to-all of the
+      ``R x R`` blocks of both level-1 results, the axis-0 projections of the rank's columns
+      with the eigenvalue epilogue ``lambda_H^2 + alpha proj`` -- which leaves exactly the
+      rank's rows of ``lambda^T``, the layout of the slab preconditioner's column pass;
+    * the global min / max (``comm.allreduce_min_max``) for the positivity check and the
+      ``1e-14 max`` clamp (precond.py:437-450), and ``d = 1 + alpha diag L > 0``
+      (precond.py:558-560); D_X kinds get ``sqrt(d)`` of their rows.
+
+    Every line is computed by the same kernels in the same order as the single-GPU assembly,
+    so the operands are bit-identical to slices of ``assemble_preconditioner`` /
+    ``DiffusionOperator`` (tests/test_gpu_slab.py).  ``u_slabs`` / ``layouts`` are this
+    process's slabs (one under :class:`TorchComm`, all ``P`` under :class:`LoopbackComm`).
+    Kinds: M, D_M (anti-reflective blur), R, D_R (reflective); zero-Neumann diffusion.
+    """
+    from .precond import IndefinitePreconditionerError
+
+    base = kind.replace("D_", "")
+    if base not in ("M", "R") or kind.endswith("_D"):
+        raise ValueError(f"slab setup supports the kinds M, D_M, R, D_R, got {kind!r}")
+    fam = nat.T_SINE_HAT if base == "M" else nat.T_DCT
+    lay0 = layouts[0]
+    n, P, R = lay0.n, lay0.nranks, lay0.rows
+    dev = u_slabs[0].device
+    lib = nat.load()
+    ctx = nat.context(dev)
+    dbl = dict(dtype=torch.float64, device=dev)
+    exts = []
+    for u, lay in zip(u_slabs, layouts):
+        ext = torch.zeros((R + 2, n), **dbl)
+        ext[1:R + 1].copy_(u)
+        exts.append(ext)
+    comm.halo_rows(exts, layouts)
+    parts, sends0, sends1 = [], [], []
+    min_d = float("inf")
+    for ext, lay in zip(exts, layouts):
+        lo = lay.row_lo
+        a_h, a_v = torch.empty((R, n + 1), **dbl), torch.empty((R + 1, n), **dbl)
+        nat.check(lib.tvd_diffusivity_rows(ctx, n, float(beta), float(spacing), ext.data_ptr(),
+                                           lo - 1, R + 2, lo, lo + R, a_h.data_ptr(),
+                                           a_v.data_ptr()))
+        diag, inner, block = (torch.empty((R, n), **dbl), torch.empty((R, n - 1), **dbl),
+                              torch.empty((R, n), **dbl))
+        nat.check(lib.tvd_diffusion_bands_rows(ctx, n, float(spacing), a_h.data_ptr(),
+                                               a_v.data_ptr(), lo, lo + R, diag.data_ptr(),
+                                               inner.data_ptr(), block.data_ptr()))
+        lam0, lam1 = torch.empty((R, n), **dbl), torch.zeros((R, n), **dbl)
+        nat.check(lib.tvd_band_project_lines(ctx, fam, n, R, diag.data_ptr(), inner.data_ptr(),
+                                             n - 1, 2.0, 0, None, 0.0, lam0.data_ptr(), None))
+        nb = R if lay.rank < P - 1 else R - 1  # block rows i <= n - 2
+        nat.check(lib.tvd_band_project_lines(ctx, fam, n, nb, block.data_ptr(), None, n, 0.0, 0,
+                                             None, 0.0, lam1.data_ptr(), None))
+        d = diag.mul(float(alpha)).add_(1.0)  # 1 + alpha diag L, numpy's two roundings
+        min_d = min(min_d, float(d.min()))
+        parts.append((a_h, a_v, d))
+        sends0.append(lam0.view(R, P, R).permute(1, 0, 2).contiguous())
+        sends1.append(lam1.view(R, P, R).permute(1, 0, 2).contiguous())
+    recv0, recv1 = comm.all_to_all_blocks(sends0), comm.all_to_all_blocks(sends1)
+    lamh_t = h_op.eigenvalues_device().t()
+    eigs, lo_hi = [], []
+    for lay, r0, r1 in zip(layouts, recv0, recv1):
+        lo = lay.row_lo
+        # line c = column lo + c of the level-1 results, element i = global row i
+        lines0 = r0.permute(2, 0, 1).reshape(R, n).contiguous()
+        lines1 = r1.permute(2, 0, 1).reshape(R, n).contiguous()
+        lh = lamh_t[lo:lo + R].contiguous()
+        eig_t = torch.empty((R, n), **dbl)
+        mm = (ctypes.c_double * 2)()
+        nat.check(lib.tvd_band_project_lines(ctx, fam, n, R, lines0.data_ptr(), lines1.data_ptr(),
+                                             n, 2.0, 1, lh.data_ptr(), float(alpha),
+                                             eig_t.data_ptr(), mm))
+        eigs.append(eig_t)
+        lo_hi.append((mm[0], mm[1]))
+    min_d = comm.allreduce_min_max([(min_d, 0.0)] * len(layouts))[0]
+    if not min_d > 0.0:
+        raise IndefinitePreconditionerError(kind, alpha, min_d)
+    mn, mx = comm.allreduce_min_max(lo_hi)
+    if not mn > 0.0:
+        raise IndefinitePreconditionerError(kind, alpha, mn)
+    floor = 1e-14 * mx
+    out = []
+    for (a_h, a_v, d), eig_t in zip(parts, eigs):
+        inv_t = 1.0 / torch.clamp(eig_t, min=floor)
+        out.append(SlabOperands(a_h, a_v, inv_t, d.sqrt() if kind.startswith("D_") else None,
+                                nat.PRE_TRANSFORM, fam, mn, mx, int((eig_t < floor).sum())))
+    return out
 
 
 def split_rows(a: torch.Tensor, nranks: int, rank: int) -> torch.Tensor:

@@ -132,6 +132,27 @@ def _comm_worker(rank, world, port, out):
         loop.allgather(ref)
         same = all(torch.equal(mine.buf(w), ref[rank].buf(w))
                    for w in (SL.BUF_P_EXT, SL.BUF_T_EXT, SL.BUF_RECV, SL.BUF_GATHER))
+        # the FP-step setup's collectives (slab_operators): u halo rows, the level-2 block
+        # all-to-all, the eigenvalue min / max
+        lays = [SL.SlabLayout(n, world, r, 1) for r in range(world)]
+        R = n // world
+
+        def ext_of(r):
+            return torch.rand((R + 2, n), generator=torch.Generator().manual_seed(7 + r),
+                              dtype=torch.float64)
+
+        def send_of(r):
+            return torch.rand((world, R, R), generator=torch.Generator().manual_seed(70 + r),
+                              dtype=torch.float64)
+
+        e_mine, e_ref = ext_of(rank), [ext_of(r) for r in range(world)]
+        comm.halo_rows([e_mine], [lays[rank]])
+        loop.halo_rows(e_ref, lays)
+        (recv,) = comm.all_to_all_blocks([send_of(rank)])
+        recv_ref = loop.all_to_all_blocks([send_of(r) for r in range(world)])[rank]
+        mm = comm.allreduce_min_max([(0.5 + rank, 2.0 * rank)])
+        same = same and torch.equal(e_mine, e_ref[rank]) and torch.equal(recv, recv_ref) and \
+            mm == loop.allreduce_min_max([(0.5 + r, 2.0 * r) for r in range(world)])
         # the whole PCG schedule over gloo with the numpy phases
         case = build_case()
         cfg = KrylovConfig(tol=1e-8, max_iterations=200)

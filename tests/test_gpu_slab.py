@@ -127,6 +127,42 @@ def test_slab_pcg_rader_8192_eight_slabs():
     assert float((x - ref.solution).norm() / ref.solution.norm()) < 1e-10
 
 
+def test_slab_first_fp_step_8192_matches_reference(golden):
+    """The config-5 problem itself (8192^2, seeded observation) over 8 row slabs against the
+    REFERENCE's own first FP step (tests/golden/c5_ops.npz, make_golden.py --c5: rhs =
+    H^T_fast v, u0 = v, kind M, tol 1e-4): count within one, iterate within 1e-8 over all
+    67M pixels (sketch) and on the subsample."""
+    from conftest import rel_err as _rel
+    from sketch import sketch_torch
+
+    g = golden("c5_ops.npz")
+    spec = CONFIGS["c5"]
+    n = spec.n
+    dev = torch.device("cuda")
+    h, v_np, _ = make_problem(spec, exact=False, device=dev)
+    v = torch.from_numpy(v_np).to(dev)
+    del v_np
+    hop = tvd.StructuredBlurOperator(tvd.SymmetricPsf(h), tvd.BoundaryCondition.ANTI_REFLECTIVE,
+                                     n, device=dev)
+    lop = tvd.DiffusionOperator(v, spec.beta, device=dev)
+    pre = tvd.assemble_preconditioner("M", hop, lop, spec.alpha)
+    system = tvd.NormalSystem(hop, lop, spec.alpha)
+    rhs = hop.apply_transpose(v)
+    P = 8
+    slabs = [SL.Slab(system, pre.apply_inverse, P, r) for r in range(P)]
+    outs = SL.slab_pcg(slabs, SL.LoopbackComm(), [SL.split_rows(rhs, P, r) for r in range(P)],
+                       [SL.split_rows(v, P, r) for r in range(P)],
+                       tvd.KrylovConfig(tol=spec.tol, max_iterations=2000))
+    x = torch.cat([o.solution for o in outs], dim=0)
+    assert outs[0].converged
+    assert abs(outs[0].iterations - int(g["fp1_iterations"])) <= 1
+    ref_norm = float(g["fp1_u_norm"])
+    sk = g["fp1_u_sketch"]
+    est = np.linalg.norm(sketch_torch(x, len(sk)) - sk) / np.sqrt(len(sk)) / ref_norm
+    assert est < 1e-8, est
+    assert _rel(x[::61, ::61].cpu().numpy(), g["fp1_u_sub"]) < 1e-8
+
+
 def test_slab_rejects_bad_geometry():
     spec = CONFIGS["c2a"]
     system, pre, rhs, v = _problem(512, spec.m, spec.sigma, spec.alpha, spec.beta)
@@ -159,6 +195,11 @@ def test_slab_pcg_over_nccl_single_rank():
                              [rhs.contiguous()], [v.contiguous()], cfg)
         assert out.converged and out.iterations == ref.iterations
         assert rel_err(out.solution.cpu().numpy(), ref.solution.cpu().numpy()) < 1e-12
+        # the distributed FP-step setup's NCCL tensor collectives (slab_operators)
+        (ops,) = SL.slab_operators(system.h_op, [v.contiguous()], [SL.SlabLayout(512, 1, 0, 1)],
+                                   SL.TorchComm(), spec.beta, spec.alpha, "M")
+        assert torch.equal(ops.inv_t, pre.inverse_eigenvalues_device.t())
+        assert torch.equal(ops.a_h, system.l_op.a_h_device)
     finally:
         dist.destroy_process_group()
 
@@ -181,3 +222,50 @@ def test_slab_pcg_graph_replay_matches_eager(nranks):
         assert a.iterations == b.iterations and a.converged and b.converged
         assert torch.equal(a.solution, b.solution)
         assert np.array_equal(a.residual_history, b.residual_history)
+
+
+@pytest.mark.parametrize("n,P,kind", [(512, 4, "M"), (512, 2, "D_M"), (2048, 8, "M"),
+                                      (512, 4, "R")])
+def test_distributed_fp_setup_is_bit_identical(n, P, kind):
+    """slab.slab_operators: each slab's diffusivity, its rows of lambda^-T (level-2
+    projection split at one all-to-all) and d_sqrt, computed from its own rows of u plus a
+    one-row halo, equal the slices of the single-GPU DiffusionOperator / assemble_preconditioner
+    bit for bit; a PCG over the resulting slabs equals one over slabs cut from the full
+    operators."""
+    bc = tvd.BoundaryCondition.REFLECTIVE if kind.endswith("R") else \
+        tvd.BoundaryCondition.ANTI_REFLECTIVE
+    g = torch.Generator(device="cpu").manual_seed(n + P)
+    u = torch.rand(n // 32, n // 32, generator=g, dtype=torch.float64)
+    u = torch.nn.functional.interpolate(u[None, None], size=(n, n), mode="bilinear")[0, 0].cuda()
+    u = u + 0.01 * torch.randn(n, n, generator=g, dtype=torch.float64).cuda()
+    hop = tvd.StructuredBlurOperator(tvd.SymmetricPsf(gen_psf("gaussian", 7, 3.0)), bc, n)
+    beta, alpha = 0.05, 1e-3
+    lop = tvd.DiffusionOperator(u, beta)
+    pre = tvd.assemble_preconditioner(kind, hop, lop, alpha)
+    layouts = [SL.SlabLayout(n, P, r, 1) for r in range(P)]
+    ops = SL.slab_operators(hop, [SL.split_rows(u, P, r) for r in range(P)], layouts,
+                            SL.LoopbackComm(), beta, alpha, kind)
+    R = n // P
+    inv_t = pre.inverse_eigenvalues_device.t()
+    for r, o in enumerate(ops):
+        lo = r * R
+        assert torch.equal(o.a_h, lop.a_h_device[lo:lo + R]), r
+        assert torch.equal(o.a_v, lop.a_v_device[lo:lo + R + 1]), r
+        assert torch.equal(o.inv_t, inv_t[lo:lo + R]), r
+        if kind.startswith("D_"):
+            assert torch.equal(o.d, pre.d_sqrt_device[lo:lo + R]), r
+    if kind.endswith("R"):
+        return  # the slab solver itself runs the M family (config 5)
+    system = tvd.NormalSystem(hop, lop, alpha)
+    rhs = hop.apply_transpose(u)
+    cfg = tvd.KrylovConfig(tol=1e-6, max_iterations=300)
+    comm = SL.LoopbackComm()
+    b_s = [SL.split_rows(rhs, P, r) for r in range(P)]
+    x_s = [SL.split_rows(u, P, r) for r in range(P)]
+    a = SL.slab_pcg([SL.Slab(system, pre.apply_inverse, P, r) for r in range(P)], comm, b_s, x_s,
+                    cfg)
+    b = SL.slab_pcg([SL.Slab.from_operands(hop, alpha, ops[r], P, r) for r in range(P)], comm,
+                    b_s, x_s, cfg)
+    assert [o.iterations for o in a] == [o.iterations for o in b]
+    for oa, ob in zip(a, b):
+        assert torch.equal(oa.solution, ob.solution)
