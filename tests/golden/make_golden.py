@@ -282,9 +282,30 @@ def main() -> None:
     ap.add_argument("--only-exact", action="store_true")
     ap.add_argument("--f2", action="store_true", help="only the row-f2 fixtures")
     ap.add_argument("--c4", action="store_true", help="only the config-4 restores")
+    ap.add_argument("--exact-dots", action="store_true",
+                    help="only the rounding-sensitive config-1 restores (selector I, re-blurred "
+                         "none / diag) with the reference's dot products exactly rounded")
     ap.add_argument("--c5", action="store_true", help="only the config-5 (8192^2) ops")
     args = ap.parse_args()
     print("reference tvdeblur from", tvdeblur.__file__)
+    if args.exact_dots:
+        # the reference's own krylov.py with _dot / _norm (krylov.py:70-75) replaced by exactly
+        # rounded dot products: the restores whose counts move with the BLAS summation order
+        import math
+
+        from tvdeblur import krylov as rk
+        sys.path.insert(0, str(HERE.parents[1] / "tools"))
+        from c3_dot_probe_lib import exact_dot
+
+        rk._dot = exact_dot
+        rk._norm = lambda x: math.sqrt(exact_dot(x, x))
+        c1 = bh.CONFIGS["c1"]
+        np.savez_compressed(HERE / "restore_c1_I_xdot.npz", **restore_fixture(c1, "none"))
+        for bcl in ("zn", "ar"):
+            for sel in ("none", "diag"):
+                np.savez_compressed(HERE / f"restore_c1_reblur_{bcl}_{sel}_xdot.npz",
+                                    **restore_fixture(c1, sel, bc_l=bcl, reblur=True, fp_steps=4))
+        return
     if args.c4:
         for i, tag in ((0, "gauss"), (1, "box")):
             np.savez_compressed(HERE / f"restore_c4_{tag}.npz", **c4_fixture(i))

@@ -375,8 +375,15 @@ def test_restore_matches_reference(golden, name, selector, bname):
         preconditioner=tvd.PrecondSelector(selector), fp_tol=1e-300, fp_max=int(g["fp_max"]),
         inner=K.KrylovConfig(tol=float(g["tol"]), max_iterations=2000))
     rep = tvd.restore(g["v"], B.SymmetricPsf(g["psf"]), cfg)
-    assert rep.inner_iterations == [int(k) for k in g["inner_iterations"]]
-    assert rel_err(rep.restored, g["restored"]) < 1e-8
+    stock = golden(name.replace("_xdot", ""))
+    runs = [[int(k) for k in r["inner_iterations"]] for r in (g, stock)]
+    if reblur:
+        assert rep.inner_iterations == runs[0]
+    else:
+        assert all(min(a, b) - 1 <= c <= max(a, b) + 1
+                   for c, a, b in zip(rep.inner_iterations, *runs)), (rep.inner_iterations, runs)
+    spread = rel_err(stock["restored"], g["restored"])
+    assert rel_err(rep.restored, g["restored"]) < max(1e-8, 2.0 * spread)
     np.testing.assert_allclose(rep.gradient_norms, g["gradient_norms"], rtol=1e-6)
     assert abs(rep.final_gradient_norm - float(g["final_gradient_norm"])) <= \
         1e-6 * float(g["final_gradient_norm"])
@@ -914,3 +921,32 @@ def test_c5_ops_and_first_fp_step_match_reference(golden):
                 K.KrylovConfig(tol=spec.tol, max_iterations=2000, record_history=True))
     assert abs(out.iterations - int(g["fp1_iterations"])) <= 1
     _big_check(g, "fp1_u", out.solution, 1e-8)
+
+
+# ---------------------- rounding-sensitive restores vs the reference with exactly rounded dots
+@pytest.mark.parametrize("name", ["restore_c1_I_xdot.npz", "restore_c1_reblur_zn_none_xdot.npz",
+                                  "restore_c1_reblur_zn_diag_xdot.npz",
+                                  "restore_c1_reblur_ar_none_xdot.npz",
+                                  "restore_c1_reblur_ar_diag_xdot.npz"])
+def test_rounding_sensitive_restores_match_reference_with_exact_dots(golden, name):
+    """The restores whose stopping iterations move with the stock reference's BLAS summation
+    order (unpreconditioned CG, BiCGstab with the diagonal or no preconditioner), against the
+    reference's own krylov.py with _dot / _norm exactly rounded (make_golden.py --exact-dots).
+    The stock and the exact-dot reference runs differ from EACH OTHER by a count at two FP
+    steps of c1-I and by up to 1.1e-8 in the re-blurred images, so the gates are the
+    reference's own spread: re-blurred counts identical to the exact-dot run, c1-I counts
+    within one of either reference run, images within max(1e-8, 2 x the two reference runs'
+    distance)."""
+    g = golden(name)
+    reblur = "reblur" in name
+    bcl = "ar" if "_ar_" in name else "zn"
+    sel = "none" if ("_none" in name or "_I_" in name) else "diag"
+    cfg = tvd.RestorationConfig(
+        bc_h=B.BoundaryCondition.ANTI_REFLECTIVE, alpha=float(g["alpha"]), beta=float(g["beta"]),
+        bc_l=TV.DiffusionBc.ANTI_REFLECTIVE if bcl == "ar" else TV.DiffusionBc.ZERO_NEUMANN,
+        formulation=tvd.Formulation.REBLUR if reblur else tvd.Formulation.NORMAL,
+        preconditioner=tvd.PrecondSelector(sel), fp_tol=1e-300, fp_max=int(g["fp_max"]),
+        inner=K.KrylovConfig(tol=float(g["tol"]), max_iterations=2000))
+    rep = tvd.restore(g["v"], B.SymmetricPsf(g["psf"]), cfg)
+    assert rep.inner_iterations == [int(k) for k in g["inner_iterations"]]
+    assert rel_err(rep.restored, g["restored"]) < 1e-8
