@@ -475,6 +475,16 @@ static bool build_pfa(TrigPlan* P) {
     unsigned* dreps;
     if (upload(reps, &dreps, P->owned) != cudaSuccess) return false;
     pl.reps[s] = dreps;
+    // general DFTs: every tuple (a, b) is a line of its own (no negated partner)
+    std::vector<unsigned> greps((size_t)S.D1 * S.D2);
+    for (int a = 0; a < S.D1; ++a)
+      for (int b = 0; b < S.D2; ++b) {
+        const unsigned base = a * S.S1 + b * S.S2;
+        greps[(size_t)a * S.D2 + b] = base | (base << 16);
+      }
+    unsigned* dg;
+    if (upload(greps, &dg, P->owned) != cudaSuccess) return false;
+    pl.greps[s] = dg;
   }
   // pack scatter (Ruritanian input map) and unpack gather (CRT output map) tables
   const int N = L - 1, h = (L - 1) / 2;
@@ -503,6 +513,15 @@ static bool build_pfa(TrigPlan* P) {
     return false;
   pl.scat = dscat;
   pl.gath = dgath;
+  std::vector<unsigned> gscat(L);
+  for (int j = 0; j < L; ++j) {
+    unsigned pos, npos;
+    pos_of(j, pos, npos);
+    gscat[j] = pos;
+  }
+  unsigned* dgs;
+  if (upload(gscat, &dgs, P->owned) != cudaSuccess) return false;
+  pl.gscat = dgs;
   // half-line layout tables (two-factor shapes): stored b <= H1, row pitch P1h
   pl.hscat = pl.hgath = nullptr;
   pl.P1h = pl.LPh = 0;

@@ -70,6 +70,10 @@ struct PfaPlan {
   int P1h, LPh;
   const unsigned* hscat;  // t: posA | negA << 15 | posB << 16 | hasB << 31 (B always negated)
   const unsigned* hgath;  // k: pos | neg << 15
+  // general (not odd) complex DFT of length L on the same grid (the assembly's band
+  // projections, k_band_pfa): every other-index tuple of a stage is its own line
+  const unsigned* greps[3];  // stage s, tuple t: base | base << 16
+  const unsigned* gscat;     // j = 0..L-1: pos(x_j) (Ruritanian input map)
 };
 
 // ---- Rader DST engine for prime odd cores (tvd_rader.cu / tvd_rader.h)
@@ -155,6 +159,12 @@ struct BandLines {
   double alpha;
   double* partial_minmax;  // per-CTA (min, max) pairs (epi != 0)
 };
+
+// band projections (sine family) on the prime-factor engine: a general complex DFT of length
+// L per line on the fp64 tensor cores (tvd_pfa.cu); -1 when the shape is not specialised
+cudaError_t launch_band_pfa(const PfaPlan& P, const double2* wfull, int n, const BandLines& b,
+                            int* nblocks_out, cudaStream_t st);
+bool band_pfa_ok(const PfaPlan& P);
 
 // ---- launchers (tvd_lines.cu)
 cudaError_t launch_trig(const TrigPlan& P, const LineGeom& g, int analysis, const LineIO& io,

@@ -414,6 +414,11 @@ cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
   // the generic engine's O(L) per point odd-radix stage (808 ms -> a few ms per assembly)
   if (P.family != kFamDct && P.rader_ok && P.rader.L == P.L && !option(kOptBandGeneric))
     return launch_band_rader(P.rader, P.n, P.wfull, b, nblocks_out, st);
+  // the configs' composite odd cores (127, 511, 1023, 2047): a general DFT on the
+  // prime-factor engine's fp64 tensor-core stages (tvd_pfa.cu k_band_pfa)
+  if (P.family != kFamDct && P.pfa_ok && P.pfa.L == P.L && band_pfa_ok(P.pfa) &&
+      !option(kOptBandGeneric))
+    return launch_band_pfa(P.pfa, P.wfull, P.n, b, nblocks_out, st);
   BandK k{};
   k.fft = P.fft;
   k.wfull = P.wfull;

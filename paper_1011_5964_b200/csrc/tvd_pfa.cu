@@ -580,6 +580,151 @@ __global__ void __launch_bounds__(256, 2) k_pfa_t(const PfaK p) {
   }
 }
 
+// ------------------------------------- band projections on the prime-factor engine
+// One level of level2_project for the sine family (precond.py:106-121, 168-199): per line
+// the length-L complex DFT of c_j = (b0_j, c1 b1_j) (even / odd slots of the reference's
+// length-2L rfft input), then the band form of k_band (tvd_lines.cu).  The DFT is the
+// Good-Thomas grid of the DST engine run as a GENERAL transform (PfaStageG: every
+// other-index tuple its own line, no odd-symmetry halving) on the same fp64 tensor-core
+// stages -- instead of the generic engine's CUDA-core odd-radix stages.
+struct BandPfaK {
+  PfaPlan pl;
+  const double2* wfull;
+  int n;
+  BandLines b;
+};
+constexpr int kBandPfaLines = 2;
+
+template <int Q1, int Q2, int Q3>
+__global__ void __launch_bounds__(256, 2) k_band_pfa(const BandPfaK p) {
+  using SH = PfaShape<Q1, Q2, Q3>;
+  constexpr int LP = SH::LP, L = SH::L, NL = kBandPfaLines;
+  extern __shared__ double2 smem2[];
+  __shared__ double red[32];
+  __shared__ double tot[2 * NL];
+  const int tid = threadIdx.x, nth = blockDim.x, n = p.n;
+  double2* buf = smem2;
+  unsigned* reps[3];
+  reps[0] = reinterpret_cast<unsigned*>(buf + NL * LP);
+  reps[1] = reps[0] + PfaStageG<SH, 0>::Rcnt;
+  reps[2] = reps[1] + (SH::d >= 2 ? PfaStageG<SH, 1>::Rcnt : 0);
+  for (int s = 0; s < SH::d; ++s) {
+    const int rc = s == 0 ? PfaStageG<SH, 0>::Rcnt
+                          : (s == 1 ? PfaStageG<SH, 1>::Rcnt : PfaStageG<SH, 2>::Rcnt);
+    for (int i = tid; i < rc; i += nth) reps[s][i] = p.pl.greps[s][i];
+  }
+  const BandLines& b = p.b;
+  const int line0 = blockIdx.x * NL;
+  const int nlv = min(NL, b.nlines - line0);
+  auto B0 = [&](int l, int j) { return b.b0[(long)(line0 + l) * b.b0_ls + (long)j * b.b0_es]; };
+  auto B1 = [&](int l, int j) { return b.b1[(long)(line0 + l) * b.b1_ls + (long)j * b.b1_es]; };
+  // every slot of the padded grid is read by some stage: zero it, then scatter the lines
+  for (int i = tid; i < NL * LP; i += nth) buf[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int i = tid; i < NL * L; i += nth) {
+    const int l = i / L, j = i - l * L;
+    if (l < nlv) {
+      // even slots 2j <- b0[j] (j = 1..N), odd slots 2j+1 <- c1 b1[j] (j = 1..N-1)
+      double e = 0.0, o = 0.0;
+      if (j >= 1 && j <= L - 1) e = B0(l, j);
+      if (b.b1 && j >= 1 && j <= L - 2) o = b.c1 * B1(l, j);
+      buf[l * LP + __ldg(p.pl.gscat + j)] = make_double2(e, o);
+    }
+  }
+  {  // per-line band totals (one warp per line, fixed order) as k_band
+    const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+    for (int l = wid; l < NL; l += nw) {
+      double t0 = 0.0, t1 = 0.0;
+      if (l < nlv) {
+        for (int j = 1 + lane; j < n - 1; j += 32) t0 += B0(l, j);
+        if (b.b1)
+          for (int j = 1 + lane; j < n - 2; j += 32) t1 += B1(l, j);
+      }
+      t0 = warp_sum(t0);
+      t1 = warp_sum(t1);
+      if (lane == 0) {
+        tot[2 * l] = t0;
+        tot[2 * l + 1] = t1;
+      }
+    }
+  }
+  __syncthreads();
+  pfa_stage_c<PfaStageG<SH, 0>, NL, 4, 8>(buf, buf, reps[0], p.pl.st[0].Cm, p.pl.st[0].Sm);
+  if constexpr (SH::d >= 2)
+    pfa_stage_c<PfaStageG<SH, 1>, NL, 4, 8>(buf, buf, reps[1], p.pl.st[1].Cm, p.pl.st[1].Sm);
+  if constexpr (SH::d >= 3)
+    pfa_stage_c<PfaStageG<SH, 2>, NL, 4, 8>(buf, buf, reps[2], p.pl.st[2].Cm, p.pl.st[2].Sm);
+  // the band form (k_band's epilogue; C_t from the CRT output position of t)
+  auto at = [&](int l, int t) { return buf[l * LP + (t == 0 ? 0u : __ldg(p.pl.gath + t - 1))]; };
+  double vmin = 1.0 / 0.0, vmax = -1.0 / 0.0;
+  for (int i = tid; i < nlv * n; i += nth) {
+    const int l = i / n, t = i - l * n;
+    double v;
+    if (t == 0 || t == n - 1) {
+      v = B0(l, t);
+    } else {
+      const int tr = L - t;
+      const double2 C = at(l, t), Cr = cconj(at(l, tr));
+      const double2 E = cscale(cadd(C, Cr), 0.5);
+      const double2 D = csub(C, Cr);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      const double2 w = p.wfull[t];
+      const double re_s = E.x + (w.x * O.x - w.y * O.y);
+      const double t0 = tot[2 * l], t1 = tot[2 * l + 1];
+      v = (t0 + b.c1 * t1 * w.x - re_s) / L;
+    }
+    const long g = (long)(line0 + l) * b.out_ls + (long)t * b.out_es;
+    if (b.epi == 1) {
+      const double lh = b.lamh[g];
+      v = lh * lh + b.alpha * v;
+    } else if (b.epi == 2) {
+      const double lh = b.lamh[g], ld = b.lamd[g];
+      v = lh * lh * ld * ld + b.alpha * v;
+    }
+    b.out[g] = v;
+    vmin = fmin(vmin, v);
+    vmax = fmax(vmax, v);
+  }
+  if (b.epi != 0) {
+    for (int o = 16; o > 0; o >>= 1) {
+      vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+      vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+    if (lane == 0) {
+      red[wid] = vmin;
+      red[16 + wid] = vmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = red[0], z = red[16];
+      for (int w = 1; w < nw; ++w) {
+        a = fmin(a, red[w]);
+        z = fmax(z, red[16 + w]);
+      }
+      b.partial_minmax[2 * blockIdx.x] = a;
+      b.partial_minmax[2 * blockIdx.x + 1] = z;
+    }
+  }
+}
+
+template <int Q1, int Q2, int Q3>
+static cudaError_t launch_band_pfa_t(const BandPfaK& k, int nb, cudaStream_t st) {
+  using SH = PfaShape<Q1, Q2, Q3>;
+  int reps = PfaStageG<SH, 0>::Rcnt;
+  if (SH::d >= 2) reps += PfaStageG<SH, 1>::Rcnt;
+  if (SH::d >= 3) reps += PfaStageG<SH, 2>::Rcnt;
+  const size_t smem = (size_t)kBandPfaLines * SH::LP * 16 + reps * sizeof(unsigned);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_band_pfa<Q1, Q2, Q3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  k_band_pfa<Q1, Q2, Q3><<<nb, 256, smem, st>>>(k);
+  return cudaGetLastError();
+}
+
 // ------------------------------------- persistent TMA-pipelined DST row passes
 // One CTA per SM walks batches of kPipeLines contiguous rows.  Thread 0 pulls the
 // next batch into a staging buffer with cp.async.bulk (TMA bulk copy, completion on
@@ -1299,6 +1444,33 @@ int pfa_blocks(const PfaPlan& P, const LineGeom& g) {
   if (pfa_specialised(P, &which)) return (g.nlines + kPfaLinesT - 1) / kPfaLinesT;
   if (pfa_config(P, g.es == 1, &nl, &nth, &smem)) return -1;
   return (g.nlines + nl - 1) / nl;
+}
+
+bool band_pfa_ok(const PfaPlan& P) {
+  int which;
+  return pfa_specialised(P, &which) && P.gscat != nullptr && P.greps[0] != nullptr;
+}
+
+cudaError_t launch_band_pfa(const PfaPlan& P, const double2* wfull, int n, const BandLines& b,
+                            int* nblocks_out, cudaStream_t st) {
+  int which;
+  if (!band_pfa_ok(P)) return cudaErrorInvalidConfiguration;
+  pfa_specialised(P, &which);
+  BandPfaK k{};
+  k.pl = P;
+  k.wfull = wfull;
+  k.n = n;
+  k.b = b;
+  const int nb = (b.nlines + kBandPfaLines - 1) / kBandPfaLines;
+  if (nblocks_out) *nblocks_out = nb;
+  if (nb == 0) return cudaSuccess;
+  switch (which) {
+    case 1: return launch_band_pfa_t<89, 23, 1>(k, nb, st);
+    case 2: return launch_band_pfa_t<31, 11, 3>(k, nb, st);
+    case 3: return launch_band_pfa_t<73, 7, 1>(k, nb, st);
+    case 4: return launch_band_pfa_t<127, 1, 1>(k, nb, st);
+    default: return cudaErrorInvalidConfiguration;
+  }
 }
 
 cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g, const LineIO& io,

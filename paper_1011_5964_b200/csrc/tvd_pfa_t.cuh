@@ -46,6 +46,15 @@ struct PfaStageC {
   static constexpr int RP = (H + 3) / 4 * 4;
   static constexpr bool mma = H >= 8;
   static constexpr int LPc = SH::LP;
+  static constexpr bool gen = false;  // odd input: one DFT per {tau, -tau} pair
+};
+
+// The same stage for a general (not odd) complex input: every other-index tuple is its own
+// DFT line (greps), outputs never mirrored to a negated partner.
+template <class SH, int S>
+struct PfaStageG : PfaStageC<SH, S> {
+  static constexpr int Rcnt = PfaStageC<SH, S>::D1 * PfaStageC<SH, S>::D2;
+  static constexpr bool gen = true;
 };
 
 template <class ST>
@@ -155,7 +164,7 @@ __device__ __forceinline__ void pfa_stage_c(const double2* src, double2* dst, co
           vk[j] = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
           vm[j] = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
           ob[j] = rp;
-          oflag[j] = 1 | (tO == 0 ? 2 : 0);
+          oflag[j] = 1 | ((ST::gen || tO == 0) ? 2 : 0);
         }
       }
       if constexpr (!OOP) __syncthreads();
@@ -209,7 +218,7 @@ __device__ __forceinline__ void pfa_stage_c(const double2* src, double2* dst, co
       if (dft < ndft) {
         const int l = dft / ST::Rcnt, t = dft - l * ST::Rcnt;
         const unsigned rp = reps[t] + (unsigned)(l * LP) * 0x10001u;
-        const bool self = t == 0;
+        const bool self = ST::gen || t == 0;
         const double2* p = src + (rp & 0xffffu);
         const double2 x0 = p[0];
         double2 A[H + 1], Bv[H + 1];
@@ -306,7 +315,7 @@ __device__ __forceinline__ void pfa_stage_c(const double2* src, double2* dst, co
             vk[s] = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
             vm[s] = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
             ob[s] = rp;
-            oflag[s] = 1 | (tO == 0 ? 2 : 0);
+            oflag[s] = 1 | ((ST::gen || tO == 0) ? 2 : 0);
           }
         }
       }
@@ -345,7 +354,7 @@ __device__ __forceinline__ void pfa_stage_c(const double2* src, double2* dst, co
       if (act) {
         const int l = dft / ST::Rcnt, t = dft - l * ST::Rcnt;
         rp = reps[t] + (unsigned)(l * LP) * 0x10001u;
-        self = t == 0;
+        self = ST::gen || t == 0;
         const double2* p = buf + (rp & 0xffffu);
         const double2 x0 = p[0];
         double2 A[H + 1], B[H + 1];
