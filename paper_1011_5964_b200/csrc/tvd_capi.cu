@@ -462,6 +462,23 @@ static bool build_pfa(TrigPlan* P) {
       return false;
     S.Cm = dcm;
     S.Sm = dsm;
+    {
+      const int nkt = S.KP / 8, nrs = S.RP / 4;
+      std::vector<double> cf((size_t)S.KP * S.RP), sf((size_t)S.KP * S.RP);
+      for (int kt = 0; kt < nkt; ++kt)
+        for (int rs = 0; rs < nrs; ++rs)
+          for (int lane = 0; lane < 32; ++lane) {
+            const size_t src = (size_t)(kt * 8 + (lane >> 2)) * S.RP + rs * 4 + (lane & 3);
+            const size_t dst = ((size_t)kt * nrs + rs) * 32 + lane;
+            cf[dst] = cm[src];
+            sf[dst] = sm[src];
+          }
+      double *dcf, *dsf;
+      if (upload(cf, &dcf, P->owned) != cudaSuccess || upload(sf, &dsf, P->owned) != cudaSuccess)
+        return false;
+      S.Cf = dcf;
+      S.Sf = dsf;
+    }
     // representative line bases of this stage (line 0): base | negated base << 16
     std::vector<unsigned> reps(S.Rcnt);
     for (int t = 0; t < S.Rcnt; ++t) {

@@ -48,6 +48,11 @@ struct PfaStage {
   int use_mma, KP, RP;
   const double* Cm;    // [k][r-1] = cos(2 pi r k / q), k = 0..H (row 0 all ones)
   const double* Sm;    // [k][r-1] = sin(2 pi r k / q)
+  // the same tables in DMMA A-fragment order: [(kt * (RP / 4) + rs) * 32 + lane] =
+  // Cm[(kt * 8 + (lane >> 2)) * RP + rs * 4 + (lane & 3)], so a warp's fragment load is one
+  // contiguous 256-byte read (2 L1 wavefronts) instead of eight 32-byte row pieces
+  const double* Cf;
+  const double* Sf;
 };
 
 // Good-Thomas line layout (row-major over the factors).  Two-factor shapes pad the

@@ -454,13 +454,16 @@ __device__ __forceinline__ void pfa_transform_c(double2* buf, unsigned* const* r
                                                 const PfaPlan& pl, int stages) {
   using SH = PfaShape<Q1, Q2, Q3>;
   if (stages >= 1)
-    pfa_stage_c<PfaStageC<SH, 0>, kPfaLinesT, 4, 8>(buf, buf, reps[0], pl.st[0].Cm, pl.st[0].Sm);
+    pfa_stage_c<PfaStageC<SH, 0>, kPfaLinesT, 4, 8>(buf, buf, reps[0], pl.st[0].Cm, pl.st[0].Sm,
+                pl.st[0].Cf, pl.st[0].Sf);
   if constexpr (SH::d >= 2)
     if (stages >= 2)
-      pfa_stage_c<PfaStageC<SH, 1>, kPfaLinesT, 4, 8>(buf, buf, reps[1], pl.st[1].Cm, pl.st[1].Sm);
+      pfa_stage_c<PfaStageC<SH, 1>, kPfaLinesT, 4, 8>(buf, buf, reps[1], pl.st[1].Cm, pl.st[1].Sm,
+                pl.st[1].Cf, pl.st[1].Sf);
   if constexpr (SH::d >= 3)
     if (stages >= 3)
-      pfa_stage_c<PfaStageC<SH, 2>, kPfaLinesT, 4, 8>(buf, buf, reps[2], pl.st[2].Cm, pl.st[2].Sm);
+      pfa_stage_c<PfaStageC<SH, 2>, kPfaLinesT, 4, 8>(buf, buf, reps[2], pl.st[2].Cm, pl.st[2].Sm,
+                pl.st[2].Cf, pl.st[2].Sf);
 }
 
 template <int Q1, int Q2, int Q3>
@@ -649,11 +652,14 @@ __global__ void __launch_bounds__(256, 2) k_band_pfa(const BandPfaK p) {
     }
   }
   __syncthreads();
-  pfa_stage_c<PfaStageG<SH, 0>, NL, 4, 8>(buf, buf, reps[0], p.pl.st[0].Cm, p.pl.st[0].Sm);
+  pfa_stage_c<PfaStageG<SH, 0>, NL, 4, 8>(buf, buf, reps[0], p.pl.st[0].Cm, p.pl.st[0].Sm,
+                p.pl.st[0].Cf, p.pl.st[0].Sf);
   if constexpr (SH::d >= 2)
-    pfa_stage_c<PfaStageG<SH, 1>, NL, 4, 8>(buf, buf, reps[1], p.pl.st[1].Cm, p.pl.st[1].Sm);
+    pfa_stage_c<PfaStageG<SH, 1>, NL, 4, 8>(buf, buf, reps[1], p.pl.st[1].Cm, p.pl.st[1].Sm,
+                p.pl.st[1].Cf, p.pl.st[1].Sf);
   if constexpr (SH::d >= 3)
-    pfa_stage_c<PfaStageG<SH, 2>, NL, 4, 8>(buf, buf, reps[2], p.pl.st[2].Cm, p.pl.st[2].Sm);
+    pfa_stage_c<PfaStageG<SH, 2>, NL, 4, 8>(buf, buf, reps[2], p.pl.st[2].Cm, p.pl.st[2].Sm,
+                p.pl.st[2].Cf, p.pl.st[2].Sf);
   // the band form (k_band's epilogue; C_t from the CRT output position of t)
   auto at = [&](int l, int t) { return buf[l * LP + (t == 0 ? 0u : __ldg(p.pl.gath + t - 1))]; };
   double vmin = 1.0 / 0.0, vmax = -1.0 / 0.0;
@@ -837,14 +843,17 @@ __device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, uns
   double2* x = a;
   double2* y = O ? b : a;
   if (stages < 1) return a;
-  pfa_stage_c<PfaStageC<SH, 0>, NL, 4, NW, TPW, O>(x, y, reps[0], pl.st[0].Cm, pl.st[0].Sm);
+  pfa_stage_c<PfaStageC<SH, 0>, NL, 4, NW, TPW, O>(x, y, reps[0], pl.st[0].Cm, pl.st[0].Sm,
+                pl.st[0].Cf, pl.st[0].Sf);
   if constexpr (SH::d >= 2) {
     if (stages < 2) return y;
-    pfa_stage_c<PfaStageC<SH, 1>, NL, 4, NW, TPW, O>(y, x, reps[1], pl.st[1].Cm, pl.st[1].Sm);
+    pfa_stage_c<PfaStageC<SH, 1>, NL, 4, NW, TPW, O>(y, x, reps[1], pl.st[1].Cm, pl.st[1].Sm,
+                pl.st[1].Cf, pl.st[1].Sf);
   }
   if constexpr (SH::d >= 3) {
     if (stages < 3) return x;
-    pfa_stage_c<PfaStageC<SH, 2>, NL, 4, NW, TPW, O>(x, y, reps[2], pl.st[2].Cm, pl.st[2].Sm);
+    pfa_stage_c<PfaStageC<SH, 2>, NL, 4, NW, TPW, O>(x, y, reps[2], pl.st[2].Cm, pl.st[2].Sm,
+                pl.st[2].Cf, pl.st[2].Sf);
   }
   return SH::d == 2 ? x : y;
 }

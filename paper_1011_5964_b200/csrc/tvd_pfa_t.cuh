@@ -75,7 +75,9 @@ __device__ __forceinline__ void rep_ab(int t, int& a, int& b) {
 // otherwise src == dst and every round holds its outputs across an in-place barrier.
 template <class ST, int NL, int MT = 4, int NW = 0, int TPWc = 3, bool OOP = false>
 __device__ __forceinline__ void pfa_stage_c(const double2* src, double2* dst, const unsigned* reps,
-                                            const double* Cm, const double* Sm) {
+                                            const double* Cm, const double* Sm,
+                                            const double* __restrict__ Cf = nullptr,
+                                            const double* __restrict__ Sf = nullptr) {
   double2* buf = dst;  // in-place paths (src == dst)
   constexpr int kMmaTiles = MT;  // output tiles a warp holds across the in-place barrier
   constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LPc;
@@ -99,9 +101,9 @@ __device__ __forceinline__ void pfa_stage_c(const double2* src, double2* dst, co
     const int krow = kt * 8 + (lane >> 2);
     double ca[nrs], sa[nrs];
 #pragma unroll
-    for (int rs = 0; rs < nrs; ++rs) {
-      ca[rs] = Cm[krow * ST::RP + rs * 4 + (lane & 3)];
-      sa[rs] = Sm[krow * ST::RP + rs * 4 + (lane & 3)];
+    for (int rs = 0; rs < nrs; ++rs) {  // fragment-ordered tables: coalesced 256-byte reads
+      ca[rs] = __ldg(Cf + (kt * nrs + rs) * 32 + lane);
+      sa[rs] = __ldg(Sf + (kt * nrs + rs) * 32 + lane);
     }
 #ifdef TVD_PIPE_TIMING
     const long long ts_ = clock64();
@@ -441,15 +443,14 @@ struct HalfStage {
 // ~60 registers.  Every output's DMMA sequence (fragments, k-step order) is the k-tile-owner
 // stage's, so the results are bit-identical.
 template <class ST, int NL, int NW>
-__device__ __forceinline__ void half_stage_co(const double2* buf, const double* __restrict__ Cm,
-                                              const double* __restrict__ Sm, double2* out) {
+__device__ __forceinline__ void half_stage_co(const double2* buf, const double* __restrict__ Cf,
+                                              const double* __restrict__ Sf, double2* out) {
   constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LP;
   constexpr bool PT = ST::partnered;
   constexpr int ndft = NL * ST::Rcnt;
   constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* bufd = reinterpret_cast<const double*>(buf);
-  const int coff = (lane >> 2) * ST::RP + (lane & 3);
   for (int ct = warp; ct < nct; ct += NW) {
     const int dB = min((ct * 8 + (lane >> 2)) >> 1, ndft - 1);
     const int lB = dB / ST::Rcnt, tB = dB - lB * ST::Rcnt;
@@ -467,9 +468,9 @@ __device__ __forceinline__ void half_stage_co(const double2* buf, const double* 
       const double fb = PT ? x1 + x2 : x1 - x2;
 #pragma unroll
       for (int kt = 0; kt < nkt; ++kt) {
-        const int o = kt * 8 * ST::RP + coff + rs * 4;
-        dmma884(acc[kt][0], acc[kt][1], __ldg(Cm + o), fa);
-        dmma884(acc[kt][2], acc[kt][3], __ldg(Sm + o), fb);
+        const int o = (kt * nrs + rs) * 32 + lane;  // A-fragment order (PfaStage::Cf)
+        dmma884(acc[kt][0], acc[kt][1], __ldg(Cf + o), fa);
+        dmma884(acc[kt][2], acc[kt][3], __ldg(Sf + o), fb);
       }
     }
     const int dO = ct * 4 + (lane & 3);
@@ -507,14 +508,16 @@ __device__ __forceinline__ void half_stage_co(const double2* buf, const double* 
 
 template <class ST, int NL, int NW, int TPWc, bool CSM = false, bool OOP = false, bool CO = false>
 __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const double* Sm,
-                                           double2* dst = nullptr) {
+                                           double2* dst = nullptr,
+                                           const double* __restrict__ Cf = nullptr,
+                                           const double* __restrict__ Sf = nullptr) {
   constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LP;
   constexpr bool PT = ST::partnered;
   const int tid = threadIdx.x, nth = blockDim.x;
   constexpr int ndft = NL * ST::Rcnt;
   double2* const out = OOP ? dst : buf;
   if constexpr (ST::mma && CO && OOP) {
-    half_stage_co<ST, NL, NW>(buf, Cm, Sm, dst);
+    half_stage_co<ST, NL, NW>(buf, Cf, Sf, dst);
     return;
   }
   if constexpr (ST::mma) {
@@ -534,9 +537,9 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
     const double* smk = Sm + krow * ST::RP + (lane & 3);
     if constexpr (!CSM) {
 #pragma unroll
-      for (int rs = 0; rs < nrs; ++rs) {
-        ca[rs] = cmk[rs * 4];
-        sa[rs] = smk[rs * 4];
+      for (int rs = 0; rs < nrs; ++rs) {  // fragment-ordered tables: coalesced 256-byte reads
+        ca[rs] = __ldg(Cf + (kt * nrs + rs) * 32 + lane);
+        sa[rs] = __ldg(Sf + (kt * nrs + rs) * 32 + lane);
       }
     }
 #ifdef TVD_PIPE_TIMING
@@ -727,12 +730,14 @@ __device__ __forceinline__ void half_transform(double2* buf, const PfaPlan& pl, 
   const double* s0 = CSM ? cs + HC::n0 : pl.st[0].Sm;
   // OOP: stage 0 buf -> buf2, stage 1 buf2 -> buf (the result lands in buf either way)
   if (stages >= 1)
-    half_stage<HalfStage<SH, 0>, NL, NW, TPW, CSM, OOP, (CO >= 1)>(buf, c0, s0, buf2);
+    half_stage<HalfStage<SH, 0>, NL, NW, TPW, CSM, OOP, (CO >= 1)>(buf, c0, s0, buf2, pl.st[0].Cf,
+                                                                   pl.st[0].Sf);
   if (stages >= 2) {
     if constexpr (OOP)
-      half_stage<HalfStage<SH, 1>, NL, NW, TPW, false, true, (CO >= 2)>(buf2, pl.st[1].Cm,
-                                                                        pl.st[1].Sm, buf);
+      half_stage<HalfStage<SH, 1>, NL, NW, TPW, false, true, (CO >= 2)>(
+          buf2, pl.st[1].Cm, pl.st[1].Sm, buf, pl.st[1].Cf, pl.st[1].Sf);
     else
-      half_stage<HalfStage<SH, 1>, NL, NW, TPW>(buf, pl.st[1].Cm, pl.st[1].Sm);
+      half_stage<HalfStage<SH, 1>, NL, NW, TPW>(buf, pl.st[1].Cm, pl.st[1].Sm, nullptr, pl.st[1].Cf,
+                                                pl.st[1].Sf);
   }
 }
