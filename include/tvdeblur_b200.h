@@ -179,6 +179,11 @@ int tvd_diffusion_bands_bc(tvd_ctx* ctx, int n, double spacing, int bc_l, const 
  * of a len x cols array when axis == 0); inverse selects DCT analysis */
 int tvd_transform_lines(tvd_ctx* ctx, int kind, int rows, int cols, int axis, const double* in,
                         double* out, int inverse);
+/* Anti-reflective transform T (inverse 0, transpose 0), T^-1 (1, 0), T^T (0, 1), T^-T (1, 1)
+ * of `rows` contiguous lines of length `cols` >= 5 (reference transforms.py:96-140 ar_apply;
+ * the transposes feed the transform-domain blur adjoint, blur.py:302-314).  in == out ok. */
+int tvd_ar_lines(tvd_ctx* ctx, int rows, int cols, const double* in, double* out, int inverse,
+                 int transpose);
 /* X G X^T on a square n x n grid: axis 0 then axis 1 (tensor_apply_2d) */
 int tvd_transform_2d(tvd_ctx* ctx, int kind, int n, const double* in, double* out, int inverse);
 

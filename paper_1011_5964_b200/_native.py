@@ -74,6 +74,7 @@ _SIGNATURES = {
     "tvd_diffusion_bands_bc": ([_vp, _i, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "tvd_transform_lines": ([_vp, _i, _i, _i, _i, _vp, _vp, _i], _i),
     "tvd_transform_2d": ([_vp, _i, _i, _vp, _vp, _i], _i),
+    "tvd_ar_lines": ([_vp, _i, _i, _vp, _vp, _i, _i], _i),
     "tvd_precond_assemble": ([_vp, _i, _i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               ctypes.POINTER(_d), ctypes.POINTER(_d), ctypes.POINTER(_ll)], _i),
     "tvd_precond_assemble_async": ([_vp, _i, _i, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -157,8 +157,26 @@ class StructuredBlurOperator:
         return self._run(u, 2)
 
     reblur_apply = apply
-    apply_fast = apply
-    apply_transpose_fast = apply_transpose
+
+    def apply_fast(self, u):
+        """Transform-domain ``H u``: analysis, eigenvalue scaling, synthesis (blur.py:293-300).
+        Equal to :meth:`apply` up to rounding; the solvers use the exact band form."""
+        from .transforms import tensor_apply_2d
+
+        t, was_np = self._check_shape(u)
+        kind = self.transform
+        mid = self.eigenvalues_device() * tensor_apply_2d(kind, t, inverse=True)
+        return nat.to_host_like(tensor_apply_2d(kind, mid), was_np)
+
+    def apply_transpose_fast(self, u):
+        """Transform-domain ``H^T u = X^-T (lam .* X^T u)`` (blur.py:302-314): the
+        anti-reflective ``T`` is not orthogonal, so this runs its transposed forms."""
+        from .transforms import tensor_apply_2d
+
+        t, was_np = self._check_shape(u)
+        kind = self.transform
+        mid = self.eigenvalues_device() * tensor_apply_2d(kind, t, transpose=True)
+        return nat.to_host_like(tensor_apply_2d(kind, mid, inverse=True, transpose=True), was_np)
 
     # -- eigen structure -------------------------------------------------
     @property

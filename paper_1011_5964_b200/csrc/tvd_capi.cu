@@ -1732,6 +1732,49 @@ int tvd_transform_lines(tvd_ctx* c, int kind, int rows, int cols, int axis, cons
   return run_lines(c, kind, geom, inverse ? 1 : 0, io, nullptr);
 }
 
+// 1D anti-reflective transform T, T^-1, T^T, T^-T over `rows` contiguous lines of length
+// `cols` (transforms.py:96-140 ar_apply): Shat line passes plus the rank-2 factor as
+// elementwise / per-line reduction kernels.  in == out is allowed.
+int tvd_ar_lines(tvd_ctx* c, int rows, int cols, const double* in, double* out, int inverse,
+                 int transpose) {
+  if (!c || !in || !out) return fail(TVD_ERR_INVALID, "null argument");
+  if (rows < 1) return fail(TVD_ERR_INVALID, "no lines");
+  DeviceGuard g(c->device);
+  const tvd_ctx::ArTables* T;
+  int rc = get_ar_tables(c, cols, &T);
+  if (rc) return rc;
+  const size_t bytes = (size_t)rows * cols * sizeof(double);
+  if (!transpose) {
+    if (!inverse) {  // T v = Shat (v + U v)
+      if (in != out)
+        TVD_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, c->stream));
+      TVD_LAUNCH(c, kCatVec, 1, launch_ar_corr_rows(out, rows, cols, 1.0, T->ql, T->qr, c->stream));
+      return tvd_transform_lines(c, TVD_TRANSFORM_SINE_HAT, rows, cols, 1, out, out, 0);
+    }
+    // T^-1 v = (I - U) Shat v (Shat keeps the borders, so the correction reads them from out)
+    rc = tvd_transform_lines(c, TVD_TRANSFORM_SINE_HAT, rows, cols, 1, in, out, 0);
+    if (rc) return rc;
+    TVD_LAUNCH(c, kCatVec, 1, launch_ar_corr_rows(out, rows, cols, -1.0, T->ql, T->qr, c->stream));
+    return TVD_OK;
+  }
+  double* sums;
+  rc = partial_capacity(c, 2 * (size_t)rows + 64, &sums);
+  if (rc) return rc;
+  if (!inverse) {  // T^T v = (I + U^T) Shat v
+    rc = tvd_transform_lines(c, TVD_TRANSFORM_SINE_HAT, rows, cols, 1, in, out, 0);
+    if (rc) return rc;
+    TVD_LAUNCH(c, kCatVec, 1, launch_ar_dots_rows(out, rows, cols, T->ql, T->qr, sums, c->stream));
+    TVD_LAUNCH(c, kCatVec, 1, launch_ar_border_add(out, rows, cols, 1.0, sums, c->stream));
+    return TVD_OK;
+  }
+  // T^-T v = Shat (I - U^T) v: the projections of the untransformed interior
+  TVD_LAUNCH(c, kCatVec, 1, launch_ar_dots_rows(in, rows, cols, T->ql, T->qr, sums, c->stream));
+  rc = tvd_transform_lines(c, TVD_TRANSFORM_SINE_HAT, rows, cols, 1, in, out, 0);
+  if (rc) return rc;
+  TVD_LAUNCH(c, kCatVec, 1, launch_ar_border_add(out, rows, cols, -1.0, sums, c->stream));
+  return TVD_OK;
+}
+
 int tvd_transform_2d(tvd_ctx* c, int kind, int n, const double* in, double* out, int inverse) {
   if (kind == TVD_TRANSFORM_ANTI_REFLECTIVE) {  // T (x) T or its inverse: two transposing row passes
     if (!c || !in || !out) return fail(TVD_ERR_INVALID, "null argument");

@@ -179,6 +179,12 @@ cudaError_t launch_band_project(const TrigPlan& P, int axis, const BandLines& b,
 int trig_lines_per_cta(const TrigPlan& P, bool contiguous, int* nthreads, size_t* smem);
 // AR (P family) projection: border eigenvalues of each projected line from its interior
 // (weights c), optionally followed by the eigenvalue epilogue with per-CTA (min, max) pairs
+cudaError_t launch_ar_corr_rows(double* x, int rows, int cols, double sign, const double* ql,
+                                const double* qr, cudaStream_t st);
+cudaError_t launch_ar_dots_rows(const double* src, int rows, int cols, const double* ql,
+                                const double* qr, double* sums, cudaStream_t st);
+cudaError_t launch_ar_border_add(double* x, int rows, int cols, double sign, const double* sums,
+                                 cudaStream_t st);
 cudaError_t launch_ar_corr(double* x, int n, int axis, double sign, const double* ql,
                            const double* qr, const int* skip, cudaStream_t st);
 cudaError_t launch_ar_lines(double* proj, int nlines, int n, long ls, long es, const double* c,

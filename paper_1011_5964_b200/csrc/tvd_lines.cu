@@ -547,4 +547,82 @@ cudaError_t launch_ar_corr(double* x, int n, int axis, double sign, const double
   return cudaGetLastError();
 }
 
+// ---- 1D anti-reflective transform over contiguous lines (rows x cols, lines = rows)
+// T = Shat (I + U), transforms.py:96-140.  The plain forms add / subtract the rank-2 border
+// correction x_0 q_L + x_last q_R on the interior (k_ar_corr_rows); the transposed forms
+// T^T = (I + U^T) Shat and T^-T = Shat (I - U^T) add / subtract the projections
+// sum_t x_t q_L[t], sum_t x_t q_R[t] of the interior on the two border entries
+// (k_ar_dots_rows: one warp per line, fixed lane-strided order + shuffle tree, then
+// k_ar_border_add).
+__global__ void k_ar_corr_rows(double* __restrict__ x, int rows, int cols, double sign,
+                               const double* __restrict__ ql, const double* __restrict__ qr) {
+  const long N = (long)rows * cols;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < N;
+       g += (long)gridDim.x * blockDim.x) {
+    const long i = g / cols;
+    const int t = (int)(g - i * cols);
+    if (t == 0 || t == cols - 1) continue;
+    const double b0 = x[i * cols], b1 = x[i * cols + cols - 1];
+    const double corr = __dadd_rn(__dmul_rn(b0, ql[t - 1]), __dmul_rn(b1, qr[t - 1]));
+    x[g] = sign > 0 ? __dadd_rn(x[g], corr) : __dsub_rn(x[g], corr);
+  }
+}
+
+__global__ void k_ar_dots_rows(const double* __restrict__ src, int rows, int cols,
+                               const double* __restrict__ ql, const double* __restrict__ qr,
+                               double* __restrict__ sums) {
+  const int lane = threadIdx.x & 31;
+  const long wpb = blockDim.x >> 5;
+  for (long line = blockIdx.x * wpb + (threadIdx.x >> 5); line < rows; line += (long)gridDim.x * wpb) {
+    const double* x = src + line * cols;
+    double sl = 0.0, sr = 0.0;
+    for (int t = 1 + lane; t < cols - 1; t += 32) {
+      sl += x[t] * ql[t - 1];
+      sr += x[t] * qr[t - 1];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      sl += __shfl_down_sync(0xffffffffu, sl, o);
+      sr += __shfl_down_sync(0xffffffffu, sr, o);
+    }
+    if (lane == 0) {
+      sums[2 * line] = sl;
+      sums[2 * line + 1] = sr;
+    }
+  }
+}
+
+__global__ void k_ar_border_add(double* __restrict__ x, int rows, int cols, double sign,
+                                const double* __restrict__ sums) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < 2L * rows;
+       i += (long)gridDim.x * blockDim.x) {
+    const long line = i >> 1;
+    double* p = x + line * cols + ((i & 1) ? cols - 1 : 0);
+    *p = sign > 0 ? __dadd_rn(*p, sums[i]) : __dsub_rn(*p, sums[i]);
+  }
+}
+
+static int ar_grid(long work, int per_block) {
+  long nb = (work + per_block - 1) / per_block;
+  if (nb > 16L * kSMs) nb = 16L * kSMs;
+  return (int)(nb < 1 ? 1 : nb);
+}
+
+cudaError_t launch_ar_corr_rows(double* x, int rows, int cols, double sign, const double* ql,
+                                const double* qr, cudaStream_t st) {
+  k_ar_corr_rows<<<ar_grid((long)rows * cols, 256), 256, 0, st>>>(x, rows, cols, sign, ql, qr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ar_dots_rows(const double* src, int rows, int cols, const double* ql,
+                                const double* qr, double* sums, cudaStream_t st) {
+  k_ar_dots_rows<<<ar_grid(rows, 8), 256, 0, st>>>(src, rows, cols, ql, qr, sums);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ar_border_add(double* x, int rows, int cols, double sign, const double* sums,
+                                 cudaStream_t st) {
+  k_ar_border_add<<<ar_grid(2L * rows, 256), 256, 0, st>>>(x, rows, cols, sign, sums);
+  return cudaGetLastError();
+}
+
 }  // namespace tvd

@@ -833,6 +833,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 // outputs held across barriers) -- measured no faster than in place on B200 at 2047, so
 // off.  Returns the buffer holding the result.
 constexpr bool kPipeOOP = false;
+constexpr bool kPipeAliasStage = true;
 
 template <int Q1, int Q2, int Q3, int NL, int NT, int TPW>
 __device__ __forceinline__ double2* pfa_transform_nl(double2* a, double2* b, unsigned* const* reps,
@@ -889,13 +890,19 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   constexpr bool OOPB = kPipeOOP || (HALF && HO);     // a second line buffer
   double2* buf2 = OOPB ? buf + B * LP : buf;          // second buffer of out-of-place stages
   double2* res = buf;                                 // buffer holding the transform result
-  double* stage = reinterpret_cast<double*>(buf + (OOPB ? 2 : 1) * B * LP);
+  // AL: the staging rows alias the second line buffer (free from the end of a batch's last
+  // stage until the next batch's first stage), so the next batch's rows are fetched while
+  // this batch unpacks; the CTA then needs two line buffers only (three CTAs per SM at 2047)
+  constexpr bool AL = HALF && HO && kPipeAliasStage;
+  double* stage = AL ? reinterpret_cast<double*>(buf2)
+                     : reinterpret_cast<double*>(buf + (OOPB ? 2 : 1) * B * LP);
   // scatter / gather tables are read coalesced (indexed by t) through L1, leaving the
   // shared memory to the padded lines and the staging rows
   const unsigned* __restrict__ scat = HALF ? p.pl.hscat : p.pl.scat;
   const unsigned* __restrict__ gath = HALF ? p.pl.hgath : p.pl.gath;
   unsigned* reps[3];
-  reps[0] = reinterpret_cast<unsigned*>(stage + B * n);
+  reps[0] = AL ? reinterpret_cast<unsigned*>(buf + 2 * B * LP)
+               : reinterpret_cast<unsigned*>(stage + B * n);
   reps[1] = reps[0] + PfaStageC<SH, 0>::Rcnt;
   reps[2] = reps[1] + (SH::d >= 2 ? PfaStageC<SH, 1>::Rcnt : 0);
   for (int s = 0; s < SH::d; ++s) {
@@ -903,9 +910,12 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
                           : (s == 1 ? PfaStageC<SH, 1>::Rcnt : PfaStageC<SH, 2>::Rcnt);
     for (int i = tid; i < rc; i += nth) reps[s][i] = p.pl.reps[s][i];
   }
-  if constexpr (HALF && HO) {  // out-of-place stages: the second buffer's pads read as zero
+  if constexpr (HALF && HO && !AL) {  // out-of-place stages: the second buffer's pads read as zero
     for (int i = tid; i < B * LP; i += nth) buf2[i] = make_double2(0.0, 0.0);
   }
+  if constexpr (AL)
+    static_assert(HalfShape<Q1, Q2>::P1h == HalfShape<Q1, Q2>::H1 + 1,
+                  "aliased staging re-zeroes only the line-end pad of the second buffer");
   // CSM: the q0 stage's cos / sin tables staged in shared memory (after the reps, 8-aligned)
   double* csm = nullptr;
   if constexpr (CSM) {
@@ -913,8 +923,8 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     csm = reinterpret_cast<double*>(smraw) +
           (((reinterpret_cast<unsigned char*>(reps[2] + 64) - smraw) + 7) / 8);
     for (int i = tid; i < HC::n0; i += nth) {
-      csm[i] = p.pl.st[0].Cm[i];
-      csm[HC::n0 + i] = p.pl.st[0].Sm[i];
+      csm[i] = p.pl.st[0].Cf[i];
+      csm[HC::n0 + i] = p.pl.st[0].Sf[i];
     }
   }
   // Batches: F full rounds in which CTA c takes lines (j G + c) B .. +B (concurrent CTAs
@@ -1090,11 +1100,20 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     }
     __syncthreads();
     PIPE_T(1);
-    if (BIN) {
-      if (jb + 1 < nb_cta) issue_blocked(jb + 1);
-    } else if (tid == 0 && jb + 1 < nb_cta) {
-      fence_proxy_async();  // staging was read through the generic proxy
-      issue(jb + 1);
+    auto issue_next = [&]() {
+      if (BIN) {
+        if (jb + 1 < nb_cta) issue_blocked(jb + 1);
+      } else if (tid == 0 && jb + 1 < nb_cta) {
+        fence_proxy_async();  // staging was read / written through the generic proxy
+        issue(jb + 1);
+      }
+    };
+    if constexpr (AL) {
+      // the rows just packed lay over the second buffer's line-end pads: zero them again
+      // (stage 0's closing barrier orders this before stage 1's padded reads)
+      if (tid < B) buf2[tid * LP + LP - 1] = make_double2(0.0, 0.0);
+    } else {
+      issue_next();
     }
     if constexpr (HALF) {
       half_transform<Q1, Q2, B, NT / 32, TPW, CSM, HO, CO>(buf, p.pl, p.stages, csm, buf2);
@@ -1164,6 +1183,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
         res = pfa_transform_nl<Q1, Q2, Q3, B, NT, TPW>(buf, buf2, reps, p.pl, p.stages);
       }
     }
+    if constexpr (AL) issue_next();  // every stage is done with the second buffer
     PIPE_T(3);
     // unpack + store (transposed: line index fastest -> B-double column segments).
     // All global loads of a group are issued before its stores.
@@ -1294,8 +1314,10 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
   if (SH::d >= 2) reps += PfaStageC<SH, 1>::Rcnt;
   if (SH::d >= 3) reps += PfaStageC<SH, 2>::Rcnt;
   constexpr int LP = HALF ? HalfShape<Q1, Q2 == 1 ? 3 : Q2>::LPh : SH::LP;
+  constexpr bool AL = HALF && HO && kPipeAliasStage;
+  if (AL && (size_t)k.n * 8 > (size_t)LP * 16) return cudaErrorInvalidConfiguration;
   size_t smem = (size_t)((kPipeOOP && !HALF) || (HALF && HO) ? 2 : 1) * BL * LP * 16 +
-                (size_t)BL * k.n * 8 + (reps + 64) * sizeof(unsigned);
+                (AL ? 0 : (size_t)BL * k.n * 8) + (reps + 64) * sizeof(unsigned);
   if (CSM) smem = (smem + 7) / 8 * 8 + (size_t)HalfCoef<HalfShape<Q1, Q2 == 1 ? 3 : Q2>>::total * 8;
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   if (HALF && !k.pl.hscat) return cudaErrorInvalidConfiguration;
@@ -1314,18 +1336,18 @@ static cudaError_t launch_pipe_t(const PipeK& k, int grid, cudaStream_t st) {
 // bit 3 pair-blocked input.  The single-GPU M^-1 runs 6 -> 15 -> 8 (row pass into the blocked
 // layout, sandwich blocked to blocked, row pass out of it); the row-slab passes 0..3.
 template <int Q1, int Q2, int Q3, int NT, int MINB, int TPW, bool HALF, bool HO = false,
-          int BL = kPipeLines, int CO = 0>
+          int BL = kPipeLines, int CO = 0, bool CSM = false>
 static cudaError_t launch_pipe_pm(const PipeK& k, int grid, cudaStream_t st) {
   const int pm = (k.mid ? 1 : 0) | (k.transposed ? 2 : 0) | (k.transposed == 2 ? 4 : 0) |
                  (k.in_blocked ? 8 : 0);
   switch (pm) {
-    case 0: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 0, HO, CO>(k, grid, st);
-    case 1: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 1, HO, CO>(k, grid, st);
-    case 2: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 2, HO, CO>(k, grid, st);
-    case 3: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 3, HO, CO>(k, grid, st);
-    case 6: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 6, HO, CO>(k, grid, st);
-    case 8: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 8, HO, CO>(k, grid, st);
-    case 15: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, false, 15, HO, CO>(k, grid, st);
+    case 0: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, 0, HO, CO>(k, grid, st);
+    case 1: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, 1, HO, CO>(k, grid, st);
+    case 2: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, 2, HO, CO>(k, grid, st);
+    case 3: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, 3, HO, CO>(k, grid, st);
+    case 6: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, 6, HO, CO>(k, grid, st);
+    case 8: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, 8, HO, CO>(k, grid, st);
+    case 15: return launch_pipe_t<Q1, Q2, Q3, NT, MINB, TPW, HALF, BL, CSM, 15, HO, CO>(k, grid, st);
     default: return cudaErrorInvalidConfiguration;
   }
 }
@@ -1335,7 +1357,10 @@ static cudaError_t launch_pipe_pm(const PipeK& k, int grid, cudaStream_t st) {
 //   buffer, two 6-warp CTAs per SM (the two CTAs overlap one batch's pack / unpack with the
 //   other's DFT stages), column-owner tensor-core stages (tvd_pfa_t.cuh half_stage_co):
 //   243.3 us per M^-1 vs 263.9 with k-tile-owner stages (bit-identical), 272.1 in place, 291
-//   for one 12-warp CTA; one line per batch or three CTAs per SM (spilling) measured slower;
+//   for one 12-warp CTA; one line per batch measured slower, and so did three CTAs per SM
+//   once the staging rows aliased the second line buffer (69 KB per CTA): 3 x 6 warps at 96
+//   registers 222 us, 3 x 4 warps at 168 registers 224 us vs 206 us for 2 x 6 warps; the
+//   q = 89 fragment tables copied to shared memory (CSM) 209 vs 206 us through L1;
 // * 1023 = 31 * 11 * 3 (config 4): four 2-warp CTAs per SM (99 vs 127 us per M^-1 for two
 //   8-warp CTAs);
 // * 511 = 73 * 7 (config 2a): half-line layout, two 6-warp CTAs (38.3 vs 40.4 us per M^-1);

@@ -442,67 +442,79 @@ struct HalfStage {
 // so the DMMA latency (29 cycles) is hidden by the warp itself instead of by more warps, at
 // ~60 registers.  Every output's DMMA sequence (fragments, k-step order) is the k-tile-owner
 // stage's, so the results are bit-identical.
-template <class ST, int NL, int NW>
-__device__ __forceinline__ void half_stage_co(const double2* buf, const double* __restrict__ Cf,
-                                              const double* __restrict__ Sf, double2* out) {
+// One column tile `ct` of the column-owner stage, k-tiles kt0 .. kt0 + NK - 1.
+template <class ST, int NL, int NK, bool SMC = false>
+__device__ __forceinline__ void co_tile(const double2* buf, const double* __restrict__ Cf,
+                                        const double* __restrict__ Sf, double2* out, int ct,
+                                        int kt0) {
   constexpr int q = ST::q, H = ST::H, st = ST::st, LP = ST::LP;
   constexpr bool PT = ST::partnered;
   constexpr int ndft = NL * ST::Rcnt;
-  constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8, nrs = ST::RP / 4;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int nrs = ST::RP / 4;
+  const int lane = threadIdx.x & 31;
   const double* bufd = reinterpret_cast<const double*>(buf);
-  for (int ct = warp; ct < nct; ct += NW) {
-    const int dB = min((ct * 8 + (lane >> 2)) >> 1, ndft - 1);
-    const int lB = dB / ST::Rcnt, tB = dB - lB * ST::Rcnt;
-    const double* p1 = bufd + 2 * (lB * LP + ST::base(tB)) + ((lane >> 2) & 1);
-    const double* p2 = bufd + 2 * (lB * LP + ST::partner(tB)) + ((lane >> 2) & 1);
-    double acc[nkt][4];
+  const int dB = min((ct * 8 + (lane >> 2)) >> 1, ndft - 1);
+  const int lB = dB / ST::Rcnt, tB = dB - lB * ST::Rcnt;
+  const double* p1 = bufd + 2 * (lB * LP + ST::base(tB)) + ((lane >> 2) & 1);
+  const double* p2 = bufd + 2 * (lB * LP + ST::partner(tB)) + ((lane >> 2) & 1);
+  const double* __restrict__ cf = Cf + kt0 * nrs * 32 + lane;  // A-fragment order (PfaStage::Cf)
+  const double* __restrict__ sf = Sf + kt0 * nrs * 32 + lane;
+  double acc[NK][4];
 #pragma unroll
-    for (int kt = 0; kt < nkt; ++kt) acc[kt][0] = acc[kt][1] = acc[kt][2] = acc[kt][3] = 0.0;
+  for (int kt = 0; kt < NK; ++kt) acc[kt][0] = acc[kt][1] = acc[kt][2] = acc[kt][3] = 0.0;
 #pragma unroll
-    for (int rs = 0; rs < nrs; ++rs) {
-      const int r = 1 + rs * 4 + (lane & 3);
-      const double x1 = p1[2 * r * st];
-      const double x2 = PT ? p2[2 * r * st] : p1[2 * (q - r) * st];
-      const double fa = PT ? x1 - x2 : x1 + x2;
-      const double fb = PT ? x1 + x2 : x1 - x2;
+  for (int rs = 0; rs < nrs; ++rs) {
+    const int r = 1 + rs * 4 + (lane & 3);
+    const double x1 = p1[2 * r * st];
+    const double x2 = PT ? p2[2 * r * st] : p1[2 * (q - r) * st];
+    const double fa = PT ? x1 - x2 : x1 + x2;
+    const double fb = PT ? x1 + x2 : x1 - x2;
 #pragma unroll
-      for (int kt = 0; kt < nkt; ++kt) {
-        const int o = (kt * nrs + rs) * 32 + lane;  // A-fragment order (PfaStage::Cf)
-        dmma884(acc[kt][0], acc[kt][1], __ldg(Cf + o), fa);
-        dmma884(acc[kt][2], acc[kt][3], __ldg(Sf + o), fb);
-      }
+    for (int kt = 0; kt < NK; ++kt) {
+      const int o = (kt * nrs + rs) * 32;
+      // SMC: the tables are a shared-memory copy (plain loads), else global through L1
+      dmma884(acc[kt][0], acc[kt][1], SMC ? cf[o] : __ldg(cf + o), fa);
+      dmma884(acc[kt][2], acc[kt][3], SMC ? sf[o] : __ldg(sf + o), fb);
     }
-    const int dO = ct * 4 + (lane & 3);
-    if (dO < ndft) {
-      const int lO = dO / ST::Rcnt, tO = dO - lO * ST::Rcnt;
-      const int ob = lO * LP + ST::base(tO), on = lO * LP + ST::partner(tO);
-      const bool self = tO == 0;
-      const double2 x0 = buf[ob];
-      double2* p = out + ob;
-      double2* pn = out + on;
+  }
+  const int dO = ct * 4 + (lane & 3);
+  if (dO < ndft) {
+    const int lO = dO / ST::Rcnt, tO = dO - lO * ST::Rcnt;
+    const int ob = lO * LP + ST::base(tO), on = lO * LP + ST::partner(tO);
+    const bool self = tO == 0;
+    const double2 x0 = buf[ob];
+    double2* p = out + ob;
+    double2* pn = out + on;
 #pragma unroll
-      for (int kt = 0; kt < nkt; ++kt) {
-        const int k = kt * 8 + (lane >> 2);
-        if (k <= H) {
-          const double a0 = acc[kt][0], a1 = acc[kt][1], b0 = acc[kt][2], b1 = acc[kt][3];
-          const double2 vk = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
-          const double2 vm = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
-          if (!PT) {
-            if (k == 0) {
-              p[0] = vk;
-            } else {
-              p[k * st] = vk;
-              p[(q - k) * st] = vm;
-            }
+    for (int kt = 0; kt < NK; ++kt) {
+      const int k = (kt0 + kt) * 8 + (lane >> 2);
+      if (k <= H) {
+        const double a0 = acc[kt][0], a1 = acc[kt][1], b0 = acc[kt][2], b1 = acc[kt][3];
+        const double2 vk = make_double2(x0.x + a0 + b1, x0.y + a1 - b0);
+        const double2 vm = make_double2(x0.x + a0 - b1, x0.y + a1 + b0);
+        if (!PT) {
+          if (k == 0) {
+            p[0] = vk;
           } else {
-            p[k] = vk;
-            if (!self) pn[k] = k == 0 ? make_double2(-vk.x, -vk.y) : make_double2(-vm.x, -vm.y);
+            p[k * st] = vk;
+            p[(q - k) * st] = vm;
           }
+        } else {
+          p[k] = vk;
+          if (!self) pn[k] = k == 0 ? make_double2(-vk.x, -vk.y) : make_double2(-vm.x, -vm.y);
         }
       }
     }
   }
+}
+
+template <class ST, int NL, int NW, bool SMC = false>
+__device__ __forceinline__ void half_stage_co(const double2* buf, const double* __restrict__ Cf,
+                                              const double* __restrict__ Sf, double2* out) {
+  constexpr int ndft = NL * ST::Rcnt;
+  constexpr int nkt = ST::KP / 8, nct = (2 * ndft + 7) / 8;
+  const int warp = threadIdx.x >> 5;
+  for (int ct = warp; ct < nct; ct += NW) co_tile<ST, NL, nkt, SMC>(buf, Cf, Sf, out, ct, 0);
   __syncthreads();
 }
 
@@ -517,7 +529,7 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
   constexpr int ndft = NL * ST::Rcnt;
   double2* const out = OOP ? dst : buf;
   if constexpr (ST::mma && CO && OOP) {
-    half_stage_co<ST, NL, NW>(buf, Cf, Sf, dst);
+    half_stage_co<ST, NL, NW, CSM>(buf, Cf, Sf, dst);
     return;
   }
   if constexpr (ST::mma) {
@@ -533,8 +545,8 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
     const int krow = kt * 8 + (lane >> 2);
     constexpr int nra = CSM ? 1 : nrs;
     double ca[nra], sa[nra];
-    const double* cmk = Cm + krow * ST::RP + (lane & 3);
-    const double* smk = Sm + krow * ST::RP + (lane & 3);
+    const double* cmk = Cf + kt * nrs * 32 + lane;  // CSM: shared copy, read per r-step
+    const double* smk = Sf + kt * nrs * 32 + lane;
     if constexpr (!CSM) {
 #pragma unroll
       for (int rs = 0; rs < nrs; ++rs) {  // fragment-ordered tables: coalesced 256-byte reads
@@ -573,8 +585,8 @@ __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const
             x1[j] = p1[j][2 * r * st];
             x2[j] = PT ? p2[j][2 * r * st] : p1[j][2 * (q - r) * st];
           }
-          const double car = CSM ? cmk[rs * 4] : ca[CSM ? 0 : rs];
-          const double sar = CSM ? smk[rs * 4] : sa[CSM ? 0 : rs];
+          const double car = CSM ? cmk[rs * 32] : ca[CSM ? 0 : rs];
+          const double sar = CSM ? smk[rs * 32] : sa[CSM ? 0 : rs];
 #pragma unroll
           for (int j = 0; j < TPW; ++j) {
             // fold: a = x_r + x_{q-r}, b = x_r - x_{q-r}; partnered x_{q-r} = -S[-a][r]
@@ -725,13 +737,13 @@ __device__ __forceinline__ void half_transform(double2* buf, const PfaPlan& pl, 
                                                double2* buf2 = nullptr) {
   using SH = HalfShape<Q0, Q1>;
   using HC = HalfCoef<SH>;
-  // stage 0 (the wide radix) reads its fragments from the shared copy when CSM
-  const double* c0 = CSM ? cs : pl.st[0].Cm;
-  const double* s0 = CSM ? cs + HC::n0 : pl.st[0].Sm;
+  // stage 0 (the wide radix) reads its fragment-ordered tables from the shared copy when CSM
+  const double* c0 = CSM ? cs : pl.st[0].Cf;
+  const double* s0 = CSM ? cs + HC::n0 : pl.st[0].Sf;
   // OOP: stage 0 buf -> buf2, stage 1 buf2 -> buf (the result lands in buf either way)
   if (stages >= 1)
-    half_stage<HalfStage<SH, 0>, NL, NW, TPW, CSM, OOP, (CO >= 1)>(buf, c0, s0, buf2, pl.st[0].Cf,
-                                                                   pl.st[0].Sf);
+    half_stage<HalfStage<SH, 0>, NL, NW, TPW, CSM, OOP, (CO >= 1)>(buf, pl.st[0].Cm, pl.st[0].Sm,
+                                                                   buf2, c0, s0);
   if (stages >= 2) {
     if constexpr (OOP)
       half_stage<HalfStage<SH, 1>, NL, NW, TPW, false, true, (CO >= 2)>(

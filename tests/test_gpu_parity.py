@@ -535,6 +535,46 @@ def test_f2_ar_transform_2d(golden, name):
 
 
 @pytest.mark.parametrize("name", F2_OPS)
+def test_ar_transform_transposes(golden, name):
+    """T^T (x) T^T and T^-T (x) T^-T against the reference's tensor_apply_2d
+    (transforms.py:130-139, 159-171), and the 1D forms along either axis against the dense
+    matrices of the defining formula."""
+    g = golden(name)
+    ark = T.TransformKind.ANTI_REFLECTIVE
+    for inv in (0, 1):
+        got = T.tensor_apply_2d(ark, g["w"], inverse=bool(inv), transpose=True)
+        assert rel_err(got, g[f"AR2_{inv}1"]) < 1e-13
+    w = g["w"]
+    n = w.shape[0]
+    for inv in (False, True):
+        m = T.dense_matrix(ark, n, inverse=inv)
+        for tr in (False, True):
+            mm = m.T if tr else m
+            assert rel_err(T.ar_apply(w, inverse=inv, transpose=tr, axis=0), mm @ w) < 1e-12
+            assert rel_err(T.ar_apply(w, inverse=inv, transpose=tr, axis=1), w @ mm.T) < 1e-12
+            assert rel_err(T.apply_1d(ark, w[3], inverse=inv, transpose=tr), mm @ w[3]) < 1e-12
+    # round trips: T^-1 T = I and T^-T T^T = I
+    for tr in (False, True):
+        back = T.ar_apply(T.ar_apply(w, transpose=tr), inverse=True, transpose=tr)
+        assert rel_err(back, w) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["ops_n16.npz", "ops_n32.npz", "ops_n33.npz"])
+def test_blur_transform_domain_paths(golden, name):
+    """apply_fast / apply_transpose_fast (blur.py:293-314): analysis, eigenvalue scaling,
+    synthesis on the device against the reference's own fast paths, both BCs; for the
+    anti-reflective adjoint this is X^-T (lam .* X^T u) with the non-orthogonal T."""
+    g = golden(name)
+    n = g["u"].shape[0]
+    for psf_name in ("gauss", "disk"):
+        for bc in ("reflective", "anti_reflective"):
+            hop = B.StructuredBlurOperator(B.SymmetricPsf(g[f"psf_{psf_name}"]), BCS[bc], n)
+            key = f"{psf_name}_{bc}"
+            assert rel_err(hop.apply_fast(g["u"]), g[f"Hfast_{key}"]) < 1e-12
+            assert rel_err(hop.apply_transpose_fast(g["u"]), g[f"HTfast_{key}"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", F2_OPS)
 def test_f2_p_family_assembly_and_solve(golden, name):
     g = golden(name)
     n = g["u"].shape[0]
