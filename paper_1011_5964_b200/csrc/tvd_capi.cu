@@ -398,6 +398,15 @@ static bool build_pfa(TrigPlan* P) {
   for (int g : groups)
     if (g > 255) return false;
   std::sort(groups.rbegin(), groups.rend());
+  // Three coprime factors: merge the two smallest into one stage (1023 = 31 . 11 . 3 ->
+  // 33 . 31).  A stage is a dense q-point DFT on the fp64 tensor cores and only needs q odd,
+  // so the composite stage costs a few more DMMAs but removes a stage (two barriers and a
+  // pass over the line) and puts the length on the two-factor half-line layout.
+  if (groups.size() == 3 && groups[1] * groups[2] <= 255) {
+    groups[1] *= groups[2];
+    groups.pop_back();
+    std::sort(groups.rbegin(), groups.rend());
+  }
   PfaPlan& pl = P->pfa;
   pl = PfaPlan{};
   pl.L = L;

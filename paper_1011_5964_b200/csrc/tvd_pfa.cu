@@ -913,9 +913,11 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
   if constexpr (HALF && HO && !AL) {  // out-of-place stages: the second buffer's pads read as zero
     for (int i = tid; i < B * LP; i += nth) buf2[i] = make_double2(0.0, 0.0);
   }
-  if constexpr (AL)
-    static_assert(HalfShape<Q1, Q2>::P1h == HalfShape<Q1, Q2>::H1 + 1,
-                  "aliased staging re-zeroes only the line-end pad of the second buffer");
+  if constexpr (AL) {
+    // aliased staging: the pads are re-zeroed after every pack (below); the tail of the
+    // second buffer that no staging row covers starts out zero as well
+    for (int i = tid + (int)((long)B * n / 2); i < B * LP; i += nth) buf2[i] = make_double2(0.0, 0.0);
+  }
   // CSM: the q0 stage's cos / sin tables staged in shared memory (after the reps, 8-aligned)
   double* csm = nullptr;
   if constexpr (CSM) {
@@ -1111,7 +1113,18 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     if constexpr (AL) {
       // the rows just packed lay over the second buffer's line-end pads: zero them again
       // (stage 0's closing barrier orders this before stage 1's padded reads)
-      if (tid < B) buf2[tid * LP + LP - 1] = make_double2(0.0, 0.0);
+      {
+        using HS = HalfShape<Q1, Q2>;
+        constexpr int PADS = HS::P1h - HS::H1 - 1;  // pad columns per grid row
+        if (tid < B) buf2[tid * LP + LP - 1] = make_double2(0.0, 0.0);
+        if constexpr (PADS > 0) {
+          for (int i = tid; i < B * HS::Q0 * PADS; i += nth) {
+            const int l = i / (HS::Q0 * PADS), rem = i - l * (HS::Q0 * PADS);
+            const int a = rem / PADS, c = rem - a * PADS;
+            buf2[l * LP + a * HS::P1h + HS::H1 + 1 + c] = make_double2(0.0, 0.0);
+          }
+        }
+      }
     } else {
       issue_next();
     }
@@ -1361,8 +1374,10 @@ static cudaError_t launch_pipe_pm(const PipeK& k, int grid, cudaStream_t st) {
 //   once the staging rows aliased the second line buffer (69 KB per CTA): 3 x 6 warps at 96
 //   registers 222 us, 3 x 4 warps at 168 registers 224 us vs 206 us for 2 x 6 warps; the
 //   q = 89 fragment tables copied to shared memory (CSM) 209 vs 206 us through L1;
-// * 1023 = 31 * 11 * 3 (config 4): four 2-warp CTAs per SM (99 vs 127 us per M^-1 for two
-//   8-warp CTAs);
+// * 1023 = 33 * 31 (config 4; the plan merges 11 . 3 into one tensor-core stage): the same
+//   half-line, out-of-place, column-owner path as 2047 with four 4-warp CTAs per SM
+//   (round 1 / early round 2: three in-place stages 31 . 11 . 3, four 2-warp CTAs, 86 us
+//   per M^-1);
 // * 511 = 73 * 7 (config 2a): half-line layout, two 6-warp CTAs (38.3 vs 40.4 us per M^-1);
 // * 127 (config 1): two 8-warp CTAs.
 // A warp-specialised producer / consumer variant of the 2047 pass measured 272-288 us per
@@ -1373,7 +1388,7 @@ struct PipeVariant {
 static PipeVariant pipe_variant(int which) {
   switch (which) {
     case 1: return {192, 2, 1, 2};
-    case 2: return {64, 4, 2, 2};
+    case 2: return {128, 4, 1, 2};
     case 3: return {192, 2, 1, 2};
     default: return {256, 2, 3, 2};
   }
@@ -1424,7 +1439,7 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
   if (grid <= 0) return cudaSuccess;
   switch (which) {
     case 1: return launch_pipe_pm<89, 23, 1, 192, 2, 1, true, true, 2, 2>(k, grid, st);
-    case 2: return launch_pipe_pm<31, 11, 3, 64, 4, 2, false>(k, grid, st);
+    case 2: return launch_pipe_pm<33, 31, 1, 128, 4, 1, true, true, 2, 2>(k, grid, st);
     case 3: return launch_pipe_pm<73, 7, 1, 192, 2, 1, true>(k, grid, st);
     case 4: return launch_pipe_pm<127, 1, 1, 256, 2, 3, false>(k, grid, st);
     default: return cudaErrorInvalidConfiguration;
@@ -1453,7 +1468,7 @@ static bool pfa_specialised(const PfaPlan& P, int* which) {
   auto is = [&](int a, int b, int c) {
     return P.q[0] == a && (P.d >= 2 ? P.q[1] : 1) == b && (P.d >= 3 ? P.q[2] : 1) == c;
   };
-  *which = is(89, 23, 1) ? 1 : is(31, 11, 3) ? 2 : is(73, 7, 1) ? 3 : is(127, 1, 1) ? 4 : 0;
+  *which = is(89, 23, 1) ? 1 : is(33, 31, 1) ? 2 : is(73, 7, 1) ? 3 : is(127, 1, 1) ? 4 : 0;
   return *which != 0 && P.scat != nullptr;
 }
 
@@ -1500,7 +1515,7 @@ cudaError_t launch_band_pfa(const PfaPlan& P, const double2* wfull, int n, const
   if (nb == 0) return cudaSuccess;
   switch (which) {
     case 1: return launch_band_pfa_t<89, 23, 1>(k, nb, st);
-    case 2: return launch_band_pfa_t<31, 11, 3>(k, nb, st);
+    case 2: return launch_band_pfa_t<33, 31, 1>(k, nb, st);
     case 3: return launch_band_pfa_t<73, 7, 1>(k, nb, st);
     case 4: return launch_band_pfa_t<127, 1, 1>(k, nb, st);
     default: return cudaErrorInvalidConfiguration;
@@ -1535,7 +1550,7 @@ cudaError_t launch_pfa(const PfaPlan& P, int family, int len, const LineGeom& g,
   if (nb == 0) return cudaSuccess;
   switch (which) {
     case 1: return launch_pfa_t<89, 23, 1>(k, nb, st);
-    case 2: return launch_pfa_t<31, 11, 3>(k, nb, st);
+    case 2: return launch_pfa_t<33, 31, 1>(k, nb, st);
     case 3: return launch_pfa_t<73, 7, 1>(k, nb, st);
     case 4: return launch_pfa_t<127, 1, 1>(k, nb, st);
     default: break;
