@@ -57,6 +57,10 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
 // at c3 (2787 vs 2782 it/s), and +17 / +31 / +24 / +20 % on single-stream c1 / c2a / c2b / c4
 // solves (round 2, tools/pcg_ab.py pdl 0,1 CONFIG), whose short kernels leave the launch
 // latency exposed; on by default, option TVD_OPT_PDL.
+// A LATE trigger (launch_dependents when a CTA of a single-wave grid -- the persistent DST
+// passes, the x / r update -- enters its last batch, with every kernel's wait moved behind its
+// constant-table prologue) measured +0.5 % on c3 and -8 % on the four-stream c4 batch, where
+// dependents parked on drained SMs starve the other streams' kernels: no kernel triggers.
 #ifndef TVD_PDL_EARLY_TRIGGER
 #define TVD_PDL_EARLY_TRIGGER 0
 #endif
