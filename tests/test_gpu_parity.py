@@ -404,7 +404,7 @@ def test_restore_unpreconditioned(golden, name):
 def test_headline_c3_restore_matches_reference():
     """Config 3 (2048^2 AR, 20 FP steps, tol 1e-5) end to end against the reference's own
     CPU runs (tests/golden/c3_parity.json, made by tests/golden/make_c3_parity.py and
-    add_c3_run.py from ~30-240-minute runs of the reference on identical inputs).
+    add_c3_run.py from five 0.5-4 h runs of the reference on identical inputs).
 
     Counts: at tol 1e-5 the stopping iteration is not a property of the algorithm.  The
     reference disagrees with ITSELF by up to 3 iterations per FP step between runs that
