@@ -555,7 +555,8 @@ static bool build_pfa(TrigPlan* P) {
     const int Q0 = pl.q[0], Q1 = pl.q[1], H1 = (Q1 - 1) / 2;
     const int P1h = H1 + 1 + ((4 - (H1 + 1) % 8) + 8) % 8;  // = 4 (mod 8): conflict-free
     pl.P1h = P1h;
-    pl.LPh = Q0 * P1h + 1;  // + one zero pad element (stage-1 padded r reads)
+    // + one zero pad element (stage-1 padded r reads), pitch = 4 (mod 8): tvd_pfa_t.cuh HalfShape
+    pl.LPh = Q0 * P1h + 1 + ((4 - (Q0 * P1h + 1) % 8) + 8) % 8;
     auto stored = [&](int a, int b, unsigned* pos, unsigned* neg) {
       if (b <= H1) {
         *pos = (unsigned)(a * P1h + b);

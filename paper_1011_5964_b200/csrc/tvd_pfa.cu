@@ -1032,7 +1032,8 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
     const int line0 = first_of(jb), nlv = rows_of(jb);
     for (int i = tid; i < B; i += nth) {
       buf[i * LP] = make_double2(0.0, 0.0);
-      if (HALF) buf[i * LP + LP - 1] = make_double2(0.0, 0.0);  // pad read by padded r
+      if constexpr (HALF)  // pad read by padded r
+        buf[i * LP + HalfShape<Q1, Q2 == 1 ? 3 : Q2>::PADI] = make_double2(0.0, 0.0);
     }
     for (int i = tid; i < (B - nlv) * LP; i += nth) buf[nlv * LP + i] = make_double2(0.0, 0.0);
     // pack from the staging rows (+ Shat borders parked in smem): thread owns
@@ -1116,7 +1117,7 @@ __global__ void __launch_bounds__(NT, MINB) k_dst_pipe(const PipeK p) {
       {
         using HS = HalfShape<Q1, Q2>;
         constexpr int PADS = HS::P1h - HS::H1 - 1;  // pad columns per grid row
-        if (tid < B) buf2[tid * LP + LP - 1] = make_double2(0.0, 0.0);
+        if (tid < B) buf2[tid * LP + HS::PADI] = make_double2(0.0, 0.0);
         if constexpr (PADS > 0) {
           for (int i = tid; i < B * HS::Q0 * PADS; i += nth) {
             const int l = i / (HS::Q0 * PADS), rem = i - l * (HS::Q0 * PADS);

@@ -413,7 +413,11 @@ struct HalfShape {
   static constexpr int L = Q0 * Q1, N = L - 1;
   static constexpr int H0 = (Q0 - 1) / 2, H1 = (Q1 - 1) / 2;
   static constexpr int P1h = H1 + 1 + ((4 - (H1 + 1) % 8) + 8) % 8;  // tvd_capi.cu build_pfa
-  static constexpr int LPh = Q0 * P1h + 1;
+  static constexpr int PADI = Q0 * P1h;  // the zero pad element read by stage 1's padded r
+  // line pitch: past the pad element, rounded up to 4 (mod 8) double2 so that the two lines of
+  // a batch sit 16 words apart modulo the 32 banks and the unpack / mid gathers of a quarter
+  // warp (four consecutive t of both lines, 16 bytes each) touch 32 distinct banks
+  static constexpr int LPh = PADI + 1 + ((4 - (PADI + 1) % 8) + 8) % 8;
 };
 
 template <class SH, int S>
