@@ -1871,6 +1871,34 @@ static int level2(tvd_ctx* c, const TrigPlan* P, int n, const double* diag, cons
       TVD_LAUNCH(c, kCatProject, 1, launch_ar_lines(lam1, n - 1, n, n, 1, ar_c, 0, nullptr, nullptr,
                                                     0.0, nullptr, nullptr, c->stream));
   }
+  // Prime-factor engine: run level 2 over contiguous lines as well -- transpose the level-1
+  // results, project the rows of the transposes, and let one kernel transpose the result
+  // back with the eigenvalue epilogue and the min / max partials (k_transpose_eig) -- instead
+  // of reading and writing 8-byte entries at a stride of n.  Same projection per line and the
+  // same epilogue expression: bit-identical eigenvalues.
+  const bool rowwise = !ar_c && P->family != kFamDct && P->pfa_ok && P->pfa.L == P->L &&
+                       band_pfa_ok(P->pfa) && !option(kOptBandGeneric) &&
+                       !(P->rader_ok && P->rader.L == P->L) && option(kOptBandPrefetch) != 6 &&
+                       band_pfa_rowwise(P->pfa);
+  if (rowwise) {
+    double *t0, *t1 = nullptr;
+    TVD_SLOT(c, kSlotTmp2, (size_t)n * n, t0);
+    TVD_LAUNCH(c, kCatVec, 1, launch_transpose(lam0, t0, n, c->stream));
+    if (lam1) {
+      TVD_SLOT(c, kSlotTmp3, (size_t)n * n, t1);
+      TVD_LAUNCH(c, kCatVec, 1, launch_transpose(lam1, t1, n, c->stream));
+    }
+    BandLines f{};
+    f.b0 = t0; f.b0_ls = n; f.b0_es = 1;
+    f.b1 = t1; f.b1_ls = n; f.b1_es = 1;
+    f.c1 = t1 ? 2.0 : 0.0;
+    f.nlines = n;
+    f.out = lam0; f.out_ls = n; f.out_es = 1;  // projT over the consumed level-1 buffer
+    TVD_LAUNCH(c, kCatProject, 1, launch_band_project(*P, 0, f, nullptr, c->stream));
+    TVD_LAUNCH(c, kCatVec, 1, launch_transpose_eig(lam0, n, epi, lamh, lamd, alpha, out,
+                                                   partial_minmax, nb_out, c->stream));
+    return TVD_OK;
+  }
   BandLines f{};
   f.b0 = lam0; f.b0_ls = 1; f.b0_es = n;
   f.b1 = lam1; f.b1_ls = 1; f.b1_es = n;

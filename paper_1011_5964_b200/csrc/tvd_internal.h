@@ -170,6 +170,9 @@ struct BandLines {
 cudaError_t launch_band_pfa(const PfaPlan& P, const double2* wfull, int n, const BandLines& b,
                             int* nblocks_out, cudaStream_t st);
 bool band_pfa_ok(const PfaPlan& P);
+// shapes whose projections run on the column-owner kernel (one line per CTA): their level-2
+// pass pays for transposed, contiguous lines
+bool band_pfa_rowwise(const PfaPlan& P);
 
 // ---- launchers (tvd_lines.cu)
 cudaError_t launch_trig(const TrigPlan& P, const LineGeom& g, int analysis, const LineIO& io,
@@ -203,6 +206,10 @@ cudaError_t launch_pipe(const PfaPlan& P, int family, int len, int nlines, int t
 int pipe_grid(const PfaPlan& P, int nlines);
 // out = in^T for an n x n fp64 array (tvd_stencil.cu)
 cudaError_t launch_transpose(const double* in, double* out, int n, cudaStream_t st);
+// eig = epilogue(transpose(projT)) with per-CTA (min, max) pairs (tvd_stencil.cu k_transpose_eig)
+cudaError_t launch_transpose_eig(const double* projT, int n, int epi, const double* lamh,
+                                 const double* lamd, double alpha, double* eig,
+                                 double* partial_minmax, int* nblocks_out, cudaStream_t st);
 // out (cols x rows) = in^T for a rows x cols fp64 array
 cudaError_t launch_transpose_rect(const double* in, double* out, int rows, int cols,
                                   const int* skip, cudaStream_t st);

@@ -714,6 +714,118 @@ __global__ void __launch_bounds__(256, 2) k_band_pfa(const BandPfaK p) {
   }
 }
 
+// The same projection on the column-owner, out-of-place stages of the DST engine (two-factor
+// shapes with two tensor-core stages: 2047 = 89 x 23, 1023 = 33 x 31): one line per CTA in
+// the full Good-Thomas layout, X -> Y -> X over two line buffers (one barrier per stage
+// instead of two per round), fragment-ordered tables, two 6-warp CTAs per SM whose scatter /
+// band-form phases overlap each other's stages.  Per output the DMMA sequence is the
+// k-tile-owner stage's: bit-identical to k_band_pfa.
+template <int Q1, int Q2, int NW>
+__global__ void __launch_bounds__(NW * 32, 2) k_band_pfa_co(const BandPfaK p) {
+  using SH = PfaShape<Q1, Q2, 1>;
+  constexpr int LP = SH::LP, L = SH::L, NT = NW * 32;
+  static_assert(FullStage<SH, 0>::mma && FullStage<SH, 1>::mma, "tensor-core stages only");
+  extern __shared__ double2 smem2[];
+  __shared__ double red[32];
+  __shared__ double tot[2];
+  const int tid = threadIdx.x, n = p.n;
+  double2* X = smem2;
+  double2* Y = smem2 + LP;
+  const BandLines& b = p.b;
+  const int line = blockIdx.x;
+  auto B0 = [&](int j) { return b.b0[(long)line * b.b0_ls + (long)j * b.b0_es]; };
+  auto B1 = [&](int j) { return b.b1[(long)line * b.b1_ls + (long)j * b.b1_es]; };
+  for (int i = tid; i < LP; i += NT) X[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int j = tid; j < L; j += NT) {
+    // even slots 2j <- b0[j] (j = 1..N), odd slots 2j+1 <- c1 b1[j] (j = 1..N-1)
+    double e = 0.0, o = 0.0;
+    if (j >= 1 && j <= L - 1) e = B0(j);
+    if (b.b1 && j >= 1 && j <= L - 2) o = b.c1 * B1(j);
+    X[__ldg(p.pl.gscat + j)] = make_double2(e, o);
+  }
+  if (tid < 32) {  // band totals (one warp, fixed order) as k_band
+    double t0 = 0.0, t1 = 0.0;
+    for (int j = 1 + tid; j < n - 1; j += 32) t0 += B0(j);
+    if (b.b1)
+      for (int j = 1 + tid; j < n - 2; j += 32) t1 += B1(j);
+    t0 = warp_sum(t0);
+    t1 = warp_sum(t1);
+    if (tid == 0) {
+      tot[0] = t0;
+      tot[1] = t1;
+    }
+  }
+  __syncthreads();
+  half_stage_co<FullStage<SH, 0>, 1, NW>(X, p.pl.st[0].Cf, p.pl.st[0].Sf, Y);
+  half_stage_co<FullStage<SH, 1>, 1, NW>(Y, p.pl.st[1].Cf, p.pl.st[1].Sf, X);
+  // the band form (k_band's epilogue; C_t from the CRT output position of t)
+  auto at = [&](int t) { return X[t == 0 ? 0u : __ldg(p.pl.gath + t - 1)]; };
+  double vmin = 1.0 / 0.0, vmax = -1.0 / 0.0;
+  for (int t = tid; t < n; t += NT) {
+    double v;
+    if (t == 0 || t == n - 1) {
+      v = B0(t);
+    } else {
+      const int tr = L - t;
+      const double2 C = at(t), Cr = cconj(at(tr));
+      const double2 E = cscale(cadd(C, Cr), 0.5);
+      const double2 D = csub(C, Cr);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      const double2 w = p.wfull[t];
+      const double re_s = E.x + (w.x * O.x - w.y * O.y);
+      const double t0 = tot[0], t1 = tot[1];
+      v = (t0 + b.c1 * t1 * w.x - re_s) / L;
+    }
+    const long g = (long)line * b.out_ls + (long)t * b.out_es;
+    if (b.epi == 1) {
+      const double lh = b.lamh[g];
+      v = lh * lh + b.alpha * v;
+    } else if (b.epi == 2) {
+      const double lh = b.lamh[g], ld = b.lamd[g];
+      v = lh * lh * ld * ld + b.alpha * v;
+    }
+    b.out[g] = v;
+    vmin = fmin(vmin, v);
+    vmax = fmax(vmax, v);
+  }
+  if (b.epi != 0) {
+    for (int o = 16; o > 0; o >>= 1) {
+      vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+      vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    const int lane = tid & 31, wid = tid >> 5;
+    if (lane == 0) {
+      red[wid] = vmin;
+      red[16 + wid] = vmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double a = red[0], z = red[16];
+      for (int w = 1; w < NW; ++w) {
+        a = fmin(a, red[w]);
+        z = fmax(z, red[16 + w]);
+      }
+      b.partial_minmax[2 * blockIdx.x] = a;
+      b.partial_minmax[2 * blockIdx.x + 1] = z;
+    }
+  }
+}
+
+template <int Q1, int Q2, int NW>
+static cudaError_t launch_band_pfa_co(const BandPfaK& k, cudaStream_t st) {
+  using SH = PfaShape<Q1, Q2, 1>;
+  const size_t smem = (size_t)2 * SH::LP * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_band_pfa_co<Q1, Q2, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  k_band_pfa_co<Q1, Q2, NW><<<k.b.nlines, NW * 32, smem, st>>>(k);
+  return cudaGetLastError();
+}
+
 template <int Q1, int Q2, int Q3>
 static cudaError_t launch_band_pfa_t(const BandPfaK& k, int nb, cudaStream_t st) {
   using SH = PfaShape<Q1, Q2, Q3>;
@@ -1501,6 +1613,11 @@ bool band_pfa_ok(const PfaPlan& P) {
   return pfa_specialised(P, &which) && P.gscat != nullptr && P.greps[0] != nullptr;
 }
 
+bool band_pfa_rowwise(const PfaPlan& P) {
+  int which;
+  return band_pfa_ok(P) && pfa_specialised(P, &which) && (which == 1 || which == 2);
+}
+
 cudaError_t launch_band_pfa(const PfaPlan& P, const double2* wfull, int n, const BandLines& b,
                             int* nblocks_out, cudaStream_t st) {
   int which;
@@ -1511,6 +1628,11 @@ cudaError_t launch_band_pfa(const PfaPlan& P, const double2* wfull, int n, const
   k.wfull = wfull;
   k.n = n;
   k.b = b;
+  if ((which == 1 || which == 2) && option(kOptBandPrefetch) != 6) {  // column-owner variant
+    if (nblocks_out) *nblocks_out = b.nlines;
+    if (b.nlines == 0) return cudaSuccess;
+    return which == 1 ? launch_band_pfa_co<89, 23, 6>(k, st) : launch_band_pfa_co<33, 31, 4>(k, st);
+  }
   const int nb = (b.nlines + kBandPfaLines - 1) / kBandPfaLines;
   if (nblocks_out) *nblocks_out = nb;
   if (nb == 0) return cudaSuccess;

@@ -522,6 +522,27 @@ __device__ __forceinline__ void half_stage_co(const double2* buf, const double* 
   __syncthreads();
 }
 
+// Stage S of a two-factor shape in the FULL Good-Thomas layout (row pitch stride[0]) for a
+// general, not odd, complex input: every column (S = 0) / row (S = 1) is a DFT line of its
+// own, outputs V_k and V_{q-k} both stored.  Same members as HalfStage, so the column-owner
+// stage (half_stage_co / co_tile) runs it unchanged (the assembly's band projections).
+template <class SH, int S>
+struct FullStage {
+  using Shape = SH;
+  static constexpr bool partnered = false;
+  static constexpr int q = S == 0 ? SH::q[0] : SH::q[1];
+  static constexpr int H = (q - 1) / 2;
+  static constexpr int P1 = SH::stride[0];
+  static constexpr int st = S == 0 ? P1 : 1;
+  static constexpr int Rcnt = S == 0 ? SH::q[1] : SH::q[0];
+  static constexpr int KP = (H + 1 + 7) / 8 * 8;
+  static constexpr int RP = (H + 3) / 4 * 4;
+  static constexpr bool mma = H >= 8;
+  static constexpr int LP = SH::LP;
+  __device__ static int base(int t) { return S == 0 ? t : t * P1; }
+  __device__ static int partner(int t) { return base(t); }
+};
+
 template <class ST, int NL, int NW, int TPWc, bool CSM = false, bool OOP = false, bool CO = false>
 __device__ __forceinline__ void half_stage(double2* buf, const double* Cm, const double* Sm,
                                            double2* dst = nullptr,

@@ -978,9 +978,82 @@ __global__ void k_transpose(const double* __restrict__ in, double* __restrict__ 
     if (i < cols && j < rows) out[(long)i * rows + j] = tile[threadIdx.x][r];
   }
 }
+// eig[s][t] = lamh[s][t]^2 [* lamd[s][t]^2] + alpha * projT[t][s]: the level-2 projection was
+// computed over the rows of the TRANSPOSED level-1 results (contiguous lines), this kernel
+// transposes it back through a shared-memory tile, applies k_band's eigenvalue epilogue with
+// coalesced reads of lamh / lamd and leaves one (min, max) pair per CTA.  Persistent CTAs over
+// the 32 x 32 tiles (at most `n` CTAs: the partial buffer holds 2 n doubles).
+__global__ void __launch_bounds__(256) k_transpose_eig(const double* __restrict__ projT, int n,
+                                                      int epi, const double* __restrict__ lamh,
+                                                      const double* __restrict__ lamd,
+                                                      double alpha, double* __restrict__ eig,
+                                                      double* __restrict__ partial_minmax) {
+  __shared__ double tile[32][33];
+  __shared__ double red[16];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int nt = (n + 31) / 32;
+  double vmin = 1.0 / 0.0, vmax = -1.0 / 0.0;
+  for (int tid = blockIdx.x; tid < nt * nt; tid += gridDim.x) {
+    const int bx = (tid % nt) * 32, by = (tid / nt) * 32;  // tile of eig: rows by.., cols bx..
+    for (int r = ty; r < 32; r += 8) {  // projT rows bx + r, cols by + tx
+      const int i = bx + r, j = by + tx;
+      if (i < n && j < n) tile[r][tx] = projT[(long)i * n + j];
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int i = by + r, j = bx + tx;
+      if (i < n && j < n) {
+        const long g = (long)i * n + j;
+        double v = tile[tx][r];
+        // k_band_pfa's epilogue expressions with the contraction ptxas gives them there
+        // (lh lh + alpha v -> fma(lh, lh, alpha v)), spelled out so both paths agree bit for bit
+        if (epi == 1) {
+          const double lh = lamh[g];
+          v = __fma_rn(lh, lh, __dmul_rn(alpha, v));
+        } else if (epi == 2) {
+          const double lh = lamh[g], ld = lamd[g];
+          v = __fma_rn(ld, __dmul_rn(__dmul_rn(lh, lh), ld), __dmul_rn(alpha, v));
+        }
+        eig[g] = v;
+        vmin = fmin(vmin, v);
+        vmax = fmax(vmax, v);
+      }
+    }
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+    vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+  }
+  if (tx == 0) {
+    red[ty] = vmin;
+    red[8 + ty] = vmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && partial_minmax) {
+    double a = red[0], z = red[8];
+    for (int w = 1; w < 8; ++w) {
+      a = fmin(a, red[w]);
+      z = fmax(z, red[8 + w]);
+    }
+    partial_minmax[2 * blockIdx.x] = a;
+    partial_minmax[2 * blockIdx.x + 1] = z;
+  }
+}
 }  // namespace tvd
 
 namespace tvd {
+cudaError_t launch_transpose_eig(const double* projT, int n, int epi, const double* lamh,
+                                 const double* lamd, double alpha, double* eig,
+                                 double* partial_minmax, int* nblocks_out, cudaStream_t st) {
+  const int nt = (n + 31) / 32;
+  long nb = (long)nt * nt;
+  if (nb > n) nb = n;
+  if (nb > 8L * kSMs) nb = 8L * kSMs;
+  k_transpose_eig<<<(int)nb, 256, 0, st>>>(projT, n, epi, lamh, lamd, alpha, eig, partial_minmax);
+  if (nblocks_out) *nblocks_out = (int)nb;
+  return cudaGetLastError();
+}
 cudaError_t launch_transpose_rect(const double* in, double* out, int rows, int cols,
                                   const int* skip, cudaStream_t st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
