@@ -735,23 +735,26 @@ __global__ void __launch_bounds__(NW * 32, 2) k_band_pfa_co(const BandPfaK p) {
   const int line = blockIdx.x;
   auto B0 = [&](int j) { return b.b0[(long)line * b.b0_ls + (long)j * b.b0_es]; };
   auto B1 = [&](int j) { return b.b1[(long)line * b.b1_ls + (long)j * b.b1_es]; };
-  for (int i = tid; i < LP; i += NT) X[i] = make_double2(0.0, 0.0);
-  __syncthreads();
-  for (int j = tid; j < L; j += NT) {
-    // even slots 2j <- b0[j] (j = 1..N), odd slots 2j+1 <- c1 b1[j] (j = 1..N-1)
-    double e = 0.0, o = 0.0;
-    if (j >= 1 && j <= L - 1) e = B0(j);
-    if (b.b1 && j >= 1 && j <= L - 2) o = b.c1 * B1(j);
-    X[__ldg(p.pl.gscat + j)] = make_double2(e, o);
-  }
-  if (tid < 32) {  // band totals (one warp, fixed order) as k_band
+  // The scatter writes every cell the stages read (the L grid cells; the column-owner stages
+  // never touch the pad columns), so the line buffer needs no zero fill.  The last warp sums
+  // the band totals (one warp, fixed lane-strided order, as k_band) while the others scatter.
+  if (tid < NT - 32) {
+    for (int j = tid; j < L; j += NT - 32) {
+      // even slots 2j <- b0[j] (j = 1..N), odd slots 2j+1 <- c1 b1[j] (j = 1..N-1)
+      double e = 0.0, o = 0.0;
+      if (j >= 1 && j <= L - 1) e = B0(j);
+      if (b.b1 && j >= 1 && j <= L - 2) o = b.c1 * B1(j);
+      X[__ldg(p.pl.gscat + j)] = make_double2(e, o);
+    }
+  } else {
+    const int lane = tid & 31;
     double t0 = 0.0, t1 = 0.0;
-    for (int j = 1 + tid; j < n - 1; j += 32) t0 += B0(j);
+    for (int j = 1 + lane; j < n - 1; j += 32) t0 += B0(j);
     if (b.b1)
-      for (int j = 1 + tid; j < n - 2; j += 32) t1 += B1(j);
+      for (int j = 1 + lane; j < n - 2; j += 32) t1 += B1(j);
     t0 = warp_sum(t0);
     t1 = warp_sum(t1);
-    if (tid == 0) {
+    if (lane == 0) {
       tot[0] = t0;
       tot[1] = t1;
     }
@@ -759,24 +762,12 @@ __global__ void __launch_bounds__(NW * 32, 2) k_band_pfa_co(const BandPfaK p) {
   __syncthreads();
   half_stage_co<FullStage<SH, 0>, 1, NW>(X, p.pl.st[0].Cf, p.pl.st[0].Sf, Y);
   half_stage_co<FullStage<SH, 1>, 1, NW>(Y, p.pl.st[1].Cf, p.pl.st[1].Sf, X);
-  // the band form (k_band's epilogue; C_t from the CRT output position of t)
-  auto at = [&](int t) { return X[t == 0 ? 0u : __ldg(p.pl.gath + t - 1)]; };
+  // the band form (k_band's epilogue; C_t from the CRT output position of t).  Outputs t and
+  // L - t read the same two grid cells, so one thread forms both (per output the operations
+  // are k_band's; the mirrored output only swaps exact negations and commutative adds).
+  auto at = [&](int t) { return X[__ldg(p.pl.gath + t - 1)]; };
   double vmin = 1.0 / 0.0, vmax = -1.0 / 0.0;
-  for (int t = tid; t < n; t += NT) {
-    double v;
-    if (t == 0 || t == n - 1) {
-      v = B0(t);
-    } else {
-      const int tr = L - t;
-      const double2 C = at(t), Cr = cconj(at(tr));
-      const double2 E = cscale(cadd(C, Cr), 0.5);
-      const double2 D = csub(C, Cr);
-      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
-      const double2 w = p.wfull[t];
-      const double re_s = E.x + (w.x * O.x - w.y * O.y);
-      const double t0 = tot[0], t1 = tot[1];
-      v = (t0 + b.c1 * t1 * w.x - re_s) / L;
-    }
+  auto emit = [&](int t, double v) {
     const long g = (long)line * b.out_ls + (long)t * b.out_es;
     if (b.epi == 1) {
       const double lh = b.lamh[g];
@@ -788,6 +779,30 @@ __global__ void __launch_bounds__(NW * 32, 2) k_band_pfa_co(const BandPfaK p) {
     b.out[g] = v;
     vmin = fmin(vmin, v);
     vmax = fmax(vmax, v);
+  };
+  if (tid < 2) emit(tid ? n - 1 : 0, B0(tid ? n - 1 : 0));
+  const double t0 = tot[0], t1 = tot[1];
+  for (int t = 1 + tid; t <= (L - 1) / 2; t += NT) {
+    const int tr = L - t;
+    const double2 Ct = at(t), Ctr = at(tr);
+    {
+      const double2 C = Ct, Cr = cconj(Ctr);
+      const double2 E = cscale(cadd(C, Cr), 0.5);
+      const double2 D = csub(C, Cr);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      const double2 w = p.wfull[t];
+      const double re_s = E.x + (w.x * O.x - w.y * O.y);
+      emit(t, (t0 + b.c1 * t1 * w.x - re_s) / L);
+    }
+    {
+      const double2 C = Ctr, Cr = cconj(Ct);
+      const double2 E = cscale(cadd(C, Cr), 0.5);
+      const double2 D = csub(C, Cr);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      const double2 w = p.wfull[tr];
+      const double re_s = E.x + (w.x * O.x - w.y * O.y);
+      emit(tr, (t0 + b.c1 * t1 * w.x - re_s) / L);
+    }
   }
   if (b.epi != 0) {
     for (int o = 16; o > 0; o >>= 1) {
