@@ -1878,8 +1878,7 @@ static int level2(tvd_ctx* c, const TrigPlan* P, int n, const double* diag, cons
   // same epilogue expression: bit-identical eigenvalues.
   const bool rowwise = !ar_c && P->family != kFamDct && P->pfa_ok && P->pfa.L == P->L &&
                        band_pfa_ok(P->pfa) && !option(kOptBandGeneric) &&
-                       !(P->rader_ok && P->rader.L == P->L) && option(kOptBandPrefetch) != 6 &&
-                       band_pfa_rowwise(P->pfa);
+                       !(P->rader_ok && P->rader.L == P->L) && band_pfa_rowwise(P->pfa);
   if (rowwise) {
     double *t0, *t1 = nullptr;
     TVD_SLOT(c, kSlotTmp2, (size_t)n * n, t0);

@@ -1643,7 +1643,7 @@ cudaError_t launch_band_pfa(const PfaPlan& P, const double2* wfull, int n, const
   k.wfull = wfull;
   k.n = n;
   k.b = b;
-  if ((which == 1 || which == 2) && option(kOptBandPrefetch) != 6) {  // column-owner variant
+  if (which == 1 || which == 2) {  // column-owner variant (two tensor-core stages)
     if (nblocks_out) *nblocks_out = b.nlines;
     if (b.nlines == 0) return cudaSuccess;
     return which == 1 ? launch_band_pfa_co<89, 23, 6>(k, st) : launch_band_pfa_co<33, 31, 4>(k, st);

@@ -1009,12 +1009,14 @@ def test_rounding_sensitive_restores_match_reference_with_exact_dots(golden, nam
     assert rel_err(rep.restored, g["restored"]) < max(1e-8, 2.0 * spread)
 
 
-@pytest.mark.parametrize("n,kind", [(2048, "M"), (1024, "D_M"), (512, "M_D"), (128, "M")])
+@pytest.mark.parametrize("n,kind", [(2048, "M"), (1024, "D_M"), (1024, "M_D"), (512, "M_D"),
+                                    (128, "M")])
 def test_assembly_band_projections_pfa_match_generic(n, kind):
     """The sine-family band projections of the assembly on the prime-factor engine's tensor-core
-    stages run as a general DFT (k_band_pfa) against the generic mixed-radix engine (option
-    band_generic) and the oracle's restatement of precond.py:369-395: eigenvalues within
-    1e-12."""
+    stages run as a general DFT (k_band_pfa; at 2048 / 1024 the column-owner k_band_pfa_co with
+    the row-wise level 2 and the fused transpose + eigenvalue epilogue, both epilogue forms)
+    against the generic mixed-radix engine (option band_generic) and the oracle's restatement
+    of precond.py:369-395: eigenvalues within 1e-12."""
     from paper_1011_5964_b200 import _native as nat
     from paper_1011_5964_b200.harness import gen_psf
 
