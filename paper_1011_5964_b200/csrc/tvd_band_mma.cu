@@ -215,7 +215,10 @@ __global__ void __launch_bounds__(256, MINB) k_bmma_cols(BandOp op, BandTaps tp,
   for (int e = tid; e < SH::HEIGHT * C2; e += blockDim.x) {
     const int r = e / C2, c = 2 * (e - r * C2);
     const int row = ib - KOFF + r, col = j0 + c;
-    const bool ok = row >= 0 && row < n && col < n;
+    // rows outside [row_lo - KOFF, row_hi + KOFF) feed only outputs past row_hi, which are
+    // dropped -- and a row slab's buffer ends there (a 128-row tile over a 64-row slab would
+    // read past its halo): zero-fill them instead of reading
+    const bool ok = row >= 0 && row < n && col < n && row >= row_lo - KOFF && row < row_hi + KOFF;
     cp16(tile + r * CP + c, ok ? in + (long)row * n + col : in + (long)ib * n, ok);
   }
   stage_fragments<KOFF>(fr, tp, op.w);
