@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
   if (skip && *skip) return;
   using SH = BmShape<KOFF>;
   constexpr int T = kBmT, S = SH::S, RP = SH::RP, W2 = SH::WIDTH / 2;
+  const unsigned long long keep = l2_keep_policy();
   extern __shared__ __align__(16) double smb[];
   double* tile = smb;
   double* fr = smb + SH::RH * RP;
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
                                       __dadd_rn(zz.y, __dmul_rn(beta, po.y)));
       *tz = pv;  // zero-filled out-of-range elements stay zero
       if (row < row_hi && col >= jb && col < jb + SH::CW && col < n)
-        *reinterpret_cast<double2*>(fz.p_new + (long)row * n + col) = pv;
+        st2_keep(fz.p_new + (long)row * n + col, pv.x, pv.y, keep);
     }
     __syncthreads();
   }
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(256, 2) k_bmma_rows(BandOp op, BandTaps tp,
     for (int t = 0; t < T; ++t) {
       const int col = o0 + 8 * t + 2 * (lane & 3);
       if (col < n)
-        *reinterpret_cast<double2*>(out + (long)row * n + col) = make_double2(acc[t][0], acc[t][1]);
+        st2_keep(out + (long)row * n + col, acc[t][0], acc[t][1], keep);
     }
   }
 }
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(256, MINB) k_bmma_cols(BandOp op, BandTaps tp,
   const int cl = col > 0 ? col - 1 : 0, cr = col + 2 < n ? col + 2 : n - 1;
   auto ld2 = [](const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); };
   constexpr int TG = 2;
+  const unsigned long long keep_policy = l2_keep_policy();
   const bool ar = ep.bc_l == 1;  // anti-reflective ghosts 2 w_0 - w_1 at the image border
   double dot = 0.0, dself = 0.0;
   if (col < n) {
@@ -318,7 +320,8 @@ __global__ void __launch_bounds__(256, MINB) k_bmma_cols(BandOp op, BandTaps tp,
           x0 = __dmul_rn(s2[k].x, x0);
           x1 = __dmul_rn(s2[k].y, x1);
         }
-        *reinterpret_cast<double2*>(out + (long)i * n + col) = make_double2(x0, x1);
+        // q is read once more, by the x / r update right after this pass: ask L2 to keep it
+        st2_keep(out + (long)i * n + col, x0, x1, keep_policy);
         if (dw) {
           dot += d2[k].x * x0;
           dot += d2[k].y * x1;
